@@ -1,0 +1,190 @@
+/*
+ * dpmrf_cuda.h -- C ABI of the B200-native DPP-PMRF optimization hot path.
+ *
+ * The drop-in boundary for the reference's engine layer
+ * (/root/reference/proj/include/dpmrf/mrf/engine.hpp:15-116 and
+ *  graph/neighborhoods.hpp:28-29).  Every entry point below cites the
+ * reference declaration it replaces.  Plain pointers and sizes only; no
+ * exception crosses the ABI -- each call returns a dpmrf_status and leaves a
+ * message for dpmrf_last_error().  The C++ drop-in (include/dpmrf_b200/
+ * engine.hpp) rethrows the matching reference exception type.
+ *
+ * Ownership: all input pointers are caller-owned HOST memory, read during
+ * the call only; all outputs are caller-allocated HOST buffers, written
+ * before the call returns ("internally parallel, externally synchronous",
+ * SPEC.md:126-127).  The region graph and neighborhoods are uploaded once
+ * into the context and stay resident in HBM across calls.
+ *
+ * Threading: a context is not re-entrant (the reference thread pool
+ * serializes submissions, proj/src/dpp/backend.cpp:45); use one context per
+ * host thread.  Calls block until their outputs are on the host.
+ */
+#ifndef DPMRF_CUDA_H
+#define DPMRF_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPMRF_ABI_VERSION 1
+
+/* Error convention of the reference. */
+typedef enum dpmrf_status {
+  DPMRF_OK = 0,
+  DPMRF_INPUT_ERROR = 1,      /* dpmrf::InputError          proj/include/dpmrf/error.hpp:11 */
+  DPMRF_INVALID_ARGUMENT = 2, /* std::invalid_argument      e.g. proj/src/mrf/engine.cpp:175-176 */
+  DPMRF_OUT_OF_RANGE = 3,     /* std::out_of_range          proj/include/dpmrf/dpp/kernels.hpp:313,337 */
+  DPMRF_CUDA_ERROR = 4,       /* device failure (no reference counterpart) */
+  DPMRF_NCCL_ERROR = 5,       /* collective failure (multi-GPU paths) */
+  DPMRF_INTERNAL_ERROR = 6    /* anything else (the CLI's exit 1, proj/tools/main.cpp:248-250) */
+} dpmrf_status;
+
+typedef struct dpmrf_context dpmrf_context;
+
+/* OptimizerConfig, proj/include/dpmrf/mrf/model.hpp:19-27 (same field order
+ * and meaning; defaults 2, 20, 10, 3, 1e-4, 1.0, 0). */
+typedef struct dpmrf_optimizer_config {
+  uint32_t num_labels;
+  int32_t em_max_iters;
+  int32_t map_max_iters;
+  int32_t convergence_window;
+  double convergence_tol;
+  double beta;
+  uint64_t rng_seed;
+} dpmrf_optimizer_config;
+
+/* Run options (no reference counterpart; all-zero = reference semantics). */
+enum {
+  DPMRF_TRACE_NONE = 0, /* labels + params only */
+  DPMRF_TRACE_EM = 1,   /* + per-EM total energy, flag, params, MAP count */
+  DPMRF_TRACE_FULL = 2  /* + every MAP iteration's hood energies and flags
+                           (OptimizeResult.trace, engine.hpp:82-99) */
+};
+enum {
+  DPMRF_RUN_FIXED_WORK = 1u,    /* drop the early exits (optimize.cpp:59,:71): fixed EM x MAP work */
+  DPMRF_RUN_MULTILABEL = 2u,    /* allow num_labels in [1,255] (extension; reference: 2 only) */
+  DPMRF_RUN_KERNEL_TIMING = 4u  /* CUDA events around the MAP kernels (dpmrf_get_stats) */
+};
+
+typedef struct dpmrf_run_options {
+  uint32_t flags;
+  int32_t trace_level;
+} dpmrf_run_options;
+
+/* Device-side measurements of the last dpmrf_optimize call. */
+typedef struct dpmrf_run_stats {
+  double optimize_ms;        /* CUDA-event time of the whole optimize phase on the context stream */
+  double vertex_kernel_ms;   /* sum over launches of the per-vertex energy/argmin kernel */
+  double hood_kernel_ms;     /* sum over launches of the per-hood sum + convergence kernel */
+  double mstep_ms;           /* M-step kernels */
+  uint64_t vertex_launches;
+  uint64_t hood_launches;
+  uint64_t kernel_launches;  /* every kernel of this library launched by the call */
+  int32_t em_iters;
+  int32_t map_iters_total;   /* MAP iterations executed, summed over EM iterations */
+  uint64_t series;           /* hood-energy series length (nonempty hoods) */
+} dpmrf_run_stats;
+
+/* ---- context ------------------------------------------------------------ */
+dpmrf_status dpmrf_context_create(int device, dpmrf_context** out);
+void dpmrf_context_destroy(dpmrf_context* ctx);
+const char* dpmrf_last_error(void); /* message of this thread's last failing call */
+int dpmrf_abi_version(void);
+
+/* ---- resident inputs ---------------------------------------------------- */
+/* RegionGraph, proj/include/dpmrf/graph/region_graph.hpp:14-25: CSR with
+ * num_vertices+1 offsets, offsets[R] neighbor ids, and R region means. */
+dpmrf_status dpmrf_set_graph(dpmrf_context* ctx, uint32_t num_vertices, const uint32_t* offsets,
+                             const uint32_t* neighbors, const double* region_mean);
+
+/* NeighborhoodSet, proj/include/dpmrf/graph/neighborhoods.hpp:15-23:
+ * num_hoods+1 offsets and offsets[num_hoods] member ids. */
+dpmrf_status dpmrf_set_hoods(dpmrf_context* ctx, uint64_t num_hoods, const uint32_t* offsets,
+                             const uint32_t* members);
+
+/* build_neighborhoods, proj/include/dpmrf/graph/neighborhoods.hpp:28-29 /
+ * proj/src/graph/neighborhoods.cpp:10-57: one sorted, duplicate-free
+ * 1-neighborhood per maximal clique, built ON THE DEVICE from the resident
+ * graph; the result becomes the context's neighborhoods.  k != 1 ->
+ * DPMRF_INPUT_ERROR.  *num_slots receives the total member count. */
+dpmrf_status dpmrf_build_neighborhoods(dpmrf_context* ctx, uint64_t num_cliques,
+                                       const uint32_t* clique_offsets,
+                                       const uint32_t* clique_members, uint32_t k,
+                                       uint64_t* num_slots);
+
+/* Copy the resident neighborhoods out (offsets: H+1, members: S,
+ * source_clique: H; any pointer may be NULL). */
+dpmrf_status dpmrf_get_hoods(dpmrf_context* ctx, uint64_t* num_hoods, uint64_t* num_slots,
+                             uint32_t* offsets, uint32_t* members, uint32_t* source_clique);
+
+/* ---- the optimization phase -------------------------------------------- */
+/* optimize, proj/include/dpmrf/mrf/engine.hpp:99-100 / proj/src/mrf/optimize.cpp:31-74,
+ * over the resident graph and neighborhoods.  labels: R entries, mu/sigma:
+ * num_labels entries.  opts may be NULL (reference semantics, full trace). */
+dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* config,
+                            const dpmrf_run_options* opts, uint32_t* labels, double* mu,
+                            double* sigma);
+
+/* Trace of the last dpmrf_optimize (EmIterationLog / MapIterationLog,
+ * engine.hpp:82-99). */
+dpmrf_status dpmrf_trace_info(dpmrf_context* ctx, int32_t* em_iters, uint64_t* series);
+dpmrf_status dpmrf_trace_em(dpmrf_context* ctx, int32_t em, int32_t* map_iters,
+                            double* total_energy, uint8_t* converged, double* mu, double* sigma);
+dpmrf_status dpmrf_trace_map(dpmrf_context* ctx, int32_t em, int32_t it, double* hood_energy,
+                             uint8_t* converged);
+dpmrf_status dpmrf_get_stats(dpmrf_context* ctx, dpmrf_run_stats* out);
+
+/* ---- step functions (engine.hpp), each on the device -------------------- */
+/* init_random, engine.hpp:20-21 / engine.cpp:28-38 (num_labels != 2 ->
+ * DPMRF_INPUT_ERROR unless allow_multilabel). */
+dpmrf_status dpmrf_init_random(dpmrf_context* ctx, uint32_t num_labels, uint32_t num_vertices,
+                               uint64_t seed, int allow_multilabel, double* mu, double* sigma,
+                               uint32_t* labels);
+/* replicate_by_label, engine.hpp:25-26 / engine.cpp:50-72; outputs M*S each. */
+dpmrf_status dpmrf_replicate_by_label(dpmrf_context* ctx, uint32_t num_labels,
+                                      uint32_t* test_label, uint32_t* old_index,
+                                      uint32_t* hood_id);
+/* slot_hood_map, engine.hpp:29-30 / engine.cpp:40-48; S outputs. */
+dpmrf_status dpmrf_slot_hood_map(dpmrf_context* ctx, uint32_t* slot_hood);
+/* discord_counts, engine.hpp:34-36 / engine.cpp:74-86; M*R outputs. */
+dpmrf_status dpmrf_discord_counts(dpmrf_context* ctx, const uint32_t* labels,
+                                  uint32_t num_labels, uint32_t* discord);
+/* compute_energies, engine.hpp:43-46 / engine.cpp:88-113 over an explicit
+ * replicated index of length E (bounds-checked like dpp::gather). */
+dpmrf_status dpmrf_compute_energies(dpmrf_context* ctx, uint64_t E, const uint32_t* test_label,
+                                    const uint32_t* old_index, uint32_t num_labels,
+                                    const double* mu, const double* sigma,
+                                    const uint32_t* labels, double beta, double* energies);
+/* min_label_energies, engine.hpp:55-56 / engine.cpp:115-145. */
+dpmrf_status dpmrf_min_label_energies(dpmrf_context* ctx, uint64_t E, const uint32_t* test_label,
+                                      const uint32_t* old_index, const double* energies,
+                                      uint64_t num_slots, double* min_energy,
+                                      uint32_t* min_label);
+/* neighborhood_energy_sums, engine.hpp:60-62 / engine.cpp:147-152: one sum
+ * per run of equal adjacent keys; *num_sums receives the run count. */
+dpmrf_status dpmrf_neighborhood_energy_sums(dpmrf_context* ctx, uint64_t S,
+                                            const uint32_t* slot_hood, const double* min_energy,
+                                            double* sums, uint64_t* num_sums);
+/* check_convergence, engine.hpp:67-69 / engine.cpp:154-169; history is
+ * row-major rows x series, oldest row first. */
+dpmrf_status dpmrf_check_convergence(dpmrf_context* ctx, uint64_t rows, uint64_t series,
+                                     const double* history, int32_t window, double tol,
+                                     uint8_t* flags);
+/* update_labels, engine.hpp:75-78 / engine.cpp:171-191 over the resident
+ * neighborhoods (argmin: S entries; old/new labels: R entries). */
+dpmrf_status dpmrf_update_labels(dpmrf_context* ctx, const uint32_t* argmin_label,
+                                 uint32_t num_vertices, const uint32_t* old_labels,
+                                 uint32_t* labels);
+/* update_parameters, engine.hpp:83-85 / engine.cpp:193-223 over the
+ * resident graph's region means. */
+dpmrf_status dpmrf_update_parameters(dpmrf_context* ctx, const uint32_t* labels,
+                                     uint32_t num_labels, const double* prev_mu,
+                                     const double* prev_sigma, double* mu, double* sigma);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPMRF_CUDA_H */

@@ -1,0 +1,128 @@
+"""ctypes bindings of the in-tree native libraries.
+
+``libdpmrf_cuda.so``   -- the C ABI of include/dpmrf_cuda.h (sm_100a kernels)
+``libdpmrf_inputs.so`` -- host-side synthetic input construction
+
+There is no fallback: if the CUDA library is missing or fails to load, every
+entry point raises.  Build with ``python -c "import __graft_entry__ as g; g.build()"``
+or ``make -C paper_1809_05018_b200/csrc``.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CUDA_LIB = os.path.join(HERE, "libdpmrf_cuda.so")
+INPUTS_LIB = os.path.join(HERE, "libdpmrf_inputs.so")
+
+u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+VP = ct.c_void_p
+U32, U64, I32, F64, INT = ct.c_uint32, ct.c_uint64, ct.c_int32, ct.c_double, ct.c_int
+ST = ct.c_int  # dpmrf_status
+
+
+class CConfig(ct.Structure):
+    """dpmrf_optimizer_config == OptimizerConfig (model.hpp:19-27)."""
+
+    _fields_ = [("num_labels", U32), ("em_max_iters", I32), ("map_max_iters", I32),
+                ("convergence_window", I32), ("convergence_tol", F64), ("beta", F64),
+                ("rng_seed", U64)]
+
+
+class CRunOptions(ct.Structure):
+    _fields_ = [("flags", U32), ("trace_level", I32)]
+
+
+class CRunStats(ct.Structure):
+    _fields_ = [("optimize_ms", F64), ("vertex_kernel_ms", F64), ("hood_kernel_ms", F64),
+                ("mstep_ms", F64), ("vertex_launches", U64), ("hood_launches", U64),
+                ("kernel_launches", U64), ("em_iters", I32), ("map_iters_total", I32),
+                ("series", U64)]
+
+
+# (name, restype, argtypes) of every C ABI entry point (include/dpmrf_cuda.h)
+CUDA_API = [
+    ("dpmrf_context_create", ST, [INT, ct.POINTER(VP)]),
+    ("dpmrf_context_destroy", None, [VP]),
+    ("dpmrf_last_error", ct.c_char_p, []),
+    ("dpmrf_abi_version", INT, []),
+    ("dpmrf_set_graph", ST, [VP, U32, VP, VP, VP]),
+    ("dpmrf_set_hoods", ST, [VP, U64, VP, VP]),
+    ("dpmrf_build_neighborhoods", ST, [VP, U64, VP, VP, U32, ct.POINTER(U64)]),
+    ("dpmrf_get_hoods", ST, [VP, ct.POINTER(U64), ct.POINTER(U64), VP, VP, VP]),
+    ("dpmrf_optimize", ST, [VP, ct.POINTER(CConfig), ct.POINTER(CRunOptions), VP, VP, VP]),
+    ("dpmrf_trace_info", ST, [VP, ct.POINTER(I32), ct.POINTER(U64)]),
+    ("dpmrf_trace_em", ST, [VP, I32, ct.POINTER(I32), ct.POINTER(F64), ct.POINTER(ct.c_uint8),
+                            VP, VP]),
+    ("dpmrf_trace_map", ST, [VP, I32, I32, VP, VP]),
+    ("dpmrf_get_stats", ST, [VP, ct.POINTER(CRunStats)]),
+    ("dpmrf_init_random", ST, [VP, U32, U32, U64, INT, VP, VP, VP]),
+    ("dpmrf_replicate_by_label", ST, [VP, U32, VP, VP, VP]),
+    ("dpmrf_slot_hood_map", ST, [VP, VP]),
+    ("dpmrf_discord_counts", ST, [VP, VP, U32, VP]),
+    ("dpmrf_compute_energies", ST, [VP, U64, VP, VP, U32, VP, VP, VP, F64, VP]),
+    ("dpmrf_min_label_energies", ST, [VP, U64, VP, VP, VP, U64, VP, VP]),
+    ("dpmrf_neighborhood_energy_sums", ST, [VP, U64, VP, VP, VP, ct.POINTER(U64)]),
+    ("dpmrf_check_convergence", ST, [VP, U64, U64, VP, I32, F64, VP]),
+    ("dpmrf_update_labels", ST, [VP, VP, U32, VP, VP]),
+    ("dpmrf_update_parameters", ST, [VP, VP, U32, VP, VP, VP, VP]),
+]
+
+INPUTS_API = [
+    ("dpmrf_in_phantom", INT, [U32, U32, F64, U64, VP, VP]),
+    ("dpmrf_in_corrupt", INT, [VP, U32, U32, F64, F64, INT, U64, VP]),
+    ("dpmrf_in_grid_oversegment", U32, [U32, U32, U32, VP]),
+    ("dpmrf_in_brick_oversegment", U32, [U32, U32, U32, VP]),
+    ("dpmrf_in_region_graph", VP, [U32, U32, VP, VP, U32, ct.POINTER(U64)]),
+    ("dpmrf_in_graph_arrays", None, [VP, VP, VP, VP, VP]),
+    ("dpmrf_in_graph_free", None, [VP]),
+    ("dpmrf_in_maximal_cliques", VP, [U32, VP, VP, ct.POINTER(U64), ct.POINTER(U64)]),
+    ("dpmrf_in_clique_arrays", None, [VP, VP, VP]),
+    ("dpmrf_in_cliques_free", None, [VP]),
+]
+
+_cuda = None
+_inputs = None
+
+
+class NativeLibraryMissing(RuntimeError):
+    pass
+
+
+def _load(path, api):
+    if not os.path.exists(path):
+        raise NativeLibraryMissing(
+            f"{os.path.basename(path)} is not built; run __graft_entry__.build() "
+            "(the CUDA path has no fallback)")
+    lib = ct.CDLL(path)
+    for name, res, args in api:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def cuda():
+    global _cuda
+    if _cuda is None:
+        _cuda = _load(CUDA_LIB, CUDA_API)
+    return _cuda
+
+
+def inputs():
+    global _inputs
+    if _inputs is None:
+        _inputs = _load(INPUTS_LIB, INPUTS_API)
+    return _inputs
+
+
+def ptr(a):
+    """Raw pointer of a contiguous numpy array (None for empty/None)."""
+    if a is None:
+        return None
+    return a.ctypes.data if a.size else None

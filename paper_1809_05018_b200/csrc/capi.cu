@@ -1,0 +1,469 @@
+// capi.cu -- the C ABI (include/dpmrf_cuda.h): context, resident inputs and
+// the optimize() driver.
+//
+// Driver shape (proj/src/mrf/optimize.cpp:31-74 re-planned for the device):
+//   * the graph and neighborhoods stay resident in HBM across calls;
+//   * every MAP iteration is two kernels (per-vertex argmin, per-hood sum +
+//     window test) launched back to back with NO host synchronization: the
+//     early exit of optimize.cpp:59 is evaluated on the device (each kernel
+//     checks the previous iteration's unconverged-hood counter);
+//   * the M-step and total energy run on the device; the host synchronizes
+//     ONCE per EM iteration to read (mu, sigma, total) and to evaluate
+//     log(sigma) with the host libm exactly as make_label_terms does
+//     (model.hpp:57), which keeps the energies bit-identical to the reference.
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "context.cuh"
+
+using namespace dpmrf_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+dpmrf_status guarded(F&& f) {
+  try {
+    f();
+    return DPMRF_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return DPMRF_INTERNAL_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return DPMRF_INTERNAL_ERROR;
+  } catch (...) {
+    g_last_error = "unknown failure";
+    return DPMRF_INTERNAL_ERROR;
+  }
+}
+
+void need(bool cond, dpmrf_status s, const char* msg) {
+  if (!cond) fail(s, msg);
+}
+
+// validate_config, proj/src/mrf/optimize.cpp:13-23 (num_labels relaxed to
+// [1, 255] under DPMRF_RUN_MULTILABEL; labels are u8 in HBM).
+void validate_config(const dpmrf_optimizer_config& c, bool multilabel) {
+  if (multilabel) {
+    if (c.num_labels < 1 || c.num_labels > uint32_t(kMaxLabels))
+      fail(DPMRF_INPUT_ERROR, "num_labels must be in [1, 255]");
+  } else if (c.num_labels != 2) {
+    fail(DPMRF_INPUT_ERROR, "only 2 labels are supported");
+  }
+  if (c.em_max_iters < 0) fail(DPMRF_INPUT_ERROR, "em_max_iters must be >= 0");
+  if (c.map_max_iters < 1) fail(DPMRF_INPUT_ERROR, "map_max_iters must be >= 1");
+  if (c.convergence_window < 1) fail(DPMRF_INPUT_ERROR, "convergence_window must be >= 1");
+  if (c.convergence_window >= c.map_max_iters)
+    fail(DPMRF_INPUT_ERROR, "convergence_window must be < map_max_iters");
+  if (!(c.convergence_tol > 0.0)) fail(DPMRF_INPUT_ERROR, "convergence_tol must be > 0");
+  if (!(c.beta >= 0.0)) fail(DPMRF_INPUT_ERROR, "beta must be >= 0");
+  if (c.map_max_iters > kMaxMapIters) fail(DPMRF_INPUT_ERROR, "map_max_iters too large");
+}
+
+double unit_of(uint64_t z) { return static_cast<double>(z >> 11) * 0x1.0p-53; }
+
+// init_random's parameter draws, engine.cpp:33-34 (draws 0..2M-1).
+void init_params(uint32_t M, uint64_t seed, double* mu, double* sigma) {
+  for (uint32_t l = 0; l < M; ++l) mu[l] = 255.0 * unit_of(splitmix_draw(seed, l));
+  for (uint32_t l = 0; l < M; ++l) {
+    const double s = 255.0 * unit_of(splitmix_draw(seed, M + l));
+    sigma[l] = s < kSigmaFloor ? kSigmaFloor : s;
+  }
+}
+
+}  // namespace
+
+void dpmrf_b200_set_error(const char* msg) { g_last_error = msg; }
+
+// ---- structure preparation ---------------------------------------------------
+void dpmrf_context::prepare() {
+  if (prepared) {
+    if (prep_status != DPMRF_OK) fail(prep_status, prep_msg);
+    return;
+  }
+  need(has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
+  need(has_hoods, DPMRF_INVALID_ARGUMENT, "no neighborhoods uploaded");
+  uint32_t* err = prep_err.ensure(2);
+  CK(cudaMemsetAsync(err, 0, 2 * sizeof(uint32_t), stream));
+  launch_validate(g_off.get(), g_nbr.get(), R, A, h_off.get(), h_mem.get(), H, S, err, err + 1,
+                  stream);
+  uint32_t h_err[2];
+  CK(cudaMemcpyAsync(h_err, err, sizeof h_err, cudaMemcpyDeviceToHost, stream));
+  sync();
+  prepared = true;
+  prep_status = DPMRF_OK;
+  if (h_err[0] & 1u) {
+    prep_status = DPMRF_OUT_OF_RANGE;
+    prep_msg = "gather: index out of range (hood member >= num_vertices)";
+  } else if (h_err[0] & 2u) {
+    prep_status = DPMRF_OUT_OF_RANGE;
+    prep_msg = "region graph neighbor >= num_vertices";
+  } else if (h_err[0] & 4u) {
+    prep_status = DPMRF_INVALID_ARGUMENT;
+    prep_msg = "neighborhood offsets are not a valid CSR";
+  } else if (h_err[0] & 8u) {
+    prep_status = DPMRF_INVALID_ARGUMENT;
+    prep_msg = "region graph offsets are not a valid CSR";
+  }
+  if (prep_status != DPMRF_OK) fail(prep_status, prep_msg);
+  launch_cover(h_mem.get(), S, cover.ensure(R), R, stream);
+  const uint32_t empties = h_err[1];
+  Hs = H - empties;
+  series_alias = empties == 0;
+  if (!series_alias) {
+    launch_series_offsets(h_off.get(), H, S, s_off_buf.ensure(Hs + 1), prep_tmp, scan, stream);
+  }
+  sync();
+}
+
+// ---- context -----------------------------------------------------------------
+extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
+  return guarded([&] {
+    need(out != nullptr, DPMRF_INVALID_ARGUMENT, "out is null");
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    need(device >= 0 && device < n, DPMRF_INVALID_ARGUMENT, "no such CUDA device");
+    auto* c = new dpmrf_context;
+    c->device = device;
+    try {
+      CK(cudaSetDevice(device));
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      CK(cudaEventCreate(&c->ev_begin));
+      CK(cudaEventCreate(&c->ev_end));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+extern "C" void dpmrf_context_destroy(dpmrf_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->ev_begin) cudaEventDestroy(ctx->ev_begin);
+  if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
+  cudaStream_t s = ctx->stream;
+  delete ctx;
+  if (s) cudaStreamDestroy(s);
+}
+
+extern "C" const char* dpmrf_last_error(void) { return g_last_error.c_str(); }
+extern "C" int dpmrf_abi_version(void) { return DPMRF_ABI_VERSION; }
+
+// ---- resident inputs -----------------------------------------------------------
+extern "C" dpmrf_status dpmrf_set_graph(dpmrf_context* ctx, uint32_t R, const uint32_t* offsets,
+                                        const uint32_t* neighbors, const double* region_mean) {
+  return guarded([&] {
+    need(ctx && offsets, DPMRF_INVALID_ARGUMENT, "null argument");
+    ctx->bind();
+    const uint64_t A = offsets[R];
+    need(A == 0 || neighbors, DPMRF_INVALID_ARGUMENT, "neighbors is null");
+    need(R == 0 || region_mean, DPMRF_INVALID_ARGUMENT, "region_mean is null");
+    CK(cudaMemcpyAsync(ctx->g_off.ensure(uint64_t(R) + 1), offsets, (uint64_t(R) + 1) * 4,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    if (A)
+      CK(cudaMemcpyAsync(ctx->g_nbr.ensure(A), neighbors, A * 4, cudaMemcpyHostToDevice,
+                         ctx->stream));
+    else
+      ctx->g_nbr.ensure(1);
+    if (R)
+      CK(cudaMemcpyAsync(ctx->g_mean.ensure(R), region_mean, uint64_t(R) * 8,
+                         cudaMemcpyHostToDevice, ctx->stream));
+    else
+      ctx->g_mean.ensure(1);
+    ctx->R = R;
+    ctx->A = A;
+    ctx->has_graph = true;
+    ctx->prepared = false;
+    ctx->sync();
+  });
+}
+
+extern "C" dpmrf_status dpmrf_set_hoods(dpmrf_context* ctx, uint64_t H, const uint32_t* offsets,
+                                        const uint32_t* members) {
+  return guarded([&] {
+    need(ctx && offsets, DPMRF_INVALID_ARGUMENT, "null argument");
+    ctx->bind();
+    const uint64_t S = offsets[H];
+    need(S == 0 || members, DPMRF_INVALID_ARGUMENT, "members is null");
+    CK(cudaMemcpyAsync(ctx->h_off.ensure(H + 1), offsets, (H + 1) * 4, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    if (S)
+      CK(cudaMemcpyAsync(ctx->h_mem.ensure(S), members, S * 4, cudaMemcpyHostToDevice,
+                         ctx->stream));
+    else
+      ctx->h_mem.ensure(1);
+    ctx->h_src.release();  // identity (neighborhoods.cpp:53-55)
+    ctx->H = H;
+    ctx->S = S;
+    ctx->has_hoods = true;
+    ctx->prepared = false;
+    ctx->sync();
+  });
+}
+
+extern "C" dpmrf_status dpmrf_build_neighborhoods(dpmrf_context* ctx, uint64_t C,
+                                                  const uint32_t* c_off, const uint32_t* c_mem,
+                                                  uint32_t k, uint64_t* num_slots) {
+  return guarded([&] {
+    need(ctx && c_off, DPMRF_INVALID_ARGUMENT, "null argument");
+    if (k != 1) fail(DPMRF_INPUT_ERROR, "only 1-neighborhoods are supported");
+    need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
+    ctx->bind();
+    build_neighborhoods_device(ctx, C, c_off, c_mem);
+    ctx->has_hoods = true;
+    ctx->prepared = false;
+    if (num_slots) *num_slots = ctx->S;
+  });
+}
+
+extern "C" dpmrf_status dpmrf_get_hoods(dpmrf_context* ctx, uint64_t* H, uint64_t* S,
+                                        uint32_t* offsets, uint32_t* members,
+                                        uint32_t* source_clique) {
+  return guarded([&] {
+    need(ctx && ctx->has_hoods, DPMRF_INVALID_ARGUMENT, "no neighborhoods");
+    ctx->bind();
+    if (H) *H = ctx->H;
+    if (S) *S = ctx->S;
+    if (offsets)
+      CK(cudaMemcpyAsync(offsets, ctx->h_off.get(), (ctx->H + 1) * 4, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    if (members && ctx->S)
+      CK(cudaMemcpyAsync(members, ctx->h_mem.get(), ctx->S * 4, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    ctx->sync();
+    if (source_clique)
+      for (uint64_t h = 0; h < ctx->H; ++h) source_clique[h] = static_cast<uint32_t>(h);
+  });
+}
+
+// ---- optimize ------------------------------------------------------------------
+extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
+                                       const dpmrf_run_options* opts, uint32_t* labels_out,
+                                       double* mu_out, double* sigma_out) {
+  return guarded([&] {
+    need(ctx && cfg, DPMRF_INVALID_ARGUMENT, "null argument");
+    const dpmrf_run_options o = opts ? *opts : dpmrf_run_options{0, DPMRF_TRACE_FULL};
+    const bool multilabel = (o.flags & DPMRF_RUN_MULTILABEL) != 0;
+    const int fixed = (o.flags & DPMRF_RUN_FIXED_WORK) ? 1 : 0;
+    const bool timing = (o.flags & DPMRF_RUN_KERNEL_TIMING) != 0;
+    validate_config(*cfg, multilabel);
+    need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
+    ctx->bind();
+    cudaStream_t st = ctx->stream;
+    const uint32_t M = cfg->num_labels;
+    const uint32_t R = ctx->R;
+    const int L = cfg->convergence_window;
+    const int map_max = cfg->map_max_iters;
+
+    ctx->trace.clear();
+    ctx->trace_level = o.trace_level;
+    ctx->trace_M = M;
+    ctx->stats = dpmrf_run_stats{};
+    uint64_t launches = 0;
+
+    // init_random (engine.cpp:28-38): params on the host, labels on the device
+    std::vector<double> mu(M), sigma(M);
+    init_params(M, cfg->rng_seed, mu.data(), sigma.data());
+    uint8_t* lab[2] = {ctx->lab[0].ensure(R), ctx->lab[1].ensure(R)};
+    CK(cudaEventRecord(ctx->ev_begin, st));
+    launch_init_labels(lab[0], R, M, cfg->rng_seed, st);
+    launches += R ? 1 : 0;
+    int cur = 0;
+
+    if (cfg->em_max_iters > 0) {
+      ctx->prepare();
+      const uint64_t Hs = ctx->Hs;
+      MapArgs a{};
+      a.g_off = ctx->g_off.get();
+      a.g_nbr = ctx->g_nbr.get();
+      a.mean = ctx->g_mean.get();
+      a.cover = ctx->cover.get();
+      a.s_off = ctx->series_alias ? ctx->h_off.get() : ctx->s_off_buf.get();
+      a.h_mem = ctx->h_mem.get();
+      a.R = R;
+      a.Hs = Hs;
+      a.M = M;
+      a.beta = cfg->beta;
+      a.tol = cfg->convergence_tol;
+      a.L = L;
+      a.fixed = fixed;
+      a.terms = ctx->terms.ensure(3 * M);
+      a.minE = ctx->minE.ensure(R);
+      a.hist = ctx->hist.ensure(uint64_t(L + 1) * Hs);
+      a.flags = o.trace_level >= DPMRF_TRACE_FULL ? ctx->flags.ensure(Hs) : nullptr;
+      a.unconv = ctx->unconv.ensure(map_max);
+      double* params = ctx->params.ensure(2 * M);
+      double* em_out = ctx->em_out.ensure(2 + 2 * M);
+      double* h_terms = ctx->h_terms.ensure(3 * M);
+      double* h_em = ctx->h_em.ensure(2 + 2 * M);
+      double* h_row = nullptr;
+      uint8_t* h_flags = nullptr;
+      if (a.flags) {
+        h_row = ctx->h_row.ensure(uint64_t(map_max) * Hs);
+        h_flags = ctx->h_flags.ensure(uint64_t(map_max) * Hs);
+      }
+      CK(cudaMemcpyAsync(params, mu.data(), M * 8, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(params + M, sigma.data(), M * 8, cudaMemcpyHostToDevice, st));
+      std::vector<double> em_hist;
+      size_t ev = 0;
+      for (int em = 0; em < cfg->em_max_iters; ++em) {
+        // make_label_terms (model.hpp:48-60) with the host's std::log
+        for (uint32_t l = 0; l < M; ++l) {
+          h_terms[l] = mu[l];
+          h_terms[M + l] = 2.0 * (sigma[l] * sigma[l]);
+          h_terms[2 * M + l] = std::log(sigma[l]);
+        }
+        CK(cudaMemcpyAsync(const_cast<double*>(a.terms), h_terms, 3 * M * 8,
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(a.unconv, 0, map_max * sizeof(uint32_t), st));
+        for (int t = 0; t < map_max; ++t) {
+          const uint8_t* lin = lab[(cur + t) & 1];
+          uint8_t* lout = lab[(cur + t + 1) & 1];
+          if (timing) CK(cudaEventRecord(ctx->event(ev++), st));
+          launch_vertex_argmin(a, lin, lout, t, st);
+          if (timing) CK(cudaEventRecord(ctx->event(ev++), st));
+          launch_hood_sums(a, t, st);
+          if (timing) CK(cudaEventRecord(ctx->event(ev++), st));
+          launches += 2;
+          if (a.flags && Hs) {
+            CK(cudaMemcpyAsync(h_row + uint64_t(t) * Hs, a.hist + uint64_t(t % (L + 1)) * Hs,
+                               Hs * 8, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(h_flags + uint64_t(t) * Hs, a.flags, Hs, cudaMemcpyDeviceToHost,
+                               st));
+          }
+        }
+        if (timing) CK(cudaEventRecord(ctx->event(ev++), st));
+        launch_mstep(a.mean, R, M, lab[cur], lab[cur ^ 1], a.hist, Hs, L, a.unconv, map_max,
+                     fixed, params, em_out, ctx->ms, st, &launches);
+        if (timing) CK(cudaEventRecord(ctx->event(ev++), st));
+        CK(cudaMemcpyAsync(h_em, em_out, (2 + 2 * M) * 8, cudaMemcpyDeviceToHost, st));
+        ctx->sync();
+        const int T = static_cast<int>(h_em[1]);
+        const double total = h_em[0];
+        std::memcpy(mu.data(), h_em + 2, M * 8);
+        std::memcpy(sigma.data(), h_em + 2 + M, M * 8);
+        cur = (cur + T) & 1;
+        ctx->stats.map_iters_total += T;
+        // EM-level window (optimize.cpp:66-69): history never resets
+        em_hist.push_back(total);
+        uint8_t conv = 0;
+        const size_t rows = em_hist.size();
+        if (rows >= size_t(L) + 1) {
+          conv = 1;
+          for (int i = 1; i <= L; ++i)
+            if (!(std::fabs(total - em_hist[rows - 1 - i]) < cfg->convergence_tol)) {
+              conv = 0;
+              break;
+            }
+        }
+        if (o.trace_level >= DPMRF_TRACE_EM) {
+          dpmrf_context::EmRecord rec;
+          rec.map_iters = T;
+          rec.total = total;
+          rec.converged = conv;
+          rec.mu = mu;
+          rec.sigma = sigma;
+          if (a.flags) {
+            rec.hood_energy.resize(T);
+            rec.hood_conv.resize(T);
+            for (int t = 0; t < T; ++t) {
+              rec.hood_energy[t].assign(h_row + uint64_t(t) * Hs, h_row + uint64_t(t + 1) * Hs);
+              rec.hood_conv[t].assign(h_flags + uint64_t(t) * Hs, h_flags + uint64_t(t + 1) * Hs);
+            }
+          }
+          ctx->trace.push_back(std::move(rec));
+        }
+        ctx->stats.em_iters = em + 1;
+        if (conv && !fixed) break;
+      }
+      ctx->stats.series = Hs;
+      if (timing) {
+        // per EM: (3 events per MAP iteration) + 2 around the M-step
+        size_t e = 0;
+        float ms = 0.f;
+        for (int em = 0; em < ctx->stats.em_iters; ++em) {
+          for (int t = 0; t < map_max; ++t) {
+            CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
+            ctx->stats.vertex_kernel_ms += ms;
+            CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e + 1], ctx->ev_pool[e + 2]));
+            ctx->stats.hood_kernel_ms += ms;
+            e += 3;
+          }
+          CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
+          ctx->stats.mstep_ms += ms;
+          e += 2;
+        }
+        ctx->stats.vertex_launches = uint64_t(ctx->stats.em_iters) * map_max;
+        ctx->stats.hood_launches = ctx->stats.vertex_launches;
+      }
+    }
+    // labels out (u8 in HBM -> the reference's u32)
+    uint32_t* l32 = ctx->labels32.ensure(R);
+    launch_u8_to_u32(lab[cur], l32, R, st);
+    launches += R ? 1 : 0;
+    CK(cudaEventRecord(ctx->ev_end, st));
+    if (labels_out && R)
+      CK(cudaMemcpyAsync(labels_out, l32, uint64_t(R) * 4, cudaMemcpyDeviceToHost, st));
+    ctx->sync();
+    float total_ms = 0.f;
+    CK(cudaEventElapsedTime(&total_ms, ctx->ev_begin, ctx->ev_end));
+    ctx->stats.optimize_ms = total_ms;
+    ctx->stats.kernel_launches = launches;
+    if (mu_out) std::memcpy(mu_out, mu.data(), M * 8);
+    if (sigma_out) std::memcpy(sigma_out, sigma.data(), M * 8);
+  });
+}
+
+extern "C" dpmrf_status dpmrf_trace_info(dpmrf_context* ctx, int32_t* em_iters, uint64_t* series) {
+  return guarded([&] {
+    need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null context");
+    if (em_iters) *em_iters = static_cast<int32_t>(ctx->trace.size());
+    if (series) *series = ctx->stats.series;
+  });
+}
+
+extern "C" dpmrf_status dpmrf_trace_em(dpmrf_context* ctx, int32_t em, int32_t* map_iters,
+                                       double* total, uint8_t* converged, double* mu,
+                                       double* sigma) {
+  return guarded([&] {
+    need(ctx && em >= 0 && size_t(em) < ctx->trace.size(), DPMRF_OUT_OF_RANGE,
+         "no such EM iteration in the trace");
+    const auto& r = ctx->trace[em];
+    if (map_iters) *map_iters = r.map_iters;
+    if (total) *total = r.total;
+    if (converged) *converged = r.converged;
+    if (mu) std::memcpy(mu, r.mu.data(), r.mu.size() * 8);
+    if (sigma) std::memcpy(sigma, r.sigma.data(), r.sigma.size() * 8);
+  });
+}
+
+extern "C" dpmrf_status dpmrf_trace_map(dpmrf_context* ctx, int32_t em, int32_t it,
+                                        double* hood_energy, uint8_t* converged) {
+  return guarded([&] {
+    need(ctx && em >= 0 && size_t(em) < ctx->trace.size(), DPMRF_OUT_OF_RANGE,
+         "no such EM iteration in the trace");
+    const auto& r = ctx->trace[em];
+    need(it >= 0 && size_t(it) < r.hood_energy.size(), DPMRF_OUT_OF_RANGE,
+         "no such MAP iteration in the trace (needs DPMRF_TRACE_FULL)");
+    if (hood_energy)
+      std::memcpy(hood_energy, r.hood_energy[it].data(), r.hood_energy[it].size() * 8);
+    if (converged) std::memcpy(converged, r.hood_conv[it].data(), r.hood_conv[it].size());
+  });
+}
+
+extern "C" dpmrf_status dpmrf_get_stats(dpmrf_context* ctx, dpmrf_run_stats* out) {
+  return guarded([&] {
+    need(ctx && out, DPMRF_INVALID_ARGUMENT, "null argument");
+    *out = ctx->stats;
+  });
+}

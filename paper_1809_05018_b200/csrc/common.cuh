@@ -1,0 +1,156 @@
+// common.cuh -- shared definitions of the sm_100a DPP-PMRF library.
+//
+// Arithmetic contract: every floating-point operation that the reference
+// evaluates in a pinned order (proj/include/dpmrf/mrf/model.hpp:62-72 and
+// the fold topology of proj/include/dpmrf/dpp/kernels.hpp:20-65) is written
+// with explicit round-to-nearest intrinsics (__dadd_rn, __dsub_rn, __dmul_rn,
+// __ddiv_rn, __dsqrt_rn) so no FMA contraction can change a bit; the library
+// is additionally compiled with -fmad=false.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "../../include/dpmrf_cuda.h"
+
+namespace dpmrf_b200 {
+
+// Internal exception; translated to dpmrf_status at the C ABI boundary.
+struct Error : std::runtime_error {
+  dpmrf_status status;
+  Error(dpmrf_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void fail(dpmrf_status s, const std::string& m) { throw Error(s, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "%s failed at %s:%d: %s", what, file, line,
+                  cudaGetErrorString(e));
+    throw Error(DPMRF_CUDA_ERROR, buf);
+  }
+}
+#define CK(x) ::dpmrf_b200::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH() ::dpmrf_b200::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+constexpr uint32_t kFoldLeaf = 1024;       // kFoldLeafSize, kernels.hpp:27
+constexpr double kSigmaFloor = 1e-3;       // kSigmaFloor, model.hpp:9
+constexpr int kMaxLabels = 255;            // labels are stored as u8 in HBM
+constexpr int kMaxMapIters = 4096;
+constexpr int kNumSMs = 148;
+
+// Growable device buffer (HBM). Contents are not preserved on growth.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  T* ensure(size_t n) {
+    if (n == 0) n = 1;
+    if (n > cap) {
+      release();
+      CK(cudaMalloc(&p, n * sizeof(T)));
+      cap = n;
+    }
+    return p;
+  }
+  T* get() const { return p; }
+};
+
+// Growable pinned host buffer.
+template <class T>
+struct HostBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  HostBuf() = default;
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  ~HostBuf() { release(); }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+  T* ensure(size_t n) {
+    if (n == 0) n = 1;
+    if (n > cap) {
+      release();
+      CK(cudaMallocHost(&p, n * sizeof(T)));
+      cap = n;
+    }
+    return p;
+  }
+};
+
+inline unsigned grid_for(uint64_t n, unsigned block) {
+  uint64_t g = (n + block - 1) / block;
+  if (g == 0) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+// ---- device helpers ---------------------------------------------------------
+
+// SplitMix64 finalizer (proj/src/mrf/engine.cpp:15-24); draw k (0-based) of
+// the stream seeded with `seed` is mix64(seed + (k+1) * golden).
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t splitmix_draw(uint64_t seed, uint64_t k) {
+  return mix64(seed + (k + 1) * 0x9E3779B97F4A7C15ull);
+}
+
+// label_energy, model.hpp:66-72: sub, mul, div, add, mul, add -- in that order.
+__device__ __forceinline__ double label_energy(double x, double mu, double two_var,
+                                               double log_sigma, double beta, uint32_t discord) {
+  const double d = __dsub_rn(x, mu);
+  const double q = __ddiv_rn(__dmul_rn(d, d), two_var);
+  const double data_term = __dadd_rn(q, log_sigma);
+  return __dadd_rn(data_term, __dmul_rn(beta, static_cast<double>(discord)));
+}
+
+// Pairwise tree of kernels.hpp:45-51 evaluated as a binary counter: push
+// leaf partials in order; equal-sized blocks merge immediately; at the end
+// the remaining blocks (sizes = binary digits of the count, decreasing)
+// combine right to left.  Identical topology to splitting at bit_floor(n-1).
+template <class T, class Op, int kDepth = 40>
+struct TreeStack {
+  T val[kDepth];
+  uint64_t count = 0;
+  int top = 0;
+  __device__ __forceinline__ void push(T x, Op op) {
+    ++count;
+    val[top++] = x;
+    // merge while the two top blocks have equal size: the lowest set bits
+    for (uint64_t c = count; (c & 1u) == 0; c >>= 1) {
+      val[top - 2] = op(val[top - 2], val[top - 1]);
+      --top;
+    }
+  }
+  __device__ __forceinline__ T finish(Op op) {
+    T acc = val[top - 1];
+    for (int i = top - 2; i >= 0; --i) acc = op(val[i], acc);
+    return acc;
+  }
+};
+
+struct AddOp {
+  __device__ __forceinline__ double operator()(double a, double b) const { return __dadd_rn(a, b); }
+};
+
+}  // namespace dpmrf_b200

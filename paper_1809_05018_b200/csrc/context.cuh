@@ -1,0 +1,83 @@
+// context.cuh -- the opaque dpmrf_context behind the C ABI (internal).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+
+struct dpmrf_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+
+  // ---- resident region graph (RegionGraph, region_graph.hpp:14-25) ----
+  bool has_graph = false;
+  uint32_t R = 0;
+  uint64_t A = 0;
+  dpmrf_b200::DevBuf<uint32_t> g_off, g_nbr;
+  dpmrf_b200::DevBuf<double> g_mean;
+
+  // ---- resident neighborhoods (NeighborhoodSet, neighborhoods.hpp:15-23) ----
+  bool has_hoods = false;
+  uint64_t H = 0, S = 0;
+  dpmrf_b200::DevBuf<uint32_t> h_off, h_mem, h_src;
+
+  // ---- derived per (graph, hoods) pair, built lazily on the device ----
+  bool prepared = false;
+  dpmrf_status prep_status = DPMRF_OK;
+  std::string prep_msg;
+  uint64_t Hs = 0;                 // nonempty hoods = reduce_by_key runs
+  bool series_alias = true;        // s_off == h_off (no empty hoods)
+  dpmrf_b200::DevBuf<uint32_t> s_off_buf, prep_tmp, prep_err;
+  dpmrf_b200::DevBuf<uint8_t> cover;  // vertex appears in >= 1 hood
+
+  // ---- optimization buffers ----
+  dpmrf_b200::DevBuf<uint8_t> lab[2];
+  dpmrf_b200::DevBuf<double> minE, hist, terms, params, em_out;
+  dpmrf_b200::DevBuf<uint8_t> flags;
+  dpmrf_b200::DevBuf<uint32_t> unconv, labels32;
+  dpmrf_b200::MStepBuffers ms;
+  dpmrf_b200::ScanWorkspace scan;
+  dpmrf_b200::HostBuf<double> h_terms, h_em, h_row;
+  dpmrf_b200::HostBuf<uint8_t> h_flags;
+
+  // ---- step-API / hood-build scratch ----
+  dpmrf_b200::DevBuf<uint32_t> tmp_u32[6];
+  dpmrf_b200::DevBuf<double> tmp_f64[3];
+  dpmrf_b200::DevBuf<uint8_t> tmp_u8[2];
+  dpmrf_b200::DevBuf<unsigned long long> tmp_u64[2];
+
+  // ---- trace of the last optimize (OptimizeResult.trace, engine.hpp:82-99) ----
+  struct EmRecord {
+    int32_t map_iters = 0;
+    double total = 0.0;
+    uint8_t converged = 0;
+    std::vector<double> mu, sigma;
+    std::vector<std::vector<double>> hood_energy;  // FULL trace only
+    std::vector<std::vector<uint8_t>> hood_conv;
+  };
+  std::vector<EmRecord> trace;
+  int32_t trace_level = DPMRF_TRACE_NONE;
+  uint32_t trace_M = 0;
+  dpmrf_run_stats stats{};
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+
+  cudaEvent_t event(size_t i) {
+    while (ev_pool.size() <= i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[i];
+  }
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+  void bind() { CK(cudaSetDevice(device)); }
+  void prepare();  // validate + cover + series offsets (capi.cu)
+};
+
+namespace dpmrf_b200 {
+// hoods.cu
+void build_neighborhoods_device(dpmrf_context* ctx, uint64_t C, const uint32_t* c_off_host,
+                                const uint32_t* c_mem_host);
+}  // namespace dpmrf_b200

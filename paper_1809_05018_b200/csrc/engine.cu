@@ -1,0 +1,650 @@
+// engine.cu -- sm_100a kernels of the EM/MAP optimization phase.
+//
+// Reference: proj/src/mrf/optimize.cpp:31-74 and the step functions of
+// proj/src/mrf/engine.cpp.  The reference replicates every hood slot once per
+// label (M*S elements), sorts by slot, reduces by key, then sorts by vertex to
+// pick each vertex's lowest-hood slot.  Because the replicated energy of an
+// element depends only on (vertex, label) (engine.cpp:96-110: the Potts term
+// counts GRAPH neighbors, not hood neighbors), every slot of a vertex carries
+// the same minimum and argmin, so the sort/reduce/sort chain collapses to one
+// per-vertex argmin (bit-identical; SURVEY.md key finding 1).  The hood sums
+// then gather the per-vertex minima in slot order.
+#include <algorithm>
+
+#include "engine.cuh"
+
+namespace dpmrf_b200 {
+
+namespace {
+
+constexpr int kVtxThreads = 256;
+constexpr int kHoodThreads = 256;
+
+__device__ __forceinline__ bool map_iter_skipped(const uint32_t* unconv, int t, int fixed) {
+  // optimize.cpp:59 -- the MAP loop stops after an iteration whose flags are
+  // all set.  Iteration t runs iff no earlier iteration had zero unconverged
+  // hoods; skipped iterations leave their counter at 0 so the chain holds.
+  return !fixed && t > 0 && unconv[t - 1] == 0;
+}
+
+// ---------------------------------------------------------------------------
+// Per-vertex energies + argmin + label commit.
+//   discord_counts       engine.cpp:74-86   (labels frozen at iteration start)
+//   compute_energies     engine.cpp:88-113  (label_energy order, model.hpp:66-72)
+//   min_label_energies   engine.cpp:115-145 (ties -> smaller label: strict <)
+//   update_labels        engine.cpp:171-191 (uncovered vertices keep labels)
+// ---------------------------------------------------------------------------
+template <int MT>
+__global__ void __launch_bounds__(kVtxThreads)
+    k_vertex_argmin(const uint32_t* __restrict__ g_off, const uint32_t* __restrict__ g_nbr,
+                    const double* __restrict__ mean, const uint8_t* __restrict__ cover,
+                    const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
+                    double* __restrict__ minE, uint32_t R, uint32_t M_rt,
+                    const double* __restrict__ terms, double beta,
+                    const uint32_t* __restrict__ unconv, int t, int fixed) {
+  if (map_iter_skipped(unconv, t, fixed)) return;
+  const uint32_t v = blockIdx.x * kVtxThreads + threadIdx.x;
+  if (v >= R) return;
+  const uint8_t old = lab_in[v];
+  if (!cover[v]) {
+    lab_out[v] = old;
+    return;
+  }
+  const uint32_t M = MT > 0 ? uint32_t(MT) : M_rt;
+  const uint32_t lo = g_off[v], hi = g_off[v + 1];
+  const uint32_t deg = hi - lo;
+  const double x = mean[v];
+  double best;
+  uint32_t best_l;
+  if constexpr (MT == 2) {
+    // labels are {0,1}: discord(0) = #neighbors labeled 1, discord(1) = deg - that
+    uint32_t ones = 0;
+    uint32_t a = lo;
+    for (; a + 4 <= hi; a += 4) {
+      const uint32_t u0 = g_nbr[a], u1 = g_nbr[a + 1], u2 = g_nbr[a + 2], u3 = g_nbr[a + 3];
+      ones += uint32_t(lab_in[u0]) + uint32_t(lab_in[u1]) + uint32_t(lab_in[u2]) +
+              uint32_t(lab_in[u3]);
+    }
+    for (; a < hi; ++a) ones += lab_in[g_nbr[a]];
+    const double e0 = label_energy(x, terms[0], terms[2], terms[4], beta, ones);
+    const double e1 = label_energy(x, terms[1], terms[3], terms[5], beta, deg - ones);
+    best = e0;
+    best_l = 0;
+    if (e1 < best) {
+      best = e1;
+      best_l = 1;
+    }
+  } else if constexpr (MT > 0) {
+    uint32_t cnt[MT];
+#pragma unroll
+    for (int l = 0; l < MT; ++l) cnt[l] = 0;
+    for (uint32_t a = lo; a < hi; ++a) {
+      const uint32_t c = lab_in[g_nbr[a]];
+#pragma unroll
+      for (int l = 0; l < MT; ++l) cnt[l] += (c == uint32_t(l));
+    }
+    best = label_energy(x, terms[0], terms[MT], terms[2 * MT], beta, deg - cnt[0]);
+    best_l = 0;
+#pragma unroll
+    for (int l = 1; l < MT; ++l) {
+      const double e = label_energy(x, terms[l], terms[MT + l], terms[2 * MT + l], beta,
+                                    deg - cnt[l]);
+      if (e < best) {
+        best = e;
+        best_l = l;
+      }
+    }
+  } else {
+    best = 0.0;
+    best_l = 0;
+    for (uint32_t l = 0; l < M; ++l) {
+      uint32_t same = 0;
+      for (uint32_t a = lo; a < hi; ++a) same += (lab_in[g_nbr[a]] == l);
+      const double e = label_energy(x, terms[l], terms[M + l], terms[2 * M + l], beta, deg - same);
+      if (l == 0 || e < best) {
+        best = e;
+        best_l = l;
+      }
+    }
+  }
+  minE[v] = best;
+  lab_out[v] = static_cast<uint8_t>(best_l);
+}
+
+// ---------------------------------------------------------------------------
+// Hood energy sums + convergence window.
+//   neighborhood_energy_sums  engine.cpp:147-152 (fold_range in slot order)
+//   check_convergence         engine.cpp:154-169 (!(|last-prev| < tol) -> 0)
+//   all_set                   optimize.cpp:25-27 (block count -> one atomic)
+// ---------------------------------------------------------------------------
+__device__ double hood_fold_long(const uint32_t* __restrict__ h_mem,
+                                 const double* __restrict__ minE, uint32_t lo, uint32_t hi) {
+  // fold_range for more than kFoldLeaf slots: leaves + pairwise tree.
+  TreeStack<double, AddOp> st;
+  for (uint32_t b = lo; b < hi; b += kFoldLeaf) {
+    const uint32_t e = min(hi, b + kFoldLeaf);
+    double acc = minE[h_mem[b]];
+    for (uint32_t s = b + 1; s < e; ++s) acc = __dadd_rn(acc, minE[h_mem[s]]);
+    st.push(acc, AddOp{});
+  }
+  return st.finish(AddOp{});
+}
+
+template <bool kFlags>
+__global__ void __launch_bounds__(kHoodThreads)
+    k_hood_sums(const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ h_mem,
+                const double* __restrict__ minE, double* __restrict__ hist,
+                uint8_t* __restrict__ flags, uint64_t Hs, int t, int L, double tol,
+                uint32_t* __restrict__ unconv, int fixed) {
+  if (map_iter_skipped(unconv, t, fixed)) return;
+  const uint64_t h = uint64_t(blockIdx.x) * kHoodThreads + threadIdx.x;
+  int not_conv = 0;
+  if (h < Hs) {
+    const uint32_t lo = s_off[h], hi = s_off[h + 1];
+    double sum;
+    if (hi - lo <= kFoldLeaf) {
+      sum = minE[h_mem[lo]];
+      uint32_t s = lo + 1;
+      for (; s + 4 <= hi; s += 4) {
+        const double a0 = minE[h_mem[s]], a1 = minE[h_mem[s + 1]];
+        const double a2 = minE[h_mem[s + 2]], a3 = minE[h_mem[s + 3]];
+        sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, a0), a1), a2), a3);
+      }
+      for (; s < hi; ++s) sum = __dadd_rn(sum, minE[h_mem[s]]);
+    } else {
+      sum = hood_fold_long(h_mem, minE, lo, hi);
+    }
+    const int R1 = L + 1;
+    hist[uint64_t(t % R1) * Hs + h] = sum;
+    int ok = 0;
+    if (t >= L) {
+      ok = 1;
+      for (int i = 1; i <= L; ++i) {
+        const double prev = hist[uint64_t((t - i) % R1) * Hs + h];
+        if (!(fabs(__dsub_rn(sum, prev)) < tol)) {
+          ok = 0;
+          break;
+        }
+      }
+    }
+    if (kFlags) flags[h] = static_cast<uint8_t>(ok);
+    not_conv = !ok;
+  }
+  const int block_unconv = __syncthreads_count(not_conv);
+  if (threadIdx.x == 0 && block_unconv) atomicAdd(&unconv[t], uint32_t(block_unconv));
+}
+
+// ---------------------------------------------------------------------------
+// M-step: stable grouping of region means by label + fixed-topology folds.
+//   update_parameters  engine.cpp:193-223 (sort_by_key stable, reduce_by_key
+//                      fold_range per run, kernels.hpp:226-253)
+//   dpp::reduce        kernels.hpp:124-139 (total energy, optimize.cpp:64-65)
+// ---------------------------------------------------------------------------
+constexpr int kTileThreads = 256;
+constexpr int kTileRounds = 16;
+constexpr int kTileVerts = kTileThreads * kTileRounds;  // 4096 vertices per tile
+
+__device__ __forceinline__ int executed_iters(const uint32_t* unconv, int map_max, int fixed) {
+  if (fixed) return map_max;
+  for (int t = 0; t < map_max; ++t)
+    if (unconv[t] == 0) return t + 1;
+  return map_max;
+}
+
+__device__ __forceinline__ const uint8_t* final_labels(const uint8_t* even, const uint8_t* odd,
+                                                       const uint32_t* unconv, int map_max,
+                                                       int fixed) {
+  if (!unconv) return even;
+  return (executed_iters(unconv, map_max, fixed) & 1) ? odd : even;
+}
+
+// Per tile and label: count (pass 0) or stable scatter (pass 1).
+template <int kPass>
+__global__ void __launch_bounds__(kTileThreads)
+    k_label_tiles(const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
+                  int map_max, int fixed, uint32_t R, uint32_t M, const double* __restrict__ mean,
+                  uint32_t* __restrict__ tile_counts, const uint32_t* __restrict__ tile_base,
+                  const uint32_t* __restrict__ layout, double* __restrict__ x) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* run = sm;                  // M running per-label counts of this tile
+  uint32_t* wcnt = sm + M;             // [warp][M] counts of the current round
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kTileThreads / 32;
+  const uint8_t* lab = final_labels(lab_even, lab_odd, unconv, map_max, fixed);
+  for (uint32_t l = threadIdx.x; l < M; l += kTileThreads) run[l] = 0;
+  const uint64_t tile = blockIdx.x;
+  const uint32_t* label_start = layout + M;
+  for (int r = 0; r < kTileRounds; ++r) {
+    for (uint32_t i = threadIdx.x; i < kWarps * M; i += kTileThreads) wcnt[i] = 0;
+    __syncthreads();
+    const uint64_t v = tile * kTileVerts + uint64_t(r) * kTileThreads + threadIdx.x;
+    const bool valid = v < R;
+    const uint32_t l = valid ? lab[v] : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, l);
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t rank_in_warp = __popc(peers & lt);
+    if (valid && rank_in_warp == 0) wcnt[warp * M + l] = __popc(peers);
+    __syncthreads();
+    if (kPass == 1 && valid) {
+      uint32_t before = run[l];
+      for (int w = 0; w < warp; ++w) before += wcnt[w * M + l];
+      const uint32_t pos = label_start[l] + tile_base[tile * M + l] + before + rank_in_warp;
+      x[pos] = mean[v];
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < M; q += kTileThreads) {
+      uint32_t add = 0;
+      for (int w = 0; w < kWarps; ++w) add += wcnt[w * M + q];
+      run[q] += add;
+    }
+    __syncthreads();
+  }
+  if (kPass == 0)
+    for (uint32_t q = threadIdx.x; q < M; q += kTileThreads) tile_counts[tile * M + q] = run[q];
+}
+
+// Single block: per-label exclusive scan over tiles; label starts; leaf layout.
+// layout = n[M] | label_start[M+1] | leaf_start[M+2] (series M = hood energies)
+__global__ void __launch_bounds__(1024)
+    k_tile_offsets(const uint32_t* __restrict__ tile_counts, uint32_t* __restrict__ tile_base,
+                   uint32_t tiles, uint32_t M, uint64_t Hs, uint32_t* __restrict__ layout) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry;
+  for (uint32_t l = 0; l < M; ++l) {
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint32_t b = 0; b < tiles; b += blockDim.x) {
+      const uint32_t i = b + threadIdx.x;
+      const uint32_t c = i < tiles ? tile_counts[uint64_t(i) * M + l] : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_exclusive_scan(c, warp_sums, &tot);
+      if (i < tiles) tile_base[uint64_t(i) * M + l] = carry + ex;
+      __syncthreads();
+      if (threadIdx.x == 0) carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) layout[l] = carry;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    uint32_t* label_start = layout + M;
+    uint32_t* leaf_start = layout + 2 * M + 1;
+    uint32_t s = 0, lf = 0;
+    for (uint32_t l = 0; l < M; ++l) {
+      label_start[l] = s;
+      leaf_start[l] = lf;
+      s += layout[l];
+      lf += (layout[l] + kFoldLeaf - 1) / kFoldLeaf;
+    }
+    label_start[M] = s;
+    leaf_start[M] = lf;
+    lf += uint32_t((Hs + kFoldLeaf - 1) / kFoldLeaf);
+    leaf_start[M + 1] = lf;
+  }
+}
+
+__device__ __forceinline__ uint32_t series_of(const uint32_t* leaf_start, uint32_t nseries,
+                                              uint32_t leaf) {
+  uint32_t s = 0;
+  while (s + 1 < nseries && leaf >= leaf_start[s + 1]) ++s;
+  return s;
+}
+
+// One thread per 1024-element leaf: left fold seeded by the first element
+// (fold_leaf, kernels.hpp:37-42).  kSq: fold (x - mu)^2 (engine.cpp:213-217).
+template <bool kSq>
+__global__ void __launch_bounds__(256)
+    k_leaf_fold(const double* __restrict__ x, const uint32_t* __restrict__ layout, uint32_t M,
+                const double* __restrict__ hood_row, uint64_t Hs,
+                const double* __restrict__ params, double* __restrict__ partials) {
+  const uint32_t* n = layout;
+  const uint32_t* label_start = layout + M;
+  const uint32_t* leaf_start = layout + 2 * M + 1;
+  const uint32_t nseries = kSq ? M : M + 1;
+  const uint32_t leaf = blockIdx.x * blockDim.x + threadIdx.x;
+  if (leaf >= leaf_start[nseries]) return;
+  const uint32_t s = series_of(leaf_start, nseries, leaf);
+  const uint32_t k = leaf - leaf_start[s];
+  const double* src;
+  uint64_t len;
+  if (s < M) {
+    src = x + label_start[s];
+    len = n[s];
+  } else {
+    src = hood_row;
+    len = Hs;
+  }
+  const uint64_t b = uint64_t(k) * kFoldLeaf;
+  const uint64_t e = min(len, b + kFoldLeaf);
+  double acc;
+  if (kSq) {
+    const double mu = params[s];
+    double d = __dsub_rn(src[b], mu);
+    acc = __dmul_rn(d, d);
+    uint64_t i = b + 1;
+    for (; i + 4 <= e; i += 4) {
+      const double y0 = src[i], y1 = src[i + 1], y2 = src[i + 2], y3 = src[i + 3];
+      const double d0 = __dsub_rn(y0, mu), d1 = __dsub_rn(y1, mu);
+      const double d2 = __dsub_rn(y2, mu), d3 = __dsub_rn(y3, mu);
+      acc = __dadd_rn(acc, __dmul_rn(d0, d0));
+      acc = __dadd_rn(acc, __dmul_rn(d1, d1));
+      acc = __dadd_rn(acc, __dmul_rn(d2, d2));
+      acc = __dadd_rn(acc, __dmul_rn(d3, d3));
+    }
+    for (; i < e; ++i) {
+      d = __dsub_rn(src[i], mu);
+      acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+  } else {
+    acc = src[b];
+    uint64_t i = b + 1;
+    for (; i + 4 <= e; i += 4) {
+      const double y0 = src[i], y1 = src[i + 1], y2 = src[i + 2], y3 = src[i + 3];
+      acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, y0), y1), y2), y3);
+    }
+    for (; i < e; ++i) acc = __dadd_rn(acc, src[i]);
+  }
+  partials[leaf] = acc;
+}
+
+// One block per series: pairwise tree over its leaf partials, bottom-up
+// adjacent pairing (== fold_tree's split at bit_floor(n-1), kernels.hpp:45-51),
+// then the parameter / total-energy epilogue.
+template <bool kSq>
+__global__ void __launch_bounds__(1024)
+    k_tree_finalize(double* partials, const uint32_t* __restrict__ layout, uint32_t M,
+                    double* params, double* em_out, const uint32_t* unconv, int map_max,
+                    int fixed) {
+  const uint32_t s = blockIdx.x;
+  const uint32_t* n = layout;
+  const uint32_t* leaf_start = layout + 2 * M + 1;
+  uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
+  double* p = partials + leaf_start[s];
+  while (cnt > 1) {
+    const uint32_t pairs = cnt / 2;
+    for (uint32_t base = 0; base < pairs; base += blockDim.x) {
+      const uint32_t i = base + threadIdx.x;
+      double v = 0.0;
+      if (i < pairs) v = __dadd_rn(p[2 * i], p[2 * i + 1]);
+      __syncthreads();
+      if (i < pairs) p[i] = v;
+      __syncthreads();
+    }
+    if (cnt & 1u) {
+      if (threadIdx.x == 0) p[pairs] = p[cnt - 1];
+      __syncthreads();
+    }
+    cnt = pairs + (cnt & 1u);
+  }
+  if (threadIdx.x != 0) return;
+  if (s < M) {
+    if (n[s] == 0) return;  // empty label keeps its previous parameters
+    const double count = static_cast<double>(n[s]);
+    if (!kSq) {
+      params[s] = __ddiv_rn(p[0], count);
+    } else {
+      const double sd = __dsqrt_rn(__ddiv_rn(p[0], count));
+      params[M + s] = sd < kSigmaFloor ? kSigmaFloor : sd;
+    }
+  } else {
+    // total energy: dpp::reduce(..., 0.0) -> identity only for empty input
+    em_out[0] = (leaf_start[M + 1] == leaf_start[M]) ? 0.0 : p[0];
+    em_out[1] = static_cast<double>(unconv ? executed_iters(unconv, map_max, fixed) : 0);
+  }
+}
+
+__global__ void k_copy_params(const double* params, double* em_out, uint32_t M) {
+  for (uint32_t i = threadIdx.x; i < 2 * M; i += blockDim.x) em_out[2 + i] = params[i];
+}
+
+__global__ void k_init_labels(uint8_t* lab, uint32_t R, uint32_t M, uint64_t seed) {
+  const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= R) return;
+  // draw 2M+v of the init_random stream (engine.cpp:29: mu, sigma, then labels)
+  lab[v] = static_cast<uint8_t>(splitmix_draw(seed, 2ull * M + v) % M);
+}
+
+__global__ void k_u8_to_u32(const uint8_t* __restrict__ in, uint32_t* __restrict__ out,
+                            uint64_t n) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
+__global__ void k_u32_to_u8_checked(const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
+                                    uint64_t n, uint32_t M, uint32_t* err) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t l = in[i];
+  if (l >= M) {
+    atomicOr(err, 1u);
+    out[i] = 0;
+  } else {
+    out[i] = static_cast<uint8_t>(l);
+  }
+}
+
+// ---- structure preparation -------------------------------------------------
+__global__ void k_validate(const uint32_t* __restrict__ g_off, const uint32_t* __restrict__ g_nbr,
+                           uint32_t R, uint64_t A, const uint32_t* __restrict__ h_off,
+                           const uint32_t* __restrict__ h_mem, uint64_t H, uint64_t S,
+                           uint32_t* err, uint32_t* empty_hoods) {
+  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  uint32_t e = 0, empties = 0;
+  for (uint64_t i = tid; i < S; i += stride)
+    if (h_mem[i] >= R) e |= 1u;
+  for (uint64_t i = tid; i < A; i += stride)
+    if (g_nbr[i] >= R) e |= 2u;
+  for (uint64_t h = tid; h < H; h += stride) {
+    const uint32_t a = h_off[h], b = h_off[h + 1];
+    if (b < a) e |= 4u;
+    empties += (a == b);
+  }
+  for (uint64_t v = tid; v < R; v += stride)
+    if (g_off[v + 1] < g_off[v]) e |= 8u;
+  if (tid == 0) {
+    if (h_off[0] != 0 || h_off[H] != S) e |= 4u;
+    if (g_off[0] != 0 || g_off[R] != A) e |= 8u;
+  }
+  if (e) atomicOr(err, e);
+  if (empties) atomicAdd(empty_hoods, empties);
+}
+
+__global__ void k_cover(const uint32_t* __restrict__ h_mem, uint64_t S, uint8_t* cover) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < S; i += stride)
+    cover[h_mem[i]] = 1;
+}
+
+__global__ void k_nonempty_flags(const uint32_t* __restrict__ h_off, uint64_t H, uint32_t* f) {
+  const uint64_t h = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (h < H) f[h] = h_off[h + 1] != h_off[h];
+}
+
+__global__ void k_compact_offsets(const uint32_t* __restrict__ h_off, uint64_t H, uint64_t S,
+                                  const uint32_t* __restrict__ pos, uint32_t* s_off) {
+  const uint64_t h = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (h < H && h_off[h + 1] != h_off[h]) s_off[pos[h]] = h_off[h];
+  if (h == 0) s_off[pos[H]] = static_cast<uint32_t>(S);
+}
+
+}  // namespace
+
+// ---- launchers -----------------------------------------------------------------
+void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out, int t,
+                          cudaStream_t s) {
+  const unsigned g = grid_for(a.R, kVtxThreads);
+#define VA_ARGS                                                                              \
+  a.g_off, a.g_nbr, a.mean, a.cover, lab_in, lab_out, a.minE, a.R, a.M, a.terms, a.beta, \
+      a.unconv, t, a.fixed
+  switch (a.M) {
+    case 2: k_vertex_argmin<2><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
+    case 3: k_vertex_argmin<3><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
+    case 4: k_vertex_argmin<4><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
+    case 5: k_vertex_argmin<5><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
+    case 6: k_vertex_argmin<6><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
+    case 7: k_vertex_argmin<7><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
+    case 8: k_vertex_argmin<8><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
+    default: k_vertex_argmin<0><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
+  }
+#undef VA_ARGS
+  CK_LAUNCH();
+}
+
+void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s) {
+  const unsigned g = grid_for(a.Hs, kHoodThreads);
+  if (a.flags)
+    k_hood_sums<true><<<g, kHoodThreads, 0, s>>>(a.s_off, a.h_mem, a.minE, a.hist, a.flags, a.Hs,
+                                                 t, a.L, a.tol, a.unconv, a.fixed);
+  else
+    k_hood_sums<false><<<g, kHoodThreads, 0, s>>>(a.s_off, a.h_mem, a.minE, a.hist, nullptr,
+                                                  a.Hs, t, a.L, a.tol, a.unconv, a.fixed);
+  CK_LAUNCH();
+}
+
+namespace {
+
+void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
+                const uint8_t* lab_odd, const uint32_t* unconv, int map_max, int fixed,
+                const double* hood_row_base, uint64_t Hs, int L, double* params, double* em_out,
+                MStepBuffers& mb, cudaStream_t s, uint64_t* launches) {
+  const uint32_t tiles = static_cast<uint32_t>((uint64_t(R) + kTileVerts - 1) / kTileVerts);
+  const uint32_t tiles_g = tiles ? tiles : 1;
+  uint32_t* tile_counts = mb.tile_counts.ensure(uint64_t(tiles_g) * M);
+  uint32_t* tile_base = mb.tile_base.ensure(uint64_t(tiles_g) * M);
+  uint32_t* layout = mb.layout.ensure(4 * M + 4);
+  double* x = mb.x.ensure(R);
+  const uint64_t max_leaves = (uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M +
+                              (Hs + kFoldLeaf - 1) / kFoldLeaf + 1;
+  double* partials = mb.partials.ensure(max_leaves);
+  const size_t smem = (M + (kTileThreads / 32) * M) * sizeof(uint32_t);
+  uint64_t n = 0;
+  if (tiles) {
+    k_label_tiles<0><<<tiles, kTileThreads, smem, s>>>(lab_even, lab_odd, unconv, map_max, fixed,
+                                                       R, M, mean, tile_counts, nullptr, nullptr,
+                                                       nullptr);
+    CK_LAUNCH();
+    ++n;
+  }
+  k_tile_offsets<<<1, 1024, 0, s>>>(tile_counts, tile_base, tiles, M, Hs, layout);
+  CK_LAUNCH();
+  ++n;
+  if (tiles) {
+    k_label_tiles<1><<<tiles, kTileThreads, smem, s>>>(lab_even, lab_odd, unconv, map_max, fixed,
+                                                       R, M, mean, nullptr, tile_base, layout, x);
+    CK_LAUNCH();
+    ++n;
+  }
+  // hood row of the last executed MAP iteration: resolved on the device via
+  // a pointer table would need the count; instead both folds read the row
+  // chosen by k_pick_row (below) -- see launch_mstep.
+  (void)L;
+  const unsigned lg = grid_for(max_leaves, 256);
+  k_leaf_fold<false><<<lg, 256, 0, s>>>(x, layout, M, hood_row_base, Hs, params, partials);
+  CK_LAUNCH();
+  k_tree_finalize<false><<<M + 1, 1024, 0, s>>>(partials, layout, M, params, em_out, unconv,
+                                                map_max, fixed);
+  CK_LAUNCH();
+  k_leaf_fold<true><<<lg, 256, 0, s>>>(x, layout, M, nullptr, 0, params, partials);
+  CK_LAUNCH();
+  k_tree_finalize<true><<<M, 1024, 0, s>>>(partials, layout, M, params, em_out, unconv, map_max,
+                                           fixed);
+  CK_LAUNCH();
+  k_copy_params<<<1, 256, 0, s>>>(params, em_out, M);
+  CK_LAUNCH();
+  n += 5;
+  if (launches) *launches += n;
+}
+
+// Copies the hood-energy row of the last executed MAP iteration into a
+// contiguous buffer the leaf folds read (the ring slot depends on the
+// device-side iteration count).
+__global__ void k_pick_row(const double* __restrict__ hist, uint64_t Hs, int L,
+                           const uint32_t* __restrict__ unconv, int map_max, int fixed,
+                           double* __restrict__ row) {
+  const int T = executed_iters(unconv, map_max, fixed);
+  const double* src = hist + uint64_t((T - 1) % (L + 1)) * Hs;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < Hs; i += stride)
+    row[i] = src[i];
+}
+
+}  // namespace
+
+void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
+                  const uint8_t* lab_odd, const double* hist, uint64_t Hs, int L,
+                  const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
+                  MStepBuffers& mb, cudaStream_t s, uint64_t* launches) {
+  // The last row is copied out of the ring (Hs doubles) so the leaf kernel
+  // can address it without the device-side iteration count.
+  double* row = mb.row.ensure(Hs);
+  if (Hs) {
+    k_pick_row<<<std::min<unsigned>(grid_for(Hs, 256), 4 * kNumSMs), 256, 0, s>>>(
+        hist, Hs, L, unconv, map_max, fixed, row);
+    CK_LAUNCH();
+    if (launches) ++*launches;
+  }
+  mstep_core(mean, R, M, lab_even, lab_odd, unconv, map_max, fixed, row, Hs, L, params, em_out,
+             mb, s, launches);
+}
+
+void launch_update_parameters_u32(const double* mean, uint32_t R, uint32_t M,
+                                  const uint32_t* labels, double* params, MStepBuffers& mb,
+                                  DevBuf<uint8_t>& lab_tmp, cudaStream_t s) {
+  uint8_t* lab = lab_tmp.ensure(R);
+  uint32_t* e = mb.err.ensure(1);
+  CK(cudaMemsetAsync(e, 0, sizeof(uint32_t), s));
+  if (R) {
+    k_u32_to_u8_checked<<<grid_for(R, 256), 256, 0, s>>>(labels, lab, R, M, e);
+    CK_LAUNCH();
+  }
+  uint32_t h_err = 0;
+  CK(cudaMemcpyAsync(&h_err, e, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h_err) fail(DPMRF_INVALID_ARGUMENT, "update_parameters: label out of range");
+  if (R == 0) return;
+  double* eo = mb.em_scratch.ensure(2 + 2 * M);
+  mstep_core(mean, R, M, lab, lab, nullptr, 1, 1, nullptr, 0, 1, params, eo, mb, s, nullptr);
+}
+
+void launch_init_labels(uint8_t* lab, uint32_t R, uint32_t M, uint64_t seed, cudaStream_t s) {
+  if (!R) return;
+  k_init_labels<<<grid_for(R, 256), 256, 0, s>>>(lab, R, M, seed);
+  CK_LAUNCH();
+}
+
+void launch_u8_to_u32(const uint8_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
+  if (!n) return;
+  k_u8_to_u32<<<grid_for(n, 256), 256, 0, s>>>(in, out, n);
+  CK_LAUNCH();
+}
+
+void launch_validate(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, uint64_t A,
+                     const uint32_t* h_off, const uint32_t* h_mem, uint64_t H, uint64_t S,
+                     uint32_t* err, uint32_t* empty_hoods, cudaStream_t s) {
+  const uint64_t work = std::max<uint64_t>({S, A, H, uint64_t(R), 1});
+  k_validate<<<std::min<unsigned>(grid_for(work, 256), 8 * kNumSMs), 256, 0, s>>>(
+      g_off, g_nbr, R, A, h_off, h_mem, H, S, err, empty_hoods);
+  CK_LAUNCH();
+}
+
+void launch_cover(const uint32_t* h_mem, uint64_t S, uint8_t* cover, uint32_t R, cudaStream_t s) {
+  CK(cudaMemsetAsync(cover, 0, R ? R : 1, s));
+  if (!S) return;
+  k_cover<<<std::min<unsigned>(grid_for(S, 256), 8 * kNumSMs), 256, 0, s>>>(h_mem, S, cover);
+  CK_LAUNCH();
+}
+
+void launch_series_offsets(const uint32_t* h_off, uint64_t H, uint64_t S, uint32_t* s_off,
+                           DevBuf<uint32_t>& tmp, ScanWorkspace& ws, cudaStream_t s) {
+  uint32_t* f = tmp.ensure(H + 1);
+  if (H) {
+    k_nonempty_flags<<<grid_for(H, 256), 256, 0, s>>>(h_off, H, f);
+    CK_LAUNCH();
+  }
+  exclusive_scan_u32(f, f, H, f + H, ws, s);
+  k_compact_offsets<<<grid_for(H ? H : 1, 256), 256, 0, s>>>(h_off, H, S, f, s_off);
+  CK_LAUNCH();
+}
+
+}  // namespace dpmrf_b200

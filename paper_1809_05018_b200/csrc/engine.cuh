@@ -1,0 +1,80 @@
+// engine.cuh -- host launchers of the optimization-phase kernels (internal).
+#pragma once
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace dpmrf_b200 {
+
+// Label terms live in HBM as [mu(M) | two_var(M) | log_sigma(M)], written by
+// the host once per EM iteration (make_label_terms, model.hpp:48-60, keeps
+// glibc's std::log for log_sigma).
+
+struct MapArgs {
+  const uint32_t* g_off;
+  const uint32_t* g_nbr;
+  const double* mean;
+  const uint8_t* cover;
+  const uint32_t* s_off;   // series offsets (nonempty hoods), Hs+1
+  const uint32_t* h_mem;
+  uint32_t R;
+  uint64_t Hs;
+  uint32_t M;
+  double beta;
+  double tol;
+  int L;         // convergence_window
+  int fixed;     // 1 = no early exit
+  const double* terms;
+  double* minE;    // R
+  double* hist;    // (L+1) x Hs ring of hood energies
+  uint8_t* flags;  // Hs (nullptr = not recorded)
+  uint32_t* unconv;  // per MAP iteration count of unconverged hoods
+};
+
+// One MAP iteration = energies against the frozen labels + per-vertex argmin
+// + label commit (engine.cpp:88-191 fused), then the hood
+// sums + window test (engine.cpp:147-169).
+void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out, int t,
+                          cudaStream_t s);
+void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s);
+
+struct MStepBuffers {
+  DevBuf<uint32_t> tile_counts;  // tiles x M
+  DevBuf<uint32_t> tile_base;    // tiles x M
+  DevBuf<uint32_t> layout;       // n[M] | label_start[M+1] | leaf_start[M+2]
+  DevBuf<double> x;              // R values grouped by label (stable)
+  DevBuf<double> partials;       // leaf partials of all series
+  DevBuf<double> row;            // hood-energy row of the last executed MAP iteration
+  DevBuf<uint32_t> err;
+  DevBuf<double> em_scratch;
+};
+
+// update_parameters (engine.cpp:193-223) over the labels left by the last
+// executed MAP iteration, plus the EM total energy (optimize.cpp:64-65) over
+// that iteration's hood-energy row.  params (2M, device) is updated in
+// place; em_out receives [total, map_iters, mu(M), sigma(M)].
+void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
+                  const uint8_t* lab_odd, const double* hist, uint64_t Hs, int L,
+                  const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
+                  MStepBuffers& mb, cudaStream_t s, uint64_t* launches);
+
+// Standalone update_parameters over caller labels (u32, validated < M).
+void launch_update_parameters_u32(const double* mean, uint32_t R, uint32_t M,
+                                  const uint32_t* labels, double* params, MStepBuffers& mb,
+                                  DevBuf<uint8_t>& lab_tmp, cudaStream_t s);
+
+void launch_init_labels(uint8_t* lab, uint32_t R, uint32_t M, uint64_t seed, cudaStream_t s);
+void launch_u8_to_u32(const uint8_t* in, uint32_t* out, uint64_t n, cudaStream_t s);
+
+// Structure preparation (once per graph/hoods pair).
+// err bits: 1 = member out of range, 2 = neighbor out of range,
+//           4 = hood offsets malformed, 8 = graph offsets malformed
+void launch_validate(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, uint64_t A,
+                     const uint32_t* h_off, const uint32_t* h_mem, uint64_t H, uint64_t S,
+                     uint32_t* err, uint32_t* empty_hoods, cudaStream_t s);
+void launch_cover(const uint32_t* h_mem, uint64_t S, uint8_t* cover, uint32_t R, cudaStream_t s);
+// Offsets of the nonempty hoods (the runs reduce_by_key sees, engine.cpp:150).
+void launch_series_offsets(const uint32_t* h_off, uint64_t H, uint64_t S, uint32_t* s_off,
+                           DevBuf<uint32_t>& tmp, ScanWorkspace& ws, cudaStream_t s);
+
+}  // namespace dpmrf_b200

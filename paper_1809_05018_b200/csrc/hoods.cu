@@ -1,0 +1,299 @@
+// hoods.cu -- build_neighborhoods on the device (north_star item 1).
+//
+// Reference: proj/src/graph/neighborhoods.cpp:10-57.  The reference writes
+// one u64 key (clique << 32 | vertex) per candidate (each clique member plus
+// its graph neighbors), sorts ALL keys globally, uniques them and rebuilds the
+// offsets.  Sorting by (clique, vertex) only ever orders candidates WITHIN a
+// clique, so the device version sorts each clique's candidate list on its own:
+//   1. count    : per clique, sum over members of 1 + degree   (neighborhoods.cpp:23-25)
+//   2. scan     : candidate offsets                            (:26)
+//   3. sort     : one warp per clique -- register bitonic sort via shuffles
+//                 for <= 32 candidates (every grid / brick hood), a
+//                 shared-memory bitonic sort for <= 1024, and a block-wide
+//                 global-memory bitonic sort beyond that; duplicates are
+//                 dropped with a ballot compaction              (:40-41)
+//   4. scan     : hood offsets from the unique counts          (:49-52)
+//   5. compact  : members                                     (:44-48)
+// source_clique is the identity (:53-55).
+#include <algorithm>
+#include <vector>
+
+#include "context.cuh"
+
+namespace dpmrf_b200 {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr uint32_t kSmemCap = 1024;  // candidates per warp in the shared-memory path
+constexpr uint32_t kPad = 0xFFFFFFFFu;
+
+__global__ void k_count_candidates(const uint32_t* __restrict__ c_off,
+                                   const uint32_t* __restrict__ c_mem, uint64_t C,
+                                   const uint32_t* __restrict__ g_off, uint32_t R,
+                                   uint32_t* __restrict__ cnt, uint32_t* err,
+                                   unsigned long long* max_cnt) {
+  const uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  uint64_t n = 0;
+  for (uint32_t s = c_off[c]; s < c_off[c + 1]; ++s) {
+    const uint32_t m = c_mem[s];
+    if (m >= R) {
+      atomicOr(err, 1u);
+      cnt[c] = 0;
+      return;
+    }
+    n += 1 + (g_off[m + 1] - g_off[m]);
+  }
+  cnt[c] = static_cast<uint32_t>(n);
+  atomicMax(max_cnt, static_cast<unsigned long long>(n));
+}
+
+// Position p of clique c's candidate list: member, then its neighbors, in
+// member order (neighborhoods.cpp:31-36).
+__device__ __forceinline__ uint32_t candidate_at(const uint32_t* c_mem, uint32_t lo, uint32_t hi,
+                                                 const uint32_t* g_off, const uint32_t* g_nbr,
+                                                 uint32_t p) {
+  for (uint32_t s = lo; s < hi; ++s) {
+    const uint32_t m = c_mem[s];
+    const uint32_t deg = g_off[m + 1] - g_off[m];
+    if (p == 0) return m;
+    if (p <= deg) return g_nbr[g_off[m] + p - 1];
+    p -= 1 + deg;
+  }
+  return kPad;
+}
+
+__device__ __forceinline__ uint32_t warp_bitonic32(uint32_t x, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      x = (lower == up) ? min(x, y) : max(x, y);
+    }
+  }
+  return x;
+}
+
+// Unique-compacts a sorted run held in lanes (chunk of 32); returns the
+// number written.  keep: lane holds a valid element.
+__device__ __forceinline__ uint32_t warp_unique_chunk(uint32_t x, bool valid, uint32_t prev_last,
+                                                      bool has_prev, uint32_t* out, int lane) {
+  uint32_t left = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane == 0) left = prev_last;
+  const bool keep = valid && ((lane == 0 && !has_prev) || x != left);
+  const unsigned mask = __ballot_sync(0xffffffffu, keep);
+  if (keep) out[__popc(mask & ((1u << lane) - 1u))] = x;
+  return __popc(mask);
+}
+
+// Sort + unique of every clique with <= kSmemCap candidates; larger ones are
+// left to k_big_clique (uniq written there).
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_sort_unique(const uint32_t* __restrict__ c_off, const uint32_t* __restrict__ c_mem,
+                  uint64_t C, const uint32_t* __restrict__ g_off,
+                  const uint32_t* __restrict__ g_nbr, const uint32_t* __restrict__ cnt,
+                  const uint32_t* __restrict__ cand_off, uint32_t* __restrict__ scratch,
+                  uint32_t* __restrict__ uniq) {
+  __shared__ uint32_t buf[kWarpsPerBlock][kSmemCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t c = uint64_t(blockIdx.x) * kWarpsPerBlock + w;
+  if (c >= C) return;
+  const uint32_t n = cnt[c];
+  const uint32_t lo = c_off[c], hi = c_off[c + 1];
+  uint32_t* out = scratch + cand_off[c];
+  if (n <= 32) {
+    uint32_t x = lane < int(n) ? candidate_at(c_mem, lo, hi, g_off, g_nbr, lane) : kPad;
+    x = warp_bitonic32(x, lane);
+    const uint32_t u = warp_unique_chunk(x, lane < int(n), 0, false, out, lane);
+    if (lane == 0) uniq[c] = u;
+    return;
+  }
+  if (n > kSmemCap) return;  // k_big_clique
+  uint32_t* b = buf[w];
+  // gather: the warp walks the members; each member's segment is copied by lanes
+  uint32_t pos = 0;
+  for (uint32_t s = lo; s < hi; ++s) {
+    const uint32_t m = c_mem[s];
+    const uint32_t a0 = g_off[m], deg = g_off[m + 1] - a0;
+    if (lane == 0) b[pos] = m;
+    for (uint32_t i = lane; i < deg; i += 32) b[pos + 1 + i] = g_nbr[a0 + i];
+    pos += 1 + deg;
+  }
+  uint32_t P = 64;
+  while (P < n) P <<= 1;
+  for (uint32_t i = n + lane; i < P; i += 32) b[i] = kPad;
+  __syncwarp();
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = lane; i < P; i += 32) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const uint32_t xi = b[i], xl = b[l];
+          const bool asc = (i & k) == 0;
+          if ((xi > xl) == asc) {
+            b[i] = xl;
+            b[l] = xi;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  uint32_t written = 0, last = 0;
+  for (uint32_t base = 0; base < n; base += 32) {
+    const uint32_t i = base + lane;
+    const uint32_t x = i < n ? b[i] : kPad;
+    written += warp_unique_chunk(x, i < n, last, base > 0, out + written, lane);
+    last = __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) uniq[c] = written;
+}
+
+// One block per oversized clique: bitonic sort in a global scratch region.
+__global__ void __launch_bounds__(1024)
+    k_big_clique(const uint32_t* __restrict__ big, const uint64_t* __restrict__ big_tmp_off,
+                 const uint32_t* __restrict__ c_off, const uint32_t* __restrict__ c_mem,
+                 const uint32_t* __restrict__ g_off, const uint32_t* __restrict__ g_nbr,
+                 const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ cand_off,
+                 uint32_t* __restrict__ scratch, uint32_t* __restrict__ tmp,
+                 uint32_t* __restrict__ uniq) {
+  const uint32_t c = big[blockIdx.x];
+  const uint32_t n = cnt[c];
+  uint32_t* b = tmp + big_tmp_off[blockIdx.x];
+  const uint64_t P = big_tmp_off[blockIdx.x + 1] - big_tmp_off[blockIdx.x];
+  uint32_t pos = 0;
+  for (uint32_t s = c_off[c]; s < c_off[c + 1]; ++s) {
+    const uint32_t m = c_mem[s];
+    const uint32_t a0 = g_off[m], deg = g_off[m + 1] - a0;
+    if (threadIdx.x == 0) b[pos] = m;
+    for (uint32_t i = threadIdx.x; i < deg; i += blockDim.x) b[pos + 1 + i] = g_nbr[a0 + i];
+    pos += 1 + deg;
+  }
+  for (uint64_t i = n + threadIdx.x; i < P; i += blockDim.x) b[i] = kPad;
+  __syncthreads();
+  for (uint64_t k = 2; k <= P; k <<= 1) {
+    for (uint64_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint64_t i = threadIdx.x; i < P; i += blockDim.x) {
+        const uint64_t l = i ^ j;
+        if (l > i) {
+          const uint32_t xi = b[i], xl = b[l];
+          const bool asc = (i & k) == 0;
+          if ((xi > xl) == asc) {
+            b[i] = xl;
+            b[l] = xi;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // unique, in order, by warp 0
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  uint32_t* out = scratch + cand_off[c];
+  uint32_t written = 0, last = 0;
+  for (uint32_t base = 0; base < n; base += 32) {
+    const uint32_t i = base + lane;
+    const uint32_t x = i < n ? b[i] : kPad;
+    written += warp_unique_chunk(x, i < n, last, base > 0, out + written, lane);
+    last = __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) uniq[c] = written;
+}
+
+__global__ void k_compact_members(const uint32_t* __restrict__ scratch,
+                                  const uint32_t* __restrict__ cand_off,
+                                  const uint32_t* __restrict__ h_off, uint64_t C,
+                                  uint32_t* __restrict__ members) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (c >= C) return;
+  const uint32_t src = cand_off[c], dst = h_off[c], n = h_off[c + 1] - dst;
+  for (uint32_t i = lane; i < n; i += 32) members[dst + i] = scratch[src + i];
+}
+
+}  // namespace
+
+void build_neighborhoods_device(dpmrf_context* ctx, uint64_t C, const uint32_t* c_off_host,
+                                const uint32_t* c_mem_host) {
+  cudaStream_t st = ctx->stream;
+  const uint64_t CS = c_off_host[C];
+  uint32_t* c_off = ctx->tmp_u32[0].ensure(C + 1);
+  uint32_t* c_mem = ctx->tmp_u32[1].ensure(CS);
+  CK(cudaMemcpyAsync(c_off, c_off_host, (C + 1) * 4, cudaMemcpyHostToDevice, st));
+  if (CS) CK(cudaMemcpyAsync(c_mem, c_mem_host, CS * 4, cudaMemcpyHostToDevice, st));
+  uint32_t* cnt = ctx->tmp_u32[2].ensure(C + 1);
+  uint32_t* cand_off = ctx->tmp_u32[3].ensure(C + 1);
+  uint32_t* err = ctx->prep_err.ensure(2);
+  unsigned long long* maxc = ctx->tmp_u64[0].ensure(1);
+  CK(cudaMemsetAsync(err, 0, 8, st));
+  CK(cudaMemsetAsync(maxc, 0, 8, st));
+  if (C) {
+    k_count_candidates<<<grid_for(C, 256), 256, 0, st>>>(c_off, c_mem, C, ctx->g_off.get(),
+                                                         ctx->R, cnt, err, maxc);
+    CK_LAUNCH();
+  }
+  exclusive_scan_u32(cnt, cand_off, C, cand_off + C, ctx->scan, st);
+  uint32_t h_err = 0, h_total = 0;
+  unsigned long long h_max = 0;
+  CK(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h_total, cand_off + C, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h_max, maxc, 8, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+  if (h_err) fail(DPMRF_OUT_OF_RANGE, "build_neighborhoods: clique member >= num_vertices");
+  uint32_t* scratch = ctx->tmp_u32[4].ensure(h_total);
+  uint32_t* uniq = ctx->tmp_u32[5].ensure(C + 1);
+  if (C) {
+    k_sort_unique<<<grid_for(C, kWarpsPerBlock), kWarpsPerBlock * 32, 0, st>>>(
+        c_off, c_mem, C, ctx->g_off.get(), ctx->g_nbr.get(), cnt, cand_off, scratch, uniq);
+    CK_LAUNCH();
+  }
+  if (h_max > kSmemCap) {
+    // rare: hoods with > 1024 candidates (very high-degree regions)
+    std::vector<uint32_t> h_cnt(C);
+    CK(cudaMemcpyAsync(h_cnt.data(), cnt, C * 4, cudaMemcpyDeviceToHost, st));
+    ctx->sync();
+    std::vector<uint32_t> big;
+    std::vector<uint64_t> toff{0};
+    for (uint64_t c = 0; c < C; ++c)
+      if (h_cnt[c] > kSmemCap) {
+        uint64_t P = 1;
+        while (P < h_cnt[c]) P <<= 1;
+        big.push_back(static_cast<uint32_t>(c));
+        toff.push_back(toff.back() + P);
+      }
+    DevBuf<uint32_t> big_list;
+    DevBuf<unsigned long long> big_off;
+    DevBuf<uint32_t> big_tmp;
+    uint32_t* bl = big_list.ensure(big.size());
+    auto* bo = reinterpret_cast<uint64_t*>(big_off.ensure(toff.size()));
+    uint32_t* bt = big_tmp.ensure(toff.back());
+    CK(cudaMemcpyAsync(bl, big.data(), big.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(bo, toff.data(), toff.size() * 8, cudaMemcpyHostToDevice, st));
+    k_big_clique<<<static_cast<unsigned>(big.size()), 1024, 0, st>>>(
+        bl, bo, c_off, c_mem, ctx->g_off.get(), ctx->g_nbr.get(), cnt, cand_off, scratch, bt,
+        uniq);
+    CK_LAUNCH();
+    ctx->sync();
+  }
+  uint32_t* h_off = ctx->h_off.ensure(C + 1);
+  exclusive_scan_u32(uniq, h_off, C, h_off + C, ctx->scan, st);
+  uint32_t S = 0;
+  CK(cudaMemcpyAsync(&S, h_off + C, 4, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+  uint32_t* members = ctx->h_mem.ensure(S);
+  if (C) {
+    k_compact_members<<<grid_for(C * 32, 256), 256, 0, st>>>(scratch, cand_off, h_off, C,
+                                                             members);
+    CK_LAUNCH();
+  }
+  ctx->H = C;
+  ctx->S = S;
+  ctx->sync();
+}
+
+}  // namespace dpmrf_b200

@@ -1,0 +1,499 @@
+"""Host-side mirror of the reference's engine interface over the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/dpmrf/mrf/engine.hpp (and
+graph/neighborhoods.hpp for build_neighborhoods), so code written against the
+reference reads the same:
+
+    backend = Backend.cuda(0)
+    result = optimize(backend, graph, hoods, OptimizerConfig(rng_seed=42))
+    result.labels, result.params.mu, result.params.sigma, result.trace
+
+Every call runs on the B200 through libdpmrf_cuda.so; there is no CPU path.
+Errors map to the reference's exception types:
+    dpmrf::InputError      -> InputError          (error.hpp:11)
+    std::invalid_argument  -> ValueError
+    std::out_of_range      -> IndexError
+    device failures        -> CudaError
+"""
+from __future__ import annotations
+
+import ctypes as ct
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _native as N
+
+# ---- errors ------------------------------------------------------------------------
+DPMRF_OK, DPMRF_INPUT_ERROR, DPMRF_INVALID_ARGUMENT, DPMRF_OUT_OF_RANGE = 0, 1, 2, 3
+DPMRF_CUDA_ERROR, DPMRF_NCCL_ERROR, DPMRF_INTERNAL_ERROR = 4, 5, 6
+
+TRACE_NONE, TRACE_EM, TRACE_FULL = 0, 1, 2
+RUN_FIXED_WORK, RUN_MULTILABEL, RUN_KERNEL_TIMING = 1, 2, 4
+
+K_SIGMA_FLOOR = 1e-3  # kSigmaFloor, model.hpp:9
+
+
+class InputError(RuntimeError):
+    """dpmrf::InputError (proj/include/dpmrf/error.hpp:11)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _check(status: int, where: str):
+    if status == DPMRF_OK:
+        return
+    msg = f"{where}: {N.cuda().dpmrf_last_error().decode(errors='replace')}"
+    if status == DPMRF_INPUT_ERROR:
+        raise InputError(msg)
+    if status == DPMRF_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == DPMRF_OUT_OF_RANGE:
+        raise IndexError(msg)
+    if status in (DPMRF_CUDA_ERROR, DPMRF_NCCL_ERROR):
+        raise CudaError(msg)
+    raise RuntimeError(msg)
+
+
+def _u32(x):
+    return np.ascontiguousarray(np.asarray(x, dtype=np.uint32))
+
+
+def _f64(x):
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+# ---- value types (model.hpp, region_graph.hpp, neighborhoods.hpp) ------------------
+@dataclass
+class OptimizerConfig:
+    """OptimizerConfig, model.hpp:19-27 (same defaults)."""
+
+    num_labels: int = 2
+    em_max_iters: int = 20
+    map_max_iters: int = 10
+    convergence_window: int = 3
+    convergence_tol: float = 1e-4
+    beta: float = 1.0
+    rng_seed: int = 0
+
+    def c(self) -> N.CConfig:
+        return N.CConfig(self.num_labels, self.em_max_iters, self.map_max_iters,
+                         self.convergence_window, self.convergence_tol, self.beta,
+                         self.rng_seed & ((1 << 64) - 1))
+
+
+@dataclass
+class LabelParams:
+    """LabelParams, model.hpp:12-17."""
+
+    mu: np.ndarray
+    sigma: np.ndarray
+
+    def num_labels(self) -> int:
+        return len(self.mu)
+
+
+@dataclass
+class RegionGraph:
+    """RegionGraph, region_graph.hpp:14-25 (CSR + per-region means)."""
+
+    offsets: np.ndarray
+    neighbors: np.ndarray
+    region_mean: np.ndarray
+    region_size: Optional[np.ndarray] = None
+
+    @property
+    def num_vertices(self) -> int:
+        return len(self.offsets) - 1
+
+    def degree(self, v: int) -> int:
+        return int(self.offsets[v + 1] - self.offsets[v])
+
+
+@dataclass
+class NeighborhoodSet:
+    """NeighborhoodSet, neighborhoods.hpp:15-23."""
+
+    offsets: np.ndarray
+    members: np.ndarray
+    source_clique: Optional[np.ndarray] = None
+
+    def size(self) -> int:
+        return len(self.offsets) - 1
+
+    def total_slots(self) -> int:
+        return len(self.members)
+
+
+@dataclass
+class CliqueSet:
+    """CliqueSet, cliques.hpp:14-22."""
+
+    offsets: np.ndarray
+    members: np.ndarray
+
+    def size(self) -> int:
+        return len(self.offsets) - 1
+
+
+@dataclass
+class ReplicatedIndex:
+    """ReplicatedIndex, model.hpp:29-37."""
+
+    test_label: np.ndarray
+    old_index: np.ndarray
+    hood_id: np.ndarray
+
+
+@dataclass
+class MinLabelEnergies:
+    """MinLabelEnergies, engine.hpp:48-51."""
+
+    energy: np.ndarray
+    label: np.ndarray
+
+
+@dataclass
+class MapIterationLog:
+    hood_energy: np.ndarray
+    converged: np.ndarray
+
+
+@dataclass
+class EmIterationLog:
+    map_iters: List[MapIterationLog]
+    total_energy: float
+    converged: bool
+    params: LabelParams
+    num_map_iters: int = 0
+
+    # flat aliases used by the parity helpers
+    @property
+    def mu(self):
+        return self.params.mu
+
+    @property
+    def sigma(self):
+        return self.params.sigma
+
+
+@dataclass
+class OptimizeResult:
+    """OptimizeResult, engine.hpp:87-91 (+ device statistics)."""
+
+    labels: np.ndarray
+    params: LabelParams
+    trace: List[EmIterationLog] = field(default_factory=list)
+    stats: Optional[dict] = None
+
+    @property
+    def mu(self):
+        return self.params.mu
+
+    @property
+    def sigma(self):
+        return self.params.sigma
+
+
+# ---- backend selector (dpp::Backend, backend.hpp:16-35, + a Cuda kind) ----------
+@dataclass(frozen=True)
+class Backend:
+    kind: str = "cuda"
+    device: int = 0
+
+    @staticmethod
+    def cuda(device: int = 0) -> "Backend":
+        return Backend("cuda", device)
+
+
+# ---- context: resident graph + hoods in HBM ---------------------------------------
+class Context:
+    """One dpmrf_context: a CUDA stream plus the resident graph and hoods."""
+
+    def __init__(self, device: int = 0):
+        self._lib = N.cuda()
+        h = ct.c_void_p()
+        _check(self._lib.dpmrf_context_create(device, ct.byref(h)), "dpmrf_context_create")
+        self.h = h
+        self.device = device
+        self._graph_key = None
+        self._hoods_key = None
+        self.R = 0
+        self.H = 0
+        self.S = 0
+
+    def close(self):
+        if self.h:
+            self._lib.dpmrf_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- resident inputs --
+    def set_graph(self, graph: RegionGraph):
+        off, nbr, mean = _u32(graph.offsets), _u32(graph.neighbors), _f64(graph.region_mean)
+        R = len(off) - 1
+        _check(self._lib.dpmrf_set_graph(self.h, R, N.ptr(off), N.ptr(nbr), N.ptr(mean)),
+               "dpmrf_set_graph")
+        self.R = R
+        self._graph_key = graph
+
+    def set_hoods(self, hoods: NeighborhoodSet):
+        off, mem = _u32(hoods.offsets), _u32(hoods.members)
+        _check(self._lib.dpmrf_set_hoods(self.h, len(off) - 1, N.ptr(off), N.ptr(mem)),
+               "dpmrf_set_hoods")
+        self.H, self.S = len(off) - 1, len(mem)
+        self._hoods_key = hoods
+
+    def build_neighborhoods(self, cliques: CliqueSet, k: int = 1) -> int:
+        off, mem = _u32(cliques.offsets), _u32(cliques.members)
+        n = ct.c_uint64(0)
+        _check(self._lib.dpmrf_build_neighborhoods(self.h, len(off) - 1, N.ptr(off), N.ptr(mem),
+                                                   k, ct.byref(n)), "build_neighborhoods")
+        self.H, self.S = len(off) - 1, n.value
+        self._hoods_key = None
+        return n.value
+
+    def get_hoods(self) -> NeighborhoodSet:
+        H, S = ct.c_uint64(0), ct.c_uint64(0)
+        _check(self._lib.dpmrf_get_hoods(self.h, ct.byref(H), ct.byref(S), None, None, None),
+               "dpmrf_get_hoods")
+        off = np.zeros(H.value + 1, np.uint32)
+        mem = np.zeros(S.value, np.uint32)
+        src = np.zeros(H.value, np.uint32)
+        _check(self._lib.dpmrf_get_hoods(self.h, None, None, N.ptr(off), N.ptr(mem), N.ptr(src)),
+               "dpmrf_get_hoods")
+        return NeighborhoodSet(off, mem, src)
+
+    # -- the optimization phase --
+    def optimize(self, config: OptimizerConfig, *, fixed_work=False, multilabel=None,
+                 trace_level=TRACE_FULL, kernel_timing=False, labels_out=None) -> OptimizeResult:
+        M = config.num_labels
+        if multilabel is None:
+            multilabel = M != 2
+        flags = (RUN_FIXED_WORK if fixed_work else 0) | (RUN_MULTILABEL if multilabel else 0) | \
+            (RUN_KERNEL_TIMING if kernel_timing else 0)
+        opts = N.CRunOptions(flags, trace_level)
+        cfg = config.c()
+        labels = labels_out if labels_out is not None else np.zeros(self.R, np.uint32)
+        mu, sigma = np.zeros(M), np.zeros(M)
+        _check(self._lib.dpmrf_optimize(self.h, ct.byref(cfg), ct.byref(opts), N.ptr(labels),
+                                        N.ptr(mu), N.ptr(sigma)), "optimize")
+        return OptimizeResult(labels, LabelParams(mu, sigma), self._trace(M, trace_level),
+                              self.stats())
+
+    def _trace(self, M, level) -> List[EmIterationLog]:
+        if level == TRACE_NONE:
+            return []
+        em_n, series = ct.c_int32(0), ct.c_uint64(0)
+        _check(self._lib.dpmrf_trace_info(self.h, ct.byref(em_n), ct.byref(series)), "trace")
+        out = []
+        for em in range(em_n.value):
+            it, tot, conv = ct.c_int32(0), ct.c_double(0), ct.c_uint8(0)
+            mu, sg = np.zeros(M), np.zeros(M)
+            _check(self._lib.dpmrf_trace_em(self.h, em, ct.byref(it), ct.byref(tot),
+                                            ct.byref(conv), N.ptr(mu), N.ptr(sg)), "trace_em")
+            maps = []
+            if level >= TRACE_FULL:
+                for t in range(it.value):
+                    e = np.zeros(series.value)
+                    f = np.zeros(series.value, np.uint8)
+                    _check(self._lib.dpmrf_trace_map(self.h, em, t, N.ptr(e), N.ptr(f)),
+                           "trace_map")
+                    maps.append(MapIterationLog(e, f))
+            out.append(EmIterationLog(maps, tot.value, bool(conv.value), LabelParams(mu, sg),
+                                      it.value))
+        return out
+
+    def stats(self) -> dict:
+        s = N.CRunStats()
+        _check(self._lib.dpmrf_get_stats(self.h, ct.byref(s)), "get_stats")
+        return {k: getattr(s, k) for k, _ in N.CRunStats._fields_}
+
+    # -- step functions (engine.hpp) on the resident structures --
+    def replicate_by_label(self, M) -> ReplicatedIndex:
+        E = M * self.S
+        tl, oi, hid = (np.zeros(E, np.uint32) for _ in range(3))
+        _check(self._lib.dpmrf_replicate_by_label(self.h, M, N.ptr(tl), N.ptr(oi), N.ptr(hid)),
+               "replicate_by_label")
+        return ReplicatedIndex(tl, oi, hid)
+
+    def slot_hood_map(self):
+        out = np.zeros(self.S, np.uint32)
+        _check(self._lib.dpmrf_slot_hood_map(self.h, N.ptr(out)), "slot_hood_map")
+        return out
+
+    def discord_counts(self, labels, M):
+        lab = _u32(labels)
+        out = np.zeros(M * self.R, np.uint32)
+        _check(self._lib.dpmrf_discord_counts(self.h, N.ptr(lab), M, N.ptr(out)), "discord_counts")
+        return out
+
+    def compute_energies(self, rep: ReplicatedIndex, params: LabelParams, labels, beta):
+        tl, oi = _u32(rep.test_label), _u32(rep.old_index)
+        mu, sg, lab = _f64(params.mu), _f64(params.sigma), _u32(labels)
+        out = np.zeros(len(tl))
+        _check(self._lib.dpmrf_compute_energies(self.h, len(tl), N.ptr(tl), N.ptr(oi), len(mu),
+                                                N.ptr(mu), N.ptr(sg), N.ptr(lab), beta,
+                                                N.ptr(out)), "compute_energies")
+        return out
+
+    def min_label_energies(self, rep: ReplicatedIndex, energies, num_slots) -> MinLabelEnergies:
+        tl, oi, en = _u32(rep.test_label), _u32(rep.old_index), _f64(energies)
+        if len(tl) != len(en) or len(oi) != len(en):
+            raise ValueError("min_label_energies: replicated index/energies mismatch")
+        oe, ol = np.zeros(num_slots), np.zeros(num_slots, np.uint32)
+        _check(self._lib.dpmrf_min_label_energies(self.h, len(en), N.ptr(tl), N.ptr(oi),
+                                                  N.ptr(en), num_slots, N.ptr(oe), N.ptr(ol)),
+               "min_label_energies")
+        return MinLabelEnergies(oe, ol)
+
+    def neighborhood_energy_sums(self, slot_hood, min_energy):
+        k, x = _u32(slot_hood), _f64(min_energy)
+        if len(k) != len(x):
+            raise ValueError("reduce_by_key: keys/values length mismatch")
+        out = np.zeros(max(len(k), 1))
+        n = ct.c_uint64(0)
+        _check(self._lib.dpmrf_neighborhood_energy_sums(self.h, len(k), N.ptr(k), N.ptr(x),
+                                                        N.ptr(out), ct.byref(n)),
+               "neighborhood_energy_sums")
+        return out[:n.value].copy()
+
+    def check_convergence(self, history, window, tol):
+        if len(history) == 0:
+            return np.zeros(0, np.uint8)
+        h = _f64(np.asarray(history, dtype=np.float64).reshape(len(history), -1))
+        out = np.zeros(h.shape[1], np.uint8)
+        _check(self._lib.dpmrf_check_convergence(self.h, h.shape[0], h.shape[1], N.ptr(h), window,
+                                                 tol, N.ptr(out)), "check_convergence")
+        return out
+
+    def update_labels(self, argmin_label, old_labels):
+        a, old = _u32(argmin_label), _u32(old_labels)
+        if len(a) != self.S:
+            raise ValueError("update_labels: one argmin per hood slot required")
+        out = np.zeros(len(old), np.uint32)
+        _check(self._lib.dpmrf_update_labels(self.h, N.ptr(a), len(old), N.ptr(old), N.ptr(out)),
+               "update_labels")
+        return out
+
+    def update_parameters(self, labels, previous: LabelParams) -> LabelParams:
+        lab = _u32(labels)
+        if len(lab) != self.R:
+            raise ValueError("update_parameters: one label per vertex required")
+        M = len(previous.mu)
+        mu, sg = np.zeros(M), np.zeros(M)
+        _check(self._lib.dpmrf_update_parameters(self.h, N.ptr(lab), M, N.ptr(_f64(previous.mu)),
+                                                 N.ptr(_f64(previous.sigma)), N.ptr(mu),
+                                                 N.ptr(sg)), "update_parameters")
+        return LabelParams(mu, sg)
+
+    def init_random(self, num_labels, num_vertices, seed, allow_multilabel=False):
+        mu, sg = np.zeros(num_labels), np.zeros(num_labels)
+        lab = np.zeros(num_vertices, np.uint32)
+        _check(self._lib.dpmrf_init_random(self.h, num_labels, num_vertices,
+                                           seed & ((1 << 64) - 1), int(allow_multilabel),
+                                           N.ptr(mu), N.ptr(sg), N.ptr(lab)), "init_random")
+        return LabelParams(mu, sg), lab
+
+
+# ---- free functions with the reference's signatures --------------------------------
+_contexts = {}
+
+
+def context_for(backend: Backend) -> Context:
+    if backend.kind != "cuda":
+        raise InputError(f"unsupported backend kind {backend.kind!r} (this build is CUDA-only)")
+    ctx = _contexts.get(backend.device)
+    if ctx is None:
+        ctx = _contexts[backend.device] = Context(backend.device)
+    return ctx
+
+
+def _resident(ctx: Context, graph: RegionGraph, hoods: Optional[NeighborhoodSet] = None):
+    if ctx._graph_key is not graph:
+        ctx.set_graph(graph)
+    if hoods is not None and ctx._hoods_key is not hoods:
+        ctx.set_hoods(hoods)
+
+
+def optimize(backend: Backend, graph: RegionGraph, hoods: NeighborhoodSet,
+             config: OptimizerConfig, **kw) -> OptimizeResult:
+    """optimize, engine.hpp:99-100 / optimize.cpp:31-74."""
+    ctx = context_for(backend)
+    _resident(ctx, graph, hoods)
+    return ctx.optimize(config, **kw)
+
+
+def build_neighborhoods(backend: Backend, graph: RegionGraph, cliques: CliqueSet,
+                        k: int = 1) -> NeighborhoodSet:
+    """build_neighborhoods, neighborhoods.hpp:28-29 / neighborhoods.cpp:10-57 (on the device)."""
+    ctx = context_for(backend)
+    _resident(ctx, graph)
+    ctx.build_neighborhoods(cliques, k)
+    return ctx.get_hoods()
+
+
+def init_random(num_labels, num_vertices, seed, backend: Backend = Backend.cuda()):
+    """init_random, engine.hpp:20-21 -> (LabelParams, labels)."""
+    return context_for(backend).init_random(num_labels, num_vertices, seed)
+
+
+def replicate_by_label(backend: Backend, hoods: NeighborhoodSet, num_labels) -> ReplicatedIndex:
+    ctx = context_for(backend)
+    if ctx._hoods_key is not hoods:
+        ctx.set_hoods(hoods)
+    return ctx.replicate_by_label(num_labels)
+
+
+def slot_hood_map(backend: Backend, hoods: NeighborhoodSet):
+    ctx = context_for(backend)
+    if ctx._hoods_key is not hoods:
+        ctx.set_hoods(hoods)
+    return ctx.slot_hood_map()
+
+
+def discord_counts(backend: Backend, graph: RegionGraph, labels, num_labels):
+    ctx = context_for(backend)
+    _resident(ctx, graph)
+    return ctx.discord_counts(labels, num_labels)
+
+
+def compute_energies(backend: Backend, graph: RegionGraph, hoods: NeighborhoodSet,
+                     rep: ReplicatedIndex, params: LabelParams, labels, beta):
+    ctx = context_for(backend)
+    _resident(ctx, graph, hoods)
+    return ctx.compute_energies(rep, params, labels, beta)
+
+
+def min_label_energies(backend: Backend, rep: ReplicatedIndex, energies, num_slots):
+    return context_for(backend).min_label_energies(rep, energies, num_slots)
+
+
+def neighborhood_energy_sums(backend: Backend, slot_hood, min_energy):
+    return context_for(backend).neighborhood_energy_sums(slot_hood, min_energy)
+
+
+def check_convergence(backend: Backend, history, window, tol):
+    return context_for(backend).check_convergence(history, window, tol)
+
+
+def update_labels(backend: Backend, hoods: NeighborhoodSet, argmin_label, old_labels):
+    ctx = context_for(backend)
+    if ctx._hoods_key is not hoods:
+        ctx.set_hoods(hoods)
+    return ctx.update_labels(argmin_label, old_labels)
+
+
+def update_parameters(backend: Backend, graph: RegionGraph, labels, previous: LabelParams):
+    ctx = context_for(backend)
+    _resident(ctx, graph)
+    return ctx.update_parameters(labels, previous)
