@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the DPP-PMRF optimization phase on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config B|C|D] [--impl ours|reference]
+
+A step is one fixed-work optimization (20 EM x 10 MAP iterations, no early
+exits) of one synthetic slice whose region graph and device-built
+neighborhoods are resident in HBM.  Each rank processes its own slice
+(seed 42 + rank): slices shard with no data-path collective ("weak").
+
+value  = EM iterations of all ranks / max-over-ranks device time (CUDA events
+         on the library's stream, L2 flushed between steps)
+e2e    = the same metric through the public C ABI with host (pinned) buffers:
+         dpmrf_set_graph + dpmrf_set_hoods + dpmrf_optimize per step, host
+         wall clock, H2D of the inputs and D2H of labels/params included.
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+compiled from /root/reference by oracle/Makefile) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MRF opt. EM-iterations/s & vertex-label evals/s @1/2/4/8 B200; %HBM peak"
+CONFIGS = {
+    "B": dict(size=2560, block=8, brick=False, M=2, em=20,
+              desc="synthetic 2560x2560 porous phantom (pore .25, s&p .05, gauss 100, ringing), "
+                   "grid oversegmentation block 8, 2 labels, fixed 20 EM x 10 MAP"),
+    "C": dict(size=2560, block=8, brick=True, M=5, em=20,
+              desc="same 2560x2560 slice, brick oversegmentation block 8 (dense 3-clique graph), "
+                   "5 labels, fixed 20 EM x 10 MAP"),
+    "D": dict(size=16384, block=7, brick=False, M=2, em=20,
+              desc="single 16384x16384 slice, grid block 7 (~5.5M regions), 2 labels, "
+                   "fixed 20 EM x 10 MAP, one GPU"),
+}
+MAP_ITERS = 10
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---- clocks sampled during the timed region ------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.lines = device, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- the reference CPU path ------------------------------------------------------------
+def reference_sample(cfg_name, seconds_budget=12.0, rank_seed=42):
+    """Times the reference's fastest CPU path on a bounded sample of the workload.
+    Returns (em_iters_per_s, detail dict)."""
+    c = CONFIGS[cfg_name]
+    import oracle
+    if oracle.ref_available():
+        kind = "reference"
+        ref = oracle.Ref()
+        threads = ref.hw_threads()
+        pipe = ref.phantom(c["size"], c["block"], brick=c["brick"], seed=rank_seed,
+                           threads=min(threads, 8))
+        cfg1 = oracle.Config(num_labels=c["M"], rng_seed=rank_seed, em_max_iters=1)
+        # fastest of: Algorithm-1 sweep on 1 core, and the DPP engine on all cores
+        t0 = time.perf_counter()
+        pipe.sweep(cfg1, mode=1, fixed_work=True)
+        sweep_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        pipe.optimize(cfg1, threads=threads, mode=1, fixed_work=True, full_trace=False)
+        dpp_s = time.perf_counter() - t0
+        best = "sweep" if sweep_s <= dpp_s else "dpp"
+        run = (lambda: pipe.sweep(cfg1, mode=1, fixed_work=True)) if best == "sweep" else \
+            (lambda: pipe.optimize(cfg1, threads=threads, mode=1, fixed_work=True,
+                                   full_trace=False))
+        cores = 1 if best == "sweep" else threads
+        sample_desc = (f"{cfg_name}: 1 EM iteration (10 MAP, fixed work) per sample of "
+                       f"{'optimize_reference sweep (1 core)' if best == 'sweep' else f'optimize DPP engine (threaded x{threads})'}; "
+                       f"probe: sweep {1/sweep_s:.3f} EM-it/s, DPP x{threads} {1/dpp_s:.3f} EM-it/s")
+    else:
+        kind = "port"
+        from oracle import C, Config, Graph, Hoods
+        from paper_1809_05018_b200 import engine as E
+        from paper_1809_05018_b200 import inputs
+        sl = inputs.synthetic_slice(c["size"], c["block"], brick=c["brick"], seed=rank_seed)
+        g = Graph(sl.graph.offsets, sl.graph.neighbors, sl.graph.region_mean)
+        h, _ = C().build_neighborhoods(g, sl.cliques.offsets, sl.cliques.members)
+        cfg1 = Config(num_labels=c["M"], rng_seed=rank_seed, em_max_iters=1)
+        run = lambda: C().optimize_reference(g, h, cfg1, fixed_work=True, allow_multilabel=True)  # noqa
+        cores = 1
+        sample_desc = f"{cfg_name}: 1 EM iteration (10 MAP) of the C port of the sweep, 1 core"
+        del E
+    times = []
+    t_end = time.perf_counter() + seconds_budget
+    while True:
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end or len(times) >= 50:
+            break
+    per_em = statistics.median(times)
+    return 1.0 / per_em, {"kind": kind, "cores": cores, "sample": sample_desc + f"; {len(times)} samples, median",
+                          "run": run, "seconds_per_em": per_em}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    _, det = reference_sample(args.config, seconds_budget=1.0)
+    run = det["run"]
+    for _ in range(args.warmup):
+        run()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    per_em = sum(times) / len(times)
+    value = 1.0 / per_em
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "EM-iterations/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": per_em * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIGS[args.config]["desc"], "sample": det["sample"]},
+            "cpu_baseline": {"value": value, "unit": "EM-iterations/s", "cores": det["cores"],
+                             "kind": det["kind"], "sample": det["sample"]},
+            "e2e": {"value": value, "unit": "EM-iterations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- our arm ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="B", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1809_05018_b200 import engine as E
+    from paper_1809_05018_b200 import inputs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    c = CONFIGS[args.config]
+    seed = 42 + rank
+    t0 = time.perf_counter()
+    sl = inputs.synthetic_slice(c["size"], c["block"], brick=c["brick"], seed=seed)
+    build_inputs_s = time.perf_counter() - t0
+    R = sl.graph.num_vertices
+    A = len(sl.graph.neighbors)
+
+    ctx = E.Context(local)
+    ctx.set_graph(sl.graph)
+    t0 = time.perf_counter()
+    ctx.build_neighborhoods(sl.cliques)
+    hood_build_ms = (time.perf_counter() - t0) * 1e3
+    hoods = ctx.get_hoods()
+    H, S = hoods.size(), hoods.total_slots()
+    cfg = E.OptimizerConfig(num_labels=c["M"], em_max_iters=c["em"], map_max_iters=MAP_ITERS,
+                            rng_seed=seed)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    labels_out = np.zeros(R, np.uint32)
+
+    def step(timing=True):
+        return ctx.optimize(cfg, fixed_work=True, multilabel=c["M"] != 2,
+                            trace_level=E.TRACE_NONE, kernel_timing=timing, labels_out=labels_out)
+
+    for _ in range(args.warmup):
+        step()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    dev_ms, wall_ms, vtx_ms, hood_ms, mstep_ms, launches = [], [], [], [], [], 0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = step()
+        wall_ms.append((time.perf_counter() - t0) * 1e3)
+        st = r.stats
+        dev_ms.append(st["optimize_ms"])
+        vtx_ms.append(st["vertex_kernel_ms"])
+        hood_ms.append(st["hood_kernel_ms"])
+        mstep_ms.append(st["mstep_ms"])
+        launches += st["kernel_launches"]
+        n_launch_map = st["vertex_launches"]
+    barrier()
+    clocks = sampler.stop()
+
+    em_per_step = c["em"]
+    map_per_step = c["em"] * MAP_ITERS
+    total_dev_s = allmax(sum(dev_ms) / 1e3)
+    total_em = allsum(em_per_step * args.steps)
+    value = total_em / total_dev_s
+    ms_per_step = total_dev_s * 1e3 / args.steps
+
+    # ---- e2e: public C ABI with host (pinned) buffers --------------------------------
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    g_pin = E.RegionGraph(pin(sl.graph.offsets), pin(sl.graph.neighbors), pin(sl.graph.region_mean))
+    h_pin = E.NeighborhoodSet(pin(hoods.offsets), pin(hoods.members))
+    lab_pin = torch.zeros(R, dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+    h2d = 4 * (R + 1) + 4 * A + 8 * R + 4 * (H + 1) + 4 * S
+    d2h = 4 * R + 16 * c["M"]
+    barrier()
+    e2e_times = []
+    for _ in range(max(3, args.steps // 2)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.set_graph(g_pin)
+        ctx.set_hoods(h_pin)
+        ctx.optimize(cfg, fixed_work=True, multilabel=c["M"] != 2, trace_level=E.TRACE_NONE,
+                     labels_out=lab_pin)
+        e2e_times.append(time.perf_counter() - t0)
+    barrier()
+    e2e_s = allmax(sum(e2e_times))
+    e2e_value = allsum(em_per_step * len(e2e_times)) / e2e_s
+
+    # ---- roofline of the dominant kernel (algorithmic bytes) ---------
+    hbm, peak_kind = peaks()
+    L = cfg.convergence_window
+    vtx_bytes = 20 * R + 4 * A + 4                    # offsets, neighbors, labels in/out, means
+    hood_bytes = 4 * (H + 1) + 4 * S + 8 * H + 8 * L * H  # offsets, members, energy out, window
+    n_launch = n_launch_map * args.steps
+    vtx_avg = sum(vtx_ms) / n_launch
+    hood_avg = sum(hood_ms) / n_launch
+    if hood_avg >= vtx_avg:
+        kname, kbytes, kavg = "k_hood_sums", hood_bytes, hood_avg
+    else:
+        kname, kbytes, kavg = "k_vertex_argmin", vtx_bytes, vtx_avg
+    achieved = kbytes / (kavg * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(args.config, {}).get(kname)
+    except Exception:
+        pass
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "EM-iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"config {args.config}: {c['desc']}; slice seed 42+rank",
+                   "regions": R, "adjacency": A, "hoods": H, "slots": S, "labels": c["M"],
+                   "em_iters_per_step": em_per_step, "map_iters_per_step": map_per_step,
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "parallelism": f"slice-sharded x{world} (no data-path collective)",
+                   "timing": "CUDA events on the library stream around each optimize(); "
+                             "max over ranks"},
+        "vertex_label_evals_per_s": c["M"] * S * map_per_step * args.steps * world / total_dev_s,
+        "unique_vertex_label_evals_per_s": c["M"] * R * map_per_step * args.steps * world / total_dev_s,
+        "kernel_ms_per_step": {"k_vertex_argmin": sum(vtx_ms) / args.steps,
+                               "k_hood_sums": sum(hood_ms) / args.steps,
+                               "mstep": sum(mstep_ms) / args.steps},
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": kbytes,
+                     "avg_launch_us": kavg * 1e3,
+                     "note": "config B's per-MAP working set (~17.5 MB) is L2-resident"
+                     if args.config in ("B", "C") else ""},
+        "e2e": {"value": e2e_value, "unit": "EM-iterations/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "setup": {"input_build_s": build_inputs_s, "hood_build_ms_device_call": hood_build_ms},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, det = reference_sample(args.config, seconds_budget=args.cpu_seconds, rank_seed=seed)
+            line["cpu_baseline"] = {"value": v, "unit": "EM-iterations/s", "cores": det["cores"],
+                                    "kind": det["kind"], "sample": det["sample"]}
+        except Exception as ex:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": str(ex)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -12,6 +12,7 @@
 //     log(sigma) with the host libm exactly as make_label_terms does
 //     (model.hpp:57), which keeps the energies bit-identical to the reference.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -131,6 +132,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     need(device >= 0 && device < n, DPMRF_INVALID_ARGUMENT, "no such CUDA device");
     auto* c = new dpmrf_context;
     c->device = device;
+    if (const char* e = std::getenv("DPMRF_NO_GRAPH")) c->use_graphs = e[0] == '0';
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -151,6 +153,7 @@ extern "C" void dpmrf_context_destroy(dpmrf_context* ctx) {
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->ev_begin) cudaEventDestroy(ctx->ev_begin);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
+  ctx->drop_graphs();
   cudaStream_t s = ctx->stream;
   delete ctx;
   if (s) cudaStreamDestroy(s);
@@ -315,26 +318,28 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       CK(cudaMemcpyAsync(params, mu.data(), M * 8, cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(params + M, sigma.data(), M * 8, cudaMemcpyHostToDevice, st));
       std::vector<double> em_hist;
-      size_t ev = 0;
-      for (int em = 0; em < cfg->em_max_iters; ++em) {
-        // make_label_terms (model.hpp:48-60) with the host's std::log
-        for (uint32_t l = 0; l < M; ++l) {
-          h_terms[l] = mu[l];
-          h_terms[M + l] = 2.0 * (sigma[l] * sigma[l]);
-          h_terms[2 * M + l] = std::log(sigma[l]);
-        }
+      const size_t ev_per_em = timing ? size_t(3 * map_max + 2) : 0;
+      for (size_t i = 0; i < ev_per_em; ++i) ctx->event(i);
+      // Everything one EM iteration puts on the stream (no host sync inside).
+      uint64_t em_kernels = 0;
+      auto record = [&](size_t i) {
+        if (timing) CK(cudaEventRecordWithFlags(ctx->ev_pool[i], st, cudaEventRecordExternal));
+      };
+      auto enqueue_em = [&](int parity) {
+        uint64_t k = 0;
+        size_t ev = 0;
         CK(cudaMemcpyAsync(const_cast<double*>(a.terms), h_terms, 3 * M * 8,
                            cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(a.unconv, 0, map_max * sizeof(uint32_t), st));
         for (int t = 0; t < map_max; ++t) {
-          const uint8_t* lin = lab[(cur + t) & 1];
-          uint8_t* lout = lab[(cur + t + 1) & 1];
-          if (timing) CK(cudaEventRecord(ctx->event(ev++), st));
+          const uint8_t* lin = lab[(parity + t) & 1];
+          uint8_t* lout = lab[(parity + t + 1) & 1];
+          record(ev++);
           launch_vertex_argmin(a, lin, lout, t, st);
-          if (timing) CK(cudaEventRecord(ctx->event(ev++), st));
+          record(ev++);
           launch_hood_sums(a, t, st);
-          if (timing) CK(cudaEventRecord(ctx->event(ev++), st));
-          launches += 2;
+          record(ev++);
+          k += 2;
           if (a.flags && Hs) {
             CK(cudaMemcpyAsync(h_row + uint64_t(t) * Hs, a.hist + uint64_t(t % (L + 1)) * Hs,
                                Hs * 8, cudaMemcpyDeviceToHost, st));
@@ -342,12 +347,103 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
                                st));
           }
         }
-        if (timing) CK(cudaEventRecord(ctx->event(ev++), st));
-        launch_mstep(a.mean, R, M, lab[cur], lab[cur ^ 1], a.hist, Hs, L, a.unconv, map_max,
-                     fixed, params, em_out, ctx->ms, st, &launches);
-        if (timing) CK(cudaEventRecord(ctx->event(ev++), st));
+        record(ev++);
+        launch_mstep(a.mean, R, M, lab[parity], lab[parity ^ 1], a.hist, Hs, L, a.unconv,
+                     map_max, fixed, params, em_out, ctx->ms, st, &k);
+        record(ev++);
         CK(cudaMemcpyAsync(h_em, em_out, (2 + 2 * M) * 8, cudaMemcpyDeviceToHost, st));
+        em_kernels = k;
+      };
+      // One CUDA graph per label-buffer parity, captured once per shape and
+      // replayed every EM iteration (the EM loop is launch-bound at 2560^2).
+      const bool use_graph = ctx->use_graphs;
+      if (use_graph) {
+        mstep_reserve(ctx->ms, R, M, Hs);
+        dpmrf_context::GraphKey key{};
+        key.R = R;
+        key.Hs = Hs;
+        key.M = M;
+        key.L = L;
+        key.map_max = map_max;
+        key.fixed = fixed;
+        key.timing = timing;
+        key.trace = o.trace_level;
+        key.beta = cfg->beta;
+        key.tol = cfg->convergence_tol;
+        key.p[0] = lab[0];
+        key.p[1] = lab[1];
+        key.p[2] = a.minE;
+        key.p[3] = a.hist;
+        key.p[4] = a.flags;
+        key.p[5] = a.unconv;
+        key.p[6] = params;
+        key.p[7] = h_em;
+        key.p[8] = h_row;
+        key.p[9] = a.s_off;
+        key.p[10] = a.h_mem;
+        key.p[11] = a.g_nbr;
+        key.p[12] = ctx->ms.x.get();
+        key.p[13] = ctx->ms.partials.get();
+        key.p[14] = a.terms;
+        key.p[15] = h_terms;
+        key.p[16] = ctx->ms.tile_counts.get();
+        key.p[17] = ctx->ms.tile_base.get();
+        key.p[18] = ctx->ms.layout.get();
+        key.p[19] = ctx->ms.row.get();
+        key.p[20] = h_flags;
+        key.p[21] = a.cover;
+        key.p[22] = a.g_off;
+        key.p[23] = em_out;
+        if (!ctx->graph_valid || std::memcmp(&key, &ctx->graph_key, sizeof key) != 0) {
+          ctx->drop_graphs();
+          for (int parity = 0; parity < 2; ++parity) {
+            cudaGraph_t g;
+            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            try {
+              enqueue_em(parity);
+            } catch (...) {
+              cudaStreamEndCapture(st, &g);
+              if (g) cudaGraphDestroy(g);
+              throw;
+            }
+            CK(cudaStreamEndCapture(st, &g));
+            CK(cudaGraphInstantiate(&ctx->graph_exec[parity], g, 0));
+            CK(cudaGraphDestroy(g));
+          }
+          ctx->graph_kernels = em_kernels;
+          ctx->graph_key = key;
+          ctx->graph_valid = true;
+        }
+      }
+      for (int em = 0; em < cfg->em_max_iters; ++em) {
+        // make_label_terms (model.hpp:48-60) with the host's std::log
+        for (uint32_t l = 0; l < M; ++l) {
+          h_terms[l] = mu[l];
+          h_terms[M + l] = 2.0 * (sigma[l] * sigma[l]);
+          h_terms[2 * M + l] = std::log(sigma[l]);
+        }
+        if (use_graph) {
+          CK(cudaGraphLaunch(ctx->graph_exec[cur], st));
+          launches += ctx->graph_kernels;
+        } else {
+          enqueue_em(cur);
+          launches += em_kernels;
+        }
         ctx->sync();
+        if (timing) {
+          float ms = 0.f;
+          size_t e = 0;
+          for (int t = 0; t < map_max; ++t, e += 3) {
+            CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
+            ctx->stats.vertex_kernel_ms += ms;
+            CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e + 1], ctx->ev_pool[e + 2]));
+            ctx->stats.hood_kernel_ms += ms;
+          }
+          CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
+          ctx->stats.mstep_ms += ms;
+          ctx->stats.vertex_launches += map_max;
+          ctx->stats.hood_launches += map_max;
+        }
         const int T = static_cast<int>(h_em[1]);
         const double total = h_em[0];
         std::memcpy(mu.data(), h_em + 2, M * 8);
@@ -387,25 +483,6 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
         if (conv && !fixed) break;
       }
       ctx->stats.series = Hs;
-      if (timing) {
-        // per EM: (3 events per MAP iteration) + 2 around the M-step
-        size_t e = 0;
-        float ms = 0.f;
-        for (int em = 0; em < ctx->stats.em_iters; ++em) {
-          for (int t = 0; t < map_max; ++t) {
-            CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
-            ctx->stats.vertex_kernel_ms += ms;
-            CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e + 1], ctx->ev_pool[e + 2]));
-            ctx->stats.hood_kernel_ms += ms;
-            e += 3;
-          }
-          CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
-          ctx->stats.mstep_ms += ms;
-          e += 2;
-        }
-        ctx->stats.vertex_launches = uint64_t(ctx->stats.em_iters) * map_max;
-        ctx->stats.hood_launches = ctx->stats.vertex_launches;
-      }
     }
     // labels out (u8 in HBM -> the reference's u32)
     uint32_t* l32 = ctx->labels32.ensure(R);

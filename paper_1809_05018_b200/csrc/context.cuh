@@ -71,6 +71,28 @@ struct dpmrf_context {
     }
     return ev_pool[i];
   }
+  // ---- CUDA graphs of one EM iteration (one per label-buffer parity) ----
+  struct GraphKey {
+    uint64_t R, Hs;
+    uint32_t M;
+    int32_t L, map_max, fixed, timing, trace;
+    double beta, tol;
+    const void* p[24];
+  };
+  bool use_graphs = true;
+  bool graph_valid = false;
+  GraphKey graph_key{};
+  cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};
+  uint64_t graph_kernels = 0;
+  void drop_graphs() {
+    for (auto& g : graph_exec)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+    graph_valid = false;
+  }
+
   void sync() { CK(cudaStreamSynchronize(stream)); }
   void bind() { CK(cudaSetDevice(device)); }
   void prepare();  // validate + cover + series offsets (capi.cu)

@@ -588,6 +588,17 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
              mb, s, launches);
 }
 
+void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs) {
+  const uint32_t tiles = static_cast<uint32_t>((uint64_t(R) + kTileVerts - 1) / kTileVerts);
+  const uint32_t tiles_g = tiles ? tiles : 1;
+  mb.tile_counts.ensure(uint64_t(tiles_g) * M);
+  mb.tile_base.ensure(uint64_t(tiles_g) * M);
+  mb.layout.ensure(4 * M + 4);
+  mb.x.ensure(R);
+  mb.partials.ensure((uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M + (Hs + kFoldLeaf - 1) / kFoldLeaf + 1);
+  mb.row.ensure(Hs);
+}
+
 void launch_update_parameters_u32(const double* mean, uint32_t R, uint32_t M,
                                   const uint32_t* labels, double* params, MStepBuffers& mb,
                                   DevBuf<uint8_t>& lab_tmp, cudaStream_t s) {

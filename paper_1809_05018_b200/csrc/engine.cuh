@@ -58,6 +58,9 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches);
 
+// Allocates every M-step buffer up front (required before stream capture).
+void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs);
+
 // Standalone update_parameters over caller labels (u32, validated < M).
 void launch_update_parameters_u32(const double* mean, uint32_t R, uint32_t M,
                                   const uint32_t* labels, double* params, MStepBuffers& mb,
