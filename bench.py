@@ -347,22 +347,29 @@ def main():
     sampler.start()
     time.sleep(0.3)
     barrier()
-    dev_ms, wall_ms, vtx_ms, hood_ms, mstep_ms, launches = [], [], [], [], [], 0
+    dev_ms, wall_ms, launches = [], [], 0
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = step()
+        r = step(timing=False)
         wall_ms.append((time.perf_counter() - t0) * 1e3)
-        st = r.stats
-        dev_ms.append(st["optimize_ms"])
-        vtx_ms.append(st["vertex_kernel_ms"])
-        hood_ms.append(st["hood_kernel_ms"])
-        mstep_ms.append(st["mstep_ms"])
-        launches += st["kernel_launches"]
-        n_launch_map = st["vertex_launches"]
+        dev_ms.append(r.stats["optimize_ms"])
+        launches += r.stats["kernel_launches"]
     barrier()
     clocks = sampler.stop()
+    # profiled pass (same workload, CUDA events around the MAP loop / M-step
+    # of every EM iteration) for the kernel split and the roofline
+    prof = {"map_loop_ms": 0.0, "map_loop_launches": 0, "vertex_kernel_ms": 0.0,
+            "hood_kernel_ms": 0.0, "vertex_launches": 0, "mstep_ms": 0.0, "optimize_ms": 0.0}
+    prof_steps = max(2, args.steps // 2)
+    for _ in range(prof_steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        st = step(timing=True).stats
+        for k in prof:
+            prof[k] += st[k]
+        persistent = bool(st["persistent"])
 
     em_per_step = c["em"]
     map_per_step = c["em"] * MAP_ITERS
@@ -396,15 +403,24 @@ def main():
     # ---- roofline of the dominant kernel (algorithmic bytes) ---------
     hbm, peak_kind = peaks()
     L = cfg.convergence_window
-    vtx_bytes = 20 * R + 4 * A + 4                    # offsets, neighbors, labels in/out, means
-    hood_bytes = 4 * (H + 1) + 4 * S + 8 * H + 8 * L * H  # offsets, members, energy out, window
-    n_launch = n_launch_map * args.steps
-    vtx_avg = sum(vtx_ms) / n_launch
-    hood_avg = sum(hood_ms) / n_launch
-    if hood_avg >= vtx_avg:
-        kname, kbytes, kavg = "k_hood_sums", hood_bytes, hood_avg
+    vtx_bytes = 20 * R + 4 * A + 4                         # offsets, neighbors, labels in/out, means
+    hood_bytes = 4 * (H + 1) + 4 * S + 8 * H + 8 * L * H   # offsets, members, energy out, window
+    if persistent:
+        kname = "k_map_loop"
+        kbytes = MAP_ITERS * (vtx_bytes + hood_bytes)      # one launch = the whole MAP loop
+        kavg = prof["map_loop_ms"] / max(1, prof["map_loop_launches"])
+        kernel_split = {"k_map_loop": prof["map_loop_ms"] / prof_steps,
+                        "mstep": prof["mstep_ms"] / prof_steps}
     else:
-        kname, kbytes, kavg = "k_vertex_argmin", vtx_bytes, vtx_avg
+        n_launch = max(1, prof["vertex_launches"])
+        vtx_avg = prof["vertex_kernel_ms"] / n_launch
+        hood_avg = prof["hood_kernel_ms"] / n_launch
+        kname, kbytes, kavg = ("k_hood_sums", hood_bytes, hood_avg) if hood_avg >= vtx_avg else \
+            ("k_vertex_argmin", vtx_bytes, vtx_avg)
+        kernel_split = {"k_vertex_argmin": prof["vertex_kernel_ms"] / prof_steps,
+                        "k_hood_sums": prof["hood_kernel_ms"] / prof_steps,
+                        "mstep": prof["mstep_ms"] / prof_steps}
+    kernel_split["optimize_ms_profiled"] = prof["optimize_ms"] / prof_steps
     achieved = kbytes / (kavg * 1e-3) / 1e9
     traffic = None
     try:
@@ -427,9 +443,7 @@ def main():
                              "max over ranks"},
         "vertex_label_evals_per_s": c["M"] * S * map_per_step * args.steps * world / total_dev_s,
         "unique_vertex_label_evals_per_s": c["M"] * R * map_per_step * args.steps * world / total_dev_s,
-        "kernel_ms_per_step": {"k_vertex_argmin": sum(vtx_ms) / args.steps,
-                               "k_hood_sums": sum(hood_ms) / args.steps,
-                               "mstep": sum(mstep_ms) / args.steps},
+        "kernel_ms_per_step": kernel_split,
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "algorithmic_bytes_per_launch": kbytes,

@@ -66,7 +66,9 @@ enum {
 enum {
   DPMRF_RUN_FIXED_WORK = 1u,    /* drop the early exits (optimize.cpp:59,:71): fixed EM x MAP work */
   DPMRF_RUN_MULTILABEL = 2u,    /* allow num_labels in [1,255] (extension; reference: 2 only) */
-  DPMRF_RUN_KERNEL_TIMING = 4u  /* CUDA events around the MAP kernels (dpmrf_get_stats) */
+  DPMRF_RUN_KERNEL_TIMING = 4u, /* CUDA events around the MAP kernels (dpmrf_get_stats) */
+  DPMRF_RUN_TWO_KERNELS = 8u,   /* two kernels per MAP iteration instead of the persistent loop */
+  DPMRF_RUN_NO_GRAPH = 16u      /* launch each EM iteration directly instead of a CUDA graph */
 };
 
 typedef struct dpmrf_run_options {
@@ -86,6 +88,10 @@ typedef struct dpmrf_run_stats {
   int32_t em_iters;
   int32_t map_iters_total;   /* MAP iterations executed, summed over EM iterations */
   uint64_t series;           /* hood-energy series length (nonempty hoods) */
+  double map_loop_ms;        /* persistent MAP-loop kernel (one cooperative launch per EM) */
+  uint64_t map_loop_launches;
+  int32_t persistent;        /* 1: persistent MAP loop, 0: two kernels per MAP iteration */
+  int32_t graphs;            /* 1: EM iterations replayed from CUDA graphs */
 } dpmrf_run_stats;
 
 /* ---- context ------------------------------------------------------------ */

@@ -42,7 +42,8 @@ class CRunStats(ct.Structure):
     _fields_ = [("optimize_ms", F64), ("vertex_kernel_ms", F64), ("hood_kernel_ms", F64),
                 ("mstep_ms", F64), ("vertex_launches", U64), ("hood_launches", U64),
                 ("kernel_launches", U64), ("em_iters", I32), ("map_iters_total", I32),
-                ("series", U64)]
+                ("series", U64), ("map_loop_ms", F64), ("map_loop_launches", U64),
+                ("persistent", I32), ("graphs", I32)]
 
 
 # (name, restype, argtypes) of every C ABI entry point (include/dpmrf_cuda.h)

@@ -133,6 +133,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     auto* c = new dpmrf_context;
     c->device = device;
     if (const char* e = std::getenv("DPMRF_NO_GRAPH")) c->use_graphs = e[0] == '0';
+    if (const char* e = std::getenv("DPMRF_MAP_KERNELS")) c->use_persistent = e[0] != '2';
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -298,12 +299,16 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       a.M = M;
       a.beta = cfg->beta;
       a.tol = cfg->convergence_tol;
+      const bool full = o.trace_level >= DPMRF_TRACE_FULL;
+      const bool persistent = ctx->use_persistent && !(o.flags & DPMRF_RUN_TWO_KERNELS);
       a.L = L;
+      a.ring = full ? map_max : L + 1;
       a.fixed = fixed;
       a.terms = ctx->terms.ensure(3 * M);
-      a.minE = ctx->minE.ensure(R);
-      a.hist = ctx->hist.ensure(uint64_t(L + 1) * Hs);
-      a.flags = o.trace_level >= DPMRF_TRACE_FULL ? ctx->flags.ensure(Hs) : nullptr;
+      double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
+      a.minE = minE2;
+      a.hist = ctx->hist.ensure(uint64_t(a.ring) * Hs);
+      a.flags = full ? ctx->flags.ensure(uint64_t(map_max) * Hs) : nullptr;
       a.unconv = ctx->unconv.ensure(map_max);
       double* params = ctx->params.ensure(2 * M);
       double* em_out = ctx->em_out.ensure(2 + 2 * M);
@@ -318,7 +323,8 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       CK(cudaMemcpyAsync(params, mu.data(), M * 8, cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(params + M, sigma.data(), M * 8, cudaMemcpyHostToDevice, st));
       std::vector<double> em_hist;
-      const size_t ev_per_em = timing ? size_t(3 * map_max + 2) : 0;
+      const size_t ev_per_em = timing ? size_t(3 * map_max + 4) : 0;
+      ctx->stats.persistent = persistent;
       for (size_t i = 0; i < ev_per_em; ++i) ctx->event(i);
       // Everything one EM iteration puts on the stream (no host sync inside).
       uint64_t em_kernels = 0;
@@ -331,24 +337,31 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
         CK(cudaMemcpyAsync(const_cast<double*>(a.terms), h_terms, 3 * M * 8,
                            cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(a.unconv, 0, map_max * sizeof(uint32_t), st));
-        for (int t = 0; t < map_max; ++t) {
-          const uint8_t* lin = lab[(parity + t) & 1];
-          uint8_t* lout = lab[(parity + t + 1) & 1];
+        if (persistent) {
           record(ev++);
-          launch_vertex_argmin(a, lin, lout, t, st);
+          launch_map_loop(a, lab[parity], lab[parity ^ 1], minE2, minE2 + R, map_max, st);
           record(ev++);
-          launch_hood_sums(a, t, st);
-          record(ev++);
-          k += 2;
-          if (a.flags && Hs) {
-            CK(cudaMemcpyAsync(h_row + uint64_t(t) * Hs, a.hist + uint64_t(t % (L + 1)) * Hs,
-                               Hs * 8, cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(h_flags + uint64_t(t) * Hs, a.flags, Hs, cudaMemcpyDeviceToHost,
-                               st));
+          k += 1;
+        } else {
+          for (int t = 0; t < map_max; ++t) {
+            const uint8_t* lin = lab[(parity + t) & 1];
+            uint8_t* lout = lab[(parity + t + 1) & 1];
+            record(ev++);
+            launch_vertex_argmin(a, lin, lout, t, st);
+            record(ev++);
+            launch_hood_sums(a, t, st);
+            record(ev++);
+            k += 2;
           }
         }
+        if (a.flags && Hs) {  // full trace: every MAP row and flag vector of this EM
+          CK(cudaMemcpyAsync(h_row, a.hist, uint64_t(map_max) * Hs * 8, cudaMemcpyDeviceToHost,
+                             st));
+          CK(cudaMemcpyAsync(h_flags, a.flags, uint64_t(map_max) * Hs, cudaMemcpyDeviceToHost,
+                             st));
+        }
         record(ev++);
-        launch_mstep(a.mean, R, M, lab[parity], lab[parity ^ 1], a.hist, Hs, L, a.unconv,
+        launch_mstep(a.mean, R, M, lab[parity], lab[parity ^ 1], a.hist, Hs, a.ring, a.unconv,
                      map_max, fixed, params, em_out, ctx->ms, st, &k);
         record(ev++);
         CK(cudaMemcpyAsync(h_em, em_out, (2 + 2 * M) * 8, cudaMemcpyDeviceToHost, st));
@@ -356,7 +369,8 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       };
       // One CUDA graph per label-buffer parity, captured once per shape and
       // replayed every EM iteration (the EM loop is launch-bound at 2560^2).
-      const bool use_graph = ctx->use_graphs;
+      const bool use_graph = ctx->use_graphs && !(o.flags & DPMRF_RUN_NO_GRAPH);
+      ctx->stats.graphs = use_graph;
       if (use_graph) {
         mstep_reserve(ctx->ms, R, M, Hs);
         dpmrf_context::GraphKey key{};
@@ -367,6 +381,7 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
         key.map_max = map_max;
         key.fixed = fixed;
         key.timing = timing;
+        key.persistent = persistent;
         key.trace = o.trace_level;
         key.beta = cfg->beta;
         key.tol = cfg->convergence_tol;
@@ -389,7 +404,7 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
         key.p[16] = ctx->ms.tile_counts.get();
         key.p[17] = ctx->ms.tile_base.get();
         key.p[18] = ctx->ms.layout.get();
-        key.p[19] = ctx->ms.row.get();
+        key.p[19] = nullptr;
         key.p[20] = h_flags;
         key.p[21] = a.cover;
         key.p[22] = a.g_off;
@@ -433,16 +448,23 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
         if (timing) {
           float ms = 0.f;
           size_t e = 0;
-          for (int t = 0; t < map_max; ++t, e += 3) {
-            CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
-            ctx->stats.vertex_kernel_ms += ms;
-            CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e + 1], ctx->ev_pool[e + 2]));
-            ctx->stats.hood_kernel_ms += ms;
+          if (persistent) {
+            CK(cudaEventElapsedTime(&ms, ctx->ev_pool[0], ctx->ev_pool[1]));
+            ctx->stats.map_loop_ms += ms;
+            ctx->stats.map_loop_launches += 1;
+            e = 2;
+          } else {
+            for (int t = 0; t < map_max; ++t, e += 3) {
+              CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
+              ctx->stats.vertex_kernel_ms += ms;
+              CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e + 1], ctx->ev_pool[e + 2]));
+              ctx->stats.hood_kernel_ms += ms;
+            }
+            ctx->stats.vertex_launches += map_max;
+            ctx->stats.hood_launches += map_max;
           }
           CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
           ctx->stats.mstep_ms += ms;
-          ctx->stats.vertex_launches += map_max;
-          ctx->stats.hood_launches += map_max;
         }
         const int T = static_cast<int>(h_em[1]);
         const double total = h_em[0];

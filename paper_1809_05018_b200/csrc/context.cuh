@@ -75,11 +75,12 @@ struct dpmrf_context {
   struct GraphKey {
     uint64_t R, Hs;
     uint32_t M;
-    int32_t L, map_max, fixed, timing, trace;
+    int32_t L, map_max, fixed, timing, trace, persistent;
     double beta, tol;
     const void* p[24];
   };
   bool use_graphs = true;
+  bool use_persistent = true;  // one cooperative MAP-loop kernel per EM iteration
   bool graph_valid = false;
   GraphKey graph_key{};
   cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};

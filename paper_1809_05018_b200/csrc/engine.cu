@@ -11,6 +11,8 @@
 // then gather the per-vertex minima in slot order.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "engine.cuh"
 
 namespace dpmrf_b200 {
@@ -35,16 +37,14 @@ __device__ __forceinline__ bool map_iter_skipped(const uint32_t* unconv, int t, 
 //   update_labels        engine.cpp:171-191 (uncovered vertices keep labels)
 // ---------------------------------------------------------------------------
 template <int MT>
-__global__ void __launch_bounds__(kVtxThreads)
-    k_vertex_argmin(const uint32_t* __restrict__ g_off, const uint32_t* __restrict__ g_nbr,
-                    const double* __restrict__ mean, const uint8_t* __restrict__ cover,
-                    const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
-                    double* __restrict__ minE, uint32_t R, uint32_t M_rt,
-                    const double* __restrict__ terms, double beta,
-                    const uint32_t* __restrict__ unconv, int t, int fixed) {
-  if (map_iter_skipped(unconv, t, fixed)) return;
-  const uint32_t v = blockIdx.x * kVtxThreads + threadIdx.x;
-  if (v >= R) return;
+__device__ __forceinline__ void vertex_body(uint32_t v, const uint32_t* __restrict__ g_off,
+                                            const uint32_t* __restrict__ g_nbr,
+                                            const double* __restrict__ mean,
+                                            const uint8_t* __restrict__ cover,
+                                            const uint8_t* __restrict__ lab_in,
+                                            uint8_t* __restrict__ lab_out,
+                                            double* __restrict__ minE, uint32_t M_rt,
+                                            const double* __restrict__ terms, double beta) {
   const uint8_t old = lab_in[v];
   if (!cover[v]) {
     lab_out[v] = old;
@@ -111,14 +111,29 @@ __global__ void __launch_bounds__(kVtxThreads)
   lab_out[v] = static_cast<uint8_t>(best_l);
 }
 
+template <int MT>
+__global__ void __launch_bounds__(kVtxThreads)
+    k_vertex_argmin(const uint32_t* __restrict__ g_off, const uint32_t* __restrict__ g_nbr,
+                    const double* __restrict__ mean, const uint8_t* __restrict__ cover,
+                    const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
+                    double* __restrict__ minE, uint32_t R, uint32_t M_rt,
+                    const double* __restrict__ terms, double beta,
+                    const uint32_t* __restrict__ unconv, int t, int fixed) {
+  if (map_iter_skipped(unconv, t, fixed)) return;
+  const uint32_t v = blockIdx.x * kVtxThreads + threadIdx.x;
+  if (v >= R) return;
+  vertex_body<MT>(v, g_off, g_nbr, mean, cover, lab_in, lab_out, minE, M_rt, terms, beta);
+}
+
 // ---------------------------------------------------------------------------
 // Hood energy sums + convergence window.
 //   neighborhood_energy_sums  engine.cpp:147-152 (fold_range in slot order)
 //   check_convergence         engine.cpp:154-169 (!(|last-prev| < tol) -> 0)
 //   all_set                   optimize.cpp:25-27 (block count -> one atomic)
 // ---------------------------------------------------------------------------
-__device__ double hood_fold_long(const uint32_t* __restrict__ h_mem,
-                                 const double* __restrict__ minE, uint32_t lo, uint32_t hi) {
+__device__ __noinline__ double hood_fold_long(const uint32_t* __restrict__ h_mem,
+                                              const double* __restrict__ minE, uint32_t lo,
+                                              uint32_t hi) {
   // fold_range for more than kFoldLeaf slots: leaves + pairwise tree.
   TreeStack<double, AddOp> st;
   for (uint32_t b = lo; b < hi; b += kFoldLeaf) {
@@ -130,48 +145,103 @@ __device__ double hood_fold_long(const uint32_t* __restrict__ h_mem,
   return st.finish(AddOp{});
 }
 
-template <bool kFlags>
+// Hood h of iteration t; returns 1 if NOT converged (0 for h >= Hs).
+__device__ __forceinline__ int hood_body(uint64_t h, const uint32_t* __restrict__ s_off,
+                                         const uint32_t* __restrict__ h_mem,
+                                         const double* __restrict__ minE,
+                                         double* __restrict__ hist, uint8_t* __restrict__ flags,
+                                         uint64_t Hs, int t, int L, int ring, double tol) {
+  if (h >= Hs) return 0;
+  const uint32_t lo = s_off[h], hi = s_off[h + 1];
+  double sum;
+  if (hi - lo <= kFoldLeaf) {
+    sum = minE[h_mem[lo]];
+    uint32_t s = lo + 1;
+    for (; s + 4 <= hi; s += 4) {
+      const double a0 = minE[h_mem[s]], a1 = minE[h_mem[s + 1]];
+      const double a2 = minE[h_mem[s + 2]], a3 = minE[h_mem[s + 3]];
+      sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, a0), a1), a2), a3);
+    }
+    for (; s < hi; ++s) sum = __dadd_rn(sum, minE[h_mem[s]]);
+  } else {
+    sum = hood_fold_long(h_mem, minE, lo, hi);
+  }
+  const int R1 = ring;  // >= L+1 rows; == map_max rows when the full trace is kept
+  hist[uint64_t(t % R1) * Hs + h] = sum;
+  int ok = 0;
+  if (t >= L) {
+    ok = 1;
+    for (int i = 1; i <= L; ++i) {
+      const double prev = hist[uint64_t((t - i) % R1) * Hs + h];
+      if (!(fabs(__dsub_rn(sum, prev)) < tol)) {
+        ok = 0;
+        break;
+      }
+    }
+  }
+  if (flags) flags[uint64_t(t) * Hs + h] = static_cast<uint8_t>(ok);
+  return !ok;
+}
+
 __global__ void __launch_bounds__(kHoodThreads)
     k_hood_sums(const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ h_mem,
                 const double* __restrict__ minE, double* __restrict__ hist,
-                uint8_t* __restrict__ flags, uint64_t Hs, int t, int L, double tol,
+                uint8_t* __restrict__ flags, uint64_t Hs, int t, int L, int ring, double tol,
                 uint32_t* __restrict__ unconv, int fixed) {
   if (map_iter_skipped(unconv, t, fixed)) return;
   const uint64_t h = uint64_t(blockIdx.x) * kHoodThreads + threadIdx.x;
-  int not_conv = 0;
-  if (h < Hs) {
-    const uint32_t lo = s_off[h], hi = s_off[h + 1];
-    double sum;
-    if (hi - lo <= kFoldLeaf) {
-      sum = minE[h_mem[lo]];
-      uint32_t s = lo + 1;
-      for (; s + 4 <= hi; s += 4) {
-        const double a0 = minE[h_mem[s]], a1 = minE[h_mem[s + 1]];
-        const double a2 = minE[h_mem[s + 2]], a3 = minE[h_mem[s + 3]];
-        sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, a0), a1), a2), a3);
-      }
-      for (; s < hi; ++s) sum = __dadd_rn(sum, minE[h_mem[s]]);
-    } else {
-      sum = hood_fold_long(h_mem, minE, lo, hi);
-    }
-    const int R1 = L + 1;
-    hist[uint64_t(t % R1) * Hs + h] = sum;
-    int ok = 0;
-    if (t >= L) {
-      ok = 1;
-      for (int i = 1; i <= L; ++i) {
-        const double prev = hist[uint64_t((t - i) % R1) * Hs + h];
-        if (!(fabs(__dsub_rn(sum, prev)) < tol)) {
-          ok = 0;
-          break;
-        }
-      }
-    }
-    if (kFlags) flags[h] = static_cast<uint8_t>(ok);
-    not_conv = !ok;
-  }
+  const int not_conv = hood_body(h, s_off, h_mem, minE, hist, flags, Hs, t, L, ring, tol);
   const int block_unconv = __syncthreads_count(not_conv);
   if (threadIdx.x == 0 && block_unconv) atomicAdd(&unconv[t], uint32_t(block_unconv));
+}
+
+// ---------------------------------------------------------------------------
+// Persistent MAP loop: all MAP iterations of one EM iteration in ONE
+// cooperative launch.  Phase p (0..map_max) runs, over a grid-stride work
+// list of 256-vertex and 256-hood tiles,
+//   * the hood sums + window test of iteration p-1 (minE[(p-1)&1]), and
+//   * the vertex pass of iteration p (minE[p&1], labels p -> p+1),
+// then one grid barrier.  The vertex pass of p is speculative: if iteration
+// p-1 turns out to be the last (all hoods converged, optimize.cpp:59), its
+// outputs are simply never read -- the committed labels are those of
+// iteration p-1, in the buffer the M-step selects from the same counters.
+// One barrier per MAP iteration instead of two kernel boundaries.
+// ---------------------------------------------------------------------------
+template <int MT>
+__global__ void __launch_bounds__(kVtxThreads)
+    k_map_loop(MapArgs a, uint8_t* lab0, uint8_t* lab1, double* minE0, double* minE1,
+               int map_max) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const uint64_t vt = (uint64_t(a.R) + kVtxThreads - 1) / kVtxThreads;
+  const uint64_t ht = (a.Hs + kHoodThreads - 1) / kHoodThreads;
+  for (int p = 0; p <= map_max; ++p) {
+    // iteration p-1 exists iff p-1 == 0 or iteration p-2 left hoods unconverged
+    const bool run_h = p >= 1 && (a.fixed || p == 1 || a.unconv[p - 2] != 0);
+    // vertex pass of p: skip once an earlier iteration is known to be the last
+    const bool run_v = p < map_max && (a.fixed || p <= 1 || a.unconv[p - 2] != 0);
+    if (!run_h && !run_v) break;
+    const uint8_t* lin = ((p & 1) ? lab1 : lab0);
+    uint8_t* lout = ((p & 1) ? lab0 : lab1);
+    double* mv = (p & 1) ? minE1 : minE0;
+    const double* mh = (p & 1) ? minE0 : minE1;
+    const uint64_t items = (run_h ? ht : 0) + (run_v ? vt : 0);
+    for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      if (run_h && it < ht) {
+        const uint64_t h = it * kHoodThreads + threadIdx.x;
+        const int nc = hood_body(h, a.s_off, a.h_mem, mh, a.hist, a.flags, a.Hs, p - 1, a.L,
+                                 a.ring, a.tol);
+        const int bu = __syncthreads_count(nc);
+        if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[p - 1], uint32_t(bu));
+      } else {
+        const uint64_t v = (it - (run_h ? ht : 0)) * kVtxThreads + threadIdx.x;
+        if (v < a.R)
+          vertex_body<MT>(static_cast<uint32_t>(v), a.g_off, a.g_nbr, a.mean, a.cover, lin, lout,
+                          mv, a.M, a.terms, a.beta);
+      }
+    }
+    grid.sync();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -181,7 +251,7 @@ __global__ void __launch_bounds__(kHoodThreads)
 //   dpp::reduce        kernels.hpp:124-139 (total energy, optimize.cpp:64-65)
 // ---------------------------------------------------------------------------
 constexpr int kTileThreads = 256;
-constexpr int kTileRounds = 16;
+constexpr int kTileRounds = 4;
 constexpr int kTileVerts = kTileThreads * kTileRounds;  // 4096 vertices per tile
 
 __device__ __forceinline__ int executed_iters(const uint32_t* unconv, int map_max, int fixed) {
@@ -290,61 +360,86 @@ __device__ __forceinline__ uint32_t series_of(const uint32_t* leaf_start, uint32
   return s;
 }
 
-// One thread per 1024-element leaf: left fold seeded by the first element
-// (fold_leaf, kernels.hpp:37-42).  kSq: fold (x - mu)^2 (engine.cpp:213-217).
+// Leaf folds (fold_leaf, kernels.hpp:37-42): each 1024-element leaf is a
+// strictly sequential left fold seeded by its first element -- the chain of
+// dependent adds cannot be reassociated without changing bits.  A block of
+// 256 threads therefore stages kLeavesPerBlock leaves into shared memory
+// with coalesced loads (the expensive part), then one lane per leaf runs the
+// dependent chain out of shared memory (rows padded to 1025 doubles so the
+// lanes hit distinct banks).  kSq folds (x - mu)^2 (engine.cpp:213-217).
+// Series M is the hood-energy row of the last executed MAP iteration (the
+// EM total energy, optimize.cpp:64-65), located from the device counters.
+constexpr int kLeavesPerBlock = 8;
+constexpr int kLeafStride = kFoldLeaf + 1;
+
 template <bool kSq>
 __global__ void __launch_bounds__(256)
     k_leaf_fold(const double* __restrict__ x, const uint32_t* __restrict__ layout, uint32_t M,
-                const double* __restrict__ hood_row, uint64_t Hs,
+                const double* __restrict__ hist, uint64_t Hs, int ring,
+                const uint32_t* __restrict__ unconv, int map_max, int fixed,
                 const double* __restrict__ params, double* __restrict__ partials) {
+  extern __shared__ double stage[];  // kLeavesPerBlock x kLeafStride
   const uint32_t* n = layout;
   const uint32_t* label_start = layout + M;
   const uint32_t* leaf_start = layout + 2 * M + 1;
   const uint32_t nseries = kSq ? M : M + 1;
-  const uint32_t leaf = blockIdx.x * blockDim.x + threadIdx.x;
-  if (leaf >= leaf_start[nseries]) return;
-  const uint32_t s = series_of(leaf_start, nseries, leaf);
-  const uint32_t k = leaf - leaf_start[s];
-  const double* src;
-  uint64_t len;
-  if (s < M) {
-    src = x + label_start[s];
-    len = n[s];
-  } else {
-    src = hood_row;
-    len = Hs;
+  const uint32_t total = leaf_start[nseries];
+  const uint32_t first = blockIdx.x * kLeavesPerBlock;
+  if (first >= total) return;
+  const double* hood_row = nullptr;
+  if (!kSq && unconv) {
+    const int T = executed_iters(unconv, map_max, fixed);
+    hood_row = hist + uint64_t((T - 1) % ring) * Hs;
   }
-  const uint64_t b = uint64_t(k) * kFoldLeaf;
-  const uint64_t e = min(len, b + kFoldLeaf);
+  __shared__ const double* src_s[kLeavesPerBlock];
+  __shared__ uint32_t len_s[kLeavesPerBlock];
+  __shared__ double mu_s[kLeavesPerBlock];
+  if (threadIdx.x < kLeavesPerBlock) {
+    const uint32_t leaf = first + threadIdx.x;
+    uint32_t len = 0;
+    const double* src = nullptr;
+    double mu = 0.0;
+    if (leaf < total) {
+      const uint32_t sr = series_of(leaf_start, nseries, leaf);
+      const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
+      const uint64_t slen = sr < M ? n[sr] : Hs;
+      src = (sr < M ? x + label_start[sr] : hood_row) + b;
+      const uint64_t rem = slen - b;
+      len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
+      if (kSq) mu = params[sr];
+    }
+    src_s[threadIdx.x] = src;
+    len_s[threadIdx.x] = len;
+    mu_s[threadIdx.x] = mu;
+  }
+  __syncthreads();
+  for (int j = 0; j < kLeavesPerBlock; ++j) {
+    const double* src = src_s[j];
+    const uint32_t len = len_s[j];
+    double* dst = stage + j * kLeafStride;
+    for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (threadIdx.x >= kLeavesPerBlock) return;
+  const uint32_t len = len_s[threadIdx.x];
+  if (len == 0) return;
+  const double* v = stage + threadIdx.x * kLeafStride;
   double acc;
   if (kSq) {
-    const double mu = params[s];
-    double d = __dsub_rn(src[b], mu);
+    const double mu = mu_s[threadIdx.x];
+    double d = __dsub_rn(v[0], mu);
     acc = __dmul_rn(d, d);
-    uint64_t i = b + 1;
-    for (; i + 4 <= e; i += 4) {
-      const double y0 = src[i], y1 = src[i + 1], y2 = src[i + 2], y3 = src[i + 3];
-      const double d0 = __dsub_rn(y0, mu), d1 = __dsub_rn(y1, mu);
-      const double d2 = __dsub_rn(y2, mu), d3 = __dsub_rn(y3, mu);
-      acc = __dadd_rn(acc, __dmul_rn(d0, d0));
-      acc = __dadd_rn(acc, __dmul_rn(d1, d1));
-      acc = __dadd_rn(acc, __dmul_rn(d2, d2));
-      acc = __dadd_rn(acc, __dmul_rn(d3, d3));
-    }
-    for (; i < e; ++i) {
-      d = __dsub_rn(src[i], mu);
+#pragma unroll 8
+    for (uint32_t i = 1; i < len; ++i) {
+      d = __dsub_rn(v[i], mu);
       acc = __dadd_rn(acc, __dmul_rn(d, d));
     }
   } else {
-    acc = src[b];
-    uint64_t i = b + 1;
-    for (; i + 4 <= e; i += 4) {
-      const double y0 = src[i], y1 = src[i + 1], y2 = src[i + 2], y3 = src[i + 3];
-      acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, y0), y1), y2), y3);
-    }
-    for (; i < e; ++i) acc = __dadd_rn(acc, src[i]);
+    acc = v[0];
+#pragma unroll 8
+    for (uint32_t i = 1; i < len; ++i) acc = __dadd_rn(acc, v[i]);
   }
-  partials[leaf] = acc;
+  partials[first + threadIdx.x] = acc;
 }
 
 // One block per series: pairwise tree over its leaf partials, bottom-up
@@ -378,13 +473,18 @@ __global__ void __launch_bounds__(1024)
   }
   if (threadIdx.x != 0) return;
   if (s < M) {
-    if (n[s] == 0) return;  // empty label keeps its previous parameters
-    const double count = static_cast<double>(n[s]);
-    if (!kSq) {
-      params[s] = __ddiv_rn(p[0], count);
-    } else {
-      const double sd = __dsqrt_rn(__ddiv_rn(p[0], count));
-      params[M + s] = sd < kSigmaFloor ? kSigmaFloor : sd;
+    if (n[s] != 0) {  // empty labels keep their previous parameters
+      const double count = static_cast<double>(n[s]);
+      if (!kSq) {
+        params[s] = __ddiv_rn(p[0], count);
+      } else {
+        const double sd = __dsqrt_rn(__ddiv_rn(p[0], count));
+        params[M + s] = sd < kSigmaFloor ? kSigmaFloor : sd;
+      }
+    }
+    if (kSq) {  // the final pass publishes (mu, sigma) of every label
+      em_out[2 + s] = params[s];
+      em_out[2 + M + s] = params[M + s];
     }
   } else {
     // total energy: dpp::reduce(..., 0.0) -> identity only for empty input
@@ -393,9 +493,6 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
-__global__ void k_copy_params(const double* params, double* em_out, uint32_t M) {
-  for (uint32_t i = threadIdx.x; i < 2 * M; i += blockDim.x) em_out[2 + i] = params[i];
-}
 
 __global__ void k_init_labels(uint8_t* lab, uint32_t R, uint32_t M, uint64_t seed) {
   const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -493,20 +590,47 @@ void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_
 
 void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s) {
   const unsigned g = grid_for(a.Hs, kHoodThreads);
-  if (a.flags)
-    k_hood_sums<true><<<g, kHoodThreads, 0, s>>>(a.s_off, a.h_mem, a.minE, a.hist, a.flags, a.Hs,
-                                                 t, a.L, a.tol, a.unconv, a.fixed);
-  else
-    k_hood_sums<false><<<g, kHoodThreads, 0, s>>>(a.s_off, a.h_mem, a.minE, a.hist, nullptr,
-                                                  a.Hs, t, a.L, a.tol, a.unconv, a.fixed);
+  k_hood_sums<<<g, kHoodThreads, 0, s>>>(a.s_off, a.h_mem, a.minE, a.hist, a.flags, a.Hs, t, a.L,
+                                         a.ring, a.tol, a.unconv, a.fixed);
   CK_LAUNCH();
+}
+
+// Cooperative launch of k_map_loop; grid = co-resident blocks (<= work tiles).
+void launch_map_loop(const MapArgs& a, uint8_t* lab_even, uint8_t* lab_odd, double* minE0,
+                     double* minE1, int map_max, cudaStream_t s) {
+  static int max_blocks[9] = {0};
+  const int mi = a.M <= 8 ? int(a.M) : 0;
+  void (*fn)(MapArgs, uint8_t*, uint8_t*, double*, double*, int);
+  switch (mi) {
+    case 2: fn = k_map_loop<2>; break;
+    case 3: fn = k_map_loop<3>; break;
+    case 4: fn = k_map_loop<4>; break;
+    case 5: fn = k_map_loop<5>; break;
+    case 6: fn = k_map_loop<6>; break;
+    case 7: fn = k_map_loop<7>; break;
+    case 8: fn = k_map_loop<8>; break;
+    default: fn = k_map_loop<0>; break;
+  }
+  if (!max_blocks[mi]) {
+    int per_sm = 0, dev = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kVtxThreads, 0));
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    max_blocks[mi] = per_sm * sms;
+  }
+  const uint64_t tiles = (uint64_t(a.R) + kVtxThreads - 1) / kVtxThreads +
+                         (a.Hs + kHoodThreads - 1) / kHoodThreads;
+  const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, max_blocks[mi])));
+  MapArgs args = a;
+  void* params[] = {&args, &lab_even, &lab_odd, &minE0, &minE1, &map_max};
+  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid), dim3(kVtxThreads), params, 0, s));
 }
 
 namespace {
 
 void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
                 const uint8_t* lab_odd, const uint32_t* unconv, int map_max, int fixed,
-                const double* hood_row_base, uint64_t Hs, int L, double* params, double* em_out,
+                const double* hist, uint64_t Hs, int ring, double* params, double* em_out,
                 MStepBuffers& mb, cudaStream_t s, uint64_t* launches) {
   const uint32_t tiles = static_cast<uint32_t>((uint64_t(R) + kTileVerts - 1) / kTileVerts);
   const uint32_t tiles_g = tiles ? tiles : 1;
@@ -535,57 +659,40 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
     CK_LAUNCH();
     ++n;
   }
-  // hood row of the last executed MAP iteration: resolved on the device via
-  // a pointer table would need the count; instead both folds read the row
-  // chosen by k_pick_row (below) -- see launch_mstep.
-  (void)L;
-  const unsigned lg = grid_for(max_leaves, 256);
-  k_leaf_fold<false><<<lg, 256, 0, s>>>(x, layout, M, hood_row_base, Hs, params, partials);
+  static bool smem_set = false;
+  const size_t leaf_smem = size_t(kLeavesPerBlock) * kLeafStride * sizeof(double);
+  if (!smem_set) {
+    CK(cudaFuncSetAttribute(k_leaf_fold<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(leaf_smem)));
+    CK(cudaFuncSetAttribute(k_leaf_fold<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(leaf_smem)));
+    smem_set = true;
+  }
+  const unsigned lg = grid_for(max_leaves, kLeavesPerBlock);
+  k_leaf_fold<false><<<lg, 256, leaf_smem, s>>>(x, layout, M, hist, Hs, ring, unconv, map_max,
+                                                fixed, params, partials);
   CK_LAUNCH();
   k_tree_finalize<false><<<M + 1, 1024, 0, s>>>(partials, layout, M, params, em_out, unconv,
                                                 map_max, fixed);
   CK_LAUNCH();
-  k_leaf_fold<true><<<lg, 256, 0, s>>>(x, layout, M, nullptr, 0, params, partials);
+  k_leaf_fold<true><<<lg, 256, leaf_smem, s>>>(x, layout, M, nullptr, 0, 1, nullptr, map_max,
+                                               fixed, params, partials);
   CK_LAUNCH();
   k_tree_finalize<true><<<M, 1024, 0, s>>>(partials, layout, M, params, em_out, unconv, map_max,
                                            fixed);
   CK_LAUNCH();
-  k_copy_params<<<1, 256, 0, s>>>(params, em_out, M);
-  CK_LAUNCH();
-  n += 5;
+  n += 4;
   if (launches) *launches += n;
-}
-
-// Copies the hood-energy row of the last executed MAP iteration into a
-// contiguous buffer the leaf folds read (the ring slot depends on the
-// device-side iteration count).
-__global__ void k_pick_row(const double* __restrict__ hist, uint64_t Hs, int L,
-                           const uint32_t* __restrict__ unconv, int map_max, int fixed,
-                           double* __restrict__ row) {
-  const int T = executed_iters(unconv, map_max, fixed);
-  const double* src = hist + uint64_t((T - 1) % (L + 1)) * Hs;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < Hs; i += stride)
-    row[i] = src[i];
 }
 
 }  // namespace
 
 void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
-                  const uint8_t* lab_odd, const double* hist, uint64_t Hs, int L,
+                  const uint8_t* lab_odd, const double* hist, uint64_t Hs, int ring,
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches) {
-  // The last row is copied out of the ring (Hs doubles) so the leaf kernel
-  // can address it without the device-side iteration count.
-  double* row = mb.row.ensure(Hs);
-  if (Hs) {
-    k_pick_row<<<std::min<unsigned>(grid_for(Hs, 256), 4 * kNumSMs), 256, 0, s>>>(
-        hist, Hs, L, unconv, map_max, fixed, row);
-    CK_LAUNCH();
-    if (launches) ++*launches;
-  }
-  mstep_core(mean, R, M, lab_even, lab_odd, unconv, map_max, fixed, row, Hs, L, params, em_out,
-             mb, s, launches);
+  mstep_core(mean, R, M, lab_even, lab_odd, unconv, map_max, fixed, hist, Hs, ring, params,
+             em_out, mb, s, launches);
 }
 
 void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs) {
@@ -596,7 +703,6 @@ void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs) {
   mb.layout.ensure(4 * M + 4);
   mb.x.ensure(R);
   mb.partials.ensure((uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M + (Hs + kFoldLeaf - 1) / kFoldLeaf + 1);
-  mb.row.ensure(Hs);
 }
 
 void launch_update_parameters_u32(const double* mean, uint32_t R, uint32_t M,

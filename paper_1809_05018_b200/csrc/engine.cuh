@@ -23,11 +23,12 @@ struct MapArgs {
   double beta;
   double tol;
   int L;         // convergence_window
+  int ring;      // rows of the hood-energy ring (L+1, or map_max for the full trace)
   int fixed;     // 1 = no early exit
   const double* terms;
   double* minE;    // R
-  double* hist;    // (L+1) x Hs ring of hood energies
-  uint8_t* flags;  // Hs (nullptr = not recorded)
+  double* hist;    // ring x Hs hood energies
+  uint8_t* flags;  // map_max x Hs convergence flags (nullptr = not recorded)
   uint32_t* unconv;  // per MAP iteration count of unconverged hoods
 };
 
@@ -37,6 +38,9 @@ struct MapArgs {
 void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out, int t,
                           cudaStream_t s);
 void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s);
+// The whole MAP loop of one EM iteration as one cooperative kernel (see engine.cu).
+void launch_map_loop(const MapArgs& a, uint8_t* lab_even, uint8_t* lab_odd, double* minE0,
+                     double* minE1, int map_max, cudaStream_t s);
 
 struct MStepBuffers {
   DevBuf<uint32_t> tile_counts;  // tiles x M
@@ -54,7 +58,7 @@ struct MStepBuffers {
 // that iteration's hood-energy row.  params (2M, device) is updated in
 // place; em_out receives [total, map_iters, mu(M), sigma(M)].
 void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
-                  const uint8_t* lab_odd, const double* hist, uint64_t Hs, int L,
+                  const uint8_t* lab_odd, const double* hist, uint64_t Hs, int ring,
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches);
 
