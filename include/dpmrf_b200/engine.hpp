@@ -121,13 +121,12 @@ struct Backend {
 
 namespace detail {
 
-// One context per (thread, device); the resident graph/hoods are re-uploaded
-// only when a different object (or a modified one) is passed.
+// One context per (thread, device).  The reference takes its inputs by const&
+// on every call, so every call uploads them (an address-based cache would be
+// fooled by a new object at a reused address); use the C ABI directly to keep
+// a graph resident across calls.
 struct Ctx {
   dpmrf_context* h = nullptr;
-  const void* graph_key = nullptr;
-  const void* hoods_key = nullptr;
-  std::size_t graph_sig = 0, hoods_sig = 0;
   explicit Ctx(int device) { throw_status(dpmrf_context_create(device, &h), "dpmrf_context_create"); }
   ~Ctx() { dpmrf_context_destroy(h); }
 };
@@ -142,22 +141,14 @@ inline Ctx& ctx_for(const dpp::Backend& b) {
 }
 
 inline void graph(Ctx& c, const RegionGraph& g) {
-  const std::size_t sig = g.neighbors.size() * 31 + g.num_vertices;
-  if (c.graph_key == &g && c.graph_sig == sig) return;
   throw_status(dpmrf_set_graph(c.h, g.num_vertices, g.offsets.data(), g.neighbors.data(),
                                g.region_mean.data()),
                "set_graph");
-  c.graph_key = &g;
-  c.graph_sig = sig;
 }
 
 inline void hoods(Ctx& c, const NeighborhoodSet& h) {
-  const std::size_t sig = h.members.size() * 31 + h.offsets.size();
-  if (c.hoods_key == &h && c.hoods_sig == sig) return;
   std::vector<std::uint32_t> off = h.offsets.empty() ? std::vector<std::uint32_t>{0} : h.offsets;
   throw_status(dpmrf_set_hoods(c.h, off.size() - 1, off.data(), h.members.data()), "set_hoods");
-  c.hoods_key = &h;
-  c.hoods_sig = sig;
 }
 
 }  // namespace detail
@@ -369,7 +360,6 @@ inline NeighborhoodSet build_neighborhoods(const dpp::Backend& b, const RegionGr
   throw_status(dpmrf_get_hoods(c.h, &H, &S, h.offsets.data(), h.members.data(),
                                h.source_clique.data()),
                "get_hoods");
-  c.hoods_key = nullptr;  // resident hoods now come from the device build
   return h;
 }
 

@@ -413,11 +413,20 @@ __global__ void __launch_bounds__(256)
     mu_s[threadIdx.x] = mu;
   }
   __syncthreads();
-  for (int j = 0; j < kLeavesPerBlock; ++j) {
-    const double* src = src_s[j];
-    const uint32_t len = len_s[j];
-    double* dst = stage + j * kLeafStride;
-    for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
+  // all kLeavesPerBlock*1024/256 = 32 loads of a thread are issued before any
+  // store so they are in flight together (one memory round trip, not 32)
+  constexpr int kPer = kLeavesPerBlock * int(kFoldLeaf) / 256;
+  double r[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
+    const uint32_t j = flat / kFoldLeaf, i = flat % kFoldLeaf;
+    r[q] = i < len_s[j] ? __ldg(src_s[j] + i) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
+    stage[(flat / kFoldLeaf) * kLeafStride + flat % kFoldLeaf] = r[q];
   }
   __syncthreads();
   if (threadIdx.x >= kLeavesPerBlock) return;

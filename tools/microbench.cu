@@ -1,0 +1,116 @@
+// microbench.cu -- latency probes that shape the optimization-phase design on
+// B200: dependent DADD chain, dependent LDS->DADD chain, cooperative grid
+// barrier cost vs grid size, and back-to-back empty kernels in a CUDA graph.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o microbench tools/microbench.cu
+#include <cooperative_groups.h>
+#include <chrono>
+#include <cstdio>
+#include <vector>
+
+namespace cg = cooperative_groups;
+
+__global__ void dadd_chain(double* out, double x, int n, long long* cycles) {
+  double acc = x;
+  const long long t0 = clock64();
+  for (int i = 0; i < n; ++i) acc = __dadd_rn(acc, x);
+  const long long t1 = clock64();
+  out[0] = acc;
+  cycles[0] = t1 - t0;
+}
+
+__global__ void lds_chain(double* out, int n, long long* cycles) {
+  __shared__ double s[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) s[i] = 1.0 + i * 1e-9;
+  __syncthreads();
+  if (threadIdx.x) return;
+  double acc = 0.0;
+  const long long t0 = clock64();
+  for (int r = 0; r < n / 1024; ++r)
+#pragma unroll 8
+    for (int i = 0; i < 1024; ++i) acc = __dadd_rn(acc, s[i]);
+  const long long t1 = clock64();
+  out[0] = acc;
+  cycles[0] = t1 - t0;
+}
+
+__global__ void grid_barriers(int iters, int* sink) {
+  cg::grid_group g = cg::this_grid();
+  for (int i = 0; i < iters; ++i) g.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) sink[0] = iters;
+}
+
+__global__ void empty_kernel(int* sink) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) sink[0] += 1;
+}
+
+int main() {
+  double* d;
+  long long* c;
+  int* sink;
+  cudaMalloc(&d, 64);
+  cudaMalloc(&c, 64);
+  cudaMalloc(&sink, 64);
+  long long h;
+  const int n = 1 << 20;
+  dadd_chain<<<1, 1>>>(d, 1e-9, n, c);
+  cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("dependent DADD: %.2f cycles/op\n", double(h) / n);
+  lds_chain<<<1, 256>>>(d, n, c);
+  cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("dependent LDS+DADD fold (unroll 8): %.2f cycles/element\n", double(h) / n);
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, grid_barriers, 256, 0);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int blocks : {sms, 2 * sms, 4 * sms, per * sms}) {
+    int iters = 1000;
+    void* args[] = {&iters, &sink};
+    cudaLaunchCooperativeKernel((void*)grid_barriers, blocks, 256, args, 0, 0);
+    cudaEventRecord(a);
+    cudaLaunchCooperativeKernel((void*)grid_barriers, blocks, 256, args, 0, 0);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("grid.sync with %d blocks x 256: %.2f us/barrier\n", blocks, ms * 1e3 / iters);
+  }
+  // 1000 dependent empty kernels captured in a graph
+  cudaStream_t s;
+  cudaStreamCreate(&s);
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  for (int i = 0; i < 1000; ++i) empty_kernel<<<1, 32, 0, s>>>(sink);
+  cudaStreamEndCapture(s, &g);
+  cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphLaunch(ge, s);
+  cudaStreamSynchronize(s);
+  cudaEventRecord(a, s);
+  cudaGraphLaunch(ge, s);
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  printf("graph of 1000 tiny kernels: %.2f us/kernel\n", ms);
+  cudaEventRecord(a, s);
+  for (int i = 0; i < 1000; ++i) empty_kernel<<<1, 32, 0, s>>>(sink);
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  cudaEventElapsedTime(&ms, a, b);
+  printf("stream of 1000 tiny kernels: %.2f us/kernel\n", ms);
+  // host round trip: launch + sync of one tiny kernel + 8-byte D2H
+  long long* hp;
+  cudaMallocHost(&hp, 64);
+  auto t0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < 1000; ++i) {
+    empty_kernel<<<1, 32, 0, s>>>(sink);
+    cudaMemcpyAsync(hp, c, 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  printf("host round trip (launch + D2H + sync): %.2f us\n",
+         std::chrono::duration<double, std::micro>(t1 - t0).count() / 1000);
+  return 0;
+}
