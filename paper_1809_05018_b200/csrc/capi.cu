@@ -134,6 +134,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     c->device = device;
     if (const char* e = std::getenv("DPMRF_NO_GRAPH")) c->use_graphs = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_MAP_KERNELS")) c->use_persistent = e[0] != '2';
+    if (const char* e = std::getenv("DPMRF_DIRECT")) c->use_staged = e[0] == '0';
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -304,6 +305,7 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       a.L = L;
       a.ring = full ? map_max : L + 1;
       a.fixed = fixed;
+      a.staged = ctx->use_staged ? 1 : 0;
       a.terms = ctx->terms.ensure(3 * M);
       double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
       a.minE = minE2;
@@ -328,8 +330,13 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       for (size_t i = 0; i < ev_per_em; ++i) ctx->event(i);
       // Everything one EM iteration puts on the stream (no host sync inside).
       uint64_t em_kernels = 0;
+      bool capturing = false;  // event records become graph nodes only when captured as external
       auto record = [&](size_t i) {
-        if (timing) CK(cudaEventRecordWithFlags(ctx->ev_pool[i], st, cudaEventRecordExternal));
+        if (!timing) return;
+        if (capturing)
+          CK(cudaEventRecordWithFlags(ctx->ev_pool[i], st, cudaEventRecordExternal));
+        else
+          CK(cudaEventRecord(ctx->ev_pool[i], st));
       };
       auto enqueue_em = [&](int parity) {
         uint64_t k = 0;
@@ -414,13 +421,16 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
           for (int parity = 0; parity < 2; ++parity) {
             cudaGraph_t g;
             CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            capturing = true;
             try {
               enqueue_em(parity);
             } catch (...) {
+              capturing = false;
               cudaStreamEndCapture(st, &g);
               if (g) cudaGraphDestroy(g);
               throw;
             }
+            capturing = false;
             CK(cudaStreamEndCapture(st, &g));
             CK(cudaGraphInstantiate(&ctx->graph_exec[parity], g, 0));
             CK(cudaGraphDestroy(g));

@@ -30,6 +30,7 @@ struct Error : std::runtime_error {
 
 inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e != cudaSuccess) {
+    (void)cudaGetLastError();  // clear a non-sticky error so later launch checks stay clean
     char buf[512];
     std::snprintf(buf, sizeof buf, "%s failed at %s:%d: %s", what, file, line,
                   cudaGetErrorString(e));

@@ -81,6 +81,7 @@ struct dpmrf_context {
   };
   bool use_graphs = true;
   bool use_persistent = true;  // one cooperative MAP-loop kernel per EM iteration
+  bool use_staged = true;      // shared-memory staged vertex / hood tiles
   bool graph_valid = false;
   GraphKey graph_key{};
   cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};

@@ -183,6 +183,180 @@ __device__ __forceinline__ int hood_body(uint64_t h, const uint32_t* __restrict_
   return !ok;
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory staged tiles (256 vertices / 256 hoods per block).
+// A tile's CSR range is contiguous, so the block reads it with coalesced
+// loads and resolves the data-dependent gathers (neighbor labels / member
+// minima) cooperatively, kBatch independent loads per thread in flight; the
+// per-vertex / per-hood arithmetic then runs out of shared memory in exactly
+// the order of the direct bodies above.  Tiles whose range exceeds the stage
+// (high-degree hubs) fall back to the direct bodies.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kVtxStageCap = 4096;   // neighbor labels per vertex tile (u8)
+constexpr uint32_t kHoodStageCap = 4096;  // member minima per hood tile (f64, 32 KB)
+constexpr int kBatch = 8;
+
+template <int MT>
+__device__ __forceinline__ void vertex_tile(uint64_t tile, const MapArgs& a,
+                                            const uint8_t* __restrict__ lab_in,
+                                            uint8_t* __restrict__ lab_out,
+                                            double* __restrict__ minE, uint8_t* sm_lab) {
+  const uint32_t v0 = static_cast<uint32_t>(tile * kVtxThreads);
+  const uint32_t vend = min(a.R, v0 + kVtxThreads);
+  const uint32_t v = v0 + threadIdx.x;
+  const uint32_t base = a.g_off[v0], cnt = a.g_off[vend] - base;
+  if (cnt > kVtxStageCap) {
+    if (v < vend) vertex_body<MT>(v, a.g_off, a.g_nbr, a.mean, a.cover, lab_in, lab_out, minE, a.M,
+                                  a.terms, a.beta);
+    return;
+  }
+  for (uint32_t c0 = 0; c0 < cnt; c0 += kBatch * kVtxThreads) {
+    uint32_t id[kBatch];
+    uint8_t lb[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const uint32_t i = c0 + q * kVtxThreads + threadIdx.x;
+      id[q] = i < cnt ? a.g_nbr[base + i] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const uint32_t i = c0 + q * kVtxThreads + threadIdx.x;
+      lb[q] = i < cnt ? lab_in[id[q]] : uint8_t(0);
+    }
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const uint32_t i = c0 + q * kVtxThreads + threadIdx.x;
+      if (i < cnt) sm_lab[i] = lb[q];
+    }
+  }
+  __syncthreads();
+  if (v < vend) {
+    const uint8_t old = lab_in[v];
+    if (!a.cover[v]) {
+      lab_out[v] = old;
+    } else {
+      const uint32_t M = MT > 0 ? uint32_t(MT) : a.M;
+      const uint32_t lo = a.g_off[v] - base, hi = a.g_off[v + 1] - base;
+      const uint32_t deg = hi - lo;
+      const double x = a.mean[v];
+      const double* T = a.terms;
+      double best;
+      uint32_t best_l;
+      if constexpr (MT == 2) {
+        uint32_t ones = 0;
+        for (uint32_t k = lo; k < hi; ++k) ones += sm_lab[k];
+        const double e0 = label_energy(x, T[0], T[2], T[4], a.beta, ones);
+        const double e1 = label_energy(x, T[1], T[3], T[5], a.beta, deg - ones);
+        best = e0;
+        best_l = 0;
+        if (e1 < best) {
+          best = e1;
+          best_l = 1;
+        }
+      } else {
+        best = 0.0;
+        best_l = 0;
+        for (uint32_t l = 0; l < M; ++l) {
+          uint32_t same = 0;
+          for (uint32_t k = lo; k < hi; ++k) same += (sm_lab[k] == l);
+          const double e = label_energy(x, T[l], T[M + l], T[2 * M + l], a.beta, deg - same);
+          if (l == 0 || e < best) {
+            best = e;
+            best_l = l;
+          }
+        }
+      }
+      minE[v] = best;
+      lab_out[v] = static_cast<uint8_t>(best_l);
+    }
+  }
+  __syncthreads();  // the stage is reused by the next tile of a persistent block
+}
+
+// Returns this thread's "not converged" flag (0 for threads past the end).
+__device__ __forceinline__ int hood_tile(uint64_t tile, const MapArgs& a,
+                                         const double* __restrict__ minE, int t, double* sm_e) {
+  const uint64_t h0 = tile * kHoodThreads;
+  const uint64_t hcap = h0 + kHoodThreads;
+  const uint64_t hend = a.Hs < hcap ? a.Hs : hcap;
+  const uint64_t h = h0 + threadIdx.x;
+  const uint32_t base = a.s_off[h0], cnt = a.s_off[hend] - base;
+  if (cnt > kHoodStageCap)
+    return hood_body(h, a.s_off, a.h_mem, minE, a.hist, a.flags, a.Hs, t, a.L, a.ring, a.tol);
+  for (uint32_t c0 = 0; c0 < cnt; c0 += kBatch * kHoodThreads) {
+    uint32_t id[kBatch];
+    double e[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const uint32_t i = c0 + q * kHoodThreads + threadIdx.x;
+      id[q] = i < cnt ? a.h_mem[base + i] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const uint32_t i = c0 + q * kHoodThreads + threadIdx.x;
+      e[q] = i < cnt ? minE[id[q]] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const uint32_t i = c0 + q * kHoodThreads + threadIdx.x;
+      if (i < cnt) sm_e[i] = e[q];
+    }
+  }
+  __syncthreads();
+  int not_conv = 0;
+  if (h < hend) {
+    const uint32_t lo = a.s_off[h] - base, hi = a.s_off[h + 1] - base;
+    double sum;
+    if (hi - lo <= kFoldLeaf) {
+      sum = sm_e[lo];
+      for (uint32_t k = lo + 1; k < hi; ++k) sum = __dadd_rn(sum, sm_e[k]);
+    } else {  // fold_range: leaves + pairwise tree (kernels.hpp:56-65)
+      TreeStack<double, AddOp> st;
+      for (uint32_t b = lo; b < hi; b += kFoldLeaf) {
+        const uint32_t e2 = min(hi, b + kFoldLeaf);
+        double acc = sm_e[b];
+        for (uint32_t k = b + 1; k < e2; ++k) acc = __dadd_rn(acc, sm_e[k]);
+        st.push(acc, AddOp{});
+      }
+      sum = st.finish(AddOp{});
+    }
+    const int R1 = a.ring;
+    a.hist[uint64_t(t % R1) * a.Hs + h] = sum;
+    int ok = 0;
+    if (t >= a.L) {
+      ok = 1;
+      for (int i = 1; i <= a.L; ++i) {
+        const double prev = a.hist[uint64_t((t - i) % R1) * a.Hs + h];
+        if (!(fabs(__dsub_rn(sum, prev)) < a.tol)) {
+          ok = 0;
+          break;
+        }
+      }
+    }
+    if (a.flags) a.flags[uint64_t(t) * a.Hs + h] = static_cast<uint8_t>(ok);
+    not_conv = !ok;
+  }
+  __syncthreads();
+  return not_conv;
+}
+
+template <int MT>
+__global__ void __launch_bounds__(kVtxThreads)
+    k_vertex_staged(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
+                    int t) {
+  __shared__ uint8_t sm_lab[kVtxStageCap];
+  if (map_iter_skipped(a.unconv, t, a.fixed)) return;
+  vertex_tile<MT>(blockIdx.x, a, lab_in, lab_out, a.minE, sm_lab);
+}
+
+__global__ void __launch_bounds__(kHoodThreads) k_hood_staged(MapArgs a, int t) {
+  __shared__ double sm_e[kHoodStageCap];
+  if (map_iter_skipped(a.unconv, t, a.fixed)) return;
+  const int nc = hood_tile(blockIdx.x, a, a.minE, t, sm_e);
+  const int bu = __syncthreads_count(nc);
+  if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[t], uint32_t(bu));
+}
+
 __global__ void __launch_bounds__(kHoodThreads)
     k_hood_sums(const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ h_mem,
                 const double* __restrict__ minE, double* __restrict__ hist,
@@ -208,11 +382,13 @@ __global__ void __launch_bounds__(kHoodThreads)
 // One barrier per MAP iteration instead of two kernel boundaries.
 // ---------------------------------------------------------------------------
 template <int MT>
-__global__ void __launch_bounds__(kVtxThreads)
+__global__ void __launch_bounds__(kVtxThreads, 6)
     k_map_loop(MapArgs a, uint8_t* lab0, uint8_t* lab1, double* minE0, double* minE1,
                int map_max) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
+  __shared__ uint8_t sm_lab[kVtxStageCap];
+  __shared__ double sm_e[kHoodStageCap];
   const uint64_t vt = (uint64_t(a.R) + kVtxThreads - 1) / kVtxThreads;
   const uint64_t ht = (a.Hs + kHoodThreads - 1) / kHoodThreads;
   for (int p = 0; p <= map_max; ++p) {
@@ -228,16 +404,11 @@ __global__ void __launch_bounds__(kVtxThreads)
     const uint64_t items = (run_h ? ht : 0) + (run_v ? vt : 0);
     for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
       if (run_h && it < ht) {
-        const uint64_t h = it * kHoodThreads + threadIdx.x;
-        const int nc = hood_body(h, a.s_off, a.h_mem, mh, a.hist, a.flags, a.Hs, p - 1, a.L,
-                                 a.ring, a.tol);
+        const int nc = hood_tile(it, a, mh, p - 1, sm_e);
         const int bu = __syncthreads_count(nc);
         if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[p - 1], uint32_t(bu));
       } else {
-        const uint64_t v = (it - (run_h ? ht : 0)) * kVtxThreads + threadIdx.x;
-        if (v < a.R)
-          vertex_body<MT>(static_cast<uint32_t>(v), a.g_off, a.g_nbr, a.mean, a.cover, lin, lout,
-                          mv, a.M, a.terms, a.beta);
+        vertex_tile<MT>(it - (run_h ? ht : 0), a, lin, lout, mv, sm_lab);
       }
     }
     grid.sync();
@@ -580,6 +751,14 @@ __global__ void k_compact_offsets(const uint32_t* __restrict__ h_off, uint64_t H
 void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out, int t,
                           cudaStream_t s) {
   const unsigned g = grid_for(a.R, kVtxThreads);
+  if (a.staged) {
+    switch (a.M) {  // M = 2 is specialised; other M share the counted-compare loop
+      case 2: k_vertex_staged<2><<<g, kVtxThreads, 0, s>>>(a, lab_in, lab_out, t); break;
+      default: k_vertex_staged<0><<<g, kVtxThreads, 0, s>>>(a, lab_in, lab_out, t); break;
+    }
+    CK_LAUNCH();
+    return;
+  }
 #define VA_ARGS                                                                              \
   a.g_off, a.g_nbr, a.mean, a.cover, lab_in, lab_out, a.minE, a.R, a.M, a.terms, a.beta, \
       a.unconv, t, a.fixed
@@ -599,8 +778,11 @@ void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_
 
 void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s) {
   const unsigned g = grid_for(a.Hs, kHoodThreads);
-  k_hood_sums<<<g, kHoodThreads, 0, s>>>(a.s_off, a.h_mem, a.minE, a.hist, a.flags, a.Hs, t, a.L,
-                                         a.ring, a.tol, a.unconv, a.fixed);
+  if (a.staged)
+    k_hood_staged<<<g, kHoodThreads, 0, s>>>(a, t);
+  else
+    k_hood_sums<<<g, kHoodThreads, 0, s>>>(a.s_off, a.h_mem, a.minE, a.hist, a.flags, a.Hs, t,
+                                           a.L, a.ring, a.tol, a.unconv, a.fixed);
   CK_LAUNCH();
 }
 

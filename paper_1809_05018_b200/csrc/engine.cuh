@@ -25,6 +25,7 @@ struct MapArgs {
   int L;         // convergence_window
   int ring;      // rows of the hood-energy ring (L+1, or map_max for the full trace)
   int fixed;     // 1 = no early exit
+  int staged;    // 1 = shared-memory staged tiles (default), 0 = one thread per item
   const double* terms;
   double* minE;    // R
   double* hist;    // ring x Hs hood energies
