@@ -67,8 +67,10 @@ enum {
   DPMRF_RUN_FIXED_WORK = 1u,    /* drop the early exits (optimize.cpp:59,:71): fixed EM x MAP work */
   DPMRF_RUN_MULTILABEL = 2u,    /* allow num_labels in [1,255] (extension; reference: 2 only) */
   DPMRF_RUN_KERNEL_TIMING = 4u, /* CUDA events around the MAP kernels (dpmrf_get_stats) */
-  DPMRF_RUN_TWO_KERNELS = 8u,   /* two kernels per MAP iteration instead of the persistent loop */
-  DPMRF_RUN_NO_GRAPH = 16u      /* launch each EM iteration directly instead of a CUDA graph */
+  DPMRF_RUN_TWO_KERNELS = 8u,   /* two kernels per MAP iteration (the default) */
+  DPMRF_RUN_NO_GRAPH = 16u,     /* launch each EM iteration directly instead of a CUDA graph */
+  DPMRF_RUN_PERSISTENT = 32u,   /* one cooperative persistent kernel per MAP loop */
+  DPMRF_RUN_STAGED = 64u        /* shared-memory staged vertex/hood tiles */
 };
 
 typedef struct dpmrf_run_options {

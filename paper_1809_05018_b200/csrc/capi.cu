@@ -133,7 +133,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     auto* c = new dpmrf_context;
     c->device = device;
     if (const char* e = std::getenv("DPMRF_NO_GRAPH")) c->use_graphs = e[0] == '0';
-    if (const char* e = std::getenv("DPMRF_MAP_KERNELS")) c->use_persistent = e[0] != '2';
+    if (const char* e = std::getenv("DPMRF_MAP_KERNELS")) c->use_persistent = e[0] == '1';
     if (const char* e = std::getenv("DPMRF_DIRECT")) c->use_staged = e[0] == '0';
     try {
       CK(cudaSetDevice(device));
@@ -301,11 +301,12 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       a.beta = cfg->beta;
       a.tol = cfg->convergence_tol;
       const bool full = o.trace_level >= DPMRF_TRACE_FULL;
-      const bool persistent = ctx->use_persistent && !(o.flags & DPMRF_RUN_TWO_KERNELS);
+      const bool persistent = (o.flags & DPMRF_RUN_PERSISTENT) ||
+                              (ctx->use_persistent && !(o.flags & DPMRF_RUN_TWO_KERNELS));
       a.L = L;
       a.ring = full ? map_max : L + 1;
       a.fixed = fixed;
-      a.staged = ctx->use_staged ? 1 : 0;
+      a.staged = (ctx->use_staged || (o.flags & DPMRF_RUN_STAGED)) ? 1 : 0;
       a.terms = ctx->terms.ensure(3 * M);
       double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
       a.minE = minE2;
@@ -388,7 +389,7 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
         key.map_max = map_max;
         key.fixed = fixed;
         key.timing = timing;
-        key.persistent = persistent;
+        key.persistent = persistent + 2 * a.staged;
         key.trace = o.trace_level;
         key.beta = cfg->beta;
         key.tol = cfg->convergence_tol;

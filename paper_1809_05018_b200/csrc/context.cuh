@@ -80,8 +80,14 @@ struct dpmrf_context {
     const void* p[24];
   };
   bool use_graphs = true;
-  bool use_persistent = true;  // one cooperative MAP-loop kernel per EM iteration
-  bool use_staged = true;      // shared-memory staged vertex / hood tiles
+  // one cooperative MAP-loop kernel per EM iteration instead of two kernels
+  // per MAP iteration: measured slower at both 2560^2 and 16384^2 (fewer
+  // resident blocks per phase + grid-barrier cost), so opt-in
+  bool use_persistent = false;
+  // shared-memory staged vertex / hood tiles: measured SLOWER than one thread
+  // per item on B200 (L1 already absorbs the CSR segment reads; the staged
+  // hood fold is bank-conflicted), so off unless DPMRF_DIRECT=0
+  bool use_staged = false;
   bool graph_valid = false;
   GraphKey graph_key{};
   cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};

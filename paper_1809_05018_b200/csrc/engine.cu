@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kHoodThreads)
 // One barrier per MAP iteration instead of two kernel boundaries.
 // ---------------------------------------------------------------------------
 template <int MT>
-__global__ void __launch_bounds__(kVtxThreads, 6)
+__global__ void __launch_bounds__(kVtxThreads)
     k_map_loop(MapArgs a, uint8_t* lab0, uint8_t* lab1, double* minE0, double* minE1,
                int map_max) {
   namespace cg = cooperative_groups;
