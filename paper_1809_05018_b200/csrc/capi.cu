@@ -313,6 +313,9 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       a.hist = ctx->hist.ensure(uint64_t(a.ring) * Hs);
       a.flags = full ? ctx->flags.ensure(uint64_t(map_max) * Hs) : nullptr;
       a.unconv = ctx->unconv.ensure(map_max);
+      mstep_reserve(ctx->ms, R, M, Hs);  // before any capture: no allocation inside a graph
+      a.tile_counts = ctx->ms.counts.get();
+      a.tiles = label_tiles(R);
       double* params = ctx->params.ensure(2 * M);
       double* em_out = ctx->em_out.ensure(2 + 2 * M);
       double* h_terms = ctx->h_terms.ensure(3 * M);
@@ -380,7 +383,6 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       const bool use_graph = ctx->use_graphs && !(o.flags & DPMRF_RUN_NO_GRAPH);
       ctx->stats.graphs = use_graph;
       if (use_graph) {
-        mstep_reserve(ctx->ms, R, M, Hs);
         dpmrf_context::GraphKey key{};
         key.R = R;
         key.Hs = Hs;
@@ -409,7 +411,7 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
         key.p[13] = ctx->ms.partials.get();
         key.p[14] = a.terms;
         key.p[15] = h_terms;
-        key.p[16] = ctx->ms.tile_counts.get();
+        key.p[16] = ctx->ms.counts.get();
         key.p[17] = ctx->ms.tile_base.get();
         key.p[18] = ctx->ms.layout.get();
         key.p[19] = nullptr;

@@ -37,7 +37,7 @@ __device__ __forceinline__ bool map_iter_skipped(const uint32_t* unconv, int t, 
 //   update_labels        engine.cpp:171-191 (uncovered vertices keep labels)
 // ---------------------------------------------------------------------------
 template <int MT>
-__device__ __forceinline__ void vertex_body(uint32_t v, const uint32_t* __restrict__ g_off,
+__device__ __forceinline__ uint32_t vertex_body(uint32_t v, const uint32_t* __restrict__ g_off,
                                             const uint32_t* __restrict__ g_nbr,
                                             const double* __restrict__ mean,
                                             const uint8_t* __restrict__ cover,
@@ -48,7 +48,7 @@ __device__ __forceinline__ void vertex_body(uint32_t v, const uint32_t* __restri
   const uint8_t old = lab_in[v];
   if (!cover[v]) {
     lab_out[v] = old;
-    return;
+    return old;
   }
   const uint32_t M = MT > 0 ? uint32_t(MT) : M_rt;
   const uint32_t lo = g_off[v], hi = g_off[v + 1];
@@ -109,6 +109,30 @@ __device__ __forceinline__ void vertex_body(uint32_t v, const uint32_t* __restri
   }
   minE[v] = best;
   lab_out[v] = static_cast<uint8_t>(best_l);
+  return best_l;
+}
+
+// Label histogram of this block's 256 new labels -> out[0..M) (the M-step's
+// per-tile counts; M == 2 needs just two block-wide counts).  Every thread
+// of the block must call it.
+__device__ __forceinline__ void block_label_counts(uint32_t* __restrict__ out, uint32_t M,
+                                                   bool valid, uint32_t label) {
+  if (M == 2) {
+    const int ones = __syncthreads_count(valid && label == 1u);
+    const int all = __syncthreads_count(valid);
+    if (threadIdx.x == 0) {
+      out[0] = uint32_t(all - ones);
+      out[1] = uint32_t(ones);
+    }
+    return;
+  }
+  __shared__ uint32_t hist[kMaxLabels + 1];
+  for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  if (valid) atomicAdd(&hist[label], 1u);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) out[i] = hist[i];
+  __syncthreads();
 }
 
 template <int MT>
@@ -118,11 +142,16 @@ __global__ void __launch_bounds__(kVtxThreads)
                     const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                     double* __restrict__ minE, uint32_t R, uint32_t M_rt,
                     const double* __restrict__ terms, double beta,
-                    const uint32_t* __restrict__ unconv, int t, int fixed) {
+                    const uint32_t* __restrict__ unconv, int t, int fixed,
+                    uint32_t* __restrict__ tile_counts, uint32_t tiles) {
   if (map_iter_skipped(unconv, t, fixed)) return;
   const uint32_t v = blockIdx.x * kVtxThreads + threadIdx.x;
-  if (v >= R) return;
-  vertex_body<MT>(v, g_off, g_nbr, mean, cover, lab_in, lab_out, minE, M_rt, terms, beta);
+  const bool valid = v < R;
+  uint32_t lab = 0;
+  if (valid) lab = vertex_body<MT>(v, g_off, g_nbr, mean, cover, lab_in, lab_out, minE, M_rt, terms, beta);
+  const uint32_t M = MT > 0 ? uint32_t(MT) : M_rt;
+  if (tile_counts && blockIdx.x < tiles)
+    block_label_counts(tile_counts + (uint64_t(t & 1) * tiles + blockIdx.x) * M, M, valid, lab);
 }
 
 // ---------------------------------------------------------------------------
@@ -200,16 +229,22 @@ template <int MT>
 __device__ __forceinline__ void vertex_tile(uint64_t tile, const MapArgs& a,
                                             const uint8_t* __restrict__ lab_in,
                                             uint8_t* __restrict__ lab_out,
-                                            double* __restrict__ minE, uint8_t* sm_lab) {
+                                            double* __restrict__ minE, uint8_t* sm_lab, int t) {
   const uint32_t v0 = static_cast<uint32_t>(tile * kVtxThreads);
   const uint32_t vend = min(a.R, v0 + kVtxThreads);
   const uint32_t v = v0 + threadIdx.x;
+  const uint32_t Mc = MT > 0 ? uint32_t(MT) : a.M;
+  uint32_t* counts = a.tile_counts + (uint64_t(t & 1) * a.tiles + tile) * Mc;
   const uint32_t base = a.g_off[v0], cnt = a.g_off[vend] - base;
   if (cnt > kVtxStageCap) {
-    if (v < vend) vertex_body<MT>(v, a.g_off, a.g_nbr, a.mean, a.cover, lab_in, lab_out, minE, a.M,
-                                  a.terms, a.beta);
+    uint32_t nl = 0;
+    if (v < vend)
+      nl = vertex_body<MT>(v, a.g_off, a.g_nbr, a.mean, a.cover, lab_in, lab_out, minE, a.M,
+                           a.terms, a.beta);
+    block_label_counts(counts, Mc, v < vend, nl);
     return;
   }
+  uint32_t newlab = 0;
   for (uint32_t c0 = 0; c0 < cnt; c0 += kBatch * kVtxThreads) {
     uint32_t id[kBatch];
     uint8_t lb[kBatch];
@@ -234,6 +269,7 @@ __device__ __forceinline__ void vertex_tile(uint64_t tile, const MapArgs& a,
     const uint8_t old = lab_in[v];
     if (!a.cover[v]) {
       lab_out[v] = old;
+      newlab = old;
     } else {
       const uint32_t M = MT > 0 ? uint32_t(MT) : a.M;
       const uint32_t lo = a.g_off[v] - base, hi = a.g_off[v + 1] - base;
@@ -268,8 +304,10 @@ __device__ __forceinline__ void vertex_tile(uint64_t tile, const MapArgs& a,
       }
       minE[v] = best;
       lab_out[v] = static_cast<uint8_t>(best_l);
+      newlab = best_l;
     }
   }
+  block_label_counts(counts, Mc, v < vend, newlab);
   __syncthreads();  // the stage is reused by the next tile of a persistent block
 }
 
@@ -346,7 +384,7 @@ __global__ void __launch_bounds__(kVtxThreads)
                     int t) {
   __shared__ uint8_t sm_lab[kVtxStageCap];
   if (map_iter_skipped(a.unconv, t, a.fixed)) return;
-  vertex_tile<MT>(blockIdx.x, a, lab_in, lab_out, a.minE, sm_lab);
+  vertex_tile<MT>(blockIdx.x, a, lab_in, lab_out, a.minE, sm_lab, t);
 }
 
 __global__ void __launch_bounds__(kHoodThreads) k_hood_staged(MapArgs a, int t) {
@@ -408,7 +446,7 @@ __global__ void __launch_bounds__(kVtxThreads)
         const int bu = __syncthreads_count(nc);
         if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[p - 1], uint32_t(bu));
       } else {
-        vertex_tile<MT>(it - (run_h ? ht : 0), a, lin, lout, mv, sm_lab);
+        vertex_tile<MT>(it - (run_h ? ht : 0), a, lin, lout, mv, sm_lab, p);
       }
     }
     grid.sync();
@@ -420,10 +458,13 @@ __global__ void __launch_bounds__(kVtxThreads)
 //   update_parameters  engine.cpp:193-223 (sort_by_key stable, reduce_by_key
 //                      fold_range per run, kernels.hpp:226-253)
 //   dpp::reduce        kernels.hpp:124-139 (total energy, optimize.cpp:64-65)
+// Launches per EM iteration: k_tile_offsets, k_label_tiles (stable scatter),
+// k_leaf_fold<sum> and k_leaf_fold<sq>, each leaf kernel finishing with the
+// pairwise tree in its last block.  The per-tile label counts come from the
+// last executed vertex pass (double-buffered by iteration parity).
 // ---------------------------------------------------------------------------
 constexpr int kTileThreads = 256;
-constexpr int kTileRounds = 4;
-constexpr int kTileVerts = kTileThreads * kTileRounds;  // 4096 vertices per tile
+constexpr int kTileVerts = kTileThreads;  // == kVtxThreads: vertex blocks are label tiles
 
 __device__ __forceinline__ int executed_iters(const uint32_t* unconv, int map_max, int fixed) {
   if (fixed) return map_max;
@@ -439,58 +480,66 @@ __device__ __forceinline__ const uint8_t* final_labels(const uint8_t* even, cons
   return (executed_iters(unconv, map_max, fixed) & 1) ? odd : even;
 }
 
-// Per tile and label: count (pass 0) or stable scatter (pass 1).
+// Counts of the final labels per 256-vertex tile: the buffer written by the
+// last executed vertex pass (iteration T-1 -> slot (T-1)&1), or slot 0 when
+// the counts were produced by k_label_tiles<0> (standalone update_parameters).
+__device__ __forceinline__ const uint32_t* final_counts(const uint32_t* counts, uint32_t tiles,
+                                                        uint32_t M, const uint32_t* unconv,
+                                                        int map_max, int fixed) {
+  if (!unconv) return counts;
+  const int T = executed_iters(unconv, map_max, fixed);
+  return counts + uint64_t((T - 1) & 1) * tiles * M;
+}
+
+// Stable rank of each vertex among the tile's vertices of the same label:
+// __match_any_sync gives the in-warp rank, per-warp counts in shared memory
+// the cross-warp offset.  kPass 0 counts, kPass 1 scatters the region mean to
+// its position in the label-grouped array x (== stable sort_by_key(labels)).
 template <int kPass>
 __global__ void __launch_bounds__(kTileThreads)
     k_label_tiles(const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
                   int map_max, int fixed, uint32_t R, uint32_t M, const double* __restrict__ mean,
                   uint32_t* __restrict__ tile_counts, const uint32_t* __restrict__ tile_base,
                   const uint32_t* __restrict__ layout, double* __restrict__ x) {
-  extern __shared__ uint32_t sm[];
-  uint32_t* run = sm;                  // M running per-label counts of this tile
-  uint32_t* wcnt = sm + M;             // [warp][M] counts of the current round
+  extern __shared__ uint32_t wcnt[];  // [warp][M]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = kTileThreads / 32;
   const uint8_t* lab = final_labels(lab_even, lab_odd, unconv, map_max, fixed);
-  for (uint32_t l = threadIdx.x; l < M; l += kTileThreads) run[l] = 0;
+  for (uint32_t i = threadIdx.x; i < kWarps * M; i += kTileThreads) wcnt[i] = 0;
+  __syncthreads();
   const uint64_t tile = blockIdx.x;
-  const uint32_t* label_start = layout + M;
-  for (int r = 0; r < kTileRounds; ++r) {
-    for (uint32_t i = threadIdx.x; i < kWarps * M; i += kTileThreads) wcnt[i] = 0;
-    __syncthreads();
-    const uint64_t v = tile * kTileVerts + uint64_t(r) * kTileThreads + threadIdx.x;
-    const bool valid = v < R;
-    const uint32_t l = valid ? lab[v] : 0xFFFFFFFFu;
-    const unsigned peers = __match_any_sync(0xffffffffu, l);
-    const unsigned lt = (1u << lane) - 1u;
-    const uint32_t rank_in_warp = __popc(peers & lt);
-    if (valid && rank_in_warp == 0) wcnt[warp * M + l] = __popc(peers);
-    __syncthreads();
-    if (kPass == 1 && valid) {
-      uint32_t before = run[l];
+  const uint64_t v = tile * kTileVerts + threadIdx.x;
+  const bool valid = v < R;
+  const uint32_t l = valid ? lab[v] : 0xFFFFFFFFu;
+  const unsigned peers = __match_any_sync(0xffffffffu, l);
+  const uint32_t rank_in_warp = __popc(peers & ((1u << lane) - 1u));
+  if (valid && rank_in_warp == 0) wcnt[warp * M + l] = __popc(peers);
+  __syncthreads();
+  if (kPass == 1) {
+    if (valid) {
+      uint32_t before = 0;
       for (int w = 0; w < warp; ++w) before += wcnt[w * M + l];
-      const uint32_t pos = label_start[l] + tile_base[tile * M + l] + before + rank_in_warp;
-      x[pos] = mean[v];
+      const uint32_t* label_start = layout + M;
+      x[label_start[l] + tile_base[tile * M + l] + before + rank_in_warp] = mean[v];
     }
-    __syncthreads();
+  } else {
     for (uint32_t q = threadIdx.x; q < M; q += kTileThreads) {
-      uint32_t add = 0;
-      for (int w = 0; w < kWarps; ++w) add += wcnt[w * M + q];
-      run[q] += add;
+      uint32_t c = 0;
+      for (int w = 0; w < kWarps; ++w) c += wcnt[w * M + q];
+      tile_counts[tile * M + q] = c;
     }
-    __syncthreads();
   }
-  if (kPass == 0)
-    for (uint32_t q = threadIdx.x; q < M; q += kTileThreads) tile_counts[tile * M + q] = run[q];
 }
 
 // Single block: per-label exclusive scan over tiles; label starts; leaf layout.
 // layout = n[M] | label_start[M+1] | leaf_start[M+2] (series M = hood energies)
 __global__ void __launch_bounds__(1024)
-    k_tile_offsets(const uint32_t* __restrict__ tile_counts, uint32_t* __restrict__ tile_base,
-                   uint32_t tiles, uint32_t M, uint64_t Hs, uint32_t* __restrict__ layout) {
+    k_tile_offsets(const uint32_t* __restrict__ counts_buf, const uint32_t* __restrict__ unconv,
+                   int map_max, int fixed, uint32_t* __restrict__ tile_base, uint32_t tiles,
+                   uint32_t M, uint64_t Hs, uint32_t* __restrict__ layout) {
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry;
+  const uint32_t* tile_counts = final_counts(counts_buf, tiles, M, unconv, map_max, fixed);
   for (uint32_t l = 0; l < M; ++l) {
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
@@ -534,12 +583,17 @@ __device__ __forceinline__ uint32_t series_of(const uint32_t* leaf_start, uint32
 // Leaf folds (fold_leaf, kernels.hpp:37-42): each 1024-element leaf is a
 // strictly sequential left fold seeded by its first element -- the chain of
 // dependent adds cannot be reassociated without changing bits.  A block of
-// 256 threads therefore stages kLeavesPerBlock leaves into shared memory
-// with coalesced loads (the expensive part), then one lane per leaf runs the
-// dependent chain out of shared memory (rows padded to 1025 doubles so the
-// lanes hit distinct banks).  kSq folds (x - mu)^2 (engine.cpp:213-217).
-// Series M is the hood-energy row of the last executed MAP iteration (the
-// EM total energy, optimize.cpp:64-65), located from the device counters.
+// 256 threads stages kLeavesPerBlock leaves into shared memory with all its
+// loads in flight at once, then one lane per leaf runs the dependent chain
+// out of shared memory (rows padded to 1025 doubles: distinct banks).
+// kSq folds (x - mu)^2 (engine.cpp:213-217).  Series M (sum pass only) is
+// the hood-energy row of the last executed MAP iteration (the EM total
+// energy, optimize.cpp:64-65), located from the device counters.
+// The LAST block to finish (atomic ticket after a fence) combines every
+// series' leaf partials with the pairwise tree of kernels.hpp:45-51 --
+// bottom-up adjacent pairing == the split at bit_floor(n-1) -- and writes
+// mu (sum pass) / sigma and the published parameters (sq pass) and the
+// total energy.
 constexpr int kLeavesPerBlock = 8;
 constexpr int kLeafStride = kFoldLeaf + 1;
 
@@ -547,8 +601,8 @@ template <bool kSq>
 __global__ void __launch_bounds__(256)
     k_leaf_fold(const double* __restrict__ x, const uint32_t* __restrict__ layout, uint32_t M,
                 const double* __restrict__ hist, uint64_t Hs, int ring,
-                const uint32_t* __restrict__ unconv, int map_max, int fixed,
-                const double* __restrict__ params, double* __restrict__ partials) {
+                const uint32_t* __restrict__ unconv, int map_max, int fixed, double* params,
+                double* partials, double* em_out, uint32_t* done) {
   extern __shared__ double stage[];  // kLeavesPerBlock x kLeafStride
   const uint32_t* n = layout;
   const uint32_t* label_start = layout + M;
@@ -556,121 +610,122 @@ __global__ void __launch_bounds__(256)
   const uint32_t nseries = kSq ? M : M + 1;
   const uint32_t total = leaf_start[nseries];
   const uint32_t first = blockIdx.x * kLeavesPerBlock;
-  if (first >= total) return;
-  const double* hood_row = nullptr;
-  if (!kSq && unconv) {
-    const int T = executed_iters(unconv, map_max, fixed);
-    hood_row = hist + uint64_t((T - 1) % ring) * Hs;
-  }
-  __shared__ const double* src_s[kLeavesPerBlock];
-  __shared__ uint32_t len_s[kLeavesPerBlock];
-  __shared__ double mu_s[kLeavesPerBlock];
-  if (threadIdx.x < kLeavesPerBlock) {
-    const uint32_t leaf = first + threadIdx.x;
-    uint32_t len = 0;
-    const double* src = nullptr;
-    double mu = 0.0;
-    if (leaf < total) {
-      const uint32_t sr = series_of(leaf_start, nseries, leaf);
-      const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
-      const uint64_t slen = sr < M ? n[sr] : Hs;
-      src = (sr < M ? x + label_start[sr] : hood_row) + b;
-      const uint64_t rem = slen - b;
-      len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
-      if (kSq) mu = params[sr];
+  if (first < total) {
+    const double* hood_row = nullptr;
+    if (!kSq && unconv) {
+      const int T = executed_iters(unconv, map_max, fixed);
+      hood_row = hist + uint64_t((T - 1) % ring) * Hs;
     }
-    src_s[threadIdx.x] = src;
-    len_s[threadIdx.x] = len;
-    mu_s[threadIdx.x] = mu;
-  }
-  __syncthreads();
-  // all kLeavesPerBlock*1024/256 = 32 loads of a thread are issued before any
-  // store so they are in flight together (one memory round trip, not 32)
-  constexpr int kPer = kLeavesPerBlock * int(kFoldLeaf) / 256;
-  double r[kPer];
+    __shared__ const double* src_s[kLeavesPerBlock];
+    __shared__ uint32_t len_s[kLeavesPerBlock];
+    __shared__ double mu_s[kLeavesPerBlock];
+    if (threadIdx.x < kLeavesPerBlock) {
+      const uint32_t leaf = first + threadIdx.x;
+      uint32_t len = 0;
+      const double* src = nullptr;
+      double mu = 0.0;
+      if (leaf < total) {
+        const uint32_t sr = series_of(leaf_start, nseries, leaf);
+        const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
+        const uint64_t slen = sr < M ? n[sr] : Hs;
+        src = (sr < M ? x + label_start[sr] : hood_row) + b;
+        const uint64_t rem = slen - b;
+        len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
+        if (kSq) mu = params[sr];
+      }
+      src_s[threadIdx.x] = src;
+      len_s[threadIdx.x] = len;
+      mu_s[threadIdx.x] = mu;
+    }
+    __syncthreads();
+    // all 32 loads of a thread are issued before any store (one round trip)
+    constexpr int kPer = kLeavesPerBlock * int(kFoldLeaf) / 256;
+    double r[kPer];
 #pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
-    const uint32_t j = flat / kFoldLeaf, i = flat % kFoldLeaf;
-    r[q] = i < len_s[j] ? __ldg(src_s[j] + i) : 0.0;
-  }
+    for (int q = 0; q < kPer; ++q) {
+      const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
+      const uint32_t j = flat / kFoldLeaf, i = flat % kFoldLeaf;
+      r[q] = i < len_s[j] ? __ldcg(src_s[j] + i) : 0.0;
+    }
 #pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
-    stage[(flat / kFoldLeaf) * kLeafStride + flat % kFoldLeaf] = r[q];
-  }
-  __syncthreads();
-  if (threadIdx.x >= kLeavesPerBlock) return;
-  const uint32_t len = len_s[threadIdx.x];
-  if (len == 0) return;
-  const double* v = stage + threadIdx.x * kLeafStride;
-  double acc;
-  if (kSq) {
-    const double mu = mu_s[threadIdx.x];
-    double d = __dsub_rn(v[0], mu);
-    acc = __dmul_rn(d, d);
+    for (int q = 0; q < kPer; ++q) {
+      const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
+      stage[(flat / kFoldLeaf) * kLeafStride + flat % kFoldLeaf] = r[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < kLeavesPerBlock && len_s[threadIdx.x] != 0) {
+      const uint32_t len = len_s[threadIdx.x];
+      const double* v = stage + threadIdx.x * kLeafStride;
+      double acc;
+      if (kSq) {
+        const double mu = mu_s[threadIdx.x];
+        double d = __dsub_rn(v[0], mu);
+        acc = __dmul_rn(d, d);
 #pragma unroll 8
-    for (uint32_t i = 1; i < len; ++i) {
-      d = __dsub_rn(v[i], mu);
-      acc = __dadd_rn(acc, __dmul_rn(d, d));
-    }
-  } else {
-    acc = v[0];
-#pragma unroll 8
-    for (uint32_t i = 1; i < len; ++i) acc = __dadd_rn(acc, v[i]);
-  }
-  partials[first + threadIdx.x] = acc;
-}
-
-// One block per series: pairwise tree over its leaf partials, bottom-up
-// adjacent pairing (== fold_tree's split at bit_floor(n-1), kernels.hpp:45-51),
-// then the parameter / total-energy epilogue.
-template <bool kSq>
-__global__ void __launch_bounds__(1024)
-    k_tree_finalize(double* partials, const uint32_t* __restrict__ layout, uint32_t M,
-                    double* params, double* em_out, const uint32_t* unconv, int map_max,
-                    int fixed) {
-  const uint32_t s = blockIdx.x;
-  const uint32_t* n = layout;
-  const uint32_t* leaf_start = layout + 2 * M + 1;
-  uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
-  double* p = partials + leaf_start[s];
-  while (cnt > 1) {
-    const uint32_t pairs = cnt / 2;
-    for (uint32_t base = 0; base < pairs; base += blockDim.x) {
-      const uint32_t i = base + threadIdx.x;
-      double v = 0.0;
-      if (i < pairs) v = __dadd_rn(p[2 * i], p[2 * i + 1]);
-      __syncthreads();
-      if (i < pairs) p[i] = v;
-      __syncthreads();
-    }
-    if (cnt & 1u) {
-      if (threadIdx.x == 0) p[pairs] = p[cnt - 1];
-      __syncthreads();
-    }
-    cnt = pairs + (cnt & 1u);
-  }
-  if (threadIdx.x != 0) return;
-  if (s < M) {
-    if (n[s] != 0) {  // empty labels keep their previous parameters
-      const double count = static_cast<double>(n[s]);
-      if (!kSq) {
-        params[s] = __ddiv_rn(p[0], count);
+        for (uint32_t i = 1; i < len; ++i) {
+          d = __dsub_rn(v[i], mu);
+          acc = __dadd_rn(acc, __dmul_rn(d, d));
+        }
       } else {
-        const double sd = __dsqrt_rn(__ddiv_rn(p[0], count));
-        params[M + s] = sd < kSigmaFloor ? kSigmaFloor : sd;
+        acc = v[0];
+#pragma unroll 8
+        for (uint32_t i = 1; i < len; ++i) acc = __dadd_rn(acc, v[i]);
+      }
+      partials[first + threadIdx.x] = acc;
+    }
+  }
+  // ---- last block: trees + epilogue ----
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (uint32_t s = 0; s < nseries; ++s) {
+    uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
+    double* p = partials + leaf_start[s];
+    while (cnt > 1) {
+      const uint32_t pairs = cnt / 2;
+      for (uint32_t base = 0; base < pairs; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        double v = 0.0;
+        if (i < pairs) v = __dadd_rn(__ldcg(p + 2 * i), __ldcg(p + 2 * i + 1));
+        __syncthreads();
+        if (i < pairs) p[i] = v;
+        __syncthreads();
+      }
+      if (cnt & 1u) {
+        if (threadIdx.x == 0) p[pairs] = __ldcg(p + cnt - 1);
+        __syncthreads();
+      }
+      cnt = pairs + (cnt & 1u);
+    }
+    if (threadIdx.x == 0) {
+      const double folded = __ldcg(p);
+      if (s < M) {
+        if (n[s] != 0) {  // empty labels keep their previous parameters
+          const double count = static_cast<double>(n[s]);
+          if (!kSq) {
+            params[s] = __ddiv_rn(folded, count);
+          } else {
+            const double sd = __dsqrt_rn(__ddiv_rn(folded, count));
+            params[M + s] = sd < kSigmaFloor ? kSigmaFloor : sd;
+          }
+        }
+        if (kSq) {  // the final pass publishes (mu, sigma) of every label
+          em_out[2 + s] = params[s];
+          em_out[2 + M + s] = params[M + s];
+        }
+      } else {
+        // total energy: dpp::reduce(..., 0.0) -> identity only for empty input
+        em_out[0] = (leaf_start[M + 1] == leaf_start[M]) ? 0.0 : folded;
+        em_out[1] = static_cast<double>(unconv ? executed_iters(unconv, map_max, fixed) : 0);
       }
     }
-    if (kSq) {  // the final pass publishes (mu, sigma) of every label
-      em_out[2 + s] = params[s];
-      em_out[2 + M + s] = params[M + s];
-    }
-  } else {
-    // total energy: dpp::reduce(..., 0.0) -> identity only for empty input
-    em_out[0] = (leaf_start[M + 1] == leaf_start[M]) ? 0.0 : p[0];
-    em_out[1] = static_cast<double>(unconv ? executed_iters(unconv, map_max, fixed) : 0);
+    __syncthreads();
   }
+  if (threadIdx.x == 0) *done = 0;  // re-arm the ticket for the next launch
 }
 
 
@@ -761,7 +816,7 @@ void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_
   }
 #define VA_ARGS                                                                              \
   a.g_off, a.g_nbr, a.mean, a.cover, lab_in, lab_out, a.minE, a.R, a.M, a.terms, a.beta, \
-      a.unconv, t, a.fixed
+      a.unconv, t, a.fixed, a.tile_counts, a.tiles
   switch (a.M) {
     case 2: k_vertex_argmin<2><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
     case 3: k_vertex_argmin<3><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
@@ -822,26 +877,27 @@ namespace {
 void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
                 const uint8_t* lab_odd, const uint32_t* unconv, int map_max, int fixed,
                 const double* hist, uint64_t Hs, int ring, double* params, double* em_out,
-                MStepBuffers& mb, cudaStream_t s, uint64_t* launches) {
+                MStepBuffers& mb, cudaStream_t s, uint64_t* launches, bool counts_ready) {
+  mstep_reserve(mb, R, M, Hs);
   const uint32_t tiles = static_cast<uint32_t>((uint64_t(R) + kTileVerts - 1) / kTileVerts);
-  const uint32_t tiles_g = tiles ? tiles : 1;
-  uint32_t* tile_counts = mb.tile_counts.ensure(uint64_t(tiles_g) * M);
-  uint32_t* tile_base = mb.tile_base.ensure(uint64_t(tiles_g) * M);
-  uint32_t* layout = mb.layout.ensure(4 * M + 4);
-  double* x = mb.x.ensure(R);
+  uint32_t* counts = mb.counts.get();
+  uint32_t* tile_base = mb.tile_base.get();
+  uint32_t* layout = mb.layout.get();
+  double* x = mb.x.get();
   const uint64_t max_leaves = (uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M +
                               (Hs + kFoldLeaf - 1) / kFoldLeaf + 1;
-  double* partials = mb.partials.ensure(max_leaves);
-  const size_t smem = (M + (kTileThreads / 32) * M) * sizeof(uint32_t);
+  double* partials = mb.partials.get();
+  const size_t smem = (kTileThreads / 32) * M * sizeof(uint32_t);
   uint64_t n = 0;
-  if (tiles) {
+  if (tiles && !counts_ready) {
     k_label_tiles<0><<<tiles, kTileThreads, smem, s>>>(lab_even, lab_odd, unconv, map_max, fixed,
-                                                       R, M, mean, tile_counts, nullptr, nullptr,
+                                                       R, M, mean, counts, nullptr, nullptr,
                                                        nullptr);
     CK_LAUNCH();
     ++n;
   }
-  k_tile_offsets<<<1, 1024, 0, s>>>(tile_counts, tile_base, tiles, M, Hs, layout);
+  k_tile_offsets<<<1, 1024, 0, s>>>(counts, counts_ready ? unconv : nullptr, map_max, fixed,
+                                    tile_base, tiles, M, Hs, layout);
   CK_LAUNCH();
   ++n;
   if (tiles) {
@@ -861,39 +917,43 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
   }
   const unsigned lg = grid_for(max_leaves, kLeavesPerBlock);
   k_leaf_fold<false><<<lg, 256, leaf_smem, s>>>(x, layout, M, hist, Hs, ring, unconv, map_max,
-                                                fixed, params, partials);
+                                                fixed, params, partials, em_out, mb.done.get());
   CK_LAUNCH();
-  k_tree_finalize<false><<<M + 1, 1024, 0, s>>>(partials, layout, M, params, em_out, unconv,
-                                                map_max, fixed);
+  k_leaf_fold<true><<<lg, 256, leaf_smem, s>>>(x, layout, M, nullptr, 0, 1, unconv, map_max,
+                                               fixed, params, partials, em_out,
+                                               mb.done.get() + 1);
   CK_LAUNCH();
-  k_leaf_fold<true><<<lg, 256, leaf_smem, s>>>(x, layout, M, nullptr, 0, 1, nullptr, map_max,
-                                               fixed, params, partials);
-  CK_LAUNCH();
-  k_tree_finalize<true><<<M, 1024, 0, s>>>(partials, layout, M, params, em_out, unconv, map_max,
-                                           fixed);
-  CK_LAUNCH();
-  n += 4;
+  n += 2;
   if (launches) *launches += n;
 }
 
 }  // namespace
+
+uint32_t label_tiles(uint32_t R) {
+  return static_cast<uint32_t>((uint64_t(R) + kTileVerts - 1) / kTileVerts);
+}
 
 void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
                   const uint8_t* lab_odd, const double* hist, uint64_t Hs, int ring,
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches) {
   mstep_core(mean, R, M, lab_even, lab_odd, unconv, map_max, fixed, hist, Hs, ring, params,
-             em_out, mb, s, launches);
+             em_out, mb, s, launches, /*counts_ready=*/true);
 }
 
 void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs) {
-  const uint32_t tiles = static_cast<uint32_t>((uint64_t(R) + kTileVerts - 1) / kTileVerts);
+  const uint32_t tiles = label_tiles(R);
   const uint32_t tiles_g = tiles ? tiles : 1;
-  mb.tile_counts.ensure(uint64_t(tiles_g) * M);
+  mb.counts.ensure(2 * uint64_t(tiles_g) * M);
   mb.tile_base.ensure(uint64_t(tiles_g) * M);
   mb.layout.ensure(4 * M + 4);
   mb.x.ensure(R);
   mb.partials.ensure((uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M + (Hs + kFoldLeaf - 1) / kFoldLeaf + 1);
+  if (!mb.done.get()) {
+    CK(cudaMalloc(reinterpret_cast<void**>(&mb.done.p), 2 * sizeof(uint32_t)));
+    mb.done.cap = 2;
+    CK(cudaMemset(mb.done.p, 0, 2 * sizeof(uint32_t)));  // tickets re-arm themselves after
+  }
 }
 
 void launch_update_parameters_u32(const double* mean, uint32_t R, uint32_t M,
@@ -912,7 +972,8 @@ void launch_update_parameters_u32(const double* mean, uint32_t R, uint32_t M,
   if (h_err) fail(DPMRF_INVALID_ARGUMENT, "update_parameters: label out of range");
   if (R == 0) return;
   double* eo = mb.em_scratch.ensure(2 + 2 * M);
-  mstep_core(mean, R, M, lab, lab, nullptr, 1, 1, nullptr, 0, 1, params, eo, mb, s, nullptr);
+  mstep_core(mean, R, M, lab, lab, nullptr, 1, 1, nullptr, 0, 1, params, eo, mb, s, nullptr,
+             /*counts_ready=*/false);
 }
 
 void launch_init_labels(uint8_t* lab, uint32_t R, uint32_t M, uint64_t seed, cudaStream_t s) {

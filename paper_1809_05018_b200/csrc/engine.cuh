@@ -31,7 +31,12 @@ struct MapArgs {
   double* hist;    // ring x Hs hood energies
   uint8_t* flags;  // map_max x Hs convergence flags (nullptr = not recorded)
   uint32_t* unconv;  // per MAP iteration count of unconverged hoods
+  uint32_t* tile_counts;  // 2 x tiles x M: label counts per 256-vertex tile, by iteration parity
+  uint32_t tiles;
 };
+
+// Number of 256-vertex label tiles (== vertex-kernel blocks).
+uint32_t label_tiles(uint32_t R);
 
 // One MAP iteration = energies against the frozen labels + per-vertex argmin
 // + label commit (engine.cpp:88-191 fused), then the hood
@@ -44,12 +49,12 @@ void launch_map_loop(const MapArgs& a, uint8_t* lab_even, uint8_t* lab_odd, doub
                      double* minE1, int map_max, cudaStream_t s);
 
 struct MStepBuffers {
-  DevBuf<uint32_t> tile_counts;  // tiles x M
+  DevBuf<uint32_t> counts;       // 2 x tiles x M label counts (slot = MAP iteration parity)
   DevBuf<uint32_t> tile_base;    // tiles x M
   DevBuf<uint32_t> layout;       // n[M] | label_start[M+1] | leaf_start[M+2]
   DevBuf<double> x;              // R values grouped by label (stable)
   DevBuf<double> partials;       // leaf partials of all series
-  DevBuf<double> row;            // hood-energy row of the last executed MAP iteration
+  DevBuf<uint32_t> done;         // last-block tickets of the two leaf-fold kernels
   DevBuf<uint32_t> err;
   DevBuf<double> em_scratch;
 };
