@@ -135,6 +135,8 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     if (const char* e = std::getenv("DPMRF_NO_GRAPH")) c->use_graphs = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_MAP_KERNELS")) c->use_persistent = e[0] == '1';
     if (const char* e = std::getenv("DPMRF_DIRECT")) c->use_staged = e[0] == '0';
+    if (const char* e = std::getenv("DPMRF_NO_L2_PERSIST")) c->use_l2_persist = e[0] == '0';
+    if (const char* e = std::getenv("DPMRF_NO_PDL")) pdl_enabled() = e[0] == '0';
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -309,6 +311,7 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       a.staged = (ctx->use_staged || (o.flags & DPMRF_RUN_STAGED)) ? 1 : 0;
       a.terms = ctx->terms.ensure(3 * M);
       double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
+      ctx->pin_in_l2(minE2, uint64_t(R) * sizeof(double));
       a.minE = minE2;
       a.hist = ctx->hist.ensure(uint64_t(a.ring) * Hs);
       a.flags = full ? ctx->flags.ensure(uint64_t(map_max) * Hs) : nullptr;

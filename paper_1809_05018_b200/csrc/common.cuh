@@ -97,6 +97,33 @@ struct HostBuf {
   }
 };
 
+// Programmatic Dependent Launch: a kernel launched this way may be scheduled
+// while its stream predecessor is still draining; it must execute pdl_wait()
+// before touching anything the predecessor writes (griddepcontrol.wait
+// returns once the predecessor has completed and its writes are visible).
+inline bool& pdl_enabled() {
+  static bool on = true;
+  return on;
+}
+
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 inline unsigned grid_for(uint64_t n, unsigned block) {
   uint64_t g = (n + block - 1) / block;
   if (g == 0) g = 1;

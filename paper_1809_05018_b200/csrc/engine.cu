@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(kVtxThreads)
                     const double* __restrict__ terms, double beta,
                     const uint32_t* __restrict__ unconv, int t, int fixed,
                     uint32_t* __restrict__ tile_counts, uint32_t tiles) {
+  pdl_wait();
   if (map_iter_skipped(unconv, t, fixed)) return;
   const uint32_t v = blockIdx.x * kVtxThreads + threadIdx.x;
   const bool valid = v < R;
@@ -181,9 +182,32 @@ __device__ __forceinline__ int hood_body(uint64_t h, const uint32_t* __restrict_
                                          double* __restrict__ hist, uint8_t* __restrict__ flags,
                                          uint64_t Hs, int t, int L, int ring, double tol) {
   if (h >= Hs) return 0;
+  const int R1 = ring;  // >= L+1 rows; == map_max rows when the full trace is kept
+  // the window rows do not depend on this iteration's sum: issue them first
+  constexpr int kWin = 8;
+  double prev[kWin];
+  const bool window = t >= L;
+  if (window) {
+#pragma unroll
+    for (int i = 0; i < kWin; ++i)
+      if (i < L) prev[i] = hist[uint64_t((t - 1 - i) % R1) * Hs + h];
+  }
   const uint32_t lo = s_off[h], hi = s_off[h + 1];
   double sum;
-  if (hi - lo <= kFoldLeaf) {
+  if (hi - lo <= 16) {
+    // every member id, then every minimum, in flight together (<= 16 slots:
+    // all grid and brick hoods); then the left fold in slot order
+    uint32_t id[16];
+    double e[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) id[k] = lo + k < hi ? h_mem[lo + k] : 0u;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) e[k] = lo + k < hi ? minE[id[k]] : 0.0;
+    sum = e[0];
+#pragma unroll
+    for (int k = 1; k < 16; ++k)
+      if (lo + k < hi) sum = __dadd_rn(sum, e[k]);
+  } else if (hi - lo <= kFoldLeaf) {
     sum = minE[h_mem[lo]];
     uint32_t s = lo + 1;
     for (; s + 4 <= hi; s += 4) {
@@ -195,17 +219,16 @@ __device__ __forceinline__ int hood_body(uint64_t h, const uint32_t* __restrict_
   } else {
     sum = hood_fold_long(h_mem, minE, lo, hi);
   }
-  const int R1 = ring;  // >= L+1 rows; == map_max rows when the full trace is kept
   hist[uint64_t(t % R1) * Hs + h] = sum;
   int ok = 0;
-  if (t >= L) {
+  if (window) {  // AND over the window (order-free: no side effects, NaN -> 0)
     ok = 1;
-    for (int i = 1; i <= L; ++i) {
-      const double prev = hist[uint64_t((t - i) % R1) * Hs + h];
-      if (!(fabs(__dsub_rn(sum, prev)) < tol)) {
-        ok = 0;
-        break;
-      }
+#pragma unroll
+    for (int i = 0; i < kWin; ++i)
+      if (i < L && !(fabs(__dsub_rn(sum, prev[i])) < tol)) ok = 0;
+    for (int i = kWin + 1; i <= L; ++i) {
+      const double p = hist[uint64_t((t - i) % R1) * Hs + h];
+      if (!(fabs(__dsub_rn(sum, p)) < tol)) ok = 0;
     }
   }
   if (flags) flags[uint64_t(t) * Hs + h] = static_cast<uint8_t>(ok);
@@ -383,12 +406,14 @@ __global__ void __launch_bounds__(kVtxThreads)
     k_vertex_staged(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                     int t) {
   __shared__ uint8_t sm_lab[kVtxStageCap];
+  pdl_wait();
   if (map_iter_skipped(a.unconv, t, a.fixed)) return;
   vertex_tile<MT>(blockIdx.x, a, lab_in, lab_out, a.minE, sm_lab, t);
 }
 
 __global__ void __launch_bounds__(kHoodThreads) k_hood_staged(MapArgs a, int t) {
   __shared__ double sm_e[kHoodStageCap];
+  pdl_wait();
   if (map_iter_skipped(a.unconv, t, a.fixed)) return;
   const int nc = hood_tile(blockIdx.x, a, a.minE, t, sm_e);
   const int bu = __syncthreads_count(nc);
@@ -400,6 +425,7 @@ __global__ void __launch_bounds__(kHoodThreads)
                 const double* __restrict__ minE, double* __restrict__ hist,
                 uint8_t* __restrict__ flags, uint64_t Hs, int t, int L, int ring, double tol,
                 uint32_t* __restrict__ unconv, int fixed) {
+  pdl_wait();
   if (map_iter_skipped(unconv, t, fixed)) return;
   const uint64_t h = uint64_t(blockIdx.x) * kHoodThreads + threadIdx.x;
   const int not_conv = hood_body(h, s_off, h_mem, minE, hist, flags, Hs, t, L, ring, tol);
@@ -502,6 +528,7 @@ __global__ void __launch_bounds__(kTileThreads)
                   uint32_t* __restrict__ tile_counts, const uint32_t* __restrict__ tile_base,
                   const uint32_t* __restrict__ layout, double* __restrict__ x) {
   extern __shared__ uint32_t wcnt[];  // [warp][M]
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = kTileThreads / 32;
   const uint8_t* lab = final_labels(lab_even, lab_odd, unconv, map_max, fixed);
@@ -539,6 +566,7 @@ __global__ void __launch_bounds__(1024)
                    uint32_t M, uint64_t Hs, uint32_t* __restrict__ layout) {
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry;
+  pdl_wait();
   const uint32_t* tile_counts = final_counts(counts_buf, tiles, M, unconv, map_max, fixed);
   for (uint32_t l = 0; l < M; ++l) {
     if (threadIdx.x == 0) carry = 0;
@@ -604,6 +632,7 @@ __global__ void __launch_bounds__(256)
                 const uint32_t* __restrict__ unconv, int map_max, int fixed, double* params,
                 double* partials, double* em_out, uint32_t* done) {
   extern __shared__ double stage[];  // kLeavesPerBlock x kLeafStride
+  pdl_wait();
   const uint32_t* n = layout;
   const uint32_t* label_start = layout + M;
   const uint32_t* leaf_start = layout + 2 * M + 1;
@@ -682,9 +711,33 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (!last) return;
   __threadfence();
+  constexpr uint32_t kStageDoubles = kLeavesPerBlock * kLeafStride;
   for (uint32_t s = 0; s < nseries; ++s) {
     uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
     double* p = partials + leaf_start[s];
+    if (cnt <= kStageDoubles) {
+      // the tree levels run in shared memory (one global round trip in total)
+      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) stage[i] = __ldcg(p + i);
+      __syncthreads();
+      while (cnt > 1) {
+        const uint32_t pairs = cnt / 2;
+        for (uint32_t base = 0; base < pairs; base += blockDim.x) {
+          const uint32_t i = base + threadIdx.x;
+          const double v = i < pairs ? __dadd_rn(stage[2 * i], stage[2 * i + 1]) : 0.0;
+          __syncthreads();
+          if (i < pairs) stage[i] = v;
+          __syncthreads();
+        }
+        if (cnt & 1u) {
+          if (threadIdx.x == 0) stage[pairs] = stage[cnt - 1];
+          __syncthreads();
+        }
+        cnt = pairs + (cnt & 1u);
+      }
+      if (threadIdx.x == 0) p[0] = stage[0];
+      __syncthreads();
+      cnt = 1;
+    }
     while (cnt > 1) {
       const uint32_t pairs = cnt / 2;
       for (uint32_t base = 0; base < pairs; base += blockDim.x) {
@@ -805,40 +858,37 @@ __global__ void k_compact_offsets(const uint32_t* __restrict__ h_off, uint64_t H
 // ---- launchers -----------------------------------------------------------------
 void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out, int t,
                           cudaStream_t s) {
-  const unsigned g = grid_for(a.R, kVtxThreads);
+  const dim3 g(grid_for(a.R, kVtxThreads)), blk(kVtxThreads);
   if (a.staged) {
-    switch (a.M) {  // M = 2 is specialised; other M share the counted-compare loop
-      case 2: k_vertex_staged<2><<<g, kVtxThreads, 0, s>>>(a, lab_in, lab_out, t); break;
-      default: k_vertex_staged<0><<<g, kVtxThreads, 0, s>>>(a, lab_in, lab_out, t); break;
-    }
-    CK_LAUNCH();
+    if (a.M == 2)  // M = 2 is specialised; other M share the counted-compare loop
+      launch_pdl(k_vertex_staged<2>, g, blk, 0, s, a, lab_in, lab_out, t);
+    else
+      launch_pdl(k_vertex_staged<0>, g, blk, 0, s, a, lab_in, lab_out, t);
     return;
   }
 #define VA_ARGS                                                                              \
   a.g_off, a.g_nbr, a.mean, a.cover, lab_in, lab_out, a.minE, a.R, a.M, a.terms, a.beta, \
       a.unconv, t, a.fixed, a.tile_counts, a.tiles
   switch (a.M) {
-    case 2: k_vertex_argmin<2><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
-    case 3: k_vertex_argmin<3><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
-    case 4: k_vertex_argmin<4><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
-    case 5: k_vertex_argmin<5><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
-    case 6: k_vertex_argmin<6><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
-    case 7: k_vertex_argmin<7><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
-    case 8: k_vertex_argmin<8><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
-    default: k_vertex_argmin<0><<<g, kVtxThreads, 0, s>>>(VA_ARGS); break;
+    case 2: launch_pdl(k_vertex_argmin<2>, g, blk, 0, s, VA_ARGS); break;
+    case 3: launch_pdl(k_vertex_argmin<3>, g, blk, 0, s, VA_ARGS); break;
+    case 4: launch_pdl(k_vertex_argmin<4>, g, blk, 0, s, VA_ARGS); break;
+    case 5: launch_pdl(k_vertex_argmin<5>, g, blk, 0, s, VA_ARGS); break;
+    case 6: launch_pdl(k_vertex_argmin<6>, g, blk, 0, s, VA_ARGS); break;
+    case 7: launch_pdl(k_vertex_argmin<7>, g, blk, 0, s, VA_ARGS); break;
+    case 8: launch_pdl(k_vertex_argmin<8>, g, blk, 0, s, VA_ARGS); break;
+    default: launch_pdl(k_vertex_argmin<0>, g, blk, 0, s, VA_ARGS); break;
   }
 #undef VA_ARGS
-  CK_LAUNCH();
 }
 
 void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s) {
-  const unsigned g = grid_for(a.Hs, kHoodThreads);
+  const dim3 g(grid_for(a.Hs, kHoodThreads)), blk(kHoodThreads);
   if (a.staged)
-    k_hood_staged<<<g, kHoodThreads, 0, s>>>(a, t);
+    launch_pdl(k_hood_staged, g, blk, 0, s, a, t);
   else
-    k_hood_sums<<<g, kHoodThreads, 0, s>>>(a.s_off, a.h_mem, a.minE, a.hist, a.flags, a.Hs, t,
-                                           a.L, a.ring, a.tol, a.unconv, a.fixed);
-  CK_LAUNCH();
+    launch_pdl(k_hood_sums, g, blk, 0, s, a.s_off, a.h_mem, (const double*)a.minE, a.hist,
+               a.flags, a.Hs, t, a.L, a.ring, a.tol, a.unconv, a.fixed);
 }
 
 // Cooperative launch of k_map_loop; grid = co-resident blocks (<= work tiles).
@@ -896,14 +946,13 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
     CK_LAUNCH();
     ++n;
   }
-  k_tile_offsets<<<1, 1024, 0, s>>>(counts, counts_ready ? unconv : nullptr, map_max, fixed,
-                                    tile_base, tiles, M, Hs, layout);
-  CK_LAUNCH();
+  launch_pdl(k_tile_offsets, dim3(1), dim3(1024), 0, s, (const uint32_t*)counts,
+             counts_ready ? unconv : nullptr, map_max, fixed, tile_base, tiles, M, Hs, layout);
   ++n;
   if (tiles) {
-    k_label_tiles<1><<<tiles, kTileThreads, smem, s>>>(lab_even, lab_odd, unconv, map_max, fixed,
-                                                       R, M, mean, nullptr, tile_base, layout, x);
-    CK_LAUNCH();
+    launch_pdl(k_label_tiles<1>, dim3(tiles), dim3(kTileThreads), smem, s, lab_even, lab_odd,
+               unconv, map_max, fixed, R, M, mean, (uint32_t*)nullptr,
+               (const uint32_t*)tile_base, (const uint32_t*)layout, x);
     ++n;
   }
   static bool smem_set = false;
@@ -916,13 +965,12 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
     smem_set = true;
   }
   const unsigned lg = grid_for(max_leaves, kLeavesPerBlock);
-  k_leaf_fold<false><<<lg, 256, leaf_smem, s>>>(x, layout, M, hist, Hs, ring, unconv, map_max,
-                                                fixed, params, partials, em_out, mb.done.get());
-  CK_LAUNCH();
-  k_leaf_fold<true><<<lg, 256, leaf_smem, s>>>(x, layout, M, nullptr, 0, 1, unconv, map_max,
-                                               fixed, params, partials, em_out,
-                                               mb.done.get() + 1);
-  CK_LAUNCH();
+  launch_pdl(k_leaf_fold<false>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
+             (const uint32_t*)layout, M, hist, Hs, ring, unconv, map_max, fixed, params, partials,
+             em_out, mb.done.get());
+  launch_pdl(k_leaf_fold<true>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
+             (const uint32_t*)layout, M, (const double*)nullptr, uint64_t(0), 1, unconv, map_max,
+             fixed, params, partials, em_out, mb.done.get() + 1);
   n += 2;
   if (launches) *launches += n;
 }
