@@ -70,7 +70,11 @@ enum {
   DPMRF_RUN_TWO_KERNELS = 8u,   /* two kernels per MAP iteration (the default) */
   DPMRF_RUN_NO_GRAPH = 16u,     /* launch each EM iteration directly instead of a CUDA graph */
   DPMRF_RUN_PERSISTENT = 32u,   /* one cooperative persistent kernel per MAP loop */
-  DPMRF_RUN_STAGED = 64u        /* shared-memory staged vertex/hood tiles */
+  DPMRF_RUN_STAGED = 64u,       /* shared-memory staged vertex/hood tiles */
+  DPMRF_RUN_HOST_LOG = 128u     /* host round trip per EM iteration (log(sigma) on the host);
+                                   default: EM iterations run back to back on the device with a
+                                   correctly rounded device log, verified against the host libm
+                                   afterwards (rerun with host logs on any difference) */
 };
 
 typedef struct dpmrf_run_options {
@@ -94,6 +98,8 @@ typedef struct dpmrf_run_stats {
   uint64_t map_loop_launches;
   int32_t persistent;        /* 1: persistent MAP loop, 0: two kernels per MAP iteration */
   int32_t graphs;            /* 1: EM iterations replayed from CUDA graphs */
+  int32_t device_loop;       /* 1: the result came from the device-resident EM loop */
+  uint32_t device_log_fallbacks; /* reruns because a device log(sigma) differed from the host's */
 } dpmrf_run_stats;
 
 /* ---- context ------------------------------------------------------------ */
@@ -191,6 +197,11 @@ dpmrf_status dpmrf_update_labels(dpmrf_context* ctx, const uint32_t* argmin_labe
 dpmrf_status dpmrf_update_parameters(dpmrf_context* ctx, const uint32_t* labels,
                                      uint32_t num_labels, const double* prev_mu,
                                      const double* prev_sigma, double* mu, double* sigma);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+/* The device's correctly rounded natural log used by the device-resident EM
+ * loop for log(sigma) (n values, host buffers). */
+dpmrf_status dpmrf_debug_log(dpmrf_context* ctx, uint64_t n, const double* x, double* out);
 
 #ifdef __cplusplus
 }

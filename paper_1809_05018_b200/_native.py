@@ -43,7 +43,8 @@ class CRunStats(ct.Structure):
                 ("mstep_ms", F64), ("vertex_launches", U64), ("hood_launches", U64),
                 ("kernel_launches", U64), ("em_iters", I32), ("map_iters_total", I32),
                 ("series", U64), ("map_loop_ms", F64), ("map_loop_launches", U64),
-                ("persistent", I32), ("graphs", I32)]
+                ("persistent", I32), ("graphs", I32), ("device_loop", I32),
+                ("device_log_fallbacks", U32)]
 
 
 # (name, restype, argtypes) of every C ABI entry point (include/dpmrf_cuda.h)
@@ -72,6 +73,7 @@ CUDA_API = [
     ("dpmrf_check_convergence", ST, [VP, U64, U64, VP, I32, F64, VP]),
     ("dpmrf_update_labels", ST, [VP, VP, U32, VP, VP]),
     ("dpmrf_update_parameters", ST, [VP, VP, U32, VP, VP, VP, VP]),
+    ("dpmrf_debug_log", ST, [VP, U64, VP, VP]),
 ]
 
 INPUTS_API = [

@@ -137,6 +137,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     if (const char* e = std::getenv("DPMRF_DIRECT")) c->use_staged = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_NO_L2_PERSIST")) c->use_l2_persist = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_NO_PDL")) pdl_enabled() = e[0] == '0';
+    if (const char* e = std::getenv("DPMRF_HOST_LOG")) c->use_device_loop = e[0] == '0';
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -254,205 +255,295 @@ extern "C" dpmrf_status dpmrf_get_hoods(dpmrf_context* ctx, uint64_t* H, uint64_
 }
 
 // ---- optimize ------------------------------------------------------------------
-extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
-                                       const dpmrf_run_options* opts, uint32_t* labels_out,
-                                       double* mu_out, double* sigma_out) {
-  return guarded([&] {
-    need(ctx && cfg, DPMRF_INVALID_ARGUMENT, "null argument");
-    const dpmrf_run_options o = opts ? *opts : dpmrf_run_options{0, DPMRF_TRACE_FULL};
-    const bool multilabel = (o.flags & DPMRF_RUN_MULTILABEL) != 0;
-    const int fixed = (o.flags & DPMRF_RUN_FIXED_WORK) ? 1 : 0;
-    const bool timing = (o.flags & DPMRF_RUN_KERNEL_TIMING) != 0;
-    validate_config(*cfg, multilabel);
-    need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
-    ctx->bind();
-    cudaStream_t st = ctx->stream;
-    const uint32_t M = cfg->num_labels;
-    const uint32_t R = ctx->R;
-    const int L = cfg->convergence_window;
-    const int map_max = cfg->map_max_iters;
+namespace {
 
-    ctx->trace.clear();
-    ctx->trace_level = o.trace_level;
-    ctx->trace_M = M;
-    ctx->stats = dpmrf_run_stats{};
-    uint64_t launches = 0;
+// One optimize() run.  device_loop = true enqueues every EM iteration back to
+// back with the EM bookkeeping and log(sigma) on the device (k_em_epilogue)
+// and synchronizes once; it returns false if any device log differs from the
+// host libm (the caller then reruns with host logs, device_loop = false,
+// which synchronizes once per EM iteration exactly as make_label_terms).
+bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
+                  const dpmrf_run_options& o, bool device_loop, uint32_t* labels_out,
+                  double* mu_out, double* sigma_out) {
+  const int fixed = (o.flags & DPMRF_RUN_FIXED_WORK) ? 1 : 0;
+  const bool timing = (o.flags & DPMRF_RUN_KERNEL_TIMING) != 0;
+  cudaStream_t st = ctx->stream;
+  const uint32_t M = cfg->num_labels;
+  const uint32_t R = ctx->R;
+  const int L = cfg->convergence_window;
+  const int map_max = cfg->map_max_iters;
+  const int em_max = cfg->em_max_iters;
 
-    // init_random (engine.cpp:28-38): params on the host, labels on the device
-    std::vector<double> mu(M), sigma(M);
-    init_params(M, cfg->rng_seed, mu.data(), sigma.data());
-    uint8_t* lab[2] = {ctx->lab[0].ensure(R), ctx->lab[1].ensure(R)};
-    CK(cudaEventRecord(ctx->ev_begin, st));
-    launch_init_labels(lab[0], R, M, cfg->rng_seed, st);
-    launches += R ? 1 : 0;
-    int cur = 0;
+  ctx->trace.clear();
+  ctx->trace_level = o.trace_level;
+  ctx->trace_M = M;
+  const uint32_t fallbacks = ctx->stats.device_log_fallbacks;
+  ctx->stats = dpmrf_run_stats{};
+  ctx->stats.device_log_fallbacks = fallbacks;
+  ctx->stats.device_loop = device_loop;
+  uint64_t launches = 0;
 
-    if (cfg->em_max_iters > 0) {
-      ctx->prepare();
-      const uint64_t Hs = ctx->Hs;
-      MapArgs a{};
-      a.g_off = ctx->g_off.get();
-      a.g_nbr = ctx->g_nbr.get();
-      a.mean = ctx->g_mean.get();
-      a.cover = ctx->cover.get();
-      a.s_off = ctx->series_alias ? ctx->h_off.get() : ctx->s_off_buf.get();
-      a.h_mem = ctx->h_mem.get();
-      a.R = R;
-      a.Hs = Hs;
-      a.M = M;
-      a.beta = cfg->beta;
-      a.tol = cfg->convergence_tol;
-      const bool full = o.trace_level >= DPMRF_TRACE_FULL;
-      const bool persistent = (o.flags & DPMRF_RUN_PERSISTENT) ||
-                              (ctx->use_persistent && !(o.flags & DPMRF_RUN_TWO_KERNELS));
-      a.L = L;
-      a.ring = full ? map_max : L + 1;
-      a.fixed = fixed;
-      a.staged = (ctx->use_staged || (o.flags & DPMRF_RUN_STAGED)) ? 1 : 0;
-      a.terms = ctx->terms.ensure(3 * M);
-      double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
-      ctx->pin_in_l2(minE2, uint64_t(R) * sizeof(double));
-      a.minE = minE2;
-      a.hist = ctx->hist.ensure(uint64_t(a.ring) * Hs);
-      a.flags = full ? ctx->flags.ensure(uint64_t(map_max) * Hs) : nullptr;
-      a.unconv = ctx->unconv.ensure(map_max);
-      mstep_reserve(ctx->ms, R, M, Hs);  // before any capture: no allocation inside a graph
-      a.tile_counts = ctx->ms.counts.get();
-      a.tiles = label_tiles(R);
-      double* params = ctx->params.ensure(2 * M);
-      double* em_out = ctx->em_out.ensure(2 + 2 * M);
-      double* h_terms = ctx->h_terms.ensure(3 * M);
-      double* h_em = ctx->h_em.ensure(2 + 2 * M);
-      double* h_row = nullptr;
-      uint8_t* h_flags = nullptr;
-      if (a.flags) {
-        h_row = ctx->h_row.ensure(uint64_t(map_max) * Hs);
-        h_flags = ctx->h_flags.ensure(uint64_t(map_max) * Hs);
-      }
-      CK(cudaMemcpyAsync(params, mu.data(), M * 8, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(params + M, sigma.data(), M * 8, cudaMemcpyHostToDevice, st));
-      std::vector<double> em_hist;
-      const size_t ev_per_em = timing ? size_t(3 * map_max + 4) : 0;
-      ctx->stats.persistent = persistent;
-      for (size_t i = 0; i < ev_per_em; ++i) ctx->event(i);
-      // Everything one EM iteration puts on the stream (no host sync inside).
-      uint64_t em_kernels = 0;
-      bool capturing = false;  // event records become graph nodes only when captured as external
-      auto record = [&](size_t i) {
-        if (!timing) return;
-        if (capturing)
-          CK(cudaEventRecordWithFlags(ctx->ev_pool[i], st, cudaEventRecordExternal));
-        else
-          CK(cudaEventRecord(ctx->ev_pool[i], st));
-      };
-      auto enqueue_em = [&](int parity) {
-        uint64_t k = 0;
-        size_t ev = 0;
+  // init_random (engine.cpp:28-38): params on the host, labels on the device
+  std::vector<double> mu(M), sigma(M);
+  init_params(M, cfg->rng_seed, mu.data(), sigma.data());
+  uint8_t* lab[2] = {ctx->lab[0].ensure(R), ctx->lab[1].ensure(R)};
+  CK(cudaEventRecord(ctx->ev_begin, st));
+  launch_init_labels(lab[0], R, M, cfg->rng_seed, st);
+  launches += R ? 1 : 0;
+  int cur = 0;
+
+  if (em_max > 0) {
+    ctx->prepare();
+    const uint64_t Hs = ctx->Hs;
+    MapArgs a{};
+    a.g_off = ctx->g_off.get();
+    a.g_nbr = ctx->g_nbr.get();
+    a.mean = ctx->g_mean.get();
+    a.cover = ctx->cover.get();
+    a.s_off = ctx->series_alias ? ctx->h_off.get() : ctx->s_off_buf.get();
+    a.h_mem = ctx->h_mem.get();
+    a.R = R;
+    a.Hs = Hs;
+    a.M = M;
+    a.beta = cfg->beta;
+    a.tol = cfg->convergence_tol;
+    const bool full = o.trace_level >= DPMRF_TRACE_FULL;
+    const bool persistent = (o.flags & DPMRF_RUN_PERSISTENT) ||
+                            (ctx->use_persistent && !(o.flags & DPMRF_RUN_TWO_KERNELS));
+    a.L = L;
+    a.ring = full ? map_max : L + 1;
+    a.fixed = fixed;
+    a.staged = (ctx->use_staged || (o.flags & DPMRF_RUN_STAGED)) ? 1 : 0;
+    a.terms = ctx->terms.ensure(3 * M);
+    double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
+    ctx->pin_in_l2(minE2, uint64_t(R) * sizeof(double));
+    a.minE = minE2;
+    a.hist = ctx->hist.ensure(uint64_t(a.ring) * Hs);
+    a.flags = full ? ctx->flags.ensure(uint64_t(map_max) * Hs) : nullptr;
+    // [em_done, pending_done, em_count, pad | per-MAP-iteration counters]
+    uint32_t* state = ctx->unconv.ensure(uint64_t(map_max) + 4);
+    a.unconv = state + 4;
+    CK(cudaMemsetAsync(state, 0, 4 * sizeof(uint32_t), st));
+    mstep_reserve(ctx->ms, R, M, Hs);  // before any capture: no allocation inside a graph
+    a.tile_counts = ctx->ms.counts.get();
+    a.tiles = label_tiles(R);
+    double* params = ctx->params.ensure(2 * M);
+    double* em_out = ctx->em_out.ensure(2 + 2 * M);
+    double* h_terms = ctx->h_terms.ensure(3 * M);
+    double* h_em = ctx->h_em.ensure(2 + 2 * M);
+    const uint64_t rec_stride = 3 + 3 * uint64_t(M);
+    double* em_rec = ctx->em_rec.ensure(uint64_t(em_max) * rec_stride);
+    double* em_hist_d = ctx->em_hist.ensure(uint64_t(em_max));
+    double* h_rec = ctx->h_rec.ensure(uint64_t(em_max) * rec_stride + 4);
+    double* h_row = nullptr;
+    uint8_t* h_flags = nullptr;
+    if (a.flags) {
+      h_row = ctx->h_row.ensure(uint64_t(map_max) * Hs);
+      h_flags = ctx->h_flags.ensure(uint64_t(map_max) * Hs);
+    }
+    CK(cudaMemcpyAsync(params, mu.data(), M * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(params + M, sigma.data(), M * 8, cudaMemcpyHostToDevice, st));
+    EmEpilogueArgs ep{};
+    ep.unconv = a.unconv;
+    ep.map_max = map_max;
+    ep.fixed = fixed;
+    ep.L = L;
+    ep.tol = cfg->convergence_tol;
+    ep.lab0 = lab[0];
+    ep.lab1 = lab[1];
+    ep.R = R;
+    ep.M = M;
+    ep.em_out = em_out;
+    ep.em_hist = em_hist_d;
+    ep.em_rec = em_rec;
+    ep.terms = const_cast<double*>(a.terms);
+    std::vector<double> em_hist;
+    const size_t ev_per_em = timing ? size_t(3 * map_max + 4) : 0;
+    ctx->stats.persistent = persistent;
+    for (size_t i = 0; i < ev_per_em; ++i) ctx->event(i);
+    // Everything one EM iteration puts on the stream (no host sync inside).
+    uint64_t em_kernels = 0;
+    bool capturing = false;  // event records become graph nodes only when captured as external
+    auto record = [&](size_t i) {
+      if (!timing) return;
+      if (capturing)
+        CK(cudaEventRecordWithFlags(ctx->ev_pool[i], st, cudaEventRecordExternal));
+      else
+        CK(cudaEventRecord(ctx->ev_pool[i], st));
+    };
+    auto enqueue_em = [&](int parity) {
+      uint64_t k = 0;
+      size_t ev = 0;
+      if (device_loop) {
+        launch_em_prologue(a.unconv, map_max, st);
+        ++k;
+      } else {
         CK(cudaMemcpyAsync(const_cast<double*>(a.terms), h_terms, 3 * M * 8,
                            cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(a.unconv, 0, map_max * sizeof(uint32_t), st));
-        if (persistent) {
-          record(ev++);
-          launch_map_loop(a, lab[parity], lab[parity ^ 1], minE2, minE2 + R, map_max, st);
-          record(ev++);
-          k += 1;
-        } else {
-          for (int t = 0; t < map_max; ++t) {
-            const uint8_t* lin = lab[(parity + t) & 1];
-            uint8_t* lout = lab[(parity + t + 1) & 1];
-            record(ev++);
-            launch_vertex_argmin(a, lin, lout, t, st);
-            record(ev++);
-            launch_hood_sums(a, t, st);
-            record(ev++);
-            k += 2;
-          }
-        }
-        if (a.flags && Hs) {  // full trace: every MAP row and flag vector of this EM
-          CK(cudaMemcpyAsync(h_row, a.hist, uint64_t(map_max) * Hs * 8, cudaMemcpyDeviceToHost,
-                             st));
-          CK(cudaMemcpyAsync(h_flags, a.flags, uint64_t(map_max) * Hs, cudaMemcpyDeviceToHost,
-                             st));
-        }
+      }
+      if (persistent) {
         record(ev++);
-        launch_mstep(a.mean, R, M, lab[parity], lab[parity ^ 1], a.hist, Hs, a.ring, a.unconv,
-                     map_max, fixed, params, em_out, ctx->ms, st, &k);
+        launch_map_loop(a, lab[parity], lab[parity ^ 1], minE2, minE2 + R, map_max, st);
         record(ev++);
-        CK(cudaMemcpyAsync(h_em, em_out, (2 + 2 * M) * 8, cudaMemcpyDeviceToHost, st));
-        em_kernels = k;
-      };
-      // One CUDA graph per label-buffer parity, captured once per shape and
-      // replayed every EM iteration (the EM loop is launch-bound at 2560^2).
-      const bool use_graph = ctx->use_graphs && !(o.flags & DPMRF_RUN_NO_GRAPH);
-      ctx->stats.graphs = use_graph;
-      if (use_graph) {
-        dpmrf_context::GraphKey key{};
-        key.R = R;
-        key.Hs = Hs;
-        key.M = M;
-        key.L = L;
-        key.map_max = map_max;
-        key.fixed = fixed;
-        key.timing = timing;
-        key.persistent = persistent + 2 * a.staged;
-        key.trace = o.trace_level;
-        key.beta = cfg->beta;
-        key.tol = cfg->convergence_tol;
-        key.p[0] = lab[0];
-        key.p[1] = lab[1];
-        key.p[2] = a.minE;
-        key.p[3] = a.hist;
-        key.p[4] = a.flags;
-        key.p[5] = a.unconv;
-        key.p[6] = params;
-        key.p[7] = h_em;
-        key.p[8] = h_row;
-        key.p[9] = a.s_off;
-        key.p[10] = a.h_mem;
-        key.p[11] = a.g_nbr;
-        key.p[12] = ctx->ms.x.get();
-        key.p[13] = ctx->ms.partials.get();
-        key.p[14] = a.terms;
-        key.p[15] = h_terms;
-        key.p[16] = ctx->ms.counts.get();
-        key.p[17] = ctx->ms.tile_base.get();
-        key.p[18] = ctx->ms.layout.get();
-        key.p[19] = nullptr;
-        key.p[20] = h_flags;
-        key.p[21] = a.cover;
-        key.p[22] = a.g_off;
-        key.p[23] = em_out;
-        if (!ctx->graph_valid || std::memcmp(&key, &ctx->graph_key, sizeof key) != 0) {
-          ctx->drop_graphs();
-          for (int parity = 0; parity < 2; ++parity) {
-            cudaGraph_t g;
-            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-            capturing = true;
-            try {
-              enqueue_em(parity);
-            } catch (...) {
-              capturing = false;
-              cudaStreamEndCapture(st, &g);
-              if (g) cudaGraphDestroy(g);
-              throw;
-            }
-            capturing = false;
-            CK(cudaStreamEndCapture(st, &g));
-            CK(cudaGraphInstantiate(&ctx->graph_exec[parity], g, 0));
-            CK(cudaGraphDestroy(g));
-          }
-          ctx->graph_kernels = em_kernels;
-          ctx->graph_key = key;
-          ctx->graph_valid = true;
+        k += 1;
+      } else {
+        for (int t = 0; t < map_max; ++t) {
+          const uint8_t* lin = lab[(parity + t) & 1];
+          uint8_t* lout = lab[(parity + t + 1) & 1];
+          record(ev++);
+          launch_vertex_argmin(a, lin, lout, t, st);
+          record(ev++);
+          launch_hood_sums(a, t, st);
+          record(ev++);
+          k += 2;
         }
       }
-      for (int em = 0; em < cfg->em_max_iters; ++em) {
-        // make_label_terms (model.hpp:48-60) with the host's std::log
-        for (uint32_t l = 0; l < M; ++l) {
-          h_terms[l] = mu[l];
-          h_terms[M + l] = 2.0 * (sigma[l] * sigma[l]);
-          h_terms[2 * M + l] = std::log(sigma[l]);
+      if (a.flags && Hs) {  // full trace: every MAP row and flag vector of this EM
+        CK(cudaMemcpyAsync(h_row, a.hist, uint64_t(map_max) * Hs * 8, cudaMemcpyDeviceToHost,
+                           st));
+        CK(cudaMemcpyAsync(h_flags, a.flags, uint64_t(map_max) * Hs, cudaMemcpyDeviceToHost,
+                           st));
+      }
+      record(ev++);
+      launch_mstep(a.mean, R, M, lab[parity], lab[parity ^ 1], a.hist, Hs, a.ring, a.unconv,
+                   map_max, fixed, params, em_out, ctx->ms, st, &k);
+      record(ev++);
+      if (device_loop) {
+        launch_em_epilogue(ep, st);
+        ++k;
+      } else {
+        CK(cudaMemcpyAsync(h_em, em_out, (2 + 2 * M) * 8, cudaMemcpyDeviceToHost, st));
+      }
+      em_kernels = k;
+    };
+    // CUDA graphs of one EM iteration, captured once per shape and replayed
+    // every EM iteration (one per label-buffer parity on the host-log path;
+    // the device loop always restarts from buffer 0).
+    const bool use_graph = ctx->use_graphs && !(o.flags & DPMRF_RUN_NO_GRAPH);
+    ctx->stats.graphs = use_graph;
+    if (use_graph) {
+      dpmrf_context::GraphKey key{};
+      key.R = R;
+      key.Hs = Hs;
+      key.M = M;
+      key.L = L;
+      key.map_max = map_max;
+      key.fixed = fixed;
+      key.timing = timing;
+      key.persistent = persistent + 2 * a.staged + 4 * device_loop;
+      key.trace = o.trace_level;
+      key.beta = cfg->beta;
+      key.tol = cfg->convergence_tol;
+      key.p[0] = lab[0];
+      key.p[1] = lab[1];
+      key.p[2] = a.minE;
+      key.p[3] = a.hist;
+      key.p[4] = a.flags;
+      key.p[5] = a.unconv;
+      key.p[6] = params;
+      key.p[7] = h_em;
+      key.p[8] = h_row;
+      key.p[9] = a.s_off;
+      key.p[10] = a.h_mem;
+      key.p[11] = a.g_nbr;
+      key.p[12] = ctx->ms.x.get();
+      key.p[13] = ctx->ms.partials.get();
+      key.p[14] = a.terms;
+      key.p[15] = h_terms;
+      key.p[16] = ctx->ms.counts.get();
+      key.p[17] = ctx->ms.tile_base.get();
+      key.p[18] = ctx->ms.layout.get();
+      key.p[19] = em_rec;
+      key.p[20] = h_flags;
+      key.p[21] = a.cover;
+      key.p[22] = a.g_off;
+      key.p[23] = em_out;
+      key.p2[0] = em_hist_d;
+      key.p2[1] = a.mean;
+      if (!ctx->graph_valid || std::memcmp(&key, &ctx->graph_key, sizeof key) != 0) {
+        ctx->drop_graphs();
+        for (int parity = 0; parity < (device_loop ? 1 : 2); ++parity) {
+          cudaGraph_t g;
+          CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          capturing = true;
+          try {
+            enqueue_em(parity);
+          } catch (...) {
+            capturing = false;
+            cudaStreamEndCapture(st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+          }
+          capturing = false;
+          CK(cudaStreamEndCapture(st, &g));
+          CK(cudaGraphInstantiate(&ctx->graph_exec[parity], g, 0));
+          CK(cudaGraphDestroy(g));
         }
+        ctx->graph_kernels = em_kernels;
+        ctx->graph_key = key;
+        ctx->graph_valid = true;
+      }
+    }
+    auto host_terms = [&] {  // make_label_terms (model.hpp:48-60) with the host's std::log
+      for (uint32_t l = 0; l < M; ++l) {
+        h_terms[l] = mu[l];
+        h_terms[M + l] = 2.0 * (sigma[l] * sigma[l]);
+        h_terms[2 * M + l] = std::log(sigma[l]);
+      }
+    };
+    if (device_loop) {
+      // ---- all EM iterations back to back, one synchronization ----
+      host_terms();
+      CK(cudaMemcpyAsync(const_cast<double*>(a.terms), h_terms, 3 * M * 8,
+                         cudaMemcpyHostToDevice, st));
+      for (int em = 0; em < em_max; ++em) {
+        if (use_graph) {
+          CK(cudaGraphLaunch(ctx->graph_exec[0], st));
+        } else {
+          enqueue_em(0);
+        }
+      }
+      CK(cudaMemcpyAsync(h_rec, state, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_rec + 4, em_rec, uint64_t(em_max) * rec_stride * 8,
+                         cudaMemcpyDeviceToHost, st));
+      ctx->sync();
+      uint32_t hstate[4];
+      std::memcpy(hstate, h_rec, sizeof hstate);
+      const int em_count = static_cast<int>(hstate[2]);
+      const double* rec = h_rec + 4;
+      // every device log(sigma) that fed a later EM iteration must equal glibc's
+      for (int e = 0; e + 1 < em_count; ++e)
+        for (uint32_t l = 0; l < M; ++l) {
+          const double sg = rec[e * rec_stride + 3 + M + l];
+          const double dev = rec[e * rec_stride + 3 + 2 * M + l];
+          const double host = std::log(sg);
+          if (std::memcmp(&dev, &host, sizeof host) != 0) return false;
+        }
+      launches += uint64_t(em_count) * (use_graph ? ctx->graph_kernels : em_kernels);
+      for (int e = 0; e < em_count; ++e) {
+        const double* r = rec + e * rec_stride;
+        const int T = static_cast<int>(r[1]);
+        ctx->stats.map_iters_total += T;
+        if (o.trace_level >= DPMRF_TRACE_EM) {
+          dpmrf_context::EmRecord er;
+          er.map_iters = T;
+          er.total = r[0];
+          er.converged = r[2] != 0.0;
+          er.mu.assign(r + 3, r + 3 + M);
+          er.sigma.assign(r + 3 + M, r + 3 + 2 * M);
+          ctx->trace.push_back(std::move(er));
+        }
+        if (e == em_count - 1) {
+          mu.assign(r + 3, r + 3 + M);
+          sigma.assign(r + 3 + M, r + 3 + 2 * M);
+        }
+      }
+      ctx->stats.em_iters = em_count;
+      cur = 0;
+    } else {
+      for (int em = 0; em < em_max; ++em) {
+        host_terms();
         if (use_graph) {
           CK(cudaGraphLaunch(ctx->graph_exec[cur], st));
           launches += ctx->graph_kernels;
@@ -520,22 +611,47 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
         ctx->stats.em_iters = em + 1;
         if (conv && !fixed) break;
       }
-      ctx->stats.series = Hs;
     }
-    // labels out (u8 in HBM -> the reference's u32)
-    uint32_t* l32 = ctx->labels32.ensure(R);
-    launch_u8_to_u32(lab[cur], l32, R, st);
-    launches += R ? 1 : 0;
-    CK(cudaEventRecord(ctx->ev_end, st));
-    if (labels_out && R)
-      CK(cudaMemcpyAsync(labels_out, l32, uint64_t(R) * 4, cudaMemcpyDeviceToHost, st));
-    ctx->sync();
-    float total_ms = 0.f;
-    CK(cudaEventElapsedTime(&total_ms, ctx->ev_begin, ctx->ev_end));
-    ctx->stats.optimize_ms = total_ms;
-    ctx->stats.kernel_launches = launches;
-    if (mu_out) std::memcpy(mu_out, mu.data(), M * 8);
-    if (sigma_out) std::memcpy(sigma_out, sigma.data(), M * 8);
+    ctx->stats.series = Hs;
+  }
+  // labels out (u8 in HBM -> the reference's u32)
+  uint32_t* l32 = ctx->labels32.ensure(R);
+  launch_u8_to_u32(lab[cur], l32, R, st);
+  launches += R ? 1 : 0;
+  CK(cudaEventRecord(ctx->ev_end, st));
+  if (labels_out && R)
+    CK(cudaMemcpyAsync(labels_out, l32, uint64_t(R) * 4, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+  float total_ms = 0.f;
+  CK(cudaEventElapsedTime(&total_ms, ctx->ev_begin, ctx->ev_end));
+  ctx->stats.optimize_ms = total_ms;
+  ctx->stats.kernel_launches = launches;
+  if (mu_out) std::memcpy(mu_out, mu.data(), M * 8);
+  if (sigma_out) std::memcpy(sigma_out, sigma.data(), M * 8);
+  return true;
+}
+
+}  // namespace
+
+extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
+                                       const dpmrf_run_options* opts, uint32_t* labels_out,
+                                       double* mu_out, double* sigma_out) {
+  return guarded([&] {
+    need(ctx && cfg, DPMRF_INVALID_ARGUMENT, "null argument");
+    const dpmrf_run_options o = opts ? *opts : dpmrf_run_options{0, DPMRF_TRACE_FULL};
+    validate_config(*cfg, (o.flags & DPMRF_RUN_MULTILABEL) != 0);
+    need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
+    ctx->bind();
+    // The device-resident EM loop serves TRACE_NONE / TRACE_EM runs; the full
+    // per-MAP trace and per-kernel timing use the host-log loop.
+    const bool device_loop = ctx->use_device_loop && !(o.flags & DPMRF_RUN_HOST_LOG) &&
+                             !(o.flags & DPMRF_RUN_KERNEL_TIMING) &&
+                             o.trace_level < DPMRF_TRACE_FULL && cfg->em_max_iters > 0;
+    if (device_loop) {
+      if (run_optimize(ctx, cfg, o, true, labels_out, mu_out, sigma_out)) return;
+      ++ctx->stats.device_log_fallbacks;  // a device log(sigma) differed from glibc's
+    }
+    run_optimize(ctx, cfg, o, false, labels_out, mu_out, sigma_out);
   });
 }
 
@@ -580,5 +696,18 @@ extern "C" dpmrf_status dpmrf_get_stats(dpmrf_context* ctx, dpmrf_run_stats* out
   return guarded([&] {
     need(ctx && out, DPMRF_INVALID_ARGUMENT, "null argument");
     *out = ctx->stats;
+  });
+}
+
+extern "C" dpmrf_status dpmrf_debug_log(dpmrf_context* ctx, uint64_t n, const double* x,
+                                        double* out) {
+  return guarded([&] {
+    need(ctx && (n == 0 || (x && out)), DPMRF_INVALID_ARGUMENT, "null argument");
+    ctx->bind();
+    double* d = ctx->tmp_f64[0].ensure(2 * n);
+    if (n) CK(cudaMemcpyAsync(d, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    launch_log_cr(d, d + n, n, ctx->stream);
+    if (n) CK(cudaMemcpyAsync(out, d + n, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
   });
 }

@@ -181,4 +181,71 @@ struct AddOp {
   __device__ __forceinline__ double operator()(double a, double b) const { return __dadd_rn(a, b); }
 };
 
+// ---- correctly rounded natural log (double-double evaluation) ---------------
+// make_label_terms takes log(sigma) from the host libm (model.hpp:57).  To run
+// EM iterations back to back on the device, log(sigma) is evaluated here to
+// ~2^-100 relative accuracy and rounded once, i.e. correctly rounded; glibc's
+// log agrees with the correctly rounded value except in rare cases (measured
+// ~5e-4 of random inputs), and the host verifies every value after the run
+// and falls back to host-evaluated logs when one differs (capi.cu).
+struct dd_t {
+  double hi, lo;
+};
+__device__ __forceinline__ dd_t dd_two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  return {s, __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb))};
+}
+__device__ __forceinline__ dd_t dd_fast_two_sum(double a, double b) {  // |a| >= |b|
+  const double s = __dadd_rn(a, b);
+  return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ dd_t dd_add(dd_t a, dd_t b) {
+  dd_t s = dd_two_sum(a.hi, b.hi);
+  const dd_t t = dd_two_sum(a.lo, b.lo);
+  s.lo = __dadd_rn(s.lo, t.hi);
+  s = dd_fast_two_sum(s.hi, s.lo);
+  s.lo = __dadd_rn(s.lo, t.lo);
+  return dd_fast_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd_t dd_mul(dd_t a, dd_t b) {
+  const double p = __dmul_rn(a.hi, b.hi);
+  double e = __fma_rn(a.hi, b.hi, -p);
+  e = __dadd_rn(e, __dadd_rn(__dmul_rn(a.hi, b.lo), __dmul_rn(a.lo, b.hi)));
+  return dd_fast_two_sum(p, e);
+}
+__device__ __forceinline__ dd_t dd_div(dd_t a, dd_t b) {
+  const double q1 = __ddiv_rn(a.hi, b.hi);
+  dd_t r = dd_add(a, dd_mul({-q1, 0.0}, b));
+  const double q2 = __ddiv_rn(r.hi, b.hi);
+  r = dd_add(r, dd_mul({-q2, 0.0}, b));
+  const double q3 = __ddiv_rn(r.hi, b.hi);
+  return dd_add(dd_fast_two_sum(q1, q2), {q3, 0.0});
+}
+// log x = e ln2 + 2 atanh(f), f = (m-1)/(m+1), m in [1/sqrt2, sqrt2):
+// |f| <= 0.1716, f^2 <= 0.0295, 23 series terms reach 2^-110.
+__device__ inline double log_cr(double x) {
+  if (!(x > 0.0) || isinf(x) || x < 2.2250738585072014e-308) return log(x);
+  int e;
+  double m = frexp(x, &e);
+  if (m < 0.70710678118654752440) {
+    m = __dmul_rn(m, 2.0);
+    e -= 1;
+  }
+  const dd_t f = dd_div({__dsub_rn(m, 1.0), 0.0}, dd_two_sum(m, 1.0));
+  const dd_t z = dd_mul(f, f);
+  constexpr int kTerms = 23;
+  auto coef = [](int k) -> dd_t {
+    const double n = 2.0 * k + 1.0;
+    const double hi = __ddiv_rn(1.0, n);
+    return {hi, __ddiv_rn(__fma_rn(-hi, n, 1.0), n)};
+  };
+  dd_t S = coef(kTerms - 1);
+  for (int k = kTerms - 2; k >= 0; --k) S = dd_add(dd_mul(S, z), coef(k));
+  const dd_t lm = dd_mul({__dmul_rn(2.0, f.hi), __dmul_rn(2.0, f.lo)}, S);
+  const dd_t ln2 = {0x1.62e42fefa39efp-1, 0x1.abc9e3b39803fp-56};
+  const dd_t r = dd_add(dd_mul({static_cast<double>(e), 0.0}, ln2), lm);
+  return __dadd_rn(r.hi, r.lo);
+}
+
 }  // namespace dpmrf_b200

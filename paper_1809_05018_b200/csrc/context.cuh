@@ -78,7 +78,11 @@ struct dpmrf_context {
     int32_t L, map_max, fixed, timing, trace, persistent;
     double beta, tol;
     const void* p[24];
+    const void* p2[4];
   };
+  bool use_device_loop = true;  // EM iterations back to back on the device (DPMRF_HOST_LOG=1 off)
+  dpmrf_b200::DevBuf<double> em_rec, em_hist;
+  dpmrf_b200::HostBuf<double> h_rec;
   bool use_graphs = true;
   // one cooperative MAP-loop kernel per EM iteration instead of two kernels
   // per MAP iteration: measured slower at both 2560^2 and 16384^2 (fewer

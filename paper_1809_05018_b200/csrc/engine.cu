@@ -22,11 +22,21 @@ namespace {
 constexpr int kVtxThreads = 256;
 constexpr int kHoodThreads = 256;
 
+// The per-MAP-iteration counters live behind a small EM state block in the
+// same allocation: unconv[kEmDone] != 0 once the EM loop has stopped on the
+// device (optimize.cpp:71 evaluated by k_em_epilogue), which turns every
+// later kernel of the device-resident EM loop into a no-op.
+constexpr int kEmDone = -4, kEmPending = -3, kEmCount = -2;
+
+__device__ __forceinline__ bool em_skipped(const uint32_t* unconv) {
+  return unconv && unconv[kEmDone] != 0;
+}
+
 __device__ __forceinline__ bool map_iter_skipped(const uint32_t* unconv, int t, int fixed) {
   // optimize.cpp:59 -- the MAP loop stops after an iteration whose flags are
   // all set.  Iteration t runs iff no earlier iteration had zero unconverged
   // hoods; skipped iterations leave their counter at 0 so the chain holds.
-  return !fixed && t > 0 && unconv[t - 1] == 0;
+  return unconv[kEmDone] != 0 || (!fixed && t > 0 && unconv[t - 1] == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -453,6 +463,7 @@ __global__ void __launch_bounds__(kVtxThreads)
   cg::grid_group grid = cg::this_grid();
   __shared__ uint8_t sm_lab[kVtxStageCap];
   __shared__ double sm_e[kHoodStageCap];
+  if (em_skipped(a.unconv)) return;
   const uint64_t vt = (uint64_t(a.R) + kVtxThreads - 1) / kVtxThreads;
   const uint64_t ht = (a.Hs + kHoodThreads - 1) / kHoodThreads;
   for (int p = 0; p <= map_max; ++p) {
@@ -531,6 +542,7 @@ __global__ void __launch_bounds__(kTileThreads)
   pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = kTileThreads / 32;
+  if (em_skipped(unconv)) return;
   const uint8_t* lab = final_labels(lab_even, lab_odd, unconv, map_max, fixed);
   for (uint32_t i = threadIdx.x; i < kWarps * M; i += kTileThreads) wcnt[i] = 0;
   __syncthreads();
@@ -567,6 +579,7 @@ __global__ void __launch_bounds__(1024)
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry;
   pdl_wait();
+  if (em_skipped(unconv)) return;
   const uint32_t* tile_counts = final_counts(counts_buf, tiles, M, unconv, map_max, fixed);
   for (uint32_t l = 0; l < M; ++l) {
     if (threadIdx.x == 0) carry = 0;
@@ -636,6 +649,7 @@ __global__ void __launch_bounds__(256)
   const uint32_t* n = layout;
   const uint32_t* label_start = layout + M;
   const uint32_t* leaf_start = layout + 2 * M + 1;
+  if (em_skipped(unconv)) return;  // uniform: no block takes a ticket
   const uint32_t nseries = kSq ? M : M + 1;
   const uint32_t total = leaf_start[nseries];
   const uint32_t first = blockIdx.x * kLeavesPerBlock;
@@ -781,6 +795,63 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) *done = 0;  // re-arm the ticket for the next launch
 }
 
+
+// ---------------------------------------------------------------------------
+// Device-resident EM loop (no host round trip between EM iterations).
+// k_em_prologue arms the MAP counters and folds the previous epilogue's stop
+// decision into the state (so every kernel of this EM sees one value);
+// k_em_epilogue moves the committed labels back to buffer 0, records the EM
+// log, applies the EM-level window (optimize.cpp:66-71) and writes the label
+// terms of the next EM with the device log (make_label_terms, model.hpp:48-60).
+// ---------------------------------------------------------------------------
+__global__ void k_em_prologue(uint32_t* unconv, int map_max) {
+  pdl_wait();
+  if (threadIdx.x == 0 && unconv[kEmPending]) unconv[kEmDone] = 1;
+  for (int t = threadIdx.x; t < map_max; t += blockDim.x) unconv[t] = 0;
+}
+
+__global__ void k_em_epilogue(EmEpilogueArgs a) {
+  pdl_wait();
+  if (a.unconv[kEmDone]) return;
+  const int T = executed_iters(a.unconv, a.map_max, a.fixed);
+  if (T & 1) {  // the last MAP iteration left the committed labels in buffer 1
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < a.R; v += stride)
+      a.lab0[v] = a.lab1[v];
+  }
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const uint32_t e = a.unconv[kEmCount];
+  const uint32_t M = a.M;
+  const double total = a.em_out[0];
+  a.em_hist[e] = total;
+  uint32_t conv = 0;
+  if (int(e) + 1 >= a.L + 1) {
+    conv = 1;
+    for (int i = 1; i <= a.L; ++i)
+      if (!(fabs(__dsub_rn(total, a.em_hist[e - i])) < a.tol)) conv = 0;
+  }
+  double* rec = a.em_rec + uint64_t(e) * (3 + 3 * M);
+  rec[0] = total;
+  rec[1] = static_cast<double>(T);
+  rec[2] = static_cast<double>(conv);
+  for (uint32_t l = 0; l < M; ++l) {
+    const double mu = a.em_out[2 + l], sg = a.em_out[2 + M + l];
+    const double ls = log_cr(sg);
+    rec[3 + l] = mu;
+    rec[3 + M + l] = sg;
+    rec[3 + 2 * M + l] = ls;
+    a.terms[l] = mu;
+    a.terms[M + l] = __dmul_rn(2.0, __dmul_rn(sg, sg));
+    a.terms[2 * M + l] = ls;
+  }
+  a.unconv[kEmCount] = e + 1;
+  if (conv && !a.fixed) a.unconv[kEmPending] = 1;
+}
+
+__global__ void k_log_cr(const double* x, double* out, uint64_t n) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = log_cr(x[i]);
+}
 
 __global__ void k_init_labels(uint8_t* lab, uint32_t R, uint32_t M, uint64_t seed) {
   const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -987,6 +1058,21 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches) {
   mstep_core(mean, R, M, lab_even, lab_odd, unconv, map_max, fixed, hist, Hs, ring, params,
              em_out, mb, s, launches, /*counts_ready=*/true);
+}
+
+void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s) {
+  launch_pdl(k_em_prologue, dim3(1), dim3(256), 0, s, unconv, map_max);
+}
+
+void launch_em_epilogue(const EmEpilogueArgs& a, cudaStream_t s) {
+  const unsigned g = std::min<unsigned>(grid_for(a.R ? a.R : 1, 256), 4 * kNumSMs);
+  launch_pdl(k_em_epilogue, dim3(g), dim3(256), 0, s, a);
+}
+
+void launch_log_cr(const double* x, double* out, uint64_t n, cudaStream_t s) {
+  if (!n) return;
+  k_log_cr<<<grid_for(n, 256), 256, 0, s>>>(x, out, n);
+  CK_LAUNCH();
 }
 
 void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs) {

@@ -68,6 +68,28 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches);
 
+// Device-resident EM loop (see engine.cu).  unconv points 4 words into its
+// allocation: [em_done, pending_done, em_count, pad | unconv[map_max]].
+struct EmEpilogueArgs {
+  uint32_t* unconv;
+  int map_max;
+  int fixed;
+  int L;
+  double tol;
+  uint8_t* lab0;
+  const uint8_t* lab1;
+  uint32_t R;
+  uint32_t M;
+  const double* em_out;  // [total, T, mu(M), sigma(M)] of this EM's M-step
+  double* em_hist;       // em_max totals
+  double* em_rec;        // em_max x (3 + 3M): total, T, conv, mu, sigma, device log(sigma)
+  double* terms;         // next EM's [mu | 2 sigma^2 | log sigma]
+};
+void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s);
+void launch_em_epilogue(const EmEpilogueArgs& a, cudaStream_t s);
+// log_cr over n values (diagnostics / tests of the device log).
+void launch_log_cr(const double* x, double* out, uint64_t n, cudaStream_t s);
+
 // Allocates every M-step buffer up front (required before stream capture).
 void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs);
 

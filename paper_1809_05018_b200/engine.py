@@ -32,7 +32,7 @@ DPMRF_CUDA_ERROR, DPMRF_NCCL_ERROR, DPMRF_INTERNAL_ERROR = 4, 5, 6
 
 TRACE_NONE, TRACE_EM, TRACE_FULL = 0, 1, 2
 RUN_FIXED_WORK, RUN_MULTILABEL, RUN_KERNEL_TIMING, RUN_TWO_KERNELS, RUN_NO_GRAPH = 1, 2, 4, 8, 16
-RUN_PERSISTENT, RUN_STAGED = 32, 64
+RUN_PERSISTENT, RUN_STAGED, RUN_HOST_LOG = 32, 64, 128
 
 K_SIGMA_FLOOR = 1e-3  # kSigmaFloor, model.hpp:9
 
@@ -277,7 +277,8 @@ class Context:
     # -- the optimization phase --
     def optimize(self, config: OptimizerConfig, *, fixed_work=False, multilabel=None,
                  trace_level=TRACE_FULL, kernel_timing=False, labels_out=None,
-                 persistent=None, graphs=True, staged=False) -> OptimizeResult:
+                 persistent=None, graphs=True, staged=False,
+                 host_log=False) -> OptimizeResult:
         """persistent: None = library default, True = one cooperative MAP-loop
         kernel per EM iteration, False = two kernels per MAP iteration."""
         M = config.num_labels
@@ -286,7 +287,7 @@ class Context:
         flags = (RUN_FIXED_WORK if fixed_work else 0) | (RUN_MULTILABEL if multilabel else 0) | \
             (RUN_KERNEL_TIMING if kernel_timing else 0) | \
             ({None: 0, True: RUN_PERSISTENT, False: RUN_TWO_KERNELS}[persistent]) | \
-            (RUN_STAGED if staged else 0) | \
+            (RUN_STAGED if staged else 0) | (RUN_HOST_LOG if host_log else 0) | \
             (0 if graphs else RUN_NO_GRAPH)
         opts = N.CRunOptions(flags, trace_level)
         cfg = config.c()
@@ -318,6 +319,13 @@ class Context:
                     maps.append(MapIterationLog(e, f))
             out.append(EmIterationLog(maps, tot.value, bool(conv.value), LabelParams(mu, sg),
                                       it.value))
+        return out
+
+    def debug_log(self, x):
+        """The device's correctly rounded log (used for log(sigma) on the device loop)."""
+        x = _f64(x)
+        out = np.zeros(len(x))
+        _check(self._lib.dpmrf_debug_log(self.h, len(x), N.ptr(x), N.ptr(out)), "debug_log")
         return out
 
     def stats(self) -> dict:
