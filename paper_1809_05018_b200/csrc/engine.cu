@@ -192,32 +192,12 @@ __device__ __forceinline__ int hood_body(uint64_t h, const uint32_t* __restrict_
                                          double* __restrict__ hist, uint8_t* __restrict__ flags,
                                          uint64_t Hs, int t, int L, int ring, double tol) {
   if (h >= Hs) return 0;
+  // (hoisting the window loads and fully unrolling <= 16-slot hoods raised
+  // register use to 64 and measured slower at both 2560^2 and 16384^2)
   const int R1 = ring;  // >= L+1 rows; == map_max rows when the full trace is kept
-  // the window rows do not depend on this iteration's sum: issue them first
-  constexpr int kWin = 8;
-  double prev[kWin];
-  const bool window = t >= L;
-  if (window) {
-#pragma unroll
-    for (int i = 0; i < kWin; ++i)
-      if (i < L) prev[i] = hist[uint64_t((t - 1 - i) % R1) * Hs + h];
-  }
   const uint32_t lo = s_off[h], hi = s_off[h + 1];
   double sum;
-  if (hi - lo <= 16) {
-    // every member id, then every minimum, in flight together (<= 16 slots:
-    // all grid and brick hoods); then the left fold in slot order
-    uint32_t id[16];
-    double e[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) id[k] = lo + k < hi ? h_mem[lo + k] : 0u;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) e[k] = lo + k < hi ? minE[id[k]] : 0.0;
-    sum = e[0];
-#pragma unroll
-    for (int k = 1; k < 16; ++k)
-      if (lo + k < hi) sum = __dadd_rn(sum, e[k]);
-  } else if (hi - lo <= kFoldLeaf) {
+  if (hi - lo <= kFoldLeaf) {
     sum = minE[h_mem[lo]];
     uint32_t s = lo + 1;
     for (; s + 4 <= hi; s += 4) {
@@ -231,14 +211,14 @@ __device__ __forceinline__ int hood_body(uint64_t h, const uint32_t* __restrict_
   }
   hist[uint64_t(t % R1) * Hs + h] = sum;
   int ok = 0;
-  if (window) {  // AND over the window (order-free: no side effects, NaN -> 0)
+  if (t >= L) {
     ok = 1;
-#pragma unroll
-    for (int i = 0; i < kWin; ++i)
-      if (i < L && !(fabs(__dsub_rn(sum, prev[i])) < tol)) ok = 0;
-    for (int i = kWin + 1; i <= L; ++i) {
-      const double p = hist[uint64_t((t - i) % R1) * Hs + h];
-      if (!(fabs(__dsub_rn(sum, p)) < tol)) ok = 0;
+    for (int i = 1; i <= L; ++i) {
+      const double prev = hist[uint64_t((t - i) % R1) * Hs + h];
+      if (!(fabs(__dsub_rn(sum, prev)) < tol)) {
+        ok = 0;
+        break;
+      }
     }
   }
   if (flags) flags[uint64_t(t) * Hs + h] = static_cast<uint8_t>(ok);
@@ -729,7 +709,7 @@ __global__ void __launch_bounds__(256)
   for (uint32_t s = 0; s < nseries; ++s) {
     uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
     double* p = partials + leaf_start[s];
-    if (cnt <= kStageDoubles) {
+    if (cnt >= 1 && cnt <= kStageDoubles) {  // (an empty label has no partials at all)
       // the tree levels run in shared memory (one global round trip in total)
       for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) stage[i] = __ldcg(p + i);
       __syncthreads();

@@ -92,6 +92,14 @@ def test_fold_topology_long_runs(ctx, orc):
         p = ctx.update_parameters(labels, E.LabelParams(np.zeros(M), np.ones(M)))
         om, os_ = orc.update_parameters(g.region_mean, labels, np.zeros(M), np.ones(M))
         assert np.array_equal(p.mu, om) and np.array_equal(p.sigma, os_)
+    # empty labels between and after populated ones keep their parameters
+    # (engine.cpp:198-213) and must not disturb their neighbors' folds
+    for used in ([0, 1, 3], [3], [1, 4], [0]):
+        labels = rng.choice(np.array(used, np.uint32), R)
+        prev = E.LabelParams(np.arange(5, dtype=np.float64) + 0.5, np.arange(5, dtype=np.float64) + 2)
+        p = ctx.update_parameters(labels, prev)
+        om, os_ = orc.update_parameters(g.region_mean, labels, prev.mu, prev.sigma)
+        assert np.array_equal(p.mu, om) and np.array_equal(p.sigma, os_), used
 
 
 def test_convergence_and_params_golden(ctx):  # mrf_engine_test.cpp:344-417
