@@ -71,6 +71,8 @@ enum {
   DPMRF_RUN_NO_GRAPH = 16u,     /* launch each EM iteration directly instead of a CUDA graph */
   DPMRF_RUN_PERSISTENT = 32u,   /* one cooperative persistent kernel per MAP loop */
   DPMRF_RUN_STAGED = 64u,       /* shared-memory staged vertex/hood tiles */
+  DPMRF_RUN_CSR = 256u,         /* read the u32 CSR in the MAP kernels instead of the packed
+                                   int16/u16 delta layouts built at preparation */
   DPMRF_RUN_HOST_LOG = 128u     /* host round trip per EM iteration (log(sigma) on the host);
                                    default: EM iterations run back to back on the device with a
                                    correctly rounded device log, verified against the host libm

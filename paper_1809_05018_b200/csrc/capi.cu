@@ -120,6 +120,23 @@ void dpmrf_context::prepare() {
   if (!series_alias) {
     launch_series_offsets(h_off.get(), H, S, s_off_buf.ensure(Hs + 1), prep_tmp, scan, stream);
   }
+  // packed layouts when every neighbor list / hood fits (all grid and brick
+  // oversegmentations do); otherwise the kernels read the CSR directly
+  adj_k = hood_k = 0;
+  if (use_packed && R > 0) {
+    uint32_t* st = prep_err.ensure(4);
+    const uint32_t* so = series_alias ? h_off.get() : s_off_buf.get();
+    launch_pack_stats(g_off.get(), g_nbr.get(), R, so, h_mem.get(), Hs, st, stream);
+    uint32_t hs[4];
+    CK(cudaMemcpyAsync(hs, st, sizeof hs, cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (hs[1] <= 32767u) adj_k = hs[0] <= 4 ? 4 : (hs[0] <= 8 ? 8 : 0);
+    if (hs[3] < 0xFFFFu && Hs > 0) hood_k = hs[2] <= 9 ? 8 : (hs[2] <= 17 ? 16 : 0);
+    if (adj_k) launch_pack_adjacency(g_off.get(), g_nbr.get(), R, adj_k,
+                                     adj_pk.ensure(uint64_t(R) * adj_k), stream);
+    if (hood_k) launch_pack_hoods(so, h_mem.get(), Hs, hood_k, hood_base.ensure(Hs),
+                                  hood_pk.ensure(Hs * hood_k), stream);
+  }
   sync();
 }
 
@@ -138,6 +155,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     if (const char* e = std::getenv("DPMRF_NO_L2_PERSIST")) c->use_l2_persist = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_NO_PDL")) pdl_enabled() = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_HOST_LOG")) c->use_device_loop = e[0] == '0';
+    if (const char* e = std::getenv("DPMRF_CSR")) c->use_packed = e[0] == '0';
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -314,6 +332,12 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     a.ring = full ? map_max : L + 1;
     a.fixed = fixed;
     a.staged = (ctx->use_staged || (o.flags & DPMRF_RUN_STAGED)) ? 1 : 0;
+    const bool packed = !(o.flags & DPMRF_RUN_CSR);
+    a.adj_k = packed ? ctx->adj_k : 0;
+    a.adj_pk = ctx->adj_pk.get();
+    a.hood_k = packed ? ctx->hood_k : 0;
+    a.hood_base = ctx->hood_base.get();
+    a.hood_pk = ctx->hood_pk.get();
     a.terms = ctx->terms.ensure(3 * M);
     double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
     ctx->pin_in_l2(minE2, uint64_t(R) * sizeof(double));
@@ -461,6 +485,10 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       key.p[23] = em_out;
       key.p2[0] = em_hist_d;
       key.p2[1] = a.mean;
+      key.p2[2] = a.adj_pk;
+      key.p2[3] = a.hood_pk;
+      key.p2[4] = a.hood_base;
+      key.layout = a.adj_k * 100 + a.hood_k;
       if (!ctx->graph_valid || std::memcmp(&key, &ctx->graph_key, sizeof key) != 0) {
         ctx->drop_graphs();
         for (int parity = 0; parity < (device_loop ? 1 : 2); ++parity) {

@@ -78,7 +78,8 @@ struct dpmrf_context {
     int32_t L, map_max, fixed, timing, trace, persistent;
     double beta, tol;
     const void* p[24];
-    const void* p2[4];
+    const void* p2[8];
+    int32_t layout;
   };
   bool use_device_loop = true;  // EM iterations back to back on the device (DPMRF_HOST_LOG=1 off)
   dpmrf_b200::DevBuf<double> em_rec, em_hist;
@@ -135,7 +136,14 @@ struct dpmrf_context {
 
   void sync() { CK(cudaStreamSynchronize(stream)); }
   void bind() { CK(cudaSetDevice(device)); }
-  void prepare();  // validate + cover + series offsets (capi.cu)
+  void prepare();  // validate + cover + series offsets + packed layouts (capi.cu)
+
+  // ---- packed static structure (engine.cuh MapArgs::adj_k / hood_k) ----
+  bool use_packed = true;
+  int adj_k = 0, hood_k = 0;
+  dpmrf_b200::DevBuf<int16_t> adj_pk;
+  dpmrf_b200::DevBuf<uint32_t> hood_base;
+  dpmrf_b200::DevBuf<uint16_t> hood_pk;
 };
 
 namespace dpmrf_b200 {

@@ -26,6 +26,15 @@ struct MapArgs {
   int ring;      // rows of the hood-energy ring (L+1, or map_max for the full trace)
   int fixed;     // 1 = no early exit
   int staged;    // 1 = shared-memory staged tiles (default), 0 = one thread per item
+  // Packed static structure (built once by launch_pack_*; k == 0: CSR only).
+  //   adjacency: adj_k (4|8) int16 deltas u - v per vertex, INT16_MIN = none
+  //   hoods: hood_base[h] = first (smallest) member, hood_pk[h*hood_k + j] =
+  //          member(j+1) - base as u16, 0xFFFF = none (members stay ascending)
+  const int16_t* adj_pk;
+  int adj_k;
+  const uint32_t* hood_base;
+  const uint16_t* hood_pk;
+  int hood_k;
   const double* terms;
   double* minE;    // R
   double* hist;    // ring x Hs hood energies
@@ -108,6 +117,15 @@ void launch_validate(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, u
                      const uint32_t* h_off, const uint32_t* h_mem, uint64_t H, uint64_t S,
                      uint32_t* err, uint32_t* empty_hoods, cudaStream_t s);
 void launch_cover(const uint32_t* h_mem, uint64_t S, uint8_t* cover, uint32_t R, cudaStream_t s);
+// Packing: stats[0] = max degree, [1] = max |u - v|, [2] = max hood size,
+// [3] = max (last - first member) over the series hoods.
+void launch_pack_stats(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R,
+                       const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs,
+                       uint32_t* stats, cudaStream_t s);
+void launch_pack_adjacency(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, int k,
+                           int16_t* out, cudaStream_t s);
+void launch_pack_hoods(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, int k,
+                       uint32_t* base, uint16_t* out, cudaStream_t s);
 // Offsets of the nonempty hoods (the runs reduce_by_key sees, engine.cpp:150).
 void launch_series_offsets(const uint32_t* h_off, uint64_t H, uint64_t S, uint32_t* s_off,
                            DevBuf<uint32_t>& tmp, ScanWorkspace& ws, cudaStream_t s);

@@ -60,25 +60,28 @@ def test_fixture_optimize(ctx, name):
     f.check(r)
 
 
-@pytest.mark.parametrize("staged", [False, True])
+@pytest.mark.parametrize("layout", ["packed", "csr", "staged"])
 @pytest.mark.parametrize("persistent", [False, True])
 @pytest.mark.parametrize("graphs", [False, True])
-def test_execution_modes_agree(ctx, persistent, graphs, staged):
+def test_execution_modes_agree(ctx, persistent, graphs, layout):
     # persistent cooperative MAP loop vs two kernels per MAP iteration, each
-    # with and without CUDA-graph replay and shared-memory staging: identical
-    # results and full traces
+    # with and without CUDA-graph replay, over the packed delta layout, the
+    # u32 CSR and shared-memory staging: identical results and full traces
     for name in ("configA_256_grid8", "m5_128_brick8", "configA_252_grid7"):
         f = Fixture(name)
         upload(ctx, f.graph, f.hoods)
         r = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, persistent=persistent,
-                         graphs=graphs, staged=staged)
+                         graphs=graphs, staged=layout == "staged", csr=layout == "csr")
         f.check(r)
         assert r.stats["persistent"] == (1 if persistent else 0)
         assert r.stats["graphs"] == (1 if graphs else 0)
         for level in (E.TRACE_NONE, E.TRACE_EM):
-            r2 = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, persistent=persistent,
-                              graphs=graphs, trace_level=level, kernel_timing=True)
-            assert np.array_equal(r2.labels, r.labels) and np.array_equal(r2.mu, r.mu)
+            for timing in (False, True):  # timing forces the host-log loop
+                r2 = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, persistent=persistent,
+                                  graphs=graphs, trace_level=level, kernel_timing=timing,
+                                  staged=layout == "staged", csr=layout == "csr")
+                assert np.array_equal(r2.labels, r.labels) and np.array_equal(r2.mu, r.mu)
+                assert np.array_equal(r2.sigma, r.sigma)
 
 
 @pytest.mark.parametrize("name", names())
