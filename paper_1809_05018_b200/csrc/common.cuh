@@ -234,14 +234,48 @@ __device__ inline double log_cr(double x) {
   }
   const dd_t f = dd_div({__dsub_rn(m, 1.0), 0.0}, dd_two_sum(m, 1.0));
   const dd_t z = dd_mul(f, f);
-  constexpr int kTerms = 23;
-  auto coef = [](int k) -> dd_t {
-    const double n = 2.0 * k + 1.0;
-    const double hi = __ddiv_rn(1.0, n);
-    return {hi, __ddiv_rn(__fma_rn(-hi, n, 1.0), n)};
+  // 1/(2k+1) as double-doubles (hi = RN(1/n), lo = RN(1/n - hi))
+  constexpr double C[23][2] = {
+      {0x1.0000000000000p+0, 0x0.0p+0},
+      {0x1.5555555555555p-2, 0x1.5555555555555p-56},
+      {0x1.999999999999ap-3, -0x1.999999999999ap-57},
+      {0x1.2492492492492p-3, 0x1.2492492492492p-57},
+      {0x1.c71c71c71c71cp-4, 0x1.c71c71c71c71cp-58},
+      {0x1.745d1745d1746p-4, -0x1.745d1745d1746p-59},
+      {0x1.3b13b13b13b14p-4, -0x1.3b13b13b13b14p-58},
+      {0x1.1111111111111p-4, 0x1.1111111111111p-60},
+      {0x1.e1e1e1e1e1e1ep-5, 0x1.e1e1e1e1e1e1ep-61},
+      {0x1.af286bca1af28p-5, 0x1.af286bca1af28p-59},
+      {0x1.8618618618618p-5, 0x1.8618618618618p-59},
+      {0x1.642c8590b2164p-5, 0x1.642c8590b2164p-60},
+      {0x1.47ae147ae147bp-5, -0x1.eb851eb851eb8p-61},
+      {0x1.2f684bda12f68p-5, 0x1.2f684bda12f68p-59},
+      {0x1.1a7b9611a7b96p-5, 0x1.1a7b9611a7b96p-61},
+      {0x1.0842108421084p-5, 0x1.0842108421084p-60},
+      {0x1.f07c1f07c1f08p-6, -0x1.f07c1f07c1f08p-61},
+      {0x1.d41d41d41d41dp-6, 0x1.0750750750750p-60},
+      {0x1.bacf914c1bad0p-6, -0x1.bacf914c1bad0p-60},
+      {0x1.a41a41a41a41ap-6, 0x1.0690690690690p-60},
+      {0x1.8f9c18f9c18fap-6, -0x1.f3831f3831f38p-61},
+      {0x1.7d05f417d05f4p-6, 0x1.7d05f417d05f4p-62},
+      {0x1.6c16c16c16c17p-6, -0x1.f49f49f49f49fp-61},
   };
-  dd_t S = coef(kTerms - 1);
-  for (int k = kTerms - 2; k >= 0; --k) S = dd_add(dd_mul(S, z), coef(k));
+  // Estrin's scheme (all terms positive: no cancellation): depth 5 instead
+  // of the 22 dependent steps of Horner's rule
+  const dd_t z2 = dd_mul(z, z), z4 = dd_mul(z2, z2), z8 = dd_mul(z4, z4);
+  const dd_t z16 = dd_mul(z8, z8);
+  dd_t p[12];
+#pragma unroll
+  for (int i = 0; i < 11; ++i)
+    p[i] = dd_add({C[2 * i][0], C[2 * i][1]}, dd_mul({C[2 * i + 1][0], C[2 * i + 1][1]}, z));
+  p[11] = {C[22][0], C[22][1]};
+  dd_t q[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) q[j] = dd_add(p[2 * j], dd_mul(p[2 * j + 1], z2));
+  const dd_t r0 = dd_add(q[0], dd_mul(q[1], z4)), r1 = dd_add(q[2], dd_mul(q[3], z4));
+  const dd_t r2 = dd_add(q[4], dd_mul(q[5], z4));
+  const dd_t s0 = dd_add(r0, dd_mul(r1, z8));
+  const dd_t S = dd_add(s0, dd_mul(r2, z16));
   const dd_t lm = dd_mul({__dmul_rn(2.0, f.hi), __dmul_rn(2.0, f.lo)}, S);
   const dd_t ln2 = {0x1.62e42fefa39efp-1, 0x1.abc9e3b39803fp-56};
   const dd_t r = dd_add(dd_mul({static_cast<double>(e), 0.0}, ln2), lm);

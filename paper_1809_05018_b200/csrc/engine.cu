@@ -706,6 +706,55 @@ __global__ void __launch_bounds__(256)
   if (!last) return;
   __threadfence();
   constexpr uint32_t kStageDoubles = kLeavesPerBlock * kLeafStride;
+  auto finish = [&](uint32_t s, double folded) {  // parameters / total energy of series s
+    if (s < M) {
+      if (n[s] != 0) {  // empty labels keep their previous parameters
+        const double count = static_cast<double>(n[s]);
+        if (!kSq) {
+          params[s] = __ddiv_rn(folded, count);
+        } else {
+          const double sd = __dsqrt_rn(__ddiv_rn(folded, count));
+          params[M + s] = sd < kSigmaFloor ? kSigmaFloor : sd;
+        }
+      }
+      if (kSq) {  // the final pass publishes (mu, sigma) of every label
+        em_out[2 + s] = params[s];
+        em_out[2 + M + s] = params[M + s];
+      }
+    } else {
+      // total energy: dpp::reduce(..., 0.0) -> identity only for empty input
+      em_out[0] = (leaf_start[M + 1] == leaf_start[M]) ? 0.0 : folded;
+      em_out[1] = static_cast<double>(unconv ? executed_iters(unconv, map_max, fixed) : 0);
+    }
+  };
+  const uint32_t all_leaves = leaf_start[nseries];
+  if (nseries <= kTileThreads / 32 && all_leaves <= kStageDoubles) {
+    // every series' tree at once: one warp per series in shared memory
+    for (uint32_t i = threadIdx.x; i < all_leaves; i += blockDim.x) stage[i] = __ldcg(partials + i);
+    __syncthreads();
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w < nseries) {
+      double* p = stage + leaf_start[w];
+      uint32_t cnt = leaf_start[w + 1] - leaf_start[w];
+      while (cnt > 1) {
+        const uint32_t pairs = cnt / 2;
+        for (uint32_t base = 0; base < pairs; base += 32) {
+          const uint32_t i = base + lane;
+          const double v = i < pairs ? __dadd_rn(p[2 * i], p[2 * i + 1]) : 0.0;
+          __syncwarp();
+          if (i < pairs) p[i] = v;
+          __syncwarp();
+        }
+        if ((cnt & 1u) && lane == 0) p[pairs] = p[cnt - 1];
+        __syncwarp();
+        cnt = pairs + (cnt & 1u);
+      }
+      if (lane == 0) finish(w, cnt ? p[0] : 0.0);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *done = 0;  // re-arm the ticket for the next launch
+    return;
+  }
   for (uint32_t s = 0; s < nseries; ++s) {
     uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
     double* p = partials + leaf_start[s];
@@ -748,28 +797,7 @@ __global__ void __launch_bounds__(256)
       }
       cnt = pairs + (cnt & 1u);
     }
-    if (threadIdx.x == 0) {
-      const double folded = __ldcg(p);
-      if (s < M) {
-        if (n[s] != 0) {  // empty labels keep their previous parameters
-          const double count = static_cast<double>(n[s]);
-          if (!kSq) {
-            params[s] = __ddiv_rn(folded, count);
-          } else {
-            const double sd = __dsqrt_rn(__ddiv_rn(folded, count));
-            params[M + s] = sd < kSigmaFloor ? kSigmaFloor : sd;
-          }
-        }
-        if (kSq) {  // the final pass publishes (mu, sigma) of every label
-          em_out[2 + s] = params[s];
-          em_out[2 + M + s] = params[M + s];
-        }
-      } else {
-        // total energy: dpp::reduce(..., 0.0) -> identity only for empty input
-        em_out[0] = (leaf_start[M + 1] == leaf_start[M]) ? 0.0 : folded;
-        em_out[1] = static_cast<double>(unconv ? executed_iters(unconv, map_max, fixed) : 0);
-      }
-    }
+    if (threadIdx.x == 0) finish(s, __ldcg(p));
     __syncthreads();
   }
   if (threadIdx.x == 0) *done = 0;  // re-arm the ticket for the next launch
@@ -799,22 +827,12 @@ __global__ void k_em_epilogue(EmEpilogueArgs a) {
     for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < a.R; v += stride)
       a.lab0[v] = a.lab1[v];
   }
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  // warp 0 of block 0: one lane per label evaluates the (long) device log
   const uint32_t e = a.unconv[kEmCount];
   const uint32_t M = a.M;
-  const double total = a.em_out[0];
-  a.em_hist[e] = total;
-  uint32_t conv = 0;
-  if (int(e) + 1 >= a.L + 1) {
-    conv = 1;
-    for (int i = 1; i <= a.L; ++i)
-      if (!(fabs(__dsub_rn(total, a.em_hist[e - i])) < a.tol)) conv = 0;
-  }
   double* rec = a.em_rec + uint64_t(e) * (3 + 3 * M);
-  rec[0] = total;
-  rec[1] = static_cast<double>(T);
-  rec[2] = static_cast<double>(conv);
-  for (uint32_t l = 0; l < M; ++l) {
+  for (uint32_t l = threadIdx.x; l < M; l += 32) {
     const double mu = a.em_out[2 + l], sg = a.em_out[2 + M + l];
     const double ls = log_cr(sg);
     rec[3 + l] = mu;
@@ -824,6 +842,18 @@ __global__ void k_em_epilogue(EmEpilogueArgs a) {
     a.terms[M + l] = __dmul_rn(2.0, __dmul_rn(sg, sg));
     a.terms[2 * M + l] = ls;
   }
+  if (threadIdx.x != 0) return;
+  const double total = a.em_out[0];
+  a.em_hist[e] = total;
+  uint32_t conv = 0;
+  if (int(e) + 1 >= a.L + 1) {
+    conv = 1;
+    for (int i = 1; i <= a.L; ++i)
+      if (!(fabs(__dsub_rn(total, a.em_hist[e - i])) < a.tol)) conv = 0;
+  }
+  rec[0] = total;
+  rec[1] = static_cast<double>(T);
+  rec[2] = static_cast<double>(conv);
   a.unconv[kEmCount] = e + 1;
   if (conv && !a.fixed) a.unconv[kEmPending] = 1;
 }

@@ -52,6 +52,12 @@ int main() {
   cudaMalloc(&sink, 64);
   long long h;
   const int n = 1 << 20;
+  int l2 = 0, persist = 0, window = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, 0);
+  cudaDeviceGetAttribute(&persist, cudaDevAttrMaxPersistingL2CacheSize, 0);
+  cudaDeviceGetAttribute(&window, cudaDevAttrMaxAccessPolicyWindowSize, 0);
+  printf("L2 %d MB, max persisting L2 %d MB, max access-policy window %d MB\n", l2 >> 20,
+         persist >> 20, window >> 20);
   dadd_chain<<<1, 1>>>(d, 1e-9, n, c);
   cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
   printf("dependent DADD: %.2f cycles/op\n", double(h) / n);
