@@ -82,6 +82,13 @@ void init_params(uint32_t M, uint64_t seed, double* mu, double* sigma) {
 
 void dpmrf_b200_set_error(const char* msg) { g_last_error = msg; }
 
+namespace dpmrf_b200 {
+void check_config(const dpmrf_optimizer_config& c, bool multilabel) { validate_config(c, multilabel); }
+void initial_params(uint32_t M, uint64_t seed, double* mu, double* sigma) {
+  init_params(M, seed, mu, sigma);
+}
+}  // namespace dpmrf_b200
+
 // ---- structure preparation ---------------------------------------------------
 void dpmrf_context::prepare() {
   if (prepared) {
@@ -322,6 +329,10 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     a.h_mem = ctx->h_mem.get();
     a.R = R;
     a.Hs = Hs;
+    a.v_begin = 0;
+    a.v_end = R;
+    a.h_begin = 0;
+    a.h_end = Hs;
     a.M = M;
     a.beta = cfg->beta;
     a.tol = cfg->convergence_tol;

@@ -147,6 +147,9 @@ struct dpmrf_context {
 };
 
 namespace dpmrf_b200 {
+// capi.cu
+void check_config(const dpmrf_optimizer_config& c, bool multilabel);  // validate_config
+void initial_params(uint32_t M, uint64_t seed, double* mu, double* sigma);  // init_random
 // hoods.cu
 void build_neighborhoods_device(dpmrf_context* ctx, uint64_t C, const uint32_t* c_off_host,
                                 const uint32_t* c_mem_host);

@@ -153,11 +153,11 @@ __global__ void __launch_bounds__(kVtxThreads)
                     double* __restrict__ minE, uint32_t R, uint32_t M_rt,
                     const double* __restrict__ terms, double beta,
                     const uint32_t* __restrict__ unconv, int t, int fixed,
-                    uint32_t* __restrict__ tile_counts, uint32_t tiles) {
+                    uint32_t* __restrict__ tile_counts, uint32_t tiles, uint32_t v_begin) {
   pdl_wait();
   if (map_iter_skipped(unconv, t, fixed)) return;
-  const uint32_t v = blockIdx.x * kVtxThreads + threadIdx.x;
-  const bool valid = v < R;
+  const uint32_t v = v_begin + blockIdx.x * kVtxThreads + threadIdx.x;
+  const bool valid = v < R;  // R = end of the owned range
   uint32_t lab = 0;
   if (valid) lab = vertex_body<MT>(v, g_off, g_nbr, mean, cover, lab_in, lab_out, minE, M_rt, terms, beta);
   const uint32_t M = MT > 0 ? uint32_t(MT) : M_rt;
@@ -414,11 +414,12 @@ __global__ void __launch_bounds__(kHoodThreads)
     k_hood_sums(const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ h_mem,
                 const double* __restrict__ minE, double* __restrict__ hist,
                 uint8_t* __restrict__ flags, uint64_t Hs, int t, int L, int ring, double tol,
-                uint32_t* __restrict__ unconv, int fixed) {
+                uint32_t* __restrict__ unconv, int fixed, uint64_t h_begin, uint64_t h_end) {
   pdl_wait();
   if (map_iter_skipped(unconv, t, fixed)) return;
-  const uint64_t h = uint64_t(blockIdx.x) * kHoodThreads + threadIdx.x;
-  const int not_conv = hood_body(h, s_off, h_mem, minE, hist, flags, Hs, t, L, ring, tol);
+  const uint64_t h = h_begin + uint64_t(blockIdx.x) * kHoodThreads + threadIdx.x;
+  const int not_conv =
+      h < h_end ? hood_body(h, s_off, h_mem, minE, hist, flags, Hs, t, L, ring, tol) : 0;
   const int block_unconv = __syncthreads_count(not_conv);
   if (threadIdx.x == 0 && block_unconv) atomicAdd(&unconv[t], uint32_t(block_unconv));
 }
@@ -948,7 +949,8 @@ __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t);
 
 void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out, int t,
                           cudaStream_t s) {
-  const dim3 g(grid_for(a.R, kVtxThreads)), blk(kVtxThreads);
+  const dim3 g(grid_for(a.v_end - a.v_begin, kVtxThreads)), blk(kVtxThreads);
+  const bool whole = a.v_begin == 0 && a.v_end == a.R;  // staged path: whole graph only
   if (a.adj_k && !a.staged) {
     if (a.M == 2) {
       if (a.adj_k == 4) launch_pdl(k_vertex_packed<2, 4>, g, blk, 0, s, a, lab_in, lab_out, t);
@@ -959,16 +961,16 @@ void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_
     }
     return;
   }
-  if (a.staged) {
+  if (a.staged && whole) {
     if (a.M == 2)  // M = 2 is specialised; other M share the counted-compare loop
       launch_pdl(k_vertex_staged<2>, g, blk, 0, s, a, lab_in, lab_out, t);
     else
       launch_pdl(k_vertex_staged<0>, g, blk, 0, s, a, lab_in, lab_out, t);
     return;
   }
-#define VA_ARGS                                                                              \
-  a.g_off, a.g_nbr, a.mean, a.cover, lab_in, lab_out, a.minE, a.R, a.M, a.terms, a.beta, \
-      a.unconv, t, a.fixed, a.tile_counts, a.tiles
+#define VA_ARGS                                                                                \
+  a.g_off, a.g_nbr, a.mean, a.cover, lab_in, lab_out, a.minE, a.v_end, a.M, a.terms, a.beta, \
+      a.unconv, t, a.fixed, a.tile_counts, a.tiles, a.v_begin
   switch (a.M) {
     case 2: launch_pdl(k_vertex_argmin<2>, g, blk, 0, s, VA_ARGS); break;
     case 3: launch_pdl(k_vertex_argmin<3>, g, blk, 0, s, VA_ARGS); break;
@@ -983,17 +985,18 @@ void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_
 }
 
 void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s) {
-  const dim3 g(grid_for(a.Hs, kHoodThreads)), blk(kHoodThreads);
+  const dim3 g(grid_for(a.h_end - a.h_begin, kHoodThreads)), blk(kHoodThreads);
+  const bool whole = a.h_begin == 0 && a.h_end == a.Hs;
   if (a.hood_k && !a.staged) {
     if (a.hood_k == 8) launch_pdl(k_hood_packed<8>, g, blk, 0, s, a, t);
     else launch_pdl(k_hood_packed<16>, g, blk, 0, s, a, t);
     return;
   }
-  if (a.staged)
+  if (a.staged && whole)
     launch_pdl(k_hood_staged, g, blk, 0, s, a, t);
   else
     launch_pdl(k_hood_sums, g, blk, 0, s, a.s_off, a.h_mem, (const double*)a.minE, a.hist,
-               a.flags, a.Hs, t, a.L, a.ring, a.tol, a.unconv, a.fixed);
+               a.flags, a.Hs, t, a.L, a.ring, a.tol, a.unconv, a.fixed, a.h_begin, a.h_end);
 }
 
 namespace {
@@ -1031,8 +1034,8 @@ __global__ void __launch_bounds__(kVtxThreads)
   pdl_wait();
   if (map_iter_skipped(a.unconv, t, a.fixed)) return;
   const uint32_t M = MT > 0 ? uint32_t(MT) : a.M;
-  const uint32_t v = blockIdx.x * kVtxThreads + threadIdx.x;
-  const bool valid = v < a.R;
+  const uint32_t v = a.v_begin + blockIdx.x * kVtxThreads + threadIdx.x;
+  const bool valid = v < a.v_end;
   uint32_t nl = 0;
   if (valid) {
     int16_t d[K];
@@ -1094,9 +1097,9 @@ __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) 
   static_assert(K == 8 || K == 16, "hood pack width");
   pdl_wait();
   if (map_iter_skipped(a.unconv, t, a.fixed)) return;
-  const uint64_t h = uint64_t(blockIdx.x) * kHoodThreads + threadIdx.x;
+  const uint64_t h = a.h_begin + uint64_t(blockIdx.x) * kHoodThreads + threadIdx.x;
   int not_conv = 0;
-  if (h < a.Hs) {
+  if (h < a.h_end) {
     const uint32_t base = a.hood_base[h];
     uint32_t u[K / 2];
     const uint4* src = reinterpret_cast<const uint4*>(a.hood_pk + h * K);
@@ -1316,9 +1319,9 @@ uint32_t label_tiles(uint32_t R) {
 void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
                   const uint8_t* lab_odd, const double* hist, uint64_t Hs, int ring,
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
-                  MStepBuffers& mb, cudaStream_t s, uint64_t* launches) {
+                  MStepBuffers& mb, cudaStream_t s, uint64_t* launches, bool counts_ready) {
   mstep_core(mean, R, M, lab_even, lab_odd, unconv, map_max, fixed, hist, Hs, ring, params,
-             em_out, mb, s, launches, /*counts_ready=*/true);
+             em_out, mb, s, launches, counts_ready);
 }
 
 void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s) {

@@ -35,6 +35,10 @@ struct MapArgs {
   const uint32_t* hood_base;
   const uint16_t* hood_pk;
   int hood_k;
+  // Owned ranges (vertex-range partitioning; [0,R) and [0,Hs) on one GPU).
+  // Arrays stay globally indexed; v_begin is a multiple of 256.
+  uint32_t v_begin, v_end;
+  uint64_t h_begin, h_end;
   const double* terms;
   double* minE;    // R
   double* hist;    // ring x Hs hood energies
@@ -75,7 +79,8 @@ struct MStepBuffers {
 void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
                   const uint8_t* lab_odd, const double* hist, uint64_t Hs, int ring,
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
-                  MStepBuffers& mb, cudaStream_t s, uint64_t* launches);
+                  MStepBuffers& mb, cudaStream_t s, uint64_t* launches,
+                  bool counts_ready = true);
 
 // Device-resident EM loop (see engine.cu).  unconv points 4 words into its
 // allocation: [em_done, pending_done, em_count, pad | unconv[map_max]].
