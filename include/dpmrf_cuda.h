@@ -200,6 +200,45 @@ dpmrf_status dpmrf_update_parameters(dpmrf_context* ctx, const uint32_t* labels,
                                      uint32_t num_labels, const double* prev_mu,
                                      const double* prev_sigma, double* mu, double* sigma);
 
+/* ---- vertex-range partitioned optimize (one giant slice, config D) --------
+ * One region graph split into `world` contiguous vertex ranges (multiples of
+ * 256) and as many series ranges; every partition holds the whole static
+ * structure (the context's graph + hoods) but computes only its own ranges.
+ * Per MAP iteration the partitions exchange the label and minimum-energy
+ * halos their neighbors / hoods read and sum the unconverged-hood counters;
+ * per EM iteration they allgather the committed labels and the hood-energy
+ * row, and every partition runs the same M-step.  Results are bit-identical
+ * to dpmrf_optimize on one device (optimize.cpp:31-74).  Trace levels NONE and
+ * EM only.
+ *   NCCL group: one process per GPU; rank 0 calls dpmrf_nccl_unique_id and
+ *     ships the 128 bytes to the others (e.g. torch.distributed), then every
+ *     rank calls dpmrf_group_create_nccl with its own context.  libnccl.so.2
+ *     is loaded at run time.
+ *   Local group: all partitions inside one context on one device, halos moved
+ *     by device copies -- the same schedule without NVLink (tests).          */
+typedef struct dpmrf_group dpmrf_group;
+dpmrf_status dpmrf_nccl_unique_id(uint8_t id[128]);
+dpmrf_status dpmrf_group_create_nccl(dpmrf_context* ctx, const uint8_t id[128], int rank,
+                                     int world, dpmrf_group** out);
+dpmrf_status dpmrf_group_create_local(dpmrf_context* ctx, int world, dpmrf_group** out);
+void dpmrf_group_destroy(dpmrf_group* group);
+/* Halo statistics of the last partitioned optimize: per-MAP-iteration bytes
+ * this rank sends (local group: all partitions), vertex/series range. */
+typedef struct dpmrf_group_info {
+  int32_t world;
+  int32_t rank;              /* -1 for a local group */
+  uint32_t vertex_begin, vertex_end;
+  uint64_t series_begin, series_end;
+  uint64_t halo_bytes_per_map;  /* labels + minima sent per MAP iteration */
+  uint64_t gather_bytes_per_em; /* labels + hood row received per EM iteration */
+} dpmrf_group_info;
+dpmrf_status dpmrf_group_info_get(dpmrf_group* group, dpmrf_group_info* out);
+/* Same outputs as dpmrf_optimize on every rank (labels: all R vertices).
+ * Stats / EM trace land on the group's context. */
+dpmrf_status dpmrf_optimize_partitioned(dpmrf_group* group, const dpmrf_optimizer_config* config,
+                                        const dpmrf_run_options* options, uint32_t* labels,
+                                        double* mu, double* sigma);
+
 /* ---- diagnostics ---------------------------------------------------------- */
 /* The device's correctly rounded natural log used by the device-resident EM
  * loop for log(sigma) (n values, host buffers). */

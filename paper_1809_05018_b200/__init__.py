@@ -11,6 +11,6 @@ from .engine import (Backend, CliqueSet, Context, CudaError, EmIterationLog, Inp
                      TRACE_EM, TRACE_FULL, TRACE_NONE, build_neighborhoods, check_convergence,
                      compute_energies, discord_counts, init_random, min_label_energies,
                      neighborhood_energy_sums, optimize, replicate_by_label, slot_hood_map,
-                     update_labels, update_parameters)
+                     update_labels, update_parameters, PartitionGroup, nccl_unique_id)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -47,6 +47,14 @@ class CRunStats(ct.Structure):
                 ("device_log_fallbacks", U32)]
 
 
+class CGroupInfo(ct.Structure):
+    """dpmrf_group_info."""
+
+    _fields_ = [("world", I32), ("rank", I32), ("vertex_begin", U32), ("vertex_end", U32),
+                ("series_begin", U64), ("series_end", U64), ("halo_bytes_per_map", U64),
+                ("gather_bytes_per_em", U64)]
+
+
 # (name, restype, argtypes) of every C ABI entry point (include/dpmrf_cuda.h)
 CUDA_API = [
     ("dpmrf_context_create", ST, [INT, ct.POINTER(VP)]),
@@ -74,6 +82,13 @@ CUDA_API = [
     ("dpmrf_update_labels", ST, [VP, VP, U32, VP, VP]),
     ("dpmrf_update_parameters", ST, [VP, VP, U32, VP, VP, VP, VP]),
     ("dpmrf_debug_log", ST, [VP, U64, VP, VP]),
+    ("dpmrf_nccl_unique_id", ST, [VP]),
+    ("dpmrf_group_create_nccl", ST, [VP, VP, INT, INT, ct.POINTER(VP)]),
+    ("dpmrf_group_create_local", ST, [VP, INT, ct.POINTER(VP)]),
+    ("dpmrf_group_destroy", None, [VP]),
+    ("dpmrf_group_info_get", ST, [VP, VP]),
+    ("dpmrf_optimize_partitioned", ST, [VP, ct.POINTER(CConfig), ct.POINTER(CRunOptions), VP, VP,
+                                        VP]),
 ]
 
 INPUTS_API = [

@@ -217,6 +217,7 @@ extern "C" dpmrf_status dpmrf_set_graph(dpmrf_context* ctx, uint32_t R, const ui
     ctx->A = A;
     ctx->has_graph = true;
     ctx->prepared = false;
+    ++ctx->generation;
     ctx->sync();
   });
 }
@@ -240,6 +241,7 @@ extern "C" dpmrf_status dpmrf_set_hoods(dpmrf_context* ctx, uint64_t H, const ui
     ctx->S = S;
     ctx->has_hoods = true;
     ctx->prepared = false;
+    ++ctx->generation;
     ctx->sync();
   });
 }
@@ -255,6 +257,7 @@ extern "C" dpmrf_status dpmrf_build_neighborhoods(dpmrf_context* ctx, uint64_t C
     build_neighborhoods_device(ctx, C, c_off, c_mem);
     ctx->has_hoods = true;
     ctx->prepared = false;
+    ++ctx->generation;
     if (num_slots) *num_slots = ctx->S;
   });
 }

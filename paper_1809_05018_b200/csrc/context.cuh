@@ -24,6 +24,7 @@ struct dpmrf_context {
 
   // ---- derived per (graph, hoods) pair, built lazily on the device ----
   bool prepared = false;
+  uint64_t generation = 0;         // bumped whenever the graph or hoods change
   dpmrf_status prep_status = DPMRF_OK;
   std::string prep_msg;
   uint64_t Hs = 0;                 // nonempty hoods = reduce_by_key runs

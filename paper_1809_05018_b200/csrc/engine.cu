@@ -859,6 +859,26 @@ __global__ void k_em_epilogue(EmEpilogueArgs a) {
   if (conv && !a.fixed) a.unconv[kEmPending] = 1;
 }
 
+// Partitioned optimize: this partition's share of the committed labels and of
+// the last executed MAP iteration's hood-energy row, copied into the buffers
+// the per-EM allgather assembles (the M-step then reads them as if the run
+// were on one device).
+__global__ void k_partition_select(const uint8_t* lab_even, const uint8_t* lab_odd,
+                                   const double* hist, int ring, uint64_t Hs,
+                                   const uint32_t* unconv, int map_max, int fixed, uint32_t vb,
+                                   uint32_t ve, uint64_t hb, uint64_t he, uint8_t* lab_full,
+                                   double* row_full) {
+  pdl_wait();
+  if (em_skipped(unconv)) return;
+  const int T = executed_iters(unconv, map_max, fixed);
+  const uint8_t* lab = (T & 1) ? lab_odd : lab_even;
+  const double* row = hist + uint64_t((T - 1) % ring) * Hs;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (uint64_t v = vb + i0; v < ve; v += stride) lab_full[v] = lab[v];
+  for (uint64_t h = hb + i0; h < he; h += stride) row_full[h] = row[h];
+}
+
 __global__ void k_log_cr(const double* x, double* out, uint64_t n) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) out[i] = log_cr(x[i]);
@@ -1331,6 +1351,16 @@ void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s) {
 void launch_em_epilogue(const EmEpilogueArgs& a, cudaStream_t s) {
   const unsigned g = std::min<unsigned>(grid_for(a.R ? a.R : 1, 256), 4 * kNumSMs);
   launch_pdl(k_em_epilogue, dim3(g), dim3(256), 0, s, a);
+}
+
+void launch_partition_select(const uint8_t* lab_even, const uint8_t* lab_odd, const double* hist,
+                             int ring, uint64_t Hs, const uint32_t* unconv, int map_max, int fixed,
+                             uint32_t vb, uint32_t ve, uint64_t hb, uint64_t he,
+                             uint8_t* lab_full, double* row_full, cudaStream_t s) {
+  const uint64_t n = std::max<uint64_t>(ve - vb, he - hb);
+  const unsigned g = std::min<unsigned>(grid_for(n ? n : 1, 256), 4 * kNumSMs);
+  launch_pdl(k_partition_select, dim3(g), dim3(256), 0, s, lab_even, lab_odd, hist, ring, Hs,
+             unconv, map_max, fixed, vb, ve, hb, he, lab_full, row_full);
 }
 
 void launch_log_cr(const double* x, double* out, uint64_t n, cudaStream_t s) {

@@ -101,6 +101,12 @@ struct EmEpilogueArgs {
 };
 void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s);
 void launch_em_epilogue(const EmEpilogueArgs& a, cudaStream_t s);
+// Partitioned optimize: own vertex / series range of the final labels and of
+// the last executed hood-energy row into the allgather buffers.
+void launch_partition_select(const uint8_t* lab_even, const uint8_t* lab_odd, const double* hist,
+                             int ring, uint64_t Hs, const uint32_t* unconv, int map_max, int fixed,
+                             uint32_t vb, uint32_t ve, uint64_t hb, uint64_t he,
+                             uint8_t* lab_full, double* row_full, cudaStream_t s);
 // log_cr over n values (diagnostics / tests of the device log).
 void launch_log_cr(const double* x, double* out, uint64_t n, cudaStream_t s);
 

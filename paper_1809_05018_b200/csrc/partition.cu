@@ -1,0 +1,814 @@
+// partition.cu -- vertex-range partitioned optimize (one giant slice over
+// several GPUs).
+//
+// The reference runs optimize() (proj/src/mrf/optimize.cpp:31-74) over one
+// address space.  Here the region graph is cut into `world` contiguous vertex
+// ranges (row bands of the superpixel grid; multiples of the 256-vertex tile)
+// and the series (nonempty hoods) into as many contiguous ranges.  Every
+// partition keeps the whole static structure resident (it is small next to
+// 180 GB) and the per-vertex / per-series arrays globally indexed, but runs
+// the MAP kernels only over what it owns:
+//
+//   per MAP iteration t        vertex pass (own vertices)
+//                              halo: labels + minima its neighbors' owners /
+//                                    hoods need (exact [lo, hi] windows per
+//                                    (source, destination) pair, planned once)
+//                              hood pass (own series)
+//                              sum of the unconverged-hood counters
+//   per EM iteration           own labels / own hood-energy row -> allgather
+//                              the same M-step + EM bookkeeping everywhere
+//
+// Everything runs in stream order with the device-side early exit of the
+// single-GPU path (skipped iterations still move their -- stale but never
+// read -- halos, so the schedule is static and capturable).  The allgathered
+// labels and row make the M-step input identical to the one-device run, so
+// the results are bit-identical to dpmrf_optimize.
+//
+// Transports: NCCL (one process per GPU; libnccl.so.2 loaded at run time,
+// grouped ncclSend/ncclRecv for the halos, ncclAllReduce for the counters,
+// in-place ncclAllGather per EM) or local (all partitions in one context on
+// one device; device-to-device copies and a counter-sum kernel -- the same
+// schedule without NVLink, which is how one GPU tests the partition logic).
+#include <dlfcn.h>
+#include <nccl.h>  // types and enums only; every symbol comes from dlsym
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "context.cuh"
+
+using namespace dpmrf_b200;
+
+void dpmrf_b200_set_error(const char* msg);
+
+namespace {
+
+constexpr int kMaxParts = 64;
+
+// ---- NCCL, resolved at run time ------------------------------------------------
+struct Nccl {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+  static Nccl& get() {
+    static Nccl n;
+    if (!n.lib) n.load();
+    return n;
+  }
+  void load() {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) fail(DPMRF_NCCL_ERROR, std::string("cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* name) {
+      void* p = dlsym(h, name);
+      if (!p) fail(DPMRF_NCCL_ERROR, std::string("libnccl.so.2 lacks ") + name);
+      return p;
+    };
+    GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(sym("ncclGetUniqueId"));
+    CommInitRank = reinterpret_cast<decltype(CommInitRank)>(sym("ncclCommInitRank"));
+    CommDestroy = reinterpret_cast<decltype(CommDestroy)>(sym("ncclCommDestroy"));
+    AllReduce = reinterpret_cast<decltype(AllReduce)>(sym("ncclAllReduce"));
+    AllGather = reinterpret_cast<decltype(AllGather)>(sym("ncclAllGather"));
+    Send = reinterpret_cast<decltype(Send)>(sym("ncclSend"));
+    Recv = reinterpret_cast<decltype(Recv)>(sym("ncclRecv"));
+    GroupStart = reinterpret_cast<decltype(GroupStart)>(sym("ncclGroupStart"));
+    GroupEnd = reinterpret_cast<decltype(GroupEnd)>(sym("ncclGroupEnd"));
+    GetErrorString = reinterpret_cast<decltype(GetErrorString)>(sym("ncclGetErrorString"));
+    lib = h;
+  }
+  void check(ncclResult_t r, const char* what) const {
+    if (r != ncclSuccess)
+      fail(DPMRF_NCCL_ERROR, std::string(what) + " failed: " + GetErrorString(r));
+  }
+};
+#define NK(call) nccl.check((call), #call)
+
+// ---- halo plan ----------------------------------------------------------------------
+struct Bounds {
+  int W;
+  uint32_t vb[kMaxParts + 1];
+  uint64_t hb[kMaxParts + 1];
+};
+
+__device__ __forceinline__ int part_of_vertex(const Bounds& b, uint32_t v) {
+  int lo = 0, hi = b.W - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (b.vb[mid] <= v) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int part_of_series(const Bounds& b, uint64_t h) {
+  int lo = 0, hi = b.W - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (b.hb[mid] <= h) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// win[(s * W + d) * 4 + {0,1}] = [lo, hi] of the source-s vertices whose labels
+// destination d's vertex pass reads (discord over neighbors, engine.cpp:74-86);
+// {2,3} = the source-s vertices whose minima d's hood pass folds.
+__global__ void k_halo_plan(Bounds b, const uint32_t* __restrict__ g_off,
+                            const uint32_t* __restrict__ g_nbr, uint32_t R,
+                            const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ h_mem,
+                            uint64_t Hs, uint32_t* win) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (uint64_t v = i0; v < R; v += stride) {
+    const int d = part_of_vertex(b, uint32_t(v));
+    for (uint32_t a = g_off[v]; a < g_off[v + 1]; ++a) {
+      const uint32_t u = g_nbr[a];
+      const int s = part_of_vertex(b, u);
+      if (s == d) continue;
+      atomicMin(&win[(s * b.W + d) * 4 + 0], u);
+      atomicMax(&win[(s * b.W + d) * 4 + 1], u);
+    }
+  }
+  for (uint64_t h = i0; h < Hs; h += stride) {
+    const int d = part_of_series(b, h);
+    for (uint32_t j = s_off[h]; j < s_off[h + 1]; ++j) {
+      const uint32_t m = h_mem[j];
+      const int s = part_of_vertex(b, m);
+      if (s == d) continue;
+      atomicMin(&win[(s * b.W + d) * 4 + 2], m);
+      atomicMax(&win[(s * b.W + d) * 4 + 3], m);
+    }
+  }
+}
+
+__global__ void k_win_init(uint32_t* win, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) win[i] = (i & 1) ? 0u : 0xFFFFFFFFu;
+}
+
+// Local transport: the sum of every partition's counter t, written back to all.
+struct CounterPtrs {
+  uint32_t* p[kMaxParts];
+};
+__global__ void k_sum_counters(CounterPtrs c, int W, int t) {
+  pdl_wait();
+  if (threadIdx.x != 0) return;
+  uint32_t s = 0;
+  for (int r = 0; r < W; ++r) s += c.p[r][t];
+  for (int r = 0; r < W; ++r) c.p[r][t] = s;
+}
+
+// ---- per-partition device state ---------------------------------------------------
+struct Part {
+  int r = 0;
+  uint32_t vb = 0, ve = 0;
+  uint64_t hb = 0, he = 0;
+  DevBuf<uint8_t> lab[2], lab_full;
+  DevBuf<double> minE, hist, row_full, params, em_out, terms, em_rec, em_hist;
+  DevBuf<uint32_t> state;  // [em_done, pending, em_count, pad | unconv[map_max]]
+  MStepBuffers ms;
+  MapArgs a{};
+  EmEpilogueArgs ep{};
+};
+
+struct Window {
+  uint32_t lo, hi;
+  bool empty() const { return lo > hi; }
+  uint64_t count() const { return empty() ? 0 : uint64_t(hi) - lo + 1; }
+};
+
+}  // namespace
+
+struct dpmrf_group {
+  dpmrf_context* ctx = nullptr;
+  int world = 1;
+  int rank = -1;  // -1: local group (every partition in this process)
+  ncclComm_t comm = nullptr;
+  std::vector<std::unique_ptr<Part>> parts;
+  // plan (per structure generation)
+  bool planned = false;
+  uint64_t plan_gen = 0;
+  uint32_t chunkV = 0;
+  uint64_t chunkH = 0;
+  std::vector<Window> lab_win, min_win;  // [s * W + d]
+  uint64_t halo_bytes = 0, gather_bytes = 0;
+  // CUDA graph of one EM iteration (device loop; local groups)
+  bool use_graph = true;
+  std::vector<uint64_t> graph_key;
+  cudaGraphExec_t graph = nullptr;
+  uint64_t graph_kernels = 0;
+  void drop_graph() {
+    if (graph) cudaGraphExecDestroy(graph);
+    graph = nullptr;
+    graph_key.clear();
+  }
+  bool local() const { return rank < 0; }
+};
+
+namespace {
+
+template <class F>
+dpmrf_status guarded(F&& f) {
+  try {
+    f();
+    return DPMRF_OK;
+  } catch (const Error& e) {
+    dpmrf_b200_set_error(e.what());
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    dpmrf_b200_set_error("host allocation failed");
+    return DPMRF_INTERNAL_ERROR;
+  } catch (const std::exception& e) {
+    dpmrf_b200_set_error(e.what());
+    return DPMRF_INTERNAL_ERROR;
+  }
+}
+
+void need(bool c, dpmrf_status s, const char* m) {
+  if (!c) fail(s, m);
+}
+
+// Ranges + halo windows for the context's current structure.
+void plan(dpmrf_group* g) {
+  dpmrf_context* ctx = g->ctx;
+  ctx->prepare();
+  if (g->planned && g->plan_gen == ctx->generation) return;
+  const int W = g->world;
+  const uint32_t R = ctx->R;
+  const uint64_t Hs = ctx->Hs;
+  // vertex ranges: equal multiples of the 256-vertex tile (row bands of the
+  // row-major superpixel grid); series ranges: equal multiples of the
+  // 1024-element fold leaf.  Equal chunks make the allgathers plain
+  // in-place ncclAllGather calls (the last chunk is padded).
+  const uint64_t cv = (uint64_t(R) + W - 1) / W;
+  g->chunkV = static_cast<uint32_t>(std::max<uint64_t>(256, (cv + 255) / 256 * 256));
+  const uint64_t ch = (Hs + W - 1) / W;
+  g->chunkH = std::max<uint64_t>(kFoldLeaf, (ch + kFoldLeaf - 1) / kFoldLeaf * kFoldLeaf);
+  Bounds b{};
+  b.W = W;
+  for (int r = 0; r <= W; ++r) {
+    b.vb[r] = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(r) * g->chunkV, R));
+    b.hb[r] = std::min<uint64_t>(uint64_t(r) * g->chunkH, Hs);
+  }
+  for (auto& p : g->parts) {
+    p->vb = b.vb[p->r];
+    p->ve = b.vb[p->r + 1];
+    p->hb = b.hb[p->r];
+    p->he = b.hb[p->r + 1];
+  }
+  const int nwin = W * W * 4;
+  uint32_t* win = ctx->tmp_u32[5].ensure(nwin);
+  cudaStream_t st = ctx->stream;
+  k_win_init<<<grid_for(nwin, 256), 256, 0, st>>>(win, nwin);
+  CK_LAUNCH();
+  const uint32_t* s_off = ctx->series_alias ? ctx->h_off.get() : ctx->s_off_buf.get();
+  const uint64_t n = std::max<uint64_t>(R, Hs);
+  const unsigned grid = std::min<unsigned>(grid_for(n ? n : 1, 256), 8 * kNumSMs);
+  k_halo_plan<<<grid, 256, 0, st>>>(b, ctx->g_off.get(), ctx->g_nbr.get(), R, s_off,
+                                    ctx->h_mem.get(), Hs, win);
+  CK_LAUNCH();
+  std::vector<uint32_t> hw(nwin);
+  CK(cudaMemcpyAsync(hw.data(), win, nwin * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+  g->lab_win.assign(W * W, Window{1, 0});
+  g->min_win.assign(W * W, Window{1, 0});
+  g->halo_bytes = 0;
+  for (int s = 0; s < W; ++s)
+    for (int d = 0; d < W; ++d) {
+      const int i = s * W + d;
+      g->lab_win[i] = Window{hw[i * 4 + 0], hw[i * 4 + 1]};
+      g->min_win[i] = Window{hw[i * 4 + 2], hw[i * 4 + 3]};
+      if (g->local() || s == g->rank)
+        g->halo_bytes += g->lab_win[i].count() + 8 * g->min_win[i].count();
+    }
+  const int mine = g->local() ? 0 : g->rank;
+  (void)mine;
+  g->gather_bytes = g->local()
+                        ? uint64_t(W) * (W - 1) * (g->chunkV + 8 * g->chunkH)
+                        : uint64_t(W - 1) * (g->chunkV + 8 * g->chunkH);
+  g->planned = true;
+  g->plan_gen = ctx->generation;
+  g->drop_graph();
+}
+
+// ---- the schedule --------------------------------------------------------------
+// Labels (u8, buffer b) and minima of iteration t's vertex pass to the
+// partitions that read them.
+void exchange_halo(dpmrf_group* g, int b, cudaStream_t st) {
+  const int W = g->world;
+  if (W == 1) return;
+  if (g->local()) {
+    for (int s = 0; s < W; ++s)
+      for (int d = 0; d < W; ++d) {
+        if (s == d) continue;
+        const Window lw = g->lab_win[s * W + d], mw = g->min_win[s * W + d];
+        Part& ps = *g->parts[s];
+        Part& pd = *g->parts[d];
+        if (!lw.empty())
+          CK(cudaMemcpyAsync(pd.lab[b].get() + lw.lo, ps.lab[b].get() + lw.lo, lw.count(),
+                             cudaMemcpyDeviceToDevice, st));
+        if (!mw.empty())
+          CK(cudaMemcpyAsync(pd.minE.get() + mw.lo, ps.minE.get() + mw.lo, 8 * mw.count(),
+                             cudaMemcpyDeviceToDevice, st));
+      }
+    return;
+  }
+  Nccl& nccl = Nccl::get();
+  Part& p = *g->parts[0];
+  const int me = g->rank;
+  NK(nccl.GroupStart());
+  for (int o = 0; o < W; ++o) {
+    if (o == me) continue;
+    const Window ls = g->lab_win[me * W + o], ms = g->min_win[me * W + o];  // me -> o
+    const Window lr = g->lab_win[o * W + me], mr = g->min_win[o * W + me];  // o -> me
+    if (!ls.empty())
+      NK(nccl.Send(p.lab[b].get() + ls.lo, ls.count(), ncclUint8, o, g->comm, st));
+    if (!ms.empty())
+      NK(nccl.Send(p.minE.get() + ms.lo, ms.count(), ncclFloat64, o, g->comm, st));
+    if (!lr.empty())
+      NK(nccl.Recv(p.lab[b].get() + lr.lo, lr.count(), ncclUint8, o, g->comm, st));
+    if (!mr.empty())
+      NK(nccl.Recv(p.minE.get() + mr.lo, mr.count(), ncclFloat64, o, g->comm, st));
+  }
+  NK(nccl.GroupEnd());
+}
+
+// Unconverged-hood counter of iteration t summed over the partitions, so the
+// early exit (optimize.cpp:59) is decided on the whole slice.
+void sum_counters(dpmrf_group* g, int t, cudaStream_t st, uint64_t* k) {
+  const int W = g->world;
+  if (W == 1) return;
+  if (g->local()) {
+    CounterPtrs c{};
+    for (int r = 0; r < W; ++r) c.p[r] = g->parts[r]->a.unconv;
+    launch_pdl(k_sum_counters, dim3(1), dim3(32), 0, st, c, W, t);
+    ++*k;
+    return;
+  }
+  Nccl& nccl = Nccl::get();
+  uint32_t* u = g->parts[0]->a.unconv + t;
+  NK(nccl.AllReduce(u, u, 1, ncclUint32, ncclSum, g->comm, st));
+}
+
+// Committed labels and the last hood-energy row, assembled on every partition.
+void allgather(dpmrf_group* g, cudaStream_t st) {
+  const int W = g->world;
+  if (W == 1) return;
+  const uint64_t cv = g->chunkV, chh = g->chunkH;
+  if (g->local()) {
+    for (int s = 0; s < W; ++s)
+      for (int d = 0; d < W; ++d) {
+        if (s == d) continue;
+        Part& ps = *g->parts[s];
+        Part& pd = *g->parts[d];
+        CK(cudaMemcpyAsync(pd.lab_full.get() + s * cv, ps.lab_full.get() + s * cv, cv,
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(pd.row_full.get() + s * chh, ps.row_full.get() + s * chh, 8 * chh,
+                           cudaMemcpyDeviceToDevice, st));
+      }
+    return;
+  }
+  Nccl& nccl = Nccl::get();
+  Part& p = *g->parts[0];
+  const int me = g->rank;
+  NK(nccl.GroupStart());
+  NK(nccl.AllGather(p.lab_full.get() + me * cv, p.lab_full.get(), cv, ncclUint8, g->comm, st));
+  NK(nccl.AllGather(p.row_full.get() + me * chh, p.row_full.get(), chh, ncclFloat64, g->comm, st));
+  NK(nccl.GroupEnd());
+}
+
+bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dpmrf_run_options& o,
+                     bool device_loop, uint32_t* labels_out, double* mu_out, double* sigma_out) {
+  dpmrf_context* ctx = g->ctx;
+  const int fixed = (o.flags & DPMRF_RUN_FIXED_WORK) ? 1 : 0;
+  cudaStream_t st = ctx->stream;
+  const uint32_t M = cfg->num_labels;
+  const uint32_t R = ctx->R;
+  const int L = cfg->convergence_window;
+  const int map_max = cfg->map_max_iters;
+  const int em_max = cfg->em_max_iters;
+  const int W = g->world;
+
+  ctx->trace.clear();
+  ctx->trace_level = o.trace_level;
+  ctx->trace_M = M;
+  const uint32_t fallbacks = ctx->stats.device_log_fallbacks;
+  ctx->stats = dpmrf_run_stats{};
+  ctx->stats.device_log_fallbacks = fallbacks;
+  ctx->stats.device_loop = device_loop;
+  uint64_t launches = 0;
+
+  std::vector<double> mu(M), sigma(M);
+  initial_params(M, cfg->rng_seed, mu.data(), sigma.data());
+  plan(g);  // (also prepares the structure)
+  const uint64_t Hs = ctx->Hs;
+  const uint64_t padV = uint64_t(g->chunkV) * W, padH = g->chunkH * W;
+  const uint64_t rec_stride = 3 + 3 * uint64_t(M);
+  const int ring = L + 1;
+  const bool packed = !(o.flags & DPMRF_RUN_CSR);
+  for (auto& pp : g->parts) {
+    Part& p = *pp;
+    p.lab[0].ensure(padV);
+    p.lab[1].ensure(padV);
+    p.lab_full.ensure(padV);
+    MapArgs& a = p.a;
+    a = MapArgs{};
+    a.g_off = ctx->g_off.get();
+    a.g_nbr = ctx->g_nbr.get();
+    a.mean = ctx->g_mean.get();
+    a.cover = ctx->cover.get();
+    a.s_off = ctx->series_alias ? ctx->h_off.get() : ctx->s_off_buf.get();
+    a.h_mem = ctx->h_mem.get();
+    a.R = R;
+    a.Hs = Hs;
+    a.v_begin = p.vb;
+    a.v_end = p.ve;
+    a.h_begin = p.hb;
+    a.h_end = p.he;
+    a.M = M;
+    a.beta = cfg->beta;
+    a.tol = cfg->convergence_tol;
+    a.L = L;
+    a.ring = ring;
+    a.fixed = fixed;
+    a.staged = 0;
+    a.adj_k = packed ? ctx->adj_k : 0;
+    a.adj_pk = ctx->adj_pk.get();
+    a.hood_k = packed ? ctx->hood_k : 0;
+    a.hood_base = ctx->hood_base.get();
+    a.hood_pk = ctx->hood_pk.get();
+    a.terms = p.terms.ensure(3 * M);
+    a.minE = p.minE.ensure(R ? R : 1);
+    a.hist = p.hist.ensure(uint64_t(ring) * (Hs ? Hs : 1));
+    a.flags = nullptr;
+    uint32_t* state = p.state.ensure(uint64_t(map_max) + 4);
+    a.unconv = state + 4;
+    a.tile_counts = nullptr;  // the M-step counts the gathered labels itself
+    a.tiles = label_tiles(R);
+    p.row_full.ensure(padH);
+    p.params.ensure(2 * M);
+    p.em_out.ensure(2 + 2 * M);
+    p.em_rec.ensure(uint64_t(em_max ? em_max : 1) * rec_stride);
+    p.em_hist.ensure(uint64_t(em_max ? em_max : 1));
+    mstep_reserve(p.ms, R, M, Hs);
+    EmEpilogueArgs& ep = p.ep;
+    ep = EmEpilogueArgs{};
+    ep.unconv = a.unconv;
+    ep.map_max = map_max;
+    ep.fixed = fixed;
+    ep.L = L;
+    ep.tol = cfg->convergence_tol;
+    ep.lab0 = p.lab[0].get();
+    ep.lab1 = p.lab[1].get();
+    ep.R = R;
+    ep.M = M;
+    ep.em_out = p.em_out.get();
+    ep.em_hist = p.em_hist.get();
+    ep.em_rec = p.em_rec.get();
+    ep.terms = p.terms.get();
+  }
+  double* h_terms = ctx->h_terms.ensure(3 * M);
+  double* h_em = ctx->h_em.ensure(2 + 2 * M);
+  double* h_rec = ctx->h_rec.ensure(uint64_t(em_max ? em_max : 1) * rec_stride + 4);
+
+  CK(cudaEventRecord(ctx->ev_begin, st));
+  for (auto& pp : g->parts) {
+    Part& p = *pp;
+    launch_init_labels(p.lab[0].get(), R, M, cfg->rng_seed, st);  // every rank: all R labels
+    ++launches;
+    CK(cudaMemsetAsync(p.state.get(), 0, 4 * sizeof(uint32_t), st));
+    CK(cudaMemcpyAsync(p.params.get(), mu.data(), M * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(p.params.get() + M, sigma.data(), M * 8, cudaMemcpyHostToDevice, st));
+  }
+  const uint8_t* result = g->parts[0]->lab[0].get();  // em_max == 0: the initial labels
+
+  if (em_max > 0) {
+    result = g->parts[0]->lab_full.get();
+    uint64_t em_kernels = 0;
+    auto enqueue_em = [&](int parity) {
+      uint64_t k = 0;
+      for (auto& pp : g->parts) {
+        Part& p = *pp;
+        if (device_loop) {
+          launch_em_prologue(p.a.unconv, map_max, st);
+          ++k;
+        } else {
+          CK(cudaMemcpyAsync(const_cast<double*>(p.a.terms), h_terms, 3 * M * 8,
+                             cudaMemcpyHostToDevice, st));
+          CK(cudaMemsetAsync(p.a.unconv, 0, map_max * sizeof(uint32_t), st));
+        }
+      }
+      for (int t = 0; t < map_max; ++t) {
+        const int bin = (parity + t) & 1, bout = bin ^ 1;
+        for (auto& pp : g->parts) {
+          launch_vertex_argmin(pp->a, pp->lab[bin].get(), pp->lab[bout].get(), t, st);
+          ++k;
+        }
+        exchange_halo(g, bout, st);
+        for (auto& pp : g->parts) {
+          launch_hood_sums(pp->a, t, st);
+          ++k;
+        }
+        sum_counters(g, t, st, &k);
+      }
+      for (auto& pp : g->parts) {
+        Part& p = *pp;
+        launch_partition_select(p.lab[parity].get(), p.lab[parity ^ 1].get(), p.a.hist, ring, Hs,
+                                p.a.unconv, map_max, fixed, p.vb, p.ve, p.hb, p.he,
+                                p.lab_full.get(), p.row_full.get(), st);
+        ++k;
+      }
+      allgather(g, st);
+      for (auto& pp : g->parts) {
+        Part& p = *pp;
+        // one row of hood energies (ring 1) and one label buffer: the same
+        // M-step + total energy as the one-device run
+        launch_mstep(p.a.mean, R, M, p.lab_full.get(), p.lab_full.get(), p.row_full.get(), Hs, 1,
+                     p.a.unconv, map_max, fixed, p.params.get(), p.em_out.get(), p.ms, st, &k,
+                     /*counts_ready=*/false);
+        if (device_loop) {
+          launch_em_epilogue(p.ep, st);
+          ++k;
+        }
+      }
+      if (!device_loop)
+        CK(cudaMemcpyAsync(h_em, g->parts[0]->em_out.get(), (2 + 2 * M) * 8,
+                           cudaMemcpyDeviceToHost, st));
+      em_kernels = k;
+    };
+    auto host_terms = [&] {  // make_label_terms (model.hpp:48-60) with the host's std::log
+      for (uint32_t l = 0; l < M; ++l) {
+        h_terms[l] = mu[l];
+        h_terms[M + l] = 2.0 * (sigma[l] * sigma[l]);
+        h_terms[2 * M + l] = std::log(sigma[l]);
+      }
+    };
+    ctx->stats.graphs = 0;
+    if (device_loop) {
+      host_terms();
+      for (auto& pp : g->parts)
+        CK(cudaMemcpyAsync(pp->terms.get(), h_terms, 3 * M * 8, cudaMemcpyHostToDevice, st));
+      const bool use_graph = g->use_graph && g->local() && !(o.flags & DPMRF_RUN_NO_GRAPH);
+      if (use_graph) {
+        std::vector<uint64_t> key = {ctx->generation, R, Hs, M, uint64_t(L), uint64_t(map_max),
+                                     uint64_t(fixed), uint64_t(packed)};
+        uint64_t bits;
+        std::memcpy(&bits, &cfg->beta, 8);
+        key.push_back(bits);
+        std::memcpy(&bits, &cfg->convergence_tol, 8);
+        key.push_back(bits);
+        for (auto& pp : g->parts) {
+          Part& p = *pp;
+          for (const void* q :
+               {(const void*)p.lab[0].get(), (const void*)p.lab[1].get(),
+                (const void*)p.lab_full.get(), (const void*)p.minE.get(),
+                (const void*)p.hist.get(), (const void*)p.row_full.get(),
+                (const void*)p.params.get(), (const void*)p.em_out.get(),
+                (const void*)p.terms.get(), (const void*)p.em_rec.get(),
+                (const void*)p.em_hist.get(), (const void*)p.state.get(),
+                (const void*)p.ms.counts.get(), (const void*)p.ms.x.get(),
+                (const void*)p.ms.partials.get(), (const void*)p.ms.layout.get(),
+                (const void*)p.ms.tile_base.get()})
+            key.push_back(reinterpret_cast<uintptr_t>(q));
+        }
+        if (!g->graph || key != g->graph_key) {
+          g->drop_graph();
+          cudaGraph_t gr = nullptr;
+          CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          try {
+            enqueue_em(0);
+          } catch (...) {
+            cudaStreamEndCapture(st, &gr);
+            if (gr) cudaGraphDestroy(gr);
+            throw;
+          }
+          CK(cudaStreamEndCapture(st, &gr));
+          CK(cudaGraphInstantiate(&g->graph, gr, 0));
+          CK(cudaGraphDestroy(gr));
+          g->graph_key = key;
+          g->graph_kernels = em_kernels;
+        }
+        for (int em = 0; em < em_max; ++em) CK(cudaGraphLaunch(g->graph, st));
+        em_kernels = g->graph_kernels;
+        ctx->stats.graphs = 1;
+      } else {
+        for (int em = 0; em < em_max; ++em) enqueue_em(0);
+      }
+      Part& p0 = *g->parts[0];
+      CK(cudaMemcpyAsync(h_rec, p0.state.get(), 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_rec + 4, p0.em_rec.get(), uint64_t(em_max) * rec_stride * 8,
+                         cudaMemcpyDeviceToHost, st));
+      ctx->sync();
+      uint32_t hstate[4];
+      std::memcpy(hstate, h_rec, sizeof hstate);
+      const int em_count = static_cast<int>(hstate[2]);
+      const double* rec = h_rec + 4;
+      for (int e = 0; e + 1 < em_count; ++e)
+        for (uint32_t l = 0; l < M; ++l) {
+          const double sg = rec[e * rec_stride + 3 + M + l];
+          const double dev = rec[e * rec_stride + 3 + 2 * M + l];
+          const double host = std::log(sg);
+          if (std::memcmp(&dev, &host, sizeof host) != 0) return false;
+        }
+      launches += uint64_t(em_max) * em_kernels;
+      for (int e = 0; e < em_count; ++e) {
+        const double* r = rec + e * rec_stride;
+        ctx->stats.map_iters_total += static_cast<int>(r[1]);
+        if (o.trace_level >= DPMRF_TRACE_EM) {
+          dpmrf_context::EmRecord er;
+          er.map_iters = static_cast<int>(r[1]);
+          er.total = r[0];
+          er.converged = r[2] != 0.0;
+          er.mu.assign(r + 3, r + 3 + M);
+          er.sigma.assign(r + 3 + M, r + 3 + 2 * M);
+          ctx->trace.push_back(std::move(er));
+        }
+        if (e == em_count - 1) {
+          mu.assign(r + 3, r + 3 + M);
+          sigma.assign(r + 3 + M, r + 3 + 2 * M);
+        }
+      }
+      ctx->stats.em_iters = em_count;
+    } else {
+      int cur = 0;
+      std::vector<double> em_hist;
+      for (int em = 0; em < em_max; ++em) {
+        host_terms();
+        enqueue_em(cur);
+        launches += em_kernels;
+        ctx->sync();
+        const int T = static_cast<int>(h_em[1]);
+        const double total = h_em[0];
+        std::memcpy(mu.data(), h_em + 2, M * 8);
+        std::memcpy(sigma.data(), h_em + 2 + M, M * 8);
+        cur = (cur + T) & 1;
+        ctx->stats.map_iters_total += T;
+        em_hist.push_back(total);  // EM-level window, optimize.cpp:66-69
+        uint8_t conv = 0;
+        const size_t rows = em_hist.size();
+        if (rows >= size_t(L) + 1) {
+          conv = 1;
+          for (int i = 1; i <= L; ++i)
+            if (!(std::fabs(total - em_hist[rows - 1 - i]) < cfg->convergence_tol)) {
+              conv = 0;
+              break;
+            }
+        }
+        if (o.trace_level >= DPMRF_TRACE_EM) {
+          dpmrf_context::EmRecord er;
+          er.map_iters = T;
+          er.total = total;
+          er.converged = conv;
+          er.mu = mu;
+          er.sigma = sigma;
+          ctx->trace.push_back(std::move(er));
+        }
+        ctx->stats.em_iters = em + 1;
+        if (conv && !fixed) break;
+      }
+    }
+    ctx->stats.series = Hs;
+  }
+  uint32_t* l32 = ctx->labels32.ensure(R);
+  launch_u8_to_u32(result, l32, R, st);
+  ++launches;
+  CK(cudaEventRecord(ctx->ev_end, st));
+  if (labels_out && R)
+    CK(cudaMemcpyAsync(labels_out, l32, uint64_t(R) * 4, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
+  float total_ms = 0.f;
+  CK(cudaEventElapsedTime(&total_ms, ctx->ev_begin, ctx->ev_end));
+  ctx->stats.optimize_ms = total_ms;
+  ctx->stats.kernel_launches = launches;
+  if (mu_out) std::memcpy(mu_out, mu.data(), M * 8);
+  if (sigma_out) std::memcpy(sigma_out, sigma.data(), M * 8);
+  return true;
+}
+
+}  // namespace
+
+// ---- C ABI -----------------------------------------------------------------------
+extern "C" dpmrf_status dpmrf_nccl_unique_id(uint8_t id[128]) {
+  return guarded([&] {
+    need(id != nullptr, DPMRF_INVALID_ARGUMENT, "null id");
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+    Nccl& nccl = Nccl::get();
+    ncclUniqueId u;
+    NK(nccl.GetUniqueId(&u));
+    std::memcpy(id, &u, sizeof u);
+  });
+}
+
+extern "C" dpmrf_status dpmrf_group_create_nccl(dpmrf_context* ctx, const uint8_t id[128],
+                                                int rank, int world, dpmrf_group** out) {
+  return guarded([&] {
+    need(ctx && id && out, DPMRF_INVALID_ARGUMENT, "null argument");
+    need(world >= 1 && world <= kMaxParts, DPMRF_INVALID_ARGUMENT, "world must be in [1, 64]");
+    need(rank >= 0 && rank < world, DPMRF_INVALID_ARGUMENT, "rank out of range");
+    ctx->bind();
+    Nccl& nccl = Nccl::get();
+    auto g = std::make_unique<dpmrf_group>();
+    g->ctx = ctx;
+    g->world = world;
+    g->rank = rank;
+    g->use_graph = false;  // NCCL calls are enqueued directly (no capture)
+    if (const char* e = std::getenv("DPMRF_GROUP_GRAPH")) g->use_graph = e[0] == '1';
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    NK(nccl.CommInitRank(&g->comm, world, u, rank));
+    auto p = std::make_unique<Part>();
+    p->r = rank;
+    g->parts.push_back(std::move(p));
+    *out = g.release();
+  });
+}
+
+extern "C" dpmrf_status dpmrf_group_create_local(dpmrf_context* ctx, int world,
+                                                 dpmrf_group** out) {
+  return guarded([&] {
+    need(ctx && out, DPMRF_INVALID_ARGUMENT, "null argument");
+    need(world >= 1 && world <= kMaxParts, DPMRF_INVALID_ARGUMENT, "world must be in [1, 64]");
+    ctx->bind();
+    auto g = std::make_unique<dpmrf_group>();
+    g->ctx = ctx;
+    g->world = world;
+    g->rank = -1;
+    if (const char* e = std::getenv("DPMRF_NO_GRAPH")) g->use_graph = e[0] == '0';
+    for (int r = 0; r < world; ++r) {
+      auto p = std::make_unique<Part>();
+      p->r = r;
+      g->parts.push_back(std::move(p));
+    }
+    *out = g.release();
+  });
+}
+
+extern "C" void dpmrf_group_destroy(dpmrf_group* g) {
+  if (!g) return;
+  cudaSetDevice(g->ctx->device);
+  cudaStreamSynchronize(g->ctx->stream);
+  g->drop_graph();
+  if (g->comm) {
+    Nccl& nccl = Nccl::get();
+    nccl.CommDestroy(g->comm);
+  }
+  delete g;
+}
+
+extern "C" dpmrf_status dpmrf_group_info_get(dpmrf_group* g, dpmrf_group_info* out) {
+  return guarded([&] {
+    need(g && out, DPMRF_INVALID_ARGUMENT, "null argument");
+    g->ctx->bind();
+    plan(g);
+    dpmrf_group_info i{};
+    i.world = g->world;
+    i.rank = g->rank;
+    const Part& p = *g->parts[0];
+    i.vertex_begin = p.vb;
+    i.vertex_end = p.ve;
+    i.series_begin = p.hb;
+    i.series_end = p.he;
+    i.halo_bytes_per_map = g->halo_bytes;
+    i.gather_bytes_per_em = g->gather_bytes;
+    *out = i;
+  });
+}
+
+extern "C" dpmrf_status dpmrf_optimize_partitioned(dpmrf_group* g,
+                                                   const dpmrf_optimizer_config* cfg,
+                                                   const dpmrf_run_options* opts,
+                                                   uint32_t* labels_out, double* mu_out,
+                                                   double* sigma_out) {
+  return guarded([&] {
+    need(g && cfg, DPMRF_INVALID_ARGUMENT, "null argument");
+    const dpmrf_run_options o = opts ? *opts : dpmrf_run_options{0, DPMRF_TRACE_EM};
+    check_config(*cfg, (o.flags & DPMRF_RUN_MULTILABEL) != 0);
+    need(o.trace_level <= DPMRF_TRACE_EM, DPMRF_INVALID_ARGUMENT,
+         "partitioned optimize records the EM trace only (trace level NONE or EM)");
+    dpmrf_context* ctx = g->ctx;
+    need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
+    need(ctx->has_hoods, DPMRF_INVALID_ARGUMENT, "no neighborhoods uploaded");
+    ctx->bind();
+    const bool device_loop = ctx->use_device_loop && !(o.flags & DPMRF_RUN_HOST_LOG) &&
+                             cfg->em_max_iters > 0;
+    if (device_loop) {
+      if (run_partitioned(g, cfg, o, true, labels_out, mu_out, sigma_out)) return;
+      ++ctx->stats.device_log_fallbacks;
+    }
+    run_partitioned(g, cfg, o, false, labels_out, mu_out, sigma_out);
+  });
+}

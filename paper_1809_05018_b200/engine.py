@@ -421,6 +421,77 @@ class Context:
         return LabelParams(mu, sg), lab
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it and ships it to the others)."""
+    buf = (ct.c_uint8 * 128)()
+    _check(N.cuda().dpmrf_nccl_unique_id(buf), "nccl_unique_id")
+    return bytes(buf)
+
+
+class PartitionGroup:
+    """Vertex-range partitioned optimize of ONE region graph (config D).
+
+    ``PartitionGroup.local(ctx, world)`` runs every partition inside ``ctx`` on
+    one device (halos by device copies); ``PartitionGroup.nccl(ctx, uid, rank,
+    world)`` is one rank of a one-process-per-GPU NCCL group.  ``optimize``
+    returns exactly what ``Context.optimize`` returns on one device."""
+
+    def __init__(self, ctx: Context, handle, world: int, rank: int):
+        self.ctx, self.h, self.world, self.rank = ctx, handle, world, rank
+        self._lib = N.cuda()
+
+    @classmethod
+    def local(cls, ctx: Context, world: int) -> "PartitionGroup":
+        h = ct.c_void_p()
+        _check(N.cuda().dpmrf_group_create_local(ctx.h, world, ct.byref(h)), "group_create_local")
+        return cls(ctx, h, world, -1)
+
+    @classmethod
+    def nccl(cls, ctx: Context, uid: bytes, rank: int, world: int) -> "PartitionGroup":
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        h = ct.c_void_p()
+        buf = (ct.c_uint8 * 128).from_buffer_copy(uid)
+        _check(N.cuda().dpmrf_group_create_nccl(ctx.h, buf, rank, world, ct.byref(h)),
+               "group_create_nccl")
+        return cls(ctx, h, world, rank)
+
+    def close(self):
+        if self.h:
+            self._lib.dpmrf_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        i = N.CGroupInfo()
+        _check(self._lib.dpmrf_group_info_get(self.h, ct.byref(i)), "group_info")
+        return {k: getattr(i, k) for k, _ in N.CGroupInfo._fields_}
+
+    def optimize(self, config: OptimizerConfig, *, fixed_work=False, multilabel=None,
+                 trace_level=TRACE_EM, host_log=False, csr=False, graphs=True,
+                 labels_out=None) -> OptimizeResult:
+        M = config.num_labels
+        if multilabel is None:
+            multilabel = M != 2
+        flags = (RUN_FIXED_WORK if fixed_work else 0) | (RUN_MULTILABEL if multilabel else 0) | \
+            (RUN_HOST_LOG if host_log else 0) | (RUN_CSR if csr else 0) | \
+            (0 if graphs else RUN_NO_GRAPH)
+        opts = N.CRunOptions(flags, trace_level)
+        cfg = config.c()
+        labels = labels_out if labels_out is not None else np.zeros(self.ctx.R, np.uint32)
+        mu, sigma = np.zeros(M), np.zeros(M)
+        _check(self._lib.dpmrf_optimize_partitioned(self.h, ct.byref(cfg), ct.byref(opts),
+                                                    N.ptr(labels), N.ptr(mu), N.ptr(sigma)),
+               "optimize_partitioned")
+        return OptimizeResult(labels, LabelParams(mu, sigma), self.ctx._trace(M, trace_level),
+                              self.ctx.stats())
+
+
 # ---- free functions with the reference's signatures --------------------------------
 _contexts = {}
 

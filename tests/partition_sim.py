@@ -1,0 +1,142 @@
+"""CPU restatement of the partitioned optimize schedule (csrc/partition.cu),
+one rank per process over torch.distributed (gloo) -- TEST INFRASTRUCTURE.
+
+Each rank runs the MAP kernels' arithmetic (numpy, the exact IEEE operation
+order of label_energy, model.hpp:66-72, and of the slot-order hood fold,
+engine.cpp:147-152) over only the vertices / series it owns, moves the halo
+windows of parallel.halo_windows with isend/irecv, sums the unconverged-hood
+counters with all_reduce and allgathers the committed labels and the last
+hood-energy row per EM iteration; the M-step and EM total are the C oracle's
+(update_parameters, engine.cpp:193-223; dpp::reduce, kernels.hpp:124-139).
+The result must equal the oracle's one-process optimize bit for bit, which
+checks the partition plan and the exchange schedule independently of CUDA.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from oracle import C
+from paper_1809_05018_b200.parallel import halo_windows
+
+
+def _exchange(arr, win, me, world):
+    """Send my windows of arr to their destinations, receive the others' windows."""
+    reqs = []
+    for o in range(world):
+        if o == me:
+            continue
+        lo, hi = int(win[me, o, 0]), int(win[me, o, 1])
+        if lo <= hi:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(arr[lo:hi + 1])), o))
+        lo, hi = int(win[o, me, 0]), int(win[o, me, 1])
+        if lo <= hi:
+            buf = torch.empty(hi - lo + 1, dtype=torch.from_numpy(arr[:1]).dtype)
+            reqs.append((dist.irecv(buf, o), lo, hi, buf))
+    for r in reqs:
+        if isinstance(r, tuple):
+            r[0].wait()
+            arr[r[1]:r[2] + 1] = r[3].numpy()
+        else:
+            r.wait()
+
+
+def _allgather(own, chunk, world):
+    parts = [torch.empty(chunk, dtype=torch.from_numpy(own[:1]).dtype) for _ in range(world)]
+    dist.all_gather(parts, torch.from_numpy(np.ascontiguousarray(own)))
+    return np.concatenate([p.numpy() for p in parts])
+
+
+def optimize_rank(graph, hoods, cfg, fixed_work=False):
+    """One rank's share of the partitioned optimize; returns (labels, mu, sigma, totals, T)."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    orc = C()
+    off = np.asarray(graph.offsets, np.int64)
+    nbr = np.asarray(graph.neighbors, np.int64)
+    mean = np.asarray(graph.region_mean, np.float64)
+    R = len(off) - 1
+    h_off = np.asarray(hoods.offsets, np.int64)
+    mem = np.asarray(hoods.members, np.int64)
+    sizes = np.diff(h_off)
+    s_off = np.concatenate([[0], np.cumsum(sizes[sizes > 0])]).astype(np.int64)
+    s_first = h_off[:-1][sizes > 0]
+    Hs = len(s_off) - 1
+    # series members in slot order (empty hoods dropped, as reduce_by_key does)
+    s_mem = np.concatenate([mem[a:a + n] for a, n in zip(s_first, sizes[sizes > 0])]) \
+        if Hs else mem[:0]
+    plan = halo_windows(off, nbr, s_off, s_mem, world)
+    vb, ve = int(plan.vb[rank]), int(plan.vb[rank + 1])
+    hb, he = int(plan.hb[rank]), int(plan.hb[rank + 1])
+    cover = np.zeros(R, bool)
+    cover[mem] = True
+    M, L, tol, beta = cfg.num_labels, cfg.convergence_window, cfg.convergence_tol, cfg.beta
+    mu, sigma, lab0 = orc.init_random(M, R, cfg.rng_seed, allow_multilabel=M != 2)
+    lab = [lab0.astype(np.int64), lab0.astype(np.int64).copy()]
+    minE = np.zeros(R)
+    own_v = np.arange(vb, ve)
+    deg = off[vb + 1:ve + 1] - off[vb:ve]
+    v_rep = np.repeat(np.arange(ve - vb), deg)
+    v_nbr = nbr[off[vb]:off[ve]]
+    own_sz = s_off[hb + 1:he + 1] - s_off[hb:he]
+    own_start = s_off[hb:he]
+    cur = 0
+    totals, em_T, em_hist = [], [], []
+    for em in range(cfg.em_max_iters):
+        _, two_var, log_sigma = orc.label_terms(mu, sigma)
+        hist = []
+        T = 0
+        for t in range(cfg.map_max_iters):
+            lin, lout = lab[(cur + t) & 1], lab[(cur + t + 1) & 1]
+            # vertex pass over the owned range (engine.cpp:74-191 fused)
+            x = mean[vb:ve]
+            best = None
+            arg = np.zeros(ve - vb, np.int64)
+            for l in range(M):
+                disc = np.zeros(ve - vb, np.int64)
+                np.add.at(disc, v_rep, (lin[v_nbr] != l).astype(np.int64))
+                d = x - mu[l]
+                e = ((d * d) / two_var[l] + log_sigma[l]) + beta * disc.astype(np.float64)
+                if best is None:
+                    best = e
+                else:
+                    take = e < best
+                    best = np.where(take, e, best)
+                    arg = np.where(take, l, arg)
+            minE[vb:ve] = best
+            lout[vb:ve] = np.where(cover[vb:ve], arg, lin[vb:ve])
+            _exchange(lout, plan.lab_win, rank, world)
+            _exchange(minE, plan.min_win, rank, world)
+            # hood pass over the owned series: left fold in slot order
+            sums = np.zeros(he - hb)
+            if he > hb:
+                sums = minE[s_mem[own_start]].copy()
+                for j in range(1, int(own_sz.max())):
+                    m = j < own_sz
+                    sums[m] = sums[m] + minE[s_mem[own_start[m] + j]]
+            hist.append(sums)
+            flags = orc.check_convergence(np.array(hist), L, tol) if he > hb else \
+                np.zeros(0, np.uint8)
+            unconv = torch.tensor([int((flags == 0).sum())], dtype=torch.int64)
+            dist.all_reduce(unconv)
+            T = t + 1
+            if not fixed_work and int(unconv.item()) == 0:
+                break
+        cur = (cur + T) & 1
+        own_lab = np.zeros(plan.chunk_v, np.int64)
+        own_lab[:ve - vb] = lab[cur][vb:ve]
+        full_lab = _allgather(own_lab, plan.chunk_v, world)[:R]
+        own_row = np.zeros(plan.chunk_h)
+        own_row[:he - hb] = hist[-1]
+        row = _allgather(own_row, plan.chunk_h, world)[:Hs]
+        lab[cur][:] = full_lab  # (every rank now holds all committed labels)
+        mu, sigma = orc.update_parameters(mean, full_lab.astype(np.uint32), mu, sigma)
+        total = orc.reduce(row)
+        totals.append(total)
+        em_T.append(T)
+        em_hist.append(total)
+        conv = len(em_hist) >= L + 1 and all(
+            abs(total - em_hist[-1 - i]) < tol for i in range(1, L + 1))
+        if conv and not fixed_work:
+            break
+    return lab[cur].astype(np.uint32), mu, sigma, totals, em_T

@@ -50,32 +50,75 @@ def test_slice_sharding_two_ranks():
         assert flat == list(range(64))  # every slice exactly once
 
 
-def test_halo_plan_grid_graph():
-    from oracle import C, graph_from_edges
-    # 6x6 grid of regions, edge cliques, hoods from the oracle's build
-    n = 6
-    edges = [(r * n + c, r * n + c + 1) for r in range(n) for c in range(n - 1)]
-    edges += [(r * n + c, (r + 1) * n + c) for r in range(n - 1) for c in range(n)]
-    g = graph_from_edges(n * n, edges)
-    cl = sorted(tuple(sorted(e)) for e in edges)
-    c_off = np.arange(0, 2 * len(cl) + 1, 2, dtype=np.uint32)
-    hoods, _ = C().build_neighborhoods(g, c_off, np.array(cl, np.uint32).ravel())
-    from paper_1809_05018_b200.parallel import halo_plan, vertex_ranges
+def _slice(size, block, brick=False, seed=3):
+    from oracle import C, Graph, Hoods
+    from paper_1809_05018_b200 import inputs
+    sl = inputs.synthetic_slice(size, block, brick=brick, seed=seed)
+    g = Graph(sl.graph.offsets, sl.graph.neighbors, sl.graph.region_mean)
+    h, _ = C().build_neighborhoods(g, sl.cliques.offsets, sl.cliques.members)
+    return g, h
+
+
+def test_halo_windows_grid_graph():
+    from paper_1809_05018_b200.parallel import halo_windows
+    g, h = _slice(320, 8)  # 40 x 40 regions
+    R = g.num_vertices
     world = 3
-    b = vertex_ranges(n * n, world)
-    owned = []
-    for r in range(world):
-        p = halo_plan(g.offsets, g.neighbors, hoods.offsets, hoods.members, world, r)
-        assert (p.lo, p.hi) == (b[r], b[r + 1])
-        owned += list(range(p.hood_lo, p.hood_hi))
-        # discord of owned vertices needs exactly the foreign neighbors
-        need = set()
-        for v in range(p.lo, p.hi):
-            need |= {int(u) for u in g.neighbors[g.offsets[v]:g.offsets[v + 1]]
-                     if not (p.lo <= u < p.hi)}
-        assert set(p.label_halo.tolist()) == need
-        # grid: halo is at most one block row on each side
-        assert len(p.label_halo) <= 2 * n
-        # hoods are owned by their smallest member: their halo lies above the range
-        assert all(p.hi <= v < p.hi + 3 * n for v in p.minE_halo)
-    assert owned == list(range(hoods.size))  # every hood owned once, in order
+    p = halo_windows(g.offsets, g.neighbors, h.offsets, h.members, world)
+    assert p.chunk_v % 256 == 0 and p.chunk_h % 1024 == 0
+    assert p.vb[0] == 0 and p.vb[-1] == R and p.hb[-1] == h.size
+    owner = np.searchsorted(p.vb[:-1], np.arange(R), side="right") - 1
+    for s in range(world):
+        for d in range(world):
+            if s == d:
+                continue
+            # every foreign neighbor label d's vertices read lies in the window
+            need = set()
+            for v in range(p.vb[d], p.vb[d + 1]):
+                need |= {int(u) for u in g.neighbors[g.offsets[v]:g.offsets[v + 1]]
+                         if owner[u] == s}
+            lo, hi = p.lab_win[s, d]
+            if need:
+                assert (lo, hi) == (min(need), max(need))
+            else:
+                assert lo > hi
+            # grid: neighbors are at most one row (40 regions) across the boundary
+            if need:
+                assert hi - lo < 2 * 40
+    # hoods are built per clique in lexicographic order: series windows stay
+    # within a few block rows of the band boundary
+    assert p.halo_bytes() < 20 * 40 * 9 * world
+
+
+def _partition_worker(rank, world, port, out, fixed):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import Config
+    from partition_sim import optimize_rank
+    g, h = _slice(320, 8)
+    cfg = Config(rng_seed=7, em_max_iters=6)
+    lab, mu, sg, totals, T = optimize_rank(g, h, cfg, fixed_work=fixed)
+    out[rank] = (lab.tolist(), mu.tolist(), sg.tolist(), totals, T)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,fixed", [(2, False), (3, True)])
+def test_partitioned_schedule_matches_oracle(world, fixed):
+    """The halo/allreduce/allgather schedule of csrc/partition.cu, run on CPU
+    ranks over gloo, reproduces the one-process oracle bit for bit."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from oracle import C, Config
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_partition_worker, args=(world, port, out, fixed), nprocs=world, join=True)
+        res = dict(out)
+    g, h = _slice(320, 8)
+    want = C().optimize(g, h, Config(rng_seed=7, em_max_iters=6), fixed_work=fixed)
+    for rank in range(world):
+        lab, mu, sg, totals, T = res[rank]
+        assert np.array_equal(np.array(lab, np.uint32), want.labels)
+        assert np.array_equal(np.array(mu), want.mu) and np.array_equal(np.array(sg), want.sigma)
+        assert totals == [e.total_energy for e in want.trace]
+        assert T == [e.num_map_iters or len(e.map_iters) for e in want.trace]
