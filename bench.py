@@ -411,6 +411,13 @@ def main():
         kavg = prof["map_loop_ms"] / max(1, prof["map_loop_launches"])
         kernel_split = {"k_map_loop": prof["map_loop_ms"] / prof_steps,
                         "mstep": prof["mstep_ms"] / prof_steps}
+    elif prof["map_loop_launches"]:
+        # fused boundaries: MAP_ITERS + 1 launches per EM move MAP_ITERS x (vertex + hood)
+        kname = "k_map_fused"
+        kbytes = MAP_ITERS * (vtx_bytes + hood_bytes) / (MAP_ITERS + 1)
+        kavg = prof["map_loop_ms"] / prof["map_loop_launches"]
+        kernel_split = {"k_map_fused": prof["map_loop_ms"] / prof_steps,
+                        "mstep": prof["mstep_ms"] / prof_steps}
     else:
         n_launch = max(1, prof["vertex_launches"])
         vtx_avg = prof["vertex_kernel_ms"] / n_launch

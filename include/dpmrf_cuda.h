@@ -67,12 +67,15 @@ enum {
   DPMRF_RUN_FIXED_WORK = 1u,    /* drop the early exits (optimize.cpp:59,:71): fixed EM x MAP work */
   DPMRF_RUN_MULTILABEL = 2u,    /* allow num_labels in [1,255] (extension; reference: 2 only) */
   DPMRF_RUN_KERNEL_TIMING = 4u, /* CUDA events around the MAP kernels (dpmrf_get_stats) */
-  DPMRF_RUN_TWO_KERNELS = 8u,   /* two kernels per MAP iteration (the default) */
+  DPMRF_RUN_TWO_KERNELS = 8u,   /* no persistent MAP-loop kernel (the default) */
   DPMRF_RUN_NO_GRAPH = 16u,     /* launch each EM iteration directly instead of a CUDA graph */
   DPMRF_RUN_PERSISTENT = 32u,   /* one cooperative persistent kernel per MAP loop */
   DPMRF_RUN_STAGED = 64u,       /* shared-memory staged vertex/hood tiles */
   DPMRF_RUN_CSR = 256u,         /* read the u32 CSR in the MAP kernels instead of the packed
                                    int16/u16 delta layouts built at preparation */
+  DPMRF_RUN_UNFUSED = 512u,     /* separate vertex and hood kernels per MAP iteration; default
+                                   (packed layouts): map_max + 1 launches per EM iteration, each
+                                   running the hood pass of t-1 with the vertex pass of t */
   DPMRF_RUN_HOST_LOG = 128u     /* host round trip per EM iteration (log(sigma) on the host);
                                    default: EM iterations run back to back on the device with a
                                    correctly rounded device log, verified against the host libm

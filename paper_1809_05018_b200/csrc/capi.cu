@@ -163,6 +163,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     if (const char* e = std::getenv("DPMRF_NO_PDL")) pdl_enabled() = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_HOST_LOG")) c->use_device_loop = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_CSR")) c->use_packed = e[0] == '0';
+    if (const char* e = std::getenv("DPMRF_UNFUSED")) c->use_fused = e[0] == '0';
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -344,6 +345,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
                             (ctx->use_persistent && !(o.flags & DPMRF_RUN_TWO_KERNELS));
     a.L = L;
     a.ring = full ? map_max : L + 1;
+    const bool fused_req = ctx->use_fused && !(o.flags & DPMRF_RUN_UNFUSED) && !persistent;
     a.fixed = fixed;
     a.staged = (ctx->use_staged || (o.flags & DPMRF_RUN_STAGED)) ? 1 : 0;
     const bool packed = !(o.flags & DPMRF_RUN_CSR);
@@ -352,9 +354,10 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     a.hood_k = packed ? ctx->hood_k : 0;
     a.hood_base = ctx->hood_base.get();
     a.hood_pk = ctx->hood_pk.get();
+    const bool fused = fused_req && !a.staged && map_fused_supported(a);
     a.terms = ctx->terms.ensure(3 * M);
     double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
-    ctx->pin_in_l2(minE2, uint64_t(R) * sizeof(double));
+    ctx->pin_in_l2(minE2, uint64_t(R) * sizeof(double) * (fused ? 2 : 1));
     a.minE = minE2;
     a.hist = ctx->hist.ensure(uint64_t(a.ring) * Hs);
     a.flags = full ? ctx->flags.ensure(uint64_t(map_max) * Hs) : nullptr;
@@ -396,7 +399,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     ep.em_rec = em_rec;
     ep.terms = const_cast<double*>(a.terms);
     std::vector<double> em_hist;
-    const size_t ev_per_em = timing ? size_t(3 * map_max + 4) : 0;
+    const size_t ev_per_em = timing ? size_t(3 * map_max + 6) : 0;
     ctx->stats.persistent = persistent;
     for (size_t i = 0; i < ev_per_em; ++i) ctx->event(i);
     // Everything one EM iteration puts on the stream (no host sync inside).
@@ -425,6 +428,16 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
         launch_map_loop(a, lab[parity], lab[parity ^ 1], minE2, minE2 + R, map_max, st);
         record(ev++);
         k += 1;
+      } else if (fused) {
+        const uint64_t half = R ? R : 1;
+        for (int t = 0; t <= map_max; ++t) {
+          record(ev++);
+          launch_map_fused(a, lab[(parity + t) & 1], lab[(parity + t + 1) & 1],
+                           minE2 + uint64_t((t + 1) & 1) * half, minE2 + uint64_t(t & 1) * half,
+                           t, map_max, st);
+          k += 1;
+        }
+        record(ev++);
       } else {
         for (int t = 0; t < map_max; ++t) {
           const uint8_t* lin = lab[(parity + t) & 1];
@@ -469,7 +482,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       key.map_max = map_max;
       key.fixed = fixed;
       key.timing = timing;
-      key.persistent = persistent + 2 * a.staged + 4 * device_loop;
+      key.persistent = persistent + 2 * a.staged + 4 * device_loop + 8 * fused;
       key.trace = o.trace_level;
       key.beta = cfg->beta;
       key.tol = cfg->convergence_tol;
@@ -602,6 +615,13 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
             ctx->stats.map_loop_ms += ms;
             ctx->stats.map_loop_launches += 1;
             e = 2;
+          } else if (fused) {
+            for (int t = 0; t <= map_max; ++t, ++e) {
+              CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));
+              ctx->stats.map_loop_ms += ms;
+            }
+            ctx->stats.map_loop_launches += map_max + 1;
+            ++e;
           } else {
             for (int t = 0; t < map_max; ++t, e += 3) {
               CK(cudaEventElapsedTime(&ms, ctx->ev_pool[e], ctx->ev_pool[e + 1]));

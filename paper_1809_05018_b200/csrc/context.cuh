@@ -94,6 +94,8 @@ struct dpmrf_context {
   // per item on B200 (L1 already absorbs the CSR segment reads; the staged
   // hood fold is bank-conflicted), so off unless DPMRF_DIRECT=0
   bool use_staged = false;
+  // hood pass of t-1 + vertex pass of t in one launch (packed layouts)
+  bool use_fused = true;
   bool graph_valid = false;
   GraphKey graph_key{};
   cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};

@@ -965,7 +965,36 @@ __global__ void __launch_bounds__(kVtxThreads)
                     int t);
 template <int K>
 __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t);
+template <int MT, int KV, int KH>
+__global__ void __launch_bounds__(kVtxThreads)
+    k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
+                const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
+                uint32_t nh);
 }  // namespace
+
+bool map_fused_supported(const MapArgs& a) { return a.adj_k && a.hood_k && !a.staged; }
+
+void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
+                      const double* minE_prev, double* minE_cur, int t, int map_max,
+                      cudaStream_t s) {
+  const uint32_t nh = t >= 1 ? grid_for(a.h_end - a.h_begin, kHoodThreads) : 0u;
+  const uint32_t nv = t < map_max ? grid_for(a.v_end - a.v_begin, kVtxThreads) : 0u;
+  const dim3 g(nh + nv), blk(kVtxThreads);
+  const int sel = (a.M == 2 ? 0 : 4) + (a.adj_k == 8 ? 2 : 0) + (a.hood_k == 16 ? 1 : 0);
+#define MF(MT, KV, KH) launch_pdl(k_map_fused<MT, KV, KH>, g, blk, 0, s, a, lab_in, lab_out, \
+                                  minE_prev, minE_cur, t, nh)
+  switch (sel) {
+    case 0: MF(2, 4, 8); break;
+    case 1: MF(2, 4, 16); break;
+    case 2: MF(2, 8, 8); break;
+    case 3: MF(2, 8, 16); break;
+    case 4: MF(0, 4, 8); break;
+    case 5: MF(0, 4, 16); break;
+    case 6: MF(0, 8, 8); break;
+    default: MF(0, 8, 16); break;
+  }
+#undef MF
+}
 
 void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out, int t,
                           cudaStream_t s) {
@@ -1048,13 +1077,13 @@ __device__ __forceinline__ void load_i16(const int16_t* __restrict__ p, int16_t 
 }
 
 template <int MT, int K>
-__global__ void __launch_bounds__(kVtxThreads)
-    k_vertex_packed(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
-                    int t) {
-  pdl_wait();
-  if (map_iter_skipped(a.unconv, t, a.fixed)) return;
+__device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
+                                                   const uint8_t* __restrict__ lab_in,
+                                                   uint8_t* __restrict__ lab_out,
+                                                   double* __restrict__ minE, int t,
+                                                   uint32_t blk) {
   const uint32_t M = MT > 0 ? uint32_t(MT) : a.M;
-  const uint32_t v = a.v_begin + blockIdx.x * kVtxThreads + threadIdx.x;
+  const uint32_t v = a.v_begin + blk * kVtxThreads + threadIdx.x;
   const bool valid = v < a.v_end;
   uint32_t nl = 0;
   if (valid) {
@@ -1103,21 +1132,30 @@ __global__ void __launch_bounds__(kVtxThreads)
           }
         }
       }
-      a.minE[v] = best;
+      minE[v] = best;
       lab_out[v] = static_cast<uint8_t>(best_l);
       nl = best_l;
     }
   }
-  if (a.tile_counts && blockIdx.x < a.tiles)
-    block_label_counts(a.tile_counts + (uint64_t(t & 1) * a.tiles + blockIdx.x) * M, M, valid, nl);
+  if (a.tile_counts && blk < a.tiles)
+    block_label_counts(a.tile_counts + (uint64_t(t & 1) * a.tiles + blk) * M, M, valid, nl);
+}
+
+template <int MT, int K>
+__global__ void __launch_bounds__(kVtxThreads)
+    k_vertex_packed(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
+                    int t) {
+  pdl_wait();
+  if (map_iter_skipped(a.unconv, t, a.fixed)) return;
+  vertex_packed_body<MT, K>(a, lab_in, lab_out, a.minE, t, blockIdx.x);
 }
 
 template <int K>
-__global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) {
+__device__ __forceinline__ void hood_packed_body(const MapArgs& a,
+                                                 const double* __restrict__ minE, int t,
+                                                 uint32_t blk) {
   static_assert(K == 8 || K == 16, "hood pack width");
-  pdl_wait();
-  if (map_iter_skipped(a.unconv, t, a.fixed)) return;
-  const uint64_t h = a.h_begin + uint64_t(blockIdx.x) * kHoodThreads + threadIdx.x;
+  const uint64_t h = a.h_begin + uint64_t(blk) * kHoodThreads + threadIdx.x;
   int not_conv = 0;
   if (h < a.h_end) {
     const uint32_t base = a.hood_base[h];
@@ -1135,9 +1173,9 @@ __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) 
 #pragma unroll
     for (int k = 0; k < K; ++k) {  // all gathers in flight before the fold
       const uint32_t dk = (u[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
-      e[k] = dk != 0xFFFFu ? a.minE[base + dk] : 0.0;
+      e[k] = dk != 0xFFFFu ? minE[base + dk] : 0.0;
     }
-    double sum = a.minE[base];
+    double sum = minE[base];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint32_t dk = (u[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
@@ -1161,6 +1199,36 @@ __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) 
   }
   const int bu = __syncthreads_count(not_conv);
   if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[t], uint32_t(bu));
+}
+
+template <int K>
+__global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) {
+  pdl_wait();
+  if (map_iter_skipped(a.unconv, t, a.fixed)) return;
+  hood_packed_body<K>(a, a.minE, t, blockIdx.x);
+}
+
+// One kernel per MAP-iteration boundary: the hood pass of iteration t-1 and
+// the vertex pass of iteration t read only what the vertex pass of t-1 wrote
+// (its minima and committed labels), so they share a launch -- blocks
+// [0, nh) fold hoods, the rest evaluate vertices.  The vertex pass of t runs
+// speculatively whenever t-1 runs: if t-1 turns out to be the last
+// iteration, the speculative pass only wrote buffers nothing reads any more
+// (labels into the buffer t-1 consumed, minima into the other half of the
+// double-buffered minima, label counts into the other parity slot).
+template <int MT, int KV, int KH>
+__global__ void __launch_bounds__(kVtxThreads)
+    k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
+                const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
+                uint32_t nh) {
+  static_assert(kVtxThreads == kHoodThreads, "one block shape for both passes");
+  pdl_wait();
+  if (blockIdx.x < nh) {
+    if (!map_iter_skipped(a.unconv, t - 1, a.fixed)) hood_packed_body<KH>(a, minE_prev, t - 1, blockIdx.x);
+  } else {
+    if (!map_iter_skipped(a.unconv, t > 0 ? t - 1 : 0, a.fixed))
+      vertex_packed_body<MT, KV>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh);
+  }
 }
 
 // ---- pack builders ----

@@ -57,6 +57,14 @@ uint32_t label_tiles(uint32_t R);
 void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out, int t,
                           cudaStream_t s);
 void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s);
+// Fused MAP-iteration boundary (packed layouts only): launch t runs the hood
+// pass of iteration t-1 and the vertex pass of iteration t (t = 0..map_max);
+// the minima are double-buffered by iteration parity (minE_cur = vertex
+// output of t, minE_prev = that of t-1).
+bool map_fused_supported(const MapArgs& a);
+void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
+                      const double* minE_prev, double* minE_cur, int t, int map_max,
+                      cudaStream_t s);
 // The whole MAP loop of one EM iteration as one cooperative kernel (see engine.cu).
 void launch_map_loop(const MapArgs& a, uint8_t* lab_even, uint8_t* lab_odd, double* minE0,
                      double* minE1, int map_max, cudaStream_t s);

@@ -32,7 +32,7 @@ DPMRF_CUDA_ERROR, DPMRF_NCCL_ERROR, DPMRF_INTERNAL_ERROR = 4, 5, 6
 
 TRACE_NONE, TRACE_EM, TRACE_FULL = 0, 1, 2
 RUN_FIXED_WORK, RUN_MULTILABEL, RUN_KERNEL_TIMING, RUN_TWO_KERNELS, RUN_NO_GRAPH = 1, 2, 4, 8, 16
-RUN_PERSISTENT, RUN_STAGED, RUN_HOST_LOG, RUN_CSR = 32, 64, 128, 256
+RUN_PERSISTENT, RUN_STAGED, RUN_HOST_LOG, RUN_CSR, RUN_UNFUSED = 32, 64, 128, 256, 512
 
 K_SIGMA_FLOOR = 1e-3  # kSigmaFloor, model.hpp:9
 
@@ -278,7 +278,7 @@ class Context:
     def optimize(self, config: OptimizerConfig, *, fixed_work=False, multilabel=None,
                  trace_level=TRACE_FULL, kernel_timing=False, labels_out=None,
                  persistent=None, graphs=True, staged=False,
-                 host_log=False, csr=False) -> OptimizeResult:
+                 host_log=False, csr=False, fused=True) -> OptimizeResult:
         """persistent: None = library default, True = one cooperative MAP-loop
         kernel per EM iteration, False = two kernels per MAP iteration."""
         M = config.num_labels
@@ -288,7 +288,7 @@ class Context:
             (RUN_KERNEL_TIMING if kernel_timing else 0) | \
             ({None: 0, True: RUN_PERSISTENT, False: RUN_TWO_KERNELS}[persistent]) | \
             (RUN_STAGED if staged else 0) | (RUN_HOST_LOG if host_log else 0) | \
-            (RUN_CSR if csr else 0) | \
+            (RUN_CSR if csr else 0) | (0 if fused else RUN_UNFUSED) | \
             (0 if graphs else RUN_NO_GRAPH)
         opts = N.CRunOptions(flags, trace_level)
         cfg = config.c()

@@ -60,7 +60,7 @@ def test_fixture_optimize(ctx, name):
     f.check(r)
 
 
-@pytest.mark.parametrize("layout", ["packed", "csr", "staged"])
+@pytest.mark.parametrize("layout", ["packed", "unfused", "csr", "staged"])
 @pytest.mark.parametrize("persistent", [False, True])
 @pytest.mark.parametrize("graphs", [False, True])
 def test_execution_modes_agree(ctx, persistent, graphs, layout):
@@ -71,7 +71,8 @@ def test_execution_modes_agree(ctx, persistent, graphs, layout):
         f = Fixture(name)
         upload(ctx, f.graph, f.hoods)
         r = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, persistent=persistent,
-                         graphs=graphs, staged=layout == "staged", csr=layout == "csr")
+                         graphs=graphs, staged=layout == "staged", csr=layout == "csr",
+                         fused=layout != "unfused")
         f.check(r)
         assert r.stats["persistent"] == (1 if persistent else 0)
         assert r.stats["graphs"] == (1 if graphs else 0)
@@ -79,7 +80,8 @@ def test_execution_modes_agree(ctx, persistent, graphs, layout):
             for timing in (False, True):  # timing forces the host-log loop
                 r2 = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, persistent=persistent,
                                   graphs=graphs, trace_level=level, kernel_timing=timing,
-                                  staged=layout == "staged", csr=layout == "csr")
+                                  staged=layout == "staged", csr=layout == "csr",
+                                  fused=layout != "unfused")
                 assert np.array_equal(r2.labels, r.labels) and np.array_equal(r2.mu, r.mu)
                 assert np.array_equal(r2.sigma, r.sigma)
 
