@@ -551,6 +551,89 @@ __global__ void __launch_bounds__(kTileThreads)
   }
 }
 
+// Small graphs (tiles * M <= kSelfScanMax): k_tile_offsets folded into the
+// scatter -- every block sums the label counts of the tiles before it (and of
+// all tiles, for the label starts) itself, block 0 publishes the layout.
+// One launch less per EM iteration where launches, not bytes, dominate.
+constexpr uint32_t kSelfScanMax = 8192;
+
+__global__ void __launch_bounds__(kTileThreads)
+    k_label_scatter_small(const uint8_t* lab_even, const uint8_t* lab_odd,
+                          const uint32_t* unconv, const uint32_t* count_sel, int map_max,
+                          int fixed, uint32_t R, uint32_t M, uint64_t Hs,
+                          const double* __restrict__ mean, const uint32_t* __restrict__ counts_buf,
+                          uint32_t tiles, uint32_t* __restrict__ layout, double* __restrict__ x) {
+  extern __shared__ uint32_t wcnt[];  // [warp][M] | base[M] | start[M] | red[kWarps]
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kTileThreads / 32;
+  if (em_skipped(unconv)) return;
+  uint32_t* base_s = wcnt + kWarps * M;
+  uint32_t* start_s = base_s + M;
+  uint32_t* red = start_s + M;
+  const uint32_t* tc = final_counts(counts_buf, tiles, M, count_sel, map_max, fixed);
+  const uint32_t tile = blockIdx.x;
+  for (uint32_t l = 0; l < M; ++l) {  // prefix (tiles before this one) and total of label l
+    uint32_t pre = 0, tot = 0;
+    for (uint32_t i = threadIdx.x; i < tiles; i += kTileThreads) {
+      const uint32_t c = tc[uint64_t(i) * M + l];
+      tot += c;
+      pre += i < tile ? c : 0u;
+    }
+    pre = __reduce_add_sync(0xffffffffu, pre);
+    tot = __reduce_add_sync(0xffffffffu, tot);
+    if (lane == 0) {
+      red[warp] = pre;
+      red[kWarps + warp] = tot;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t p = 0, q = 0;
+      for (int w = 0; w < kWarps; ++w) {
+        p += red[w];
+        q += red[kWarps + w];
+      }
+      base_s[l] = p;
+      start_s[l] = q;  // (total; turned into label starts below)
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    uint32_t s = 0, lf = 0;
+    for (uint32_t l = 0; l < M; ++l) {
+      const uint32_t n = start_s[l];
+      if (blockIdx.x == 0) {
+        layout[l] = n;
+        layout[M + l] = s;
+        layout[2 * M + 1 + l] = lf;
+      }
+      start_s[l] = s;
+      s += n;
+      lf += (n + kFoldLeaf - 1) / kFoldLeaf;
+    }
+    if (blockIdx.x == 0) {
+      layout[2 * M] = s;
+      layout[3 * M + 1] = lf;
+      layout[3 * M + 2] = lf + uint32_t((Hs + kFoldLeaf - 1) / kFoldLeaf);
+    }
+  }
+  const uint8_t* lab = final_labels(lab_even, lab_odd, unconv, map_max, fixed);
+  for (uint32_t i = threadIdx.x; i < kWarps * M; i += kTileThreads) wcnt[i] = 0;
+  __syncthreads();
+  const uint64_t v = uint64_t(tile) * kTileVerts + threadIdx.x;
+  const bool valid = v < R;
+  const uint32_t l = valid ? lab[v] : 0xFFFFFFFFu;
+  const unsigned peers = __match_any_sync(0xffffffffu, l);
+  const uint32_t rank_in_warp = __popc(peers & ((1u << lane) - 1u));
+  if (valid && rank_in_warp == 0) wcnt[warp * M + l] = __popc(peers);
+  __syncthreads();
+  if (valid) {
+    uint32_t before = 0;
+    for (int w = 0; w < warp; ++w) before += wcnt[w * M + l];
+    x[start_s[l] + base_s[l] + before + rank_in_warp] = mean[v];
+  }
+}
+
 // Single block: per-label exclusive scan over tiles; label starts; leaf layout.
 // layout = n[M] | label_start[M+1] | leaf_start[M+2] (series M = hood energies)
 __global__ void __launch_bounds__(1024)
@@ -680,21 +763,39 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x < kLeavesPerBlock && len_s[threadIdx.x] != 0) {
       const uint32_t len = len_s[threadIdx.x];
       const double* v = stage + threadIdx.x * kLeafStride;
-      double acc;
-      if (kSq) {
-        const double mu = mu_s[threadIdx.x];
-        double d = __dsub_rn(v[0], mu);
-        acc = __dmul_rn(d, d);
-#pragma unroll 8
-        for (uint32_t i = 1; i < len; ++i) {
-          d = __dsub_rn(v[i], mu);
-          acc = __dadd_rn(acc, __dmul_rn(d, d));
+      const double mu = kSq ? mu_s[threadIdx.x] : 0.0;
+      // element term: x (sum pass) or (x - mu)^2 (sq pass); independent of acc
+      auto term = [&](double x) {
+        if (kSq) {
+          const double d = __dsub_rn(x, mu);
+          return __dmul_rn(d, d);
         }
-      } else {
-        acc = v[0];
-#pragma unroll 8
-        for (uint32_t i = 1; i < len; ++i) acc = __dadd_rn(acc, v[i]);
+        return x;
+      };
+      // Software-pipelined chain: the next 16 operands are read from shared
+      // memory while the current 16 dependent adds retire, so the chain runs
+      // at the DADD latency instead of LDS + DADD per group.
+      constexpr int kG = 16;
+      double acc = term(v[0]);
+      uint32_t i = 1;
+      double cur[kG], nxt[kG];
+      if (i + kG <= len) {
+#pragma unroll
+        for (int j = 0; j < kG; ++j) cur[j] = v[i + j];
+        while (i + 2 * kG <= len) {
+#pragma unroll
+          for (int j = 0; j < kG; ++j) nxt[j] = v[i + kG + j];
+#pragma unroll
+          for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, term(cur[j]));
+#pragma unroll
+          for (int j = 0; j < kG; ++j) cur[j] = nxt[j];
+          i += kG;
+        }
+#pragma unroll
+        for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, term(cur[j]));
+        i += kG;
       }
+      for (; i < len; ++i) acc = __dadd_rn(acc, term(v[i]));
       partials[first + threadIdx.x] = acc;
     }
   }
@@ -1369,10 +1470,19 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
     CK_LAUNCH();
     ++n;
   }
-  launch_pdl(k_tile_offsets, dim3(1), dim3(1024), 0, s, (const uint32_t*)counts,
-             counts_ready ? unconv : nullptr, map_max, fixed, tile_base, tiles, M, Hs, layout);
-  ++n;
-  if (tiles) {
+  if (tiles && uint64_t(tiles) * M <= kSelfScanMax) {
+    const size_t smem_s = ((kTileThreads / 32) * M + 2 * M + 2 * (kTileThreads / 32)) *
+                          sizeof(uint32_t);
+    launch_pdl(k_label_scatter_small, dim3(tiles), dim3(kTileThreads), smem_s, s, lab_even,
+               lab_odd, unconv, counts_ready ? unconv : (const uint32_t*)nullptr, map_max, fixed,
+               R, M, Hs, mean, (const uint32_t*)counts, tiles, layout, x);
+    ++n;
+  } else {
+    launch_pdl(k_tile_offsets, dim3(1), dim3(1024), 0, s, (const uint32_t*)counts,
+               counts_ready ? unconv : nullptr, map_max, fixed, tile_base, tiles, M, Hs, layout);
+    ++n;
+  }
+  if (tiles && uint64_t(tiles) * M > kSelfScanMax) {
     launch_pdl(k_label_tiles<1>, dim3(tiles), dim3(kTileThreads), smem, s, lab_even, lab_odd,
                unconv, map_max, fixed, R, M, mean, (uint32_t*)nullptr,
                (const uint32_t*)tile_base, (const uint32_t*)layout, x);
