@@ -122,6 +122,10 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
+// No kernel issues griddepcontrol.launch_dependents: releasing the next grid
+// early (its blocks resident and parked in pdl_wait while this grid runs)
+// measured 6% SLOWER at 2560^2 (11.9k vs 12.7k EM-it/s) and neutral at
+// 16384^2 -- the parked blocks take slots from this grid's tail.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 inline unsigned grid_for(uint64_t n, unsigned block) {
