@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-CUDA_LIB = os.path.join(HERE, "libdpmrf_cuda.so")
+# DPMRF_CUDA_LIB overrides the path (A/B builds of the same library, tools/ab.py)
+CUDA_LIB = os.environ.get("DPMRF_CUDA_LIB") or os.path.join(HERE, "libdpmrf_cuda.so")
 INPUTS_LIB = os.path.join(HERE, "libdpmrf_inputs.so")
 
 u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")

@@ -1059,7 +1059,14 @@ __global__ void k_compact_offsets(const uint32_t* __restrict__ h_off, uint64_t H
 }  // namespace
 
 // ---- launchers -----------------------------------------------------------------
+#ifndef DPMRF_FUSED_MINB
+#define DPMRF_FUSED_MINB 8  // 8 x 256 threads per SM: caps the fused kernel at 32 registers
+#endif
 namespace {
+// The 2-label, <= 8-slot instance fits 32 registers without spilling, so it
+// runs 8 blocks per SM; the wider instances keep the compiler's choice.
+constexpr int fused_min_blocks(int mt, int kh) { return mt == 2 && kh == 8 ? DPMRF_FUSED_MINB : 1; }
+constexpr int kWinRegs = 3;  // window rows held in registers (default L = 3)
 template <int MT, int K>
 __global__ void __launch_bounds__(kVtxThreads)
     k_vertex_packed(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
@@ -1067,7 +1074,7 @@ __global__ void __launch_bounds__(kVtxThreads)
 template <int K>
 __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t);
 template <int MT, int KV, int KH>
-__global__ void __launch_bounds__(kVtxThreads)
+__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
                 uint32_t nh);
@@ -1270,6 +1277,17 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
       u[4 * q + 2] = w.z;
       u[4 * q + 3] = w.w;
     }
+    // The window rows are loaded up front, independent of the gathers, so a
+    // hood costs two dependent memory round trips (structure -> minima)
+    // rather than one more per window row: +4% at 16384^2.  (Measured and
+    // rejected: evict-first hints on the streamed structure and rows, two
+    // hoods per thread, and any variant that spills under the 32-register cap.)
+    const int R1 = a.ring;
+    const int nwin = t >= a.L ? a.L : 0;
+    double prev[kWinRegs];
+#pragma unroll
+    for (int i = 0; i < kWinRegs; ++i)
+      prev[i] = i < nwin ? a.hist[uint64_t((t - 1 - i) % R1) * a.Hs + h] : 0.0;
     double e[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {  // all gathers in flight before the fold
@@ -1282,18 +1300,14 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
       const uint32_t dk = (u[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
       if (dk != 0xFFFFu) sum = __dadd_rn(sum, e[k]);
     }
-    const int R1 = a.ring;
     a.hist[uint64_t(t % R1) * a.Hs + h] = sum;
-    int ok = 0;
-    if (t >= a.L) {
-      ok = 1;
-      for (int i = 1; i <= a.L; ++i) {
-        const double prev = a.hist[uint64_t((t - i) % R1) * a.Hs + h];
-        if (!(fabs(__dsub_rn(sum, prev)) < a.tol)) {
-          ok = 0;
-          break;
-        }
-      }
+    int ok = nwin > 0;
+#pragma unroll
+    for (int i = 0; i < kWinRegs; ++i)
+      if (i < nwin && !(fabs(__dsub_rn(sum, prev[i])) < a.tol)) ok = 0;
+    for (int i = kWinRegs; i < nwin; ++i) {  // windows longer than kWinRegs
+      const double p = a.hist[uint64_t((t - 1 - i) % R1) * a.Hs + h];
+      if (!(fabs(__dsub_rn(sum, p)) < a.tol)) ok = 0;
     }
     if (a.flags) a.flags[uint64_t(t) * a.Hs + h] = static_cast<uint8_t>(ok);
     not_conv = !ok;
@@ -1318,7 +1332,7 @@ __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) 
 // (labels into the buffer t-1 consumed, minima into the other half of the
 // double-buffered minima, label counts into the other parity slot).
 template <int MT, int KV, int KH>
-__global__ void __launch_bounds__(kVtxThreads)
+__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
                 uint32_t nh) {

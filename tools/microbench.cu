@@ -39,6 +39,28 @@ __global__ void grid_barriers(int iters, int* sink) {
   if (blockIdx.x == 0 && threadIdx.x == 0) sink[0] = iters;
 }
 
+// Hand-rolled grid barrier: one release-add per block on a monotone counter,
+// thread 0 spins with acquire loads until the counter reaches the epoch target.
+__device__ __forceinline__ void flag_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__global__ void flag_barriers(int iters, unsigned* ctr) {
+  for (int i = 0; i < iters; ++i) flag_barrier(ctr, (i + 1u) * gridDim.x);
+}
+
+__global__ void wide_empty(int* sink) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) sink[0] += 1;
+}
+
 __global__ void empty_kernel(int* sink) {
   if (threadIdx.x == 0 && blockIdx.x == 0) sink[0] += 1;
 }
@@ -82,6 +104,22 @@ int main() {
     cudaEventElapsedTime(&ms, a, b);
     printf("grid.sync with %d blocks x 256: %.2f us/barrier\n", blocks, ms * 1e3 / iters);
   }
+  unsigned* ctr;
+  cudaMalloc(&ctr, 64);
+  for (int blocks : {sms, 4 * sms, 8 * sms}) {
+    int iters = 1000;
+    cudaMemset(ctr, 0, 64);
+    void* args[] = {&iters, &ctr};
+    cudaLaunchCooperativeKernel((void*)flag_barriers, blocks, 256, args, 0, 0);
+    cudaMemset(ctr, 0, 64);
+    cudaEventRecord(a);
+    cudaLaunchCooperativeKernel((void*)flag_barriers, blocks, 256, args, 0, 0);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("flag barrier with %d blocks x 256: %.2f us/barrier\n", blocks, ms * 1e3 / iters);
+  }
   // 1000 dependent empty kernels captured in a graph
   cudaStream_t s;
   cudaStreamCreate(&s);
@@ -106,6 +144,22 @@ int main() {
   cudaEventSynchronize(b);
   cudaEventElapsedTime(&ms, a, b);
   printf("stream of 1000 tiny kernels: %.2f us/kernel\n", ms);
+  for (int blocks : {sms * 8, 1600}) {
+    cudaGraph_t g2;
+    cudaGraphExec_t ge2;
+    cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    for (int i = 0; i < 1000; ++i) wide_empty<<<blocks, 256, 0, s>>>(sink);
+    cudaStreamEndCapture(s, &g2);
+    cudaGraphInstantiate(&ge2, g2, 0);
+    cudaGraphLaunch(ge2, s);
+    cudaStreamSynchronize(s);
+    cudaEventRecord(a, s);
+    cudaGraphLaunch(ge2, s);
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    printf("graph of 1000 empty kernels x %d blocks x 256: %.2f us/kernel\n", blocks, ms);
+  }
   // host round trip: launch + sync of one tiny kernel + 8-byte D2H
   long long* hp;
   cudaMallocHost(&hp, 64);
