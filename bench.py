@@ -264,6 +264,90 @@ def run_stack(args, E, inputs, torch, world, rank, local, barrier, allmax, allsu
     return 0
 
 
+# ---- config D: one giant slice partitioned by vertex range across the ranks ----------------
+def run_partitioned(args, E, inputs, torch, dist, world, rank, local, barrier, allmax):
+    """Every rank holds the whole 16384^2 structure in HBM but owns a contiguous
+    vertex range and the hoods that follow it (csrc/partition.cu).  Per MAP
+    iteration the ranks exchange label and minima halos (grouped ncclSend/Recv),
+    per EM iteration they allgather labels + the last hood-energy row and repeat
+    the (bit-exact) M-step redundantly.  Total work is fixed: "strong" scaling."""
+    c = CONFIGS["D"]
+    seed = 42
+    t0 = time.perf_counter()
+    sl = inputs.synthetic_slice(c["size"], c["block"], brick=c["brick"], seed=seed)
+    build_inputs_s = time.perf_counter() - t0
+    R, A = sl.graph.num_vertices, len(sl.graph.neighbors)
+    ctx = E.Context(local)
+    ctx.set_graph(sl.graph)
+    ctx.build_neighborhoods(sl.cliques)
+    hoods = ctx.get_hoods()
+    H, S = hoods.size(), hoods.total_slots()
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(E.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        group = E.PartitionGroup.nccl(ctx, bytes(uid.cpu().numpy().tobytes()), rank, world)
+        parts = world
+    else:
+        group = E.PartitionGroup.local(ctx, args.local_parts)
+        parts = args.local_parts
+    info = group.info()
+    cfg = E.OptimizerConfig(num_labels=c["M"], em_max_iters=c["em"], map_max_iters=MAP_ITERS,
+                            rng_seed=seed)
+    labels_out = np.zeros(R, np.uint32)
+
+    def step():
+        return group.optimize(cfg, fixed_work=True, trace_level=E.TRACE_NONE, labels_out=labels_out)
+
+    for _ in range(args.warmup):
+        step()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    dev_ms, launches = [], 0
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        r = step()
+        dev_ms.append(r.stats["optimize_ms"])
+        launches += r.stats["kernel_launches"]
+    barrier()
+    clocks = sampler.stop()
+    total_dev_s = allmax(sum(dev_ms) / 1e3)
+    value = c["em"] * args.steps / total_dev_s
+    map_per_step = c["em"] * MAP_ITERS
+    line = {
+        "metric": METRIC, "value": value, "unit": "EM-iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_dev_s * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"config D: {c['desc']}; one slice (seed 42) partitioned by vertex "
+                               f"range into {parts} parts",
+                   "regions": R, "adjacency": A, "hoods": H, "slots": S, "labels": c["M"],
+                   "partitions": parts,
+                   "transport": "nccl (grouped send/recv halos, allreduce counters, allgather per EM)"
+                   if world > 1 else "local (all partitions on one device, device-copy halos)",
+                   "halo_bytes_per_map_rank0": info["halo_bytes_per_map"],
+                   "gather_bytes_per_em_rank0": info["gather_bytes_per_em"],
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "timing": "CUDA events on the library stream around each optimize(); "
+                             "max over ranks"},
+        "vertex_label_evals_per_s": c["M"] * S * map_per_step * args.steps / total_dev_s,
+        "unique_vertex_label_evals_per_s": c["M"] * R * map_per_step * args.steps / total_dev_s,
+        "gpu_launches": launches, "clocks": clocks,
+        "setup": {"input_build_s": build_inputs_s},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    group.close()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 # ---- our arm ---------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
@@ -275,6 +359,11 @@ def main():
     ap.add_argument("--slices-fixed", action="store_true",
                     help="config E: the stack is the fixed total (strong scaling)")
     ap.add_argument("--stack-threads", type=int, default=8)
+    ap.add_argument("--replicas", action="store_true",
+                    help="config D at N>1: independent replicas instead of one partitioned slice")
+    ap.add_argument("--local-parts", type=int, default=1,
+                    help="config D on one GPU: K vertex-range partitions in one context "
+                         "(the multi-GPU schedule with device-copy halos; diagnostic)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -316,6 +405,8 @@ def main():
 
     if args.config == "E":
         return run_stack(args, E, inputs, torch, world, rank, local, barrier, allmax, allsum)
+    if args.config == "D" and (world > 1 or args.local_parts > 1) and not args.replicas:
+        return run_partitioned(args, E, inputs, torch, dist, world, rank, local, barrier, allmax)
 
     c = CONFIGS[args.config]
     seed = 42 + rank

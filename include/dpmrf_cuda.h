@@ -139,6 +139,44 @@ dpmrf_status dpmrf_build_neighborhoods(dpmrf_context* ctx, uint64_t num_cliques,
 dpmrf_status dpmrf_get_hoods(dpmrf_context* ctx, uint64_t* num_hoods, uint64_t* num_slots,
                              uint32_t* offsets, uint32_t* members, uint32_t* source_clique);
 
+/* ---- device structure builders -------------- */
+/* build_region_graph, proj/include/dpmrf/graph/region_graph.hpp:31-33 /
+ * proj/src/graph/region_graph.cpp:10-73, ON THE DEVICE: `pixels` is the
+ * width x height u8 GrayImage (image.hpp), `region` the validated LabelMap's
+ * u32 region id per pixel (label_map.hpp), num_regions its region count.
+ * The graph (offsets, neighbors, region_mean, region_size) becomes the
+ * context's resident graph, as after dpmrf_set_graph.  Region id >=
+ * num_regions -> DPMRF_OUT_OF_RANGE; an unused id (map not validated) or
+ * num_regions == 0 -> DPMRF_INPUT_ERROR (region_graph.cpp:13-15).
+ * *num_adjacency (may be NULL) receives offsets[num_regions]. */
+dpmrf_status dpmrf_build_region_graph(dpmrf_context* ctx, uint32_t width, uint32_t height,
+                                      const uint8_t* pixels, const uint32_t* region,
+                                      uint32_t num_regions, uint64_t* num_adjacency);
+
+/* Copy the resident graph out (offsets: R+1, neighbors: A, region_mean: R,
+ * region_size: R -- only for a graph built by dpmrf_build_region_graph; any
+ * pointer may be NULL). */
+dpmrf_status dpmrf_get_graph(dpmrf_context* ctx, uint32_t* num_vertices, uint64_t* num_adjacency,
+                             uint32_t* offsets, uint32_t* neighbors, double* region_mean,
+                             uint32_t* region_size);
+
+/* enumerate_maximal_cliques, proj/include/dpmrf/graph/cliques.hpp:24-27 /
+ * proj/src/graph/cliques.cpp:53-106, ON THE DEVICE over the resident graph
+ * (which must satisfy RegionGraph's invariants: sorted, symmetric, no
+ * self-loops).  The CliqueSet stays resident for
+ * dpmrf_build_neighborhoods_resident; sizes go to *num_cliques /
+ * *num_members (may be NULL). */
+dpmrf_status dpmrf_enumerate_maximal_cliques(dpmrf_context* ctx, uint64_t* num_cliques,
+                                             uint64_t* num_members);
+
+/* Copy the resident cliques out (offsets: C+1, members: CS; either may be NULL). */
+dpmrf_status dpmrf_get_cliques(dpmrf_context* ctx, uint32_t* offsets, uint32_t* members);
+
+/* build_neighborhoods (as dpmrf_build_neighborhoods) from the resident
+ * cliques, with no host round trip of the CliqueSet. */
+dpmrf_status dpmrf_build_neighborhoods_resident(dpmrf_context* ctx, uint32_t k,
+                                                uint64_t* num_slots);
+
 /* ---- the optimization phase -------------------------------------------- */
 /* optimize, proj/include/dpmrf/mrf/engine.hpp:99-100 / proj/src/mrf/optimize.cpp:31-74,
  * over the resident graph and neighborhoods.  labels: R entries, mu/sigma:

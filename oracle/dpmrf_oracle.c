@@ -642,3 +642,212 @@ int orc_optimize_reference(uint32_t R, const uint32_t *g_off, const uint32_t *g_
   free(hist); free(em_hist); free(win);
   return rc;
 }
+
+/* ------------------------------------------------------------------ */
+/* Structure builders.                      */
+/* Outputs of variable length are malloc'd; release with orc_free.      */
+/* ------------------------------------------------------------------ */
+void orc_free(void *p) { free(p); }
+
+static int cmp_u64(const void *a, const void *b) {
+  const uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* build_region_graph, region_graph.cpp:10-73: directed (a,b) and (b,a) keys
+ * for every right / down pixel pair in different regions (:21-38), sorted,
+ * uniqued (:40-42), split by source into the CSR (:44-53); region sizes and
+ * integer intensity sums divided once per region (:57-71).  R == 0 ->
+ * INPUT_ERROR (:14); an id >= R -> OUT_OF_RANGE; an unused id (map not
+ * validated) -> INPUT_ERROR. */
+int orc_region_graph(uint32_t w, uint32_t h, const uint8_t *px, const uint32_t *reg, uint32_t R,
+                     uint32_t *off, uint32_t **nbr_out, uint64_t *A_out, double *mean,
+                     uint32_t *size) {
+  const uint64_t n = (uint64_t)w * h;
+  *nbr_out = NULL;
+  *A_out = 0;
+  if (R == 0) return ORC_INPUT_ERROR;
+  for (uint64_t i = 0; i < n; ++i)
+    if (reg[i] >= R) return ORC_OUT_OF_RANGE;
+  uint64_t cnt = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t x = (uint32_t)(i % w);
+    if (x + 1 < w && reg[i] != reg[i + 1]) cnt += 2;
+    if (i + w < n && reg[i] != reg[i + w]) cnt += 2;
+  }
+  uint64_t *keys = (uint64_t *)malloc((cnt ? cnt : 1) * sizeof(uint64_t));
+  uint64_t *sum = (uint64_t *)calloc(R, sizeof(uint64_t));
+  if (!keys || !sum) {
+    free(keys);
+    free(sum);
+    return ORC_NOMEM;
+  }
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t x = (uint32_t)(i % w);
+    if (x + 1 < w && reg[i] != reg[i + 1]) {
+      keys[k++] = ((uint64_t)reg[i] << 32) | reg[i + 1];
+      keys[k++] = ((uint64_t)reg[i + 1] << 32) | reg[i];
+    }
+    if (i + w < n && reg[i] != reg[i + w]) {
+      keys[k++] = ((uint64_t)reg[i] << 32) | reg[i + w];
+      keys[k++] = ((uint64_t)reg[i + w] << 32) | reg[i];
+    }
+  }
+  qsort(keys, cnt, sizeof(uint64_t), cmp_u64);
+  uint64_t A = 0;
+  for (uint64_t i = 0; i < cnt; ++i)
+    if (i == 0 || keys[i] != keys[i - 1]) keys[A++] = keys[i];
+  uint32_t *nbr = (uint32_t *)malloc((A ? A : 1) * sizeof(uint32_t));
+  if (!nbr) {
+    free(keys);
+    free(sum);
+    return ORC_NOMEM;
+  }
+  memset(off, 0, ((size_t)R + 1) * sizeof(uint32_t));
+  for (uint64_t i = 0; i < A; ++i) {
+    nbr[i] = (uint32_t)keys[i];
+    off[(keys[i] >> 32) + 1] += 1;
+  }
+  for (uint32_t v = 0; v < R; ++v) off[v + 1] += off[v];
+  memset(size, 0, (size_t)R * sizeof(uint32_t));
+  for (uint64_t i = 0; i < n; ++i) {
+    size[reg[i]] += 1;
+    sum[reg[i]] += px[i];
+  }
+  int rc = ORC_OK;
+  for (uint32_t r = 0; r < R; ++r) {
+    if (size[r] == 0) rc = ORC_INPUT_ERROR;
+    mean[r] = size[r] ? (double)sum[r] / (double)size[r] : 0.0;
+  }
+  free(keys);
+  free(sum);
+  if (rc) {
+    free(nbr);
+    return rc;
+  }
+  *nbr_out = nbr;
+  *A_out = A;
+  return ORC_OK;
+}
+
+/* growable u32 vector */
+typedef struct {
+  uint32_t *p;
+  uint64_t n, cap;
+} orc_vec;
+
+static int vec_push(orc_vec *v, uint32_t x) {
+  if (v->n == v->cap) {
+    const uint64_t c = v->cap ? 2 * v->cap : 64;
+    uint32_t *q = (uint32_t *)realloc(v->p, c * sizeof(uint32_t));
+    if (!q) return ORC_NOMEM;
+    v->p = q;
+    v->cap = c;
+  }
+  v->p[v->n++] = x;
+  return ORC_OK;
+}
+
+static int adj_has(const uint32_t *off, const uint32_t *nbr, uint32_t v, uint32_t u) {
+  for (uint32_t s = off[v]; s < off[v + 1]; ++s)
+    if (nbr[s] == u) return 1;
+  return 0;
+}
+
+/* canonical_sort comparison (cliques.cpp:33-38): lexicographic over mixed lengths */
+static const uint32_t *g_cl_mem;
+static const uint64_t *g_cl_off;
+static int cmp_clique(const void *a, const void *b) {
+  const uint64_t i = *(const uint64_t *)a, j = *(const uint64_t *)b;
+  const uint32_t *x = g_cl_mem + g_cl_off[i], *y = g_cl_mem + g_cl_off[j];
+  const uint64_t nx = g_cl_off[i + 1] - g_cl_off[i], ny = g_cl_off[j + 1] - g_cl_off[j];
+  for (uint64_t k = 0; k < nx && k < ny; ++k) {
+    if (x[k] < y[k]) return -1;
+    if (y[k] < x[k]) return 1;
+  }
+  return nx < ny ? -1 : (nx > ny ? 1 : 0);
+}
+
+/* enumerate_maximal_cliques, cliques.cpp:53-106: level k holds the k-cliques
+ * (stride k); common_neighbors (:16-27) = adjacency of member 0 intersected
+ * with every other member's; maximal iff empty (:91-96); children = members
+ * + each common neighbor above the last member (:82-89); canonical_sort of
+ * the emitted cliques (:30-49, :104). */
+int orc_maximal_cliques(uint32_t R, const uint32_t *off, const uint32_t *nbr, uint32_t **c_off_out,
+                        uint64_t *C_out, uint32_t **c_mem_out, uint64_t *CS_out) {
+  orc_vec out_mem = {0}, out_off = {0}, front = {0}, next = {0}, common = {0};
+  int rc = ORC_OK;
+  *c_off_out = *c_mem_out = NULL;
+  *C_out = *CS_out = 0;
+  for (uint32_t v = 0; v < R && !rc; ++v) rc = vec_push(&front, v);
+  rc = rc ? rc : vec_push(&out_off, 0);
+  for (uint64_t k = 1; front.n && !rc; ++k) {
+    const uint64_t fk = front.n / k;
+    next.n = 0;
+    for (uint64_t i = 0; i < fk && !rc; ++i) {
+      const uint32_t *m = front.p + i * k;
+      common.n = 0;
+      for (uint32_t s = off[m[0]]; s < off[m[0] + 1] && !rc; ++s) {
+        const uint32_t u = nbr[s];
+        int all = 1;
+        for (uint64_t j = 1; j < k && all; ++j) all = adj_has(off, nbr, m[j], u);
+        if (all) rc = vec_push(&common, u);
+      }
+      for (uint64_t c = 0; c < common.n && !rc; ++c) {
+        if (common.p[c] <= m[k - 1]) continue;
+        for (uint64_t j = 0; j < k && !rc; ++j) rc = vec_push(&next, m[j]);
+        if (!rc) rc = vec_push(&next, common.p[c]);
+      }
+      if (common.n == 0 && !rc) {
+        for (uint64_t j = 0; j < k && !rc; ++j) rc = vec_push(&out_mem, m[j]);
+        if (!rc) rc = vec_push(&out_off, (uint32_t)out_mem.n);
+      }
+    }
+    orc_vec t = front;
+    front = next;
+    next = t;
+  }
+  free(front.p);
+  free(next.p);
+  free(common.p);
+  if (rc) {
+    free(out_mem.p);
+    free(out_off.p);
+    return rc;
+  }
+  const uint64_t C = out_off.n - 1;
+  uint64_t *ord = (uint64_t *)malloc((C ? C : 1) * sizeof(uint64_t));
+  uint64_t *off64 = (uint64_t *)malloc((C + 1) * sizeof(uint64_t));
+  uint32_t *c_off = (uint32_t *)malloc((C + 1) * sizeof(uint32_t));
+  uint32_t *c_mem = (uint32_t *)malloc((out_mem.n ? out_mem.n : 1) * sizeof(uint32_t));
+  if (!ord || !off64 || !c_off || !c_mem) {
+    free(ord);
+    free(off64);
+    free(c_off);
+    free(c_mem);
+    free(out_mem.p);
+    free(out_off.p);
+    return ORC_NOMEM;
+  }
+  for (uint64_t c = 0; c <= C; ++c) off64[c] = out_off.p[c];
+  for (uint64_t c = 0; c < C; ++c) ord[c] = c;
+  g_cl_mem = out_mem.p;
+  g_cl_off = off64;
+  qsort(ord, C, sizeof(uint64_t), cmp_clique);
+  uint64_t pos = 0;
+  c_off[0] = 0;
+  for (uint64_t c = 0; c < C; ++c) {
+    for (uint64_t s = off64[ord[c]]; s < off64[ord[c] + 1]; ++s) c_mem[pos++] = out_mem.p[s];
+    c_off[c + 1] = (uint32_t)pos;
+  }
+  free(ord);
+  free(off64);
+  free(out_mem.p);
+  free(out_off.p);
+  *c_off_out = c_off;
+  *c_mem_out = c_mem;
+  *C_out = C;
+  *CS_out = pos;
+  return ORC_OK;
+}

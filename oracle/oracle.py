@@ -190,6 +190,12 @@ class _COracle:
         L.orc_update_parameters.argtypes = [U32, f64p, u32p, U32, f64p, f64p, f64p, f64p]
         L.orc_build_neighborhoods.argtypes = [U32, u32p, u32p, U64, u32p, u32p, U32, VP, VP, VP,
                                               ct.POINTER(U64)]
+        PU32 = ct.POINTER(ct.POINTER(ct.c_uint32))
+        L.orc_region_graph.argtypes = [U32, U32, u8p, u32p, U32, u32p, PU32, ct.POINTER(U64), f64p,
+                                       u32p]
+        L.orc_maximal_cliques.argtypes = [U32, u32p, u32p, PU32, ct.POINTER(U64), PU32,
+                                          ct.POINTER(U64)]
+        L.orc_free.argtypes = [VP]
         for fn in (L.orc_optimize, L.orc_optimize_reference):
             fn.argtypes = [U32, u32p, u32p, f64p, U64, u32p, u32p, ct.POINTER(Config), ct.c_int,
                            ct.c_int, u32p, f64p, f64p, ct.POINTER(_Trace)]
@@ -318,6 +324,35 @@ class _COracle:
         self._chk(rc, fn.__name__)
         return Result(lab, mu, sig, buf.trace(cfg, hoods.size))
 
+    def _take(self, p, n):
+        out = np.ctypeslib.as_array(p, shape=(max(n, 1),))[:n].copy() if n else \
+            np.zeros(0, np.uint32)
+        self.L.orc_free(ct.cast(p, VP))
+        return out
+
+    def region_graph(self, width, height, pixels, region, R):
+        """build_region_graph (region_graph.cpp:10-73) -> (Graph, region_size)."""
+        off = np.zeros(R + 1, np.uint32)
+        mean, size = np.zeros(max(R, 1)), np.zeros(max(R, 1), np.uint32)
+        nbr_p, A = ct.POINTER(ct.c_uint32)(), U64(0)
+        self._chk(self.L.orc_region_graph(width, height, _a(pixels, np.uint8), _a(region, np.uint32),
+                                          R, off, ct.byref(nbr_p), ct.byref(A), mean, size),
+                  "region_graph")
+        return Graph(off, self._take(nbr_p, A.value), mean[:R].copy()), size[:R].copy()
+
+    def maximal_cliques(self, g: Graph):
+        """enumerate_maximal_cliques (cliques.cpp:53-106) -> (offsets, members)."""
+        po, pm = ct.POINTER(ct.c_uint32)(), ct.POINTER(ct.c_uint32)()
+        C, CS = U64(0), U64(0)
+        nbr = _a(g.neighbors, np.uint32)
+        if len(nbr) == 0:
+            nbr = np.zeros(1, np.uint32)
+        self._chk(self.L.orc_maximal_cliques(g.num_vertices, _a(g.offsets, np.uint32), nbr,
+                                             ct.byref(po), ct.byref(C), ct.byref(pm),
+                                             ct.byref(CS)), "maximal_cliques")
+        off = self._take(po, C.value + 1)
+        return off, self._take(pm, CS.value)
+
     def optimize(self, g, hoods, cfg, fixed_work=False, allow_multilabel=False, full_trace=True):
         return self._run(self.L.orc_optimize, g, hoods, cfg, fixed_work, allow_multilabel,
                          full_trace)
@@ -430,6 +465,8 @@ class _Ref:
         L.ref_pipe_phantom.restype = VP
         L.ref_pipe_arrays.argtypes = [U32, u32p, u32p, f64p, U64, VP, VP, U64, VP, VP, ip]
         L.ref_pipe_arrays.restype = VP
+        L.ref_pipe_labelmap.argtypes = [U32, U32, u8p, u32p, U32, ct.c_int, ip]
+        L.ref_pipe_labelmap.restype = VP
         L.ref_pipe_free.argtypes = [VP]
         L.ref_pipe_sizes.argtypes = [VP, np.ctypeslib.ndpointer(np.uint64)]
         L.ref_pipe_times.argtypes = [VP, f64p]
@@ -490,6 +527,15 @@ class _Ref:
             h_mem.ctypes.data if h_mem is not None else None, ct.byref(st))
         if st.value:
             raise OracleError(st.value, "ref_pipe_arrays")
+        return Pipe(self, h)
+
+    def labelmap(self, width, height, pixels, region, num_regions, threads=1) -> Pipe:
+        """Graph, cliques and hoods of the caller's image + label map, by the reference."""
+        st = ct.c_int(0)
+        h = self.L.ref_pipe_labelmap(width, height, _a(pixels, np.uint8), _a(region, np.uint32),
+                                     num_regions, threads, ct.byref(st))
+        if st.value:
+            raise OracleError(st.value, "ref_pipe_labelmap")
         return Pipe(self, h)
 
     def hw_threads(self) -> int:

@@ -395,6 +395,39 @@ void* ref_pipe_arrays(std::uint32_t R, const std::uint32_t* g_off, const std::ui
   return p;
 }
 
+// Caller's image + label map (num_regions = the validated map's region
+// count): region graph, maximal cliques and neighborhoods by the reference.
+void* ref_pipe_labelmap(std::uint32_t w, std::uint32_t h, const std::uint8_t* pixels,
+                        const std::uint32_t* region, std::uint32_t num_regions, int threads,
+                        int* status) {
+  Pipe* p = new Pipe;
+  *status = guarded([&] {
+    const std::size_t n = std::size_t(w) * h;
+    p->image.width = w;
+    p->image.height = h;
+    p->image.pixels.assign(pixels, pixels + n);
+    p->map.width = w;
+    p->map.height = h;
+    p->map.region.assign(region, region + n);
+    p->map.num_regions = num_regions;
+    const auto b = backend_of(threads);
+    auto t0 = std::chrono::steady_clock::now();
+    p->graph = build_region_graph(b, p->image, p->map);
+    p->t_graph = secs(t0);
+    t0 = std::chrono::steady_clock::now();
+    p->cliques = enumerate_maximal_cliques(b, p->graph);
+    p->t_cliques = secs(t0);
+    t0 = std::chrono::steady_clock::now();
+    p->hoods = build_neighborhoods(b, p->graph, p->cliques);
+    p->t_hoods = secs(t0);
+  });
+  if (*status) {
+    delete p;
+    return nullptr;
+  }
+  return p;
+}
+
 void ref_pipe_free(void* h) { delete static_cast<Pipe*>(h); }
 
 // out: R, A, C, clique slots, H, S, width, height

@@ -66,6 +66,11 @@ CUDA_API = [
     ("dpmrf_set_hoods", ST, [VP, U64, VP, VP]),
     ("dpmrf_build_neighborhoods", ST, [VP, U64, VP, VP, U32, ct.POINTER(U64)]),
     ("dpmrf_get_hoods", ST, [VP, ct.POINTER(U64), ct.POINTER(U64), VP, VP, VP]),
+    ("dpmrf_build_region_graph", ST, [VP, U32, U32, VP, VP, U32, ct.POINTER(U64)]),
+    ("dpmrf_get_graph", ST, [VP, ct.POINTER(U32), ct.POINTER(U64), VP, VP, VP, VP]),
+    ("dpmrf_enumerate_maximal_cliques", ST, [VP, ct.POINTER(U64), ct.POINTER(U64)]),
+    ("dpmrf_get_cliques", ST, [VP, VP, VP]),
+    ("dpmrf_build_neighborhoods_resident", ST, [VP, U32, ct.POINTER(U64)]),
     ("dpmrf_optimize", ST, [VP, ct.POINTER(CConfig), ct.POINTER(CRunOptions), VP, VP, VP]),
     ("dpmrf_trace_info", ST, [VP, ct.POINTER(I32), ct.POINTER(U64)]),
     ("dpmrf_trace_em", ST, [VP, I32, ct.POINTER(I32), ct.POINTER(F64), ct.POINTER(ct.c_uint8),

@@ -217,6 +217,7 @@ extern "C" dpmrf_status dpmrf_set_graph(dpmrf_context* ctx, uint32_t R, const ui
     ctx->R = R;
     ctx->A = A;
     ctx->has_graph = true;
+    ctx->has_sizes = ctx->has_cliques = false;
     ctx->prepared = false;
     ++ctx->generation;
     ctx->sync();
@@ -280,6 +281,101 @@ extern "C" dpmrf_status dpmrf_get_hoods(dpmrf_context* ctx, uint64_t* H, uint64_
     ctx->sync();
     if (source_clique)
       for (uint64_t h = 0; h < ctx->H; ++h) source_clique[h] = static_cast<uint32_t>(h);
+  });
+}
+
+// ---- device structure builders (structure.cu) ------------------------------------
+extern "C" dpmrf_status dpmrf_build_region_graph(dpmrf_context* ctx, uint32_t w, uint32_t h,
+                                                 const uint8_t* pixels, const uint32_t* region,
+                                                 uint32_t R, uint64_t* num_adjacency) {
+  return guarded([&] {
+    need(ctx, DPMRF_INVALID_ARGUMENT, "null argument");
+    const uint64_t n = uint64_t(w) * h;
+    need(n == 0 || (pixels && region), DPMRF_INVALID_ARGUMENT, "null image or label map");
+    if (R == 0) fail(DPMRF_INPUT_ERROR, "region graph: label map not validated");
+    ctx->bind();
+    cudaStream_t st = ctx->stream;
+    uint8_t* px = ctx->img_px.ensure(n);
+    uint32_t* reg = ctx->img_reg.ensure(n);
+    if (n) {
+      CK(cudaMemcpyAsync(px, pixels, n, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(reg, region, n * 4, cudaMemcpyHostToDevice, st));
+    }
+    // the previous graph (and everything derived from it) is gone from here on
+    ctx->has_graph = ctx->has_sizes = ctx->has_cliques = ctx->has_hoods = false;
+    ctx->prepared = false;
+    ++ctx->generation;
+    build_region_graph_device(ctx, w, h, px, reg, R);
+    ctx->has_graph = ctx->has_sizes = true;
+    if (num_adjacency) *num_adjacency = ctx->A;
+  });
+}
+
+extern "C" dpmrf_status dpmrf_get_graph(dpmrf_context* ctx, uint32_t* R, uint64_t* A,
+                                        uint32_t* offsets, uint32_t* neighbors, double* mean,
+                                        uint32_t* size) {
+  return guarded([&] {
+    need(ctx && ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph");
+    need(!size || ctx->has_sizes, DPMRF_INVALID_ARGUMENT,
+         "region sizes exist only for a graph built by dpmrf_build_region_graph");
+    ctx->bind();
+    cudaStream_t st = ctx->stream;
+    if (R) *R = ctx->R;
+    if (A) *A = ctx->A;
+    if (offsets)
+      CK(cudaMemcpyAsync(offsets, ctx->g_off.get(), (uint64_t(ctx->R) + 1) * 4,
+                         cudaMemcpyDeviceToHost, st));
+    if (neighbors && ctx->A)
+      CK(cudaMemcpyAsync(neighbors, ctx->g_nbr.get(), ctx->A * 4, cudaMemcpyDeviceToHost, st));
+    if (mean && ctx->R)
+      CK(cudaMemcpyAsync(mean, ctx->g_mean.get(), uint64_t(ctx->R) * 8, cudaMemcpyDeviceToHost, st));
+    if (size && ctx->R)
+      CK(cudaMemcpyAsync(size, ctx->g_size.get(), uint64_t(ctx->R) * 4, cudaMemcpyDeviceToHost, st));
+    ctx->sync();
+  });
+}
+
+extern "C" dpmrf_status dpmrf_enumerate_maximal_cliques(dpmrf_context* ctx, uint64_t* C,
+                                                        uint64_t* CS) {
+  return guarded([&] {
+    need(ctx && ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph");
+    ctx->bind();
+    ctx->has_cliques = false;
+    enumerate_maximal_cliques_device(ctx);
+    ctx->has_cliques = true;
+    if (C) *C = ctx->C;
+    if (CS) *CS = ctx->CS;
+  });
+}
+
+extern "C" dpmrf_status dpmrf_get_cliques(dpmrf_context* ctx, uint32_t* offsets,
+                                          uint32_t* members) {
+  return guarded([&] {
+    need(ctx && ctx->has_cliques, DPMRF_INVALID_ARGUMENT, "no cliques enumerated");
+    ctx->bind();
+    if (offsets)
+      CK(cudaMemcpyAsync(offsets, ctx->c_off.get(), (ctx->C + 1) * 4, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    if (members && ctx->CS)
+      CK(cudaMemcpyAsync(members, ctx->c_mem.get(), ctx->CS * 4, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    ctx->sync();
+  });
+}
+
+extern "C" dpmrf_status dpmrf_build_neighborhoods_resident(dpmrf_context* ctx, uint32_t k,
+                                                           uint64_t* num_slots) {
+  return guarded([&] {
+    need(ctx, DPMRF_INVALID_ARGUMENT, "null argument");
+    if (k != 1) fail(DPMRF_INPUT_ERROR, "only 1-neighborhoods are supported");
+    need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
+    need(ctx->has_cliques, DPMRF_INVALID_ARGUMENT, "no cliques enumerated");
+    ctx->bind();
+    build_neighborhoods_from(ctx, ctx->C, ctx->c_off.get(), ctx->c_mem.get());
+    ctx->has_hoods = true;
+    ctx->prepared = false;
+    ++ctx->generation;
+    if (num_slots) *num_slots = ctx->S;
   });
 }
 

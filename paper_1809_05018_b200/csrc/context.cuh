@@ -17,6 +17,22 @@ struct dpmrf_context {
   dpmrf_b200::DevBuf<uint32_t> g_off, g_nbr;
   dpmrf_b200::DevBuf<double> g_mean;
 
+  // region_size (region_graph.hpp:23): known only when the graph was built
+  // on the device (dpmrf_build_region_graph); dpmrf_set_graph carries none.
+  bool has_sizes = false;
+  dpmrf_b200::DevBuf<uint32_t> g_size;
+
+  // ---- device structure builders (structure.cu) ----
+  // input image / label map of dpmrf_build_region_graph, and the resident
+  // maximal cliques (CliqueSet, cliques.hpp:14-22) of the current graph
+  bool has_cliques = false;
+  uint64_t C = 0, CS = 0;
+  dpmrf_b200::DevBuf<uint32_t> c_off, c_mem;
+  dpmrf_b200::DevBuf<uint8_t> img_px;
+  dpmrf_b200::DevBuf<uint32_t> img_reg;
+  dpmrf_b200::DevBuf<uint32_t> st_u32[6];
+  dpmrf_b200::DevBuf<unsigned long long> st_u64[2];
+
   // ---- resident neighborhoods (NeighborhoodSet, neighborhoods.hpp:15-23) ----
   bool has_hoods = false;
   uint64_t H = 0, S = 0;
@@ -156,4 +172,10 @@ void initial_params(uint32_t M, uint64_t seed, double* mu, double* sigma);  // i
 // hoods.cu
 void build_neighborhoods_device(dpmrf_context* ctx, uint64_t C, const uint32_t* c_off_host,
                                 const uint32_t* c_mem_host);
+void build_neighborhoods_from(dpmrf_context* ctx, uint64_t C, const uint32_t* c_off_dev,
+                              const uint32_t* c_mem_dev);
+// structure.cu
+void build_region_graph_device(dpmrf_context* ctx, uint32_t width, uint32_t height,
+                               const uint8_t* pixels_dev, const uint32_t* region_dev, uint32_t R);
+void enumerate_maximal_cliques_device(dpmrf_context* ctx);
 }  // namespace dpmrf_b200

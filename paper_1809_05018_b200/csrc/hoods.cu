@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "context.cuh"
+#include "segsort.cuh"
 
 namespace dpmrf_b200 {
 
@@ -26,7 +27,6 @@ namespace {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr uint32_t kSmemCap = 1024;  // candidates per warp in the shared-memory path
-constexpr uint32_t kPad = 0xFFFFFFFFu;
 
 __global__ void k_count_candidates(const uint32_t* __restrict__ c_off,
                                    const uint32_t* __restrict__ c_mem, uint64_t C,
@@ -62,32 +62,6 @@ __device__ __forceinline__ uint32_t candidate_at(const uint32_t* c_mem, uint32_t
     p -= 1 + deg;
   }
   return kPad;
-}
-
-__device__ __forceinline__ uint32_t warp_bitonic32(uint32_t x, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
-      const bool up = (lane & k) == 0;
-      const bool lower = (lane & j) == 0;
-      x = (lower == up) ? min(x, y) : max(x, y);
-    }
-  }
-  return x;
-}
-
-// Unique-compacts a sorted run held in lanes (chunk of 32); returns the
-// number written.  keep: lane holds a valid element.
-__device__ __forceinline__ uint32_t warp_unique_chunk(uint32_t x, bool valid, uint32_t prev_last,
-                                                      bool has_prev, uint32_t* out, int lane) {
-  uint32_t left = __shfl_up_sync(0xffffffffu, x, 1);
-  if (lane == 0) left = prev_last;
-  const bool keep = valid && ((lane == 0 && !has_prev) || x != left);
-  const unsigned mask = __ballot_sync(0xffffffffu, keep);
-  if (keep) out[__popc(mask & ((1u << lane) - 1u))] = x;
-  return __popc(mask);
 }
 
 // Sort + unique of every clique with <= kSmemCap candidates; larger ones are
@@ -127,29 +101,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   while (P < n) P <<= 1;
   for (uint32_t i = n + lane; i < P; i += 32) b[i] = kPad;
   __syncwarp();
-  for (uint32_t k = 2; k <= P; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = lane; i < P; i += 32) {
-        const uint32_t l = i ^ j;
-        if (l > i) {
-          const uint32_t xi = b[i], xl = b[l];
-          const bool asc = (i & k) == 0;
-          if ((xi > xl) == asc) {
-            b[i] = xl;
-            b[l] = xi;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
-  uint32_t written = 0, last = 0;
-  for (uint32_t base = 0; base < n; base += 32) {
-    const uint32_t i = base + lane;
-    const uint32_t x = i < n ? b[i] : kPad;
-    written += warp_unique_chunk(x, i < n, last, base > 0, out + written, lane);
-    last = __shfl_sync(0xffffffffu, x, 31);
-  }
+  bitonic_sort(b, P, lane, 32, [] { __syncwarp(); });
+  const uint32_t written = warp_unique_sorted(b, n, out, lane);
   if (lane == 0) uniq[c] = written;
 }
 
@@ -175,34 +128,11 @@ __global__ void __launch_bounds__(1024)
   }
   for (uint64_t i = n + threadIdx.x; i < P; i += blockDim.x) b[i] = kPad;
   __syncthreads();
-  for (uint64_t k = 2; k <= P; k <<= 1) {
-    for (uint64_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint64_t i = threadIdx.x; i < P; i += blockDim.x) {
-        const uint64_t l = i ^ j;
-        if (l > i) {
-          const uint32_t xi = b[i], xl = b[l];
-          const bool asc = (i & k) == 0;
-          if ((xi > xl) == asc) {
-            b[i] = xl;
-            b[l] = xi;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
+  bitonic_sort(b, P, threadIdx.x, blockDim.x, [] { __syncthreads(); });
   // unique, in order, by warp 0
   if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  uint32_t* out = scratch + cand_off[c];
-  uint32_t written = 0, last = 0;
-  for (uint32_t base = 0; base < n; base += 32) {
-    const uint32_t i = base + lane;
-    const uint32_t x = i < n ? b[i] : kPad;
-    written += warp_unique_chunk(x, i < n, last, base > 0, out + written, lane);
-    last = __shfl_sync(0xffffffffu, x, 31);
-  }
-  if (lane == 0) uniq[c] = written;
+  const uint32_t written = warp_unique_sorted(b, n, scratch + cand_off[c], threadIdx.x);
+  if (threadIdx.x == 0) uniq[c] = written;
 }
 
 __global__ void k_compact_members(const uint32_t* __restrict__ scratch,
@@ -226,6 +156,13 @@ void build_neighborhoods_device(dpmrf_context* ctx, uint64_t C, const uint32_t* 
   uint32_t* c_mem = ctx->tmp_u32[1].ensure(CS);
   CK(cudaMemcpyAsync(c_off, c_off_host, (C + 1) * 4, cudaMemcpyHostToDevice, st));
   if (CS) CK(cudaMemcpyAsync(c_mem, c_mem_host, CS * 4, cudaMemcpyHostToDevice, st));
+  build_neighborhoods_from(ctx, C, c_off, c_mem);
+}
+
+// Same, from device-resident cliques (e.g. dpmrf_enumerate_maximal_cliques).
+void build_neighborhoods_from(dpmrf_context* ctx, uint64_t C, const uint32_t* c_off,
+                              const uint32_t* c_mem) {
+  cudaStream_t st = ctx->stream;
   uint32_t* cnt = ctx->tmp_u32[2].ensure(C + 1);
   uint32_t* cand_off = ctx->tmp_u32[3].ensure(C + 1);
   uint32_t* err = ctx->prep_err.ensure(2);

@@ -226,6 +226,7 @@ class Context:
         self.R = 0
         self.H = 0
         self.S = 0
+        self._cliques_n = (0, 0)
 
     def close(self):
         if self.h:
@@ -273,6 +274,59 @@ class Context:
         _check(self._lib.dpmrf_get_hoods(self.h, None, None, N.ptr(off), N.ptr(mem), N.ptr(src)),
                "dpmrf_get_hoods")
         return NeighborhoodSet(off, mem, src)
+
+    # -- device structure builders --
+    def build_region_graph(self, width: int, height: int, pixels, region, num_regions: int) -> int:
+        """build_region_graph (region_graph.cpp:10-73) on the device from a u8
+        image and a validated u32 label map; the graph becomes resident.
+        Returns the adjacency length A."""
+        px = np.ascontiguousarray(pixels, np.uint8).reshape(-1)
+        reg = _u32(np.asarray(region).reshape(-1))
+        if len(px) != width * height or len(reg) != width * height:
+            raise InputError("region graph: image and label map dimensions differ")
+        A = ct.c_uint64(0)
+        _check(self._lib.dpmrf_build_region_graph(self.h, width, height, N.ptr(px), N.ptr(reg),
+                                                  num_regions, ct.byref(A)), "build_region_graph")
+        self.R = num_regions
+        self._graph_key = None
+        self._hoods_key = None
+        return A.value
+
+    def get_graph(self, sizes: bool = True) -> RegionGraph:
+        R, A = ct.c_uint32(0), ct.c_uint64(0)
+        _check(self._lib.dpmrf_get_graph(self.h, ct.byref(R), ct.byref(A), None, None, None, None),
+               "get_graph")
+        off = np.zeros(R.value + 1, np.uint32)
+        nbr = np.zeros(A.value, np.uint32)
+        mean = np.zeros(R.value)
+        size = np.zeros(R.value, np.uint32) if sizes else None
+        _check(self._lib.dpmrf_get_graph(self.h, None, None, N.ptr(off), N.ptr(nbr), N.ptr(mean),
+                                         N.ptr(size) if sizes else None), "get_graph")
+        return RegionGraph(off, nbr, mean, size)
+
+    def enumerate_maximal_cliques(self):
+        """enumerate_maximal_cliques (cliques.cpp:53-106) on the device over the
+        resident graph; the cliques stay resident.  Returns (C, members)."""
+        C, CS = ct.c_uint64(0), ct.c_uint64(0)
+        _check(self._lib.dpmrf_enumerate_maximal_cliques(self.h, ct.byref(C), ct.byref(CS)),
+               "enumerate_maximal_cliques")
+        self._cliques_n = (C.value, CS.value)
+        return C.value, CS.value
+
+    def get_cliques(self) -> CliqueSet:
+        C, CS = self._cliques_n
+        off = np.zeros(C + 1, np.uint32)
+        mem = np.zeros(CS, np.uint32)
+        _check(self._lib.dpmrf_get_cliques(self.h, N.ptr(off), N.ptr(mem)), "get_cliques")
+        return CliqueSet(off, mem)
+
+    def build_neighborhoods_resident(self, k: int = 1) -> int:
+        n = ct.c_uint64(0)
+        _check(self._lib.dpmrf_build_neighborhoods_resident(self.h, k, ct.byref(n)),
+               "build_neighborhoods_resident")
+        self.H, self.S = self._cliques_n[0], n.value
+        self._hoods_key = None
+        return n.value
 
     # -- the optimization phase --
     def optimize(self, config: OptimizerConfig, *, fixed_work=False, multilabel=None,
@@ -518,6 +572,24 @@ def optimize(backend: Backend, graph: RegionGraph, hoods: NeighborhoodSet,
     ctx = context_for(backend)
     _resident(ctx, graph, hoods)
     return ctx.optimize(config, **kw)
+
+
+def build_region_graph(backend: Backend, width: int, height: int, pixels, region,
+                       num_regions: int) -> RegionGraph:
+    """build_region_graph, region_graph.hpp:31-33 (GrayImage + LabelMap as arrays), on the device."""
+    ctx = context_for(backend)
+    ctx.build_region_graph(width, height, pixels, region, num_regions)
+    g = ctx.get_graph()
+    ctx._graph_key = g
+    return g
+
+
+def enumerate_maximal_cliques(backend: Backend, graph: RegionGraph) -> CliqueSet:
+    """enumerate_maximal_cliques, cliques.hpp:24-27 / cliques.cpp:53-106, on the device."""
+    ctx = context_for(backend)
+    _resident(ctx, graph)
+    ctx.enumerate_maximal_cliques()
+    return ctx.get_cliques()
 
 
 def build_neighborhoods(backend: Backend, graph: RegionGraph, cliques: CliqueSet,
