@@ -153,6 +153,13 @@ dpmrf_status dpmrf_build_region_graph(dpmrf_context* ctx, uint32_t width, uint32
                                       const uint8_t* pixels, const uint32_t* region,
                                       uint32_t num_regions, uint64_t* num_adjacency);
 
+/* Same, with pixels / region already in device memory of the context's
+ * device (no host copies; e.g. an image produced on the GPU). */
+dpmrf_status dpmrf_build_region_graph_device(dpmrf_context* ctx, uint32_t width, uint32_t height,
+                                             const uint8_t* pixels_dev,
+                                             const uint32_t* region_dev, uint32_t num_regions,
+                                             uint64_t* num_adjacency);
+
 /* Copy the resident graph out (offsets: R+1, neighbors: A, region_mean: R,
  * region_size: R -- only for a graph built by dpmrf_build_region_graph; any
  * pointer may be NULL). */

@@ -67,6 +67,7 @@ CUDA_API = [
     ("dpmrf_build_neighborhoods", ST, [VP, U64, VP, VP, U32, ct.POINTER(U64)]),
     ("dpmrf_get_hoods", ST, [VP, ct.POINTER(U64), ct.POINTER(U64), VP, VP, VP]),
     ("dpmrf_build_region_graph", ST, [VP, U32, U32, VP, VP, U32, ct.POINTER(U64)]),
+    ("dpmrf_build_region_graph_device", ST, [VP, U32, U32, VP, VP, U32, ct.POINTER(U64)]),
     ("dpmrf_get_graph", ST, [VP, ct.POINTER(U32), ct.POINTER(U64), VP, VP, VP, VP]),
     ("dpmrf_enumerate_maximal_cliques", ST, [VP, ct.POINTER(U64), ct.POINTER(U64)]),
     ("dpmrf_get_cliques", ST, [VP, VP, VP]),

@@ -311,6 +311,25 @@ extern "C" dpmrf_status dpmrf_build_region_graph(dpmrf_context* ctx, uint32_t w,
   });
 }
 
+extern "C" dpmrf_status dpmrf_build_region_graph_device(dpmrf_context* ctx, uint32_t w,
+                                                        uint32_t h, const uint8_t* pixels,
+                                                        const uint32_t* region, uint32_t R,
+                                                        uint64_t* num_adjacency) {
+  return guarded([&] {
+    need(ctx, DPMRF_INVALID_ARGUMENT, "null argument");
+    need(uint64_t(w) * h == 0 || (pixels && region), DPMRF_INVALID_ARGUMENT,
+         "null image or label map");
+    if (R == 0) fail(DPMRF_INPUT_ERROR, "region graph: label map not validated");
+    ctx->bind();
+    ctx->has_graph = ctx->has_sizes = ctx->has_cliques = ctx->has_hoods = false;
+    ctx->prepared = false;
+    ++ctx->generation;
+    build_region_graph_device(ctx, w, h, pixels, region, R);
+    ctx->has_graph = ctx->has_sizes = true;
+    if (num_adjacency) *num_adjacency = ctx->A;
+  });
+}
+
 extern "C" dpmrf_status dpmrf_get_graph(dpmrf_context* ctx, uint32_t* R, uint64_t* A,
                                         uint32_t* offsets, uint32_t* neighbors, double* mean,
                                         uint32_t* size) {

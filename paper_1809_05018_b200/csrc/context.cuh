@@ -1,6 +1,7 @@
 // context.cuh -- the opaque dpmrf_context behind the C ABI (internal).
 #pragma once
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -31,7 +32,9 @@ struct dpmrf_context {
   dpmrf_b200::DevBuf<uint8_t> img_px;
   dpmrf_b200::DevBuf<uint32_t> img_reg;
   dpmrf_b200::DevBuf<uint32_t> st_u32[6];
-  dpmrf_b200::DevBuf<unsigned long long> st_u64[2];
+  dpmrf_b200::DevBuf<unsigned long long> st_u64[3];
+  dpmrf_b200::DevBuf<uint32_t> cl_tmp[5];               // frontier x2, counts, flags, positions
+  std::vector<std::unique_ptr<dpmrf_b200::DevBuf<uint32_t>>> cl_level;  // maximal cliques per level
 
   // ---- resident neighborhoods (NeighborhoodSet, neighborhoods.hpp:15-23) ----
   bool has_hoods = false;

@@ -34,19 +34,104 @@ __global__ void k_count_candidates(const uint32_t* __restrict__ c_off,
                                    uint32_t* __restrict__ cnt, uint32_t* err,
                                    unsigned long long* max_cnt) {
   const uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= C) return;
   uint64_t n = 0;
-  for (uint32_t s = c_off[c]; s < c_off[c + 1]; ++s) {
-    const uint32_t m = c_mem[s];
-    if (m >= R) {
-      atomicOr(err, 1u);
-      cnt[c] = 0;
-      return;
+  if (c < C) {
+    bool bad = false;
+    for (uint32_t s = c_off[c]; s < c_off[c + 1]; ++s) {
+      const uint32_t m = c_mem[s];
+      if (m >= R) {
+        bad = true;
+        break;
+      }
+      n += 1 + (g_off[m + 1] - g_off[m]);
     }
-    n += 1 + (g_off[m + 1] - g_off[m]);
+    if (bad) {
+      atomicOr(err, 1u);
+      n = 0;
+    }
+    cnt[c] = static_cast<uint32_t>(n);
   }
-  cnt[c] = static_cast<uint32_t>(n);
-  atomicMax(max_cnt, static_cast<unsigned long long>(n));
+  // one atomic per warp (a single contended address otherwise serializes C atomics)
+  const uint32_t n32 = n > 0xFFFFFFFFull ? 0xFFFFFFFFu : uint32_t(n);
+  const uint32_t wmax = __reduce_max_sync(0xffffffffu, n32);
+  if ((threadIdx.x & 31) == 0 && wmax) atomicMax(max_cnt, static_cast<unsigned long long>(wmax));
+}
+
+// Hoods with <= G candidates (every grid / brick hood): G lanes per clique.
+// Lanes j < k load member j, its adjacency base and length; a segment scan
+// of the lengths places candidate l (members in order, each followed by its
+// neighbors, neighborhoods.cpp:31-36); the group sorts + uniques in
+// registers.  kPass 0 writes the unique counts, kPass 1 the members at the
+// scanned hood offsets -- no candidate scratch, no compaction pass.
+template <int G, int kPass>
+__global__ void __launch_bounds__(256)
+    k_hood_small(const uint32_t* __restrict__ c_off, const uint32_t* __restrict__ c_mem,
+                 uint64_t C, const uint32_t* __restrict__ g_off,
+                 const uint32_t* __restrict__ g_nbr, uint32_t* __restrict__ uniq,
+                 const uint32_t* __restrict__ h_off, uint32_t* __restrict__ members) {
+  const int lane = threadIdx.x & 31;
+  const int l = lane & (G - 1);
+  const uint64_t c = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+  const bool cv = c < C;
+  uint32_t lo = 0, k = 0;
+  if (cv) {
+    lo = c_off[c];
+    k = c_off[c + 1] - lo;  // <= candidates <= G
+  }
+  uint32_t m = 0, base = 0, len = 0;
+  if (cv && uint32_t(l) < k) {
+    m = c_mem[lo + l];
+    base = g_off[m];
+    len = 1 + (g_off[m + 1] - base);
+  }
+  uint32_t incl = len;
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o, G);
+    if (l >= o) incl += y;
+  }
+  const uint32_t start = incl - len;
+  const uint32_t kmax = __reduce_max_sync(0xffffffffu, k);
+  uint32_t x = kPad;
+  for (uint32_t j = 0; j < kmax; ++j) {
+    const uint32_t sj = __shfl_sync(0xffffffffu, start, j, G);
+    const uint32_t lj = __shfl_sync(0xffffffffu, len, j, G);
+    const uint32_t mj = __shfl_sync(0xffffffffu, m, j, G);
+    const uint32_t bj = __shfl_sync(0xffffffffu, base, j, G);
+    if (j < k && uint32_t(l) >= sj && uint32_t(l) < sj + lj)
+      x = uint32_t(l) == sj ? mj : g_nbr[bj + (uint32_t(l) - sj - 1)];
+  }
+  bool keep;
+  uint32_t rank;
+  const uint32_t u = group_sort_unique<G>(x, lane, keep, rank);
+  if (!cv) return;
+  if (kPass == 0) {
+    if (l == 0) uniq[c] = u;
+  } else if (keep) {
+    members[h_off[c] + rank] = x;
+  }
+}
+
+template <int G>
+void launch_hood_small(const uint32_t* c_off, const uint32_t* c_mem, uint64_t C,
+                       const uint32_t* g_off, const uint32_t* g_nbr, uint32_t* uniq,
+                       uint32_t* h_off, uint32_t* members, int pass, cudaStream_t st) {
+  const unsigned grid = grid_for(C * G, 256);
+  if (pass == 0)
+    k_hood_small<G, 0><<<grid, 256, 0, st>>>(c_off, c_mem, C, g_off, g_nbr, uniq, h_off, members);
+  else
+    k_hood_small<G, 1><<<grid, 256, 0, st>>>(c_off, c_mem, C, g_off, g_nbr, uniq, h_off, members);
+  CK_LAUNCH();
+}
+
+void hood_small(int G, const uint32_t* c_off, const uint32_t* c_mem, uint64_t C,
+                const uint32_t* g_off, const uint32_t* g_nbr, uint32_t* uniq, uint32_t* h_off,
+                uint32_t* members, int pass, cudaStream_t st) {
+  switch (G) {
+    case 8: launch_hood_small<8>(c_off, c_mem, C, g_off, g_nbr, uniq, h_off, members, pass, st); break;
+    case 16: launch_hood_small<16>(c_off, c_mem, C, g_off, g_nbr, uniq, h_off, members, pass, st); break;
+    default: launch_hood_small<32>(c_off, c_mem, C, g_off, g_nbr, uniq, h_off, members, pass, st); break;
+  }
 }
 
 // Position p of clique c's candidate list: member, then its neighbors, in
@@ -174,14 +259,33 @@ void build_neighborhoods_from(dpmrf_context* ctx, uint64_t C, const uint32_t* c_
                                                          ctx->R, cnt, err, maxc);
     CK_LAUNCH();
   }
-  exclusive_scan_u32(cnt, cand_off, C, cand_off + C, ctx->scan, st);
   uint32_t h_err = 0, h_total = 0;
   unsigned long long h_max = 0;
   CK(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&h_total, cand_off + C, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&h_max, maxc, 8, cudaMemcpyDeviceToHost, st));
   ctx->sync();
   if (h_err) fail(DPMRF_OUT_OF_RANGE, "build_neighborhoods: clique member >= num_vertices");
+  if (h_max <= 32) {  // every hood fits a lane group: two register passes, no scratch
+    const int G = h_max <= 8 ? 8 : (h_max <= 16 ? 16 : 32);
+    uint32_t* uniq = ctx->tmp_u32[5].ensure(C + 1);
+    uint32_t* h_off = ctx->h_off.ensure(C + 1);
+    if (C) hood_small(G, c_off, c_mem, C, ctx->g_off.get(), ctx->g_nbr.get(), uniq, h_off,
+                      nullptr, 0, st);
+    exclusive_scan_u32(uniq, h_off, C, h_off + C, ctx->scan, st);
+    uint32_t S = 0;
+    CK(cudaMemcpyAsync(&S, h_off + C, 4, cudaMemcpyDeviceToHost, st));
+    ctx->sync();
+    uint32_t* members = ctx->h_mem.ensure(S);
+    if (C) hood_small(G, c_off, c_mem, C, ctx->g_off.get(), ctx->g_nbr.get(), uniq, h_off,
+                      members, 1, st);
+    ctx->H = C;
+    ctx->S = S;
+    ctx->sync();
+    return;
+  }
+  exclusive_scan_u32(cnt, cand_off, C, cand_off + C, ctx->scan, st);
+  CK(cudaMemcpyAsync(&h_total, cand_off + C, 4, cudaMemcpyDeviceToHost, st));
+  ctx->sync();
   uint32_t* scratch = ctx->tmp_u32[4].ensure(h_total);
   uint32_t* uniq = ctx->tmp_u32[5].ensure(C + 1);
   if (C) {

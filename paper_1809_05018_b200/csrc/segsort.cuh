@@ -75,4 +75,32 @@ __device__ __forceinline__ uint32_t warp_unique_sorted(const uint32_t* b, uint32
   return written;
 }
 
+// Sort + unique of one short segment held by a G-lane group of the warp
+// (G in {2, 4, ..., 32}; every lane of the warp calls this; lane l = lane % G
+// holds key x, kPad for none).  Returns the segment's unique count; keep /
+// rank tell a lane whether and where (within the segment) its key goes.
+template <int G>
+__device__ __forceinline__ uint32_t group_sort_unique(uint32_t& x, int lane, bool& keep,
+                                                      uint32_t& rank) {
+  static_assert(G >= 2 && G <= 32 && (G & (G - 1)) == 0, "group width");
+  const int l = lane & (G - 1);
+#pragma unroll
+  for (int k = 2; k <= G; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool up = (l & k) == 0;
+      const bool lower = (l & j) == 0;
+      x = (lower == up) ? min(x, y) : max(x, y);
+    }
+  }
+  const uint32_t left = __shfl_up_sync(0xffffffffu, x, 1, G);
+  keep = x != kPad && (l == 0 || x != left);
+  const unsigned all = __ballot_sync(0xffffffffu, keep);
+  const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+  const unsigned seg = (all >> (lane & ~(G - 1))) & gmask;
+  rank = __popc(seg & ((1u << l) - 1u));
+  return __popc(seg);
+}
+
 }  // namespace dpmrf_b200

@@ -108,6 +108,9 @@ __global__ void __launch_bounds__(kTileThreads)
   __syncthreads();
   const uint32_t x = blockIdx.x * kTile + (tid & (kTile - 1));
   const uint32_t y = blockIdx.y * kTile + (tid / kTile);
+  // (Folding pixel runs with __match_any_sync before the shared-memory
+  // atomics measured slower: three warp matches per pixel cost more than
+  // the atomics they save.)
   unsigned long long k1 = kEmpty64, k2 = kEmpty64;
   if (x < w && y < h) {
     const uint64_t i = uint64_t(y) * w + x;
@@ -214,6 +217,49 @@ __global__ void __launch_bounds__(kSegWarps * 32)
   bitonic_sort(b, P, lane, 32, [] { __syncwarp(); });
   const uint32_t u = warp_unique_sorted(b, n, seg, lane);
   if (lane == 0) ucnt[v] = u;
+}
+
+// Buckets of <= G keys (every grid / brick region): G lanes per region sort +
+// unique in registers; kPass 0 -> unique counts, kPass 1 -> the neighbors at
+// the scanned offsets (no separate compaction).
+template <int G, int kPass>
+__global__ void __launch_bounds__(256)
+    k_bucket_small(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ off,
+                   uint32_t n_seg, uint32_t* __restrict__ ucnt,
+                   const uint32_t* __restrict__ out_off, uint32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int l = lane & (G - 1);
+  const uint64_t v = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+  uint32_t x = kPad;
+  if (v < n_seg) {
+    const uint32_t lo = off[v], n = off[v + 1] - lo;
+    if (uint32_t(l) < n) x = keys[lo + l];
+  }
+  bool keep;
+  uint32_t rank;
+  const uint32_t u = group_sort_unique<G>(x, lane, keep, rank);
+  if (v >= n_seg) return;
+  if (kPass == 0) {
+    if (l == 0) ucnt[v] = u;
+  } else if (keep) {
+    out[out_off[v] + rank] = x;
+  }
+}
+
+template <int G>
+void bucket_small(const uint32_t* keys, const uint32_t* off, uint32_t n, uint32_t* ucnt,
+                  const uint32_t* out_off, uint32_t* out, int pass, cudaStream_t st) {
+  const unsigned grid = grid_for(uint64_t(n) * G, 256);
+  if (pass == 0) k_bucket_small<G, 0><<<grid, 256, 0, st>>>(keys, off, n, ucnt, out_off, out);
+  else k_bucket_small<G, 1><<<grid, 256, 0, st>>>(keys, off, n, ucnt, out_off, out);
+  CK_LAUNCH();
+}
+
+__global__ void k_max_u32(const uint32_t* __restrict__ x, uint64_t n, uint32_t* __restrict__ out) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint32_t v = i < n ? x[i] : 0u;
+  const uint32_t m = __reduce_max_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
 // One block per long segment: bitonic sort in a power-of-two scratch slice.
@@ -520,19 +566,34 @@ void build_region_graph_device(dpmrf_context* ctx, uint32_t w, uint32_t h, const
   }
   exclusive_scan_u32(deg, boff, R, boff + R, ctx->scan, st);
   uint32_t* bucket = ctx->st_u32[3].ensure(2 * P);
+  uint32_t* dmax = err + 1;  // (err[1] is free scratch)
   if (P) {
     k_pair_fill<<<grid_for(P, 256), 256, 0, st>>>(pairs, P, boff, fill, bucket);
     CK_LAUNCH();
+    k_max_u32<<<grid_for(R, 256), 256, 0, st>>>(deg, R, dmax);
+    CK_LAUNCH();
   }
-  segmented_sort_unique(bucket, boff, R, ucnt, ctx->st_u32[4], st);
+  const uint32_t max_bucket = d2h(dmax, st);
   uint32_t* g_off = ctx->g_off.ensure(uint64_t(R) + 1);
+  const int G = max_bucket <= 8 ? 8 : (max_bucket <= 16 ? 16 : (max_bucket <= 32 ? 32 : 0));
+  auto small = [&](int pass, uint32_t* out) {
+    if (G == 8) bucket_small<8>(bucket, boff, R, ucnt, g_off, out, pass, st);
+    else if (G == 16) bucket_small<16>(bucket, boff, R, ucnt, g_off, out, pass, st);
+    else bucket_small<32>(bucket, boff, R, ucnt, g_off, out, pass, st);
+  };
+  if (G) small(0, nullptr);
+  else segmented_sort_unique(bucket, boff, R, ucnt, ctx->st_u32[4], st);
   exclusive_scan_u32(ucnt, g_off, R, g_off + R, ctx->scan, st);
   const uint64_t A = d2h(g_off + R, st);
   uint32_t* g_nbr = ctx->g_nbr.ensure(A);
   if (R) {
-    k_compact_segments<<<grid_for(uint64_t(R) * 32, 256), 256, 0, st>>>(bucket, boff, g_off, R,
-                                                                         g_nbr);
-    CK_LAUNCH();
+    if (G) {
+      small(1, g_nbr);
+    } else {
+      k_compact_segments<<<grid_for(uint64_t(R) * 32, 256), 256, 0, st>>>(bucket, boff, g_off,
+                                                                           R, g_nbr);
+      CK_LAUNCH();
+    }
     k_region_means<<<grid_for(R, 256), 256, 0, st>>>(rsize, rsum, R, ctx->g_mean.ensure(R), err);
     CK_LAUNCH();
   }
@@ -548,11 +609,19 @@ void enumerate_maximal_cliques_device(dpmrf_context* ctx) {
   const uint32_t R = ctx->R;
   const uint32_t* g_off = ctx->g_off.get();
   const uint32_t* g_nbr = ctx->g_nbr.get();
-  // per-level maximal cliques (owned here until the final merge)
-  std::vector<std::unique_ptr<DevBuf<uint32_t>>> lv_data;
+  // per-level maximal cliques (context scratch: no allocation once warm)
+  std::vector<uint32_t*> lv_data;
   std::vector<uint64_t> lv_count;
   std::vector<int> lv_k;
-  DevBuf<uint32_t> front[2], cnt, flag, pos;
+  DevBuf<uint32_t>* front = ctx->cl_tmp;  // [0], [1]
+  DevBuf<uint32_t>& cnt = ctx->cl_tmp[2];
+  DevBuf<uint32_t>& flag = ctx->cl_tmp[3];
+  DevBuf<uint32_t>& pos = ctx->cl_tmp[4];
+  auto level_buf = [&](uint64_t n) {
+    const size_t i = lv_data.size();
+    if (ctx->cl_level.size() <= i) ctx->cl_level.push_back(std::make_unique<DevBuf<uint32_t>>());
+    return ctx->cl_level[i]->ensure(n);
+  };
   if (R == 0) {
     ctx->C = ctx->CS = 0;
     CK(cudaMemsetAsync(ctx->c_off.ensure(1), 0, 4, st));
@@ -571,10 +640,10 @@ void enumerate_maximal_cliques_device(dpmrf_context* ctx) {
     const uint64_t n_max = d2h(p + R, st), n_next = d2h(c + R, st);
     if (n_max) {
       // isolated vertices: singleton cliques, already in order
-      auto d = std::make_unique<DevBuf<uint32_t>>();
-      k_clique_isolated<<<grid_for(R, 256), 256, 0, st>>>(R, f, p, d->ensure(n_max));
+      uint32_t* d = level_buf(n_max);
+      k_clique_isolated<<<grid_for(R, 256), 256, 0, st>>>(R, f, p, d);
       CK_LAUNCH();
-      lv_data.push_back(std::move(d));
+      lv_data.push_back(d);
       lv_count.push_back(n_max);
       lv_k.push_back(1);
     }
@@ -599,10 +668,10 @@ void enumerate_maximal_cliques_device(dpmrf_context* ctx) {
       exclusive_scan_u32(ff, pp, fk, pp + fk, ctx->scan, st);
       const uint64_t nm = d2h(pp + fk, st), nn = d2h(cc + fk, st);
       if (nm) {
-        auto d = std::make_unique<DevBuf<uint32_t>>();
-        k_clique_compact<<<grid_for(fk, 256), 256, 0, st>>>(F, fk, k, ff, pp, d->ensure(nm * k));
+        uint32_t* d = level_buf(nm * k);
+        k_clique_compact<<<grid_for(fk, 256), 256, 0, st>>>(F, fk, k, ff, pp, d);
         CK_LAUNCH();
-        lv_data.push_back(std::move(d));
+        lv_data.push_back(d);
         lv_count.push_back(nm);
         lv_k.push_back(k);
       }
@@ -622,7 +691,7 @@ void enumerate_maximal_cliques_device(dpmrf_context* ctx) {
   L.n = static_cast<int>(lv_data.size());
   uint64_t total = 0, members = 0;
   for (int i = 0; i < L.n; ++i) {
-    L.l[i] = LevelDesc{lv_data[i]->get(), lv_count[i], total, lv_k[i]};
+    L.l[i] = LevelDesc{lv_data[i], lv_count[i], total, lv_k[i]};
     total += lv_count[i];
     members += lv_count[i] * lv_k[i];
   }
@@ -631,8 +700,7 @@ void enumerate_maximal_cliques_device(dpmrf_context* ctx) {
   uint32_t* c_off = ctx->c_off.ensure(total + 1);
   uint32_t* c_mem = ctx->c_mem.ensure(members);
   if (total) {
-    DevBuf<unsigned long long> src;
-    unsigned long long* sa = src.ensure(total);
+    unsigned long long* sa = ctx->st_u64[2].ensure(total);
     k_clique_rank<<<grid_for(total, 256), 256, 0, st>>>(L, total, c_off, sa);
     CK_LAUNCH();
     exclusive_scan_u32(c_off, c_off, total, c_off + total, ctx->scan, st);

@@ -292,6 +292,19 @@ class Context:
         self._hoods_key = None
         return A.value
 
+    def build_region_graph_device(self, width: int, height: int, pixels_ptr: int,
+                                  region_ptr: int, num_regions: int) -> int:
+        """build_region_graph from device-resident u8 pixels / u32 region ids
+        (raw device pointers, e.g. torch tensors' data_ptr())."""
+        A = ct.c_uint64(0)
+        _check(self._lib.dpmrf_build_region_graph_device(self.h, width, height, pixels_ptr,
+                                                         region_ptr, num_regions, ct.byref(A)),
+               "build_region_graph_device")
+        self.R = num_regions
+        self._graph_key = None
+        self._hoods_key = None
+        return A.value
+
     def get_graph(self, sizes: bool = True) -> RegionGraph:
         R, A = ct.c_uint32(0), ct.c_uint64(0)
         _check(self._lib.dpmrf_get_graph(self.h, ct.byref(R), ct.byref(A), None, None, None, None),
