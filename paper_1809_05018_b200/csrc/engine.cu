@@ -1067,13 +1067,14 @@ namespace {
 // runs 8 blocks per SM; the wider instances keep the compiler's choice.
 constexpr int fused_min_blocks(int mt, int kh) { return mt == 2 && kh == 8 ? DPMRF_FUSED_MINB : 1; }
 constexpr int kWinRegs = 3;  // window rows held in registers (default L = 3)
+constexpr uint32_t kVertsPerThreadMin = 1u << 20;  // owned vertices for 2 per thread
 template <int MT, int K>
 __global__ void __launch_bounds__(kVtxThreads)
     k_vertex_packed(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                     int t);
 template <int K>
 __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t);
-template <int MT, int KV, int KH>
+template <int MT, int KV, int KH, int VP>
 __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
@@ -1085,14 +1086,25 @@ bool map_fused_supported(const MapArgs& a) { return a.adj_k && a.hood_k && !a.st
 void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
                       const double* minE_prev, double* minE_cur, int t, int map_max,
                       cudaStream_t s) {
-  const uint32_t nh = t >= 1 ? grid_for(a.h_end - a.h_begin, kHoodThreads) : 0u;
-  const uint32_t nv = t < map_max ? grid_for(a.v_end - a.v_begin, kVtxThreads) : 0u;
-  const dim3 g(nh + nv), blk(kVtxThreads);
   const int sel = (a.M == 2 ? 0 : 4) + (a.adj_k == 8 ? 2 : 0) + (a.hood_k == 16 ? 1 : 0);
-#define MF(MT, KV, KH) launch_pdl(k_map_fused<MT, KV, KH>, g, blk, 0, s, a, lab_in, lab_out, \
+  // Two vertices per thread on large graphs (+4% at 16384^2: more loads in
+  // flight per thread); one on small ones, where the extra per-thread
+  // latency shows (-3% at 2560^2).
+  const int vp = sel == 0 && a.v_end - a.v_begin >= kVertsPerThreadMin ? 2 : 1;
+  const uint32_t nh = t >= 1 ? grid_for(a.h_end - a.h_begin, kHoodThreads) : 0u;
+  const uint32_t nv =
+      t < map_max ? grid_for(a.v_end - a.v_begin, uint64_t(kVtxThreads) * vp) : 0u;
+  const dim3 g(nh + nv), blk(kVtxThreads);
+#define MF(MT, KV, KH) launch_pdl(k_map_fused<MT, KV, KH, 1>, g, blk, 0, s, a, lab_in, lab_out, \
                                   minE_prev, minE_cur, t, nh)
   switch (sel) {
-    case 0: MF(2, 4, 8); break;
+    case 0:
+      if (vp == 2)
+        launch_pdl(k_map_fused<2, 4, 8, 2>, g, blk, 0, s, a, lab_in, lab_out, minE_prev, minE_cur,
+                   t, nh);
+      else
+        MF(2, 4, 8);
+      break;
     case 1: MF(2, 4, 16); break;
     case 2: MF(2, 8, 8); break;
     case 3: MF(2, 8, 16); break;
@@ -1184,69 +1196,90 @@ __device__ __forceinline__ void load_i16(const int16_t* __restrict__ p, int16_t 
   }
 }
 
-template <int MT, int K>
+// Vertex pass over P vertices per thread (v, v + 256, ...: block blk covers
+// the P label tiles P*blk .. P*blk + P-1).  All structure loads of the P
+// vertices are issued before their label gathers.
+template <int MT, int K, int P = 1>
 __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
                                                    const uint8_t* __restrict__ lab_in,
                                                    uint8_t* __restrict__ lab_out,
                                                    double* __restrict__ minE, int t,
                                                    uint32_t blk) {
   const uint32_t M = MT > 0 ? uint32_t(MT) : a.M;
-  const uint32_t v = a.v_begin + blk * kVtxThreads + threadIdx.x;
-  const bool valid = v < a.v_end;
-  uint32_t nl = 0;
-  if (valid) {
-    int16_t d[K];
-    load_i16<K>(a.adj_pk + uint64_t(v) * K, d);
-    const uint8_t old = lab_in[v];
-    if (!a.cover[v]) {
-      lab_out[v] = old;
-      nl = old;
-    } else {
-      uint8_t nb[K];
-      uint32_t deg = 0;
+  const uint32_t v0 = a.v_begin + blk * (kVtxThreads * P) + threadIdx.x;
+  int16_t d[P][K];
+  uint8_t old[P], cov[P];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const bool ok = d[k] != INT16_MIN;
-        deg += ok;
-        nb[k] = ok ? lab_in[int64_t(v) + d[k]] : uint8_t(0xFF);
-      }
-      const double x = a.mean[v];
-      const double* T = a.terms;
-      double best;
-      uint32_t best_l;
-      if constexpr (MT == 2) {
-        uint32_t ones = 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) ones += (nb[k] == 1);
-        const double e0 = label_energy(x, T[0], T[2], T[4], a.beta, ones);
-        const double e1 = label_energy(x, T[1], T[3], T[5], a.beta, deg - ones);
-        best = e0;
-        best_l = 0;
-        if (e1 < best) {
-          best = e1;
-          best_l = 1;
-        }
-      } else {
-        best = 0.0;
-        best_l = 0;
-        for (uint32_t l = 0; l < M; ++l) {
-          uint32_t same = 0;
-#pragma unroll
-          for (int k = 0; k < K; ++k) same += (nb[k] == l);
-          const double e = label_energy(x, T[l], T[M + l], T[2 * M + l], a.beta, deg - same);
-          if (l == 0 || e < best) {
-            best = e;
-            best_l = l;
-          }
-        }
-      }
-      minE[v] = best;
-      lab_out[v] = static_cast<uint8_t>(best_l);
-      nl = best_l;
+  for (int j = 0; j < P; ++j) {
+    const uint32_t v = v0 + j * kVtxThreads;
+    if (v < a.v_end) {
+      load_i16<K>(a.adj_pk + uint64_t(v) * K, d[j]);
+      old[j] = lab_in[v];
+      cov[j] = a.cover[v];
     }
   }
-  if (a.tile_counts && blk < a.tiles)
-    block_label_counts(a.tile_counts + (uint64_t(t & 1) * a.tiles + blk) * M, M, valid, nl);
+  uint32_t nl[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const uint32_t v = v0 + j * kVtxThreads;
+    nl[j] = 0;
+    if (v >= a.v_end) continue;
+    if (!cov[j]) {
+      lab_out[v] = old[j];
+      nl[j] = old[j];
+      continue;
+    }
+    uint8_t nb[K];
+    uint32_t deg = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool ok = d[j][k] != INT16_MIN;
+      deg += ok;
+      nb[k] = ok ? lab_in[int64_t(v) + d[j][k]] : uint8_t(0xFF);
+    }
+    const double x = a.mean[v];
+    const double* T = a.terms;
+    double best;
+    uint32_t best_l;
+    if constexpr (MT == 2) {
+      uint32_t ones = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) ones += (nb[k] == 1);
+      const double e0 = label_energy(x, T[0], T[2], T[4], a.beta, ones);
+      const double e1 = label_energy(x, T[1], T[3], T[5], a.beta, deg - ones);
+      best = e0;
+      best_l = 0;
+      if (e1 < best) {
+        best = e1;
+        best_l = 1;
+      }
+    } else {
+      best = 0.0;
+      best_l = 0;
+      for (uint32_t l = 0; l < M; ++l) {
+        uint32_t same = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) same += (nb[k] == l);
+        const double e = label_energy(x, T[l], T[M + l], T[2 * M + l], a.beta, deg - same);
+        if (l == 0 || e < best) {
+          best = e;
+          best_l = l;
+        }
+      }
+    }
+    minE[v] = best;
+    lab_out[v] = static_cast<uint8_t>(best_l);
+    nl[j] = best_l;
+  }
+  if (a.tile_counts) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const uint32_t tile = blk * P + j;
+      if (tile < a.tiles)  // (uniform per block)
+        block_label_counts(a.tile_counts + (uint64_t(t & 1) * a.tiles + tile) * M, M,
+                           v0 + j * kVtxThreads < a.v_end, nl[j]);
+    }
+  }
 }
 
 template <int MT, int K>
@@ -1331,7 +1364,7 @@ __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) 
 // iteration, the speculative pass only wrote buffers nothing reads any more
 // (labels into the buffer t-1 consumed, minima into the other half of the
 // double-buffered minima, label counts into the other parity slot).
-template <int MT, int KV, int KH>
+template <int MT, int KV, int KH, int VP>
 __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
@@ -1342,7 +1375,7 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
     if (!map_iter_skipped(a.unconv, t - 1, a.fixed)) hood_packed_body<KH>(a, minE_prev, t - 1, blockIdx.x);
   } else {
     if (!map_iter_skipped(a.unconv, t > 0 ? t - 1 : 0, a.fixed))
-      vertex_packed_body<MT, KV>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh);
+      vertex_packed_body<MT, KV, VP>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh);
   }
 }
 

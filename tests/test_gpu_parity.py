@@ -233,3 +233,26 @@ def test_errors(ctx):
         ctx.init_random(3, 4, 0)
     with pytest.raises(ValueError):
         ctx.update_parameters([0, 0, 2, 1], E.LabelParams(np.zeros(2), np.ones(2)))
+
+
+def test_two_vertices_per_thread_path(ctx):
+    """R >= 2^20 switches the fused launch to two vertices per thread
+    (engine.cu kVertsPerThreadMin); it must equal the unfused two-kernel
+    path (one vertex per thread, pinned to the oracle above) bit for bit."""
+    from paper_1809_05018_b200 import inputs
+    sl = inputs.synthetic_slice(4096, 4, seed=21)
+    assert sl.graph.num_vertices >= 1 << 20
+    ctx.set_graph(sl.graph)
+    ctx.build_neighborhoods(sl.cliques)
+    for fixed in (True, False):
+        cfg = E.OptimizerConfig(em_max_iters=4, rng_seed=21)
+        a = ctx.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_FULL)
+        b = ctx.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_FULL, fused=False)
+        assert np.array_equal(a.labels, b.labels)
+        assert np.array_equal(a.mu, b.mu) and np.array_equal(a.sigma, b.sigma)
+        assert [e.total_energy for e in a.trace] == [e.total_energy for e in b.trace]
+        for ea, eb in zip(a.trace, b.trace):
+            assert len(ea.map_iters) == len(eb.map_iters)
+            for ma, mb in zip(ea.map_iters, eb.map_iters):
+                assert np.array_equal(ma.hood_energy, mb.hood_energy)
+                assert np.array_equal(ma.converged, mb.converged)
