@@ -527,10 +527,29 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       else
         CK(cudaEventRecord(ctx->ev_pool[i], st));
     };
+    // Device loop over the fused path on graphs whose M-step scatter fits
+    // the self-scanning kernel: the scatter joins the last fused launch and
+    // the EM bookkeeping joins the sq-pass tail -- 3 launches fewer per EM
+    // (no k_em_prologue / k_label_scatter_small / k_em_epilogue).
+    const bool merged = device_loop && fused && !a.flags && mstep_tail_fusable(R, M);
+    ScatterArgs sc{};
+    sc.mean = a.mean;
+    sc.counts = ctx->ms.counts.get();
+    sc.tiles = label_tiles(R);
+    sc.R = R;
+    sc.M = M;
+    sc.Hs = Hs;
+    sc.layout = ctx->ms.layout.get();
+    sc.x = ctx->ms.x.get();
+    if (merged)  // the MAP counters of the first EM (later ones are re-armed by the tail)
+      CK(cudaMemsetAsync(a.unconv, 0, map_max * sizeof(uint32_t), st));
     auto enqueue_em = [&](int parity) {
       uint64_t k = 0;
       size_t ev = 0;
-      if (device_loop) {
+      sc.lab_even = lab[parity];
+      sc.lab_odd = lab[parity ^ 1];
+      if (merged) {
+      } else if (device_loop) {
         launch_em_prologue(a.unconv, map_max, st);
         ++k;
       } else {
@@ -549,7 +568,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
           record(ev++);
           launch_map_fused(a, lab[(parity + t) & 1], lab[(parity + t + 1) & 1],
                            minE2 + uint64_t((t + 1) & 1) * half, minE2 + uint64_t(t & 1) * half,
-                           t, map_max, st);
+                           t, map_max, st, merged ? &sc : nullptr);
           k += 1;
         }
         record(ev++);
@@ -573,9 +592,11 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       }
       record(ev++);
       launch_mstep(a.mean, R, M, lab[parity], lab[parity ^ 1], a.hist, Hs, a.ring, a.unconv,
-                   map_max, fixed, params, em_out, ctx->ms, st, &k);
+                   map_max, fixed, params, em_out, ctx->ms, st, &k, /*counts_ready=*/true,
+                   /*scattered=*/merged, merged ? &ep : nullptr);
       record(ev++);
-      if (device_loop) {
+      if (merged) {
+      } else if (device_loop) {
         launch_em_epilogue(ep, st);
         ++k;
       } else {

@@ -491,21 +491,41 @@ __device__ __forceinline__ int executed_iters(const uint32_t* unconv, int map_ma
   return map_max;
 }
 
+// The same number, read while the hood pass of the last iteration is still
+// running (the tail blocks of the last fused launch): iteration map_max-1 ran
+// unless an earlier counter was zero, and the loop ends after it either way,
+// so its own (in-flight) counter is never needed.
+__device__ __forceinline__ int executed_iters_known(const uint32_t* unconv, int map_max,
+                                                    int fixed) {
+  if (fixed) return map_max;
+  for (int t = 0; t + 1 < map_max; ++t)
+    if (unconv[t] == 0) return t + 1;
+  return map_max;
+}
+
+template <bool kKnown = false>
+__device__ __forceinline__ int final_iters(const uint32_t* unconv, int map_max, int fixed) {
+  return kKnown ? executed_iters_known(unconv, map_max, fixed)
+                : executed_iters(unconv, map_max, fixed);
+}
+
+template <bool kKnown = false>
 __device__ __forceinline__ const uint8_t* final_labels(const uint8_t* even, const uint8_t* odd,
                                                        const uint32_t* unconv, int map_max,
                                                        int fixed) {
   if (!unconv) return even;
-  return (executed_iters(unconv, map_max, fixed) & 1) ? odd : even;
+  return (final_iters<kKnown>(unconv, map_max, fixed) & 1) ? odd : even;
 }
 
 // Counts of the final labels per 256-vertex tile: the buffer written by the
 // last executed vertex pass (iteration T-1 -> slot (T-1)&1), or slot 0 when
 // the counts were produced by k_label_tiles<0> (standalone update_parameters).
+template <bool kKnown = false>
 __device__ __forceinline__ const uint32_t* final_counts(const uint32_t* counts, uint32_t tiles,
                                                         uint32_t M, const uint32_t* unconv,
                                                         int map_max, int fixed) {
   if (!unconv) return counts;
-  const int T = executed_iters(unconv, map_max, fixed);
+  const int T = final_iters<kKnown>(unconv, map_max, fixed);
   return counts + uint64_t((T - 1) & 1) * tiles * M;
 }
 
@@ -557,22 +577,23 @@ __global__ void __launch_bounds__(kTileThreads)
 // One launch less per EM iteration where launches, not bytes, dominate.
 constexpr uint32_t kSelfScanMax = 8192;
 
-__global__ void __launch_bounds__(kTileThreads)
-    k_label_scatter_small(const uint8_t* lab_even, const uint8_t* lab_odd,
-                          const uint32_t* unconv, const uint32_t* count_sel, int map_max,
-                          int fixed, uint32_t R, uint32_t M, uint64_t Hs,
-                          const double* __restrict__ mean, const uint32_t* __restrict__ counts_buf,
-                          uint32_t tiles, uint32_t* __restrict__ layout, double* __restrict__ x) {
-  extern __shared__ uint32_t wcnt[];  // [warp][M] | base[M] | start[M] | red[kWarps]
-  pdl_wait();
+// smem: [kWarps x M] | base[M] | start[M] | red[2 kWarps]
+inline size_t scatter_small_smem(uint32_t M) {
+  return ((kTileThreads / 32) * M + 2 * M + 2 * (kTileThreads / 32)) * sizeof(uint32_t);
+}
+
+template <bool kKnown>
+__device__ __forceinline__ void label_scatter_small_body(
+    const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
+    const uint32_t* count_sel, int map_max, int fixed, uint32_t R, uint32_t M, uint64_t Hs,
+    const double* __restrict__ mean, const uint32_t* __restrict__ counts_buf, uint32_t tiles,
+    uint32_t* __restrict__ layout, double* __restrict__ x, uint32_t tile, uint32_t* wcnt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = kTileThreads / 32;
-  if (em_skipped(unconv)) return;
   uint32_t* base_s = wcnt + kWarps * M;
   uint32_t* start_s = base_s + M;
   uint32_t* red = start_s + M;
-  const uint32_t* tc = final_counts(counts_buf, tiles, M, count_sel, map_max, fixed);
-  const uint32_t tile = blockIdx.x;
+  const uint32_t* tc = final_counts<kKnown>(counts_buf, tiles, M, count_sel, map_max, fixed);
   for (uint32_t l = 0; l < M; ++l) {  // prefix (tiles before this one) and total of label l
     uint32_t pre = 0, tot = 0;
     for (uint32_t i = threadIdx.x; i < tiles; i += kTileThreads) {
@@ -602,7 +623,7 @@ __global__ void __launch_bounds__(kTileThreads)
     uint32_t s = 0, lf = 0;
     for (uint32_t l = 0; l < M; ++l) {
       const uint32_t n = start_s[l];
-      if (blockIdx.x == 0) {
+      if (tile == 0) {
         layout[l] = n;
         layout[M + l] = s;
         layout[2 * M + 1 + l] = lf;
@@ -611,13 +632,13 @@ __global__ void __launch_bounds__(kTileThreads)
       s += n;
       lf += (n + kFoldLeaf - 1) / kFoldLeaf;
     }
-    if (blockIdx.x == 0) {
+    if (tile == 0) {
       layout[2 * M] = s;
       layout[3 * M + 1] = lf;
       layout[3 * M + 2] = lf + uint32_t((Hs + kFoldLeaf - 1) / kFoldLeaf);
     }
   }
-  const uint8_t* lab = final_labels(lab_even, lab_odd, unconv, map_max, fixed);
+  const uint8_t* lab = final_labels<kKnown>(lab_even, lab_odd, unconv, map_max, fixed);
   for (uint32_t i = threadIdx.x; i < kWarps * M; i += kTileThreads) wcnt[i] = 0;
   __syncthreads();
   const uint64_t v = uint64_t(tile) * kTileVerts + threadIdx.x;
@@ -632,6 +653,19 @@ __global__ void __launch_bounds__(kTileThreads)
     for (int w = 0; w < warp; ++w) before += wcnt[w * M + l];
     x[start_s[l] + base_s[l] + before + rank_in_warp] = mean[v];
   }
+}
+
+__global__ void __launch_bounds__(kTileThreads)
+    k_label_scatter_small(const uint8_t* lab_even, const uint8_t* lab_odd,
+                          const uint32_t* unconv, const uint32_t* count_sel, int map_max,
+                          int fixed, uint32_t R, uint32_t M, uint64_t Hs,
+                          const double* __restrict__ mean, const uint32_t* __restrict__ counts_buf,
+                          uint32_t tiles, uint32_t* __restrict__ layout, double* __restrict__ x) {
+  extern __shared__ uint32_t wcnt[];
+  pdl_wait();
+  if (em_skipped(unconv)) return;
+  label_scatter_small_body<false>(lab_even, lab_odd, unconv, count_sel, map_max, fixed, R, M, Hs,
+                                  mean, counts_buf, tiles, layout, x, blockIdx.x, wcnt);
 }
 
 // Single block: per-label exclusive scan over tiles; label starts; leaf layout.
@@ -702,12 +736,55 @@ __device__ __forceinline__ uint32_t series_of(const uint32_t* leaf_start, uint32
 constexpr int kLeavesPerBlock = 8;
 constexpr int kLeafStride = kFoldLeaf + 1;
 
+// EM bookkeeping after the M-step (one warp): record the EM log, apply the
+// EM-level window (optimize.cpp:66-71) and write the next EM's label terms
+// with the device log (make_label_terms, model.hpp:48-60).  merged: called
+// from the sq-pass tail of the device-resident loop, which also stops the
+// loop directly and re-arms the MAP counters for the next EM (no separate
+// prologue / epilogue launches); otherwise the stop is left pending for
+// k_em_prologue.
+__device__ void em_record(const EmEpilogueArgs& a, bool merged) {
+  const int lane = threadIdx.x & 31;
+  const int T = executed_iters(a.unconv, a.map_max, a.fixed);
+  const uint32_t e = a.unconv[kEmCount];
+  const uint32_t M = a.M;
+  double* rec = a.em_rec + uint64_t(e) * (3 + 3 * M);
+  for (uint32_t l = lane; l < M; l += 32) {  // one lane per label evaluates the (long) device log
+    const double mu = a.em_out[2 + l], sg = a.em_out[2 + M + l];
+    const double ls = log_cr(sg);
+    rec[3 + l] = mu;
+    rec[3 + M + l] = sg;
+    rec[3 + 2 * M + l] = ls;
+    a.terms[l] = mu;
+    a.terms[M + l] = __dmul_rn(2.0, __dmul_rn(sg, sg));
+    a.terms[2 * M + l] = ls;
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  const double total = a.em_out[0];
+  a.em_hist[e] = total;
+  uint32_t conv = 0;
+  if (int(e) + 1 >= a.L + 1) {
+    conv = 1;
+    for (int i = 1; i <= a.L; ++i)
+      if (!(fabs(__dsub_rn(total, a.em_hist[e - i])) < a.tol)) conv = 0;
+  }
+  rec[0] = total;
+  rec[1] = static_cast<double>(T);
+  rec[2] = static_cast<double>(conv);
+  a.unconv[kEmCount] = e + 1;
+  if (conv && !a.fixed) a.unconv[merged ? kEmDone : kEmPending] = 1;
+  if (merged)
+    for (int t = 0; t < a.map_max; ++t) a.unconv[t] = 0;
+}
+
 template <bool kSq>
 __global__ void __launch_bounds__(256)
     k_leaf_fold(const double* __restrict__ x, const uint32_t* __restrict__ layout, uint32_t M,
                 const double* __restrict__ hist, uint64_t Hs, int ring,
                 const uint32_t* __restrict__ unconv, int map_max, int fixed, double* params,
-                double* partials, double* em_out, uint32_t* done) {
+                double* partials, double* em_out, uint32_t* done, EmEpilogueArgs ep,
+                int merged) {
   extern __shared__ double stage[];  // kLeavesPerBlock x kLeafStride
   pdl_wait();
   const uint32_t* n = layout;
@@ -799,6 +876,15 @@ __global__ void __launch_bounds__(256)
       partials[first + threadIdx.x] = acc;
     }
   }
+  if (kSq && merged) {
+    // device-resident loop: the next EM starts from buffer 0, so an odd
+    // number of MAP iterations leaves the committed labels to move back
+    if (executed_iters(unconv, map_max, fixed) & 1) {
+      const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+      for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < ep.R; v += stride)
+        ep.lab0[v] = ep.lab1[v];
+    }
+  }
   // ---- last block: trees + epilogue ----
   __shared__ bool last;
   __threadfence();
@@ -854,6 +940,7 @@ __global__ void __launch_bounds__(256)
       if (lane == 0) finish(w, cnt ? p[0] : 0.0);
     }
     __syncthreads();
+    if (kSq && merged && threadIdx.x < 32) em_record(ep, true);
     if (threadIdx.x == 0) *done = 0;  // re-arm the ticket for the next launch
     return;
   }
@@ -902,6 +989,7 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) finish(s, __ldcg(p));
     __syncthreads();
   }
+  if (kSq && merged && threadIdx.x < 32) em_record(ep, true);
   if (threadIdx.x == 0) *done = 0;  // re-arm the ticket for the next launch
 }
 
@@ -930,34 +1018,7 @@ __global__ void k_em_epilogue(EmEpilogueArgs a) {
       a.lab0[v] = a.lab1[v];
   }
   if (blockIdx.x != 0 || threadIdx.x >= 32) return;
-  // warp 0 of block 0: one lane per label evaluates the (long) device log
-  const uint32_t e = a.unconv[kEmCount];
-  const uint32_t M = a.M;
-  double* rec = a.em_rec + uint64_t(e) * (3 + 3 * M);
-  for (uint32_t l = threadIdx.x; l < M; l += 32) {
-    const double mu = a.em_out[2 + l], sg = a.em_out[2 + M + l];
-    const double ls = log_cr(sg);
-    rec[3 + l] = mu;
-    rec[3 + M + l] = sg;
-    rec[3 + 2 * M + l] = ls;
-    a.terms[l] = mu;
-    a.terms[M + l] = __dmul_rn(2.0, __dmul_rn(sg, sg));
-    a.terms[2 * M + l] = ls;
-  }
-  if (threadIdx.x != 0) return;
-  const double total = a.em_out[0];
-  a.em_hist[e] = total;
-  uint32_t conv = 0;
-  if (int(e) + 1 >= a.L + 1) {
-    conv = 1;
-    for (int i = 1; i <= a.L; ++i)
-      if (!(fabs(__dsub_rn(total, a.em_hist[e - i])) < a.tol)) conv = 0;
-  }
-  rec[0] = total;
-  rec[1] = static_cast<double>(T);
-  rec[2] = static_cast<double>(conv);
-  a.unconv[kEmCount] = e + 1;
-  if (conv && !a.fixed) a.unconv[kEmPending] = 1;
+  em_record(a, false);
 }
 
 // Partitioned optimize: this partition's share of the committed labels and of
@@ -1078,14 +1139,19 @@ template <int MT, int KV, int KH, int VP>
 __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
-                uint32_t nh);
+                uint32_t nh, uint32_t nv, ScatterArgs sc);
 }  // namespace
 
 bool map_fused_supported(const MapArgs& a) { return a.adj_k && a.hood_k && !a.staged; }
 
+bool mstep_tail_fusable(uint32_t R, uint32_t M) {
+  const uint64_t tiles = (uint64_t(R) + kTileVerts - 1) / kTileVerts;
+  return tiles && tiles * M <= kSelfScanMax;
+}
+
 void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
                       const double* minE_prev, double* minE_cur, int t, int map_max,
-                      cudaStream_t s) {
+                      cudaStream_t s, const ScatterArgs* sc) {
   const int sel = (a.M == 2 ? 0 : 4) + (a.adj_k == 8 ? 2 : 0) + (a.hood_k == 16 ? 1 : 0);
   // Two vertices per thread on large graphs (+4% at 16384^2: more loads in
   // flight per thread); one on small ones, where the extra per-thread
@@ -1094,14 +1160,18 @@ void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
   const uint32_t nh = t >= 1 ? grid_for(a.h_end - a.h_begin, kHoodThreads) : 0u;
   const uint32_t nv =
       t < map_max ? grid_for(a.v_end - a.v_begin, uint64_t(kVtxThreads) * vp) : 0u;
-  const dim3 g(nh + nv), blk(kVtxThreads);
-#define MF(MT, KV, KH) launch_pdl(k_map_fused<MT, KV, KH, 1>, g, blk, 0, s, a, lab_in, lab_out, \
-                                  minE_prev, minE_cur, t, nh)
+  const bool tail = sc && t == map_max;
+  const uint32_t ns = tail ? sc->tiles : 0u;
+  const ScatterArgs scv = tail ? *sc : ScatterArgs{};
+  const size_t smem = tail ? scatter_small_smem(sc->M) : 0;
+  const dim3 g(nh + nv + ns), blk(kVtxThreads);
+#define MF(MT, KV, KH) launch_pdl(k_map_fused<MT, KV, KH, 1>, g, blk, smem, s, a, lab_in, lab_out, \
+                                  minE_prev, minE_cur, t, nh, nv, scv)
   switch (sel) {
     case 0:
       if (vp == 2)
-        launch_pdl(k_map_fused<2, 4, 8, 2>, g, blk, 0, s, a, lab_in, lab_out, minE_prev, minE_cur,
-                   t, nh);
+        launch_pdl(k_map_fused<2, 4, 8, 2>, g, blk, smem, s, a, lab_in, lab_out, minE_prev,
+                   minE_cur, t, nh, nv, scv);
       else
         MF(2, 4, 8);
       break;
@@ -1368,11 +1438,21 @@ template <int MT, int KV, int KH, int VP>
 __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
-                uint32_t nh) {
+                uint32_t nh, uint32_t nv, ScatterArgs sc) {
   static_assert(kVtxThreads == kHoodThreads, "one block shape for both passes");
+  static_assert(kVtxThreads == kTileThreads, "scatter tiles are vertex blocks");
+  extern __shared__ uint32_t fused_smem[];
   pdl_wait();
   if (blockIdx.x < nh) {
     if (!map_iter_skipped(a.unconv, t - 1, a.fixed)) hood_packed_body<KH>(a, minE_prev, t - 1, blockIdx.x);
+  } else if (blockIdx.x >= nh + nv) {
+    // last launch (t = map_max): the M-step's label scatter runs beside the
+    // hood pass of the last iteration -- it reads only the committed labels
+    // and label counts of the last vertex pass (see executed_iters_known)
+    if (!em_skipped(a.unconv))
+      label_scatter_small_body<true>(sc.lab_even, sc.lab_odd, a.unconv, a.unconv, t, a.fixed,
+                                     sc.R, sc.M, sc.Hs, sc.mean, sc.counts, sc.tiles, sc.layout,
+                                     sc.x, blockIdx.x - nh - nv, fused_smem);
   } else {
     if (!map_iter_skipped(a.unconv, t > 0 ? t - 1 : 0, a.fixed))
       vertex_packed_body<MT, KV, VP>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh);
@@ -1498,7 +1578,8 @@ namespace {
 void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
                 const uint8_t* lab_odd, const uint32_t* unconv, int map_max, int fixed,
                 const double* hist, uint64_t Hs, int ring, double* params, double* em_out,
-                MStepBuffers& mb, cudaStream_t s, uint64_t* launches, bool counts_ready) {
+                MStepBuffers& mb, cudaStream_t s, uint64_t* launches, bool counts_ready,
+                bool scattered, const EmEpilogueArgs* ep) {
   mstep_reserve(mb, R, M, Hs);
   const uint32_t tiles = static_cast<uint32_t>((uint64_t(R) + kTileVerts - 1) / kTileVerts);
   uint32_t* counts = mb.counts.get();
@@ -1510,16 +1591,18 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
   double* partials = mb.partials.get();
   const size_t smem = (kTileThreads / 32) * M * sizeof(uint32_t);
   uint64_t n = 0;
-  if (tiles && !counts_ready) {
+  if (scattered) {
+    // the grouping already ran beside the last hood pass (launch_map_fused)
+  } else if (tiles && !counts_ready) {
     k_label_tiles<0><<<tiles, kTileThreads, smem, s>>>(lab_even, lab_odd, unconv, map_max, fixed,
                                                        R, M, mean, counts, nullptr, nullptr,
                                                        nullptr);
     CK_LAUNCH();
     ++n;
   }
-  if (tiles && uint64_t(tiles) * M <= kSelfScanMax) {
-    const size_t smem_s = ((kTileThreads / 32) * M + 2 * M + 2 * (kTileThreads / 32)) *
-                          sizeof(uint32_t);
+  if (scattered) {
+  } else if (tiles && uint64_t(tiles) * M <= kSelfScanMax) {
+    const size_t smem_s = scatter_small_smem(M);
     launch_pdl(k_label_scatter_small, dim3(tiles), dim3(kTileThreads), smem_s, s, lab_even,
                lab_odd, unconv, counts_ready ? unconv : (const uint32_t*)nullptr, map_max, fixed,
                R, M, Hs, mean, (const uint32_t*)counts, tiles, layout, x);
@@ -1529,7 +1612,7 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
                counts_ready ? unconv : nullptr, map_max, fixed, tile_base, tiles, M, Hs, layout);
     ++n;
   }
-  if (tiles && uint64_t(tiles) * M > kSelfScanMax) {
+  if (!scattered && tiles && uint64_t(tiles) * M > kSelfScanMax) {
     launch_pdl(k_label_tiles<1>, dim3(tiles), dim3(kTileThreads), smem, s, lab_even, lab_odd,
                unconv, map_max, fixed, R, M, mean, (uint32_t*)nullptr,
                (const uint32_t*)tile_base, (const uint32_t*)layout, x);
@@ -1545,12 +1628,13 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
     smem_set = true;
   }
   const unsigned lg = grid_for(max_leaves, kLeavesPerBlock);
+  const EmEpilogueArgs epv = ep ? *ep : EmEpilogueArgs{};
   launch_pdl(k_leaf_fold<false>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
              (const uint32_t*)layout, M, hist, Hs, ring, unconv, map_max, fixed, params, partials,
-             em_out, mb.done.get());
+             em_out, mb.done.get(), epv, 0);
   launch_pdl(k_leaf_fold<true>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
              (const uint32_t*)layout, M, (const double*)nullptr, uint64_t(0), 1, unconv, map_max,
-             fixed, params, partials, em_out, mb.done.get() + 1);
+             fixed, params, partials, em_out, mb.done.get() + 1, epv, ep ? 1 : 0);
   n += 2;
   if (launches) *launches += n;
 }
@@ -1564,9 +1648,10 @@ uint32_t label_tiles(uint32_t R) {
 void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_even,
                   const uint8_t* lab_odd, const double* hist, uint64_t Hs, int ring,
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
-                  MStepBuffers& mb, cudaStream_t s, uint64_t* launches, bool counts_ready) {
+                  MStepBuffers& mb, cudaStream_t s, uint64_t* launches, bool counts_ready,
+                  bool scattered, const EmEpilogueArgs* ep) {
   mstep_core(mean, R, M, lab_even, lab_odd, unconv, map_max, fixed, hist, Hs, ring, params,
-             em_out, mb, s, launches, counts_ready);
+             em_out, mb, s, launches, counts_ready, scattered, ep);
 }
 
 void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s) {
@@ -1626,7 +1711,7 @@ void launch_update_parameters_u32(const double* mean, uint32_t R, uint32_t M,
   if (R == 0) return;
   double* eo = mb.em_scratch.ensure(2 + 2 * M);
   mstep_core(mean, R, M, lab, lab, nullptr, 1, 1, nullptr, 0, 1, params, eo, mb, s, nullptr,
-             /*counts_ready=*/false);
+             /*counts_ready=*/false, /*scattered=*/false, nullptr);
 }
 
 void launch_init_labels(uint8_t* lab, uint32_t R, uint32_t M, uint64_t seed, cudaStream_t s) {

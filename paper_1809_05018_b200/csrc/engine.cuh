@@ -62,9 +62,42 @@ void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s);
 // the minima are double-buffered by iteration parity (minE_cur = vertex
 // output of t, minE_prev = that of t-1).
 bool map_fused_supported(const MapArgs& a);
+struct EmEpilogueArgs {
+  uint32_t* unconv;
+  int map_max;
+  int fixed;
+  int L;
+  double tol;
+  uint8_t* lab0;
+  const uint8_t* lab1;
+  uint32_t R;
+  uint32_t M;
+  const double* em_out;  // [total, T, mu(M), sigma(M)] of this EM's M-step
+  double* em_hist;       // em_max totals
+  double* em_rec;        // em_max x (3 + 3M): total, T, conv, mu, sigma, device log(sigma)
+  double* terms;         // next EM's [mu | 2 sigma^2 | log sigma]
+};
+
+// The M-step's stable grouping of region means by label, run by the extra
+// blocks of the last fused MAP launch (t = map_max) on graphs whose label
+// tiles fit the self-scanning scatter (mstep_tail_fusable).
+struct ScatterArgs {
+  const double* mean;
+  const uint8_t* lab_even;
+  const uint8_t* lab_odd;
+  const uint32_t* counts;  // 2 x tiles x M (by MAP-iteration parity)
+  uint32_t tiles;
+  uint32_t R;
+  uint32_t M;
+  uint64_t Hs;
+  uint32_t* layout;
+  double* x;
+};
+bool mstep_tail_fusable(uint32_t R, uint32_t M);
+
 void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
                       const double* minE_prev, double* minE_cur, int t, int map_max,
-                      cudaStream_t s);
+                      cudaStream_t s, const ScatterArgs* sc = nullptr);
 // The whole MAP loop of one EM iteration as one cooperative kernel (see engine.cu).
 void launch_map_loop(const MapArgs& a, uint8_t* lab_even, uint8_t* lab_odd, double* minE0,
                      double* minE1, int map_max, cudaStream_t s);
@@ -88,25 +121,12 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
                   const uint8_t* lab_odd, const double* hist, uint64_t Hs, int ring,
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches,
-                  bool counts_ready = true);
+                  bool counts_ready = true, bool scattered = false,
+                  const EmEpilogueArgs* ep = nullptr);
 
 // Device-resident EM loop (see engine.cu).  unconv points 4 words into its
 // allocation: [em_done, pending_done, em_count, pad | unconv[map_max]].
-struct EmEpilogueArgs {
-  uint32_t* unconv;
-  int map_max;
-  int fixed;
-  int L;
-  double tol;
-  uint8_t* lab0;
-  const uint8_t* lab1;
-  uint32_t R;
-  uint32_t M;
-  const double* em_out;  // [total, T, mu(M), sigma(M)] of this EM's M-step
-  double* em_hist;       // em_max totals
-  double* em_rec;        // em_max x (3 + 3M): total, T, conv, mu, sigma, device log(sigma)
-  double* terms;         // next EM's [mu | 2 sigma^2 | log sigma]
-};
+
 void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s);
 void launch_em_epilogue(const EmEpilogueArgs& a, cudaStream_t s);
 // Partitioned optimize: own vertex / series range of the final labels and of
