@@ -432,8 +432,8 @@ def main():
         return ctx.optimize(cfg, fixed_work=True, multilabel=c["M"] != 2,
                             trace_level=E.TRACE_NONE, kernel_timing=timing, labels_out=labels_out)
 
-    for _ in range(args.warmup):
-        step()
+    for _ in range(args.warmup):  # the timed configuration (graphs captured here, not timed)
+        step(timing=False)
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
