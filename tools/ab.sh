@@ -3,7 +3,7 @@
 #   bash tools/ab.sh OUTDIR "B D" base hoist ...      (runs on the GPU box)
 O=$1; CFGS=$2; shift 2
 mkdir -p $O
-for round in 1 2; do
+for round in 1 2 3; do
 for v in "$@"; do
   for c in $CFGS; do
     steps=10; [ "$c" = D ] && steps=5
