@@ -104,6 +104,18 @@ int main() {
     cudaEventElapsedTime(&ms, a, b);
     printf("grid.sync with %d blocks x 256: %.2f us/barrier\n", blocks, ms * 1e3 / iters);
   }
+  for (int threads : {512, 1024}) {
+    int iters = 1000;
+    void* args[] = {&iters, &sink};
+    cudaLaunchCooperativeKernel((void*)grid_barriers, sms, threads, args, 0, 0);
+    cudaEventRecord(a);
+    cudaLaunchCooperativeKernel((void*)grid_barriers, sms, threads, args, 0, 0);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("grid.sync with %d blocks x %d: %.2f us/barrier\n", sms, threads, ms * 1e3 / iters);
+  }
   unsigned* ctr;
   cudaMalloc(&ctr, 64);
   for (int blocks : {sms, 4 * sms, 8 * sms}) {
