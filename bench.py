@@ -11,8 +11,9 @@ neighborhoods are resident in HBM.  Each rank processes its own slice
 value  = EM iterations of all ranks / max-over-ranks device time (CUDA events
          on the library's stream, L2 flushed between steps)
 e2e    = the same metric through the public C ABI with host (pinned) buffers:
-         dpmrf_set_graph + dpmrf_set_hoods + dpmrf_optimize per step, host
-         wall clock, H2D of the inputs and D2H of labels/params included.
+         one dpmrf_optimize_arrays call per step (optimize(graph, hoods,
+         config), engine.hpp:99-100), host wall clock, H2D of the graph and
+         hoods and D2H of labels/params included.
 --impl reference times the reference's own CPU implementation (oracle/_ref,
 compiled from /root/reference by oracle/Makefile) on this host's cores.
 """
@@ -482,10 +483,9 @@ def main():
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ctx.set_graph(g_pin)
-        ctx.set_hoods(h_pin)
-        ctx.optimize(cfg, fixed_work=True, multilabel=c["M"] != 2, trace_level=E.TRACE_NONE,
-                     labels_out=lab_pin)
+        # the reference-facing call: optimize(graph, hoods, config) on host arrays
+        ctx.optimize_arrays(g_pin, h_pin, cfg, fixed_work=True, multilabel=c["M"] != 2,
+                            trace_level=E.TRACE_NONE, labels_out=lab_pin)
         e2e_times.append(time.perf_counter() - t0)
     barrier()
     e2e_s = allmax(sum(e2e_times))

@@ -300,8 +300,6 @@ inline OptimizeResult optimize(const dpp::Backend& b, const RegionGraph& g,
                                const NeighborhoodSet& h, const OptimizerConfig& config,
                                int trace_level = DPMRF_TRACE_FULL, unsigned run_flags = 0) {
   auto& c = detail::ctx_for(b);
-  detail::graph(c, g);
-  detail::hoods(c, h);
   dpmrf_optimizer_config cfg{config.num_labels, config.em_max_iters, config.map_max_iters,
                              config.convergence_window, config.convergence_tol, config.beta,
                              config.rng_seed};
@@ -310,8 +308,13 @@ inline OptimizeResult optimize(const dpp::Backend& b, const RegionGraph& g,
   r.labels.resize(g.num_vertices);
   r.params.mu.resize(config.num_labels);
   r.params.sigma.resize(config.num_labels);
-  throw_status(dpmrf_optimize(c.h, &cfg, &opts, r.labels.data(), r.params.mu.data(),
-                              r.params.sigma.data()),
+  // graph + hoods upload and the run in one call (engine.hpp:99-100's shape)
+  const std::vector<std::uint32_t> h_off =
+      h.offsets.empty() ? std::vector<std::uint32_t>{0} : h.offsets;
+  throw_status(dpmrf_optimize_arrays(c.h, g.num_vertices, g.offsets.data(), g.neighbors.data(),
+                                     g.region_mean.data(), h_off.size() - 1, h_off.data(),
+                                     h.members.data(), &cfg, &opts, r.labels.data(),
+                                     r.params.mu.data(), r.params.sigma.data()),
                "optimize");
   std::int32_t em_n = 0;
   std::uint64_t series = 0;

@@ -192,6 +192,18 @@ dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* co
                             const dpmrf_run_options* opts, uint32_t* labels, double* mu,
                             double* sigma);
 
+/* optimize(backend, graph, hoods, config) in one call, the exact shape of
+ * proj/include/dpmrf/mrf/engine.hpp:99-100: uploads the graph (as
+ * dpmrf_set_graph) and the neighborhoods (as dpmrf_set_hoods), then runs
+ * dpmrf_optimize -- one host round trip fewer per upload. */
+dpmrf_status dpmrf_optimize_arrays(dpmrf_context* ctx, uint32_t num_vertices,
+                                   const uint32_t* graph_offsets, const uint32_t* graph_neighbors,
+                                   const double* region_mean, uint64_t num_hoods,
+                                   const uint32_t* hood_offsets, const uint32_t* hood_members,
+                                   const dpmrf_optimizer_config* config,
+                                   const dpmrf_run_options* opts, uint32_t* labels, double* mu,
+                                   double* sigma);
+
 /* Trace of the last dpmrf_optimize (EmIterationLog / MapIterationLog,
  * engine.hpp:82-99). */
 dpmrf_status dpmrf_trace_info(dpmrf_context* ctx, int32_t* em_iters, uint64_t* series);

@@ -73,6 +73,8 @@ CUDA_API = [
     ("dpmrf_get_cliques", ST, [VP, VP, VP]),
     ("dpmrf_build_neighborhoods_resident", ST, [VP, U32, ct.POINTER(U64)]),
     ("dpmrf_optimize", ST, [VP, ct.POINTER(CConfig), ct.POINTER(CRunOptions), VP, VP, VP]),
+    ("dpmrf_optimize_arrays", ST, [VP, U32, VP, VP, VP, U64, VP, VP, ct.POINTER(CConfig),
+                                   ct.POINTER(CRunOptions), VP, VP, VP]),
     ("dpmrf_trace_info", ST, [VP, ct.POINTER(I32), ct.POINTER(U64)]),
     ("dpmrf_trace_em", ST, [VP, I32, ct.POINTER(I32), ct.POINTER(F64), ct.POINTER(ct.c_uint8),
                             VP, VP]),

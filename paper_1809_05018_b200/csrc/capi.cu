@@ -97,11 +97,15 @@ void dpmrf_context::prepare() {
   }
   need(has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
   need(has_hoods, DPMRF_INVALID_ARGUMENT, "no neighborhoods uploaded");
-  uint32_t* err = prep_err.ensure(2);
-  CK(cudaMemsetAsync(err, 0, 2 * sizeof(uint32_t), stream));
+  // validation and the packing statistics in one batch, one host sync
+  uint32_t* err = prep_err.ensure(6);  // [error bits, empty hoods | deg, dist, size, span]
+  CK(cudaMemsetAsync(err, 0, 6 * sizeof(uint32_t), stream));
   launch_validate(g_off.get(), g_nbr.get(), R, A, h_off.get(), h_mem.get(), H, S, err, err + 1,
                   stream);
-  uint32_t h_err[2];
+  if (use_packed && R > 0)
+    launch_pack_stats(g_off.get(), g_nbr.get(), R, A, h_off.get(), h_mem.get(), H, S, err + 2,
+                      stream);
+  uint32_t h_err[6];
   CK(cudaMemcpyAsync(h_err, err, sizeof h_err, cudaMemcpyDeviceToHost, stream));
   sync();
   prepared = true;
@@ -131,12 +135,8 @@ void dpmrf_context::prepare() {
   // oversegmentations do); otherwise the kernels read the CSR directly
   adj_k = hood_k = 0;
   if (use_packed && R > 0) {
-    uint32_t* st = prep_err.ensure(4);
+    const uint32_t* hs = h_err + 2;
     const uint32_t* so = series_alias ? h_off.get() : s_off_buf.get();
-    launch_pack_stats(g_off.get(), g_nbr.get(), R, so, h_mem.get(), Hs, st, stream);
-    uint32_t hs[4];
-    CK(cudaMemcpyAsync(hs, st, sizeof hs, cudaMemcpyDeviceToHost, stream));
-    sync();
     if (hs[1] <= 32767u) adj_k = hs[0] <= 4 ? 4 : (hs[0] <= 8 ? 8 : 0);
     if (hs[3] < 0xFFFFu && Hs > 0) hood_k = hs[2] <= 9 ? 8 : (hs[2] <= 17 ? 16 : 0);
     if (adj_k) launch_pack_adjacency(g_off.get(), g_nbr.get(), R, adj_k,
@@ -144,7 +144,7 @@ void dpmrf_context::prepare() {
     if (hood_k) launch_pack_hoods(so, h_mem.get(), Hs, hood_k, hood_base.ensure(Hs),
                                   hood_pk.ensure(Hs * hood_k), stream);
   }
-  sync();
+  // (no sync: everything that reads these runs later on the same stream)
 }
 
 // ---- context -----------------------------------------------------------------
@@ -194,32 +194,65 @@ extern "C" const char* dpmrf_last_error(void) { return g_last_error.c_str(); }
 extern "C" int dpmrf_abi_version(void) { return DPMRF_ABI_VERSION; }
 
 // ---- resident inputs -----------------------------------------------------------
+namespace {
+
+// Asynchronous uploads on the context stream; the caller synchronizes before
+// returning (the C ABI is externally synchronous: host buffers may be reused
+// as soon as a call returns).
+void upload_graph(dpmrf_context* ctx, uint32_t R, const uint32_t* offsets,
+                  const uint32_t* neighbors, const double* region_mean) {
+  need(offsets != nullptr, DPMRF_INVALID_ARGUMENT, "null argument");
+  const uint64_t A = offsets[R];
+  need(A == 0 || neighbors, DPMRF_INVALID_ARGUMENT, "neighbors is null");
+  need(R == 0 || region_mean, DPMRF_INVALID_ARGUMENT, "region_mean is null");
+  CK(cudaMemcpyAsync(ctx->g_off.ensure(uint64_t(R) + 1), offsets, (uint64_t(R) + 1) * 4,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  if (A)
+    CK(cudaMemcpyAsync(ctx->g_nbr.ensure(A), neighbors, A * 4, cudaMemcpyHostToDevice,
+                       ctx->stream));
+  else
+    ctx->g_nbr.ensure(1);
+  if (R)
+    CK(cudaMemcpyAsync(ctx->g_mean.ensure(R), region_mean, uint64_t(R) * 8,
+                       cudaMemcpyHostToDevice, ctx->stream));
+  else
+    ctx->g_mean.ensure(1);
+  ctx->R = R;
+  ctx->A = A;
+  ctx->has_graph = true;
+  ctx->has_sizes = ctx->has_cliques = false;
+  ctx->prepared = false;
+  ++ctx->generation;
+}
+
+void upload_hoods(dpmrf_context* ctx, uint64_t H, const uint32_t* offsets,
+                  const uint32_t* members) {
+  need(offsets != nullptr, DPMRF_INVALID_ARGUMENT, "null argument");
+  const uint64_t S = offsets[H];
+  need(S == 0 || members, DPMRF_INVALID_ARGUMENT, "members is null");
+  CK(cudaMemcpyAsync(ctx->h_off.ensure(H + 1), offsets, (H + 1) * 4, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  if (S)
+    CK(cudaMemcpyAsync(ctx->h_mem.ensure(S), members, S * 4, cudaMemcpyHostToDevice,
+                       ctx->stream));
+  else
+    ctx->h_mem.ensure(1);
+  ctx->h_src.release();  // identity (neighborhoods.cpp:53-55)
+  ctx->H = H;
+  ctx->S = S;
+  ctx->has_hoods = true;
+  ctx->prepared = false;
+  ++ctx->generation;
+}
+
+}  // namespace
+
 extern "C" dpmrf_status dpmrf_set_graph(dpmrf_context* ctx, uint32_t R, const uint32_t* offsets,
                                         const uint32_t* neighbors, const double* region_mean) {
   return guarded([&] {
-    need(ctx && offsets, DPMRF_INVALID_ARGUMENT, "null argument");
+    need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null argument");
     ctx->bind();
-    const uint64_t A = offsets[R];
-    need(A == 0 || neighbors, DPMRF_INVALID_ARGUMENT, "neighbors is null");
-    need(R == 0 || region_mean, DPMRF_INVALID_ARGUMENT, "region_mean is null");
-    CK(cudaMemcpyAsync(ctx->g_off.ensure(uint64_t(R) + 1), offsets, (uint64_t(R) + 1) * 4,
-                       cudaMemcpyHostToDevice, ctx->stream));
-    if (A)
-      CK(cudaMemcpyAsync(ctx->g_nbr.ensure(A), neighbors, A * 4, cudaMemcpyHostToDevice,
-                         ctx->stream));
-    else
-      ctx->g_nbr.ensure(1);
-    if (R)
-      CK(cudaMemcpyAsync(ctx->g_mean.ensure(R), region_mean, uint64_t(R) * 8,
-                         cudaMemcpyHostToDevice, ctx->stream));
-    else
-      ctx->g_mean.ensure(1);
-    ctx->R = R;
-    ctx->A = A;
-    ctx->has_graph = true;
-    ctx->has_sizes = ctx->has_cliques = false;
-    ctx->prepared = false;
-    ++ctx->generation;
+    upload_graph(ctx, R, offsets, neighbors, region_mean);
     ctx->sync();
   });
 }
@@ -227,23 +260,9 @@ extern "C" dpmrf_status dpmrf_set_graph(dpmrf_context* ctx, uint32_t R, const ui
 extern "C" dpmrf_status dpmrf_set_hoods(dpmrf_context* ctx, uint64_t H, const uint32_t* offsets,
                                         const uint32_t* members) {
   return guarded([&] {
-    need(ctx && offsets, DPMRF_INVALID_ARGUMENT, "null argument");
+    need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null argument");
     ctx->bind();
-    const uint64_t S = offsets[H];
-    need(S == 0 || members, DPMRF_INVALID_ARGUMENT, "members is null");
-    CK(cudaMemcpyAsync(ctx->h_off.ensure(H + 1), offsets, (H + 1) * 4, cudaMemcpyHostToDevice,
-                       ctx->stream));
-    if (S)
-      CK(cudaMemcpyAsync(ctx->h_mem.ensure(S), members, S * 4, cudaMemcpyHostToDevice,
-                         ctx->stream));
-    else
-      ctx->h_mem.ensure(1);
-    ctx->h_src.release();  // identity (neighborhoods.cpp:53-55)
-    ctx->H = H;
-    ctx->S = S;
-    ctx->has_hoods = true;
-    ctx->prepared = false;
-    ++ctx->generation;
+    upload_hoods(ctx, H, offsets, members);
     ctx->sync();
   });
 }
@@ -831,11 +850,45 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
 
 }  // namespace
 
+namespace {
+
+void optimize_resident(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
+                       const dpmrf_run_options* opts, uint32_t* labels_out, double* mu_out,
+                       double* sigma_out);
+
+}  // namespace
+
 extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
                                        const dpmrf_run_options* opts, uint32_t* labels_out,
                                        double* mu_out, double* sigma_out) {
   return guarded([&] {
     need(ctx && cfg, DPMRF_INVALID_ARGUMENT, "null argument");
+    optimize_resident(ctx, cfg, opts, labels_out, mu_out, sigma_out);
+  });
+}
+
+extern "C" dpmrf_status dpmrf_optimize_arrays(
+    dpmrf_context* ctx, uint32_t R, const uint32_t* g_offsets, const uint32_t* g_neighbors,
+    const double* region_mean, uint64_t H, const uint32_t* h_offsets, const uint32_t* h_members,
+    const dpmrf_optimizer_config* cfg, const dpmrf_run_options* opts, uint32_t* labels_out,
+    double* mu_out, double* sigma_out) {
+  return guarded([&] {
+    need(ctx && cfg, DPMRF_INVALID_ARGUMENT, "null argument");
+    ctx->bind();
+    upload_graph(ctx, R, g_offsets, g_neighbors, region_mean);
+    upload_hoods(ctx, H, h_offsets, h_members);
+    // (the copies complete before optimize's first synchronization; the
+    // host buffers are not touched after this call returns)
+    optimize_resident(ctx, cfg, opts, labels_out, mu_out, sigma_out);
+  });
+}
+
+namespace {
+
+void optimize_resident(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
+                       const dpmrf_run_options* opts, uint32_t* labels_out, double* mu_out,
+                       double* sigma_out) {
+  {
     const dpmrf_run_options o = opts ? *opts : dpmrf_run_options{0, DPMRF_TRACE_FULL};
     validate_config(*cfg, (o.flags & DPMRF_RUN_MULTILABEL) != 0);
     need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
@@ -850,8 +903,10 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
       ++ctx->stats.device_log_fallbacks;  // a device log(sigma) differed from glibc's
     }
     run_optimize(ctx, cfg, o, false, labels_out, mu_out, sigma_out);
-  });
+  }
 }
+
+}  // namespace
 
 extern "C" dpmrf_status dpmrf_trace_info(dpmrf_context* ctx, int32_t* em_iters, uint64_t* series) {
   return guarded([&] {

@@ -1460,13 +1460,20 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
 }
 
 // ---- pack builders ----
+// Runs beside k_validate (one host sync for both), so every read is clamped
+// to the array bounds: on an invalid CSR the stats are meaningless but safe,
+// and prepare() fails on the validation result before using them.  Empty
+// hoods do not move any maximum, so the raw hood offsets serve as well as the
+// series offsets.
 __global__ void k_pack_stats(const uint32_t* __restrict__ g_off, const uint32_t* __restrict__ g_nbr,
-                             uint32_t R, const uint32_t* __restrict__ s_off,
-                             const uint32_t* __restrict__ h_mem, uint64_t Hs, uint32_t* stats) {
+                             uint32_t R, uint64_t A, const uint32_t* __restrict__ s_off,
+                             const uint32_t* __restrict__ h_mem, uint64_t Hs, uint64_t S,
+                             uint32_t* stats) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   uint32_t deg = 0, dist = 0, size = 0, span = 0;
   for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < R; v += stride) {
-    const uint32_t lo = g_off[v], hi = g_off[v + 1];
+    const uint32_t lo = g_off[v], hi = uint64_t(g_off[v + 1]) < A ? g_off[v + 1] : uint32_t(A);
+    if (hi < lo) continue;
     deg = max(deg, hi - lo);
     for (uint32_t i = lo; i < hi; ++i) {
       const uint32_t u = g_nbr[i];
@@ -1474,7 +1481,8 @@ __global__ void k_pack_stats(const uint32_t* __restrict__ g_off, const uint32_t*
     }
   }
   for (uint64_t h = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; h < Hs; h += stride) {
-    const uint32_t lo = s_off[h], hi = s_off[h + 1];
+    const uint32_t lo = s_off[h], hi = uint64_t(s_off[h + 1]) < S ? s_off[h + 1] : uint32_t(S);
+    if (hi < lo) continue;
     size = max(size, hi - lo);
     if (hi > lo) span = max(span, h_mem[hi - 1] - h_mem[lo]);
   }
@@ -1512,13 +1520,12 @@ __global__ void k_pack_hoods(const uint32_t* __restrict__ s_off, const uint32_t*
 
 }  // namespace
 
-void launch_pack_stats(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R,
-                       const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs,
+void launch_pack_stats(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, uint64_t A,
+                       const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, uint64_t S,
                        uint32_t* stats, cudaStream_t s) {
-  CK(cudaMemsetAsync(stats, 0, 4 * sizeof(uint32_t), s));
   const uint64_t work = std::max<uint64_t>(std::max<uint64_t>(R, Hs), 1);
   k_pack_stats<<<std::min<unsigned>(grid_for(work, 256), 8 * kNumSMs), 256, 0, s>>>(
-      g_off, g_nbr, R, s_off, h_mem, Hs, stats);
+      g_off, g_nbr, R, A, s_off, h_mem, Hs, S, stats);
   CK_LAUNCH();
 }
 

@@ -158,8 +158,8 @@ void launch_validate(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, u
 void launch_cover(const uint32_t* h_mem, uint64_t S, uint8_t* cover, uint32_t R, cudaStream_t s);
 // Packing: stats[0] = max degree, [1] = max |u - v|, [2] = max hood size,
 // [3] = max (last - first member) over the series hoods.
-void launch_pack_stats(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R,
-                       const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs,
+void launch_pack_stats(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, uint64_t A,
+                       const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, uint64_t S,
                        uint32_t* stats, cudaStream_t s);
 void launch_pack_adjacency(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, int k,
                            int16_t* out, cudaStream_t s);

@@ -366,6 +366,31 @@ class Context:
         return OptimizeResult(labels, LabelParams(mu, sigma), self._trace(M, trace_level),
                               self.stats())
 
+    def optimize_arrays(self, graph: RegionGraph, hoods: NeighborhoodSet,
+                        config: OptimizerConfig, *, fixed_work=False, multilabel=None,
+                        trace_level=TRACE_FULL, labels_out=None) -> OptimizeResult:
+        """optimize(backend, graph, hoods, config) in ONE C-ABI call
+        (dpmrf_optimize_arrays): host arrays in, labels / params out."""
+        M = config.num_labels
+        if multilabel is None:
+            multilabel = M != 2
+        flags = (RUN_FIXED_WORK if fixed_work else 0) | (RUN_MULTILABEL if multilabel else 0)
+        opts = N.CRunOptions(flags, trace_level)
+        cfg = config.c()
+        off, nbr, mean = _u32(graph.offsets), _u32(graph.neighbors), _f64(graph.region_mean)
+        hoff, hmem = _u32(hoods.offsets), _u32(hoods.members)
+        R = len(off) - 1
+        labels = labels_out if labels_out is not None else np.zeros(R, np.uint32)
+        mu, sigma = np.zeros(M), np.zeros(M)
+        _check(self._lib.dpmrf_optimize_arrays(self.h, R, N.ptr(off), N.ptr(nbr), N.ptr(mean),
+                                               len(hoff) - 1, N.ptr(hoff), N.ptr(hmem),
+                                               ct.byref(cfg), ct.byref(opts), N.ptr(labels),
+                                               N.ptr(mu), N.ptr(sigma)), "optimize_arrays")
+        self.R, self.H, self.S = R, len(hoff) - 1, len(hmem)
+        self._graph_key, self._hoods_key = graph, hoods
+        return OptimizeResult(labels, LabelParams(mu, sigma), self._trace(M, trace_level),
+                              self.stats())
+
     def _trace(self, M, level) -> List[EmIterationLog]:
         if level == TRACE_NONE:
             return []

@@ -256,3 +256,25 @@ def test_two_vertices_per_thread_path(ctx):
             for ma, mb in zip(ea.map_iters, eb.map_iters):
                 assert np.array_equal(ma.hood_energy, mb.hood_energy)
                 assert np.array_equal(ma.converged, mb.converged)
+
+
+def test_optimize_arrays_one_call(ctx):
+    """dpmrf_optimize_arrays (upload + optimize in one call) == set_graph +
+    set_hoods + optimize, including after the context held another graph."""
+    from paper_1809_05018_b200 import inputs
+    sl = inputs.synthetic_slice(512, 8, seed=17)
+    ctx.set_graph(sl.graph)
+    ctx.build_neighborhoods(sl.cliques)
+    hoods = ctx.get_hoods()
+    cfg = E.OptimizerConfig(em_max_iters=6, rng_seed=17)
+    want = ctx.optimize(cfg, trace_level=E.TRACE_EM)
+    other = inputs.synthetic_slice(256, 8, seed=1)  # replace the resident inputs first
+    ctx.set_graph(other.graph)
+    ctx.build_neighborhoods(other.cliques)
+    got = ctx.optimize_arrays(sl.graph, hoods, cfg, trace_level=E.TRACE_EM)
+    assert np.array_equal(got.labels, want.labels)
+    assert np.array_equal(got.mu, want.mu) and np.array_equal(got.sigma, want.sigma)
+    assert [e.total_energy for e in got.trace] == [e.total_energy for e in want.trace]
+    with pytest.raises(ValueError):  # a bad CSR is reported, not run
+        bad = E.NeighborhoodSet(np.array([0, 5, 3], np.uint32), hoods.members[:5])
+        ctx.optimize_arrays(sl.graph, bad, cfg)
