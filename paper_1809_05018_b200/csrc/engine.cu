@@ -670,32 +670,69 @@ __global__ void __launch_bounds__(kTileThreads)
 
 // Single block: per-label exclusive scan over tiles; label starts; leaf layout.
 // layout = n[M] | label_start[M+1] | leaf_start[M+2] (series M = hood energies)
+// Large graphs: per-label tile offsets with two many-block kernels (one
+// block per 1024 tiles): k_tile_chunks sums each chunk's counts per label,
+// k_tile_offsets adds the preceding chunks' sums to a block scan of its own
+// tiles.  Integer sums -- any order gives the same offsets.
+// layout = n[M] | label_start[M+1] | leaf_start[M+2] (series M = hood energies)
+constexpr uint32_t kTileChunk = 1024;
+
+__device__ __forceinline__ uint32_t block_sum_1024(uint32_t v, uint32_t* red) {
+  v = __reduce_add_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint32_t t = 0;
+  if (threadIdx.x < 32) t = __reduce_add_sync(0xffffffffu, threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u);
+  if (threadIdx.x == 0) red[32] = t;
+  __syncthreads();
+  const uint32_t r = red[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024)
+    k_tile_chunks(const uint32_t* __restrict__ counts_buf, const uint32_t* __restrict__ unconv,
+                  int map_max, int fixed, uint32_t tiles, uint32_t M,
+                  uint32_t* __restrict__ chunk_sum) {
+  __shared__ uint32_t red[33];
+  pdl_wait();
+  if (em_skipped(unconv)) return;
+  const uint32_t* tc = final_counts(counts_buf, tiles, M, unconv, map_max, fixed);
+  const uint64_t i = uint64_t(blockIdx.x) * kTileChunk + threadIdx.x;
+  for (uint32_t l = 0; l < M; ++l) {
+    const uint32_t c = i < tiles ? tc[i * M + l] : 0u;
+    const uint32_t s = block_sum_1024(c, red);
+    if (threadIdx.x == 0) chunk_sum[uint64_t(blockIdx.x) * M + l] = s;
+  }
+}
+
 __global__ void __launch_bounds__(1024)
     k_tile_offsets(const uint32_t* __restrict__ counts_buf, const uint32_t* __restrict__ unconv,
                    int map_max, int fixed, uint32_t* __restrict__ tile_base, uint32_t tiles,
-                   uint32_t M, uint64_t Hs, uint32_t* __restrict__ layout) {
+                   uint32_t M, uint64_t Hs, uint32_t* __restrict__ layout,
+                   const uint32_t* __restrict__ chunk_sum, uint32_t nchunks) {
   __shared__ uint32_t warp_sums[32];
-  __shared__ uint32_t carry;
+  __shared__ uint32_t red[33];
   pdl_wait();
   if (em_skipped(unconv)) return;
-  const uint32_t* tile_counts = final_counts(counts_buf, tiles, M, unconv, map_max, fixed);
+  const uint32_t* tc = final_counts(counts_buf, tiles, M, unconv, map_max, fixed);
+  const uint64_t i = uint64_t(blockIdx.x) * kTileChunk + threadIdx.x;
   for (uint32_t l = 0; l < M; ++l) {
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (uint32_t b = 0; b < tiles; b += blockDim.x) {
-      const uint32_t i = b + threadIdx.x;
-      const uint32_t c = i < tiles ? tile_counts[uint64_t(i) * M + l] : 0u;
-      uint32_t tot;
-      const uint32_t ex = block_exclusive_scan(c, warp_sums, &tot);
-      if (i < tiles) tile_base[uint64_t(i) * M + l] = carry + ex;
-      __syncthreads();
-      if (threadIdx.x == 0) carry += tot;
-      __syncthreads();
+    uint32_t pre = 0, tot = 0;  // preceding chunks / all chunks of label l
+    for (uint32_t c = threadIdx.x; c < nchunks; c += blockDim.x) {
+      const uint32_t v = chunk_sum[uint64_t(c) * M + l];
+      tot += v;
+      pre += c < blockIdx.x ? v : 0u;
     }
-    if (threadIdx.x == 0) layout[l] = carry;
-    __syncthreads();
+    pre = block_sum_1024(pre, red);
+    tot = block_sum_1024(tot, red);
+    const uint32_t cnt = i < tiles ? tc[i * M + l] : 0u;
+    const uint32_t ex = block_exclusive_scan(cnt, warp_sums, nullptr);
+    if (i < tiles) tile_base[i * M + l] = pre + ex;
+    if (blockIdx.x == 0 && threadIdx.x == 0) layout[l] = tot;
   }
-  if (threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_block();
     uint32_t* label_start = layout + M;
     uint32_t* leaf_start = layout + 2 * M + 1;
     uint32_t s = 0, lf = 0;
@@ -894,6 +931,7 @@ __global__ void __launch_bounds__(256)
   if (!last) return;
   __threadfence();
   constexpr uint32_t kStageDoubles = kLeavesPerBlock * kLeafStride;
+  static_assert(8 * 1056 >= kStageDoubles, "tail stage");
   auto finish = [&](uint32_t s, double folded) {  // parameters / total energy of series s
     if (s < M) {
       if (n[s] != 0) {  // empty labels keep their previous parameters
@@ -947,6 +985,43 @@ __global__ void __launch_bounds__(256)
   for (uint32_t s = 0; s < nseries; ++s) {
     uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
     double* p = partials + leaf_start[s];
+    // Long series: reduce aligned 1024-partial chunks first (one warp per
+    // chunk, bottom-up adjacent pairing in shared memory); a chunk's root is
+    // exactly the level-10 node of the series' tree, and the tree continues
+    // over the roots (written in place, below every unread element).
+    while (cnt > kStageDoubles) {
+      const uint32_t nch = (cnt + 1023) / 1024;
+      const uint32_t wch = threadIdx.x >> 5, ln = threadIdx.x & 31;
+      for (uint32_t c0 = 0; c0 < nch; c0 += blockDim.x >> 5) {
+        const uint32_t c = c0 + wch;
+        double* q = stage + wch * 1056;
+        uint32_t m = 0;
+        if (c < nch) {
+          m = min(1024u, cnt - c * 1024);
+          for (uint32_t i = ln; i < m; i += 32) q[i] = __ldcg(p + uint64_t(c) * 1024 + i);
+        }
+        __syncthreads();  // every chunk of this group is read before any root is written
+        if (c < nch) {
+          __syncwarp();
+          while (m > 1) {
+            const uint32_t pairs = m / 2;
+            for (uint32_t i0 = 0; i0 < pairs; i0 += 32) {
+              const uint32_t i = i0 + ln;
+              const double v = i < pairs ? __dadd_rn(q[2 * i], q[2 * i + 1]) : 0.0;
+              __syncwarp();
+              if (i < pairs) q[i] = v;
+              __syncwarp();
+            }
+            if ((m & 1u) && ln == 0) q[pairs] = q[m - 1];
+            __syncwarp();
+            m = pairs + (m & 1u);
+          }
+          if (ln == 0) p[c] = q[0];
+        }
+        __syncthreads();
+      }
+      cnt = nch;
+    }
     if (cnt >= 1 && cnt <= kStageDoubles) {  // (an empty label has no partials at all)
       // the tree levels run in shared memory (one global round trip in total)
       for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) stage[i] = __ldcg(p + i);
@@ -1615,8 +1690,17 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
                R, M, Hs, mean, (const uint32_t*)counts, tiles, layout, x);
     ++n;
   } else {
-    launch_pdl(k_tile_offsets, dim3(1), dim3(1024), 0, s, (const uint32_t*)counts,
-               counts_ready ? unconv : nullptr, map_max, fixed, tile_base, tiles, M, Hs, layout);
+    const uint32_t nchunks = (tiles + kTileChunk - 1) / kTileChunk;
+    uint32_t* chunk_sum = mb.chunk_sum.ensure(uint64_t(nchunks ? nchunks : 1) * M);
+    const uint32_t* sel = counts_ready ? unconv : nullptr;
+    if (nchunks) {
+      launch_pdl(k_tile_chunks, dim3(nchunks), dim3(1024), 0, s, (const uint32_t*)counts, sel,
+                 map_max, fixed, tiles, M, chunk_sum);
+      ++n;
+    }
+    launch_pdl(k_tile_offsets, dim3(nchunks ? nchunks : 1), dim3(1024), 0, s,
+               (const uint32_t*)counts, sel, map_max, fixed, tile_base, tiles, M, Hs, layout,
+               (const uint32_t*)chunk_sum, nchunks);
     ++n;
   }
   if (!scattered && tiles && uint64_t(tiles) * M > kSelfScanMax) {
@@ -1626,7 +1710,7 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
     ++n;
   }
   static bool smem_set = false;
-  const size_t leaf_smem = size_t(kLeavesPerBlock) * kLeafStride * sizeof(double);
+  const size_t leaf_smem = size_t(8) * 1056 * sizeof(double);  // 8 leaves (the tail: 8 x 1056)
   if (!smem_set) {
     CK(cudaFuncSetAttribute(k_leaf_fold<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(leaf_smem)));
@@ -1691,6 +1775,7 @@ void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs) {
   const uint32_t tiles_g = tiles ? tiles : 1;
   mb.counts.ensure(2 * uint64_t(tiles_g) * M);
   mb.tile_base.ensure(uint64_t(tiles_g) * M);
+  mb.chunk_sum.ensure(((uint64_t(tiles_g) + kTileChunk - 1) / kTileChunk) * M);
   mb.layout.ensure(4 * M + 4);
   mb.x.ensure(R);
   mb.partials.ensure((uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M + (Hs + kFoldLeaf - 1) / kFoldLeaf + 1);

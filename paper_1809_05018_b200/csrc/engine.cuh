@@ -109,6 +109,7 @@ struct MStepBuffers {
   DevBuf<double> x;              // R values grouped by label (stable)
   DevBuf<double> partials;       // leaf partials of all series
   DevBuf<uint32_t> done;         // last-block tickets of the two leaf-fold kernels
+  DevBuf<uint32_t> chunk_sum;    // per-1024-tile-chunk label counts (large graphs)
   DevBuf<uint32_t> err;
   DevBuf<double> em_scratch;
 };

@@ -240,7 +240,7 @@ def test_two_vertices_per_thread_path(ctx):
     (engine.cu kVertsPerThreadMin); it must equal the unfused two-kernel
     path (one vertex per thread, pinned to the oracle above) bit for bit."""
     from paper_1809_05018_b200 import inputs
-    sl = inputs.synthetic_slice(4096, 4, seed=21)
+    sl = inputs.synthetic_slice(4104, 4, seed=21)  # > 2^20 vertices: also the many-block tile scan
     assert sl.graph.num_vertices >= 1 << 20
     ctx.set_graph(sl.graph)
     ctx.build_neighborhoods(sl.cliques)

@@ -119,3 +119,22 @@ def test_convergence_and_params_golden(ctx):  # mrf_engine_test.cpp:344-417
     assert p.mu.tolist() == [50.0, 123.5] and p.sigma.tolist() == [10.0, 4.5]
     ctx.set_hoods(E.NeighborhoodSet(*WORKED))
     assert ctx.update_labels([0, 0, 1, 1, 1, 0, 0], [1] * 6).tolist() == [0, 0, 1, 0, 0, 1]
+
+
+@pytest.mark.parametrize("R,frac0", [(9_000_000, 0.97), (20_000_000, 0.5), (3_000_000, 0.0)])
+def test_update_parameters_long_series(orc, R, frac0):
+    """Series of > 8200 leaves (> 8.4M elements) take the chunked tree in the
+    leaf-fold tail (aligned 1024-partial chunks, then the roots); labels of
+    one class only leave the other label empty (keeps its parameters)."""
+    rng = np.random.default_rng(R)
+    mean = rng.random(R) * 255.0
+    labels = (rng.random(R) >= frac0).astype(np.uint32)
+    c = E.Context(0)
+    try:
+        c.set_graph(E.RegionGraph(np.zeros(R + 1, np.uint32), np.zeros(0, np.uint32), mean))
+        prev = E.LabelParams(np.array([10.0, 20.0]), np.array([3.0, 4.0]))
+        got = c.update_parameters(labels, prev)
+    finally:
+        c.close()
+    mu, sg = orc.update_parameters(mean, labels, prev.mu, prev.sigma)
+    assert np.array_equal(got.mu, mu) and np.array_equal(got.sigma, sg)
