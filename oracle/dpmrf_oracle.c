@@ -96,6 +96,10 @@ double orc_fold_range_add(const double *x, size_t n) {
   return r;
 }
 
+/* fold_tree<plus> over given leaf partials (kernels.hpp:45-51), count >= 1:
+ * the combine step of a fold whose leaves were folded elsewhere. */
+double orc_fold_tree_add(const double *p, size_t count) { return fold_tree_add(p, count); }
+
 /* dpp::reduce<plus> with identity 0.0, kernels.hpp:124-139. */
 double orc_reduce_add(const double *x, size_t n) {
   if (n == 0) return 0.0;

@@ -173,6 +173,8 @@ class _COracle:
         L.orc_init_random.argtypes = [U32, U32, U64, ct.c_int, f64p, f64p, u32p]
         L.orc_fold_range_add.argtypes = [f64p, ct.c_size_t]
         L.orc_fold_range_add.restype = F64
+        L.orc_fold_tree_add.argtypes = [f64p, ct.c_size_t]
+        L.orc_fold_tree_add.restype = F64
         L.orc_reduce_add.argtypes = [f64p, ct.c_size_t]
         L.orc_reduce_add.restype = F64
         L.orc_slot_hood_map.argtypes = [U64, u32p, u32p]
@@ -214,6 +216,11 @@ class _COracle:
     def fold_range(self, x):
         x = _a(x, np.float64)
         return self.L.orc_fold_range_add(x, len(x))
+
+    def fold_tree(self, partials):
+        """fold_tree<plus> (kernels.hpp:45-51) over leaf partials (len >= 1)."""
+        p = _a(partials, np.float64)
+        return self.L.orc_fold_tree_add(p, len(p))
 
     def reduce(self, x):
         x = _a(x, np.float64)

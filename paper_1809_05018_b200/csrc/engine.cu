@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ hist, uint64_t Hs, int ring,
                 const uint32_t* __restrict__ unconv, int map_max, int fixed, double* params,
                 double* partials, double* em_out, uint32_t* done, EmEpilogueArgs ep,
-                int merged) {
+                int merged, const double* __restrict__ hood_parts) {
   extern __shared__ double stage[];  // kLeavesPerBlock x kLeafStride
   pdl_wait();
   const uint32_t* n = layout;
@@ -833,7 +833,7 @@ __global__ void __launch_bounds__(256)
   const uint32_t first = blockIdx.x * kLeavesPerBlock;
   if (first < total) {
     const double* hood_row = nullptr;
-    if (!kSq && unconv) {
+    if (!kSq && unconv && !hood_parts) {
       const int T = executed_iters(unconv, map_max, fixed);
       hood_row = hist + uint64_t((T - 1) % ring) * Hs;
     }
@@ -847,12 +847,17 @@ __global__ void __launch_bounds__(256)
       double mu = 0.0;
       if (leaf < total) {
         const uint32_t sr = series_of(leaf_start, nseries, leaf);
-        const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
-        const uint64_t slen = sr < M ? n[sr] : Hs;
-        src = (sr < M ? x + label_start[sr] : hood_row) + b;
-        const uint64_t rem = slen - b;
-        len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
-        if (kSq) mu = params[sr];
+        if (!kSq && sr == M && hood_parts) {
+          // partitioned run: each rank folded its own hood-series leaves
+          partials[leaf] = hood_parts[leaf - leaf_start[M]];
+        } else {
+          const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
+          const uint64_t slen = sr < M ? n[sr] : Hs;
+          src = (sr < M ? x + label_start[sr] : hood_row) + b;
+          const uint64_t rem = slen - b;
+          len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
+          if (kSq) mu = params[sr];
+        }
       }
       src_s[threadIdx.x] = src;
       len_s[threadIdx.x] = len;
@@ -1113,7 +1118,47 @@ __global__ void k_partition_select(const uint8_t* lab_even, const uint8_t* lab_o
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   for (uint64_t v = vb + i0; v < ve; v += stride) lab_full[v] = lab[v];
-  for (uint64_t h = hb + i0; h < he; h += stride) row_full[h] = row[h];
+  if (row_full)
+    for (uint64_t h = hb + i0; h < he; h += stride) row_full[h] = row[h];
+}
+
+// Partitioned optimize: this rank's leaves of the hood-energy series (its
+// series range starts on a leaf boundary) folded from the last executed MAP
+// row -- fold_leaf, kernels.hpp:37-42 -- into out[leaf - first_leaf], so the
+// per-EM exchange carries H/1024 partials instead of the H-element row.
+__global__ void __launch_bounds__(256)
+    k_row_leaves(const double* __restrict__ hist, int ring, uint64_t Hs,
+                 const uint32_t* __restrict__ unconv, int map_max, int fixed, uint64_t hb,
+                 uint64_t he, double* __restrict__ out) {
+  extern __shared__ double stage[];  // kLeavesPerBlock x kLeafStride
+  __shared__ uint32_t len_s[kLeavesPerBlock];
+  pdl_wait();
+  if (em_skipped(unconv)) return;
+  const int T = executed_iters(unconv, map_max, fixed);
+  const double* row = hist + uint64_t((T - 1) % ring) * Hs;
+  const uint64_t first = hb / kFoldLeaf + uint64_t(blockIdx.x) * kLeavesPerBlock;
+  const uint64_t nleaf = (he + kFoldLeaf - 1) / kFoldLeaf;
+  if (threadIdx.x < kLeavesPerBlock) {
+    const uint64_t leaf = first + threadIdx.x;
+    uint32_t len = 0;
+    if (leaf < nleaf) {
+      const uint64_t rem = he - leaf * kFoldLeaf;
+      len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
+    }
+    len_s[threadIdx.x] = len;
+  }
+  __syncthreads();
+  for (uint32_t f = threadIdx.x; f < kLeavesPerBlock * kFoldLeaf; f += blockDim.x) {
+    const uint32_t j = f / kFoldLeaf, i = f % kFoldLeaf;
+    stage[j * kLeafStride + i] = i < len_s[j] ? __ldcg(row + (first + j) * kFoldLeaf + i) : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < kLeavesPerBlock && len_s[threadIdx.x]) {
+    const double* v = stage + threadIdx.x * kLeafStride;
+    double acc = v[0];
+    for (uint32_t i = 1; i < len_s[threadIdx.x]; ++i) acc = __dadd_rn(acc, v[i]);
+    out[first + threadIdx.x - hb / kFoldLeaf] = acc;
+  }
 }
 
 __global__ void k_log_cr(const double* x, double* out, uint64_t n) {
@@ -1661,7 +1706,7 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
                 const uint8_t* lab_odd, const uint32_t* unconv, int map_max, int fixed,
                 const double* hist, uint64_t Hs, int ring, double* params, double* em_out,
                 MStepBuffers& mb, cudaStream_t s, uint64_t* launches, bool counts_ready,
-                bool scattered, const EmEpilogueArgs* ep) {
+                bool scattered, const EmEpilogueArgs* ep, const double* hood_parts) {
   mstep_reserve(mb, R, M, Hs);
   const uint32_t tiles = static_cast<uint32_t>((uint64_t(R) + kTileVerts - 1) / kTileVerts);
   uint32_t* counts = mb.counts.get();
@@ -1722,10 +1767,11 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
   const EmEpilogueArgs epv = ep ? *ep : EmEpilogueArgs{};
   launch_pdl(k_leaf_fold<false>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
              (const uint32_t*)layout, M, hist, Hs, ring, unconv, map_max, fixed, params, partials,
-             em_out, mb.done.get(), epv, 0);
+             em_out, mb.done.get(), epv, 0, hood_parts);
   launch_pdl(k_leaf_fold<true>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
              (const uint32_t*)layout, M, (const double*)nullptr, uint64_t(0), 1, unconv, map_max,
-             fixed, params, partials, em_out, mb.done.get() + 1, epv, ep ? 1 : 0);
+             fixed, params, partials, em_out, mb.done.get() + 1, epv, ep ? 1 : 0,
+             (const double*)nullptr);
   n += 2;
   if (launches) *launches += n;
 }
@@ -1740,9 +1786,9 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
                   const uint8_t* lab_odd, const double* hist, uint64_t Hs, int ring,
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches, bool counts_ready,
-                  bool scattered, const EmEpilogueArgs* ep) {
+                  bool scattered, const EmEpilogueArgs* ep, const double* hood_parts) {
   mstep_core(mean, R, M, lab_even, lab_odd, unconv, map_max, fixed, hist, Hs, ring, params,
-             em_out, mb, s, launches, counts_ready, scattered, ep);
+             em_out, mb, s, launches, counts_ready, scattered, ep, hood_parts);
 }
 
 void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s) {
@@ -1762,6 +1808,21 @@ void launch_partition_select(const uint8_t* lab_even, const uint8_t* lab_odd, co
   const unsigned g = std::min<unsigned>(grid_for(n ? n : 1, 256), 4 * kNumSMs);
   launch_pdl(k_partition_select, dim3(g), dim3(256), 0, s, lab_even, lab_odd, hist, ring, Hs,
              unconv, map_max, fixed, vb, ve, hb, he, lab_full, row_full);
+}
+
+void launch_row_leaves(const double* hist, int ring, uint64_t Hs, const uint32_t* unconv,
+                       int map_max, int fixed, uint64_t hb, uint64_t he, double* out,
+                       cudaStream_t s) {
+  if (he <= hb) return;
+  const uint64_t nl = (he + kFoldLeaf - 1) / kFoldLeaf - hb / kFoldLeaf;
+  const size_t smem = size_t(kLeavesPerBlock) * kLeafStride * sizeof(double);
+  static bool smem_set = false;
+  if (!smem_set) {
+    CK(cudaFuncSetAttribute(k_row_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    smem_set = true;
+  }
+  launch_pdl(k_row_leaves, dim3(grid_for(nl, kLeavesPerBlock)), dim3(256), smem, s, hist, ring,
+             Hs, unconv, map_max, fixed, hb, he, out);
 }
 
 void launch_log_cr(const double* x, double* out, uint64_t n, cudaStream_t s) {
@@ -1803,7 +1864,7 @@ void launch_update_parameters_u32(const double* mean, uint32_t R, uint32_t M,
   if (R == 0) return;
   double* eo = mb.em_scratch.ensure(2 + 2 * M);
   mstep_core(mean, R, M, lab, lab, nullptr, 1, 1, nullptr, 0, 1, params, eo, mb, s, nullptr,
-             /*counts_ready=*/false, /*scattered=*/false, nullptr);
+             /*counts_ready=*/false, /*scattered=*/false, nullptr, nullptr);
 }
 
 void launch_init_labels(uint8_t* lab, uint32_t R, uint32_t M, uint64_t seed, cudaStream_t s) {

@@ -123,7 +123,12 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
                   const uint32_t* unconv, int map_max, int fixed, double* params, double* em_out,
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches,
                   bool counts_ready = true, bool scattered = false,
-                  const EmEpilogueArgs* ep = nullptr);
+                  const EmEpilogueArgs* ep = nullptr, const double* hood_parts = nullptr);
+// Partitioned optimize: fold this rank's leaves [hb/1024, ceil(he/1024)) of
+// the last executed hood-energy row into out (hood_parts of launch_mstep).
+void launch_row_leaves(const double* hist, int ring, uint64_t Hs, const uint32_t* unconv,
+                       int map_max, int fixed, uint64_t hb, uint64_t he, double* out,
+                       cudaStream_t s);
 
 // Device-resident EM loop (see engine.cu).  unconv points 4 words into its
 // allocation: [em_done, pending_done, em_count, pad | unconv[map_max]].

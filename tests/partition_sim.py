@@ -5,8 +5,9 @@ Each rank runs the MAP kernels' arithmetic (numpy, the exact IEEE operation
 order of label_energy, model.hpp:66-72, and of the slot-order hood fold,
 engine.cpp:147-152) over only the vertices / series it owns, moves the halo
 windows of parallel.halo_windows with isend/irecv, sums the unconverged-hood
-counters with all_reduce and allgathers the committed labels and the last
-hood-energy row per EM iteration; the M-step and EM total are the C oracle's
+counters with all_reduce and allgathers the committed labels and the leaf
+partials of the last hood-energy row (each rank folds its own 1024-element
+leaves) per EM iteration; the M-step and EM total are the C oracle's
 (update_parameters, engine.cpp:193-223; dpp::reduce, kernels.hpp:124-139).
 The result must equal the oracle's one-process optimize bit for bit, which
 checks the partition plan and the exchange schedule independently of CUDA.
@@ -126,12 +127,17 @@ def optimize_rank(graph, hoods, cfg, fixed_work=False):
         own_lab = np.zeros(plan.chunk_v, np.int64)
         own_lab[:ve - vb] = lab[cur][vb:ve]
         full_lab = _allgather(own_lab, plan.chunk_v, world)[:R]
-        own_row = np.zeros(plan.chunk_h)
-        own_row[:he - hb] = hist[-1]
-        row = _allgather(own_row, plan.chunk_h, world)[:Hs]
+        # the rank's hood-series leaves (its series range starts on a leaf
+        # boundary) folded locally; only the leaf partials are exchanged
+        chunk_l = plan.chunk_h // 1024
+        own_parts = np.zeros(chunk_l)
+        row_own = hist[-1]
+        for i in range((he - hb + 1023) // 1024):
+            own_parts[i] = orc.fold_range(row_own[i * 1024:(i + 1) * 1024])
+        parts = _allgather(own_parts, chunk_l, world)[:(Hs + 1023) // 1024]
         lab[cur][:] = full_lab  # (every rank now holds all committed labels)
         mu, sigma = orc.update_parameters(mean, full_lab.astype(np.uint32), mu, sigma)
-        total = orc.reduce(row)
+        total = orc.fold_tree(parts) if len(parts) else 0.0
         totals.append(total)
         em_T.append(T)
         em_hist.append(total)
