@@ -202,18 +202,15 @@ def run_stack(args, E, inputs, torch, world, rank, local, barrier, allmax, allsu
     c = CONFIGS["B"]
     zs = shard_slices(args.slices, world, rank)
     t0 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
-        slices = list(ex.map(lambda z: inputs.synthetic_slice(c["size"], c["block"], seed=42 + z), zs))
-    build_s = time.perf_counter() - t0
     ctxs, cfgs, S_tot, R_tot = [], [], 0, 0
-    for z, sl in zip(zs, slices):
+    for z in zs:  # every slice built on the device, resident in its own context
         ctx = E.Context(local)
-        ctx.set_graph(sl.graph)
-        ctx.build_neighborhoods(sl.cliques)
+        ctx.synthetic_slice(c["size"], c["block"], seed=42 + z)
         ctxs.append(ctx)
         cfgs.append(E.OptimizerConfig(em_max_iters=c["em"], map_max_iters=MAP_ITERS, rng_seed=42 + z))
         S_tot += ctx.S
         R_tot += ctx.R
+    build_s = time.perf_counter() - t0
     workers = min(args.stack_threads, len(ctxs)) or 1
 
     def run_one(i):
@@ -256,7 +253,10 @@ def run_stack(args, E, inputs, torch, world, rank, local, barrier, allmax, allsu
         "slices_per_s": allsum(len(ctxs) * args.steps) / tot,
         "vertex_label_evals_per_s": allsum(2 * S_tot * c["em"] * MAP_ITERS * args.steps) / tot,
         "unique_vertex_label_evals_per_s": allsum(2 * R_tot * c["em"] * MAP_ITERS * args.steps) / tot,
-        "gpu_launches": launches, "clocks": clocks, "setup": {"input_build_s": build_s},
+        "gpu_launches": launches, "clocks": clocks,
+        "setup": {"device_input_build_s": build_s,
+                  "note": "phantom -> corrupt -> oversegment -> graph -> cliques -> hoods "
+                          "on the device (csrc/synth.cu, structure.cu, hoods.cu)"},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -275,12 +275,10 @@ def run_partitioned(args, E, inputs, torch, dist, world, rank, local, barrier, a
     c = CONFIGS["D"]
     seed = 42
     t0 = time.perf_counter()
-    sl = inputs.synthetic_slice(c["size"], c["block"], brick=c["brick"], seed=seed)
-    build_inputs_s = time.perf_counter() - t0
-    R, A = sl.graph.num_vertices, len(sl.graph.neighbors)
     ctx = E.Context(local)
-    ctx.set_graph(sl.graph)
-    ctx.build_neighborhoods(sl.cliques)
+    info = ctx.synthetic_slice(c["size"], c["block"], brick=c["brick"], seed=seed)
+    build_inputs_s = time.perf_counter() - t0
+    R, A = info["regions"], info["adjacency"]
     hoods = ctx.get_hoods()
     H, S = hoods.size(), hoods.total_slots()
     if world > 1:
@@ -338,7 +336,7 @@ def run_partitioned(args, E, inputs, torch, dist, world, rank, local, barrier, a
         "vertex_label_evals_per_s": c["M"] * S * map_per_step * args.steps / total_dev_s,
         "unique_vertex_label_evals_per_s": c["M"] * R * map_per_step * args.steps / total_dev_s,
         "gpu_launches": launches, "clocks": clocks,
-        "setup": {"input_build_s": build_inputs_s},
+        "setup": {"device_input_build_s": build_inputs_s},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -411,17 +409,14 @@ def main():
 
     c = CONFIGS[args.config]
     seed = 42 + rank
-    t0 = time.perf_counter()
-    sl = inputs.synthetic_slice(c["size"], c["block"], brick=c["brick"], seed=seed)
-    build_inputs_s = time.perf_counter() - t0
-    R = sl.graph.num_vertices
-    A = len(sl.graph.neighbors)
-
+    # the slice is built on the device: phantom -> corrupt -> oversegment ->
+    # region graph -> maximal cliques -> neighborhoods (all resident)
     ctx = E.Context(local)
-    ctx.set_graph(sl.graph)
     t0 = time.perf_counter()
-    ctx.build_neighborhoods(sl.cliques)
-    hood_build_ms = (time.perf_counter() - t0) * 1e3
+    info = ctx.synthetic_slice(c["size"], c["block"], brick=c["brick"], seed=seed)
+    build_inputs_s = time.perf_counter() - t0
+    R, A = info["regions"], info["adjacency"]
+    graph_host = ctx.get_graph(sizes=False)  # host copies for the e2e leg
     hoods = ctx.get_hoods()
     H, S = hoods.size(), hoods.total_slots()
     cfg = E.OptimizerConfig(num_labels=c["M"], em_max_iters=c["em"], map_max_iters=MAP_ITERS,
@@ -472,7 +467,8 @@ def main():
 
     # ---- e2e: public C ABI with host (pinned) buffers --------------------------------
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-    g_pin = E.RegionGraph(pin(sl.graph.offsets), pin(sl.graph.neighbors), pin(sl.graph.region_mean))
+    g_pin = E.RegionGraph(pin(graph_host.offsets), pin(graph_host.neighbors),
+                          pin(graph_host.region_mean))
     h_pin = E.NeighborhoodSet(pin(hoods.offsets), pin(hoods.members))
     lab_pin = torch.zeros(R, dtype=torch.int32).pin_memory().numpy().view(np.uint32)
     h2d = 4 * (R + 1) + 4 * A + 8 * R + 4 * (H + 1) + 4 * S
@@ -552,7 +548,9 @@ def main():
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clocks,
-        "setup": {"input_build_s": build_inputs_s, "hood_build_ms_device_call": hood_build_ms},
+        "setup": {"device_input_build_s": build_inputs_s, "host_ties": info["host_ties"],
+                  "note": "phantom -> corrupt -> oversegment -> graph -> cliques -> hoods "
+                          "on the device (csrc/synth.cu, structure.cu, hoods.cu)"},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

@@ -139,6 +139,38 @@ dpmrf_status dpmrf_build_neighborhoods(dpmrf_context* ctx, uint64_t num_cliques,
 dpmrf_status dpmrf_get_hoods(dpmrf_context* ctx, uint64_t* num_hoods, uint64_t* num_slots,
                              uint32_t* offsets, uint32_t* members, uint32_t* source_clique);
 
+/* ---- synthetic inputs on the device ------------ */
+/* PhantomSpec, proj/include/dpmrf/eval/phantom.hpp:9-17. */
+typedef struct dpmrf_phantom_spec {
+  uint32_t width, height;
+  double pore_fraction;  /* [0, 1) */
+  double sp_rate;        /* salt-and-pepper rate, [0, 1] */
+  double gauss_sigma;    /* >= 0 */
+  int32_t ringing;
+  uint64_t seed;
+} dpmrf_phantom_spec;
+
+/* gen_phantom + corrupt (proj/src/eval/phantom.cpp:54-150) ON THE DEVICE,
+ * bit-identical to the reference: the corrupted image becomes the context's
+ * resident image (input of dpmrf_build_region_graph_resident).  truth / image
+ * (width*height bytes each) may be NULL, else receive copies.  *host_ties
+ * (may be NULL) receives the number of pixels whose value fell within 1e-7
+ * of a rounding boundary and was therefore evaluated with the host's libm.
+ * An invalid spec -> DPMRF_INPUT_ERROR (validate_spec, phantom.cpp:46-52). */
+dpmrf_status dpmrf_make_phantom(dpmrf_context* ctx, const dpmrf_phantom_spec* spec,
+                                uint8_t* truth, uint8_t* image, uint32_t* host_ties);
+
+/* grid_oversegment (proj/src/graph/label_map.cpp:79-94), or with brick != 0
+ * the brick oversegmentation of config C (block rows of height `block`, odd
+ * rows shifted by block/2, ids first-seen row-major), ON THE DEVICE for the
+ * resident image's dimensions; the region map becomes resident.
+ * *num_regions receives the region count; region (w*h) may be NULL. */
+dpmrf_status dpmrf_oversegment(dpmrf_context* ctx, uint32_t block, int32_t brick,
+                               uint32_t* num_regions, uint32_t* region);
+
+/* build_region_graph from the resident image and region map. */
+dpmrf_status dpmrf_build_region_graph_resident(dpmrf_context* ctx, uint64_t* num_adjacency);
+
 /* ---- device structure builders -------------- */
 /* build_region_graph, proj/include/dpmrf/graph/region_graph.hpp:31-33 /
  * proj/src/graph/region_graph.cpp:10-73, ON THE DEVICE: `pixels` is the

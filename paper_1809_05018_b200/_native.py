@@ -48,6 +48,13 @@ class CRunStats(ct.Structure):
                 ("device_log_fallbacks", U32)]
 
 
+class CPhantomSpec(ct.Structure):
+    """dpmrf_phantom_spec == PhantomSpec (phantom.hpp:9-17)."""
+
+    _fields_ = [("width", U32), ("height", U32), ("pore_fraction", F64), ("sp_rate", F64),
+                ("gauss_sigma", F64), ("ringing", I32), ("seed", U64)]
+
+
 class CGroupInfo(ct.Structure):
     """dpmrf_group_info."""
 
@@ -66,6 +73,9 @@ CUDA_API = [
     ("dpmrf_set_hoods", ST, [VP, U64, VP, VP]),
     ("dpmrf_build_neighborhoods", ST, [VP, U64, VP, VP, U32, ct.POINTER(U64)]),
     ("dpmrf_get_hoods", ST, [VP, ct.POINTER(U64), ct.POINTER(U64), VP, VP, VP]),
+    ("dpmrf_make_phantom", ST, [VP, ct.POINTER(CPhantomSpec), VP, VP, ct.POINTER(U32)]),
+    ("dpmrf_oversegment", ST, [VP, U32, I32, ct.POINTER(U32), VP]),
+    ("dpmrf_build_region_graph_resident", ST, [VP, ct.POINTER(U64)]),
     ("dpmrf_build_region_graph", ST, [VP, U32, U32, VP, VP, U32, ct.POINTER(U64)]),
     ("dpmrf_build_region_graph_device", ST, [VP, U32, U32, VP, VP, U32, ct.POINTER(U64)]),
     ("dpmrf_get_graph", ST, [VP, ct.POINTER(U32), ct.POINTER(U64), VP, VP, VP, VP]),

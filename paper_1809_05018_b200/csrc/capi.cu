@@ -322,6 +322,7 @@ extern "C" dpmrf_status dpmrf_build_region_graph(dpmrf_context* ctx, uint32_t w,
     }
     // the previous graph (and everything derived from it) is gone from here on
     ctx->has_graph = ctx->has_sizes = ctx->has_cliques = ctx->has_hoods = false;
+    ctx->has_image = ctx->has_regions = false;  // (img_px / img_reg now hold these inputs)
     ctx->prepared = false;
     ++ctx->generation;
     build_region_graph_device(ctx, w, h, px, reg, R);
@@ -344,6 +345,55 @@ extern "C" dpmrf_status dpmrf_build_region_graph_device(dpmrf_context* ctx, uint
     ctx->prepared = false;
     ++ctx->generation;
     build_region_graph_device(ctx, w, h, pixels, region, R);
+    ctx->has_graph = ctx->has_sizes = true;
+    if (num_adjacency) *num_adjacency = ctx->A;
+  });
+}
+
+extern "C" dpmrf_status dpmrf_make_phantom(dpmrf_context* ctx, const dpmrf_phantom_spec* spec,
+                                           uint8_t* truth, uint8_t* image, uint32_t* host_ties) {
+  return guarded([&] {
+    need(ctx && spec, DPMRF_INVALID_ARGUMENT, "null argument");
+    ctx->bind();
+    ctx->has_image = ctx->has_regions = false;
+    const uint32_t ties = make_phantom_device(ctx, *spec);
+    ctx->has_image = true;
+    const uint64_t n = uint64_t(spec->width) * spec->height;
+    if (truth) CK(cudaMemcpyAsync(truth, ctx->img_truth.get(), n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (image) CK(cudaMemcpyAsync(image, ctx->img_px.get(), n, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (host_ties) *host_ties = ties;
+  });
+}
+
+extern "C" dpmrf_status dpmrf_oversegment(dpmrf_context* ctx, uint32_t block, int32_t brick,
+                                          uint32_t* num_regions, uint32_t* region) {
+  return guarded([&] {
+    need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null argument");
+    need(ctx->has_image, DPMRF_INVALID_ARGUMENT, "no resident image (dpmrf_make_phantom)");
+    ctx->bind();
+    const uint32_t R = oversegment_device(ctx, block, brick != 0);
+    ctx->has_regions = true;
+    if (region)
+      CK(cudaMemcpyAsync(region, ctx->img_reg.get(), uint64_t(ctx->img_w) * ctx->img_h * 4,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (num_regions) *num_regions = R;
+  });
+}
+
+extern "C" dpmrf_status dpmrf_build_region_graph_resident(dpmrf_context* ctx,
+                                                          uint64_t* num_adjacency) {
+  return guarded([&] {
+    need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null argument");
+    need(ctx->has_image && ctx->has_regions, DPMRF_INVALID_ARGUMENT,
+         "no resident image / region map");
+    ctx->bind();
+    ctx->has_graph = ctx->has_sizes = ctx->has_cliques = ctx->has_hoods = false;
+    ctx->prepared = false;
+    ++ctx->generation;
+    build_region_graph_device(ctx, ctx->img_w, ctx->img_h, ctx->img_px.get(), ctx->img_reg.get(),
+                              ctx->img_regions);
     ctx->has_graph = ctx->has_sizes = true;
     if (num_adjacency) *num_adjacency = ctx->A;
   });

@@ -29,8 +29,11 @@ struct dpmrf_context {
   bool has_cliques = false;
   uint64_t C = 0, CS = 0;
   dpmrf_b200::DevBuf<uint32_t> c_off, c_mem;
-  dpmrf_b200::DevBuf<uint8_t> img_px;
+  dpmrf_b200::DevBuf<uint8_t> img_px, img_truth;
   dpmrf_b200::DevBuf<uint32_t> img_reg;
+  uint32_t img_w = 0, img_h = 0, img_regions = 0;  // resident image / region map (synth.cu)
+  bool has_image = false, has_regions = false;
+  dpmrf_b200::HostBuf<unsigned long long> h_syn;
   dpmrf_b200::DevBuf<uint32_t> st_u32[6];
   dpmrf_b200::DevBuf<unsigned long long> st_u64[3];
   dpmrf_b200::DevBuf<uint32_t> cl_tmp[5];               // frontier x2, counts, flags, positions
@@ -181,4 +184,7 @@ void build_neighborhoods_from(dpmrf_context* ctx, uint64_t C, const uint32_t* c_
 void build_region_graph_device(dpmrf_context* ctx, uint32_t width, uint32_t height,
                                const uint8_t* pixels_dev, const uint32_t* region_dev, uint32_t R);
 void enumerate_maximal_cliques_device(dpmrf_context* ctx);
+// synth.cu
+uint32_t make_phantom_device(dpmrf_context* ctx, const dpmrf_phantom_spec& spec);
+uint32_t oversegment_device(dpmrf_context* ctx, uint32_t block, bool brick);
 }  // namespace dpmrf_b200

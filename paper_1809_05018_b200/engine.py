@@ -275,6 +275,60 @@ class Context:
                "dpmrf_get_hoods")
         return NeighborhoodSet(off, mem, src)
 
+    # -- synthetic inputs on the device --
+    def make_phantom(self, width, height, pore_fraction=0.25, sp_rate=0.0, gauss_sigma=0.0,
+                     ringing=False, seed=0, copy_out=True):
+        """gen_phantom + corrupt (phantom.cpp:54-150) on the device; the image
+        stays resident.  Returns (truth, image, host_ties) -- arrays are None
+        unless copy_out."""
+        spec = N.CPhantomSpec(width, height, pore_fraction, sp_rate, gauss_sigma, int(ringing),
+                              seed)
+        n = width * height
+        self._img_n = n
+        truth = np.zeros(n, np.uint8) if copy_out else None
+        image = np.zeros(n, np.uint8) if copy_out else None
+        ties = ct.c_uint32(0)
+        _check(self._lib.dpmrf_make_phantom(self.h, ct.byref(spec), N.ptr(truth), N.ptr(image),
+                                            ct.byref(ties)), "make_phantom")
+        return truth, image, ties.value
+
+    def oversegment(self, block: int, brick: bool = False, copy_out=True):
+        """Grid (label_map.cpp:79-94) or brick oversegmentation of the resident
+        image on the device -> (num_regions, region map or None)."""
+        R = ct.c_uint32(0)
+        n = 0
+        region = None
+        if copy_out:
+            # dimensions of the resident image are known to the caller; size from R later
+            region = np.zeros(self._img_n, np.uint32) if getattr(self, "_img_n", 0) else None
+        _check(self._lib.dpmrf_oversegment(self.h, block, int(brick), ct.byref(R), N.ptr(region)),
+               "oversegment")
+        del n
+        return R.value, region
+
+    def build_region_graph_resident(self) -> int:
+        A = ct.c_uint64(0)
+        _check(self._lib.dpmrf_build_region_graph_resident(self.h, ct.byref(A)),
+               "build_region_graph_resident")
+        self._graph_key = None
+        self._hoods_key = None
+        return A.value
+
+    def synthetic_slice(self, size=2560, block=8, brick=False, seed=42, pore=0.25, sp=0.05,
+                        gauss=100.0, ringing=True, height=None) -> dict:
+        """The BASELINE.json synthetic slice built entirely on the device:
+        phantom -> corrupt -> oversegment -> region graph -> maximal cliques
+        -> neighborhoods, all resident (ready for optimize)."""
+        h = height or size
+        self._img_n = size * h
+        _, _, ties = self.make_phantom(size, h, pore, sp, gauss, ringing, seed, copy_out=False)
+        R, _ = self.oversegment(block, brick, copy_out=False)
+        A = self.build_region_graph_resident()
+        self.R = R
+        C, CS = self.enumerate_maximal_cliques()
+        S = self.build_neighborhoods_resident()
+        return {"regions": R, "adjacency": A, "cliques": C, "slots": S, "host_ties": ties}
+
     # -- device structure builders (SURVEY.md §8(f) items 1-2) --
     def build_region_graph(self, width: int, height: int, pixels, region, num_regions: int) -> int:
         """build_region_graph (region_graph.cpp:10-73) on the device from a u8

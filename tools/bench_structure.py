@@ -69,6 +69,25 @@ def main():
                 steps["graph"].append((t1 - t0) * 1e3)
                 steps["cliques"].append((t2 - t1) * 1e3)
                 steps["hoods"].append((t3 - t2) * 1e3)
+        # the whole synthetic slice on the device: phantom + corrupt, oversegmentation
+        syn = {"phantom": [], "oversegment": [], "graph": [], "cliques": [], "hoods": []}
+        ties = 0
+        for rep in range(args.reps + 1):
+            t0 = time.perf_counter()
+            _, _, ties = ctx.make_phantom(size, size, 0.25, 0.05, 100.0, True, 42, copy_out=False)
+            t1 = time.perf_counter()
+            ctx.oversegment(block, brick, copy_out=False)
+            t2 = time.perf_counter()
+            ctx.build_region_graph_resident()
+            t3 = time.perf_counter()
+            ctx.enumerate_maximal_cliques()
+            t4 = time.perf_counter()
+            ctx.build_neighborhoods_resident()
+            t5 = time.perf_counter()
+            if rep:
+                for k, a, b in (("phantom", t0, t1), ("oversegment", t1, t2), ("graph", t2, t3),
+                                ("cliques", t3, t4), ("hoods", t4, t5)):
+                    syn[k].append((b - a) * 1e3)
         g = ctx.get_graph()
         cl = ctx.get_cliques()
         same = bool(np.array_equal(g.offsets, g_host.offsets) and
@@ -81,7 +100,9 @@ def main():
                 "device_ms": {k: statistics.median(v) for k, v in steps.items()},
                 "host_cpp_builder_s": {"graph": t_host_graph, "cliques": t_host_cliques},
                 "device_equals_host_builder": same,
-                "h2d_bytes": 5 * size * size}
+                "h2d_bytes": 5 * size * size,
+                "device_synthetic_ms": {k: statistics.median(v) for k, v in syn.items()},
+                "device_synthetic_host_ties": ties}
         if name in args.ref_configs.split(","):
             import oracle
             if oracle.ref_available():
