@@ -545,6 +545,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     a.minE = minE2;
     a.hist = ctx->hist.ensure(uint64_t(a.ring) * Hs);
     a.flags = full ? ctx->flags.ensure(uint64_t(map_max) * Hs) : nullptr;
+    a.eq = a.hood_k ? ctx->hood_eq.ensure(Hs) : nullptr;  // (packed hood pass only)
     // [em_done, pending_done, em_count, pad | per-MAP-iteration counters]
     uint32_t* state = ctx->unconv.ensure(uint64_t(map_max) + 4);
     a.unconv = state + 4;

@@ -57,7 +57,7 @@ struct dpmrf_context {
   // ---- optimization buffers ----
   dpmrf_b200::DevBuf<uint8_t> lab[2];
   dpmrf_b200::DevBuf<double> minE, hist, terms, params, em_out;
-  dpmrf_b200::DevBuf<uint8_t> flags;
+  dpmrf_b200::DevBuf<uint8_t> flags, hood_eq;
   dpmrf_b200::DevBuf<uint32_t> unconv, labels32;
   dpmrf_b200::MStepBuffers ms;
   dpmrf_b200::ScanWorkspace scan;

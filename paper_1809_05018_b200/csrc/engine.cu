@@ -1500,17 +1500,23 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
       u[4 * q + 2] = w.z;
       u[4 * q + 3] = w.w;
     }
-    // The window rows are loaded up front, independent of the gathers, so a
-    // hood costs two dependent memory round trips (structure -> minima)
-    // rather than one more per window row: +4% at 16384^2.  (Measured and
-    // rejected: evict-first hints on the streamed structure and rows, two
-    // hoods per thread, and any variant that spills under the 32-register cap.)
     const int R1 = a.ring;
     const int nwin = t >= a.L ? a.L : 0;
-    double prev[kWinRegs];
-#pragma unroll
-    for (int i = 0; i < kWinRegs; ++i)
-      prev[i] = i < nwin ? a.hist[uint64_t((t - 1 - i) % R1) * a.Hs + h] : 0.0;
+    // Window test with an equal-run count: eq[h] = how many predecessors of
+    // the previous row are bit-identical to it (a hood whose members' minima
+    // did not change sums to the same bits).  Only row t-1 and the count are
+    // read up front; an older row is read only when its comparison is not
+    // already implied -- the previous comparison passed and the row is not
+    // inside the equal run.  Same flags as reading every row (the skipped
+    // comparisons are |x - x| = 0 < tol), 18 instead of 32 window bytes per
+    // hood.
+    // (a.eq is always set when the packed hood layout is in use)
+    double p1 = 0.0;
+    uint32_t e1 = 0;
+    if (t >= 1) {
+      p1 = a.hist[uint64_t((t - 1) % R1) * a.Hs + h];
+      e1 = a.eq[h];
+    }
     double e[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {  // all gathers in flight before the fold
@@ -1525,12 +1531,21 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
     }
     a.hist[uint64_t(t % R1) * a.Hs + h] = sum;
     int ok = nwin > 0;
-#pragma unroll
-    for (int i = 0; i < kWinRegs; ++i)
-      if (i < nwin && !(fabs(__dsub_rn(sum, prev[i])) < a.tol)) ok = 0;
-    for (int i = kWinRegs; i < nwin; ++i) {  // windows longer than kWinRegs
-      const double p = a.hist[uint64_t((t - 1 - i) % R1) * a.Hs + h];
-      if (!(fabs(__dsub_rn(sum, p)) < a.tol)) ok = 0;
+    const bool same = t >= 1 && sum == p1;  // (false for NaN)
+    a.eq[h] = static_cast<uint8_t>(same ? min(e1 + 1u, 255u) : 0u);
+    if (nwin) {
+      if (!(fabs(__dsub_rn(sum, p1)) < a.tol)) {
+        ok = 0;
+      } else if (e1 + 1 < uint32_t(nwin)) {
+        // rows t-1-e1 .. t-1 equal p1 (their comparisons are implied); read the rest
+        for (int i = int(e1) + 2; i <= nwin; ++i) {
+          const double p = a.hist[uint64_t((t - i) % R1) * a.Hs + h];
+          if (!(fabs(__dsub_rn(sum, p)) < a.tol)) {
+            ok = 0;
+            break;
+          }
+        }
+      }
     }
     if (a.flags) a.flags[uint64_t(t) * a.Hs + h] = static_cast<uint8_t>(ok);
     not_conv = !ok;

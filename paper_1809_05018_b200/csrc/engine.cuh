@@ -43,6 +43,7 @@ struct MapArgs {
   double* minE;    // R
   double* hist;    // ring x Hs hood energies
   uint8_t* flags;  // map_max x Hs convergence flags (nullptr = not recorded)
+  uint8_t* eq;     // Hs equal-run counts of the window test (packed hood pass; nullptr = off)
   uint32_t* unconv;  // per MAP iteration count of unconverged hoods
   uint32_t* tile_counts;  // 2 x tiles x M: label counts per 256-vertex tile, by iteration parity
   uint32_t tiles;

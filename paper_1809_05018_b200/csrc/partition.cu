@@ -186,6 +186,7 @@ struct Part {
   // hpart: the hood-energy series' leaf partials of every rank (W x chunkH/1024)
   DevBuf<double> minE, hist, hpart, params, em_out, terms, em_rec, em_hist;
   DevBuf<uint32_t> state;  // [em_done, pending, em_count, pad | unconv[map_max]]
+  DevBuf<uint8_t> eq;      // equal-run counts of the window test (owned series)
   MStepBuffers ms;
   MapArgs a{};
   EmEpilogueArgs ep{};
@@ -462,6 +463,7 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
     a.minE = p.minE.ensure(R ? R : 1);
     a.hist = p.hist.ensure(uint64_t(ring) * (Hs ? Hs : 1));
     a.flags = nullptr;
+    a.eq = a.hood_k ? p.eq.ensure(Hs ? Hs : 1) : nullptr;
     uint32_t* state = p.state.ensure(uint64_t(map_max) + 4);
     a.unconv = state + 4;
     a.tile_counts = nullptr;  // the M-step counts the gathered labels itself
