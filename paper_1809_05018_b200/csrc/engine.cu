@@ -1389,12 +1389,17 @@ __device__ __forceinline__ void load_i16(const int16_t* __restrict__ p, int16_t 
 // Vertex pass over P vertices per thread (v, v + 256, ...: block blk covers
 // the P label tiles P*blk .. P*blk + P-1).  All structure loads of the P
 // vertices are issued before their label gathers.
+// The static structure (packed adjacency, cover flags) is read BEFORE
+// griddepcontrol.wait -- it never changes during optimize, so the loads
+// overlap the predecessor's drain -- and the skip decision (the previous
+// iteration's unconverged counter) is read beside the first dependent loads
+// rather than ahead of them: one memory round trip less per launch.
 template <int MT, int K, int P = 1>
 __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
                                                    const uint8_t* __restrict__ lab_in,
                                                    uint8_t* __restrict__ lab_out,
                                                    double* __restrict__ minE, int t,
-                                                   uint32_t blk) {
+                                                   uint32_t blk, int skip_t) {
   const uint32_t M = MT > 0 ? uint32_t(MT) : a.M;
   const uint32_t v0 = a.v_begin + blk * (kVtxThreads * P) + threadIdx.x;
   int16_t d[P][K];
@@ -1404,10 +1409,16 @@ __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
     const uint32_t v = v0 + j * kVtxThreads;
     if (v < a.v_end) {
       load_i16<K>(a.adj_pk + uint64_t(v) * K, d[j]);
-      old[j] = lab_in[v];
       cov[j] = a.cover[v];
     }
   }
+  pdl_wait();
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const uint32_t v = v0 + j * kVtxThreads;
+    if (v < a.v_end) old[j] = lab_in[v];
+  }
+  if (map_iter_skipped(a.unconv, skip_t, a.fixed)) return;  // uniform over the grid
   uint32_t nl[P];
 #pragma unroll
   for (int j = 0; j < P; ++j) {
@@ -1476,21 +1487,22 @@ template <int MT, int K>
 __global__ void __launch_bounds__(kVtxThreads)
     k_vertex_packed(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                     int t) {
-  pdl_wait();
-  if (map_iter_skipped(a.unconv, t, a.fixed)) return;
-  vertex_packed_body<MT, K>(a, lab_in, lab_out, a.minE, t, blockIdx.x);
+  vertex_packed_body<MT, K>(a, lab_in, lab_out, a.minE, t, blockIdx.x, t);
 }
 
+// (static structure before griddepcontrol.wait, skip decision beside the
+// first dependent loads -- see vertex_packed_body)
 template <int K>
 __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
                                                  const double* __restrict__ minE, int t,
-                                                 uint32_t blk) {
+                                                 uint32_t blk, int skip_t) {
   static_assert(K == 8 || K == 16, "hood pack width");
   const uint64_t h = a.h_begin + uint64_t(blk) * kHoodThreads + threadIdx.x;
-  int not_conv = 0;
-  if (h < a.h_end) {
-    const uint32_t base = a.hood_base[h];
-    uint32_t u[K / 2];
+  const bool live = h < a.h_end;
+  uint32_t base = 0;
+  uint32_t u[K / 2];
+  if (live) {
+    base = a.hood_base[h];
     const uint4* src = reinterpret_cast<const uint4*>(a.hood_pk + h * K);
 #pragma unroll
     for (int q = 0; q < K / 8; ++q) {
@@ -1500,6 +1512,11 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
       u[4 * q + 2] = w.z;
       u[4 * q + 3] = w.w;
     }
+  }
+  pdl_wait();
+  int not_conv = 0;
+  if (live) {
+    if (map_iter_skipped(a.unconv, skip_t, a.fixed)) return;  // uniform over the grid
     const int R1 = a.ring;
     const int nwin = t >= a.L ? a.L : 0;
     // Window test with an equal-run count: eq[h] = how many predecessors of
@@ -1550,15 +1567,14 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
     if (a.flags) a.flags[uint64_t(t) * a.Hs + h] = static_cast<uint8_t>(ok);
     not_conv = !ok;
   }
+  if (!live && map_iter_skipped(a.unconv, skip_t, a.fixed)) return;
   const int bu = __syncthreads_count(not_conv);
   if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[t], uint32_t(bu));
 }
 
 template <int K>
 __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) {
-  pdl_wait();
-  if (map_iter_skipped(a.unconv, t, a.fixed)) return;
-  hood_packed_body<K>(a, a.minE, t, blockIdx.x);
+  hood_packed_body<K>(a, a.minE, t, blockIdx.x, t);
 }
 
 // One kernel per MAP-iteration boundary: the hood pass of iteration t-1 and
@@ -1577,20 +1593,20 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
   static_assert(kVtxThreads == kHoodThreads, "one block shape for both passes");
   static_assert(kVtxThreads == kTileThreads, "scatter tiles are vertex blocks");
   extern __shared__ uint32_t fused_smem[];
-  pdl_wait();
   if (blockIdx.x < nh) {
-    if (!map_iter_skipped(a.unconv, t - 1, a.fixed)) hood_packed_body<KH>(a, minE_prev, t - 1, blockIdx.x);
+    hood_packed_body<KH>(a, minE_prev, t - 1, blockIdx.x, t - 1);
   } else if (blockIdx.x >= nh + nv) {
     // last launch (t = map_max): the M-step's label scatter runs beside the
     // hood pass of the last iteration -- it reads only the committed labels
     // and label counts of the last vertex pass (see executed_iters_known)
+    pdl_wait();
     if (!em_skipped(a.unconv))
       label_scatter_small_body<true>(sc.lab_even, sc.lab_odd, a.unconv, a.unconv, t, a.fixed,
                                      sc.R, sc.M, sc.Hs, sc.mean, sc.counts, sc.tiles, sc.layout,
                                      sc.x, blockIdx.x - nh - nv, fused_smem);
   } else {
-    if (!map_iter_skipped(a.unconv, t > 0 ? t - 1 : 0, a.fixed))
-      vertex_packed_body<MT, KV, VP>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh);
+    vertex_packed_body<MT, KV, VP>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh,
+                                   t > 0 ? t - 1 : 0);
   }
 }
 
