@@ -827,9 +827,9 @@ __global__ void __launch_bounds__(256)
   const uint32_t* n = layout;
   const uint32_t* label_start = layout + M;
   const uint32_t* leaf_start = layout + 2 * M + 1;
-  if (em_skipped(unconv)) return;  // uniform: no block takes a ticket
   const uint32_t nseries = kSq ? M : M + 1;
-  const uint32_t total = leaf_start[nseries];
+  const uint32_t total = leaf_start[nseries];  // (issued beside the skip flag's load)
+  if (em_skipped(unconv)) return;  // uniform: no block takes a ticket
   const uint32_t first = blockIdx.x * kLeavesPerBlock;
   if (first < total) {
     const double* hood_row = nullptr;
