@@ -780,10 +780,28 @@ constexpr int kLeafStride = kFoldLeaf + 1;
 // loop directly and re-arms the MAP counters for the next EM (no separate
 // prologue / epilogue launches); otherwise the stop is left pending for
 // k_em_prologue.
-__device__ void em_record(const EmEpilogueArgs& a, bool merged) {
-  const int lane = threadIdx.x & 31;
-  const int T = executed_iters(a.unconv, a.map_max, a.fixed);
+// What em_record reads from global state that does not depend on the
+// M-step's results: loaded by the sq-pass tail before its trees, so those
+// round trips overlap the tree instead of following it.
+constexpr int kPrefetchWin = 8;
+struct EmPrefetch {
+  int T;
+  uint32_t e;
+  double hist[kPrefetchWin];  // em_hist[e - 1 - i]
+};
+
+__device__ __forceinline__ void em_prefetch(const EmEpilogueArgs& a, EmPrefetch* pf) {
+  pf->T = executed_iters(a.unconv, a.map_max, a.fixed);
   const uint32_t e = a.unconv[kEmCount];
+  pf->e = e;
+  for (int i = 1; i <= a.L && i <= kPrefetchWin; ++i)
+    pf->hist[i - 1] = int(e) >= i ? a.em_hist[e - i] : 0.0;
+}
+
+__device__ void em_record(const EmEpilogueArgs& a, bool merged, const EmPrefetch* pf = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const int T = pf ? pf->T : executed_iters(a.unconv, a.map_max, a.fixed);
+  const uint32_t e = pf ? pf->e : a.unconv[kEmCount];
   const uint32_t M = a.M;
   double* rec = a.em_rec + uint64_t(e) * (3 + 3 * M);
   for (uint32_t l = lane; l < M; l += 32) {  // one lane per label evaluates the (long) device log
@@ -803,8 +821,10 @@ __device__ void em_record(const EmEpilogueArgs& a, bool merged) {
   uint32_t conv = 0;
   if (int(e) + 1 >= a.L + 1) {
     conv = 1;
-    for (int i = 1; i <= a.L; ++i)
-      if (!(fabs(__dsub_rn(total, a.em_hist[e - i])) < a.tol)) conv = 0;
+    for (int i = 1; i <= a.L; ++i) {
+      const double prev = pf && i <= kPrefetchWin ? pf->hist[i - 1] : a.em_hist[e - i];
+      if (!(fabs(__dsub_rn(total, prev)) < a.tol)) conv = 0;
+    }
   }
   rec[0] = total;
   rec[1] = static_cast<double>(T);
@@ -864,25 +884,51 @@ __global__ void __launch_bounds__(256)
       mu_s[threadIdx.x] = mu;
     }
     __syncthreads();
-    // all 32 loads of a thread are issued before any store (one round trip)
-    constexpr int kPer = kLeavesPerBlock * int(kFoldLeaf) / 256;
-    double r[kPer];
+    // Two-stage staging: all warps stage the first half of every leaf; then
+    // warp 0's chain lanes fold those 512 elements while warps 1-7 stage the
+    // second halves and signal named barrier 1, which the chain lanes wait on
+    // at the midpoint -- the second half's loads hide behind the first
+    // half's dependent adds.
+    constexpr uint32_t kHalf = kFoldLeaf / 2;
+    {
+      constexpr int kPerA = kLeavesPerBlock * int(kHalf) / 256;  // 16
+      double r[kPerA];
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
-      const uint32_t j = flat / kFoldLeaf, i = flat % kFoldLeaf;
-      r[q] = i < len_s[j] ? __ldcg(src_s[j] + i) : 0.0;
-    }
+      for (int q = 0; q < kPerA; ++q) {
+        const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
+        const uint32_t j = flat / kHalf, i = flat % kHalf;
+        r[q] = i < len_s[j] ? __ldcg(src_s[j] + i) : 0.0;
+      }
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
-      stage[(flat / kFoldLeaf) * kLeafStride + flat % kFoldLeaf] = r[q];
+      for (int q = 0; q < kPerA; ++q) {
+        const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
+        stage[(flat / kHalf) * kLeafStride + flat % kHalf] = r[q];
+      }
     }
     __syncthreads();
-    if (threadIdx.x < kLeavesPerBlock && len_s[threadIdx.x] != 0) {
-      const uint32_t len = len_s[threadIdx.x];
+    if (threadIdx.x >= 32) {
+      constexpr uint32_t kN = kLeavesPerBlock * kHalf;  // 4096 second-half elements
+      constexpr int kPerB = int((kN + 223) / 224);       // over warps 1-7
+      double r[kPerB];
+      const uint32_t tb = threadIdx.x - 32;
+#pragma unroll
+      for (int q = 0; q < kPerB; ++q) {
+        const uint32_t flat = uint32_t(q) * 224u + tb;
+        const uint32_t j = flat / kHalf, i = kHalf + flat % kHalf;
+        r[q] = flat < kN && i < len_s[j] ? __ldcg(src_s[j] + i) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kPerB; ++q) {
+        const uint32_t flat = uint32_t(q) * 224u + tb;
+        if (flat < kN) stage[(flat / kHalf) * kLeafStride + kHalf + flat % kHalf] = r[q];
+      }
+      __threadfence_block();
+      asm volatile("bar.arrive 1, 256;" ::: "memory");
+    } else {
+      const bool chain = threadIdx.x < kLeavesPerBlock && len_s[threadIdx.x] != 0;
+      const uint32_t len = chain ? len_s[threadIdx.x] : 0u;
       const double* v = stage + threadIdx.x * kLeafStride;
-      const double mu = kSq ? mu_s[threadIdx.x] : 0.0;
+      const double mu = (kSq && chain) ? mu_s[threadIdx.x] : 0.0;
       // element term: x (sum pass) or (x - mu)^2 (sq pass); independent of acc
       auto term = [&](double x) {
         if (kSq) {
@@ -891,31 +937,38 @@ __global__ void __launch_bounds__(256)
         }
         return x;
       };
-      // Software-pipelined chain: the next 16 operands are read from shared
-      // memory while the current 16 dependent adds retire, so the chain runs
-      // at the DADD latency instead of LDS + DADD per group.
-      constexpr int kG = 16;
-      double acc = term(v[0]);
-      uint32_t i = 1;
-      double cur[kG], nxt[kG];
-      if (i + kG <= len) {
+      // Software-pipelined chain over [i, end): the next 16 operands are read
+      // from shared memory while the current 16 dependent adds retire.
+      auto fold = [&](double acc, uint32_t i, uint32_t end) {
+        constexpr int kG = 16;
+        double cur[kG], nxt[kG];
+        if (i + kG <= end) {
 #pragma unroll
-        for (int j = 0; j < kG; ++j) cur[j] = v[i + j];
-        while (i + 2 * kG <= len) {
+          for (int j = 0; j < kG; ++j) cur[j] = v[i + j];
+          while (i + 2 * kG <= end) {
 #pragma unroll
-          for (int j = 0; j < kG; ++j) nxt[j] = v[i + kG + j];
+            for (int j = 0; j < kG; ++j) nxt[j] = v[i + kG + j];
+#pragma unroll
+            for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, term(cur[j]));
+#pragma unroll
+            for (int j = 0; j < kG; ++j) cur[j] = nxt[j];
+            i += kG;
+          }
 #pragma unroll
           for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, term(cur[j]));
-#pragma unroll
-          for (int j = 0; j < kG; ++j) cur[j] = nxt[j];
           i += kG;
         }
-#pragma unroll
-        for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, term(cur[j]));
-        i += kG;
+        for (; i < end; ++i) acc = __dadd_rn(acc, term(v[i]));
+        return acc;
+      };
+      double acc = 0.0;
+      if (chain) acc = fold(term(v[0]), 1, len < kHalf ? len : kHalf);
+      __syncwarp();
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // the second halves are staged
+      if (chain) {
+        if (len > kHalf) acc = fold(acc, kHalf, len);
+        partials[first + threadIdx.x] = acc;
       }
-      for (; i < len; ++i) acc = __dadd_rn(acc, term(v[i]));
-      partials[first + threadIdx.x] = acc;
     }
   }
   if (kSq && merged) {
@@ -935,6 +988,8 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (!last) return;
   __threadfence();
+  __shared__ EmPrefetch pf;
+  if (kSq && merged && threadIdx.x == 0) em_prefetch(ep, &pf);
   constexpr uint32_t kStageDoubles = kLeavesPerBlock * kLeafStride;
   static_assert(8 * 1056 >= kStageDoubles, "tail stage");
   auto finish = [&](uint32_t s, double folded) {  // parameters / total energy of series s
@@ -983,7 +1038,7 @@ __global__ void __launch_bounds__(256)
       if (lane == 0) finish(w, cnt ? p[0] : 0.0);
     }
     __syncthreads();
-    if (kSq && merged && threadIdx.x < 32) em_record(ep, true);
+    if (kSq && merged && threadIdx.x < 32) em_record(ep, true, &pf);
     if (threadIdx.x == 0) *done = 0;  // re-arm the ticket for the next launch
     return;
   }
@@ -1069,7 +1124,10 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) finish(s, __ldcg(p));
     __syncthreads();
   }
-  if (kSq && merged && threadIdx.x < 32) em_record(ep, true);
+  if (kSq && merged && threadIdx.x < 32) {
+    __syncwarp();
+    em_record(ep, true, &pf);
+  }
   if (threadIdx.x == 0) *done = 0;  // re-arm the ticket for the next launch
 }
 
