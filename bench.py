@@ -379,9 +379,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DPMRF_BENCH_SHARED_GPU=1 (testing the multi-rank plumbing on a one-GPU
+    # box): every rank uses device local % device_count and the gloo backend
+    # for the timing collectives (NCCL refuses two ranks on one device).
+    shared = os.environ.get("DPMRF_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    coll_dev = "cpu" if shared else "cuda"
 
     def barrier():
         if world > 1:
@@ -391,14 +401,14 @@ def main():
     def allmax(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def allsum(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
