@@ -532,7 +532,10 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
           launch_hood_sums(pp->a, t, st);
           ++k;
         }
-        sum_counters(g, t, st, &k);
+        // The summed counter decides the MAP early exit (optimize.cpp:59);
+        // fixed-work runs never read it (executed_iters == map_max), so they
+        // skip one latency-bound collective per MAP iteration.
+        if (!fixed) sum_counters(g, t, st, &k);
       }
       for (auto& pp : g->parts) {
         Part& p = *pp;
