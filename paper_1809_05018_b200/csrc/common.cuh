@@ -12,8 +12,11 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <utility>
 
 #include "../../include/dpmrf_cuda.h"
@@ -96,6 +99,21 @@ struct HostBuf {
     return p;
   }
 };
+
+// Opt a kernel into `bytes` of dynamic shared memory on the current device,
+// once per (kernel, device); thread-safe.
+template <class F>
+inline void ensure_dynamic_smem(F* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, size_t>> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, bytes);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(key)) return;
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  done.insert(key);
+}
 
 // Programmatic Dependent Launch: a kernel launched this way may be scheduled
 // while its stream predecessor is still draining; it must execute pdl_wait()

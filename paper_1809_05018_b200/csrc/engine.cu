@@ -1843,15 +1843,9 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
                (const uint32_t*)tile_base, (const uint32_t*)layout, x);
     ++n;
   }
-  static bool smem_set = false;
   const size_t leaf_smem = size_t(8) * 1056 * sizeof(double);  // 8 leaves (the tail: 8 x 1056)
-  if (!smem_set) {
-    CK(cudaFuncSetAttribute(k_leaf_fold<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(leaf_smem)));
-    CK(cudaFuncSetAttribute(k_leaf_fold<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(leaf_smem)));
-    smem_set = true;
-  }
+  ensure_dynamic_smem(k_leaf_fold<false>, leaf_smem);
+  ensure_dynamic_smem(k_leaf_fold<true>, leaf_smem);
   const unsigned lg = grid_for(max_leaves, kLeavesPerBlock);
   const EmEpilogueArgs epv = ep ? *ep : EmEpilogueArgs{};
   launch_pdl(k_leaf_fold<false>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
@@ -1905,11 +1899,7 @@ void launch_row_leaves(const double* hist, int ring, uint64_t Hs, const uint32_t
   if (he <= hb) return;
   const uint64_t nl = (he + kFoldLeaf - 1) / kFoldLeaf - hb / kFoldLeaf;
   const size_t smem = size_t(kLeavesPerBlock) * kLeafStride * sizeof(double);
-  static bool smem_set = false;
-  if (!smem_set) {
-    CK(cudaFuncSetAttribute(k_row_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    smem_set = true;
-  }
+  ensure_dynamic_smem(k_row_leaves, smem);
   launch_pdl(k_row_leaves, dim3(grid_for(nl, kLeavesPerBlock)), dim3(256), smem, s, hist, ring,
              Hs, unconv, map_max, fixed, hb, he, out);
 }

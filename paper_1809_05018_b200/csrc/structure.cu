@@ -544,8 +544,7 @@ void build_region_graph_device(dpmrf_context* ctx, uint32_t w, uint32_t h, const
   CK(cudaMemsetAsync(err, 0, (uint64_t(R) * 4 + 8) * 4, st));
   CK(cudaMemsetAsync(rsum, 0, uint64_t(R) * 8, st));
   const size_t smem = kPairSlots * 8 + 3 * kRegSlots * 4;
-  CK(cudaFuncSetAttribute(k_boundary_tiles<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          int(smem)));
+  ensure_dynamic_smem(k_boundary_tiles<0>, smem);
   const dim3 grid(tx, ty);
   k_boundary_tiles<0><<<grid, kTileThreads, smem, st>>>(reg, px, w, h, R, tile_cnt, nullptr,
                                                         nullptr, rsize, rsum, err);
