@@ -1345,6 +1345,10 @@ void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
   const dim3 g(nh + nv + ns), blk(kVtxThreads);
 #define MF(MT, KV, KH) launch_pdl(k_map_fused<MT, KV, KH, 1>, g, blk, smem, s, a, lab_in, lab_out, \
                                   minE_prev, minE_cur, t, nh, nv, scv)
+  if (a.M == 5 && a.adj_k == 8 && a.hood_k == 16) {  // config C's layout: label loop unrolled
+    MF(5, 8, 16);
+    return;
+  }
   switch (sel) {
     case 0:
       if (vp == 2)
