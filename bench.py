@@ -485,7 +485,7 @@ def main():
     d2h = 4 * R + 16 * c["M"]
     barrier()
     e2e_times = []
-    for _ in range(max(3, args.steps // 2)):
+    for _ in range(max(3, args.steps)):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
