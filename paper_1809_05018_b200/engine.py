@@ -227,6 +227,7 @@ class Context:
         self.H = 0
         self.S = 0
         self._cliques_n = (0, 0)
+        self._img_n = 0  # pixels of the resident image (make_phantom)
 
     def close(self):
         if self.h:
@@ -284,26 +285,21 @@ class Context:
         spec = N.CPhantomSpec(width, height, pore_fraction, sp_rate, gauss_sigma, int(ringing),
                               seed)
         n = width * height
-        self._img_n = n
         truth = np.zeros(n, np.uint8) if copy_out else None
         image = np.zeros(n, np.uint8) if copy_out else None
         ties = ct.c_uint32(0)
         _check(self._lib.dpmrf_make_phantom(self.h, ct.byref(spec), N.ptr(truth), N.ptr(image),
                                             ct.byref(ties)), "make_phantom")
+        self._img_n = n
         return truth, image, ties.value
 
     def oversegment(self, block: int, brick: bool = False, copy_out=True):
         """Grid (label_map.cpp:79-94) or brick oversegmentation of the resident
         image on the device -> (num_regions, region map or None)."""
         R = ct.c_uint32(0)
-        n = 0
-        region = None
-        if copy_out:
-            # dimensions of the resident image are known to the caller; size from R later
-            region = np.zeros(self._img_n, np.uint32) if getattr(self, "_img_n", 0) else None
+        region = np.zeros(self._img_n, np.uint32) if copy_out and self._img_n else None
         _check(self._lib.dpmrf_oversegment(self.h, block, int(brick), ct.byref(R), N.ptr(region)),
                "oversegment")
-        del n
         return R.value, region
 
     def build_region_graph_resident(self) -> int:
@@ -320,7 +316,6 @@ class Context:
         phantom -> corrupt -> oversegment -> region graph -> maximal cliques
         -> neighborhoods, all resident (ready for optimize)."""
         h = height or size
-        self._img_n = size * h
         _, _, ties = self.make_phantom(size, h, pore, sp, gauss, ringing, seed, copy_out=False)
         R, _ = self.oversegment(block, brick, copy_out=False)
         A = self.build_region_graph_resident()
