@@ -33,6 +33,55 @@ __global__ void lds_chain(double* out, int n, long long* cycles) {
   cycles[0] = t1 - t0;
 }
 
+// The leaf-fold chain as k_leaf_fold runs it: 8 lanes of one warp, each a
+// 1023-add dependent chain over its own shared-memory row (stride 1025),
+// next 16 operands loaded while the current 16 adds retire.
+__global__ void leaf_chain_smem(double* out, long long* cycles) {
+  __shared__ double s[4 * 1025];  // (48 KB static limit: 4 rows)
+  for (int i = threadIdx.x; i < 4 * 1025; i += blockDim.x) s[i] = 1.0 + i * 1e-9;
+  __syncthreads();
+  if (threadIdx.x >= 4) return;
+  const double* v = s + threadIdx.x * 1025;
+  const long long t0 = clock64();
+  constexpr int kG = 16;
+  double acc = v[0], cur[kG], nxt[kG];
+  unsigned i = 1;
+#pragma unroll
+  for (int j = 0; j < kG; ++j) cur[j] = v[i + j];
+  while (i + 2 * kG <= 1024) {
+#pragma unroll
+    for (int j = 0; j < kG; ++j) nxt[j] = v[i + kG + j];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, cur[j]);
+#pragma unroll
+    for (int j = 0; j < kG; ++j) cur[j] = nxt[j];
+    i += kG;
+  }
+#pragma unroll
+  for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, cur[j]);
+  i += kG;
+  for (; i < 1024; ++i) acc = __dadd_rn(acc, v[i]);
+  const long long t1 = clock64();
+  out[threadIdx.x] = acc;
+  if (threadIdx.x == 0) cycles[0] = t1 - t0;
+}
+
+// Same chain with operands already in registers (the DADD-latency floor).
+__global__ void leaf_chain_regs(double* out, long long* cycles) {
+  if (threadIdx.x >= 8) return;
+  double r[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) r[j] = 1.0 + (threadIdx.x * 32 + j) * 1e-9;
+  const long long t0 = clock64();
+  double acc = r[0];
+  for (int rep = 0; rep < 32; ++rep)
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc = __dadd_rn(acc, r[j]);
+  const long long t1 = clock64();
+  out[threadIdx.x] = acc;
+  if (threadIdx.x == 0) cycles[0] = t1 - t0;
+}
+
 __global__ void grid_barriers(int iters, int* sink) {
   cg::grid_group g = cg::this_grid();
   for (int i = 0; i < iters; ++i) g.sync();
@@ -86,6 +135,12 @@ int main() {
   lds_chain<<<1, 256>>>(d, n, c);
   cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
   printf("dependent LDS+DADD fold (unroll 8): %.2f cycles/element\n", double(h) / n);
+  leaf_chain_smem<<<1, 256>>>(d, c);
+  cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("leaf chain (4 lanes, smem rows, 16-deep prefetch): %.2f cycles/add\n", double(h) / 1023);
+  leaf_chain_regs<<<1, 32>>>(d, c);
+  cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("leaf chain (8 lanes, register operands): %.2f cycles/add\n", double(h) / 1024);
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, grid_barriers, 256, 0);
