@@ -841,16 +841,24 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ hist, uint64_t Hs, int ring,
                 const uint32_t* __restrict__ unconv, int map_max, int fixed, double* params,
                 double* partials, double* em_out, uint32_t* done, EmEpilogueArgs ep,
-                int merged, const double* __restrict__ hood_parts) {
+                int merged, const double* __restrict__ hood_parts, uint32_t leaf_lo,
+                uint32_t leaf_hi, int tail_mode) {
+  // tail_mode 0: fold [leaf_lo, leaf_hi) of every series, the last block
+  //              (ticket) runs the trees and the parameter update;
+  //           1: fold this rank's [leaf_lo, leaf_hi) of the label series only,
+  //              no trees (partitioned run: the partials are allgathered);
+  //           2: one block, trees only, over allgathered label partials and
+  //              the hood-series partials in hood_parts.
   extern __shared__ double stage[];  // kLeavesPerBlock x kLeafStride
   pdl_wait();
   const uint32_t* n = layout;
   const uint32_t* label_start = layout + M;
   const uint32_t* leaf_start = layout + 2 * M + 1;
   const uint32_t nseries = kSq ? M : M + 1;
-  const uint32_t total = leaf_start[nseries];  // (issued beside the skip flag's load)
+  const uint32_t all_end = leaf_start[tail_mode == 1 ? M : nseries];  // (beside the skip flag)
   if (em_skipped(unconv)) return;  // uniform: no block takes a ticket
-  const uint32_t first = blockIdx.x * kLeavesPerBlock;
+  const uint32_t total = tail_mode == 2 ? 0u : min(all_end, leaf_hi);
+  const uint32_t first = leaf_lo + blockIdx.x * kLeavesPerBlock;
   if (first < total) {
     const double* hood_row = nullptr;
     if (!kSq && unconv && !hood_parts) {
@@ -981,13 +989,20 @@ __global__ void __launch_bounds__(256)
     }
   }
   // ---- last block: trees + epilogue ----
+  if (tail_mode == 1) return;
   __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
+  if (tail_mode == 0) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+  } else if (!kSq && hood_parts) {  // trees only: place the hood-series partials
+    const uint32_t h0 = leaf_start[M], nh = leaf_start[M + 1] - h0;
+    for (uint32_t i = threadIdx.x; i < nh; i += blockDim.x) partials[h0 + i] = hood_parts[i];
+    __syncthreads();
+  }
   __shared__ EmPrefetch pf;
   if (kSq && merged && threadIdx.x == 0) em_prefetch(ep, &pf);
   constexpr uint32_t kStageDoubles = kLeavesPerBlock * kLeafStride;
@@ -1039,7 +1054,7 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     if (kSq && merged && threadIdx.x < 32) em_record(ep, true, &pf);
-    if (threadIdx.x == 0) *done = 0;  // re-arm the ticket for the next launch
+    if (threadIdx.x == 0 && tail_mode == 0) *done = 0;  // re-arm the ticket for the next launch
     return;
   }
   for (uint32_t s = 0; s < nseries; ++s) {
@@ -1128,7 +1143,7 @@ __global__ void __launch_bounds__(256)
     __syncwarp();
     em_record(ep, true, &pf);
   }
-  if (threadIdx.x == 0) *done = 0;  // re-arm the ticket for the next launch
+  if (threadIdx.x == 0 && tail_mode == 0) *done = 0;  // re-arm the ticket for the next launch
 }
 
 
@@ -1799,7 +1814,8 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
                 const uint8_t* lab_odd, const uint32_t* unconv, int map_max, int fixed,
                 const double* hist, uint64_t Hs, int ring, double* params, double* em_out,
                 MStepBuffers& mb, cudaStream_t s, uint64_t* launches, bool counts_ready,
-                bool scattered, const EmEpilogueArgs* ep, const double* hood_parts) {
+                bool scattered, const EmEpilogueArgs* ep, const double* hood_parts,
+                bool scatter_only = false) {
   mstep_reserve(mb, R, M, Hs);
   const uint32_t tiles = static_cast<uint32_t>((uint64_t(R) + kTileVerts - 1) / kTileVerts);
   uint32_t* counts = mb.counts.get();
@@ -1852,14 +1868,16 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
   ensure_dynamic_smem(k_leaf_fold<true>, leaf_smem);
   const unsigned lg = grid_for(max_leaves, kLeavesPerBlock);
   const EmEpilogueArgs epv = ep ? *ep : EmEpilogueArgs{};
-  launch_pdl(k_leaf_fold<false>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
-             (const uint32_t*)layout, M, hist, Hs, ring, unconv, map_max, fixed, params, partials,
-             em_out, mb.done.get(), epv, 0, hood_parts);
-  launch_pdl(k_leaf_fold<true>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
-             (const uint32_t*)layout, M, (const double*)nullptr, uint64_t(0), 1, unconv, map_max,
-             fixed, params, partials, em_out, mb.done.get() + 1, epv, ep ? 1 : 0,
-             (const double*)nullptr);
-  n += 2;
+  if (!scatter_only) {
+    launch_pdl(k_leaf_fold<false>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
+               (const uint32_t*)layout, M, hist, Hs, ring, unconv, map_max, fixed, params,
+               partials, em_out, mb.done.get(), epv, 0, hood_parts, 0u, ~0u, 0);
+    launch_pdl(k_leaf_fold<true>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
+               (const uint32_t*)layout, M, (const double*)nullptr, uint64_t(0), 1, unconv,
+               map_max, fixed, params, partials, em_out, mb.done.get() + 1, epv, ep ? 1 : 0,
+               (const double*)nullptr, 0u, ~0u, 0);
+    n += 2;
+  }
   if (launches) *launches += n;
 }
 
@@ -1876,6 +1894,60 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
                   bool scattered, const EmEpilogueArgs* ep, const double* hood_parts) {
   mstep_core(mean, R, M, lab_even, lab_odd, unconv, map_max, fixed, hist, Hs, ring, params,
              em_out, mb, s, launches, counts_ready, scattered, ep, hood_parts);
+}
+
+// Partitioned M-step, distributed folds (see partition.cu): the grouping on
+// every rank, then per pass this rank's label-series leaves [lo, hi) (no
+// trees), and -- after the partials are allgathered -- the trees in one block.
+void launch_mstep_scatter(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab,
+                          const uint32_t* unconv, int map_max, int fixed, uint64_t Hs,
+                          double* params, double* em_out, MStepBuffers& mb, cudaStream_t s,
+                          uint64_t* launches) {
+  mstep_core(mean, R, M, lab, lab, unconv, map_max, fixed, nullptr, Hs, 1, params, em_out, mb, s,
+             launches, /*counts_ready=*/false, /*scattered=*/false, nullptr, nullptr,
+             /*scatter_only=*/true);
+}
+
+void launch_leaf_range(bool sq, uint32_t M, uint64_t Hs, const uint32_t* unconv, int map_max,
+                       int fixed, double* params, double* em_out, MStepBuffers& mb, uint32_t lo,
+                       uint32_t hi, cudaStream_t s) {
+  if (hi <= lo) return;
+  const size_t leaf_smem = size_t(8) * 1056 * sizeof(double);
+  const dim3 g(grid_for(hi - lo, kLeavesPerBlock));
+  const EmEpilogueArgs epv{};
+  if (sq) {
+    ensure_dynamic_smem(k_leaf_fold<true>, leaf_smem);
+    launch_pdl(k_leaf_fold<true>, g, dim3(256), leaf_smem, s, (const double*)mb.x.get(),
+               (const uint32_t*)mb.layout.get(), M, (const double*)nullptr, Hs, 1, unconv,
+               map_max, fixed, params, mb.partials.get(), em_out, mb.done.get() + 1, epv, 0,
+               (const double*)nullptr, lo, hi, 1);
+  } else {
+    ensure_dynamic_smem(k_leaf_fold<false>, leaf_smem);
+    launch_pdl(k_leaf_fold<false>, g, dim3(256), leaf_smem, s, (const double*)mb.x.get(),
+               (const uint32_t*)mb.layout.get(), M, (const double*)nullptr, Hs, 1, unconv,
+               map_max, fixed, params, mb.partials.get(), em_out, mb.done.get(), epv, 0,
+               (const double*)nullptr, lo, hi, 1);
+  }
+}
+
+void launch_fold_trees(bool sq, uint32_t M, uint64_t Hs, const uint32_t* unconv, int map_max,
+                       int fixed, double* params, double* em_out, MStepBuffers& mb,
+                       const double* hood_parts, cudaStream_t s) {
+  const size_t leaf_smem = size_t(8) * 1056 * sizeof(double);
+  const EmEpilogueArgs epv{};
+  if (sq) {
+    ensure_dynamic_smem(k_leaf_fold<true>, leaf_smem);
+    launch_pdl(k_leaf_fold<true>, dim3(1), dim3(256), leaf_smem, s, (const double*)mb.x.get(),
+               (const uint32_t*)mb.layout.get(), M, (const double*)nullptr, Hs, 1, unconv,
+               map_max, fixed, params, mb.partials.get(), em_out, mb.done.get() + 1, epv, 0,
+               (const double*)nullptr, 0u, 0u, 2);
+  } else {
+    ensure_dynamic_smem(k_leaf_fold<false>, leaf_smem);
+    launch_pdl(k_leaf_fold<false>, dim3(1), dim3(256), leaf_smem, s, (const double*)mb.x.get(),
+               (const uint32_t*)mb.layout.get(), M, (const double*)nullptr, Hs, 1, unconv,
+               map_max, fixed, params, mb.partials.get(), em_out, mb.done.get(), epv, 0,
+               hood_parts, 0u, 0u, 2);
+  }
 }
 
 void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s) {

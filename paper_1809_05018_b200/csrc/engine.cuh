@@ -125,6 +125,19 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches,
                   bool counts_ready = true, bool scattered = false,
                   const EmEpilogueArgs* ep = nullptr, const double* hood_parts = nullptr);
+// Partitioned optimize, distributed M-step folds: the label grouping (every
+// rank), this rank's label-series leaves [lo, hi) of one pass (no trees), the
+// trees in one block over allgathered partials (+ hood-series partials).
+void launch_mstep_scatter(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab,
+                          const uint32_t* unconv, int map_max, int fixed, uint64_t Hs,
+                          double* params, double* em_out, MStepBuffers& mb, cudaStream_t s,
+                          uint64_t* launches);
+void launch_leaf_range(bool sq, uint32_t M, uint64_t Hs, const uint32_t* unconv, int map_max,
+                       int fixed, double* params, double* em_out, MStepBuffers& mb, uint32_t lo,
+                       uint32_t hi, cudaStream_t s);
+void launch_fold_trees(bool sq, uint32_t M, uint64_t Hs, const uint32_t* unconv, int map_max,
+                       int fixed, double* params, double* em_out, MStepBuffers& mb,
+                       const double* hood_parts, cudaStream_t s);
 // Partitioned optimize: fold this rank's leaves [hb/1024, ceil(he/1024)) of
 // the last executed hood-energy row into out (hood_parts of launch_mstep).
 void launch_row_leaves(const double* hist, int ring, uint64_t Hs, const uint32_t* unconv,

@@ -399,6 +399,26 @@ void allgather(dpmrf_group* g, cudaStream_t st) {
   NK(nccl.GroupEnd());
 }
 
+// The M-step's label-series leaf partials of every rank (equal chunks of
+// chunk_l leaves, in place in each rank's partials array).
+void allgather_partials(dpmrf_group* g, uint64_t chunk_l, cudaStream_t st) {
+  const int W = g->world;
+  if (W == 1) return;
+  if (g->local()) {
+    for (int s = 0; s < W; ++s)
+      for (int d = 0; d < W; ++d) {
+        if (s == d) continue;
+        CK(cudaMemcpyAsync(g->parts[d]->ms.partials.get() + s * chunk_l,
+                           g->parts[s]->ms.partials.get() + s * chunk_l, 8 * chunk_l,
+                           cudaMemcpyDeviceToDevice, st));
+      }
+    return;
+  }
+  Nccl& nccl = Nccl::get();
+  double* buf = g->parts[0]->ms.partials.get();
+  NK(nccl.AllGather(buf + g->rank * chunk_l, buf, chunk_l, ncclFloat64, g->comm, st));
+}
+
 bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dpmrf_run_options& o,
                      bool device_loop, uint32_t* labels_out, double* mu_out, double* sigma_out) {
   dpmrf_context* ctx = g->ctx;
@@ -427,6 +447,8 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
   const uint64_t padV = uint64_t(g->chunkV) * W, padH = g->chunkH * W;
   const uint64_t rec_stride = 3 + 3 * uint64_t(M);
   const int ring = L + 1;
+  // label-series leaves per rank in the distributed folds (upper bound R/1024 + M)
+  const uint64_t chunk_l = ((uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M + W - 1) / W;
   const bool packed = !(o.flags & DPMRF_RUN_CSR);
   for (auto& pp : g->parts) {
     Part& p = *pp;
@@ -474,6 +496,9 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
     p.em_rec.ensure(uint64_t(em_max ? em_max : 1) * rec_stride);
     p.em_hist.ensure(uint64_t(em_max ? em_max : 1));
     mstep_reserve(p.ms, R, M, Hs);
+    p.ms.partials.ensure(std::max<uint64_t>(uint64_t(W) * chunk_l + (Hs + kFoldLeaf - 1) / kFoldLeaf + 1,
+                                            (uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M +
+                                                (Hs + kFoldLeaf - 1) / kFoldLeaf + 1));
     EmEpilogueArgs& ep = p.ep;
     ep = EmEpilogueArgs{};
     ep.unconv = a.unconv;
@@ -549,11 +574,31 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
       allgather(g, st);
       for (auto& pp : g->parts) {
         Part& p = *pp;
-        // one row of hood energies (ring 1) and one label buffer: the same
-        // M-step + total energy as the one-device run
-        launch_mstep(p.a.mean, R, M, p.lab_full.get(), p.lab_full.get(), nullptr, Hs, 1,
-                     p.a.unconv, map_max, fixed, p.params.get(), p.em_out.get(), p.ms, st, &k,
-                     /*counts_ready=*/false, /*scattered=*/false, nullptr, p.hpart.get());
+        // the grouping by label on every rank (all labels are gathered)
+        launch_mstep_scatter(p.a.mean, R, M, p.lab_full.get(), p.a.unconv, map_max, fixed, Hs,
+                             p.params.get(), p.em_out.get(), p.ms, st, &k);
+      }
+      // Distributed folds: each rank folds its chunk of the label-series
+      // leaves, the partials are allgathered, every rank runs the trees (the
+      // same bits everywhere) -- per pass, sum then (x - mu)^2.
+      for (int pass = 0; pass < 2; ++pass) {
+        for (auto& pp : g->parts) {
+          Part& p = *pp;
+          const uint32_t lo = uint32_t(uint64_t(p.r) * chunk_l);
+          launch_leaf_range(pass == 1, M, Hs, p.a.unconv, map_max, fixed, p.params.get(),
+                            p.em_out.get(), p.ms, lo, uint32_t(lo + chunk_l), st);
+          ++k;
+        }
+        allgather_partials(g, chunk_l, st);
+        for (auto& pp : g->parts) {
+          Part& p = *pp;
+          launch_fold_trees(pass == 1, M, Hs, p.a.unconv, map_max, fixed, p.params.get(),
+                            p.em_out.get(), p.ms, p.hpart.get(), st);
+          ++k;
+        }
+      }
+      for (auto& pp : g->parts) {
+        Part& p = *pp;
         if (device_loop) {
           launch_em_epilogue(p.ep, st);
           ++k;
