@@ -8,7 +8,8 @@ windows of parallel.halo_windows with isend/irecv, sums the unconverged-hood
 counters with all_reduce and allgathers the committed labels and the leaf
 partials of the last hood-energy row (each rank folds its own 1024-element
 leaves) per EM iteration; the M-step and EM total are the C oracle's
-(update_parameters, engine.cpp:193-223; dpp::reduce, kernels.hpp:124-139).
+(update_parameters, engine.cpp:193-223, with its folds distributed over the
+ranks as in partition.cu; dpp::reduce, kernels.hpp:124-139).
 The result must equal the oracle's one-process optimize bit for bit, which
 checks the partition plan and the exchange schedule independently of CUDA.
 """
@@ -20,6 +21,48 @@ import torch.distributed as dist
 
 from oracle import C
 from paper_1809_05018_b200.parallel import halo_windows
+
+
+def _distributed_update(orc, mean, labels, mu, sigma, world, rank):
+    """update_parameters (engine.cpp:193-223) with the folds distributed as in
+    partition.cu: stable grouping by label on every rank, each rank folds an
+    equal chunk of the label-series leaves (fold_leaf), the partials are
+    allgathered, every rank runs fold_tree per label -- sum pass, then the
+    (x - mu)^2 pass."""
+    M = len(mu)
+    R = len(mean)
+    order = np.argsort(labels, kind="stable")
+    counts = np.bincount(labels, minlength=M)
+    starts = np.concatenate([[0], np.cumsum(counts)])
+    x = mean[order]
+    leaves_of = [(int(n) + 1023) // 1024 for n in counts]
+    leaf_start = np.concatenate([[0], np.cumsum(leaves_of)]).astype(np.int64)
+    chunk = ((R + 1023) // 1024 + M + world - 1) // world
+    mu, sigma = mu.copy(), sigma.copy()
+    for sq in (False, True):
+        own = np.zeros(chunk)
+        for k in range(chunk):
+            leaf = rank * chunk + k
+            if leaf >= leaf_start[M]:
+                break
+            lbl = int(np.searchsorted(leaf_start, leaf, side="right") - 1)
+            b = starts[lbl] + (leaf - leaf_start[lbl]) * 1024
+            e = min(b + 1024, starts[lbl + 1])
+            seg = x[b:e]
+            if sq:
+                d = seg - mu[lbl]
+                seg = d * d
+            own[k] = orc.fold_range(seg)
+        parts = _allgather(own, chunk, world)
+        for lbl in range(M):
+            if counts[lbl] == 0:
+                continue  # empty labels keep their parameters (engine.cpp:209-211)
+            folded = orc.fold_tree(parts[leaf_start[lbl]:leaf_start[lbl + 1]])
+            if not sq:
+                mu[lbl] = folded / float(counts[lbl])
+            else:
+                sigma[lbl] = max(np.sqrt(folded / float(counts[lbl])), 1e-3)
+    return mu, sigma
 
 
 def _exchange(arr, win, me, world):
@@ -136,7 +179,7 @@ def optimize_rank(graph, hoods, cfg, fixed_work=False):
             own_parts[i] = orc.fold_range(row_own[i * 1024:(i + 1) * 1024])
         parts = _allgather(own_parts, chunk_l, world)[:(Hs + 1023) // 1024]
         lab[cur][:] = full_lab  # (every rank now holds all committed labels)
-        mu, sigma = orc.update_parameters(mean, full_lab.astype(np.uint32), mu, sigma)
+        mu, sigma = _distributed_update(orc, mean, full_lab, mu, sigma, world, rank)
         total = orc.fold_tree(parts) if len(parts) else 0.0
         totals.append(total)
         em_T.append(T)
