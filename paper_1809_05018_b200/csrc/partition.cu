@@ -182,6 +182,9 @@ struct Part {
   int r = 0;
   uint32_t vb = 0, ve = 0;
   uint64_t hb = 0, he = 0;
+  // [ia, ib) of the owned series: hoods whose members are all owned (their
+  // hood pass runs while the halo exchange is in flight)
+  uint64_t ia = 0, ib = 0;
   DevBuf<uint8_t> lab[2], lab_full;
   // hpart: the hood-energy series' leaf partials of every rank (W x chunkH/1024)
   DevBuf<double> minE, hist, hpart, params, em_out, terms, em_rec, em_hist;
@@ -213,6 +216,13 @@ struct dpmrf_group {
   uint64_t chunkH = 0;
   std::vector<Window> lab_win, min_win;  // [s * W + d]
   uint64_t halo_bytes = 0, gather_bytes = 0;
+  // halo exchange on its own stream, overlapping the interior hood pass
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_v = nullptr, ev_x = nullptr;
+  // split hood pass (interior during the exchange, boundary after): NCCL
+  // groups; local groups only with DPMRF_GROUP_SPLIT=1 (one device gains
+  // nothing from the overlap and pays two more launches per iteration)
+  bool split = true;
   // CUDA graph of one EM iteration (device loop; local groups)
   bool use_graph = true;
   std::vector<uint64_t> graph_key;
@@ -247,6 +257,26 @@ dpmrf_status guarded(F&& f) {
 
 void need(bool c, dpmrf_status s, const char* m) {
   if (!c) fail(s, m);
+}
+
+// The owned series whose members all lie in the owned vertex range form an
+// interior range [ia, ib): every boundary hood below mid moves ia past it,
+// every boundary hood at or above mid moves ib below it (exact for any
+// partition shape; row bands give thin boundary strips at both ends).
+__global__ void k_interior(const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ h_mem,
+                           uint32_t hb, uint32_t he, uint32_t vb, uint32_t ve, uint32_t* out) {
+  const uint32_t mid = hb + (he - hb) / 2;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t h = hb + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; h < he; h += stride) {
+    bool boundary = false;
+    for (uint32_t j = s_off[h]; j < s_off[h + 1] && !boundary; ++j) {
+      const uint32_t m = h_mem[j];
+      boundary = m < vb || m >= ve;
+    }
+    if (!boundary) continue;
+    if (h < mid) atomicMax(&out[0], uint32_t(h) + 1);
+    else atomicMin(&out[1], uint32_t(h));
+  }
 }
 
 // Ranges + halo windows for the context's current structure.
@@ -308,6 +338,30 @@ void plan(dpmrf_group* g) {
   g->gather_bytes = g->local()
                         ? uint64_t(W) * (W - 1) * (g->chunkV + 8 * (g->chunkH / kFoldLeaf))
                         : uint64_t(W - 1) * (g->chunkV + 8 * (g->chunkH / kFoldLeaf));
+  // interior series ranges (one small D2H per partition, planning time only)
+  {
+    uint32_t* io = ctx->tmp_u32[4].ensure(2 * W);
+    std::vector<uint32_t> init(2 * W);
+    for (auto& pp : g->parts) {
+      init[2 * pp->r] = uint32_t(pp->hb);
+      init[2 * pp->r + 1] = uint32_t(pp->he);
+    }
+    CK(cudaMemcpyAsync(io, init.data(), init.size() * 4, cudaMemcpyHostToDevice, st));
+    for (auto& pp : g->parts) {
+      if (pp->he > pp->hb)
+        k_interior<<<std::min<unsigned>(grid_for(pp->he - pp->hb, 256), 8 * kNumSMs), 256, 0, st>>>(
+            s_off, ctx->h_mem.get(), uint32_t(pp->hb), uint32_t(pp->he), pp->vb, pp->ve,
+            io + 2 * pp->r);
+      CK_LAUNCH();
+    }
+    std::vector<uint32_t> res(2 * W);
+    CK(cudaMemcpyAsync(res.data(), io, res.size() * 4, cudaMemcpyDeviceToHost, st));
+    ctx->sync();
+    for (auto& pp : g->parts) {
+      pp->ia = res[2 * pp->r];
+      pp->ib = std::max<uint64_t>(res[2 * pp->r + 1], pp->ia);
+    }
+  }
   g->planned = true;
   g->plan_gen = ctx->generation;
   g->drop_graph();
@@ -552,10 +606,45 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
           launch_vertex_argmin(pp->a, pp->lab[bin].get(), pp->lab[bout].get(), t, st);
           ++k;
         }
-        exchange_halo(g, bout, st);
+        if (W > 1 && !g->split) {
+          exchange_halo(g, bout, st);
+          for (auto& pp : g->parts) {
+            launch_hood_sums(pp->a, t, st);
+            ++k;
+          }
+        } else {
+        if (W > 1) {
+          // exchange on the side stream; interior hoods meanwhile, boundary
+          // hoods once the halos have landed
+          CK(cudaEventRecord(g->ev_v, st));
+          CK(cudaStreamWaitEvent(g->cs, g->ev_v, 0));
+          exchange_halo(g, bout, g->cs);
+          CK(cudaEventRecord(g->ev_x, g->cs));
+        }
         for (auto& pp : g->parts) {
-          launch_hood_sums(pp->a, t, st);
-          ++k;
+          if (pp->ib > pp->ia) {
+            MapArgs ai = pp->a;
+            ai.h_begin = pp->ia;
+            ai.h_end = pp->ib;
+            launch_hood_sums(ai, t, st);
+            ++k;
+          }
+        }
+        if (W > 1) CK(cudaStreamWaitEvent(st, g->ev_x, 0));
+        for (auto& pp : g->parts) {
+          if (pp->ia > pp->hb) {
+            MapArgs lo = pp->a;
+            lo.h_end = pp->ia;
+            launch_hood_sums(lo, t, st);
+            ++k;
+          }
+          if (pp->he > pp->ib) {
+            MapArgs hi = pp->a;
+            hi.h_begin = pp->ib;
+            launch_hood_sums(hi, t, st);
+            ++k;
+          }
+        }
         }
         // The summed counter decides the MAP early exit (optimize.cpp:59);
         // fixed-work runs never read it (executed_iters == map_max), so they
@@ -772,6 +861,14 @@ extern "C" dpmrf_status dpmrf_nccl_unique_id(uint8_t id[128]) {
   });
 }
 
+namespace {
+void init_side_stream(dpmrf_group* g) {
+  CK(cudaStreamCreateWithFlags(&g->cs, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&g->ev_v, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&g->ev_x, cudaEventDisableTiming));
+}
+}  // namespace
+
 extern "C" dpmrf_status dpmrf_group_create_nccl(dpmrf_context* ctx, const uint8_t id[128],
                                                 int rank, int world, dpmrf_group** out) {
   return guarded([&] {
@@ -792,6 +889,7 @@ extern "C" dpmrf_status dpmrf_group_create_nccl(dpmrf_context* ctx, const uint8_
     auto p = std::make_unique<Part>();
     p->r = rank;
     g->parts.push_back(std::move(p));
+    init_side_stream(g.get());
     *out = g.release();
   });
 }
@@ -807,11 +905,14 @@ extern "C" dpmrf_status dpmrf_group_create_local(dpmrf_context* ctx, int world,
     g->world = world;
     g->rank = -1;
     if (const char* e = std::getenv("DPMRF_NO_GRAPH")) g->use_graph = e[0] == '0';
+    const char* sp = std::getenv("DPMRF_GROUP_SPLIT");
+    g->split = sp && sp[0] == '1';
     for (int r = 0; r < world; ++r) {
       auto p = std::make_unique<Part>();
       p->r = r;
       g->parts.push_back(std::move(p));
     }
+    init_side_stream(g.get());
     *out = g.release();
   });
 }
@@ -821,6 +922,12 @@ extern "C" void dpmrf_group_destroy(dpmrf_group* g) {
   cudaSetDevice(g->ctx->device);
   cudaStreamSynchronize(g->ctx->stream);
   g->drop_graph();
+  if (g->cs) {
+    cudaStreamSynchronize(g->cs);
+    cudaStreamDestroy(g->cs);
+  }
+  if (g->ev_v) cudaEventDestroy(g->ev_v);
+  if (g->ev_x) cudaEventDestroy(g->ev_x);
   if (g->comm) {
     Nccl& nccl = Nccl::get();
     nccl.CommDestroy(g->comm);

@@ -124,3 +124,22 @@ def test_nccl_single_rank_group(ctx):
     g = E.PartitionGroup.nccl(ctx, uid, 0, 1)
     _same(g.optimize(cfg), want)
     g.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_local_group_split_hood_pass(ctx, world, monkeypatch):
+    """DPMRF_GROUP_SPLIT=1: the schedule of NCCL groups -- halo exchange on a
+    side stream while the interior hoods are folded, boundary hoods after --
+    on the local transport; results equal the one-device run bit for bit."""
+    _load(ctx, 1024, 8, seed=13)
+    cfg = E.OptimizerConfig(em_max_iters=6, rng_seed=13)
+    for fixed in (False, True):
+        want = ctx.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_EM)
+        monkeypatch.setenv("DPMRF_GROUP_SPLIT", "1")
+        g = E.PartitionGroup.local(ctx, world)
+        monkeypatch.delenv("DPMRF_GROUP_SPLIT")
+        try:
+            got = g.optimize(cfg, fixed_work=fixed)
+        finally:
+            g.close()
+        _same(got, want)
