@@ -250,6 +250,7 @@ void upload_hoods(dpmrf_context* ctx, uint64_t H, const uint32_t* offsets,
 extern "C" dpmrf_status dpmrf_set_graph(dpmrf_context* ctx, uint32_t R, const uint32_t* offsets,
                                         const uint32_t* neighbors, const double* region_mean) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null argument");
     ctx->bind();
     upload_graph(ctx, R, offsets, neighbors, region_mean);
@@ -260,6 +261,7 @@ extern "C" dpmrf_status dpmrf_set_graph(dpmrf_context* ctx, uint32_t R, const ui
 extern "C" dpmrf_status dpmrf_set_hoods(dpmrf_context* ctx, uint64_t H, const uint32_t* offsets,
                                         const uint32_t* members) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null argument");
     ctx->bind();
     upload_hoods(ctx, H, offsets, members);
@@ -271,6 +273,7 @@ extern "C" dpmrf_status dpmrf_build_neighborhoods(dpmrf_context* ctx, uint64_t C
                                                   const uint32_t* c_off, const uint32_t* c_mem,
                                                   uint32_t k, uint64_t* num_slots) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && c_off, DPMRF_INVALID_ARGUMENT, "null argument");
     if (k != 1) fail(DPMRF_INPUT_ERROR, "only 1-neighborhoods are supported");
     need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
@@ -287,6 +290,7 @@ extern "C" dpmrf_status dpmrf_get_hoods(dpmrf_context* ctx, uint64_t* H, uint64_
                                         uint32_t* offsets, uint32_t* members,
                                         uint32_t* source_clique) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && ctx->has_hoods, DPMRF_INVALID_ARGUMENT, "no neighborhoods");
     ctx->bind();
     if (H) *H = ctx->H;
@@ -308,6 +312,7 @@ extern "C" dpmrf_status dpmrf_build_region_graph(dpmrf_context* ctx, uint32_t w,
                                                  const uint8_t* pixels, const uint32_t* region,
                                                  uint32_t R, uint64_t* num_adjacency) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx, DPMRF_INVALID_ARGUMENT, "null argument");
     const uint64_t n = uint64_t(w) * h;
     need(n == 0 || (pixels && region), DPMRF_INVALID_ARGUMENT, "null image or label map");
@@ -336,6 +341,7 @@ extern "C" dpmrf_status dpmrf_build_region_graph_device(dpmrf_context* ctx, uint
                                                         const uint32_t* region, uint32_t R,
                                                         uint64_t* num_adjacency) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx, DPMRF_INVALID_ARGUMENT, "null argument");
     need(uint64_t(w) * h == 0 || (pixels && region), DPMRF_INVALID_ARGUMENT,
          "null image or label map");
@@ -353,6 +359,7 @@ extern "C" dpmrf_status dpmrf_build_region_graph_device(dpmrf_context* ctx, uint
 extern "C" dpmrf_status dpmrf_make_phantom(dpmrf_context* ctx, const dpmrf_phantom_spec* spec,
                                            uint8_t* truth, uint8_t* image, uint32_t* host_ties) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && spec, DPMRF_INVALID_ARGUMENT, "null argument");
     ctx->bind();
     ctx->has_image = ctx->has_regions = false;
@@ -369,6 +376,7 @@ extern "C" dpmrf_status dpmrf_make_phantom(dpmrf_context* ctx, const dpmrf_phant
 extern "C" dpmrf_status dpmrf_oversegment(dpmrf_context* ctx, uint32_t block, int32_t brick,
                                           uint32_t* num_regions, uint32_t* region) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null argument");
     need(ctx->has_image, DPMRF_INVALID_ARGUMENT, "no resident image (dpmrf_make_phantom)");
     ctx->bind();
@@ -385,6 +393,7 @@ extern "C" dpmrf_status dpmrf_oversegment(dpmrf_context* ctx, uint32_t block, in
 extern "C" dpmrf_status dpmrf_build_region_graph_resident(dpmrf_context* ctx,
                                                           uint64_t* num_adjacency) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null argument");
     need(ctx->has_image && ctx->has_regions, DPMRF_INVALID_ARGUMENT,
          "no resident image / region map");
@@ -403,6 +412,7 @@ extern "C" dpmrf_status dpmrf_get_graph(dpmrf_context* ctx, uint32_t* R, uint64_
                                         uint32_t* offsets, uint32_t* neighbors, double* mean,
                                         uint32_t* size) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph");
     need(!size || ctx->has_sizes, DPMRF_INVALID_ARGUMENT,
          "region sizes exist only for a graph built by dpmrf_build_region_graph");
@@ -426,6 +436,7 @@ extern "C" dpmrf_status dpmrf_get_graph(dpmrf_context* ctx, uint32_t* R, uint64_
 extern "C" dpmrf_status dpmrf_enumerate_maximal_cliques(dpmrf_context* ctx, uint64_t* C,
                                                         uint64_t* CS) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph");
     ctx->bind();
     ctx->has_cliques = false;
@@ -439,6 +450,7 @@ extern "C" dpmrf_status dpmrf_enumerate_maximal_cliques(dpmrf_context* ctx, uint
 extern "C" dpmrf_status dpmrf_get_cliques(dpmrf_context* ctx, uint32_t* offsets,
                                           uint32_t* members) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && ctx->has_cliques, DPMRF_INVALID_ARGUMENT, "no cliques enumerated");
     ctx->bind();
     if (offsets)
@@ -454,6 +466,7 @@ extern "C" dpmrf_status dpmrf_get_cliques(dpmrf_context* ctx, uint32_t* offsets,
 extern "C" dpmrf_status dpmrf_build_neighborhoods_resident(dpmrf_context* ctx, uint32_t k,
                                                            uint64_t* num_slots) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx, DPMRF_INVALID_ARGUMENT, "null argument");
     if (k != 1) fail(DPMRF_INPUT_ERROR, "only 1-neighborhoods are supported");
     need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
@@ -913,6 +926,7 @@ extern "C" dpmrf_status dpmrf_optimize(dpmrf_context* ctx, const dpmrf_optimizer
                                        const dpmrf_run_options* opts, uint32_t* labels_out,
                                        double* mu_out, double* sigma_out) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && cfg, DPMRF_INVALID_ARGUMENT, "null argument");
     optimize_resident(ctx, cfg, opts, labels_out, mu_out, sigma_out);
   });
@@ -924,6 +938,7 @@ extern "C" dpmrf_status dpmrf_optimize_arrays(
     const dpmrf_optimizer_config* cfg, const dpmrf_run_options* opts, uint32_t* labels_out,
     double* mu_out, double* sigma_out) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && cfg, DPMRF_INVALID_ARGUMENT, "null argument");
     ctx->bind();
     upload_graph(ctx, R, g_offsets, g_neighbors, region_mean);
@@ -961,6 +976,7 @@ void optimize_resident(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
 
 extern "C" dpmrf_status dpmrf_trace_info(dpmrf_context* ctx, int32_t* em_iters, uint64_t* series) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null context");
     if (em_iters) *em_iters = static_cast<int32_t>(ctx->trace.size());
     if (series) *series = ctx->stats.series;
@@ -971,6 +987,7 @@ extern "C" dpmrf_status dpmrf_trace_em(dpmrf_context* ctx, int32_t em, int32_t* 
                                        double* total, uint8_t* converged, double* mu,
                                        double* sigma) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && em >= 0 && size_t(em) < ctx->trace.size(), DPMRF_OUT_OF_RANGE,
          "no such EM iteration in the trace");
     const auto& r = ctx->trace[em];
@@ -985,6 +1002,7 @@ extern "C" dpmrf_status dpmrf_trace_em(dpmrf_context* ctx, int32_t em, int32_t* 
 extern "C" dpmrf_status dpmrf_trace_map(dpmrf_context* ctx, int32_t em, int32_t it,
                                         double* hood_energy, uint8_t* converged) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && em >= 0 && size_t(em) < ctx->trace.size(), DPMRF_OUT_OF_RANGE,
          "no such EM iteration in the trace");
     const auto& r = ctx->trace[em];
@@ -998,6 +1016,7 @@ extern "C" dpmrf_status dpmrf_trace_map(dpmrf_context* ctx, int32_t em, int32_t 
 
 extern "C" dpmrf_status dpmrf_get_stats(dpmrf_context* ctx, dpmrf_run_stats* out) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && out, DPMRF_INVALID_ARGUMENT, "null argument");
     *out = ctx->stats;
   });
@@ -1006,6 +1025,7 @@ extern "C" dpmrf_status dpmrf_get_stats(dpmrf_context* ctx, dpmrf_run_stats* out
 extern "C" dpmrf_status dpmrf_debug_log(dpmrf_context* ctx, uint64_t n, const double* x,
                                         double* out) {
   return guarded([&] {
+    ContextLock lock_(ctx);
     need(ctx && (n == 0 || (x && out)), DPMRF_INVALID_ARGUMENT, "null argument");
     ctx->bind();
     double* d = ctx->tmp_f64[0].ensure(2 * n);

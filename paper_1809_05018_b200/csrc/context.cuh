@@ -2,6 +2,7 @@
 #pragma once
 
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -161,6 +162,12 @@ struct dpmrf_context {
 
   void sync() { CK(cudaStreamSynchronize(stream)); }
   void bind() { CK(cudaSetDevice(device)); }
+
+  // Every C-ABI entry point holds this for its whole call: calls on one
+  // context from several host threads serialize (the reference's pool
+  // serializes concurrent submissions, proj/src/dpp/backend.cpp:45); the
+  // lock is recursive because entry points call each other.
+  std::recursive_mutex mu;
   void prepare();  // validate + cover + series offsets + packed layouts (capi.cu)
 
   // ---- packed static structure (engine.cuh MapArgs::adj_k / hood_k) ----
@@ -170,6 +177,19 @@ struct dpmrf_context {
   dpmrf_b200::DevBuf<uint32_t> hood_base;
   dpmrf_b200::DevBuf<uint16_t> hood_pk;
 };
+
+namespace dpmrf_b200 {
+// Entry-point guard: a null context is DPMRF_INVALID_ARGUMENT, otherwise the
+// context's mutex is held until the call returns.
+struct ContextLock {
+  std::unique_lock<std::recursive_mutex> lk;
+  explicit ContextLock(dpmrf_context* c) {
+    if (c == nullptr) fail(DPMRF_INVALID_ARGUMENT, "null context");
+    lk = std::unique_lock<std::recursive_mutex>(c->mu);
+  }
+};
+}  // namespace dpmrf_b200
+
 
 namespace dpmrf_b200 {
 // capi.cu

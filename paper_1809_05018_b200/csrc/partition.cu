@@ -873,6 +873,7 @@ extern "C" dpmrf_status dpmrf_group_create_nccl(dpmrf_context* ctx, const uint8_
                                                 int rank, int world, dpmrf_group** out) {
   return guarded([&] {
     need(ctx && id && out, DPMRF_INVALID_ARGUMENT, "null argument");
+    ContextLock lock_(ctx);
     need(world >= 1 && world <= kMaxParts, DPMRF_INVALID_ARGUMENT, "world must be in [1, 64]");
     need(rank >= 0 && rank < world, DPMRF_INVALID_ARGUMENT, "rank out of range");
     ctx->bind();
@@ -898,6 +899,7 @@ extern "C" dpmrf_status dpmrf_group_create_local(dpmrf_context* ctx, int world,
                                                  dpmrf_group** out) {
   return guarded([&] {
     need(ctx && out, DPMRF_INVALID_ARGUMENT, "null argument");
+    ContextLock lock_(ctx);
     need(world >= 1 && world <= kMaxParts, DPMRF_INVALID_ARGUMENT, "world must be in [1, 64]");
     ctx->bind();
     auto g = std::make_unique<dpmrf_group>();
@@ -966,6 +968,7 @@ extern "C" dpmrf_status dpmrf_optimize_partitioned(dpmrf_group* g,
     need(o.trace_level <= DPMRF_TRACE_EM, DPMRF_INVALID_ARGUMENT,
          "partitioned optimize records the EM trace only (trace level NONE or EM)");
     dpmrf_context* ctx = g->ctx;
+    ContextLock lock_(ctx);  // the group runs on its context's stream and inputs
     need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
     need(ctx->has_hoods, DPMRF_INVALID_ARGUMENT, "no neighborhoods uploaded");
     ctx->bind();

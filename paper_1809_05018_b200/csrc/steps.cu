@@ -249,6 +249,7 @@ extern "C" dpmrf_status dpmrf_init_random(dpmrf_context* ctx, uint32_t M, uint32
                                           uint64_t seed, int allow_multilabel, double* mu,
                                           double* sigma, uint32_t* labels) {
   STEP_GUARD({
+    ContextLock lock_(ctx);
     need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null context");
     if (M != 2 && !(allow_multilabel && M >= 1)) fail(DPMRF_INPUT_ERROR, "only 2 labels are supported");
     ctx->bind();
@@ -271,6 +272,7 @@ extern "C" dpmrf_status dpmrf_init_random(dpmrf_context* ctx, uint32_t M, uint32
 extern "C" dpmrf_status dpmrf_replicate_by_label(dpmrf_context* ctx, uint32_t M, uint32_t* tl,
                                                  uint32_t* oi, uint32_t* hid) {
   STEP_GUARD({
+    ContextLock lock_(ctx);
     need(ctx && ctx->has_hoods, DPMRF_INVALID_ARGUMENT, "no neighborhoods");
     ctx->bind();
     const uint64_t E = uint64_t(M) * ctx->S;
@@ -291,6 +293,7 @@ extern "C" dpmrf_status dpmrf_replicate_by_label(dpmrf_context* ctx, uint32_t M,
 
 extern "C" dpmrf_status dpmrf_slot_hood_map(dpmrf_context* ctx, uint32_t* slot_hood) {
   STEP_GUARD({
+    ContextLock lock_(ctx);
     need(ctx && ctx->has_hoods, DPMRF_INVALID_ARGUMENT, "no neighborhoods");
     ctx->bind();
     uint32_t* a = ctx->tmp_u32[0].ensure(ctx->S);
@@ -307,6 +310,7 @@ extern "C" dpmrf_status dpmrf_slot_hood_map(dpmrf_context* ctx, uint32_t* slot_h
 extern "C" dpmrf_status dpmrf_discord_counts(dpmrf_context* ctx, const uint32_t* labels,
                                              uint32_t M, uint32_t* discord) {
   STEP_GUARD({
+    ContextLock lock_(ctx);
     need(ctx && ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph");
     ctx->bind();
     const uint32_t R = ctx->R;
@@ -328,6 +332,7 @@ extern "C" dpmrf_status dpmrf_compute_energies(dpmrf_context* ctx, uint64_t E,
                                                const uint32_t* labels, double beta,
                                                double* energies) {
   STEP_GUARD({
+    ContextLock lock_(ctx);
     need(ctx && ctx->has_graph && ctx->has_hoods, DPMRF_INVALID_ARGUMENT,
          "graph and neighborhoods required");
     ctx->bind();
@@ -362,6 +367,7 @@ extern "C" dpmrf_status dpmrf_min_label_energies(dpmrf_context* ctx, uint64_t E,
                                                  const double* energies, uint64_t num_slots,
                                                  double* min_energy, uint32_t* min_label) {
   STEP_GUARD({
+    ContextLock lock_(ctx);
     need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null context");
     ctx->bind();
     cudaStream_t st = ctx->stream;
@@ -407,6 +413,7 @@ extern "C" dpmrf_status dpmrf_neighborhood_energy_sums(dpmrf_context* ctx, uint6
                                                        const double* mins, double* sums,
                                                        uint64_t* num_sums) {
   STEP_GUARD({
+    ContextLock lock_(ctx);
     need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null context");
     ctx->bind();
     cudaStream_t st = ctx->stream;
@@ -440,6 +447,7 @@ extern "C" dpmrf_status dpmrf_check_convergence(dpmrf_context* ctx, uint64_t row
                                                 uint64_t series, const double* history,
                                                 int32_t window, double tol, uint8_t* flags) {
   STEP_GUARD({
+    ContextLock lock_(ctx);
     need(ctx != nullptr, DPMRF_INVALID_ARGUMENT, "null context");
     if (rows == 0 || series == 0) return DPMRF_OK;  // empty history -> {} (engine.cpp:160)
     if (rows < uint64_t(window) + 1) {
@@ -461,6 +469,7 @@ extern "C" dpmrf_status dpmrf_update_labels(dpmrf_context* ctx, const uint32_t* 
                                             uint32_t R, const uint32_t* old_labels,
                                             uint32_t* labels) {
   STEP_GUARD({
+    ContextLock lock_(ctx);
     need(ctx && ctx->has_hoods, DPMRF_INVALID_ARGUMENT, "no neighborhoods");
     ctx->bind();
     cudaStream_t st = ctx->stream;
@@ -493,6 +502,7 @@ extern "C" dpmrf_status dpmrf_update_parameters(dpmrf_context* ctx, const uint32
                                                 const double* prev_sigma, double* mu,
                                                 double* sigma) {
   STEP_GUARD({
+    ContextLock lock_(ctx);
     need(ctx && ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph");
     need(M >= 1 && M <= uint32_t(kMaxLabels), DPMRF_INVALID_ARGUMENT,
          "update_parameters: num_labels must be in [1, 255]");

@@ -278,3 +278,39 @@ def test_optimize_arrays_one_call(ctx):
     with pytest.raises(ValueError):  # a bad CSR is reported, not run
         bad = E.NeighborhoodSet(np.array([0, 5, 3], np.uint32), hoods.members[:5])
         ctx.optimize_arrays(sl.graph, bad, cfg)
+
+
+def test_concurrent_calls_on_one_context_serialize(ctx):
+    """Entry points hold the context's mutex: two host threads interleaving
+    optimize_arrays on ONE context with DIFFERENT graphs each get their own
+    result (the reference's pool serializes submissions, backend.cpp:45)."""
+    import threading
+    from paper_1809_05018_b200 import inputs
+    cfg = E.OptimizerConfig(em_max_iters=4, rng_seed=5)
+    cases = []
+    for n, seed in ((512, 3), (384, 4)):
+        sl = inputs.synthetic_slice(n, 8, seed=seed)
+        ctx.set_graph(sl.graph)
+        ctx.build_neighborhoods(sl.cliques)
+        hoods = ctx.get_hoods()
+        want = ctx.optimize(cfg, fixed_work=True, trace_level=E.TRACE_NONE)
+        cases.append((sl.graph, hoods, want))
+    errors = []
+
+    def worker(graph, hoods, want):
+        try:
+            for _ in range(6):
+                got = ctx.optimize_arrays(graph, hoods, cfg, fixed_work=True,
+                                          trace_level=E.TRACE_NONE)
+                assert np.array_equal(got.labels, want.labels)
+                assert np.array_equal(got.mu, want.mu)
+                assert np.array_equal(got.sigma, want.sigma)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=c) for c in cases]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors

@@ -40,6 +40,19 @@ def test_cuda_library_exports_every_declared_symbol():
         assert hasattr(lib, name)
 
 
+def test_null_context_is_invalid_argument():
+    """Every context entry point rejects a null context before touching the
+    device (the context lock checks it), with a message, not a crash."""
+    import ctypes as ct
+    from paper_1809_05018_b200 import _native as N
+    lib = N.cuda()
+    st = N.CRunStats()
+    assert lib.dpmrf_get_stats(None, ct.byref(st)) == 2  # DPMRF_INVALID_ARGUMENT
+    assert b"null context" in lib.dpmrf_last_error()
+    em, series = ct.c_int32(), ct.c_uint64()
+    assert lib.dpmrf_trace_info(None, ct.byref(em), ct.byref(series)) == 2
+
+
 def test_cuda_library_is_sm100a():
     from paper_1809_05018_b200 import _native as N
     out = subprocess.run(["cuobjdump", "--list-elf", N.CUDA_LIB], capture_output=True, text=True)
