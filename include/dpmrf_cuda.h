@@ -101,7 +101,8 @@ typedef struct dpmrf_run_stats {
   uint64_t series;           /* hood-energy series length (nonempty hoods) */
   double map_loop_ms;        /* persistent MAP-loop kernel (one cooperative launch per EM) */
   uint64_t map_loop_launches;
-  int32_t persistent;        /* 1: persistent MAP loop, 0: two kernels per MAP iteration */
+  int32_t persistent;        /* 1: persistent MAP loop, 2: dataflow MAP loop (one launch per EM),
+                                0: kernels per MAP iteration */
   int32_t graphs;            /* 1: EM iterations replayed from CUDA graphs */
   int32_t device_loop;       /* 1: the result came from the device-resident EM loop */
   uint32_t device_log_fallbacks; /* reruns because a device log(sigma) differed from the host's */

@@ -134,6 +134,9 @@ void dpmrf_context::prepare() {
   // packed layouts when every neighbor list / hood fits (all grid and brick
   // oversegmentations do); otherwise the kernels read the CSR directly
   adj_k = hood_k = 0;
+  dict_ok = false;
+  dict_patterns[0] = dict_patterns[1] = 0;
+  flow_hp = 0;  // dependency ranges follow the structure
   if (use_packed && R > 0) {
     const uint32_t* hs = h_err + 2;
     const uint32_t* so = series_alias ? h_off.get() : s_off_buf.get();
@@ -143,6 +146,22 @@ void dpmrf_context::prepare() {
                                      adj_pk.ensure(uint64_t(R) * adj_k), stream);
     if (hood_k) launch_pack_hoods(so, h_mem.get(), Hs, hood_k, hood_base.ensure(Hs),
                                   hood_pk.ensure(Hs * hood_k), stream);
+    // dictionary form (MapArgs::vcode): one more pass and a 16-byte read-back
+    if (use_dict && adj_k && hood_k && R <= (1u << 24)) {
+      const size_t w = dict_ws_words();
+      uint32_t* ws = dict_ws.ensure(2 * w);
+      launch_dict_adjacency(g_off.get(), g_nbr.get(), R, adj_k, cover.get(), ws, vcode.ensure(R),
+                            adj_pat.ensure(uint64_t(kDictMax) * adj_k), stream);
+      launch_dict_hoods(so, h_mem.get(), Hs, hood_k, ws + w, hcode.ensure(Hs),
+                        hood_pat.ensure(uint64_t(kDictMax) * hood_k), stream);
+      uint32_t hd[4];
+      CK(cudaMemcpyAsync(hd, ws, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+      CK(cudaMemcpyAsync(hd + 2, ws + w, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+      sync();
+      dict_ok = hd[1] == 0 && hd[3] == 0;
+      dict_patterns[0] = hd[0];
+      dict_patterns[1] = hd[2];
+    }
   }
   // (no sync: everything that reads these runs later on the same stream)
 }
@@ -163,6 +182,9 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     if (const char* e = std::getenv("DPMRF_NO_PDL")) pdl_enabled() = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_HOST_LOG")) c->use_device_loop = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_CSR")) c->use_packed = e[0] == '0';
+    if (const char* e = std::getenv("DPMRF_DICT")) c->use_dict = e[0] == '1';
+    if (const char* e = std::getenv("DPMRF_FLOW")) c->use_flow = e[0] == '1';
+    if (const char* e = std::getenv("DPMRF_FLOW_SLEEP")) c->flow_sleep_ns = uint32_t(std::atoi(e));
     if (const char* e = std::getenv("DPMRF_UNFUSED")) c->use_fused = e[0] == '0';
     try {
       CK(cudaSetDevice(device));
@@ -551,6 +573,12 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     a.hood_k = packed ? ctx->hood_k : 0;
     a.hood_base = ctx->hood_base.get();
     a.hood_pk = ctx->hood_pk.get();
+    if (packed && ctx->dict_ok) {
+      a.vcode = ctx->vcode.get();
+      a.adj_pat = ctx->adj_pat.get();
+      a.hcode = ctx->hcode.get();
+      a.hood_pat = ctx->hood_pat.get();
+    }
     const bool fused = fused_req && !a.staged && map_fused_supported(a);
     a.terms = ctx->terms.ensure(3 * M);
     double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
@@ -615,6 +643,38 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     // the EM bookkeeping joins the sq-pass tail -- 3 launches fewer per EM
     // (no k_em_prologue / k_label_scatter_small / k_em_epilogue).
     const bool merged = device_loop && fused && !a.flags && mstep_tail_fusable(R, M);
+    // dataflow MAP loop (k_map_flow): one launch per EM instead of map_max+1
+    // when the whole grid fits resident; the M-step's scatter then runs as
+    // its own kernel (it needs every tile's final counts)
+    FlowArgs fl{};
+    int flow_hp = 0;
+    if (merged && ctx->use_flow) flow_hp = flow_plan(a, &fl.nvt, &fl.nht);
+    const bool flow = flow_hp > 0;
+    if (flow) ctx->stats.persistent = 2;
+    if (flow) {
+      if (ctx->flow_hp != flow_hp || ctx->flow_nvt != fl.nvt || ctx->flow_nht != fl.nht) {
+        launch_flow_deps(a.g_off, a.g_nbr, R, a.s_off, a.h_mem, Hs, flow_hp, fl.nvt, fl.nht,
+                         ctx->flow_vdep.ensure(2 * uint64_t(fl.nvt)),
+                         ctx->flow_hdep.ensure(2 * uint64_t(fl.nht ? fl.nht : 1)), st);
+        // progress flags one per 128-byte line: nvt vertex tiles, map_max hood counters, ticket
+        const uint64_t nf = (uint64_t(fl.nvt) + kMaxMapIters + 1) * 32;
+        uint32_t* z = ctx->flow_flags.ensure(nf);
+        CK(cudaMemsetAsync(z, 0, nf * sizeof(uint32_t), st));
+        ctx->flow_hp = flow_hp;
+        ctx->flow_nvt = fl.nvt;
+        ctx->flow_nht = fl.nht;
+      }
+      fl.vdep = ctx->flow_vdep.get();
+      fl.hdep = ctx->flow_hdep.get();
+      fl.vflag = ctx->flow_flags.get();
+      fl.hdone = fl.vflag + uint64_t(fl.nvt) * 32;
+      fl.ticket = fl.hdone + uint64_t(kMaxMapIters) * 32;
+      fl.minE_all = ctx->minE_flow.ensure(uint64_t(map_max) * R);
+      fl.lab_a = lab[0];
+      fl.lab_b = lab[1];
+      fl.map_max = map_max;
+      fl.sleep_ns = ctx->flow_sleep_ns;
+    }
     ScatterArgs sc{};
     sc.mean = a.mean;
     sc.counts = ctx->ms.counts.get();
@@ -640,7 +700,12 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
                            cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(a.unconv, 0, map_max * sizeof(uint32_t), st));
       }
-      if (persistent) {
+      if (flow) {
+        record(ev++);
+        launch_map_flow(a, fl, flow_hp, &sc, st);
+        record(ev++);
+        k += 1;
+      } else if (persistent) {
         record(ev++);
         launch_map_loop(a, lab[parity], lab[parity ^ 1], minE2, minE2 + R, map_max, st);
         record(ev++);
@@ -736,7 +801,9 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       key.p2[2] = a.adj_pk;
       key.p2[3] = a.hood_pk;
       key.p2[4] = a.hood_base;
-      key.layout = a.adj_k * 100 + a.hood_k;
+      key.p2[5] = a.vcode;
+      key.p2[6] = a.hcode;
+      key.layout = a.adj_k * 100 + a.hood_k + flow_hp * 100000;
       if (!ctx->graph_valid || std::memcmp(&key, &ctx->graph_key, sizeof key) != 0) {
         ctx->drop_graphs();
         for (int parity = 0; parity < (device_loop ? 1 : 2); ++parity) {
@@ -831,7 +898,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
         if (timing) {
           float ms = 0.f;
           size_t e = 0;
-          if (persistent) {
+          if (persistent || flow) {
             CK(cudaEventElapsedTime(&ms, ctx->ev_pool[0], ctx->ev_pool[1]));
             ctx->stats.map_loop_ms += ms;
             ctx->stats.map_loop_launches += 1;

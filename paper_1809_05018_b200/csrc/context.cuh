@@ -176,6 +176,24 @@ struct dpmrf_context {
   dpmrf_b200::DevBuf<int16_t> adj_pk;
   dpmrf_b200::DevBuf<uint32_t> hood_base;
   dpmrf_b200::DevBuf<uint16_t> hood_pk;
+  // dictionary form of the packed layouts (engine.cuh MapArgs::vcode);
+  // opt-in (DPMRF_DICT=1): measured slower than the plain packed layout
+  //
+  bool use_dict = false, dict_ok = false;
+  uint32_t dict_patterns[2] = {0, 0};  // distinct adjacency / hood patterns
+  dpmrf_b200::DevBuf<uint8_t> vcode;
+  dpmrf_b200::DevBuf<int16_t> adj_pat;
+  dpmrf_b200::DevBuf<uint32_t> hcode;
+  dpmrf_b200::DevBuf<uint16_t> hood_pat;
+  dpmrf_b200::DevBuf<uint32_t> dict_ws;
+  // dataflow MAP loop (engine.cuh FlowArgs): opt-in (DPMRF_FLOW=1), measured
+  // slower than the PDL chain of fused launches
+  bool use_flow = false;
+  int flow_hp = 0;  // 0: dependency ranges not built for the current structure
+  uint32_t flow_nvt = 0, flow_nht = 0;
+  uint32_t flow_sleep_ns = 32;  // DPMRF_FLOW_SLEEP
+  dpmrf_b200::DevBuf<uint32_t> flow_vdep, flow_hdep, flow_flags;
+  dpmrf_b200::DevBuf<double> minE_flow;
 };
 
 namespace dpmrf_b200 {

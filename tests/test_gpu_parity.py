@@ -314,3 +314,39 @@ def test_concurrent_calls_on_one_context_serialize(ctx):
     for t in th:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("env", ["DPMRF_FLOW", "DPMRF_DICT"])
+def test_opt_in_layouts_agree(env, monkeypatch):
+    """The measured-and-rejected variants stay correct: the dataflow MAP loop
+    (DPMRF_FLOW=1: one launch per EM, tiles synchronised by progress flags,
+    early exit decided two iterations behind) and the dictionary-coded
+    structure (DPMRF_DICT=1) reproduce the fixtures and the default path."""
+    from paper_1809_05018_b200 import inputs
+    monkeypatch.setenv(env, "1")
+    c = E.Context(0)
+    monkeypatch.delenv(env)
+    base = E.Context(0)
+    try:
+        for name in ("configA_256_grid8", "m5_128_brick8", "configA_252_grid7"):
+            f = Fixture(name)
+            upload(c, f.graph, f.hoods)
+            for fixed in (f.fixed, True):
+                r = c.optimize(to_cfg(f.cfg), fixed_work=fixed, trace_level=E.TRACE_EM)
+                if fixed == f.fixed:
+                    f.check(r)
+                if env == "DPMRF_FLOW" and name != "m5_128_brick8":
+                    assert r.stats["persistent"] == 2  # the flow kernel ran
+        for size, seed in ((1024, 3), (2560, 42)):
+            sl = inputs.synthetic_slice(size, 8, seed=seed)
+            for ctx_ in (c, base):
+                ctx_.set_graph(sl.graph)
+                ctx_.build_neighborhoods(sl.cliques)
+            for fixed in (False, True):
+                cfg = E.OptimizerConfig(em_max_iters=8, rng_seed=seed)
+                got = c.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_EM)
+                want = base.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_EM)
+                same(got, want, full=False)
+    finally:
+        c.close()
+        base.close()
