@@ -216,9 +216,10 @@ def run_stack(args, E, inputs, torch, world, rank, local, barrier, allmax, allsu
     def run_one(i):
         return ctxs[i].optimize(cfgs[i], fixed_work=True, trace_level=E.TRACE_NONE)
 
+    pool = ThreadPoolExecutor(max_workers=workers)  # (threads started once, not per step)
+
     def step():
-        with ThreadPoolExecutor(max_workers=workers) as ex:
-            return list(ex.map(run_one, range(len(ctxs))))
+        return list(pool.map(run_one, range(len(ctxs))))
 
     for _ in range(args.warmup):
         step()
@@ -260,6 +261,7 @@ def run_stack(args, E, inputs, torch, world, rank, local, barrier, allmax, allsu
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    pool.shutdown()
     for ctx in ctxs:
         ctx.close()
     return 0

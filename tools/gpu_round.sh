@@ -13,7 +13,7 @@ timeout 600 python bench.py > $O/bench_B.jsonl 2> $O/bench_B.err
 timeout 600 python bench.py --config C --cpu-seconds 20 > $O/bench_C.jsonl 2> $O/bench_C.err
 timeout 900 python bench.py --config D --steps 5 --no-cpu-baseline > $O/bench_D.jsonl 2> $O/bench_D.err
 timeout 900 python bench.py --config D --steps 3 --local-parts 2 > $O/bench_D_local2.jsonl 2> $O/bench_D_local2.err
-timeout 600 python bench.py --config E --slices 16 --steps 3 > $O/bench_E16.jsonl 2> $O/bench_E16.err
+timeout 600 python bench.py --config E --slices 64 --steps 3 > $O/bench_E64.jsonl 2> $O/bench_E64.err
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref_B.jsonl 2> $O/bench_ref_B.err
 timeout 900 python tools/bench_structure.py > $O/structure.jsonl 2> $O/structure.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_B.csv \
