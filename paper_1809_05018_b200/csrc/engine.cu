@@ -1318,8 +1318,16 @@ __global__ void k_compact_offsets(const uint32_t* __restrict__ h_off, uint64_t H
 #endif
 namespace {
 // The 2-label, <= 8-slot instance fits 32 registers without spilling, so it
-// runs 8 blocks per SM; the wider instances keep the compiler's choice.
-constexpr int fused_min_blocks(int mt, int kh) { return mt == 2 && kh == 8 ? DPMRF_FUSED_MINB : 1; }
+// runs 8 blocks per SM.
+// The config C instance (5 labels, <= 16 slots) at 5 blocks per SM: 48
+// registers, an 8-byte spill, +2.5% over the compiler's 56 (6 or 8 blocks
+// spill more and lose 4-8%); the other wide instances keep the compiler's choice.
+#ifndef DPMRF_FUSED_MINB_M5
+#define DPMRF_FUSED_MINB_M5 5
+#endif
+constexpr int fused_min_blocks(int mt, int kh) {
+  return mt == 2 && kh == 8 ? DPMRF_FUSED_MINB : (mt == 5 ? DPMRF_FUSED_MINB_M5 : 1);
+}
 constexpr int kWinRegs = 3;  // window rows held in registers (default L = 3)
 constexpr uint32_t kVertsPerThreadMin = 1u << 20;  // owned vertices for 2 per thread
 template <int MT, int K>
