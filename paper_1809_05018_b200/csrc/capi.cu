@@ -656,8 +656,9 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
         launch_flow_deps(a.g_off, a.g_nbr, R, a.s_off, a.h_mem, Hs, flow_hp, fl.nvt, fl.nht,
                          ctx->flow_vdep.ensure(2 * uint64_t(fl.nvt)),
                          ctx->flow_hdep.ensure(2 * uint64_t(fl.nht ? fl.nht : 1)), st);
-        // progress flags one per 128-byte line: nvt vertex tiles, map_max hood counters, ticket
-        const uint64_t nf = (uint64_t(fl.nvt) + kMaxMapIters + 1) * 32;
+        // progress flags one per 128-byte line: nvt vertex tiles, map_max hood
+        // counters, the exit ticket and the scatter's done counter
+        const uint64_t nf = (uint64_t(fl.nvt) + kMaxMapIters + 2) * 32;
         uint32_t* z = ctx->flow_flags.ensure(nf);
         CK(cudaMemsetAsync(z, 0, nf * sizeof(uint32_t), st));
         ctx->flow_hp = flow_hp;
