@@ -573,6 +573,15 @@ def main():
                   "note": "phantom -> corrupt -> oversegment -> graph -> cliques -> hoods "
                           "on the device (csrc/synth.cu, structure.cu, hoods.cu)"},
     }
+    if c["M"] == 2:
+        # segmentation quality of the timed result (not timed): the segment
+        # write-back against the phantom truth, on the device
+        _, cc = ctx.segment_mask(r.labels, r.mu, mask=False)
+        mt = E.compute_metrics(cc)
+        line["quality"] = {"precision": mt.precision, "recall": mt.recall,
+                           "accuracy": mt.accuracy,
+                           "source": "device segment write-back (main.cpp:157-165) vs the "
+                                     "phantom truth, confusion on the device; not timed"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             v, det = reference_sample(args.config, seconds_budget=args.cpu_seconds, rank_seed=seed)

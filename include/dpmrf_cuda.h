@@ -169,6 +169,24 @@ dpmrf_status dpmrf_make_phantom(dpmrf_context* ctx, const dpmrf_phantom_spec* sp
 dpmrf_status dpmrf_oversegment(dpmrf_context* ctx, uint32_t block, int32_t brick,
                                uint32_t* num_regions, uint32_t* region);
 
+/* ---- evaluation ---------------------------------
+ * confusion(pred, truth), proj/include/dpmrf/eval/metrics.hpp:17-18 and
+ * proj/src/eval/metrics.cpp:8-14 (simd::confusion_u8, scalar_kernels.cpp:48-63)
+ * over n host pixels (nonzero = positive): counts = {tp, tn, fp, fn}.  The
+ * shape check of confusion() (InputError) is the caller's (both images are n
+ * pixels here). */
+dpmrf_status dpmrf_confusion(dpmrf_context* ctx, uint64_t n, const uint8_t* pred,
+                             const uint8_t* truth, uint64_t counts[4]);
+/* The segment write-back of proj/tools/main.cpp:157-165 (== the acceptance
+ * test's labels_to_mask, proj/tests/acceptance.cpp:359-370) over the resident
+ * label map (dpmrf_oversegment): mask[p] = labels[region[p]] == pore, pore =
+ * mu[0] <= mu[1] ? 0 : 1 (the darker class).  labels: num_vertices host values
+ * (an optimize result, num_vertices == the map's regions); mask: width*height
+ * bytes or NULL; counts: {tp, tn, fp, fn} against the resident phantom truth
+ * (dpmrf_make_phantom), or NULL. */
+dpmrf_status dpmrf_segment_mask(dpmrf_context* ctx, uint32_t num_vertices, const uint32_t* labels,
+                                const double* mu, uint8_t* mask, uint64_t counts[4]);
+
 /* build_region_graph from the resident image and region map. */
 dpmrf_status dpmrf_build_region_graph_resident(dpmrf_context* ctx, uint64_t* num_adjacency);
 

@@ -648,6 +648,35 @@ int orc_optimize_reference(uint32_t R, const uint32_t *g_off, const uint32_t *g_
 }
 
 /* ------------------------------------------------------------------ */
+/* Evaluation.                                 */
+/* ------------------------------------------------------------------ */
+/* confusion_u8, scalar_kernels.cpp:48-63 (behind confusion(),
+ * metrics.cpp:8-14): nonzero = positive; counts = {tp, tn, fp, fn}. */
+void orc_confusion(uint64_t n, const uint8_t *pred, const uint8_t *truth, uint64_t counts[4]) {
+  uint64_t tp = 0, tn = 0, fp = 0, fn = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const int p = pred[i] != 0, t = truth[i] != 0;
+    tp += p && t;
+    tn += !p && !t;
+    fp += p && !t;
+    fn += !p && t;
+  }
+  counts[0] = tp;
+  counts[1] = tn;
+  counts[2] = fp;
+  counts[3] = fn;
+}
+
+/* The segment write-back, tools/main.cpp:157-165 (acceptance.cpp:359-370):
+ * the darker class (mu[0] <= mu[1] ? 0 : 1) is the pore phase; mask[p] =
+ * labels[region[p]] == pore. */
+void orc_labels_to_mask(uint64_t n, const uint32_t *region, const uint32_t *labels,
+                        const double *mu, uint8_t *mask) {
+  const uint32_t pore = mu[0] <= mu[1] ? 0u : 1u;
+  for (uint64_t i = 0; i < n; ++i) mask[i] = labels[region[i]] == pore ? 1 : 0;
+}
+
+/* ------------------------------------------------------------------ */
 /* Structure builders.                      */
 /* Outputs of variable length are malloc'd; release with orc_free.      */
 /* ------------------------------------------------------------------ */

@@ -198,6 +198,8 @@ class _COracle:
         L.orc_maximal_cliques.argtypes = [U32, u32p, u32p, PU32, ct.POINTER(U64), PU32,
                                           ct.POINTER(U64)]
         L.orc_free.argtypes = [VP]
+        L.orc_confusion.argtypes = [U64, u8p, u8p, ct.POINTER(U64)]
+        L.orc_labels_to_mask.argtypes = [U64, u32p, u32p, f64p, u8p]
         for fn in (L.orc_optimize, L.orc_optimize_reference):
             fn.argtypes = [U32, u32p, u32p, f64p, U64, u32p, u32p, ct.POINTER(Config), ct.c_int,
                            ct.c_int, u32p, f64p, f64p, ct.POINTER(_Trace)]
@@ -360,6 +362,20 @@ class _COracle:
         off = self._take(po, C.value + 1)
         return off, self._take(pm, CS.value)
 
+    def confusion(self, pred, truth):
+        """confusion_u8 (scalar_kernels.cpp:48-63) -> (tp, tn, fp, fn)."""
+        a, b = _a(pred, np.uint8), _a(truth, np.uint8)
+        c = (U64 * 4)()
+        self.L.orc_confusion(a.size, a, b, c)
+        return tuple(int(x) for x in c)
+
+    def labels_to_mask(self, region, labels, mu):
+        """main.cpp:157-165 -> u8 mask."""
+        reg = _a(region, np.uint32)
+        out = np.zeros(reg.size, np.uint8)
+        self.L.orc_labels_to_mask(reg.size, reg, _a(labels, np.uint32), _a(mu, np.float64), out)
+        return out
+
     def optimize(self, g, hoods, cfg, fixed_work=False, allow_multilabel=False, full_trace=True):
         return self._run(self.L.orc_optimize, g, hoods, cfg, fixed_work, allow_multilabel,
                          full_trace)
@@ -498,6 +514,10 @@ class _Ref:
         L.ref_reduce_add.argtypes = [U64, f64p]
         L.ref_reduce_add.restype = F64
         L.ref_hw_threads.restype = U32
+        L.ref_confusion.argtypes = [U32, U32, u8p, U32, U32, u8p, ct.POINTER(U64)]
+        L.ref_compute_metrics.argtypes = [ct.POINTER(U64), ct.POINTER(F64), ct.POINTER(ct.c_int)]
+        L.ref_porosity.argtypes = [U32, U32, u8p]
+        L.ref_porosity.restype = F64
 
     def phantom(self, size=256, block=8, pore=0.25, sp=0.05, gauss=100.0, ringing=True, seed=42,
                 brick=False, threads=1, height=None) -> Pipe:
@@ -547,6 +567,29 @@ class _Ref:
 
     def hw_threads(self) -> int:
         return int(self.L.ref_hw_threads())
+
+    def confusion(self, w1, h1, pred, w2, h2, truth):
+        """dpmrf::confusion on two BinaryImages -> (tp, tn, fp, fn); OracleError on
+        the reference's InputError."""
+        c = (U64 * 4)()
+        a = _a(pred, np.uint8) if len(pred) else np.zeros(1, np.uint8)
+        b = _a(truth, np.uint8) if len(truth) else np.zeros(1, np.uint8)
+        rc = self.L.ref_confusion(w1, h1, a, w2, h2, b, c)
+        if rc:
+            raise OracleError(rc, "ref_confusion")
+        return tuple(int(x) for x in c)
+
+    def compute_metrics(self, counts):
+        """dpmrf::compute_metrics -> (precision, recall, accuracy, p_def, r_def)."""
+        c = (U64 * 4)(*counts)
+        m = (F64 * 3)()
+        d = (ct.c_int * 2)()
+        self.L.ref_compute_metrics(c, m, d)
+        return m[0], m[1], m[2], bool(d[0]), bool(d[1])
+
+    def porosity(self, w, h, pixels):
+        a = _a(pixels, np.uint8) if len(pixels) else np.zeros(1, np.uint8)
+        return float(self.L.ref_porosity(w, h, a))
 
 
 _C = None

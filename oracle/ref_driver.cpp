@@ -28,6 +28,7 @@
 
 #include "dpmrf/dpp/kernels.hpp"
 #include "dpmrf/error.hpp"
+#include "dpmrf/eval/metrics.hpp"
 #include "dpmrf/eval/phantom.hpp"
 #include "dpmrf/graph/cliques.hpp"
 #include "dpmrf/graph/label_map.hpp"
@@ -648,5 +649,46 @@ double ref_reduce_add(std::uint64_t n, const double* x) {
 }
 
 std::uint32_t ref_hw_threads() { return std::max(1u, std::thread::hardware_concurrency()); }
+
+// dpmrf::confusion (metrics.cpp:8-14) on two BinaryImages (w x h pixels each).
+int ref_confusion(std::uint32_t w1, std::uint32_t h1, const std::uint8_t* pred, std::uint32_t w2,
+                  std::uint32_t h2, const std::uint8_t* truth, std::uint64_t* counts) {
+  return guarded([&] {
+    BinaryImage a, b;
+    a.width = w1;
+    a.height = h1;
+    a.pixels.assign(pred, pred + std::size_t(w1) * h1);
+    b.width = w2;
+    b.height = h2;
+    b.pixels.assign(truth, truth + std::size_t(w2) * h2);
+    const ConfusionCounts c = confusion(a, b);
+    counts[0] = c.tp;
+    counts[1] = c.tn;
+    counts[2] = c.fp;
+    counts[3] = c.fn;
+  });
+}
+
+void ref_compute_metrics(const std::uint64_t* counts, double* out, int* defined) {
+  ConfusionCounts c;
+  c.tp = counts[0];
+  c.tn = counts[1];
+  c.fp = counts[2];
+  c.fn = counts[3];
+  const Metrics m = compute_metrics(c);
+  out[0] = m.precision;
+  out[1] = m.recall;
+  out[2] = m.accuracy;
+  defined[0] = m.precision_defined;
+  defined[1] = m.recall_defined;
+}
+
+double ref_porosity(std::uint32_t w, std::uint32_t h, const std::uint8_t* px) {
+  BinaryImage a;
+  a.width = w;
+  a.height = h;
+  a.pixels.assign(px, px + std::size_t(w) * h);
+  return porosity(a);
+}
 
 }  // extern "C"

@@ -395,6 +395,52 @@ extern "C" dpmrf_status dpmrf_make_phantom(dpmrf_context* ctx, const dpmrf_phant
   });
 }
 
+extern "C" dpmrf_status dpmrf_confusion(dpmrf_context* ctx, uint64_t n, const uint8_t* pred,
+                                        const uint8_t* truth, uint64_t counts[4]) {
+  return guarded([&] {
+    ContextLock lock_(ctx);
+    need(counts && (n == 0 || (pred && truth)), DPMRF_INVALID_ARGUMENT, "null argument");
+    ctx->bind();
+    uint8_t* a = ctx->eval_a.ensure(n ? n : 1);
+    uint8_t* b = ctx->eval_b.ensure(n ? n : 1);
+    if (n) {
+      CK(cudaMemcpyAsync(a, pred, n, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemcpyAsync(b, truth, n, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    confusion_device(ctx, a, b, n, counts);
+  });
+}
+
+extern "C" dpmrf_status dpmrf_segment_mask(dpmrf_context* ctx, uint32_t num_vertices,
+                                           const uint32_t* labels, const double* mu,
+                                           uint8_t* mask, uint64_t counts[4]) {
+  return guarded([&] {
+    ContextLock lock_(ctx);
+    need(labels && mu, DPMRF_INVALID_ARGUMENT, "null argument");
+    need(ctx->has_regions, DPMRF_INVALID_ARGUMENT, "no resident label map (dpmrf_oversegment)");
+    need(num_vertices == ctx->img_regions, DPMRF_INVALID_ARGUMENT,
+         "labels do not match the resident label map's regions");
+    need(!counts || ctx->has_image, DPMRF_INVALID_ARGUMENT,
+         "no resident phantom truth (dpmrf_make_phantom)");
+    ctx->bind();
+    const uint64_t n = uint64_t(ctx->img_w) * ctx->img_h;
+    uint32_t* d_lab = ctx->eval_labels.ensure(num_vertices ? num_vertices : 1);
+    if (num_vertices)
+      CK(cudaMemcpyAsync(d_lab, labels, uint64_t(num_vertices) * 4, cudaMemcpyHostToDevice,
+                         ctx->stream));
+    uint8_t* d_mask = mask ? ctx->eval_a.ensure(n ? n : 1) : nullptr;
+    // the darker class (smaller mean) is the pore phase (main.cpp:157)
+    const uint32_t pore = mu[0] <= mu[1] ? 0u : 1u;
+    uint64_t c[4];
+    segment_mask_device(ctx, d_lab, pore, d_mask, counts != nullptr, c);
+    if (mask && n) {
+      CK(cudaMemcpyAsync(mask, d_mask, n, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+    }
+    if (counts) std::memcpy(counts, c, sizeof c);
+  });
+}
+
 extern "C" dpmrf_status dpmrf_oversegment(dpmrf_context* ctx, uint32_t block, int32_t brick,
                                           uint32_t* num_regions, uint32_t* region) {
   return guarded([&] {

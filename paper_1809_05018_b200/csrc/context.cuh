@@ -32,6 +32,9 @@ struct dpmrf_context {
   dpmrf_b200::DevBuf<uint32_t> c_off, c_mem;
   dpmrf_b200::DevBuf<uint8_t> img_px, img_truth;
   dpmrf_b200::DevBuf<uint32_t> img_reg;
+  dpmrf_b200::DevBuf<uint64_t> eval_counts;     // {tp, tn, fp, fn}
+  dpmrf_b200::DevBuf<uint8_t> eval_a, eval_b;   // uploaded masks / the written-back mask
+  dpmrf_b200::DevBuf<uint32_t> eval_labels;
   uint32_t img_w = 0, img_h = 0, img_regions = 0;  // resident image / region map (synth.cu)
   bool has_image = false, has_regions = false;
   dpmrf_b200::HostBuf<unsigned long long> h_syn;
@@ -225,4 +228,11 @@ void enumerate_maximal_cliques_device(dpmrf_context* ctx);
 // synth.cu
 uint32_t make_phantom_device(dpmrf_context* ctx, const dpmrf_phantom_spec& spec);
 uint32_t oversegment_device(dpmrf_context* ctx, uint32_t block, bool brick);
+// Evaluation (synth.cu): confusion of two device u8 masks; the segment
+// write-back of device labels over the resident region map (mask: device
+// buffer or nullptr), counted against the resident truth when with_truth.
+void confusion_device(dpmrf_context* ctx, const uint8_t* pred, const uint8_t* truth, uint64_t n,
+                      uint64_t counts[4]);
+void segment_mask_device(dpmrf_context* ctx, const uint32_t* labels, uint32_t pore,
+                         uint8_t* mask, bool with_truth, uint64_t counts[4]);
 }  // namespace dpmrf_b200

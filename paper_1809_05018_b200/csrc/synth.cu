@@ -33,6 +33,8 @@ namespace dpmrf_b200 {
 
 namespace {
 
+constexpr int kEvalThreads = 256;
+
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kRingAmplitude = 15.0;
 constexpr double kTieBand = 1e-7;
@@ -181,6 +183,64 @@ uint8_t corrupt_pixel_host(uint8_t clean, uint64_t i, const CorruptArgs& a) {
   return static_cast<uint8_t>(std::lround(val));
 }
 
+// ---- evaluation (proj/src/eval/metrics.cpp:8-14, tools/main.cpp:157-165) ----
+// confusion_u8 (scalar_kernels.cpp:48-63): nonzero = positive.  Per-thread
+// counts over a grid-stride loop, then one block reduction.
+__global__ void __launch_bounds__(kEvalThreads)
+    k_confusion(const uint8_t* __restrict__ pred, const uint8_t* __restrict__ truth, uint64_t n,
+                unsigned long long* counts) {
+  uint32_t c[4] = {0, 0, 0, 0};
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const bool p = pred[i] != 0, t = truth[i] != 0;
+    c[0] += p && t;
+    c[1] += !p && !t;
+    c[2] += p && !t;
+    c[3] += !p && t;
+  }
+  __shared__ unsigned long long part[4];
+  if (threadIdx.x < 4) part[threadIdx.x] = 0;
+  __syncthreads();
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t w = __reduce_add_sync(0xFFFFFFFFu, c[q]);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(&part[q], static_cast<unsigned long long>(w));
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && part[threadIdx.x]) atomicAdd(counts + threadIdx.x, part[threadIdx.x]);
+}
+
+// The segment write-back: mask[p] = labels[region[p]] == pore (main.cpp:157-165,
+// acceptance.cpp:359-370), optionally counted against the phantom truth.
+__global__ void __launch_bounds__(kEvalThreads)
+    k_segment_mask(const uint32_t* __restrict__ region, uint64_t n,
+                   const uint32_t* __restrict__ labels, uint32_t pore,
+                   const uint8_t* __restrict__ truth, uint8_t* __restrict__ mask,
+                   unsigned long long* counts) {
+  uint32_t c[4] = {0, 0, 0, 0};
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const bool p = labels[region[i]] == pore;
+    if (mask) mask[i] = p ? 1 : 0;
+    if (truth) {
+      const bool t = truth[i] != 0;
+      c[0] += p && t;
+      c[1] += !p && !t;
+      c[2] += p && !t;
+      c[3] += !p && t;
+    }
+  }
+  if (!truth) return;  // (uniform)
+  __shared__ unsigned long long part[4];
+  if (threadIdx.x < 4) part[threadIdx.x] = 0;
+  __syncthreads();
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t w = __reduce_add_sync(0xFFFFFFFFu, c[q]);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(&part[q], static_cast<unsigned long long>(w));
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && part[threadIdx.x]) atomicAdd(counts + threadIdx.x, part[threadIdx.x]);
+}
+
 }  // namespace
 
 uint32_t make_phantom_device(dpmrf_context* ctx, const dpmrf_phantom_spec& spec) {
@@ -295,6 +355,36 @@ uint32_t oversegment_device(dpmrf_context* ctx, uint32_t b, bool brick) {
   if (R >= (1ull << 32)) fail(DPMRF_INPUT_ERROR, "oversegment: too many regions");
   ctx->img_regions = uint32_t(R);
   return uint32_t(R);
+}
+
+void confusion_device(dpmrf_context* ctx, const uint8_t* pred, const uint8_t* truth, uint64_t n,
+                      uint64_t counts[4]) {
+  auto* d = reinterpret_cast<unsigned long long*>(ctx->eval_counts.ensure(4));
+  CK(cudaMemsetAsync(d, 0, 4 * sizeof(uint64_t), ctx->stream));
+  if (n) {
+    const unsigned g = std::min<uint64_t>((n + kEvalThreads - 1) / kEvalThreads, 8 * kNumSMs);
+    k_confusion<<<g, kEvalThreads, 0, ctx->stream>>>(pred, truth, n, d);
+    CK_LAUNCH();
+  }
+  CK(cudaMemcpyAsync(counts, d, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+}
+
+void segment_mask_device(dpmrf_context* ctx, const uint32_t* labels, uint32_t pore,
+                         uint8_t* mask, bool with_truth, uint64_t counts[4]) {
+  const uint64_t n = uint64_t(ctx->img_w) * ctx->img_h;
+  auto* d = reinterpret_cast<unsigned long long*>(ctx->eval_counts.ensure(4));
+  CK(cudaMemsetAsync(d, 0, 4 * sizeof(uint64_t), ctx->stream));
+  if (n) {
+    const unsigned g = std::min<uint64_t>((n + kEvalThreads - 1) / kEvalThreads, 8 * kNumSMs);
+    k_segment_mask<<<g, kEvalThreads, 0, ctx->stream>>>(
+        ctx->img_reg.get(), n, labels, pore, with_truth ? ctx->img_truth.get() : nullptr, mask, d);
+    CK_LAUNCH();
+  }
+  if (counts) {
+    CK(cudaMemcpyAsync(counts, d, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  ctx->sync();
 }
 
 }  // namespace dpmrf_b200

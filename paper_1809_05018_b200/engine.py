@@ -228,6 +228,7 @@ class Context:
         self.S = 0
         self._cliques_n = (0, 0)
         self._img_n = 0  # pixels of the resident image (make_phantom)
+        self._img_regions = 0  # regions of the resident label map (oversegment)
 
     def close(self):
         if self.h:
@@ -300,12 +301,14 @@ class Context:
         region = np.zeros(self._img_n, np.uint32) if copy_out and self._img_n else None
         _check(self._lib.dpmrf_oversegment(self.h, block, int(brick), ct.byref(R), N.ptr(region)),
                "oversegment")
+        self._img_regions = R.value
         return R.value, region
 
     def build_region_graph_resident(self) -> int:
         A = ct.c_uint64(0)
         _check(self._lib.dpmrf_build_region_graph_resident(self.h, ct.byref(A)),
                "build_region_graph_resident")
+        self.R = self._img_regions  # (the graph's vertices are the map's regions)
         self._graph_key = None
         self._hoods_key = None
         return A.value
@@ -323,6 +326,31 @@ class Context:
         C, CS = self.enumerate_maximal_cliques()
         S = self.build_neighborhoods_resident()
         return {"regions": R, "adjacency": A, "cliques": C, "slots": S, "host_ties": ties}
+
+    # -- evaluation on the device --
+    def confusion(self, pred, truth) -> "ConfusionCounts":
+        """confusion_u8 (metrics.cpp:8-14, scalar_kernels.cpp:48-63) of two
+        equally long u8 arrays (nonzero = positive) on the device."""
+        a, b = np.ascontiguousarray(pred, np.uint8), np.ascontiguousarray(truth, np.uint8)
+        if a.size != b.size:
+            raise InputError("confusion: image dimensions differ")
+        c = np.zeros(4, np.uint64)
+        _check(self._lib.dpmrf_confusion(self.h, a.size, N.ptr(a), N.ptr(b), N.ptr(c)),
+               "confusion")
+        return ConfusionCounts(*(int(x) for x in c))
+
+    def segment_mask(self, labels, mu, *, mask=True, counts=True):
+        """The segment write-back (main.cpp:157-165): mask[p] =
+        labels[region[p]] == pore (the darker class) over the resident label
+        map, and its confusion against the resident phantom truth.  Returns
+        (mask or None, ConfusionCounts or None)."""
+        lab = np.ascontiguousarray(labels, np.uint32)
+        m = np.asarray(mu, np.float64)
+        out = np.zeros(self._img_n, np.uint8) if mask else None
+        c = np.zeros(4, np.uint64) if counts else None
+        _check(self._lib.dpmrf_segment_mask(self.h, lab.size, N.ptr(lab), N.ptr(m), N.ptr(out),
+                                            N.ptr(c)), "segment_mask")
+        return out, (ConfusionCounts(*(int(x) for x in c)) if counts else None)
 
     # -- device structure builders (SURVEY.md §8(f) items 1-2) --
     def build_region_graph(self, width: int, height: int, pixels, region, num_regions: int) -> int:
@@ -743,3 +771,64 @@ def update_parameters(backend: Backend, graph: RegionGraph, labels, previous: La
     ctx = context_for(backend)
     _resident(ctx, graph)
     return ctx.update_parameters(labels, previous)
+
+
+# ---- evaluation (proj/include/dpmrf/eval/metrics.hpp) ------------------------------
+@dataclass
+class ConfusionCounts:
+    """ConfusionCounts, metrics.hpp:9-14 (class 1 / pore positive)."""
+    tp: int = 0
+    tn: int = 0
+    fp: int = 0
+    fn: int = 0
+
+
+@dataclass
+class Metrics:
+    """Metrics, metrics.hpp:20-26."""
+    precision: float = 0.0
+    recall: float = 0.0
+    accuracy: float = 0.0
+    precision_defined: bool = True
+    recall_defined: bool = True
+
+
+@dataclass
+class BinaryImage:
+    """BinaryImage, image.hpp:22-28: width x height u8 pixels, 1 = pore."""
+    width: int
+    height: int
+    pixels: np.ndarray
+
+
+def confusion(backend: Backend, pred: BinaryImage, truth: BinaryImage) -> ConfusionCounts:
+    """confusion, metrics.hpp:17-18 / metrics.cpp:8-14, counted on the device;
+    InputError on a shape mismatch as in the reference."""
+    if pred.width != truth.width or pred.height != truth.height:
+        raise InputError("confusion: image dimensions differ")
+    return context_for(backend).confusion(pred.pixels, truth.pixels)
+
+
+def compute_metrics(c: ConfusionCounts) -> Metrics:
+    """compute_metrics, metrics.cpp:16-35 (host arithmetic, same expressions)."""
+    m = Metrics()
+    tp, tn, fp, fn = float(c.tp), float(c.tn), float(c.fp), float(c.fn)
+    if c.tp + c.fp == 0:
+        m.precision_defined = False
+    else:
+        m.precision = tp / (tp + fp)
+    if c.tp + c.fn == 0:
+        m.recall_defined = False
+    else:
+        m.recall = tp / (tp + fn)
+    total = tp + tn + fp + fn
+    m.accuracy = 0.0 if total == 0.0 else (tp + tn) / total
+    return m
+
+
+def porosity(img: BinaryImage) -> float:
+    """porosity, metrics.cpp:37-42: fraction of pixels equal to 1."""
+    px = np.asarray(img.pixels, np.uint8)
+    if px.size == 0:
+        return 0.0
+    return float(int(px.astype(np.uint64).sum())) / float(px.size)
