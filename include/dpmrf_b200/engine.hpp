@@ -366,4 +366,107 @@ inline NeighborhoodSet build_neighborhoods(const dpp::Backend& b, const RegionGr
   return h;
 }
 
+// ---- graph/image.hpp, graph/label_map.hpp value types ----
+struct GrayImage {
+  std::uint32_t width = 0;
+  std::uint32_t height = 0;
+  std::vector<std::uint8_t> pixels;
+  std::size_t size() const { return pixels.size(); }
+};
+struct BinaryImage {
+  std::uint32_t width = 0;
+  std::uint32_t height = 0;
+  std::vector<std::uint8_t> pixels;
+  std::size_t size() const { return pixels.size(); }
+};
+struct LabelMap {
+  std::uint32_t width = 0;
+  std::uint32_t height = 0;
+  std::vector<std::uint32_t> region;
+  std::uint32_t num_regions = 0;  // set by the reference's validate_label_map
+};
+
+// ---- region_graph.hpp:29-30 (built on the device) ----
+inline RegionGraph build_region_graph(const dpp::Backend& b, const GrayImage& image,
+                                      const LabelMap& labels) {
+  if (image.width != labels.width || image.height != labels.height)
+    throw InputError("region graph: image and label map dimensions differ");
+  auto& c = detail::ctx_for(b);
+  std::uint64_t A = 0;
+  throw_status(dpmrf_build_region_graph(c.h, image.width, image.height, image.pixels.data(),
+                                        labels.region.data(), labels.num_regions, &A),
+               "build_region_graph");
+  RegionGraph g;
+  g.num_vertices = labels.num_regions;
+  g.offsets.resize(std::size_t(g.num_vertices) + 1);
+  g.neighbors.resize(A);
+  g.region_mean.resize(g.num_vertices);
+  g.region_size.resize(g.num_vertices);
+  throw_status(dpmrf_get_graph(c.h, nullptr, nullptr, g.offsets.data(), g.neighbors.data(),
+                               g.region_mean.data(), g.region_size.data()),
+               "get_graph");
+  return g;
+}
+
+// ---- cliques.hpp:26 (enumerated on the device) ----
+inline CliqueSet enumerate_maximal_cliques(const dpp::Backend& b, const RegionGraph& g) {
+  auto& c = detail::ctx_for(b);
+  detail::graph(c, g);
+  std::uint64_t C = 0, CS = 0;
+  throw_status(dpmrf_enumerate_maximal_cliques(c.h, &C, &CS), "enumerate_maximal_cliques");
+  CliqueSet out;
+  out.offsets.resize(C + 1);
+  out.members.resize(CS);
+  throw_status(dpmrf_get_cliques(c.h, out.offsets.data(), out.members.data()), "get_cliques");
+  return out;
+}
+
+// ---- eval/metrics.hpp (confusion counted on the device) ----
+struct ConfusionCounts {
+  std::uint64_t tp = 0;
+  std::uint64_t tn = 0;
+  std::uint64_t fp = 0;
+  std::uint64_t fn = 0;
+};
+struct Metrics {
+  double precision = 0.0;
+  double recall = 0.0;
+  double accuracy = 0.0;
+  bool precision_defined = true;
+  bool recall_defined = true;
+};
+
+inline ConfusionCounts confusion(const BinaryImage& pred, const BinaryImage& truth,
+                                 const dpp::Backend& b = dpp::Backend::cuda()) {
+  if (pred.width != truth.width || pred.height != truth.height)
+    throw InputError("confusion: image dimensions differ");
+  auto& c = detail::ctx_for(b);
+  std::uint64_t k[4] = {0, 0, 0, 0};
+  throw_status(dpmrf_confusion(c.h, pred.pixels.size(), pred.pixels.data(), truth.pixels.data(), k),
+               "confusion");
+  return {k[0], k[1], k[2], k[3]};
+}
+
+// metrics.cpp:16-35 (host arithmetic)
+inline Metrics compute_metrics(const ConfusionCounts& c) {
+  Metrics m;
+  const double tp = static_cast<double>(c.tp), tn = static_cast<double>(c.tn);
+  const double fp = static_cast<double>(c.fp), fn = static_cast<double>(c.fn);
+  if (c.tp + c.fp == 0) m.precision_defined = false;
+  else m.precision = tp / (tp + fp);
+  if (c.tp + c.fn == 0) m.recall_defined = false;
+  else m.recall = tp / (tp + fn);
+  const double total = tp + tn + fp + fn;
+  m.accuracy = total == 0.0 ? 0.0 : (tp + tn) / total;
+  return m;
+}
+
+// metrics.cpp:37-42
+inline double porosity(const BinaryImage& img) {
+  if (img.pixels.empty()) return 0.0;
+  std::uint64_t pore = 0;
+  for (std::uint8_t p : img.pixels) pore += p;
+  return static_cast<double>(pore) / static_cast<double>(img.pixels.size());
+}
+
 }  // namespace dpmrf_b200

@@ -170,6 +170,63 @@ int main() {
     CHECK_THROWS_AS(optimize(B, g, hoods, bad), InputError);
     CHECK_THROWS_AS(build_neighborhoods(B, g, cl, 2), InputError);
   }
+  {
+    // graph_test.cpp:215-223 -- a 2x2 block grid is the 4-cycle
+    GrayImage img;
+    img.width = img.height = 4;
+    for (std::uint32_t i = 0; i < 16; ++i) img.pixels.push_back(static_cast<std::uint8_t>(i * 13));
+    LabelMap lm;
+    lm.width = lm.height = 4;
+    lm.num_regions = 4;
+    for (std::uint32_t y = 0; y < 4; ++y)
+      for (std::uint32_t x = 0; x < 4; ++x) lm.region.push_back((y / 2) * 2 + x / 2);
+    const auto rg = build_region_graph(B, img, lm);
+    CHECK(rg.num_vertices == 4);
+    CHECK((rg.offsets == V{0, 2, 4, 6, 8}));
+    CHECK((rg.neighbors == V{1, 2, 0, 3, 0, 3, 1, 2}));
+    CHECK((rg.region_size == V{4, 4, 4, 4}));
+    // graph_test.cpp:225-233 -- uniform image: exact means
+    GrayImage flat = img;
+    flat.pixels.assign(16, 77);
+    for (double m : build_region_graph(B, flat, lm).region_mean) CHECK(m == 77.0);
+    LabelMap bad = lm;
+    bad.width = 2;
+    CHECK_THROWS_AS(build_region_graph(B, img, bad), InputError);
+    // the 4-cycle's maximal cliques are its edges, in lexicographic order
+    const auto cq = enumerate_maximal_cliques(B, rg);
+    CHECK((cq.offsets == V{0, 2, 4, 6, 8}));
+    CHECK((cq.members == V{0, 1, 0, 2, 1, 3, 2, 3}));
+    // K4 plus a pendant vertex: {0,1,2,3} and {3,4} (cliques_test.cpp style)
+    const auto k4 = make_graph(5, {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}, {3, 4}});
+    const auto ck = enumerate_maximal_cliques(B, k4);
+    CHECK((ck.offsets == V{0, 4, 6}));
+    CHECK((ck.members == V{0, 1, 2, 3, 3, 4}));
+  }
+  {
+    // eval_test.cpp:149-210 -- confusion and metrics
+    auto bin = [](std::uint32_t w, std::uint32_t h, std::vector<std::uint8_t> px) {
+      BinaryImage b;
+      b.width = w;
+      b.height = h;
+      b.pixels = std::move(px);
+      return b;
+    };
+    const auto truth = bin(4, 1, {1, 1, 0, 0});
+    const auto c = confusion(bin(4, 1, {1, 0, 0, 1}), truth, B);
+    CHECK(c.tp == 1 && c.fn == 1 && c.tn == 1 && c.fp == 1);
+    const auto perfect = confusion(truth, truth, B);
+    CHECK(perfect.tp == 2 && perfect.tn == 2 && perfect.fp == 0 && perfect.fn == 0);
+    const auto inv = confusion(bin(4, 1, {0, 0, 1, 1}), truth, B);
+    CHECK(inv.tp == 0 && inv.tn == 0 && inv.fp == 2 && inv.fn == 2);
+    CHECK_THROWS_AS(confusion(truth, bin(2, 2, {1, 1, 0, 0}), B), InputError);
+    const auto m = compute_metrics(c);
+    CHECK(m.precision == 0.5 && m.recall == 0.5 && m.accuracy == 0.5);
+    ConfusionCounts none;
+    none.tn = 3;
+    const auto mn = compute_metrics(none);
+    CHECK(!mn.precision_defined && !mn.recall_defined && mn.accuracy == 1.0);
+    CHECK(porosity(truth) == 0.5);
+  }
   if (failures) {
     std::fprintf(stderr, "%d check(s) failed\n", failures);
     return 1;
