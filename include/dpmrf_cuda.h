@@ -169,6 +169,17 @@ dpmrf_status dpmrf_make_phantom(dpmrf_context* ctx, const dpmrf_phantom_spec* sp
 dpmrf_status dpmrf_oversegment(dpmrf_context* ctx, uint32_t block, int32_t brick,
                                uint32_t* num_regions, uint32_t* region);
 
+/* validate_label_map, proj/src/graph/label_map.cpp:38-78 (called by
+ * read_rlm, :131), on the device: every id in [0, max] must be used and every
+ * region must be one 4-connected component.  region: width*height host ids
+ * (the size check of the reference is the caller's: the buffer IS w*h).  On
+ * success *num_regions = max id + 1; otherwise DPMRF_INPUT_ERROR with the
+ * reference's message ("label map: empty", "label map: region id K unused" for
+ * the lowest unused K, "label map: region K is not 4-connected" for the region
+ * of the first pixel in scan order outside its region's first component). */
+dpmrf_status dpmrf_validate_label_map(dpmrf_context* ctx, uint32_t width, uint32_t height,
+                                      const uint32_t* region, uint32_t* num_regions);
+
 /* ---- evaluation ---------------------------------
  * confusion(pred, truth), proj/include/dpmrf/eval/metrics.hpp:17-18 and
  * proj/src/eval/metrics.cpp:8-14 (simd::confusion_u8, scalar_kernels.cpp:48-63)

@@ -676,6 +676,80 @@ void orc_labels_to_mask(uint64_t n, const uint32_t *region, const uint32_t *labe
   for (uint64_t i = 0; i < n; ++i) mask[i] = labels[region[i]] == pore ? 1 : 0;
 }
 
+/* validate_label_map, label_map.cpp:38-78: serial union-find over same-id
+ * right / down pixel pairs (:60-67), roots compared per region in scan order
+ * (:68-76).  Returns 0 and *num_regions, or INPUT_ERROR with *detail = the
+ * lowest unused id (*kind = 1) or the region that is not 4-connected
+ * (*kind = 2); *kind = 3 for an empty map. */
+static uint32_t uf_find(uint32_t *p, uint32_t x) {
+  while (p[x] != x) {
+    p[x] = p[p[x]];
+    x = p[x];
+  }
+  return x;
+}
+
+int orc_validate_label_map(uint32_t w, uint32_t h, const uint32_t *region, uint32_t *num_regions,
+                           int *kind, uint32_t *detail) {
+  const uint64_t n = (uint64_t)w * h;
+  *kind = 0;
+  if (n == 0) {
+    *kind = 3;
+    return ORC_INPUT_ERROR;
+  }
+  uint32_t max_id = 0;
+  for (uint64_t i = 0; i < n; ++i)
+    if (region[i] > max_id) max_id = region[i];
+  const uint64_t num = (uint64_t)max_id + 1;
+  uint8_t *used = (uint8_t *)calloc(num, 1);
+  uint32_t *parent = (uint32_t *)malloc(n * sizeof(uint32_t));
+  uint32_t *root_of = (uint32_t *)malloc(num * sizeof(uint32_t));
+  int rc = 0;
+  if (!used || !parent || !root_of) {
+    rc = ORC_NOMEM;
+    goto done;
+  }
+  for (uint64_t i = 0; i < n; ++i) used[region[i]] = 1;
+  for (uint64_t id = 0; id < num; ++id)
+    if (!used[id]) {
+      *kind = 1;
+      *detail = (uint32_t)id;
+      rc = ORC_INPUT_ERROR;
+      goto done;
+    }
+  for (uint64_t i = 0; i < n; ++i) parent[i] = (uint32_t)i;
+  for (uint32_t y = 0; y < h; ++y)
+    for (uint32_t x = 0; x < w; ++x) {
+      const uint64_t i = (uint64_t)y * w + x;
+      if (x + 1 < w && region[i] == region[i + 1]) {
+        const uint32_t a = uf_find(parent, (uint32_t)i), b = uf_find(parent, (uint32_t)(i + 1));
+        if (a != b) parent[b] = a;
+      }
+      if (y + 1 < h && region[i] == region[i + w]) {
+        const uint32_t a = uf_find(parent, (uint32_t)i), b = uf_find(parent, (uint32_t)(i + w));
+        if (a != b) parent[b] = a;
+      }
+    }
+  for (uint64_t id = 0; id < num; ++id) root_of[id] = 0xFFFFFFFFu;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t id = region[i], r = uf_find(parent, (uint32_t)i);
+    if (root_of[id] == 0xFFFFFFFFu) {
+      root_of[id] = r;
+    } else if (root_of[id] != r) {
+      *kind = 2;
+      *detail = id;
+      rc = ORC_INPUT_ERROR;
+      goto done;
+    }
+  }
+  *num_regions = (uint32_t)num;
+done:
+  free(used);
+  free(parent);
+  free(root_of);
+  return rc;
+}
+
 /* ------------------------------------------------------------------ */
 /* Structure builders.                      */
 /* Outputs of variable length are malloc'd; release with orc_free.      */

@@ -200,6 +200,8 @@ class _COracle:
         L.orc_free.argtypes = [VP]
         L.orc_confusion.argtypes = [U64, u8p, u8p, ct.POINTER(U64)]
         L.orc_labels_to_mask.argtypes = [U64, u32p, u32p, f64p, u8p]
+        L.orc_validate_label_map.argtypes = [U32, U32, u32p, ct.POINTER(U32),
+                                             ct.POINTER(ct.c_int), ct.POINTER(U32)]
         for fn in (L.orc_optimize, L.orc_optimize_reference):
             fn.argtypes = [U32, u32p, u32p, f64p, U64, u32p, u32p, ct.POINTER(Config), ct.c_int,
                            ct.c_int, u32p, f64p, f64p, ct.POINTER(_Trace)]
@@ -369,6 +371,23 @@ class _COracle:
         self.L.orc_confusion(a.size, a, b, c)
         return tuple(int(x) for x in c)
 
+    def validate_label_map(self, w, h, region):
+        """label_map.cpp:38-78 -> num_regions, or the reference's InputError
+        message (as a string) when the map is invalid."""
+        reg = _a(region, np.uint32) if len(region) else np.zeros(1, np.uint32)
+        num, kind, det = U32(0), ct.c_int(0), U32(0)
+        rc = self.L.orc_validate_label_map(w, h, reg, ct.byref(num), ct.byref(kind),
+                                           ct.byref(det))
+        if rc == 0:
+            return num.value
+        if kind.value == 1:
+            return f"label map: region id {det.value} unused"
+        if kind.value == 2:
+            return f"label map: region {det.value} is not 4-connected"
+        if kind.value == 3:
+            return "label map: empty"
+        raise OracleError(rc, "validate_label_map")
+
     def labels_to_mask(self, region, labels, mu):
         """main.cpp:157-165 -> u8 mask."""
         reg = _a(region, np.uint32)
@@ -516,6 +535,8 @@ class _Ref:
         L.ref_hw_threads.restype = U32
         L.ref_confusion.argtypes = [U32, U32, u8p, U32, U32, u8p, ct.POINTER(U64)]
         L.ref_compute_metrics.argtypes = [ct.POINTER(U64), ct.POINTER(F64), ct.POINTER(ct.c_int)]
+        L.ref_validate_label_map.argtypes = [U32, U32, u32p, U64, ct.POINTER(U32), ct.c_char_p,
+                                             U64]
         L.ref_porosity.argtypes = [U32, U32, u8p]
         L.ref_porosity.restype = F64
 
@@ -586,6 +607,13 @@ class _Ref:
         d = (ct.c_int * 2)()
         self.L.ref_compute_metrics(c, m, d)
         return m[0], m[1], m[2], bool(d[0]), bool(d[1])
+
+    def validate_label_map(self, w, h, region):
+        """dpmrf::validate_label_map -> num_regions, or its what() string."""
+        reg = _a(region, np.uint32) if len(region) else np.zeros(1, np.uint32)
+        num, msg = U32(0), ct.create_string_buffer(256)
+        rc = self.L.ref_validate_label_map(w, h, reg, len(region), ct.byref(num), msg, 256)
+        return num.value if rc == 0 else msg.value.decode()
 
     def porosity(self, w, h, pixels):
         a = _a(pixels, np.uint8) if len(pixels) else np.zeros(1, np.uint8)

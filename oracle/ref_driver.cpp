@@ -22,6 +22,7 @@
 #include <functional>
 #include <map>
 #include <stdexcept>
+#include <string>
 #include <thread>
 #include <utility>
 #include <vector>
@@ -681,6 +682,31 @@ void ref_compute_metrics(const std::uint64_t* counts, double* out, int* defined)
   out[2] = m.accuracy;
   defined[0] = m.precision_defined;
   defined[1] = m.recall_defined;
+}
+
+// dpmrf::validate_label_map (label_map.cpp:38-78); msg receives what() on failure.
+int ref_validate_label_map(std::uint32_t w, std::uint32_t h, const std::uint32_t* region,
+                           std::uint64_t n, std::uint32_t* num_regions, char* msg,
+                           std::uint64_t msg_len) {
+  std::string what;
+  const int rc = guarded([&] {
+    LabelMap m;
+    m.width = w;
+    m.height = h;
+    m.region.assign(region, region + n);
+    try {
+      validate_label_map(m);
+    } catch (const std::exception& e) {
+      what = e.what();
+      throw;
+    }
+    *num_regions = m.num_regions;
+  });
+  if (msg && msg_len) {
+    std::strncpy(msg, what.c_str(), msg_len - 1);
+    msg[msg_len - 1] = 0;
+  }
+  return rc;
 }
 
 double ref_porosity(std::uint32_t w, std::uint32_t h, const std::uint8_t* px) {

@@ -76,6 +76,7 @@ CUDA_API = [
     ("dpmrf_make_phantom", ST, [VP, ct.POINTER(CPhantomSpec), VP, VP, ct.POINTER(U32)]),
     ("dpmrf_oversegment", ST, [VP, U32, I32, ct.POINTER(U32), VP]),
     ("dpmrf_confusion", ST, [VP, U64, VP, VP, VP]),
+    ("dpmrf_validate_label_map", ST, [VP, U32, U32, VP, ct.POINTER(U32)]),
     ("dpmrf_segment_mask", ST, [VP, U32, VP, VP, VP, VP]),
     ("dpmrf_build_region_graph_resident", ST, [VP, ct.POINTER(U64)]),
     ("dpmrf_build_region_graph", ST, [VP, U32, U32, VP, VP, U32, ct.POINTER(U64)]),

@@ -395,6 +395,20 @@ extern "C" dpmrf_status dpmrf_make_phantom(dpmrf_context* ctx, const dpmrf_phant
   });
 }
 
+extern "C" dpmrf_status dpmrf_validate_label_map(dpmrf_context* ctx, uint32_t width,
+                                                 uint32_t height, const uint32_t* region,
+                                                 uint32_t* num_regions) {
+  return guarded([&] {
+    ContextLock lock_(ctx);
+    const uint64_t n = uint64_t(width) * height;
+    need(num_regions && (n == 0 || region), DPMRF_INVALID_ARGUMENT, "null argument");
+    ctx->bind();
+    uint32_t* d = ctx->lm_region.ensure(n ? n : 1);
+    if (n) CK(cudaMemcpyAsync(d, region, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    *num_regions = validate_label_map_device(ctx, width, height, d);
+  });
+}
+
 extern "C" dpmrf_status dpmrf_confusion(dpmrf_context* ctx, uint64_t n, const uint8_t* pred,
                                         const uint8_t* truth, uint64_t counts[4]) {
   return guarded([&] {

@@ -35,6 +35,9 @@ struct dpmrf_context {
   dpmrf_b200::DevBuf<uint64_t> eval_counts;     // {tp, tn, fp, fn}
   dpmrf_b200::DevBuf<uint8_t> eval_a, eval_b;   // uploaded masks / the written-back mask
   dpmrf_b200::DevBuf<uint32_t> eval_labels;
+  // validate_label_map scratch (labelmap.cu)
+  dpmrf_b200::DevBuf<uint32_t> lm_parent, lm_state, lm_first, lm_region;
+  dpmrf_b200::DevBuf<uint8_t> lm_used;
   uint32_t img_w = 0, img_h = 0, img_regions = 0;  // resident image / region map (synth.cu)
   bool has_image = false, has_regions = false;
   dpmrf_b200::HostBuf<unsigned long long> h_syn;
@@ -235,4 +238,8 @@ void confusion_device(dpmrf_context* ctx, const uint8_t* pred, const uint8_t* tr
                       uint64_t counts[4]);
 void segment_mask_device(dpmrf_context* ctx, const uint32_t* labels, uint32_t pore,
                          uint8_t* mask, bool with_truth, uint64_t counts[4]);
+// validate_label_map (labelmap.cu) of a device label map: returns num_regions
+// or fails with the reference's InputError message.
+uint32_t validate_label_map_device(dpmrf_context* ctx, uint32_t width, uint32_t height,
+                                   const uint32_t* region);
 }  // namespace dpmrf_b200

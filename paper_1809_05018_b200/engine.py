@@ -327,6 +327,17 @@ class Context:
         S = self.build_neighborhoods_resident()
         return {"regions": R, "adjacency": A, "cliques": C, "slots": S, "host_ties": ties}
 
+    def validate_label_map(self, width: int, height: int, region) -> int:
+        """validate_label_map (label_map.cpp:38-78) on the device -> num_regions;
+        InputError with the reference's message otherwise."""
+        reg = np.ascontiguousarray(region, np.uint32)
+        if reg.size != width * height:
+            raise InputError("label map: size does not match dimensions")
+        num = ct.c_uint32(0)
+        _check(self._lib.dpmrf_validate_label_map(self.h, width, height, N.ptr(reg),
+                                                  ct.byref(num)), "validate_label_map")
+        return num.value
+
     # -- evaluation on the device (SURVEY.md §8(f) item 3) --
     def confusion(self, pred, truth) -> "ConfusionCounts":
         """confusion_u8 (metrics.cpp:8-14, scalar_kernels.cpp:48-63) of two
@@ -832,3 +843,61 @@ def porosity(img: BinaryImage) -> float:
     if px.size == 0:
         return 0.0
     return float(int(px.astype(np.uint64).sum())) / float(px.size)
+
+
+# ---- label maps and RLM1 I/O (proj/include/dpmrf/graph/label_map.hpp) ------------------
+@dataclass
+class LabelMap:
+    """LabelMap, label_map.hpp:12-17: row-major region ids; num_regions is set
+    by validation."""
+    width: int
+    height: int
+    region: np.ndarray
+    num_regions: int = 0
+
+
+def validate_label_map(m: LabelMap, backend: Backend = Backend.cuda()) -> LabelMap:
+    """validate_label_map (label_map.cpp:38-78), on the device; fills num_regions."""
+    if np.asarray(m.region).size != m.width * m.height:  # (:40, before any device work)
+        raise InputError("label map: size does not match dimensions")
+    m.num_regions = context_for(backend).validate_label_map(m.width, m.height, m.region)
+    return m
+
+
+def read_rlm(path: str, backend: Backend = Backend.cuda()) -> LabelMap:
+    """read_rlm, label_map.cpp:114-133: 'RLM1', u32le width, height, then
+    width*height u32le ids; InputError on a bad magic, zero dimension, an image
+    over 2^31 pixels or truncation; the map is validated (on the device)."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise InputError("cannot open " + path) from None
+    if len(data) < 4 or data[:4] != b"RLM1":
+        raise InputError(path + ": not an RLM1 file")
+    if len(data) < 12:
+        raise InputError(path + ": truncated")
+    w, h = (int(x) for x in np.frombuffer(data, "<u4", 2, 4))
+    if w == 0 or h == 0:
+        raise InputError(path + ": zero dimension")
+    n = w * h
+    if n > (1 << 31):
+        raise InputError(path + ": image too large")
+    if len(data) < 12 + 4 * n:
+        raise InputError(path + ": truncated")
+    region = np.frombuffer(data, "<u4", n, 12).astype(np.uint32)
+    return validate_label_map(LabelMap(w, h, region), backend)
+
+
+def write_rlm(m: LabelMap, path: str) -> None:
+    """write_rlm, label_map.cpp:135-145."""
+    region = np.asarray(m.region)
+    if region.size != m.width * m.height:
+        raise InputError("rlm write: region buffer does not match dimensions")
+    try:
+        with open(path, "wb") as f:
+            f.write(b"RLM1")
+            f.write(np.array([m.width, m.height], "<u4").tobytes())
+            f.write(region.astype("<u4").tobytes())
+    except OSError:
+        raise InputError("rlm write failed: " + path) from None

@@ -88,6 +88,14 @@ def main():
                 for k, a, b in (("phantom", t0, t1), ("oversegment", t1, t2), ("graph", t2, t3),
                                 ("cliques", t3, t4), ("hoods", t4, t5)):
                     syn[k].append((b - a) * 1e3)
+        # validate_label_map of the (host) label map on the device, H2D included
+        val = []
+        for rep in range(args.reps + 1):
+            t0 = time.perf_counter()
+            nreg = ctx.validate_label_map(size, size, reg)
+            if rep:
+                val.append((time.perf_counter() - t0) * 1e3)
+        assert nreg == R
         g = ctx.get_graph()
         cl = ctx.get_cliques()
         same = bool(np.array_equal(g.offsets, g_host.offsets) and
@@ -102,7 +110,8 @@ def main():
                 "device_equals_host_builder": same,
                 "h2d_bytes": 5 * size * size,
                 "device_synthetic_ms": {k: statistics.median(v) for k, v in syn.items()},
-                "device_synthetic_host_ties": ties}
+                "device_synthetic_host_ties": ties,
+                "device_validate_label_map_ms": statistics.median(val)}
         if name in args.ref_configs.split(","):
             import oracle
             if oracle.ref_available():
@@ -114,6 +123,9 @@ def main():
                     line[f"reference_s_threads{threads}"] = {"graph": t[0], "cliques": t[1],
                                                              "hoods": t[2]}
                     del p
+                t0 = time.perf_counter()
+                assert ref.validate_label_map(size, size, reg) == R
+                line["reference_validate_label_map_s"] = time.perf_counter() - t0
         print(json.dumps(line), flush=True)
     ctx.close()
 
