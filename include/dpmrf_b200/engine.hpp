@@ -386,6 +386,17 @@ struct LabelMap {
   std::uint32_t num_regions = 0;  // set by the reference's validate_label_map
 };
 
+// ---- label_map.hpp validate_label_map (label_map.cpp:38-78, on the device) ----
+inline void validate_label_map(LabelMap& map, const dpp::Backend& b = dpp::Backend::cuda()) {
+  if (map.region.size() != std::size_t(map.width) * map.height)
+    throw InputError("label map: size does not match dimensions");
+  auto& c = detail::ctx_for(b);
+  std::uint32_t num = 0;
+  throw_status(dpmrf_validate_label_map(c.h, map.width, map.height, map.region.data(), &num),
+               "validate_label_map");
+  map.num_regions = num;
+}
+
 // ---- region_graph.hpp:29-30 (built on the device) ----
 inline RegionGraph build_region_graph(const dpp::Backend& b, const GrayImage& image,
                                       const LabelMap& labels) {

@@ -180,6 +180,27 @@ int main() {
     lm.num_regions = 4;
     for (std::uint32_t y = 0; y < 4; ++y)
       for (std::uint32_t x = 0; x < 4; ++x) lm.region.push_back((y / 2) * 2 + x / 2);
+    // graph_test.cpp:160-190 -- validation
+    LabelMap v = lm;
+    v.num_regions = 0;
+    validate_label_map(v, B);
+    CHECK(v.num_regions == 4);
+    auto lm_of = [](std::uint32_t w, std::uint32_t h, V r) {
+      LabelMap m;
+      m.width = w;
+      m.height = h;
+      m.region = std::move(r);
+      return m;
+    };
+    LabelMap ok = lm_of(2, 2, {0, 0, 1, 1});
+    validate_label_map(ok, B);
+    CHECK(ok.num_regions == 2);
+    LabelMap gap = lm_of(2, 1, {0, 2}), split = lm_of(3, 1, {0, 1, 0});
+    LabelMap diag = lm_of(2, 2, {0, 1, 1, 0}), shortm = lm_of(2, 2, {0, 0, 0});
+    CHECK_THROWS_AS(validate_label_map(gap, B), InputError);
+    CHECK_THROWS_AS(validate_label_map(split, B), InputError);
+    CHECK_THROWS_AS(validate_label_map(diag, B), InputError);
+    CHECK_THROWS_AS(validate_label_map(shortm, B), InputError);
     const auto rg = build_region_graph(B, img, lm);
     CHECK(rg.num_vertices == 4);
     CHECK((rg.offsets == V{0, 2, 4, 6, 8}));
