@@ -141,7 +141,8 @@ void dpmrf_context::prepare() {
     const uint32_t* hs = h_err + 2;
     const uint32_t* so = series_alias ? h_off.get() : s_off_buf.get();
     if (hs[1] <= 32767u) adj_k = hs[0] <= 4 ? 4 : (hs[0] <= 8 ? 8 : 0);
-    if (hs[3] < 0xFFFFu && Hs > 0) hood_k = hs[2] <= 9 ? 8 : (hs[2] <= 17 ? 16 : 0);
+    if (hs[3] < 0xFFFFu && Hs > 0)
+      hood_k = hs[2] <= 9 ? 8 : (hs[2] <= 13 && use_k12 ? 12 : (hs[2] <= 17 ? 16 : 0));
     if (adj_k) launch_pack_adjacency(g_off.get(), g_nbr.get(), R, adj_k,
                                      adj_pk.ensure(uint64_t(R) * adj_k), stream);
     if (hood_k) launch_pack_hoods(so, h_mem.get(), Hs, hood_k, hood_base.ensure(Hs),
@@ -183,6 +184,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     if (const char* e = std::getenv("DPMRF_HOST_LOG")) c->use_device_loop = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_CSR")) c->use_packed = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_DICT")) c->use_dict = e[0] == '1';
+    if (const char* e = std::getenv("DPMRF_NO_K12")) c->use_k12 = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_FLOW")) c->use_flow = e[0] == '1';
     if (const char* e = std::getenv("DPMRF_FLOW_SLEEP")) c->flow_sleep_ns = uint32_t(std::atoi(e));
     if (const char* e = std::getenv("DPMRF_UNFUSED")) c->use_fused = e[0] == '0';

@@ -1354,6 +1354,7 @@ void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
                       const double* minE_prev, double* minE_cur, int t, int map_max,
                       cudaStream_t s, const ScatterArgs* sc) {
   const int sel = (a.M == 2 ? 0 : 4) + (a.adj_k == 8 ? 2 : 0) + (a.hood_k == 16 ? 1 : 0);
+  const bool k12 = a.hood_k == 12;  // brick hoods (<= 13 slots)
   // Two vertices per thread on large graphs (+4% at 16384^2: more loads in
   // flight per thread); one on small ones, where the extra per-thread
   // latency shows (-3% at 2560^2).
@@ -1376,6 +1377,17 @@ void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
 #define MF(MT, KV, KH) MF4(MT, KV, KH, 1)
   if (a.M == 5 && a.adj_k == 8 && a.hood_k == 16) {  // config C's layout: label loop unrolled
     MF(5, 8, 16);
+    return;
+  }
+  if (k12) {
+    if (a.M == 5 && a.adj_k == 8) MF(5, 8, 12);  // config C
+    else if (a.M == 2) {
+      if (a.adj_k == 4) MF(2, 4, 12);
+      else MF(2, 8, 12);
+    } else {
+      if (a.adj_k == 4) MF(0, 4, 12);
+      else MF(0, 8, 12);
+    }
     return;
   }
   switch (sel) {
@@ -1439,6 +1451,7 @@ void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s) {
   const bool whole = a.h_begin == 0 && a.h_end == a.Hs;
   if (a.hood_k && !a.staged) {
     if (a.hood_k == 8) launch_pdl(k_hood_packed<8>, g, blk, 0, s, a, t);
+    else if (a.hood_k == 12) launch_pdl(k_hood_packed<12>, g, blk, 0, s, a, t);
     else launch_pdl(k_hood_packed<16>, g, blk, 0, s, a, t);
     return;
   }
@@ -1595,6 +1608,33 @@ __global__ void __launch_bounds__(kVtxThreads)
   vertex_packed_body<MT, K>(a, lab_in, lab_out, a.minE, t, blockIdx.x, t);
 }
 
+// A hood's K u16 deltas as K/2 words: 16-byte loads for K = 8 / 16, three
+// 8-byte loads for K = 12 (rows of 24 bytes are only 8-byte aligned).
+template <int K>
+__device__ __forceinline__ void load_hood_row(const uint16_t* __restrict__ row,
+                                              uint32_t (&u)[K / 2]) {
+  if constexpr (K % 8 == 0) {
+    const uint4* src = reinterpret_cast<const uint4*>(row);
+#pragma unroll
+    for (int q = 0; q < K / 8; ++q) {
+      const uint4 w = src[q];
+      u[4 * q] = w.x;
+      u[4 * q + 1] = w.y;
+      u[4 * q + 2] = w.z;
+      u[4 * q + 3] = w.w;
+    }
+  } else {
+    static_assert(K == 12, "hood pack width");
+    const uint2* src = reinterpret_cast<const uint2*>(row);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const uint2 w = src[q];
+      u[2 * q] = w.x;
+      u[2 * q + 1] = w.y;
+    }
+  }
+}
+
 // One hood's sum (left fold of its members' minima in slot order,
 // engine.cpp:147-152) + record + window test (engine.cpp:154-169); returns 1
 // when the hood is not converged.  CG: minima read around L1 (written by
@@ -1659,29 +1699,22 @@ template <int K, bool DICT = false>
 __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
                                                  const double* __restrict__ minE, int t,
                                                  uint32_t blk, int skip_t) {
-  static_assert(K == 8 || K == 16, "hood pack width");
+  static_assert(K == 8 || K == 12 || K == 16, "hood pack width");
   const uint64_t h = a.h_begin + uint64_t(blk) * kHoodThreads + threadIdx.x;
   const bool live = h < a.h_end;
   uint32_t base = 0;
   uint32_t u[K / 2];
   if (live) {
-    const uint4* src;
+    const uint16_t* row;
     if constexpr (DICT) {
       const uint32_t c = a.hcode[h];
       base = c & 0xFFFFFFu;
-      src = reinterpret_cast<const uint4*>(a.hood_pat + (c >> 24) * K);
+      row = a.hood_pat + (c >> 24) * K;
     } else {
       base = a.hood_base[h];
-      src = reinterpret_cast<const uint4*>(a.hood_pk + h * K);
+      row = a.hood_pk + h * K;
     }
-#pragma unroll
-    for (int q = 0; q < K / 8; ++q) {
-      const uint4 w = src[q];
-      u[4 * q] = w.x;
-      u[4 * q + 1] = w.y;
-      u[4 * q + 2] = w.z;
-      u[4 * q + 3] = w.w;
-    }
+    load_hood_row<K>(row, u);
   }
   pdl_wait();
   int not_conv = 0;
@@ -2203,6 +2236,8 @@ void launch_pack_hoods(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs
   if (!Hs) return;
   if (k == 8)
     k_pack_hoods<8><<<grid_for(Hs, 256), 256, 0, s>>>(s_off, h_mem, Hs, base, out);
+  else if (k == 12)
+    k_pack_hoods<12><<<grid_for(Hs, 256), 256, 0, s>>>(s_off, h_mem, Hs, base, out);
   else
     k_pack_hoods<16><<<grid_for(Hs, 256), 256, 0, s>>>(s_off, h_mem, Hs, base, out);
   CK_LAUNCH();
@@ -2285,6 +2320,8 @@ void launch_dict_hoods(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs
   uint32_t* p = reinterpret_cast<uint32_t*>(pat);
   if (k == 8)
     k_dict_hoods<8><<<grid_for(Hs, 256), 256, 0, s>>>(s_off, h_mem, Hs, ws, hcode, p);
+  else if (k == 12)
+    k_dict_hoods<12><<<grid_for(Hs, 256), 256, 0, s>>>(s_off, h_mem, Hs, ws, hcode, p);
   else
     k_dict_hoods<16><<<grid_for(Hs, 256), 256, 0, s>>>(s_off, h_mem, Hs, ws, hcode, p);
   CK_LAUNCH();

@@ -316,12 +316,13 @@ def test_concurrent_calls_on_one_context_serialize(ctx):
     assert not errors, errors
 
 
-@pytest.mark.parametrize("env", ["DPMRF_FLOW", "DPMRF_DICT"])
+@pytest.mark.parametrize("env", ["DPMRF_FLOW", "DPMRF_DICT", "DPMRF_NO_K12"])
 def test_opt_in_layouts_agree(env, monkeypatch):
     """The measured-and-rejected variants stay correct: the dataflow MAP loop
     (DPMRF_FLOW=1: one launch per EM, tiles synchronised by progress flags,
-    early exit decided two iterations behind) and the dictionary-coded
-    structure (DPMRF_DICT=1) reproduce the fixtures and the default path."""
+    early exit decided two iterations behind), the dictionary-coded structure
+    (DPMRF_DICT=1) and 16-slot rows for brick hoods (DPMRF_NO_K12=1) reproduce
+    the fixtures and the default path."""
     from paper_1809_05018_b200 import inputs
     monkeypatch.setenv(env, "1")
     c = E.Context(0)
@@ -337,8 +338,8 @@ def test_opt_in_layouts_agree(env, monkeypatch):
                     f.check(r)
                 if env == "DPMRF_FLOW" and name != "m5_128_brick8":
                     assert r.stats["persistent"] == 2  # the flow kernel ran
-        for size, seed in ((1024, 3), (2560, 42)):
-            sl = inputs.synthetic_slice(size, 8, seed=seed)
+        for size, seed, brick in ((1024, 3, False), (2560, 42, False), (1000, 5, True)):
+            sl = inputs.synthetic_slice(size, 8, seed=seed, brick=brick)
             for ctx_ in (c, base):
                 ctx_.set_graph(sl.graph)
                 ctx_.build_neighborhoods(sl.cliques)
