@@ -145,8 +145,11 @@ void dpmrf_context::prepare() {
       hood_k = hs[2] <= 9 ? 8 : (hs[2] <= 13 && use_k12 ? 12 : (hs[2] <= 17 ? 16 : 0));
     if (adj_k) launch_pack_adjacency(g_off.get(), g_nbr.get(), R, adj_k,
                                      adj_pk.ensure(uint64_t(R) * adj_k), stream);
-    if (hood_k) launch_pack_hoods(so, h_mem.get(), Hs, hood_k, hood_base.ensure(Hs),
-                                  hood_pk.ensure(Hs * hood_k), stream);
+    // (rows padded to whole 256-hood tiles: the streamed hood pass copies
+    // full tiles with cp.async.bulk)
+    const uint64_t Hp = (Hs + 255) / 256 * 256;
+    if (hood_k) launch_pack_hoods(so, h_mem.get(), Hs, hood_k, hood_base.ensure(Hp),
+                                  hood_pk.ensure(Hp * hood_k), stream);
     // dictionary form (MapArgs::vcode): one more pass and a 16-byte read-back
     if (use_dict && adj_k && hood_k && R <= (1u << 24)) {
       const size_t w = dict_ws_words();
@@ -185,6 +188,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     if (const char* e = std::getenv("DPMRF_CSR")) c->use_packed = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_DICT")) c->use_dict = e[0] == '1';
     if (const char* e = std::getenv("DPMRF_NO_K12")) c->use_k12 = e[0] == '0';
+    if (const char* e = std::getenv("DPMRF_STREAM")) c->stream_hb = std::atoi(e);
     if (const char* e = std::getenv("DPMRF_FLOW")) c->use_flow = e[0] == '1';
     if (const char* e = std::getenv("DPMRF_FLOW_SLEEP")) c->flow_sleep_ns = uint32_t(std::atoi(e));
     if (const char* e = std::getenv("DPMRF_UNFUSED")) c->use_fused = e[0] == '0';
@@ -635,6 +639,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     a.hood_k = packed ? ctx->hood_k : 0;
     a.hood_base = ctx->hood_base.get();
     a.hood_pk = ctx->hood_pk.get();
+    a.stream_hb = ctx->stream_hb;
     if (packed && ctx->dict_ok) {
       a.vcode = ctx->vcode.get();
       a.adj_pat = ctx->adj_pat.get();
@@ -866,6 +871,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       key.p2[4] = a.hood_base;
       key.p2[5] = a.vcode;
       key.p2[6] = a.hcode;
+      key.p2[7] = reinterpret_cast<const void*>(uintptr_t(a.stream_hb));
       key.layout = a.adj_k * 100 + a.hood_k + flow_hp * 100000;
       if (!ctx->graph_valid || std::memcmp(&key, &ctx->graph_key, sizeof key) != 0) {
         ctx->drop_graphs();

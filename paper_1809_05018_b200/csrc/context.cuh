@@ -178,7 +178,8 @@ struct dpmrf_context {
 
   // ---- packed static structure (engine.cuh MapArgs::adj_k / hood_k) ----
   bool use_packed = true;
-  bool use_k12 = true;  // 12-slot hood rows for <= 13-slot hoods (DPMRF_NO_K12=1: 16)
+  bool use_k12 = true;
+  int stream_hb = 0;    // streamed hood pass blocks per SM (DPMRF_STREAM; 0 = off)  // 12-slot hood rows for <= 13-slot hoods (DPMRF_NO_K12=1: 16)
   int adj_k = 0, hood_k = 0;
   dpmrf_b200::DevBuf<int16_t> adj_pk;
   dpmrf_b200::DevBuf<uint32_t> hood_base;

@@ -1341,7 +1341,13 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
                 uint32_t nh, uint32_t nv, ScatterArgs sc);
+template <int MT, int KV, int KH, int VP>
+__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
+    k_map_fused_stream(MapArgs a, const uint8_t* __restrict__ lab_in,
+                       uint8_t* __restrict__ lab_out, const double* __restrict__ minE_prev,
+                       double* __restrict__ minE_cur, int t, uint32_t nh, uint32_t nv);
 }  // namespace
+
 
 bool map_fused_supported(const MapArgs& a) { return a.adj_k && a.hood_k && !a.staged; }
 
@@ -1367,6 +1373,20 @@ void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
   const ScatterArgs scv = tail ? *sc : ScatterArgs{};
   const size_t smem = tail ? scatter_small_smem(sc->M) : 0;
   const dim3 g(nh + nv + ns), blk(kVtxThreads);
+  // streamed hood pass (opt-in): large graphs, plain packed rows, no tail
+  const int shb = a.stream_hb;
+  if (shb > 0 && !tail && !a.vcode && a.M == 2 && a.adj_k == 4 && a.hood_k == 8) {
+    const uint32_t tiles = t >= 1 ? grid_for(a.h_end - a.h_begin, kHoodThreads) : 0u;
+    const uint32_t nhs = std::min<uint32_t>(tiles, uint32_t(shb) * kNumSMs);
+    const dim3 gs(nhs + nv);
+    if (vp == 2)
+      launch_pdl(k_map_fused_stream<2, 4, 8, 2>, gs, blk, 0, s, a, lab_in, lab_out, minE_prev,
+                 minE_cur, t, nhs, nv);
+    else
+      launch_pdl(k_map_fused_stream<2, 4, 8, 1>, gs, blk, 0, s, a, lab_in, lab_out, minE_prev,
+                 minE_cur, t, nhs, nv);
+    return;
+  }
   // dictionary-coded structure when both dictionaries fit (MapArgs::vcode)
   const bool dict = a.vcode && a.hcode;
 #define MF4(MT, KV, KH, VP)                                                              \
@@ -2029,6 +2049,121 @@ __global__ void k_fill_pairs(uint32_t* p, uint64_t n) {
     p[2 * i] = 0xFFFFFFFFu;
     p[2 * i + 1] = 0;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Streamed hood pass (opt-in): the fused launch's hood blocks become
+// persistent (G per SM-slot budget), each looping over 256-hood tiles; the
+// next tile's packed rows (first members + deltas, two contiguous ranges)
+// are fetched by one thread with cp.async.bulk into the other half of a
+// double buffer, completion tracked by an mbarrier with expect_tx -- the
+// static structure's DRAM latency overlaps the current tile's gathers.
+// Arithmetic: hood_eval, unchanged.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  const uint64_t t0 = global_ns();
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+    if (!done && global_ns() - t0 > 2000000000ull) __trap();
+  }
+}
+
+template <int K>
+struct StreamSmem {
+  uint32_t base[2][kHoodThreads];
+  uint16_t pk[2][kHoodThreads * K];
+  uint64_t bar[2];
+};
+
+template <int K>
+__device__ __forceinline__ void stream_issue(const MapArgs& a, StreamSmem<K>& sm, uint64_t tile,
+                                             int buf) {
+  const uint64_t h0 = a.h_begin + tile * kHoodThreads;  // (rows padded to whole tiles)
+  constexpr uint32_t kBase = kHoodThreads * 4, kRows = kHoodThreads * K * 2;
+  mbar_expect_tx(&sm.bar[buf], kBase + kRows);
+  bulk_g2s(sm.base[buf], a.hood_base + h0, kBase, &sm.bar[buf]);
+  bulk_g2s(sm.pk[buf], a.hood_pk + h0 * K, kRows, &sm.bar[buf]);
+}
+
+template <int K>
+__device__ __forceinline__ void hood_stream_body(const MapArgs& a, const double* minE, int t,
+                                                 uint32_t slot, uint32_t nslots, int skip_t) {
+  static_assert(K == 8 || K == 16, "streamed rows: 16-byte deltas");
+  __shared__ __align__(128) StreamSmem<K> sm;
+  const uint64_t ntiles = (a.h_end - a.h_begin + kHoodThreads - 1) / kHoodThreads;
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.bar[0]);
+    mbar_init(&sm.bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (slot >= ntiles) return;
+  if (threadIdx.x == 0) stream_issue<K>(a, sm, slot, 0);
+  pdl_wait();
+  const bool skip = map_iter_skipped(a.unconv, skip_t, a.fixed);  // (uniform)
+  uint32_t k = 0;
+  for (uint64_t tile = slot; tile < ntiles; tile += nslots, ++k) {
+    const int buf = k & 1;
+    const uint64_t next = tile + nslots;
+    if (!skip && threadIdx.x == 0 && next < ntiles) stream_issue<K>(a, sm, next, buf ^ 1);
+    mbar_wait(&sm.bar[buf], (k >> 1) & 1);
+    if (skip) return;  // (the only copy in flight has landed)
+    const uint64_t h = a.h_begin + tile * kHoodThreads + threadIdx.x;
+    int not_conv = 0;
+    if (h < a.h_end) {
+      uint32_t u[K / 2];
+      const uint4* src = reinterpret_cast<const uint4*>(sm.pk[buf] + threadIdx.x * K);
+#pragma unroll
+      for (int q = 0; q < K / 8; ++q) {
+        const uint4 w = src[q];
+        u[4 * q] = w.x;
+        u[4 * q + 1] = w.y;
+        u[4 * q + 2] = w.z;
+        u[4 * q + 3] = w.w;
+      }
+      not_conv = hood_eval<K, false>(a, minE, t, h, sm.base[buf][threadIdx.x], u);
+    }
+    // (also: every thread is done with buffer buf before it is refilled)
+    const int bu = __syncthreads_count(not_conv);
+    if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[t], uint32_t(bu));
+  }
+}
+
+template <int MT, int KV, int KH, int VP>
+__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
+    k_map_fused_stream(MapArgs a, const uint8_t* __restrict__ lab_in,
+                       uint8_t* __restrict__ lab_out, const double* __restrict__ minE_prev,
+                       double* __restrict__ minE_cur, int t, uint32_t nh, uint32_t nv) {
+  if (blockIdx.x < nh)
+    hood_stream_body<KH>(a, minE_prev, t - 1, blockIdx.x, nh, t - 1);
+  else
+    vertex_packed_body<MT, KV, VP, false>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh,
+                                          t > 0 ? t - 1 : 0);
 }
 
 // ---- pack builders ----

@@ -45,6 +45,10 @@ struct MapArgs {
   const int16_t* adj_pat;
   const uint32_t* hcode;
   const uint16_t* hood_pat;
+  // Streamed hood pass (opt-in, DPMRF_STREAM=<hood blocks per SM>, 0 = off):
+  // persistent hood blocks prefetch the next tile's packed rows with
+  // cp.async.bulk into shared memory while folding the current one.
+  int stream_hb;
   // Owned ranges (vertex-range partitioning; [0,R) and [0,Hs) on one GPU).
   // Arrays stay globally indexed; v_begin is a multiple of 256.
   uint32_t v_begin, v_end;

@@ -535,6 +535,7 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
     a.hood_k = packed ? ctx->hood_k : 0;
     a.hood_base = ctx->hood_base.get();
     a.hood_pk = ctx->hood_pk.get();
+    a.stream_hb = ctx->stream_hb;
     if (packed && ctx->dict_ok) {
       a.vcode = ctx->vcode.get();
       a.adj_pat = ctx->adj_pat.get();

@@ -351,3 +351,29 @@ def test_opt_in_layouts_agree(env, monkeypatch):
     finally:
         c.close()
         base.close()
+
+
+@pytest.mark.parametrize("hb", [1, 4])
+def test_streamed_hood_pass_agrees(hb, monkeypatch):
+    """DPMRF_STREAM=<hood blocks per SM>: persistent hood blocks prefetching
+    packed rows with cp.async.bulk reproduce the default path bit for bit
+    (converging and fixed work; both vertex-per-thread widths)."""
+    from paper_1809_05018_b200 import inputs
+    monkeypatch.setenv("DPMRF_STREAM", str(hb))
+    c = E.Context(0)
+    monkeypatch.setenv("DPMRF_STREAM", "0")
+    base = E.Context(0)
+    try:
+        for size, seed in ((1000, 9), (2560, 42), (8192, 3)):
+            sl = inputs.synthetic_slice(size, 8, seed=seed)
+            for ctx_ in (c, base):
+                ctx_.set_graph(sl.graph)
+                ctx_.build_neighborhoods(sl.cliques)
+            for fixed in (False, True):
+                cfg = E.OptimizerConfig(em_max_iters=4, rng_seed=seed)
+                got = c.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_EM)
+                want = base.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_EM)
+                same(got, want, full=False)
+    finally:
+        c.close()
+        base.close()
