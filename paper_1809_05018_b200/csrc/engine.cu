@@ -770,7 +770,10 @@ __device__ __forceinline__ uint32_t series_of(const uint32_t* leaf_start, uint32
 // bottom-up adjacent pairing == the split at bit_floor(n-1) -- and writes
 // mu (sum pass) / sigma and the published parameters (sq pass) and the
 // total energy.
-constexpr int kLeavesPerBlock = 8;
+#ifndef DPMRF_LEAVES_PER_BLOCK
+#define DPMRF_LEAVES_PER_BLOCK 8
+#endif
+constexpr int kLeavesPerBlock = DPMRF_LEAVES_PER_BLOCK;
 constexpr int kLeafStride = kFoldLeaf + 1;
 
 // EM bookkeeping after the M-step (one warp): record the EM log, apply the
