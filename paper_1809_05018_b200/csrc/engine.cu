@@ -838,7 +838,7 @@ __device__ void em_record(const EmEpilogueArgs& a, bool merged, const EmPrefetch
     for (int t = 0; t < a.map_max; ++t) a.unconv[t] = 0;
 }
 
-template <bool kSq>
+template <bool kSq, int kLPB = kLeavesPerBlock>
 __global__ void __launch_bounds__(256)
     k_leaf_fold(const double* __restrict__ x, const uint32_t* __restrict__ layout, uint32_t M,
                 const double* __restrict__ hist, uint64_t Hs, int ring,
@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(256)
   //              no trees (partitioned run: the partials are allgathered);
   //           2: one block, trees only, over allgathered label partials and
   //              the hood-series partials in hood_parts.
-  extern __shared__ double stage[];  // kLeavesPerBlock x kLeafStride
+  extern __shared__ double stage[];  // kLPB x kLeafStride
   pdl_wait();
   const uint32_t* n = layout;
   const uint32_t* label_start = layout + M;
@@ -861,17 +861,17 @@ __global__ void __launch_bounds__(256)
   const uint32_t all_end = leaf_start[tail_mode == 1 ? M : nseries];  // (beside the skip flag)
   if (em_skipped(unconv)) return;  // uniform: no block takes a ticket
   const uint32_t total = tail_mode == 2 ? 0u : min(all_end, leaf_hi);
-  const uint32_t first = leaf_lo + blockIdx.x * kLeavesPerBlock;
+  const uint32_t first = leaf_lo + blockIdx.x * kLPB;
   if (first < total) {
     const double* hood_row = nullptr;
     if (!kSq && unconv && !hood_parts) {
       const int T = executed_iters(unconv, map_max, fixed);
       hood_row = hist + uint64_t((T - 1) % ring) * Hs;
     }
-    __shared__ const double* src_s[kLeavesPerBlock];
-    __shared__ uint32_t len_s[kLeavesPerBlock];
-    __shared__ double mu_s[kLeavesPerBlock];
-    if (threadIdx.x < kLeavesPerBlock) {
+    __shared__ const double* src_s[kLPB];
+    __shared__ uint32_t len_s[kLPB];
+    __shared__ double mu_s[kLPB];
+    if (threadIdx.x < kLPB) {
       const uint32_t leaf = first + threadIdx.x;
       uint32_t len = 0;
       const double* src = nullptr;
@@ -902,7 +902,7 @@ __global__ void __launch_bounds__(256)
     // half's dependent adds.
     constexpr uint32_t kHalf = kFoldLeaf / 2;
     {
-      constexpr int kPerA = kLeavesPerBlock * int(kHalf) / 256;  // 16
+      constexpr int kPerA = kLPB * int(kHalf) / 256;  // 16
       double r[kPerA];
 #pragma unroll
       for (int q = 0; q < kPerA; ++q) {
@@ -918,7 +918,7 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     if (threadIdx.x >= 32) {
-      constexpr uint32_t kN = kLeavesPerBlock * kHalf;  // 4096 second-half elements
+      constexpr uint32_t kN = kLPB * kHalf;  // 4096 second-half elements
       constexpr int kPerB = int((kN + 223) / 224);       // over warps 1-7
       double r[kPerB];
       const uint32_t tb = threadIdx.x - 32;
@@ -936,7 +936,7 @@ __global__ void __launch_bounds__(256)
       __threadfence_block();
       asm volatile("bar.arrive 1, 256;" ::: "memory");
     } else {
-      const bool chain = threadIdx.x < kLeavesPerBlock && len_s[threadIdx.x] != 0;
+      const bool chain = threadIdx.x < kLPB && len_s[threadIdx.x] != 0;
       const uint32_t len = chain ? len_s[threadIdx.x] : 0u;
       const double* v = stage + threadIdx.x * kLeafStride;
       const double mu = (kSq && chain) ? mu_s[threadIdx.x] : 0.0;
@@ -1008,7 +1008,7 @@ __global__ void __launch_bounds__(256)
   }
   __shared__ EmPrefetch pf;
   if (kSq && merged && threadIdx.x == 0) em_prefetch(ep, &pf);
-  constexpr uint32_t kStageDoubles = kLeavesPerBlock * kLeafStride;
+  constexpr uint32_t kStageDoubles = 8 * kLeafStride;  // (the tail's stage: 8 x 1056)
   static_assert(8 * 1056 >= kStageDoubles, "tail stage");
   auto finish = [&](uint32_t s, double folded) {  // parameters / total energy of series s
     if (s < M) {
@@ -2552,11 +2552,26 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
     ++n;
   }
   const size_t leaf_smem = size_t(8) * 1056 * sizeof(double);  // 8 leaves (the tail: 8 x 1056)
-  ensure_dynamic_smem(k_leaf_fold<false>, leaf_smem);
-  ensure_dynamic_smem(k_leaf_fold<true>, leaf_smem);
-  const unsigned lg = grid_for(max_leaves, kLeavesPerBlock);
+  // few leaves (2560^2: ~300): 2 per block -- more SMs stage, the first
+  // stage is shorter (+1%); many (16384^2: ~16 000): 8 per block (the 67 KB
+  // stage caps 3 blocks per SM)
+  const bool few = max_leaves <= uint64_t(4) * kNumSMs;
+  const unsigned lg = grid_for(max_leaves, few ? 2 : kLeavesPerBlock);
   const EmEpilogueArgs epv = ep ? *ep : EmEpilogueArgs{};
-  if (!scatter_only) {
+  if (!scatter_only && few) {
+    ensure_dynamic_smem(k_leaf_fold<false, 2>, leaf_smem);
+    ensure_dynamic_smem(k_leaf_fold<true, 2>, leaf_smem);
+    launch_pdl(k_leaf_fold<false, 2>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
+               (const uint32_t*)layout, M, hist, Hs, ring, unconv, map_max, fixed, params,
+               partials, em_out, mb.done.get(), epv, 0, hood_parts, 0u, ~0u, 0);
+    launch_pdl(k_leaf_fold<true, 2>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
+               (const uint32_t*)layout, M, (const double*)nullptr, uint64_t(0), 1, unconv,
+               map_max, fixed, params, partials, em_out, mb.done.get() + 1, epv, ep ? 1 : 0,
+               (const double*)nullptr, 0u, ~0u, 0);
+    n += 2;
+  } else if (!scatter_only) {
+    ensure_dynamic_smem(k_leaf_fold<false>, leaf_smem);
+    ensure_dynamic_smem(k_leaf_fold<true>, leaf_smem);
     launch_pdl(k_leaf_fold<false>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
                (const uint32_t*)layout, M, hist, Hs, ring, unconv, map_max, fixed, params,
                partials, em_out, mb.done.get(), epv, 0, hood_parts, 0u, ~0u, 0);
