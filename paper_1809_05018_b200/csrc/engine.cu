@@ -1328,8 +1328,12 @@ namespace {
 #ifndef DPMRF_FUSED_MINB_M5
 #define DPMRF_FUSED_MINB_M5 5
 #endif
-constexpr int fused_min_blocks(int mt, int kh) {
-  return mt == 2 && kh == 8 ? DPMRF_FUSED_MINB : (mt == 5 ? DPMRF_FUSED_MINB_M5 : 1);
+#ifndef DPMRF_FUSED_MINB_VP2
+#define DPMRF_FUSED_MINB_VP2 8
+#endif
+constexpr int fused_min_blocks(int mt, int kh, int vp = 1) {
+  return mt == 2 && kh == 8 ? (vp == 2 ? DPMRF_FUSED_MINB_VP2 : DPMRF_FUSED_MINB)
+                            : (mt == 5 ? DPMRF_FUSED_MINB_M5 : 1);
 }
 constexpr int kWinRegs = 3;  // window rows held in registers (default L = 3)
 constexpr uint32_t kVertsPerThreadMin = 1u << 20;  // owned vertices for 2 per thread
@@ -1340,7 +1344,7 @@ __global__ void __launch_bounds__(kVtxThreads)
 template <int K>
 __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t);
 template <int MT, int KV, int KH, int VP, bool DICT>
-__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
+__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
                 uint32_t nh, uint32_t nv, ScatterArgs sc);
@@ -1764,7 +1768,7 @@ __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) 
 // (labels into the buffer t-1 consumed, minima into the other half of the
 // double-buffered minima, label counts into the other parity slot).
 template <int MT, int KV, int KH, int VP, bool DICT>
-__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
+__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
                 uint32_t nh, uint32_t nv, ScatterArgs sc) {
