@@ -190,7 +190,7 @@ dpmrf_status dpmrf_confusion(dpmrf_context* ctx, uint64_t n, const uint8_t* pred
                              const uint8_t* truth, uint64_t counts[4]);
 /* The segment write-back of proj/tools/main.cpp:157-165 (== the acceptance
  * test's labels_to_mask, proj/tests/acceptance.cpp:359-370) over the resident
- * label map (dpmrf_oversegment): mask[p] = labels[region[p]] == pore, pore =
+ * label map (dpmrf_oversegment, or the map given to dpmrf_build_region_graph): mask[p] = labels[region[p]] == pore, pore =
  * mu[0] <= mu[1] ? 0 : 1 (the darker class).  labels: num_vertices host values
  * (an optimize result, num_vertices == the map's regions); mask: width*height
  * bytes or NULL; counts: {tp, tn, fp, fn} against the resident phantom truth

@@ -360,6 +360,11 @@ extern "C" dpmrf_status dpmrf_build_region_graph(dpmrf_context* ctx, uint32_t w,
     ++ctx->generation;
     build_region_graph_device(ctx, w, h, px, reg, R);
     ctx->has_graph = ctx->has_sizes = true;
+    // the uploaded label map stays resident for dpmrf_segment_mask (no truth)
+    ctx->img_w = w;
+    ctx->img_h = h;
+    ctx->img_regions = R;
+    ctx->has_regions = true;
     if (num_adjacency) *num_adjacency = ctx->A;
   });
 }

@@ -376,6 +376,7 @@ class Context:
         _check(self._lib.dpmrf_build_region_graph(self.h, width, height, N.ptr(px), N.ptr(reg),
                                                   num_regions, ct.byref(A)), "build_region_graph")
         self.R = num_regions
+        self._img_n, self._img_regions = width * height, num_regions
         self._graph_key = None
         self._hoods_key = None
         return A.value

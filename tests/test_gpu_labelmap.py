@@ -71,3 +71,28 @@ def test_read_rlm_round_trip(tmp_path):  # graph_test.cpp:139-157
         f.write(b"RLM1\x02\x00\x00\x00\x01\x00\x00\x00\x00\x00\x00\x00\x02\x00\x00\x00")
     with pytest.raises(E.InputError):
         E.read_rlm(path)
+
+
+def test_rlm_pipeline_to_mask(ctx, orc, tmp_path):
+    """A label map from disk through the whole path: read_rlm (validated on
+    the device) -> region graph from host arrays -> cliques -> hoods ->
+    optimize -> segment write-back over the uploaded map == the oracle's."""
+    from paper_1809_05018_b200 import inputs
+    truth, image, _ = ctx.make_phantom(300, 200, 0.25, 0.05, 100.0, True, 77)
+    reg, R = inputs.oversegment(300, 200, 6, True)
+    path = str(tmp_path / "brick.rlm")
+    E.write_rlm(E.LabelMap(300, 200, reg), path)
+    lm = E.read_rlm(path)
+    assert lm.num_regions == R
+    ctx.build_region_graph(lm.width, lm.height, image, lm.region, lm.num_regions)
+    ctx.enumerate_maximal_cliques()
+    ctx.build_neighborhoods_resident()
+    res = ctx.optimize(E.OptimizerConfig(rng_seed=77), trace_level=E.TRACE_NONE)
+    mask, none = ctx.segment_mask(res.labels, res.mu, counts=False)
+    assert none is None
+    want = orc.labels_to_mask(reg, res.labels, res.mu)
+    assert np.array_equal(mask, want)
+    c = ctx.confusion(mask, truth)
+    assert (c.tp, c.tn, c.fp, c.fn) == orc.confusion(want, truth)
+    with pytest.raises(ValueError):  # no phantom truth behind an uploaded map
+        ctx.segment_mask(res.labels, res.mu)
