@@ -2,15 +2,20 @@
 // the optimize() driver.
 //
 // Driver shape (proj/src/mrf/optimize.cpp:31-74 re-planned for the device):
-//   * the graph and neighborhoods stay resident in HBM across calls;
-//   * every MAP iteration is two kernels (per-vertex argmin, per-hood sum +
-//     window test) launched back to back with NO host synchronization: the
-//     early exit of optimize.cpp:59 is evaluated on the device (each kernel
-//     checks the previous iteration's unconverged-hood counter);
-//   * the M-step and total energy run on the device; the host synchronizes
-//     ONCE per EM iteration to read (mu, sigma, total) and to evaluate
-//     log(sigma) with the host libm exactly as make_label_terms does
-//     (model.hpp:57), which keeps the energies bit-identical to the reference.
+//   * the graph and neighborhoods stay resident in HBM across calls, re-laid
+//     out once per upload by prepare() (validation + packed rows, one sync);
+//   * one fused kernel per MAP-iteration boundary (hood pass of t-1 + vertex
+//     pass of t), launched back to back with programmatic dependent launch and
+//     NO host synchronization: the early exit of optimize.cpp:59 is evaluated
+//     on the device from the previous iteration's unconverged-hood counter;
+//   * the M-step, total energy, EM window and the next EM's label terms (a
+//     correctly rounded device log) run on the device, one CUDA graph per EM,
+//     all EM iterations enqueued at once; the host synchronizes once at the
+//     end, checks every device log against the host libm (make_label_terms,
+//     model.hpp:57) and reruns with host logs in the (never observed) case
+//     of a difference -- so the energies stay bit-identical to the reference.
+//   * the host-log loop (one sync per EM) remains for kernel timing and the
+//     full per-MAP trace.
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
