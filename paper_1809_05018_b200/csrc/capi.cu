@@ -12,7 +12,7 @@
 //     correctly rounded device log) run on the device, one CUDA graph per EM,
 //     all EM iterations enqueued at once; the host synchronizes once at the
 //     end, checks every device log against the host libm (make_label_terms,
-//     model.hpp:57) and reruns with host logs in the (never observed) case
+//     model.hpp:57) and reruns with host logs in the (not yet observed) case
 //     of a difference -- so the energies stay bit-identical to the reference.
 //   * the host-log loop (one sync per EM) remains for kernel timing and the
 //     full per-MAP trace.
