@@ -13,7 +13,10 @@
 //                              halo: labels + minima its neighbors' owners /
 //                                    hoods need (exact [lo, hi] windows per
 //                                    (source, destination) pair, planned once)
-//                              hood pass (own series)
+//                              hood pass (own series; NCCL groups fold the
+//                                    interior series while the halo exchange
+//                                    runs on a side stream, the boundary
+//                                    series after it)
 //                              sum of the unconverged-hood counters
 //   per EM iteration           own labels + own hood-series leaf partials
 //                              (the row folded into 1024-element leaves on the
