@@ -67,10 +67,8 @@ enum {
   DPMRF_RUN_FIXED_WORK = 1u,    /* drop the early exits (optimize.cpp:59,:71): fixed EM x MAP work */
   DPMRF_RUN_MULTILABEL = 2u,    /* allow num_labels in [1,255] (extension; reference: 2 only) */
   DPMRF_RUN_KERNEL_TIMING = 4u, /* CUDA events around the MAP kernels (dpmrf_get_stats) */
-  DPMRF_RUN_TWO_KERNELS = 8u,   /* no persistent MAP-loop kernel (the default) */
   DPMRF_RUN_NO_GRAPH = 16u,     /* launch each EM iteration directly instead of a CUDA graph */
-  DPMRF_RUN_PERSISTENT = 32u,   /* one cooperative persistent kernel per MAP loop */
-  DPMRF_RUN_STAGED = 64u,       /* shared-memory staged vertex/hood tiles */
+  /* (8u, 32u, 64u: reserved -- measured-and-rejected variants) */
   DPMRF_RUN_CSR = 256u,         /* read the u32 CSR in the MAP kernels instead of the packed
                                    int16/u16 delta layouts built at preparation */
   DPMRF_RUN_UNFUSED = 512u,     /* separate vertex and hood kernels per MAP iteration; default
@@ -99,10 +97,9 @@ typedef struct dpmrf_run_stats {
   int32_t em_iters;
   int32_t map_iters_total;   /* MAP iterations executed, summed over EM iterations */
   uint64_t series;           /* hood-energy series length (nonempty hoods) */
-  double map_loop_ms;        /* persistent MAP-loop kernel (one cooperative launch per EM) */
+  double map_loop_ms;        /* fused MAP launches (events around each EM's chain of them) */
   uint64_t map_loop_launches;
-  int32_t persistent;        /* 1: persistent MAP loop, 2: dataflow MAP loop (one launch per EM),
-                                0: kernels per MAP iteration */
+  int32_t reserved0;         /* always 0 */
   int32_t graphs;            /* 1: EM iterations replayed from CUDA graphs */
   int32_t device_loop;       /* 1: the result came from the device-resident EM loop */
   uint32_t device_log_fallbacks; /* reruns because a device log(sigma) differed from the host's */
@@ -274,6 +271,18 @@ dpmrf_status dpmrf_trace_em(dpmrf_context* ctx, int32_t em, int32_t* map_iters,
 dpmrf_status dpmrf_trace_map(dpmrf_context* ctx, int32_t em, int32_t it, double* hood_energy,
                              uint8_t* converged);
 dpmrf_status dpmrf_get_stats(dpmrf_context* ctx, dpmrf_run_stats* out);
+/* Caller-owned destination of the full trace (DPMRF_TRACE_FULL) of later
+ * optimize calls on ctx: MAP iteration t of EM iteration em lands in row
+ * em * map_max_iters + t of hood_energy (f64) and converged (u8), each row
+ * `series` values long (dpmrf_trace_info) at a pitch of row_stride values;
+ * rows (capacity) must be >= em_max_iters * map_max_iters and row_stride >=
+ * the number of hoods, else the call falls back to the library's own
+ * buffers.  Rows arrive by DMA while the run proceeds (pinned memory:
+ * link-rate copies, no extra host copy); rows t >= the EM's map_iters are
+ * unspecified.  NULL detaches.  dpmrf_trace_map keeps working either way.
+ * (OptimizeResult.trace, engine.hpp:82-99, optimize.cpp:53-58.) */
+dpmrf_status dpmrf_set_trace_sink(dpmrf_context* ctx, double* hood_energy, uint8_t* converged,
+                                  uint64_t rows, uint64_t row_stride);
 
 /* ---- step functions (engine.hpp), each on the device -------------------- */
 /* init_random, engine.hpp:20-21 / engine.cpp:28-38 (num_labels != 2 ->

@@ -44,7 +44,7 @@ class CRunStats(ct.Structure):
                 ("mstep_ms", F64), ("vertex_launches", U64), ("hood_launches", U64),
                 ("kernel_launches", U64), ("em_iters", I32), ("map_iters_total", I32),
                 ("series", U64), ("map_loop_ms", F64), ("map_loop_launches", U64),
-                ("persistent", I32), ("graphs", I32), ("device_loop", I32),
+                ("reserved0", I32), ("graphs", I32), ("device_loop", I32),
                 ("device_log_fallbacks", U32)]
 
 
@@ -92,6 +92,7 @@ CUDA_API = [
     ("dpmrf_trace_em", ST, [VP, I32, ct.POINTER(I32), ct.POINTER(F64), ct.POINTER(ct.c_uint8),
                             VP, VP]),
     ("dpmrf_trace_map", ST, [VP, I32, I32, VP, VP]),
+    ("dpmrf_set_trace_sink", ST, [VP, VP, VP, U64, U64]),
     ("dpmrf_get_stats", ST, [VP, ct.POINTER(CRunStats)]),
     ("dpmrf_init_random", ST, [VP, U32, U32, U64, INT, VP, VP, VP]),
     ("dpmrf_replicate_by_label", ST, [VP, U32, VP, VP, VP]),

@@ -139,9 +139,6 @@ void dpmrf_context::prepare() {
   // packed layouts when every neighbor list / hood fits (all grid and brick
   // oversegmentations do); otherwise the kernels read the CSR directly
   adj_k = hood_k = 0;
-  dict_ok = false;
-  dict_patterns[0] = dict_patterns[1] = 0;
-  flow_hp = 0;  // dependency ranges follow the structure
   if (use_packed && R > 0) {
     const uint32_t* hs = h_err + 2;
     const uint32_t* so = series_alias ? h_off.get() : s_off_buf.get();
@@ -150,27 +147,10 @@ void dpmrf_context::prepare() {
       hood_k = hs[2] <= 9 ? 8 : (hs[2] <= 13 && use_k12 ? 12 : (hs[2] <= 17 ? 16 : 0));
     if (adj_k) launch_pack_adjacency(g_off.get(), g_nbr.get(), R, adj_k,
                                      adj_pk.ensure(uint64_t(R) * adj_k), stream);
-    // (rows padded to whole 256-hood tiles: the streamed hood pass copies
-    // full tiles with cp.async.bulk)
+    // (rows padded to whole 256-hood tiles)
     const uint64_t Hp = (Hs + 255) / 256 * 256;
     if (hood_k) launch_pack_hoods(so, h_mem.get(), Hs, hood_k, hood_base.ensure(Hp),
                                   hood_pk.ensure(Hp * hood_k), stream);
-    // dictionary form (MapArgs::vcode): one more pass and a 16-byte read-back
-    if (use_dict && adj_k && hood_k && R <= (1u << 24)) {
-      const size_t w = dict_ws_words();
-      uint32_t* ws = dict_ws.ensure(2 * w);
-      launch_dict_adjacency(g_off.get(), g_nbr.get(), R, adj_k, cover.get(), ws, vcode.ensure(R),
-                            adj_pat.ensure(uint64_t(kDictMax) * adj_k), stream);
-      launch_dict_hoods(so, h_mem.get(), Hs, hood_k, ws + w, hcode.ensure(Hs),
-                        hood_pat.ensure(uint64_t(kDictMax) * hood_k), stream);
-      uint32_t hd[4];
-      CK(cudaMemcpyAsync(hd, ws, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
-      CK(cudaMemcpyAsync(hd + 2, ws + w, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
-      sync();
-      dict_ok = hd[1] == 0 && hd[3] == 0;
-      dict_patterns[0] = hd[0];
-      dict_patterns[1] = hd[2];
-    }
   }
   // (no sync: everything that reads these runs later on the same stream)
 }
@@ -185,17 +165,11 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     auto* c = new dpmrf_context;
     c->device = device;
     if (const char* e = std::getenv("DPMRF_NO_GRAPH")) c->use_graphs = e[0] == '0';
-    if (const char* e = std::getenv("DPMRF_MAP_KERNELS")) c->use_persistent = e[0] == '1';
-    if (const char* e = std::getenv("DPMRF_DIRECT")) c->use_staged = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_NO_L2_PERSIST")) c->use_l2_persist = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_NO_PDL")) pdl_enabled() = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_HOST_LOG")) c->use_device_loop = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_CSR")) c->use_packed = e[0] == '0';
-    if (const char* e = std::getenv("DPMRF_DICT")) c->use_dict = e[0] == '1';
     if (const char* e = std::getenv("DPMRF_NO_K12")) c->use_k12 = e[0] == '0';
-    if (const char* e = std::getenv("DPMRF_STREAM")) c->stream_hb = std::atoi(e);
-    if (const char* e = std::getenv("DPMRF_FLOW")) c->use_flow = e[0] == '1';
-    if (const char* e = std::getenv("DPMRF_FLOW_SLEEP")) c->flow_sleep_ns = uint32_t(std::atoi(e));
     if (const char* e = std::getenv("DPMRF_UNFUSED")) c->use_fused = e[0] == '0';
     try {
       CK(cudaSetDevice(device));
@@ -215,6 +189,9 @@ extern "C" void dpmrf_context_destroy(dpmrf_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->trace_stream) cudaStreamSynchronize(ctx->trace_stream);
+  for (auto e : ctx->trace_ev) cudaEventDestroy(e);
+  if (ctx->trace_stream) cudaStreamDestroy(ctx->trace_stream);
   if (ctx->ev_begin) cudaEventDestroy(ctx->ev_begin);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
   ctx->drop_graphs();
@@ -599,6 +576,8 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
   const int em_max = cfg->em_max_iters;
 
   ctx->trace.clear();
+  ctx->trace_rows = nullptr;
+  ctx->trace_rowsf = nullptr;
   ctx->trace_level = o.trace_level;
   ctx->trace_M = M;
   const uint32_t fallbacks = ctx->stats.device_log_fallbacks;
@@ -636,27 +615,17 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     a.beta = cfg->beta;
     a.tol = cfg->convergence_tol;
     const bool full = o.trace_level >= DPMRF_TRACE_FULL;
-    const bool persistent = (o.flags & DPMRF_RUN_PERSISTENT) ||
-                            (ctx->use_persistent && !(o.flags & DPMRF_RUN_TWO_KERNELS));
     a.L = L;
     a.ring = full ? map_max : L + 1;
-    const bool fused_req = ctx->use_fused && !(o.flags & DPMRF_RUN_UNFUSED) && !persistent;
+    const bool fused_req = ctx->use_fused && !(o.flags & DPMRF_RUN_UNFUSED);
     a.fixed = fixed;
-    a.staged = (ctx->use_staged || (o.flags & DPMRF_RUN_STAGED)) ? 1 : 0;
     const bool packed = !(o.flags & DPMRF_RUN_CSR);
     a.adj_k = packed ? ctx->adj_k : 0;
     a.adj_pk = ctx->adj_pk.get();
     a.hood_k = packed ? ctx->hood_k : 0;
     a.hood_base = ctx->hood_base.get();
     a.hood_pk = ctx->hood_pk.get();
-    a.stream_hb = ctx->stream_hb;
-    if (packed && ctx->dict_ok) {
-      a.vcode = ctx->vcode.get();
-      a.adj_pat = ctx->adj_pat.get();
-      a.hcode = ctx->hcode.get();
-      a.hood_pat = ctx->hood_pat.get();
-    }
-    const bool fused = fused_req && !a.staged && map_fused_supported(a);
+    const bool fused = fused_req && map_fused_supported(a);
     a.terms = ctx->terms.ensure(3 * M);
     double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
     ctx->pin_in_l2(minE2, uint64_t(R) * sizeof(double) * (fused ? 2 : 1));
@@ -703,7 +672,6 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     ep.terms = const_cast<double*>(a.terms);
     std::vector<double> em_hist;
     const size_t ev_per_em = timing ? size_t(3 * map_max + 6) : 0;
-    ctx->stats.persistent = persistent;
     for (size_t i = 0; i < ev_per_em; ++i) ctx->event(i);
     // Everything one EM iteration puts on the stream (no host sync inside).
     uint64_t em_kernels = 0;
@@ -719,40 +687,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     // the self-scanning kernel: the scatter joins the last fused launch and
     // the EM bookkeeping joins the sq-pass tail -- 3 launches fewer per EM
     // (no k_em_prologue / k_label_scatter_small / k_em_epilogue).
-    const bool merged = device_loop && fused && !a.flags && mstep_tail_fusable(R, M);
-    // dataflow MAP loop (k_map_flow): one launch per EM instead of map_max+1
-    // when the whole grid fits resident; the M-step's scatter then runs as
-    // its own kernel (it needs every tile's final counts)
-    FlowArgs fl{};
-    int flow_hp = 0;
-    if (merged && ctx->use_flow) flow_hp = flow_plan(a, &fl.nvt, &fl.nht);
-    const bool flow = flow_hp > 0;
-    if (flow) ctx->stats.persistent = 2;
-    if (flow) {
-      if (ctx->flow_hp != flow_hp || ctx->flow_nvt != fl.nvt || ctx->flow_nht != fl.nht) {
-        launch_flow_deps(a.g_off, a.g_nbr, R, a.s_off, a.h_mem, Hs, flow_hp, fl.nvt, fl.nht,
-                         ctx->flow_vdep.ensure(2 * uint64_t(fl.nvt)),
-                         ctx->flow_hdep.ensure(2 * uint64_t(fl.nht ? fl.nht : 1)), st);
-        // progress flags one per 128-byte line: nvt vertex tiles, map_max hood
-        // counters, the exit ticket and the scatter's done counter
-        const uint64_t nf = (uint64_t(fl.nvt) + kMaxMapIters + 2) * 32;
-        uint32_t* z = ctx->flow_flags.ensure(nf);
-        CK(cudaMemsetAsync(z, 0, nf * sizeof(uint32_t), st));
-        ctx->flow_hp = flow_hp;
-        ctx->flow_nvt = fl.nvt;
-        ctx->flow_nht = fl.nht;
-      }
-      fl.vdep = ctx->flow_vdep.get();
-      fl.hdep = ctx->flow_hdep.get();
-      fl.vflag = ctx->flow_flags.get();
-      fl.hdone = fl.vflag + uint64_t(fl.nvt) * 32;
-      fl.ticket = fl.hdone + uint64_t(kMaxMapIters) * 32;
-      fl.minE_all = ctx->minE_flow.ensure(uint64_t(map_max) * R);
-      fl.lab_a = lab[0];
-      fl.lab_b = lab[1];
-      fl.map_max = map_max;
-      fl.sleep_ns = ctx->flow_sleep_ns;
-    }
+    const bool merged = device_loop && fused && mstep_tail_fusable(R, M);
     ScatterArgs sc{};
     sc.mean = a.mean;
     sc.counts = ctx->ms.counts.get();
@@ -778,17 +713,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
                            cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(a.unconv, 0, map_max * sizeof(uint32_t), st));
       }
-      if (flow) {
-        record(ev++);
-        launch_map_flow(a, fl, flow_hp, &sc, st);
-        record(ev++);
-        k += 1;
-      } else if (persistent) {
-        record(ev++);
-        launch_map_loop(a, lab[parity], lab[parity ^ 1], minE2, minE2 + R, map_max, st);
-        record(ev++);
-        k += 1;
-      } else if (fused) {
+      if (fused) {
         const uint64_t half = R ? R : 1;
         // timing: events around the whole chain of fused launches only, so
         // the PDL overlap between consecutive launches stays in the figure
@@ -812,7 +737,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
           k += 2;
         }
       }
-      if (a.flags && Hs) {  // full trace: every MAP row and flag vector of this EM
+      if (a.flags && Hs && !device_loop) {  // host-log full trace: this EM's MAP rows + flags
         CK(cudaMemcpyAsync(h_row, a.hist, uint64_t(map_max) * Hs * 8, cudaMemcpyDeviceToHost,
                            st));
         CK(cudaMemcpyAsync(h_flags, a.flags, uint64_t(map_max) * Hs, cudaMemcpyDeviceToHost,
@@ -846,7 +771,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       key.map_max = map_max;
       key.fixed = fixed;
       key.timing = timing;
-      key.persistent = persistent + 2 * a.staged + 4 * device_loop + 8 * fused;
+      key.mode = device_loop + 2 * fused;
       key.trace = o.trace_level;
       key.beta = cfg->beta;
       key.tol = cfg->convergence_tol;
@@ -879,10 +804,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       key.p2[2] = a.adj_pk;
       key.p2[3] = a.hood_pk;
       key.p2[4] = a.hood_base;
-      key.p2[5] = a.vcode;
-      key.p2[6] = a.hcode;
-      key.p2[7] = reinterpret_cast<const void*>(uintptr_t(a.stream_hb));
-      key.layout = a.adj_k * 100 + a.hood_k + flow_hp * 100000;
+      key.layout = a.adj_k * 100 + a.hood_k;
       if (!ctx->graph_valid || std::memcmp(&key, &ctx->graph_key, sizeof key) != 0) {
         ctx->drop_graphs();
         for (int parity = 0; parity < (device_loop ? 1 : 2); ++parity) {
@@ -919,17 +841,61 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       host_terms();
       CK(cudaMemcpyAsync(const_cast<double*>(a.terms), h_terms, 3 * M * 8,
                          cudaMemcpyHostToDevice, st));
+      // Full trace: after each EM its MAP rows (hood energies + flags) are
+      // stashed in HBM (one slice per EM); fixed-work runs stream every
+      // slice to the host on a side stream while later EMs compute, runs with
+      // early exits copy the rows of the executed iterations after the loop.
+      const uint64_t slice = uint64_t(map_max) * Hs;
+      const bool stash = a.flags && Hs;
+      double* dte = nullptr;
+      uint8_t* dtf = nullptr;
+      double* hte = nullptr;
+      uint8_t* htf = nullptr;
+      uint64_t pitch = Hs;
+      if (stash) {
+        dte = ctx->trace_dev.ensure(uint64_t(em_max) * slice);
+        dtf = ctx->trace_devf.ensure(uint64_t(em_max) * slice);
+        const uint64_t rows = uint64_t(em_max) * map_max;
+        if (ctx->sink_e && ctx->sink_f && ctx->sink_rows >= rows && ctx->sink_stride >= Hs) {
+          hte = ctx->sink_e;
+          htf = ctx->sink_f;
+          pitch = ctx->sink_stride;
+        } else {
+          hte = ctx->trace_arena.ensure(rows * Hs);
+          htf = ctx->trace_arenaf.ensure(rows * Hs);
+        }
+        if (!ctx->trace_stream)
+          CK(cudaStreamCreateWithFlags(&ctx->trace_stream, cudaStreamNonBlocking));
+      }
+      auto rows_d2h = [&](int e, uint64_t nrows, cudaStream_t cs) {
+        if (!nrows) return;
+        CK(cudaMemcpy2DAsync(hte + uint64_t(e) * map_max * pitch, pitch * 8, dte + e * slice,
+                             Hs * 8, Hs * 8, nrows, cudaMemcpyDeviceToHost, cs));
+        CK(cudaMemcpy2DAsync(htf + uint64_t(e) * map_max * pitch, pitch, dtf + e * slice, Hs, Hs,
+                             nrows, cudaMemcpyDeviceToHost, cs));
+      };
       for (int em = 0; em < em_max; ++em) {
         if (use_graph) {
           CK(cudaGraphLaunch(ctx->graph_exec[0], st));
         } else {
           enqueue_em(0);
         }
+        if (stash) {
+          CK(cudaMemcpyAsync(dte + em * slice, a.hist, slice * 8, cudaMemcpyDeviceToDevice, st));
+          CK(cudaMemcpyAsync(dtf + em * slice, a.flags, slice, cudaMemcpyDeviceToDevice, st));
+          if (fixed) {
+            cudaEvent_t ev = ctx->trace_event(em);
+            CK(cudaEventRecord(ev, st));
+            CK(cudaStreamWaitEvent(ctx->trace_stream, ev, 0));
+            rows_d2h(em, uint64_t(map_max), ctx->trace_stream);
+          }
+        }
       }
       CK(cudaMemcpyAsync(h_rec, state, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(h_rec + 4, em_rec, uint64_t(em_max) * rec_stride * 8,
                          cudaMemcpyDeviceToHost, st));
       ctx->sync();
+      if (stash && fixed) CK(cudaStreamSynchronize(ctx->trace_stream));
       uint32_t hstate[4];
       std::memcpy(hstate, h_rec, sizeof hstate);
       const int em_count = static_cast<int>(hstate[2]);
@@ -954,6 +920,10 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
           er.converged = r[2] != 0.0;
           er.mu.assign(r + 3, r + 3 + M);
           er.sigma.assign(r + 3 + M, r + 3 + 2 * M);
+          if (stash) {
+            er.row0 = int64_t(e) * map_max;
+            if (!fixed) rows_d2h(e, uint64_t(T), st);
+          }
           ctx->trace.push_back(std::move(er));
         }
         if (e == em_count - 1) {
@@ -962,6 +932,11 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
         }
       }
       ctx->stats.em_iters = em_count;
+      if (stash) {
+        ctx->trace_rows = hte;
+        ctx->trace_rowsf = htf;
+        ctx->trace_stride = pitch;
+      }
       cur = 0;
     } else {
       for (int em = 0; em < em_max; ++em) {
@@ -977,12 +952,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
         if (timing) {
           float ms = 0.f;
           size_t e = 0;
-          if (persistent || flow) {
-            CK(cudaEventElapsedTime(&ms, ctx->ev_pool[0], ctx->ev_pool[1]));
-            ctx->stats.map_loop_ms += ms;
-            ctx->stats.map_loop_launches += 1;
-            e = 2;
-          } else if (fused) {
+          if (fused) {
             CK(cudaEventElapsedTime(&ms, ctx->ev_pool[0], ctx->ev_pool[1]));
             ctx->stats.map_loop_ms += ms;
             ctx->stats.map_loop_launches += map_max + 1;
@@ -1105,11 +1075,14 @@ void optimize_resident(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     validate_config(*cfg, (o.flags & DPMRF_RUN_MULTILABEL) != 0);
     need(ctx->has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
     ctx->bind();
-    // The device-resident EM loop serves TRACE_NONE / TRACE_EM runs; the full
-    // per-MAP trace and per-kernel timing use the host-log loop.
+    // The device-resident EM loop serves every trace level (the full trace's
+    // rows are stashed in HBM per EM, up to kTraceStashBytes); per-kernel
+    // timing uses the host-log loop.
+    const bool full = o.trace_level >= DPMRF_TRACE_FULL;
+    const double stash = full ? double(cfg->em_max_iters) * cfg->map_max_iters * ctx->H * 9.0 : 0;
     const bool device_loop = ctx->use_device_loop && !(o.flags & DPMRF_RUN_HOST_LOG) &&
-                             !(o.flags & DPMRF_RUN_KERNEL_TIMING) &&
-                             o.trace_level < DPMRF_TRACE_FULL && cfg->em_max_iters > 0;
+                             !(o.flags & DPMRF_RUN_KERNEL_TIMING) && stash <= kTraceStashBytes &&
+                             cfg->em_max_iters > 0;
     if (device_loop) {
       if (run_optimize(ctx, cfg, o, true, labels_out, mu_out, sigma_out)) return;
       ++ctx->stats.device_log_fallbacks;  // a device log(sigma) differed from glibc's
@@ -1145,6 +1118,19 @@ extern "C" dpmrf_status dpmrf_trace_em(dpmrf_context* ctx, int32_t em, int32_t* 
   });
 }
 
+extern "C" dpmrf_status dpmrf_set_trace_sink(dpmrf_context* ctx, double* hood_energy,
+                                            uint8_t* converged, uint64_t rows,
+                                            uint64_t row_stride) {
+  return guarded([&] {
+    ContextLock lock_(ctx);
+    const bool on = hood_energy && converged;
+    ctx->sink_e = on ? hood_energy : nullptr;
+    ctx->sink_f = on ? converged : nullptr;
+    ctx->sink_rows = on ? rows : 0;
+    ctx->sink_stride = on ? row_stride : 0;
+  });
+}
+
 extern "C" dpmrf_status dpmrf_trace_map(dpmrf_context* ctx, int32_t em, int32_t it,
                                         double* hood_energy, uint8_t* converged) {
   return guarded([&] {
@@ -1152,6 +1138,14 @@ extern "C" dpmrf_status dpmrf_trace_map(dpmrf_context* ctx, int32_t em, int32_t 
     need(ctx && em >= 0 && size_t(em) < ctx->trace.size(), DPMRF_OUT_OF_RANGE,
          "no such EM iteration in the trace");
     const auto& r = ctx->trace[em];
+    if (r.row0 >= 0 && ctx->trace_rows) {  // device-loop full trace: host rows
+      need(it >= 0 && it < r.map_iters, DPMRF_OUT_OF_RANGE, "no such MAP iteration in the trace");
+      const uint64_t row = uint64_t(r.row0 + it) * ctx->trace_stride;
+      const uint64_t n = ctx->stats.series;
+      if (hood_energy) std::memcpy(hood_energy, ctx->trace_rows + row, n * 8);
+      if (converged) std::memcpy(converged, ctx->trace_rowsf + row, n);
+      return;
+    }
     need(it >= 0 && size_t(it) < r.hood_energy.size(), DPMRF_OUT_OF_RANGE,
          "no such MAP iteration in the trace (needs DPMRF_TRACE_FULL)");
     if (hood_energy)

@@ -48,6 +48,10 @@ constexpr double kSigmaFloor = 1e-3;       // kSigmaFloor, model.hpp:9
 constexpr int kMaxLabels = 255;            // labels are stored as u8 in HBM
 constexpr int kMaxMapIters = 4096;
 constexpr int kNumSMs = 148;
+// HBM budget of the full-trace stash of the device-resident EM loop (every
+// EM's map_max x H rows of f64 energies + u8 flags); larger runs take the
+// host-log loop.
+constexpr double kTraceStashBytes = 24.0 * (1ull << 30);
 
 // Growable device buffer (HBM). Contents are not preserved on growth.
 template <class T>

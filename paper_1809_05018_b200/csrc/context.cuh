@@ -85,8 +85,32 @@ struct dpmrf_context {
     std::vector<double> mu, sigma;
     std::vector<std::vector<double>> hood_energy;  // FULL trace only
     std::vector<std::vector<uint8_t>> hood_conv;
+    int64_t row0 = -1;  // device-loop full trace: first host row (trace_rows)
   };
   std::vector<EmRecord> trace;
+  // Full trace of the device-resident loop: every EM's MAP rows stashed in
+  // HBM (trace_dev*), streamed by DMA on trace_stream into the caller's sink
+  // or the library's pinned arena; EmRecord::row0 indexes those host rows.
+  dpmrf_b200::DevBuf<double> trace_dev;
+  dpmrf_b200::DevBuf<uint8_t> trace_devf;
+  dpmrf_b200::HostBuf<double> trace_arena;
+  dpmrf_b200::HostBuf<uint8_t> trace_arenaf;
+  double* sink_e = nullptr;
+  uint8_t* sink_f = nullptr;
+  uint64_t sink_rows = 0, sink_stride = 0;
+  const double* trace_rows = nullptr;    // host rows of the last run (sink or arena)
+  const uint8_t* trace_rowsf = nullptr;
+  uint64_t trace_stride = 0;
+  cudaStream_t trace_stream = nullptr;
+  std::vector<cudaEvent_t> trace_ev;
+  cudaEvent_t trace_event(size_t i) {
+    while (trace_ev.size() <= i) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      trace_ev.push_back(e);
+    }
+    return trace_ev[i];
+  }
   int32_t trace_level = DPMRF_TRACE_NONE;
   uint32_t trace_M = 0;
   dpmrf_run_stats stats{};
@@ -105,7 +129,7 @@ struct dpmrf_context {
   struct GraphKey {
     uint64_t R, Hs;
     uint32_t M;
-    int32_t L, map_max, fixed, timing, trace, persistent;
+    int32_t L, map_max, fixed, timing, trace, mode;
     double beta, tol;
     const void* p[24];
     const void* p2[8];
@@ -115,14 +139,6 @@ struct dpmrf_context {
   dpmrf_b200::DevBuf<double> em_rec, em_hist;
   dpmrf_b200::HostBuf<double> h_rec;
   bool use_graphs = true;
-  // one cooperative MAP-loop kernel per EM iteration instead of two kernels
-  // per MAP iteration: measured slower at both 2560^2 and 16384^2 (fewer
-  // resident blocks per phase + grid-barrier cost), so opt-in
-  bool use_persistent = false;
-  // shared-memory staged vertex / hood tiles: measured SLOWER than one thread
-  // per item on B200 (L1 already absorbs the CSR segment reads; the staged
-  // hood fold is bank-conflicted), so off unless DPMRF_DIRECT=0
-  bool use_staged = false;
   // hood pass of t-1 + vertex pass of t in one launch (packed layouts)
   bool use_fused = true;
   bool graph_valid = false;
@@ -178,30 +194,11 @@ struct dpmrf_context {
 
   // ---- packed static structure (engine.cuh MapArgs::adj_k / hood_k) ----
   bool use_packed = true;
-  bool use_k12 = true;
-  int stream_hb = 0;    // streamed hood pass blocks per SM (DPMRF_STREAM; 0 = off)  // 12-slot hood rows for <= 13-slot hoods (DPMRF_NO_K12=1: 16)
+  bool use_k12 = true;  // 12-slot hood rows for <= 13-slot hoods (DPMRF_NO_K12=1: 16)
   int adj_k = 0, hood_k = 0;
   dpmrf_b200::DevBuf<int16_t> adj_pk;
   dpmrf_b200::DevBuf<uint32_t> hood_base;
   dpmrf_b200::DevBuf<uint16_t> hood_pk;
-  // dictionary form of the packed layouts (engine.cuh MapArgs::vcode);
-  // opt-in (DPMRF_DICT=1): measured slower than the plain packed layout
-  //
-  bool use_dict = false, dict_ok = false;
-  uint32_t dict_patterns[2] = {0, 0};  // distinct adjacency / hood patterns
-  dpmrf_b200::DevBuf<uint8_t> vcode;
-  dpmrf_b200::DevBuf<int16_t> adj_pat;
-  dpmrf_b200::DevBuf<uint32_t> hcode;
-  dpmrf_b200::DevBuf<uint16_t> hood_pat;
-  dpmrf_b200::DevBuf<uint32_t> dict_ws;
-  // dataflow MAP loop (engine.cuh FlowArgs): opt-in (DPMRF_FLOW=1), measured
-  // slower than the PDL chain of fused launches
-  bool use_flow = false;
-  int flow_hp = 0;  // 0: dependency ranges not built for the current structure
-  uint32_t flow_nvt = 0, flow_nht = 0;
-  uint32_t flow_sleep_ns = 32;  // DPMRF_FLOW_SLEEP
-  dpmrf_b200::DevBuf<uint32_t> flow_vdep, flow_hdep, flow_flags;
-  dpmrf_b200::DevBuf<double> minE_flow;
 };
 
 namespace dpmrf_b200 {

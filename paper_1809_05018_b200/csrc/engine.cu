@@ -11,8 +11,6 @@
 // then gather the per-vertex minima in slot order.
 #include <algorithm>
 
-#include <cooperative_groups.h>
-
 #include "engine.cuh"
 
 namespace dpmrf_b200 {
@@ -225,191 +223,6 @@ __device__ __forceinline__ int hood_body(uint64_t h, const uint32_t* __restrict_
   return !ok;
 }
 
-// ---------------------------------------------------------------------------
-// Shared-memory staged tiles (256 vertices / 256 hoods per block).
-// A tile's CSR range is contiguous, so the block reads it with coalesced
-// loads and resolves the data-dependent gathers (neighbor labels / member
-// minima) cooperatively, kBatch independent loads per thread in flight; the
-// per-vertex / per-hood arithmetic then runs out of shared memory in exactly
-// the order of the direct bodies above.  Tiles whose range exceeds the stage
-// (high-degree hubs) fall back to the direct bodies.
-// ---------------------------------------------------------------------------
-constexpr uint32_t kVtxStageCap = 4096;   // neighbor labels per vertex tile (u8)
-constexpr uint32_t kHoodStageCap = 4096;  // member minima per hood tile (f64, 32 KB)
-constexpr int kBatch = 8;
-
-template <int MT>
-__device__ __forceinline__ void vertex_tile(uint64_t tile, const MapArgs& a,
-                                            const uint8_t* __restrict__ lab_in,
-                                            uint8_t* __restrict__ lab_out,
-                                            double* __restrict__ minE, uint8_t* sm_lab, int t) {
-  const uint32_t v0 = static_cast<uint32_t>(tile * kVtxThreads);
-  const uint32_t vend = min(a.R, v0 + kVtxThreads);
-  const uint32_t v = v0 + threadIdx.x;
-  const uint32_t Mc = MT > 0 ? uint32_t(MT) : a.M;
-  uint32_t* counts = a.tile_counts + (uint64_t(t & 1) * a.tiles + tile) * Mc;
-  const uint32_t base = a.g_off[v0], cnt = a.g_off[vend] - base;
-  if (cnt > kVtxStageCap) {
-    uint32_t nl = 0;
-    if (v < vend)
-      nl = vertex_body<MT>(v, a.g_off, a.g_nbr, a.mean, a.cover, lab_in, lab_out, minE, a.M,
-                           a.terms, a.beta);
-    block_label_counts(counts, Mc, v < vend, nl);
-    return;
-  }
-  uint32_t newlab = 0;
-  for (uint32_t c0 = 0; c0 < cnt; c0 += kBatch * kVtxThreads) {
-    uint32_t id[kBatch];
-    uint8_t lb[kBatch];
-#pragma unroll
-    for (int q = 0; q < kBatch; ++q) {
-      const uint32_t i = c0 + q * kVtxThreads + threadIdx.x;
-      id[q] = i < cnt ? a.g_nbr[base + i] : 0u;
-    }
-#pragma unroll
-    for (int q = 0; q < kBatch; ++q) {
-      const uint32_t i = c0 + q * kVtxThreads + threadIdx.x;
-      lb[q] = i < cnt ? lab_in[id[q]] : uint8_t(0);
-    }
-#pragma unroll
-    for (int q = 0; q < kBatch; ++q) {
-      const uint32_t i = c0 + q * kVtxThreads + threadIdx.x;
-      if (i < cnt) sm_lab[i] = lb[q];
-    }
-  }
-  __syncthreads();
-  if (v < vend) {
-    const uint8_t old = lab_in[v];
-    if (!a.cover[v]) {
-      lab_out[v] = old;
-      newlab = old;
-    } else {
-      const uint32_t M = MT > 0 ? uint32_t(MT) : a.M;
-      const uint32_t lo = a.g_off[v] - base, hi = a.g_off[v + 1] - base;
-      const uint32_t deg = hi - lo;
-      const double x = a.mean[v];
-      const double* T = a.terms;
-      double best;
-      uint32_t best_l;
-      if constexpr (MT == 2) {
-        uint32_t ones = 0;
-        for (uint32_t k = lo; k < hi; ++k) ones += sm_lab[k];
-        const double e0 = label_energy(x, T[0], T[2], T[4], a.beta, ones);
-        const double e1 = label_energy(x, T[1], T[3], T[5], a.beta, deg - ones);
-        best = e0;
-        best_l = 0;
-        if (e1 < best) {
-          best = e1;
-          best_l = 1;
-        }
-      } else {
-        best = 0.0;
-        best_l = 0;
-        for (uint32_t l = 0; l < M; ++l) {
-          uint32_t same = 0;
-          for (uint32_t k = lo; k < hi; ++k) same += (sm_lab[k] == l);
-          const double e = label_energy(x, T[l], T[M + l], T[2 * M + l], a.beta, deg - same);
-          if (l == 0 || e < best) {
-            best = e;
-            best_l = l;
-          }
-        }
-      }
-      minE[v] = best;
-      lab_out[v] = static_cast<uint8_t>(best_l);
-      newlab = best_l;
-    }
-  }
-  block_label_counts(counts, Mc, v < vend, newlab);
-  __syncthreads();  // the stage is reused by the next tile of a persistent block
-}
-
-// Returns this thread's "not converged" flag (0 for threads past the end).
-__device__ __forceinline__ int hood_tile(uint64_t tile, const MapArgs& a,
-                                         const double* __restrict__ minE, int t, double* sm_e) {
-  const uint64_t h0 = tile * kHoodThreads;
-  const uint64_t hcap = h0 + kHoodThreads;
-  const uint64_t hend = a.Hs < hcap ? a.Hs : hcap;
-  const uint64_t h = h0 + threadIdx.x;
-  const uint32_t base = a.s_off[h0], cnt = a.s_off[hend] - base;
-  if (cnt > kHoodStageCap)
-    return hood_body(h, a.s_off, a.h_mem, minE, a.hist, a.flags, a.Hs, t, a.L, a.ring, a.tol);
-  for (uint32_t c0 = 0; c0 < cnt; c0 += kBatch * kHoodThreads) {
-    uint32_t id[kBatch];
-    double e[kBatch];
-#pragma unroll
-    for (int q = 0; q < kBatch; ++q) {
-      const uint32_t i = c0 + q * kHoodThreads + threadIdx.x;
-      id[q] = i < cnt ? a.h_mem[base + i] : 0u;
-    }
-#pragma unroll
-    for (int q = 0; q < kBatch; ++q) {
-      const uint32_t i = c0 + q * kHoodThreads + threadIdx.x;
-      e[q] = i < cnt ? minE[id[q]] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < kBatch; ++q) {
-      const uint32_t i = c0 + q * kHoodThreads + threadIdx.x;
-      if (i < cnt) sm_e[i] = e[q];
-    }
-  }
-  __syncthreads();
-  int not_conv = 0;
-  if (h < hend) {
-    const uint32_t lo = a.s_off[h] - base, hi = a.s_off[h + 1] - base;
-    double sum;
-    if (hi - lo <= kFoldLeaf) {
-      sum = sm_e[lo];
-      for (uint32_t k = lo + 1; k < hi; ++k) sum = __dadd_rn(sum, sm_e[k]);
-    } else {  // fold_range: leaves + pairwise tree (kernels.hpp:56-65)
-      TreeStack<double, AddOp> st;
-      for (uint32_t b = lo; b < hi; b += kFoldLeaf) {
-        const uint32_t e2 = min(hi, b + kFoldLeaf);
-        double acc = sm_e[b];
-        for (uint32_t k = b + 1; k < e2; ++k) acc = __dadd_rn(acc, sm_e[k]);
-        st.push(acc, AddOp{});
-      }
-      sum = st.finish(AddOp{});
-    }
-    const int R1 = a.ring;
-    a.hist[uint64_t(t % R1) * a.Hs + h] = sum;
-    int ok = 0;
-    if (t >= a.L) {
-      ok = 1;
-      for (int i = 1; i <= a.L; ++i) {
-        const double prev = a.hist[uint64_t((t - i) % R1) * a.Hs + h];
-        if (!(fabs(__dsub_rn(sum, prev)) < a.tol)) {
-          ok = 0;
-          break;
-        }
-      }
-    }
-    if (a.flags) a.flags[uint64_t(t) * a.Hs + h] = static_cast<uint8_t>(ok);
-    not_conv = !ok;
-  }
-  __syncthreads();
-  return not_conv;
-}
-
-template <int MT>
-__global__ void __launch_bounds__(kVtxThreads)
-    k_vertex_staged(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
-                    int t) {
-  __shared__ uint8_t sm_lab[kVtxStageCap];
-  pdl_wait();
-  if (map_iter_skipped(a.unconv, t, a.fixed)) return;
-  vertex_tile<MT>(blockIdx.x, a, lab_in, lab_out, a.minE, sm_lab, t);
-}
-
-__global__ void __launch_bounds__(kHoodThreads) k_hood_staged(MapArgs a, int t) {
-  __shared__ double sm_e[kHoodStageCap];
-  pdl_wait();
-  if (map_iter_skipped(a.unconv, t, a.fixed)) return;
-  const int nc = hood_tile(blockIdx.x, a, a.minE, t, sm_e);
-  const int bu = __syncthreads_count(nc);
-  if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[t], uint32_t(bu));
-}
-
 __global__ void __launch_bounds__(kHoodThreads)
     k_hood_sums(const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ h_mem,
                 const double* __restrict__ minE, double* __restrict__ hist,
@@ -422,53 +235,6 @@ __global__ void __launch_bounds__(kHoodThreads)
       h < h_end ? hood_body(h, s_off, h_mem, minE, hist, flags, Hs, t, L, ring, tol) : 0;
   const int block_unconv = __syncthreads_count(not_conv);
   if (threadIdx.x == 0 && block_unconv) atomicAdd(&unconv[t], uint32_t(block_unconv));
-}
-
-// ---------------------------------------------------------------------------
-// Persistent MAP loop: all MAP iterations of one EM iteration in ONE
-// cooperative launch.  Phase p (0..map_max) runs, over a grid-stride work
-// list of 256-vertex and 256-hood tiles,
-//   * the hood sums + window test of iteration p-1 (minE[(p-1)&1]), and
-//   * the vertex pass of iteration p (minE[p&1], labels p -> p+1),
-// then one grid barrier.  The vertex pass of p is speculative: if iteration
-// p-1 turns out to be the last (all hoods converged, optimize.cpp:59), its
-// outputs are simply never read -- the committed labels are those of
-// iteration p-1, in the buffer the M-step selects from the same counters.
-// One barrier per MAP iteration instead of two kernel boundaries.
-// ---------------------------------------------------------------------------
-template <int MT>
-__global__ void __launch_bounds__(kVtxThreads)
-    k_map_loop(MapArgs a, uint8_t* lab0, uint8_t* lab1, double* minE0, double* minE1,
-               int map_max) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  __shared__ uint8_t sm_lab[kVtxStageCap];
-  __shared__ double sm_e[kHoodStageCap];
-  if (em_skipped(a.unconv)) return;
-  const uint64_t vt = (uint64_t(a.R) + kVtxThreads - 1) / kVtxThreads;
-  const uint64_t ht = (a.Hs + kHoodThreads - 1) / kHoodThreads;
-  for (int p = 0; p <= map_max; ++p) {
-    // iteration p-1 exists iff p-1 == 0 or iteration p-2 left hoods unconverged
-    const bool run_h = p >= 1 && (a.fixed || p == 1 || a.unconv[p - 2] != 0);
-    // vertex pass of p: skip once an earlier iteration is known to be the last
-    const bool run_v = p < map_max && (a.fixed || p <= 1 || a.unconv[p - 2] != 0);
-    if (!run_h && !run_v) break;
-    const uint8_t* lin = ((p & 1) ? lab1 : lab0);
-    uint8_t* lout = ((p & 1) ? lab0 : lab1);
-    double* mv = (p & 1) ? minE1 : minE0;
-    const double* mh = (p & 1) ? minE0 : minE1;
-    const uint64_t items = (run_h ? ht : 0) + (run_v ? vt : 0);
-    for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
-      if (run_h && it < ht) {
-        const int nc = hood_tile(it, a, mh, p - 1, sm_e);
-        const int bu = __syncthreads_count(nc);
-        if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[p - 1], uint32_t(bu));
-      } else {
-        vertex_tile<MT>(it - (run_h ? ht : 0), a, lin, lout, mv, sm_lab, p);
-      }
-    }
-    grid.sync();
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1343,20 +1109,15 @@ __global__ void __launch_bounds__(kVtxThreads)
                     int t);
 template <int K>
 __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t);
-template <int MT, int KV, int KH, int VP, bool DICT>
+template <int MT, int KV, int KH, int VP>
 __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
                 uint32_t nh, uint32_t nv, ScatterArgs sc);
-template <int MT, int KV, int KH, int VP>
-__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
-    k_map_fused_stream(MapArgs a, const uint8_t* __restrict__ lab_in,
-                       uint8_t* __restrict__ lab_out, const double* __restrict__ minE_prev,
-                       double* __restrict__ minE_cur, int t, uint32_t nh, uint32_t nv);
 }  // namespace
 
 
-bool map_fused_supported(const MapArgs& a) { return a.adj_k && a.hood_k && !a.staged; }
+bool map_fused_supported(const MapArgs& a) { return a.adj_k && a.hood_k; }
 
 bool mstep_tail_fusable(uint32_t R, uint32_t M) {
   const uint64_t tiles = (uint64_t(R) + kTileVerts - 1) / kTileVerts;
@@ -1380,27 +1141,9 @@ void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
   const ScatterArgs scv = tail ? *sc : ScatterArgs{};
   const size_t smem = tail ? scatter_small_smem(sc->M) : 0;
   const dim3 g(nh + nv + ns), blk(kVtxThreads);
-  // streamed hood pass (opt-in): large graphs, plain packed rows, no tail
-  const int shb = a.stream_hb;
-  if (shb > 0 && !tail && !a.vcode && a.M == 2 && a.adj_k == 4 && a.hood_k == 8) {
-    const uint32_t tiles = t >= 1 ? grid_for(a.h_end - a.h_begin, kHoodThreads) : 0u;
-    const uint32_t nhs = std::min<uint32_t>(tiles, uint32_t(shb) * kNumSMs);
-    const dim3 gs(nhs + nv);
-    if (vp == 2)
-      launch_pdl(k_map_fused_stream<2, 4, 8, 2>, gs, blk, 0, s, a, lab_in, lab_out, minE_prev,
-                 minE_cur, t, nhs, nv);
-    else
-      launch_pdl(k_map_fused_stream<2, 4, 8, 1>, gs, blk, 0, s, a, lab_in, lab_out, minE_prev,
-                 minE_cur, t, nhs, nv);
-    return;
-  }
-  // dictionary-coded structure when both dictionaries fit (MapArgs::vcode)
-  const bool dict = a.vcode && a.hcode;
 #define MF4(MT, KV, KH, VP)                                                              \
-  (dict ? launch_pdl(k_map_fused<MT, KV, KH, VP, true>, g, blk, smem, s, a, lab_in, lab_out, \
-                     minE_prev, minE_cur, t, nh, nv, scv)                                   \
-        : launch_pdl(k_map_fused<MT, KV, KH, VP, false>, g, blk, smem, s, a, lab_in,        \
-                     lab_out, minE_prev, minE_cur, t, nh, nv, scv))
+  launch_pdl(k_map_fused<MT, KV, KH, VP>, g, blk, smem, s, a, lab_in, lab_out, minE_prev,  \
+             minE_cur, t, nh, nv, scv)
 #define MF(MT, KV, KH) MF4(MT, KV, KH, 1)
   if (a.M == 5 && a.adj_k == 8 && a.hood_k == 16) {  // config C's layout: label loop unrolled
     MF(5, 8, 16);
@@ -1439,8 +1182,7 @@ void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
 void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out, int t,
                           cudaStream_t s) {
   const dim3 g(grid_for(a.v_end - a.v_begin, kVtxThreads)), blk(kVtxThreads);
-  const bool whole = a.v_begin == 0 && a.v_end == a.R;  // staged path: whole graph only
-  if (a.adj_k && !a.staged) {
+  if (a.adj_k) {
     if (a.M == 2) {
       if (a.adj_k == 4) launch_pdl(k_vertex_packed<2, 4>, g, blk, 0, s, a, lab_in, lab_out, t);
       else launch_pdl(k_vertex_packed<2, 8>, g, blk, 0, s, a, lab_in, lab_out, t);
@@ -1448,13 +1190,6 @@ void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_
       if (a.adj_k == 4) launch_pdl(k_vertex_packed<0, 4>, g, blk, 0, s, a, lab_in, lab_out, t);
       else launch_pdl(k_vertex_packed<0, 8>, g, blk, 0, s, a, lab_in, lab_out, t);
     }
-    return;
-  }
-  if (a.staged && whole) {
-    if (a.M == 2)  // M = 2 is specialised; other M share the counted-compare loop
-      launch_pdl(k_vertex_staged<2>, g, blk, 0, s, a, lab_in, lab_out, t);
-    else
-      launch_pdl(k_vertex_staged<0>, g, blk, 0, s, a, lab_in, lab_out, t);
     return;
   }
 #define VA_ARGS                                                                                \
@@ -1475,17 +1210,13 @@ void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_
 
 void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s) {
   const dim3 g(grid_for(a.h_end - a.h_begin, kHoodThreads)), blk(kHoodThreads);
-  const bool whole = a.h_begin == 0 && a.h_end == a.Hs;
-  if (a.hood_k && !a.staged) {
+  if (a.hood_k) {
     if (a.hood_k == 8) launch_pdl(k_hood_packed<8>, g, blk, 0, s, a, t);
     else if (a.hood_k == 12) launch_pdl(k_hood_packed<12>, g, blk, 0, s, a, t);
     else launch_pdl(k_hood_packed<16>, g, blk, 0, s, a, t);
     return;
   }
-  if (a.staged && whole)
-    launch_pdl(k_hood_staged, g, blk, 0, s, a, t);
-  else
-    launch_pdl(k_hood_sums, g, blk, 0, s, a.s_off, a.h_mem, (const double*)a.minE, a.hist,
+  launch_pdl(k_hood_sums, g, blk, 0, s, a.s_off, a.h_mem, (const double*)a.minE, a.hist,
                a.flags, a.Hs, t, a.L, a.ring, a.tol, a.unconv, a.fixed, a.h_begin, a.h_end);
 }
 
@@ -1525,7 +1256,7 @@ __device__ __forceinline__ void load_i16(const int16_t* __restrict__ p, int16_t 
 // overlap the predecessor's drain -- and the skip decision (the previous
 // iteration's unconverged counter) is read beside the first dependent loads
 // rather than ahead of them: one memory round trip less per launch.
-template <int MT, int K, int P = 1, bool DICT = false>
+template <int MT, int K, int P = 1>
 __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
                                                    const uint8_t* __restrict__ lab_in,
                                                    uint8_t* __restrict__ lab_out,
@@ -1535,26 +1266,12 @@ __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
   const uint32_t v0 = a.v_begin + blk * (kVtxThreads * P) + threadIdx.x;
   int16_t d[P][K];
   uint8_t old[P], cov[P];
-  if constexpr (DICT) {  // pattern ids first, then the (L1-resident) patterns
-    uint32_t c[P];
 #pragma unroll
-    for (int j = 0; j < P; ++j) {
-      const uint32_t v = v0 + j * kVtxThreads;
-      c[j] = v < a.v_end ? a.vcode[v] : kDictNone;
-    }
-#pragma unroll
-    for (int j = 0; j < P; ++j) {
-      cov[j] = c[j] != kDictNone;
-      if (cov[j]) load_i16<K>(a.adj_pat + c[j] * K, d[j]);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < P; ++j) {
-      const uint32_t v = v0 + j * kVtxThreads;
-      if (v < a.v_end) {
-        load_i16<K>(a.adj_pk + uint64_t(v) * K, d[j]);
-        cov[j] = a.cover[v];
-      }
+  for (int j = 0; j < P; ++j) {
+    const uint32_t v = v0 + j * kVtxThreads;
+    if (v < a.v_end) {
+      load_i16<K>(a.adj_pk + uint64_t(v) * K, d[j]);
+      cov[j] = a.cover[v];
     }
   }
   pdl_wait();
@@ -1664,9 +1381,8 @@ __device__ __forceinline__ void load_hood_row(const uint16_t* __restrict__ row,
 
 // One hood's sum (left fold of its members' minima in slot order,
 // engine.cpp:147-152) + record + window test (engine.cpp:154-169); returns 1
-// when the hood is not converged.  CG: minima read around L1 (written by
-// other blocks of the same launch, k_map_flow).
-template <int K, bool CG>
+// when the hood is not converged.
+template <int K>
 __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restrict__ minE, int t,
                                          uint64_t h, uint32_t base, const uint32_t (&u)[K / 2]) {
   const int R1 = a.ring;
@@ -1690,9 +1406,9 @@ __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restr
 #pragma unroll
   for (int k = 0; k < K; ++k) {  // all gathers in flight before the fold
     const uint32_t dk = (u[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
-    e[k] = dk != 0xFFFFu ? (CG ? __ldcg(minE + base + dk) : minE[base + dk]) : 0.0;
+    e[k] = dk != 0xFFFFu ? minE[base + dk] : 0.0;
   }
-  double sum = CG ? __ldcg(minE + base) : minE[base];
+  double sum = minE[base];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const uint32_t dk = (u[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
@@ -1722,7 +1438,7 @@ __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restr
 
 // (static structure before griddepcontrol.wait, skip decision beside the
 // first dependent loads -- see vertex_packed_body)
-template <int K, bool DICT = false>
+template <int K>
 __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
                                                  const double* __restrict__ minE, int t,
                                                  uint32_t blk, int skip_t) {
@@ -1732,22 +1448,14 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
   uint32_t base = 0;
   uint32_t u[K / 2];
   if (live) {
-    const uint16_t* row;
-    if constexpr (DICT) {
-      const uint32_t c = a.hcode[h];
-      base = c & 0xFFFFFFu;
-      row = a.hood_pat + (c >> 24) * K;
-    } else {
-      base = a.hood_base[h];
-      row = a.hood_pk + h * K;
-    }
-    load_hood_row<K>(row, u);
+    base = a.hood_base[h];
+    load_hood_row<K>(a.hood_pk + h * K, u);
   }
   pdl_wait();
   int not_conv = 0;
   if (live) {
     if (map_iter_skipped(a.unconv, skip_t, a.fixed)) return;  // uniform over the grid
-    not_conv = hood_eval<K, false>(a, minE, t, h, base, u);
+    not_conv = hood_eval<K>(a, minE, t, h, base, u);
   }
   if (!live && map_iter_skipped(a.unconv, skip_t, a.fixed)) return;
   const int bu = __syncthreads_count(not_conv);
@@ -1767,7 +1475,7 @@ __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) 
 // iteration, the speculative pass only wrote buffers nothing reads any more
 // (labels into the buffer t-1 consumed, minima into the other half of the
 // double-buffered minima, label counts into the other parity slot).
-template <int MT, int KV, int KH, int VP, bool DICT>
+template <int MT, int KV, int KH, int VP>
 __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
@@ -1776,7 +1484,7 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
   static_assert(kVtxThreads == kTileThreads, "scatter tiles are vertex blocks");
   extern __shared__ uint32_t fused_smem[];
   if (blockIdx.x < nh) {
-    hood_packed_body<KH, DICT>(a, minE_prev, t - 1, blockIdx.x, t - 1);
+    hood_packed_body<KH>(a, minE_prev, t - 1, blockIdx.x, t - 1);
   } else if (blockIdx.x >= nh + nv) {
     // last launch (t = map_max): the M-step's label scatter runs beside the
     // hood pass of the last iteration -- it reads only the committed labels
@@ -1787,390 +1495,9 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
                                      sc.R, sc.M, sc.Hs, sc.mean, sc.counts, sc.tiles, sc.layout,
                                      sc.x, blockIdx.x - nh - nv, fused_smem);
   } else {
-    vertex_packed_body<MT, KV, VP, DICT>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh,
+    vertex_packed_body<MT, KV, VP>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh,
                                    t > 0 ? t - 1 : 0);
   }
-}
-
-// ---------------------------------------------------------------------------
-// Dataflow MAP loop (small graphs): the whole MAP loop of one EM iteration in
-// ONE launch whose blocks are all resident, synchronised point to point
-// instead of by launch boundaries.  Vertex-tile blocks run the vertex pass of
-// iteration t once the tiles their neighbors lie in have finished t-1
-// (per-tile progress flags, release/acquire at gpu scope); hood-tile blocks
-// fold iteration t once the tiles their members lie in have finished it.
-// The arithmetic is exactly that of the fused kernel (same bodies).
-//   * labels stay double-buffered: a tile overwrites the buffer its
-//     neighbors read one iteration earlier only after waiting for them (the
-//     graph is symmetric, and the dependency ranges are built from both edge
-//     directions), the minima are per iteration (map_max x R);
-//   * the early exit (optimize.cpp:59) is decided two iterations behind:
-//     iteration t starts once every hood tile has finished t-2 and no
-//     counter of 0..t-2 is zero; so iteration T (one past the exit) may run
-//     speculatively, writing only what nothing reads any more (as in the
-//     fused chain), and iteration T+1 never runs;
-//   * waits are bounded (2 s -> trap) so a broken dependency fails loudly.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t global_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// Poll relaxed (no L1 invalidation per poll), then one acquire load.
-__device__ __forceinline__ void spin_until_ge(const uint32_t* p, uint32_t need,
-                                              uint32_t sleep_ns = 32) {
-  if (ld_relaxed_u32(p) < need) {
-    const uint64_t t0 = global_ns();
-    while (ld_relaxed_u32(p) < need) {
-      if (sleep_ns) __nanosleep(sleep_ns);
-      if (global_ns() - t0 > 2000000000ull) __trap();
-    }
-  }
-  (void)ld_acquire_u32(p);
-}
-
-// Progress flags one per 128-byte line (polled by several blocks each).
-constexpr uint32_t kFlagStride = 32;
-
-// Block-wide: wait until flags[lo..hi] >= need.
-__device__ __forceinline__ void flow_wait(const uint32_t* flags, uint32_t lo, uint32_t hi,
-                                          uint32_t need, uint32_t sleep_ns) {
-  if (lo <= hi)
-    for (uint32_t i = lo + threadIdx.x; i <= hi; i += blockDim.x)
-      spin_until_ge(flags + uint64_t(i) * kFlagStride, need, sleep_ns);
-  __syncthreads();
-}
-
-// Block-uniform: does iteration t start (see above)?
-__device__ __forceinline__ bool flow_runs(const MapArgs& a, const FlowArgs& f, int t,
-                                          int* run_s) {
-  if (a.fixed || t < 2) return true;
-  if (threadIdx.x == 0) {
-    spin_until_ge(f.hdone + (t - 2) * kFlagStride, f.nht);
-    int run = 1;
-    for (int s = 0; s <= t - 2; ++s)  // (complete: ordered by the acquire above)
-      if (__ldcg(a.unconv + s) == 0) run = 0;
-    *run_s = run;
-  }
-  __syncthreads();
-  const int run = *run_s;
-  __syncthreads();
-  return run != 0;
-}
-
-template <int KV, int KH, int HP>
-__global__ void __launch_bounds__(kVtxThreads, HP <= 2 ? 6 : 4)
-    k_map_flow(MapArgs a, FlowArgs f, ScatterArgs sc) {
-  extern __shared__ uint32_t flow_smem[];
-  __shared__ int run_s;
-  __shared__ uint32_t ticket_s;
-  const uint32_t R = a.R;
-  if (blockIdx.x < f.nvt) {
-    // ---- vertex tile: its structure and means stay in registers ----
-    const uint32_t tile = blockIdx.x;
-    const uint32_t v = tile * kVtxThreads + threadIdx.x;
-    const bool live = v < R;
-    int16_t d[KV];
-    uint8_t cov = 0;
-    double x = 0.0;
-    if (live) {
-      load_i16<KV>(a.adj_pk + uint64_t(v) * KV, d);
-      cov = a.cover[v];
-      x = a.mean[v];
-    }
-    const uint32_t lo = f.vdep[2 * tile], hi = f.vdep[2 * tile + 1];
-    pdl_wait();
-    if (em_skipped(a.unconv)) return;  // (uniform: no flag was touched)
-    for (int t = 0; t < f.map_max; ++t) {
-      if (!flow_runs(a, f, t, &run_s)) break;
-      if (t > 0) flow_wait(f.vflag, lo, hi, uint32_t(t), f.sleep_ns);
-      const uint8_t* lin = (t & 1) ? f.lab_b : f.lab_a;
-      uint8_t* lout = (t & 1) ? f.lab_a : f.lab_b;
-      uint32_t nl = 0;
-      if (live) {
-        const uint32_t old = __ldcg(lin + v);
-        if (!cov) {
-          lout[v] = static_cast<uint8_t>(old);
-          nl = old;
-        } else {
-          uint32_t ones = 0, deg = 0;
-#pragma unroll
-          for (int k = 0; k < KV; ++k) {
-            const bool ok = d[k] != INT16_MIN;
-            deg += ok;
-            ones += ok && __ldcg(lin + int64_t(v) + d[k]) == 1;
-          }
-          const double* T = a.terms;
-          const double e0 = label_energy(x, T[0], T[2], T[4], a.beta, ones);
-          const double e1 = label_energy(x, T[1], T[3], T[5], a.beta, deg - ones);
-          const bool one = e1 < e0;
-          f.minE_all[uint64_t(t) * R + v] = one ? e1 : e0;
-          lout[v] = one ? 1 : 0;
-          nl = one;
-        }
-      }
-      // one barrier: the block's label / minimum stores, then the release;
-      // the tile's label counts (M-step) follow off the critical path
-      const int ones = __syncthreads_count(live && nl == 1u);
-      if (threadIdx.x == 0) {
-        st_release_u32(f.vflag + uint64_t(tile) * kFlagStride, uint32_t(t + 1));
-        const uint32_t nlive = min(R - tile * kVtxThreads, uint32_t(kVtxThreads));
-        uint32_t* out = a.tile_counts + (uint64_t(t & 1) * a.tiles + tile) * 2;
-        out[0] = nlive - uint32_t(ones);
-        out[1] = uint32_t(ones);
-      }
-    }
-  } else {
-    // ---- hood tile: HP x 256 consecutive series ----
-    const uint32_t j = blockIdx.x - f.nvt;
-    uint32_t base[HP];
-    uint32_t u[HP][KH / 2];
-    bool live[HP];
-#pragma unroll
-    for (int q = 0; q < HP; ++q) {
-      const uint64_t h = (uint64_t(j) * HP + q) * kHoodThreads + threadIdx.x;
-      live[q] = h < a.Hs;
-      base[q] = 0;
-      if (live[q]) {
-        base[q] = a.hood_base[h];
-        const uint4* src = reinterpret_cast<const uint4*>(a.hood_pk + h * KH);
-#pragma unroll
-        for (int w = 0; w < KH / 8; ++w) {
-          const uint4 x4 = src[w];
-          u[q][4 * w] = x4.x;
-          u[q][4 * w + 1] = x4.y;
-          u[q][4 * w + 2] = x4.z;
-          u[q][4 * w + 3] = x4.w;
-        }
-      }
-    }
-    const uint32_t lo = f.hdep[2 * j], hi = f.hdep[2 * j + 1];
-    pdl_wait();
-    if (em_skipped(a.unconv)) return;
-    for (int t = 0; t < f.map_max; ++t) {
-      if (!flow_runs(a, f, t, &run_s)) break;
-      flow_wait(f.vflag, lo, hi, uint32_t(t + 1), f.sleep_ns);
-      const double* minE = f.minE_all + uint64_t(t) * R;
-      int nc = 0;
-#pragma unroll
-      for (int q = 0; q < HP; ++q)
-        if (live[q])
-          nc += hood_eval<KH, true>(a, minE, t, (uint64_t(j) * HP + q) * kHoodThreads + threadIdx.x,
-                                    base[q], u[q]);
-      const int bu = __syncthreads_count(nc);
-      if (threadIdx.x == 0) {
-        if (bu) atomicAdd(&a.unconv[t], uint32_t(bu));
-        red_release_add(f.hdone + t * kFlagStride, 1u);
-      }
-    }
-  }
-  const uint32_t total = f.nvt + f.nht;
-  uint32_t* done = f.ticket + kFlagStride;
-  __syncthreads();
-  if (sc.layout) {
-    // the M-step's label scatter: every block's loop is over (all counters
-    // final, so the executed iteration count is known), vertex tiles group
-    if (threadIdx.x == 0) red_release_add(done, 1u);
-    if (blockIdx.x < f.nvt) {
-      if (threadIdx.x == 0) spin_until_ge(done, total, f.sleep_ns);
-      __syncthreads();
-      label_scatter_small_body<false>(sc.lab_even, sc.lab_odd, a.unconv, a.unconv, f.map_max,
-                                      a.fixed, sc.R, sc.M, sc.Hs, sc.mean, sc.counts, sc.tiles,
-                                      sc.layout, sc.x, blockIdx.x, flow_smem);
-      __syncthreads();
-    }
-  }
-  // the last block out re-arms the flags for the next launch
-  if (threadIdx.x == 0) {
-    __threadfence();
-    ticket_s = atomicAdd(f.ticket, 1u);
-  }
-  __syncthreads();
-  if (ticket_s == total - 1) {
-    __threadfence();
-    for (uint32_t i = threadIdx.x; i < f.nvt; i += blockDim.x) f.vflag[uint64_t(i) * kFlagStride] = 0;
-    for (int i = threadIdx.x; i < f.map_max; i += blockDim.x) f.hdone[i * kFlagStride] = 0;
-    if (threadIdx.x == 0) {
-      *done = 0;
-      *f.ticket = 0;
-    }
-  }
-}
-
-// Dependency ranges: vdep[2i..2i+1] = first/last vertex tile adjacent to tile
-// i (either edge direction, and i itself); hdep[2j..] = first/last vertex
-// tile holding a member of hood tile j.  (Pre-set to {~0, 0}.)
-__global__ void k_flow_deps(const uint32_t* __restrict__ g_off, const uint32_t* __restrict__ g_nbr,
-                            uint32_t R, const uint32_t* __restrict__ s_off,
-                            const uint32_t* __restrict__ h_mem, uint64_t Hs, uint32_t hood_tile,
-                            uint32_t* vdep, uint32_t* hdep) {
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < R; v += stride) {
-    const uint32_t tv = uint32_t(v / kVtxThreads);
-    uint32_t lo = tv, hi = tv;
-    for (uint32_t i = g_off[v]; i < g_off[v + 1]; ++i) {
-      const uint32_t tu = g_nbr[i] / kVtxThreads;
-      lo = min(lo, tu);
-      hi = max(hi, tu);
-      if (tu != tv) {  // the reverse direction
-        atomicMin(vdep + 2 * tu, tv);
-        atomicMax(vdep + 2 * tu + 1, tv);
-      }
-    }
-    atomicMin(vdep + 2 * tv, lo);
-    atomicMax(vdep + 2 * tv + 1, hi);
-  }
-  for (uint64_t h = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; h < Hs; h += stride) {
-    const uint32_t lo = s_off[h], hi = s_off[h + 1];
-    if (hi <= lo) continue;
-    uint32_t mn = h_mem[lo], mx = h_mem[lo];
-    for (uint32_t i = lo + 1; i < hi; ++i) {
-      mn = min(mn, h_mem[i]);
-      mx = max(mx, h_mem[i]);
-    }
-    const uint64_t j = h / hood_tile;
-    atomicMin(hdep + 2 * j, mn / kVtxThreads);
-    atomicMax(hdep + 2 * j + 1, mx / kVtxThreads);
-  }
-}
-
-__global__ void k_fill_pairs(uint32_t* p, uint64_t n) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) {
-    p[2 * i] = 0xFFFFFFFFu;
-    p[2 * i + 1] = 0;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Streamed hood pass (opt-in): the fused launch's hood blocks become
-// persistent (G per SM-slot budget), each looping over 256-hood tiles; the
-// next tile's packed rows (first members + deltas, two contiguous ranges)
-// are fetched by one thread with cp.async.bulk into the other half of a
-// double buffer, completion tracked by an mbarrier with expect_tx -- the
-// static structure's DRAM latency overlaps the current tile's gathers.
-// Arithmetic: hood_eval, unchanged.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  const uint64_t t0 = global_ns();
-  while (!done) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
-        "selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(smem_addr(bar)), "r"(phase)
-        : "memory");
-    if (!done && global_ns() - t0 > 2000000000ull) __trap();
-  }
-}
-
-template <int K>
-struct StreamSmem {
-  uint32_t base[2][kHoodThreads];
-  uint16_t pk[2][kHoodThreads * K];
-  uint64_t bar[2];
-};
-
-template <int K>
-__device__ __forceinline__ void stream_issue(const MapArgs& a, StreamSmem<K>& sm, uint64_t tile,
-                                             int buf) {
-  const uint64_t h0 = a.h_begin + tile * kHoodThreads;  // (rows padded to whole tiles)
-  constexpr uint32_t kBase = kHoodThreads * 4, kRows = kHoodThreads * K * 2;
-  mbar_expect_tx(&sm.bar[buf], kBase + kRows);
-  bulk_g2s(sm.base[buf], a.hood_base + h0, kBase, &sm.bar[buf]);
-  bulk_g2s(sm.pk[buf], a.hood_pk + h0 * K, kRows, &sm.bar[buf]);
-}
-
-template <int K>
-__device__ __forceinline__ void hood_stream_body(const MapArgs& a, const double* minE, int t,
-                                                 uint32_t slot, uint32_t nslots, int skip_t) {
-  static_assert(K == 8 || K == 16, "streamed rows: 16-byte deltas");
-  __shared__ __align__(128) StreamSmem<K> sm;
-  const uint64_t ntiles = (a.h_end - a.h_begin + kHoodThreads - 1) / kHoodThreads;
-  if (threadIdx.x == 0) {
-    mbar_init(&sm.bar[0]);
-    mbar_init(&sm.bar[1]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (slot >= ntiles) return;
-  if (threadIdx.x == 0) stream_issue<K>(a, sm, slot, 0);
-  pdl_wait();
-  const bool skip = map_iter_skipped(a.unconv, skip_t, a.fixed);  // (uniform)
-  uint32_t k = 0;
-  for (uint64_t tile = slot; tile < ntiles; tile += nslots, ++k) {
-    const int buf = k & 1;
-    const uint64_t next = tile + nslots;
-    if (!skip && threadIdx.x == 0 && next < ntiles) stream_issue<K>(a, sm, next, buf ^ 1);
-    mbar_wait(&sm.bar[buf], (k >> 1) & 1);
-    if (skip) return;  // (the only copy in flight has landed)
-    const uint64_t h = a.h_begin + tile * kHoodThreads + threadIdx.x;
-    int not_conv = 0;
-    if (h < a.h_end) {
-      uint32_t u[K / 2];
-      const uint4* src = reinterpret_cast<const uint4*>(sm.pk[buf] + threadIdx.x * K);
-#pragma unroll
-      for (int q = 0; q < K / 8; ++q) {
-        const uint4 w = src[q];
-        u[4 * q] = w.x;
-        u[4 * q + 1] = w.y;
-        u[4 * q + 2] = w.z;
-        u[4 * q + 3] = w.w;
-      }
-      not_conv = hood_eval<K, false>(a, minE, t, h, sm.base[buf][threadIdx.x], u);
-    }
-    // (also: every thread is done with buffer buf before it is refilled)
-    const int bu = __syncthreads_count(not_conv);
-    if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[t], uint32_t(bu));
-  }
-}
-
-template <int MT, int KV, int KH, int VP>
-__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH))
-    k_map_fused_stream(MapArgs a, const uint8_t* __restrict__ lab_in,
-                       uint8_t* __restrict__ lab_out, const double* __restrict__ minE_prev,
-                       double* __restrict__ minE_cur, int t, uint32_t nh, uint32_t nv) {
-  if (blockIdx.x < nh)
-    hood_stream_body<KH>(a, minE_prev, t - 1, blockIdx.x, nh, t - 1);
-  else
-    vertex_packed_body<MT, KV, VP, false>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh,
-                                          t > 0 ? t - 1 : 0);
 }
 
 // ---- pack builders ----
@@ -2232,126 +1559,6 @@ __global__ void k_pack_hoods(const uint32_t* __restrict__ s_off, const uint32_t*
     out[h * K + k] = lo + 1 + k < hi ? static_cast<uint16_t>(h_mem[lo + 1 + k] - b) : uint16_t(0xFFFF);
 }
 
-
-// ---- dictionary encoding (MapArgs::vcode / hcode) ----
-// Insert-or-find of one W-word key in the device hash set ws (linear probing;
-// slot state 0 empty / 1 being written / 2 ready).  The inserting thread
-// numbers the pattern and writes it to the pattern table.
-template <int W>
-__device__ uint32_t dict_insert(uint32_t* ws, const uint32_t (&key)[W], uint32_t* pat) {
-  uint32_t* state = ws + 2;
-  uint32_t* ids = ws + 2 + kDictCap;
-  uint32_t* keys = ws + 2 + 2 * kDictCap;
-  uint32_t hsh = 2166136261u;
-#pragma unroll
-  for (int w = 0; w < W; ++w) hsh = (hsh ^ key[w]) * 16777619u;
-  hsh ^= hsh >> 15;
-  uint32_t slot = hsh & (kDictCap - 1);
-  for (uint32_t probe = 0; probe < kDictCap; ++probe, slot = (slot + 1) & (kDictCap - 1)) {
-    uint32_t st = *reinterpret_cast<volatile uint32_t*>(state + slot);
-    if (st == 0) {
-      st = atomicCAS(state + slot, 0u, 1u);
-      if (st == 0) {
-        const uint32_t id = atomicAdd(ws, 1u);
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          keys[slot * W + w] = key[w];
-          if (id < kDictMax) pat[id * W + w] = key[w];
-        }
-        ids[slot] = id;
-        __threadfence();
-        atomicExch(state + slot, 2u);
-        if (id >= kDictMax) atomicExch(ws + 1, 1u);
-        return id;
-      }
-    }
-    while (st != 2) st = *reinterpret_cast<volatile uint32_t*>(state + slot);
-    __threadfence();
-    bool eq = true;
-#pragma unroll
-    for (int w = 0; w < W; ++w)
-      eq &= reinterpret_cast<volatile uint32_t*>(keys)[slot * W + w] == key[w];
-    if (eq) return reinterpret_cast<volatile uint32_t*>(ids)[slot];
-  }
-  atomicExch(ws + 1, 1u);
-  return kDictMax;
-}
-
-// Warp-cooperative lookup: one insert per distinct key of the warp (the
-// lanes of a grid row mostly share one pattern).  All 32 lanes call it.
-template <int W>
-__device__ uint32_t dict_lookup_warp(uint32_t* ws, const uint32_t (&key)[W], bool active,
-                                     uint32_t* pat) {
-  const int lane = threadIdx.x & 31;
-  uint32_t pending = __ballot_sync(0xFFFFFFFFu, active);
-  uint32_t mine = kDictMax;
-  while (pending) {
-    const int leader = __ffs(pending) - 1;
-    bool eq = true;
-#pragma unroll
-    for (int w = 0; w < W; ++w) eq &= __shfl_sync(0xFFFFFFFFu, key[w], leader) == key[w];
-    const uint32_t m = __ballot_sync(0xFFFFFFFFu, eq && active) & pending;
-    uint32_t id = 0;
-    if (lane == leader) id = dict_insert<W>(ws, key, pat);
-    id = __shfl_sync(0xFFFFFFFFu, id, leader);
-    if ((m >> lane) & 1u) mine = id;
-    pending &= ~m;
-  }
-  return mine;
-}
-
-// vcode[v] = id of v's k_pack_adjacency delta vector; kDictNone for vertices
-// in no hood (the MAP kernel never reads their neighbors).
-template <int K>
-__global__ void k_dict_adjacency(const uint32_t* __restrict__ g_off,
-                                 const uint32_t* __restrict__ g_nbr, uint32_t R,
-                                 const uint8_t* __restrict__ cover, uint32_t* ws,
-                                 uint8_t* __restrict__ vcode, uint32_t* pat) {
-  constexpr int W = K / 2;
-  const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool active = v < R && cover[v];
-  uint32_t key[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) key[w] = 0;
-  if (active) {
-    const uint32_t lo = g_off[v], hi = g_off[v + 1];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int16_t d = lo + k < hi ? static_cast<int16_t>(int64_t(g_nbr[lo + k]) - int64_t(v))
-                                    : int16_t(INT16_MIN);
-      key[k >> 1] |= uint32_t(static_cast<uint16_t>(d)) << (16 * (k & 1));
-    }
-  }
-  const uint32_t id = dict_lookup_warp<W>(ws, key, active, pat);
-  if (v < R) vcode[v] = active && id < kDictMax ? static_cast<uint8_t>(id) : kDictNone;
-}
-
-// hcode[h] = first member | id << 24 of h's k_pack_hoods delta vector
-// (callers guarantee R <= 2^24).
-template <int K>
-__global__ void k_dict_hoods(const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ h_mem,
-                             uint64_t Hs, uint32_t* ws, uint32_t* __restrict__ hcode,
-                             uint32_t* pat) {
-  constexpr int W = K / 2;
-  const uint64_t h = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool active = h < Hs;
-  uint32_t key[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) key[w] = 0;
-  uint32_t b = 0;
-  if (active) {
-    const uint32_t lo = s_off[h], hi = s_off[h + 1];
-    b = h_mem[lo];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t d = lo + 1 + k < hi ? (h_mem[lo + 1 + k] - b) & 0xFFFFu : 0xFFFFu;
-      key[k >> 1] |= d << (16 * (k & 1));
-    }
-  }
-  const uint32_t id = dict_lookup_warp<W>(ws, key, active, pat);
-  if (active) hcode[h] = b | ((id < kDictMax ? id : 0u) << 24);
-}
-
 }  // namespace
 
 void launch_pack_stats(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, uint64_t A,
@@ -2385,120 +1592,6 @@ void launch_pack_hoods(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs
   CK_LAUNCH();
 }
 
-int flow_plan(const MapArgs& a, uint32_t* nvt, uint32_t* nht) {
-  if (a.M != 2 || a.adj_k != 4 || a.hood_k != 8 || a.v_begin != 0 || a.v_end != a.R ||
-      a.h_begin != 0 || a.h_end != a.Hs || a.R == 0 || a.flags)
-    return 0;
-  static int cap[3] = {-1, -1, -1};
-  static std::mutex mu;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    if (cap[0] < 0) {
-      int dev = 0, sms = 0, b1 = 0, b2 = 0, b4 = 0;
-      CK(cudaGetDevice(&dev));
-      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_map_flow<4, 8, 1>, kVtxThreads, scatter_small_smem(2)));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_map_flow<4, 8, 2>, kVtxThreads, scatter_small_smem(2)));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_map_flow<4, 8, 4>, kVtxThreads, scatter_small_smem(2)));
-      cap[0] = b1 * sms;
-      cap[1] = b2 * sms;
-      cap[2] = b4 * sms;
-    }
-  }
-  const uint64_t v = (uint64_t(a.R) + kVtxThreads - 1) / kVtxThreads;
-  for (int i = 0, hp = 1; i < 3; ++i, hp *= 2) {
-    const uint64_t h = (a.Hs + uint64_t(kHoodThreads) * hp - 1) / (uint64_t(kHoodThreads) * hp);
-    if (v + h <= uint64_t(cap[i])) {
-      *nvt = uint32_t(v);
-      *nht = uint32_t(h);
-      return hp;
-    }
-  }
-  return 0;
-}
-
-void launch_flow_deps(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R,
-                      const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, int hp,
-                      uint32_t nvt, uint32_t nht, uint32_t* vdep, uint32_t* hdep, cudaStream_t s) {
-  k_fill_pairs<<<grid_for(nvt, 256), 256, 0, s>>>(vdep, nvt);
-  CK_LAUNCH();
-  if (nht) {
-    k_fill_pairs<<<grid_for(nht, 256), 256, 0, s>>>(hdep, nht);
-    CK_LAUNCH();
-  }
-  const uint64_t work = std::max<uint64_t>(std::max<uint64_t>(R, Hs), 1);
-  k_flow_deps<<<std::min<unsigned>(grid_for(work, 256), 8 * kNumSMs), 256, 0, s>>>(
-      g_off, g_nbr, R, s_off, h_mem, Hs, uint32_t(kHoodThreads * hp), vdep, hdep);
-  CK_LAUNCH();
-}
-
-void launch_map_flow(const MapArgs& a, const FlowArgs& f, int hp, const ScatterArgs* sc,
-                     cudaStream_t s) {
-  const dim3 g(f.nvt + f.nht), blk(kVtxThreads);
-  const ScatterArgs scv = sc ? *sc : ScatterArgs{};
-  const size_t smem = sc ? scatter_small_smem(sc->M) : 0;
-  if (hp == 1) launch_pdl(k_map_flow<4, 8, 1>, g, blk, smem, s, a, f, scv);
-  else if (hp == 2) launch_pdl(k_map_flow<4, 8, 2>, g, blk, smem, s, a, f, scv);
-  else launch_pdl(k_map_flow<4, 8, 4>, g, blk, smem, s, a, f, scv);
-}
-
-void launch_dict_adjacency(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, int k,
-                           const uint8_t* cover, uint32_t* ws, uint8_t* vcode, int16_t* pat,
-                           cudaStream_t s) {
-  CK(cudaMemsetAsync(ws, 0, (2 + kDictCap) * sizeof(uint32_t), s));  // counters + slot states
-  if (!R) return;
-  uint32_t* p = reinterpret_cast<uint32_t*>(pat);
-  if (k == 4)
-    k_dict_adjacency<4><<<grid_for(R, 256), 256, 0, s>>>(g_off, g_nbr, R, cover, ws, vcode, p);
-  else
-    k_dict_adjacency<8><<<grid_for(R, 256), 256, 0, s>>>(g_off, g_nbr, R, cover, ws, vcode, p);
-  CK_LAUNCH();
-}
-
-void launch_dict_hoods(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, int k,
-                       uint32_t* ws, uint32_t* hcode, uint16_t* pat, cudaStream_t s) {
-  CK(cudaMemsetAsync(ws, 0, (2 + kDictCap) * sizeof(uint32_t), s));
-  if (!Hs) return;
-  uint32_t* p = reinterpret_cast<uint32_t*>(pat);
-  if (k == 8)
-    k_dict_hoods<8><<<grid_for(Hs, 256), 256, 0, s>>>(s_off, h_mem, Hs, ws, hcode, p);
-  else if (k == 12)
-    k_dict_hoods<12><<<grid_for(Hs, 256), 256, 0, s>>>(s_off, h_mem, Hs, ws, hcode, p);
-  else
-    k_dict_hoods<16><<<grid_for(Hs, 256), 256, 0, s>>>(s_off, h_mem, Hs, ws, hcode, p);
-  CK_LAUNCH();
-}
-
-// Cooperative launch of k_map_loop; grid = co-resident blocks (<= work tiles).
-void launch_map_loop(const MapArgs& a, uint8_t* lab_even, uint8_t* lab_odd, double* minE0,
-                     double* minE1, int map_max, cudaStream_t s) {
-  static int max_blocks[9] = {0};
-  const int mi = a.M <= 8 ? int(a.M) : 0;
-  void (*fn)(MapArgs, uint8_t*, uint8_t*, double*, double*, int);
-  switch (mi) {
-    case 2: fn = k_map_loop<2>; break;
-    case 3: fn = k_map_loop<3>; break;
-    case 4: fn = k_map_loop<4>; break;
-    case 5: fn = k_map_loop<5>; break;
-    case 6: fn = k_map_loop<6>; break;
-    case 7: fn = k_map_loop<7>; break;
-    case 8: fn = k_map_loop<8>; break;
-    default: fn = k_map_loop<0>; break;
-  }
-  if (!max_blocks[mi]) {
-    int per_sm = 0, dev = 0, sms = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kVtxThreads, 0));
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    max_blocks[mi] = per_sm * sms;
-  }
-  const uint64_t tiles = (uint64_t(a.R) + kVtxThreads - 1) / kVtxThreads +
-                         (a.Hs + kHoodThreads - 1) / kHoodThreads;
-  const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, max_blocks[mi])));
-  MapArgs args = a;
-  void* params[] = {&args, &lab_even, &lab_odd, &minE0, &minE1, &map_max};
-  CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid), dim3(kVtxThreads), params, 0, s));
-}
 
 namespace {
 

@@ -25,7 +25,6 @@ struct MapArgs {
   int L;         // convergence_window
   int ring;      // rows of the hood-energy ring (L+1, or map_max for the full trace)
   int fixed;     // 1 = no early exit
-  int staged;    // 1 = shared-memory staged tiles (default), 0 = one thread per item
   // Packed static structure (built once by launch_pack_*; k == 0: CSR only).
   //   adjacency: adj_k (4|8) int16 deltas u - v per vertex, INT16_MIN = none
   //   hoods: hood_base[h] = first (smallest) member, hood_pk[h*hood_k + j] =
@@ -35,20 +34,6 @@ struct MapArgs {
   const uint32_t* hood_base;
   const uint16_t* hood_pk;
   int hood_k;
-  // Dictionary form of the packed structure (launch_dict_*; nullptr = off).
-  // The vertices and hoods of an oversegmentation share a handful of delta
-  // patterns, so each stores only a pattern id: vcode[v] (kDictNone = in no
-  // hood) selects adj_pat[id*adj_k ..], hcode[h] = first member | id << 24
-  // selects hood_pat[id*hood_k ..].  1 + 4 instead of 8 + 1 + 20 bytes per
-  // vertex + hood; read by the fused MAP kernel.
-  const uint8_t* vcode;
-  const int16_t* adj_pat;
-  const uint32_t* hcode;
-  const uint16_t* hood_pat;
-  // Streamed hood pass (opt-in, DPMRF_STREAM=<hood blocks per SM>, 0 = off):
-  // persistent hood blocks prefetch the next tile's packed rows with
-  // cp.async.bulk into shared memory while folding the current one.
-  int stream_hb;
   // Owned ranges (vertex-range partitioning; [0,R) and [0,Hs) on one GPU).
   // Arrays stay globally indexed; v_begin is a multiple of 256.
   uint32_t v_begin, v_end;
@@ -113,10 +98,6 @@ bool mstep_tail_fusable(uint32_t R, uint32_t M);
 void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
                       const double* minE_prev, double* minE_cur, int t, int map_max,
                       cudaStream_t s, const ScatterArgs* sc = nullptr);
-// The whole MAP loop of one EM iteration as one cooperative kernel (see engine.cu).
-void launch_map_loop(const MapArgs& a, uint8_t* lab_even, uint8_t* lab_odd, double* minE0,
-                     double* minE1, int map_max, cudaStream_t s);
-
 struct MStepBuffers {
   DevBuf<uint32_t> counts;       // 2 x tiles x M label counts (slot = MAP iteration parity)
   DevBuf<uint32_t> tile_base;    // tiles x M
@@ -199,46 +180,6 @@ void launch_pack_adjacency(const uint32_t* g_off, const uint32_t* g_nbr, uint32_
                            int16_t* out, cudaStream_t s);
 void launch_pack_hoods(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, int k,
                        uint32_t* base, uint16_t* out, cudaStream_t s);
-// Dataflow MAP loop (engine.cu k_map_flow): one launch per EM iteration's
-// MAP loop, tiles synchronised by progress flags.  Grids that fit resident.
-struct FlowArgs {
-  uint32_t nvt, nht;          // vertex-tile blocks, hood-tile blocks
-  const uint32_t* vdep;       // 2 per vertex tile: first / last vertex tile it depends on
-  const uint32_t* hdep;       // 2 per hood tile: first / last vertex tile of its members
-  uint32_t* vflag;            // nvt: iterations finished (zero between launches)
-  uint32_t* hdone;            // map_max: hood tiles finished with iteration t
-  uint32_t* ticket;           // 1
-  double* minE_all;           // map_max x R minima, per iteration
-  uint8_t* lab_a;             // labels before iteration 0 (iteration t reads a if t even)
-  uint8_t* lab_b;
-  int map_max;
-  uint32_t sleep_ns;          // poll back-off
-};
-// hoods per thread (1/2/4) of a co-resident flow grid for this MapArgs, or 0
-// (not supported: M != 2, other pack widths, ranges, full trace, too large).
-int flow_plan(const MapArgs& a, uint32_t* nvt, uint32_t* nht);
-void launch_flow_deps(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R,
-                      const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, int hp,
-                      uint32_t nvt, uint32_t nht, uint32_t* vdep, uint32_t* hdep, cudaStream_t s);
-struct ScatterArgs;
-// sc: the M-step's label scatter joins the launch (mstep_tail_fusable graphs)
-void launch_map_flow(const MapArgs& a, const FlowArgs& f, int hp, const ScatterArgs* sc,
-                     cudaStream_t s);
-
-// Dictionary encoding of the packed layouts (MapArgs::vcode / hcode): a
-// device hash set of the distinct delta patterns (<= kDictMax), built in one
-// pass; ws[0] = patterns found, ws[1] = 1 when they do not fit (the caller
-// then keeps the plain packed layout).  ws holds dict_ws_words() u32 and is
-// cleared by the launch.
-constexpr uint32_t kDictCap = 1024;  // hash slots
-constexpr uint32_t kDictMax = 255;   // pattern ids 0..254; 255 = none / overflow
-constexpr uint8_t kDictNone = 255;
-constexpr size_t dict_ws_words() { return 2 + 2 * kDictCap + 8 * kDictCap; }
-void launch_dict_adjacency(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, int k,
-                           const uint8_t* cover, uint32_t* ws, uint8_t* vcode, int16_t* pat,
-                           cudaStream_t s);
-void launch_dict_hoods(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, int k,
-                       uint32_t* ws, uint32_t* hcode, uint16_t* pat, cudaStream_t s);
 // Offsets of the nonempty hoods (the runs reduce_by_key sees, engine.cpp:150).
 void launch_series_offsets(const uint32_t* h_off, uint64_t H, uint64_t S, uint32_t* s_off,
                            DevBuf<uint32_t>& tmp, ScanWorkspace& ws, cudaStream_t s);

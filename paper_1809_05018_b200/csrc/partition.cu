@@ -532,19 +532,11 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
     a.L = L;
     a.ring = ring;
     a.fixed = fixed;
-    a.staged = 0;
     a.adj_k = packed ? ctx->adj_k : 0;
     a.adj_pk = ctx->adj_pk.get();
     a.hood_k = packed ? ctx->hood_k : 0;
     a.hood_base = ctx->hood_base.get();
     a.hood_pk = ctx->hood_pk.get();
-    a.stream_hb = ctx->stream_hb;
-    if (packed && ctx->dict_ok) {
-      a.vcode = ctx->vcode.get();
-      a.adj_pat = ctx->adj_pat.get();
-      a.hcode = ctx->hcode.get();
-      a.hood_pat = ctx->hood_pat.get();
-    }
     a.terms = p.terms.ensure(3 * M);
     a.minE = p.minE.ensure(R ? R : 1);
     a.hist = p.hist.ensure(uint64_t(ring) * (Hs ? Hs : 1));

@@ -31,8 +31,8 @@ DPMRF_OK, DPMRF_INPUT_ERROR, DPMRF_INVALID_ARGUMENT, DPMRF_OUT_OF_RANGE = 0, 1, 
 DPMRF_CUDA_ERROR, DPMRF_NCCL_ERROR, DPMRF_INTERNAL_ERROR = 4, 5, 6
 
 TRACE_NONE, TRACE_EM, TRACE_FULL = 0, 1, 2
-RUN_FIXED_WORK, RUN_MULTILABEL, RUN_KERNEL_TIMING, RUN_TWO_KERNELS, RUN_NO_GRAPH = 1, 2, 4, 8, 16
-RUN_PERSISTENT, RUN_STAGED, RUN_HOST_LOG, RUN_CSR, RUN_UNFUSED = 32, 64, 128, 256, 512
+RUN_FIXED_WORK, RUN_MULTILABEL, RUN_KERNEL_TIMING, RUN_NO_GRAPH = 1, 2, 4, 16
+RUN_HOST_LOG, RUN_CSR, RUN_UNFUSED = 128, 256, 512
 
 K_SIGMA_FLOOR = 1e-3  # kSigmaFloor, model.hpp:9
 
@@ -211,6 +211,37 @@ class Backend:
         return Backend("cuda", device)
 
 
+# ---- full-trace destination ----------------------------------------------------------
+class TraceSink:
+    """Caller-owned buffers for the full trace (dpmrf_set_trace_sink): row
+    em * map_max_iters + t holds MAP iteration t of EM iteration em (hood
+    energies f64 / flags u8, ``stride`` values per row).  ``pinned`` allocates
+    page-locked memory (link-rate DMA straight from the device)."""
+
+    def __init__(self, energy: np.ndarray, flags: np.ndarray, rows: int, stride: int):
+        assert energy.dtype == np.float64 and flags.dtype == np.uint8
+        assert energy.size >= rows * stride and flags.size >= rows * stride
+        self.energy, self.flags, self.rows, self.stride = energy, flags, rows, stride
+        self.energy_rows = energy[:rows * stride].reshape(rows, stride)
+        self.flag_rows = flags[:rows * stride].reshape(rows, stride)
+
+    @classmethod
+    def host(cls, em_max_iters: int, map_max_iters: int, num_hoods: int) -> "TraceSink":
+        rows, stride = max(1, em_max_iters * map_max_iters), max(1, num_hoods)
+        return cls(np.empty(rows * stride), np.empty(rows * stride, np.uint8), rows, stride)
+
+    @classmethod
+    def pinned(cls, em_max_iters: int, map_max_iters: int, num_hoods: int, torch) -> "TraceSink":
+        rows, stride = max(1, em_max_iters * map_max_iters), max(1, num_hoods)
+        e = torch.empty(rows * stride, dtype=torch.float64).pin_memory().numpy()
+        f = torch.empty(rows * stride, dtype=torch.uint8).pin_memory().numpy()
+        return cls(e, f, rows, stride)
+
+    def fits(self, config, series: int) -> bool:
+        return (config is not None and self.rows >= config.em_max_iters * config.map_max_iters
+                and self.stride >= series)
+
+
 # ---- context: resident graph + hoods in HBM ---------------------------------------
 class Context:
     """One dpmrf_context: a CUDA stream plus the resident graph and hoods."""
@@ -229,6 +260,7 @@ class Context:
         self._cliques_n = (0, 0)
         self._img_n = 0  # pixels of the resident image (make_phantom)
         self._img_regions = 0  # regions of the resident label map (oversegment)
+        self._sink = None  # attached TraceSink (dpmrf_set_trace_sink)
 
     def close(self):
         if self.h:
@@ -431,38 +463,49 @@ class Context:
         return n.value
 
     # -- the optimization phase --
-    def optimize(self, config: OptimizerConfig, *, fixed_work=False, multilabel=None,
+    def optimize(self, config: OptimizerConfig, *, fixed_work=False, multilabel=False,
                  trace_level=TRACE_FULL, kernel_timing=False, labels_out=None,
-                 persistent=None, graphs=True, staged=False,
-                 host_log=False, csr=False, fused=True) -> OptimizeResult:
-        """persistent: None = library default, True = one cooperative MAP-loop
-        kernel per EM iteration, False = two kernels per MAP iteration."""
+                 graphs=True, host_log=False, csr=False, fused=True,
+                 trace_sink: Optional["TraceSink"] = None) -> OptimizeResult:
+        """optimize (optimize.cpp:31-74) on the resident graph + hoods.
+        multilabel=True allows num_labels != 2 (extension; the reference's
+        validate_config rejects it, optimize.cpp:14).  trace_sink: caller-owned
+        (pinned) buffers the full trace is streamed into (dpmrf_set_trace_sink);
+        the returned MapIterationLogs are views into it."""
         M = config.num_labels
-        if multilabel is None:
-            multilabel = M != 2
         flags = (RUN_FIXED_WORK if fixed_work else 0) | (RUN_MULTILABEL if multilabel else 0) | \
-            (RUN_KERNEL_TIMING if kernel_timing else 0) | \
-            ({None: 0, True: RUN_PERSISTENT, False: RUN_TWO_KERNELS}[persistent]) | \
-            (RUN_STAGED if staged else 0) | (RUN_HOST_LOG if host_log else 0) | \
+            (RUN_KERNEL_TIMING if kernel_timing else 0) | (RUN_HOST_LOG if host_log else 0) | \
             (RUN_CSR if csr else 0) | (0 if fused else RUN_UNFUSED) | \
             (0 if graphs else RUN_NO_GRAPH)
         opts = N.CRunOptions(flags, trace_level)
         cfg = config.c()
         labels = labels_out if labels_out is not None else np.zeros(self.R, np.uint32)
         mu, sigma = np.zeros(M), np.zeros(M)
+        self._attach(trace_sink)
         _check(self._lib.dpmrf_optimize(self.h, ct.byref(cfg), ct.byref(opts), N.ptr(labels),
                                         N.ptr(mu), N.ptr(sigma)), "optimize")
-        return OptimizeResult(labels, LabelParams(mu, sigma), self._trace(M, trace_level),
-                              self.stats())
+        return OptimizeResult(labels, LabelParams(mu, sigma),
+                              self._trace(M, trace_level, trace_sink, config), self.stats())
+
+    def _attach(self, sink: Optional["TraceSink"]):
+        if sink is None:
+            if self._sink is not None:
+                _check(self._lib.dpmrf_set_trace_sink(self.h, None, None, 0, 0), "trace_sink")
+                self._sink = None
+            return
+        if sink is not self._sink:
+            _check(self._lib.dpmrf_set_trace_sink(self.h, N.ptr(sink.energy), N.ptr(sink.flags),
+                                                  sink.rows, sink.stride), "trace_sink")
+            self._sink = sink
 
     def optimize_arrays(self, graph: RegionGraph, hoods: NeighborhoodSet,
-                        config: OptimizerConfig, *, fixed_work=False, multilabel=None,
-                        trace_level=TRACE_FULL, labels_out=None) -> OptimizeResult:
+                        config: OptimizerConfig, *, fixed_work=False, multilabel=False,
+                        trace_level=TRACE_FULL, labels_out=None,
+                        trace_sink: Optional["TraceSink"] = None) -> OptimizeResult:
         """optimize(backend, graph, hoods, config) in ONE C-ABI call
         (dpmrf_optimize_arrays): host arrays in, labels / params out."""
         M = config.num_labels
-        if multilabel is None:
-            multilabel = M != 2
+        self._attach(trace_sink)
         flags = (RUN_FIXED_WORK if fixed_work else 0) | (RUN_MULTILABEL if multilabel else 0)
         opts = N.CRunOptions(flags, trace_level)
         cfg = config.c()
@@ -476,15 +519,15 @@ class Context:
                                                ct.byref(cfg), ct.byref(opts), N.ptr(labels),
                                                N.ptr(mu), N.ptr(sigma)), "optimize_arrays")
         self.R, self.H, self.S = R, len(hoff) - 1, len(hmem)
-        self._graph_key, self._hoods_key = graph, hoods
-        return OptimizeResult(labels, LabelParams(mu, sigma), self._trace(M, trace_level),
-                              self.stats())
+        return OptimizeResult(labels, LabelParams(mu, sigma),
+                              self._trace(M, trace_level, trace_sink, config), self.stats())
 
-    def _trace(self, M, level) -> List[EmIterationLog]:
+    def _trace(self, M, level, sink=None, config=None) -> List[EmIterationLog]:
         if level == TRACE_NONE:
             return []
         em_n, series = ct.c_int32(0), ct.c_uint64(0)
         _check(self._lib.dpmrf_trace_info(self.h, ct.byref(em_n), ct.byref(series)), "trace")
+        on_device = sink is not None and self.stats()["device_loop"] == 1  # rows in the sink
         out = []
         for em in range(em_n.value):
             it, tot, conv = ct.c_int32(0), ct.c_double(0), ct.c_uint8(0)
@@ -492,7 +535,13 @@ class Context:
             _check(self._lib.dpmrf_trace_em(self.h, em, ct.byref(it), ct.byref(tot),
                                             ct.byref(conv), N.ptr(mu), N.ptr(sg)), "trace_em")
             maps = []
-            if level >= TRACE_FULL:
+            if level >= TRACE_FULL and sink is not None and on_device and \
+                    sink.fits(config, series.value):
+                for t in range(it.value):
+                    row = em * config.map_max_iters + t
+                    maps.append(MapIterationLog(sink.energy_rows[row, :series.value],
+                                                sink.flag_rows[row, :series.value]))
+            elif level >= TRACE_FULL:
                 for t in range(it.value):
                     e = np.zeros(series.value)
                     f = np.zeros(series.value, np.uint8)
@@ -653,12 +702,10 @@ class PartitionGroup:
         _check(self._lib.dpmrf_group_info_get(self.h, ct.byref(i)), "group_info")
         return {k: getattr(i, k) for k, _ in N.CGroupInfo._fields_}
 
-    def optimize(self, config: OptimizerConfig, *, fixed_work=False, multilabel=None,
+    def optimize(self, config: OptimizerConfig, *, fixed_work=False, multilabel=False,
                  trace_level=TRACE_EM, host_log=False, csr=False, graphs=True,
                  labels_out=None) -> OptimizeResult:
         M = config.num_labels
-        if multilabel is None:
-            multilabel = M != 2
         flags = (RUN_FIXED_WORK if fixed_work else 0) | (RUN_MULTILABEL if multilabel else 0) | \
             (RUN_HOST_LOG if host_log else 0) | (RUN_CSR if csr else 0) | \
             (0 if graphs else RUN_NO_GRAPH)
@@ -687,9 +734,11 @@ def context_for(backend: Backend) -> Context:
 
 
 def _resident(ctx: Context, graph: RegionGraph, hoods: Optional[NeighborhoodSet] = None):
-    if ctx._graph_key is not graph:
-        ctx.set_graph(graph)
-    if hoods is not None and ctx._hoods_key is not hoods:
+    """The reference reads its inputs by const& on every call, so the free
+    functions upload them on every call (a caller may mutate the arrays
+    between calls); keep them resident with an explicit Context instead."""
+    ctx.set_graph(graph)
+    if hoods is not None:
         ctx.set_hoods(hoods)
 
 
@@ -735,15 +784,13 @@ def init_random(num_labels, num_vertices, seed, backend: Backend = Backend.cuda(
 
 def replicate_by_label(backend: Backend, hoods: NeighborhoodSet, num_labels) -> ReplicatedIndex:
     ctx = context_for(backend)
-    if ctx._hoods_key is not hoods:
-        ctx.set_hoods(hoods)
+    ctx.set_hoods(hoods)
     return ctx.replicate_by_label(num_labels)
 
 
 def slot_hood_map(backend: Backend, hoods: NeighborhoodSet):
     ctx = context_for(backend)
-    if ctx._hoods_key is not hoods:
-        ctx.set_hoods(hoods)
+    ctx.set_hoods(hoods)
     return ctx.slot_hood_map()
 
 
@@ -774,8 +821,7 @@ def check_convergence(backend: Backend, history, window, tol):
 
 def update_labels(backend: Backend, hoods: NeighborhoodSet, argmin_label, old_labels):
     ctx = context_for(backend)
-    if ctx._hoods_key is not hoods:
-        ctx.set_hoods(hoods)
+    ctx.set_hoods(hoods)
     return ctx.update_labels(argmin_label, old_labels)
 
 

@@ -56,16 +56,24 @@ def test_device_loop_matches_host_log_loop(ctx, name):
     cfg = E.OptimizerConfig(f.cfg.num_labels, f.cfg.em_max_iters, f.cfg.map_max_iters,
                             f.cfg.convergence_window, f.cfg.convergence_tol, f.cfg.beta,
                             f.cfg.rng_seed)
-    for persistent in (False, True):
-        dev = ctx.optimize(cfg, fixed_work=f.fixed, trace_level=E.TRACE_EM, persistent=persistent)
-        host = ctx.optimize(cfg, fixed_work=f.fixed, trace_level=E.TRACE_EM, persistent=persistent,
+    for level in (E.TRACE_EM, E.TRACE_FULL):
+        dev = ctx.optimize(cfg, fixed_work=f.fixed, trace_level=level, multilabel=f.multilabel)
+        host = ctx.optimize(cfg, fixed_work=f.fixed, trace_level=level, multilabel=f.multilabel,
                             host_log=True)
+        assert dev.stats["device_loop"] == 1 or dev.stats["device_log_fallbacks"] >= 1
         assert host.stats["device_loop"] == 0
         assert np.array_equal(dev.labels, host.labels)
         assert np.array_equal(dev.mu, host.mu) and np.array_equal(dev.sigma, host.sigma)
         assert [(e.total_energy, e.converged, e.num_map_iters) for e in dev.trace] == \
                [(e.total_energy, e.converged, e.num_map_iters) for e in host.trace]
-        f.check(dev, exact_trace=False)
+        f.check(dev, exact_trace=level == E.TRACE_FULL)
+        if level == E.TRACE_FULL:  # every MAP row of every EM equal to the host-log loop's
+            for a, b in zip(dev.trace, host.trace):
+                assert len(a.map_iters) == len(b.map_iters) == a.num_map_iters
+                for m, n in zip(a.map_iters, b.map_iters):
+                    assert np.array_equal(m.hood_energy.view(np.uint64),
+                                          n.hood_energy.view(np.uint64))
+                    assert np.array_equal(m.converged, n.converged)
 
 
 def test_device_loop_long_runs(ctx, orc):

@@ -56,32 +56,30 @@ def same(a, b, full=True):
 def test_fixture_optimize(ctx, name):
     f = Fixture(name)
     upload(ctx, f.graph, f.hoods)
-    r = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed)
+    r = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, multilabel=f.multilabel)
     f.check(r)
 
 
-@pytest.mark.parametrize("layout", ["packed", "unfused", "csr", "staged"])
-@pytest.mark.parametrize("persistent", [False, True])
+@pytest.mark.parametrize("layout", ["packed", "unfused", "csr"])
 @pytest.mark.parametrize("graphs", [False, True])
-def test_execution_modes_agree(ctx, persistent, graphs, layout):
-    # persistent cooperative MAP loop vs two kernels per MAP iteration, each
-    # with and without CUDA-graph replay, over the packed delta layout, the
-    # u32 CSR and shared-memory staging: identical results and full traces
+def test_execution_modes_agree(ctx, graphs, layout):
+    # fused MAP-boundary launches vs two kernels per MAP iteration, each with
+    # and without CUDA-graph replay, over the packed delta layout and the u32
+    # CSR: identical results and full traces (device loop and host-log loop)
     for name in ("configA_256_grid8", "m5_128_brick8", "configA_252_grid7"):
         f = Fixture(name)
         upload(ctx, f.graph, f.hoods)
-        r = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, persistent=persistent,
-                         graphs=graphs, staged=layout == "staged", csr=layout == "csr",
-                         fused=layout != "unfused")
-        f.check(r)
-        assert r.stats["persistent"] == (1 if persistent else 0)
-        assert r.stats["graphs"] == (1 if graphs else 0)
+        for host_log in (False, True):
+            r = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, multilabel=f.multilabel,
+                             graphs=graphs, csr=layout == "csr", fused=layout != "unfused",
+                             host_log=host_log)
+            f.check(r)
+            assert r.stats["graphs"] == (1 if graphs else 0)
         for level in (E.TRACE_NONE, E.TRACE_EM):
             for timing in (False, True):  # timing forces the host-log loop
-                r2 = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, persistent=persistent,
+                r2 = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, multilabel=f.multilabel,
                                   graphs=graphs, trace_level=level, kernel_timing=timing,
-                                  staged=layout == "staged", csr=layout == "csr",
-                                  fused=layout != "unfused")
+                                  csr=layout == "csr", fused=layout != "unfused")
                 assert np.array_equal(r2.labels, r.labels) and np.array_equal(r2.mu, r.mu)
                 assert np.array_equal(r2.sigma, r.sigma)
 
@@ -97,7 +95,7 @@ def test_fixture_build_neighborhoods(ctx, name):
     assert np.array_equal(h.members, f.hoods.members)
     assert np.array_equal(h.source_clique, np.arange(len(h.offsets) - 1, dtype=np.uint32))
     # the device-built hoods drive optimize to the same fixture
-    r = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed)
+    r = ctx.optimize(to_cfg(f.cfg), fixed_work=f.fixed, multilabel=f.multilabel)
     f.check(r)
 
 
@@ -316,13 +314,10 @@ def test_concurrent_calls_on_one_context_serialize(ctx):
     assert not errors, errors
 
 
-@pytest.mark.parametrize("env", ["DPMRF_FLOW", "DPMRF_DICT", "DPMRF_NO_K12"])
+@pytest.mark.parametrize("env", ["DPMRF_NO_K12"])
 def test_opt_in_layouts_agree(env, monkeypatch):
-    """The measured-and-rejected variants stay correct: the dataflow MAP loop
-    (DPMRF_FLOW=1: one launch per EM, tiles synchronised by progress flags,
-    early exit decided two iterations behind), the dictionary-coded structure
-    (DPMRF_DICT=1) and 16-slot rows for brick hoods (DPMRF_NO_K12=1) reproduce
-    the fixtures and the default path."""
+    """16-slot rows for brick hoods (DPMRF_NO_K12=1) reproduce the fixtures
+    and the default path."""
     from paper_1809_05018_b200 import inputs
     monkeypatch.setenv(env, "1")
     c = E.Context(0)
@@ -333,11 +328,10 @@ def test_opt_in_layouts_agree(env, monkeypatch):
             f = Fixture(name)
             upload(c, f.graph, f.hoods)
             for fixed in (f.fixed, True):
-                r = c.optimize(to_cfg(f.cfg), fixed_work=fixed, trace_level=E.TRACE_EM)
+                r = c.optimize(to_cfg(f.cfg), fixed_work=fixed, multilabel=f.multilabel,
+                               trace_level=E.TRACE_EM)
                 if fixed == f.fixed:
                     f.check(r)
-                if env == "DPMRF_FLOW" and name != "m5_128_brick8":
-                    assert r.stats["persistent"] == 2  # the flow kernel ran
         for size, seed, brick in ((1024, 3, False), (2560, 42, False), (1000, 5, True)):
             sl = inputs.synthetic_slice(size, 8, seed=seed, brick=brick)
             for ctx_ in (c, base):
@@ -345,32 +339,6 @@ def test_opt_in_layouts_agree(env, monkeypatch):
                 ctx_.build_neighborhoods(sl.cliques)
             for fixed in (False, True):
                 cfg = E.OptimizerConfig(em_max_iters=8, rng_seed=seed)
-                got = c.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_EM)
-                want = base.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_EM)
-                same(got, want, full=False)
-    finally:
-        c.close()
-        base.close()
-
-
-@pytest.mark.parametrize("hb", [1, 4])
-def test_streamed_hood_pass_agrees(hb, monkeypatch):
-    """DPMRF_STREAM=<hood blocks per SM>: persistent hood blocks prefetching
-    packed rows with cp.async.bulk reproduce the default path bit for bit
-    (converging and fixed work; both vertex-per-thread widths)."""
-    from paper_1809_05018_b200 import inputs
-    monkeypatch.setenv("DPMRF_STREAM", str(hb))
-    c = E.Context(0)
-    monkeypatch.setenv("DPMRF_STREAM", "0")
-    base = E.Context(0)
-    try:
-        for size, seed in ((1000, 9), (2560, 42), (8192, 3)):
-            sl = inputs.synthetic_slice(size, 8, seed=seed)
-            for ctx_ in (c, base):
-                ctx_.set_graph(sl.graph)
-                ctx_.build_neighborhoods(sl.cliques)
-            for fixed in (False, True):
-                cfg = E.OptimizerConfig(em_max_iters=4, rng_seed=seed)
                 got = c.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_EM)
                 want = base.optimize(cfg, fixed_work=fixed, trace_level=E.TRACE_EM)
                 same(got, want, full=False)

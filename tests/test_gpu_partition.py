@@ -70,9 +70,9 @@ def test_local_group_matches_oracle_and_paths(ctx):
 def test_local_group_brick_multilabel(ctx):
     _load(ctx, 1024, 8, brick=True, seed=9)
     cfg = E.OptimizerConfig(num_labels=5, em_max_iters=5, rng_seed=9)
-    want = ctx.optimize(cfg, fixed_work=True, trace_level=E.TRACE_EM)
+    want = ctx.optimize(cfg, fixed_work=True, trace_level=E.TRACE_EM, multilabel=True)
     g = E.PartitionGroup.local(ctx, 4)
-    _same(g.optimize(cfg, fixed_work=True), want)
+    _same(g.optimize(cfg, fixed_work=True, multilabel=True), want)
     g.close()
 
 
