@@ -141,8 +141,13 @@ inline Ctx& ctx_for(const dpp::Backend& b) {
 }
 
 inline void graph(Ctx& c, const RegionGraph& g) {
-  throw_status(dpmrf_set_graph(c.h, g.num_vertices, g.offsets.data(), g.neighbors.data(),
-                               g.region_mean.data()),
+  // a default-constructed (empty) graph has no offsets at all: the reference
+  // accepts it, so pass the one-entry CSR {0}
+  static const std::uint32_t zero = 0;
+  if (g.offsets.empty() && g.num_vertices != 0)
+    throw std::invalid_argument("region graph: offsets must hold num_vertices + 1 entries");
+  throw_status(dpmrf_set_graph(c.h, g.num_vertices, g.offsets.empty() ? &zero : g.offsets.data(),
+                               g.neighbors.data(), g.region_mean.data()),
                "set_graph");
 }
 
@@ -311,7 +316,9 @@ inline OptimizeResult optimize(const dpp::Backend& b, const RegionGraph& g,
   // graph + hoods upload and the run in one call (engine.hpp:99-100's shape)
   const std::vector<std::uint32_t> h_off =
       h.offsets.empty() ? std::vector<std::uint32_t>{0} : h.offsets;
-  throw_status(dpmrf_optimize_arrays(c.h, g.num_vertices, g.offsets.data(), g.neighbors.data(),
+  static const std::uint32_t zero = 0;
+  throw_status(dpmrf_optimize_arrays(c.h, g.num_vertices, g.offsets.empty() ? &zero : g.offsets.data(),
+                                     g.neighbors.data(),
                                      g.region_mean.data(), h_off.size() - 1, h_off.data(),
                                      h.members.data(), &cfg, &opts, r.labels.data(),
                                      r.params.mu.data(), r.params.sigma.data()),

@@ -942,6 +942,7 @@ extern "C" void dpmrf_group_destroy(dpmrf_group* g) {
 extern "C" dpmrf_status dpmrf_group_info_get(dpmrf_group* g, dpmrf_group_info* out) {
   return guarded([&] {
     need(g && out, DPMRF_INVALID_ARGUMENT, "null argument");
+    ContextLock lock_(g->ctx);  // plan() prepares the context and uses its scratch + stream
     g->ctx->bind();
     plan(g);
     dpmrf_group_info i{};
