@@ -176,6 +176,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       CK(cudaEventCreate(&c->ev_begin));
       CK(cudaEventCreate(&c->ev_end));
+      init_log_table();  // (once per device)
     } catch (...) {
       delete c;
       throw;
@@ -630,7 +631,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     double* minE2 = ctx->minE.ensure(2 * uint64_t(R ? R : 1));
     ctx->pin_in_l2(minE2, uint64_t(R) * sizeof(double) * (fused ? 2 : 1));
     a.minE = minE2;
-    a.hist = ctx->hist.ensure(uint64_t(a.ring) * Hs);
+    a.hist = ctx->hist.ensure(uint64_t(a.ring) * Hs + 2);  // (+2: aligned leaf fetches)
     a.flags = full ? ctx->flags.ensure(uint64_t(map_max) * Hs) : nullptr;
     a.eq = a.hood_k ? ctx->hood_eq.ensure(Hs) : nullptr;  // (packed hood pass only)
     // [em_done, pending_done, em_count, pad | per-MAP-iteration counters]

@@ -37,6 +37,29 @@ __device__ __forceinline__ bool map_iter_skipped(const uint32_t* unconv, int t, 
   return unconv[kEmDone] != 0 || (!fixed && t > 0 && unconv[t - 1] == 0);
 }
 
+
+// Phase probe (build with EXTRA=-DDPMRF_PROBE only): %globaltimer stamps of
+// the M-step folds, per block (entry, after pdl_wait, staged, chain done) and
+// for the ticket block (ticket, trees done, end); read by dpmrf_probe_read.
+#ifdef DPMRF_PROBE
+__device__ unsigned long long g_probe_blk[2][256][8];
+__device__ unsigned long long g_probe_tail[2][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROBE_BLK(k, i) \
+  do { if (threadIdx.x == 0 && blockIdx.x < 256) g_probe_blk[k][blockIdx.x][i] = gtimer(); } while (0)
+#define PROBE_BLK_T(k, i) \
+  do { if (blockIdx.x < 256) g_probe_blk[k][blockIdx.x][i] = gtimer(); } while (0)
+#define PROBE_TAIL(k, i) do { if (threadIdx.x == 0) g_probe_tail[k][i] = gtimer(); } while (0)
+#else
+#define PROBE_BLK(k, i) do {} while (0)
+#define PROBE_BLK_T(k, i) do {} while (0)
+#define PROBE_TAIL(k, i) do {} while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // Per-vertex energies + argmin + label commit.
 //   discord_counts       engine.cpp:74-86   (labels frozen at iteration start)
@@ -567,15 +590,28 @@ __device__ __forceinline__ void em_prefetch(const EmEpilogueArgs& a, EmPrefetch*
     pf->hist[i - 1] = int(e) >= i ? a.em_hist[e - i] : 0.0;
 }
 
-__device__ void em_record(const EmEpilogueArgs& a, bool merged, const EmPrefetch* pf = nullptr) {
+// log c_k of log_fast (common.cuh), per device, built once (init_log_table).
+__device__ LogTable g_log_table;
+
+__global__ void k_init_log_table() {
+  const int k = threadIdx.x;
+  if (k < kLogTable) {
+    const dd_t r = log_dd(0.75 + k * 0.0078125);
+    g_log_table.hi[k] = r.hi;
+    g_log_table.lo[k] = r.lo;
+  }
+}
+
+__device__ void em_record(const EmEpilogueArgs& a, bool merged, const EmPrefetch* pf = nullptr,
+                          const double* thi = g_log_table.hi, const double* tlo = g_log_table.lo) {
   const int lane = threadIdx.x & 31;
   const int T = pf ? pf->T : executed_iters(a.unconv, a.map_max, a.fixed);
   const uint32_t e = pf ? pf->e : a.unconv[kEmCount];
   const uint32_t M = a.M;
   double* rec = a.em_rec + uint64_t(e) * (3 + 3 * M);
-  for (uint32_t l = lane; l < M; l += 32) {  // one lane per label evaluates the (long) device log
+  for (uint32_t l = lane; l < M; l += 32) {  // one lane per label evaluates the device log
     const double mu = a.em_out[2 + l], sg = a.em_out[2 + M + l];
-    const double ls = log_cr(sg);
+    const double ls = log_fast(sg, thi, tlo);
     rec[3 + l] = mu;
     rec[3 + M + l] = sg;
     rec[3 + 2 * M + l] = ls;
@@ -619,7 +655,9 @@ __global__ void __launch_bounds__(256)
   //           2: one block, trees only, over allgathered label partials and
   //              the hood-series partials in hood_parts.
   extern __shared__ double stage[];  // kLPB x kLeafStride
+  PROBE_BLK(kSq, 0);
   pdl_wait();
+  PROBE_BLK(kSq, 1);
   const uint32_t* n = layout;
   const uint32_t* label_start = layout + M;
   const uint32_t* leaf_start = layout + 2 * M + 1;
@@ -683,6 +721,7 @@ __global__ void __launch_bounds__(256)
       }
     }
     __syncthreads();
+    PROBE_BLK(kSq, 2);
     if (threadIdx.x >= 32) {
       constexpr uint32_t kN = kLPB * kHalf;  // 4096 second-half elements
       constexpr int kPerB = int((kN + 223) / 224);       // over warps 1-7
@@ -741,10 +780,13 @@ __global__ void __launch_bounds__(256)
       double acc = 0.0;
       if (chain) acc = fold(term(v[0]), 1, len < kHalf ? len : kHalf);
       __syncwarp();
+      if (threadIdx.x == 0) PROBE_BLK_T(kSq, 4);
       asm volatile("bar.sync 1, 256;" ::: "memory");  // the second halves are staged
+      if (threadIdx.x == 0) PROBE_BLK_T(kSq, 5);
       if (chain) {
         if (len > kHalf) acc = fold(acc, kHalf, len);
         partials[first + threadIdx.x] = acc;
+        if (threadIdx.x == 0) PROBE_BLK_T(kSq, 3);
       }
     }
   }
@@ -767,6 +809,7 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (!last) return;
     __threadfence();
+    PROBE_TAIL(kSq, 0);
   } else if (!kSq && hood_parts) {  // trees only: place the hood-series partials
     const uint32_t h0 = leaf_start[M], nh = leaf_start[M + 1] - h0;
     for (uint32_t i = threadIdx.x; i < nh; i += blockDim.x) partials[h0 + i] = hood_parts[i];
@@ -822,8 +865,10 @@ __global__ void __launch_bounds__(256)
       if (lane == 0) finish(w, cnt ? p[0] : 0.0);
     }
     __syncthreads();
+    PROBE_TAIL(kSq, 1);
     if (kSq && merged && threadIdx.x < 32) em_record(ep, true, &pf);
     if (threadIdx.x == 0 && tail_mode == 0) *done = 0;  // re-arm the ticket for the next launch
+    PROBE_TAIL(kSq, 2);
     return;
   }
   for (uint32_t s = 0; s < nseries; ++s) {
@@ -917,6 +962,604 @@ __global__ void __launch_bounds__(256)
 
 
 // ---------------------------------------------------------------------------
+// M-step folds, TMA-fed (the single-device path; k_leaf_fold above serves the
+// partitioned schedule's distributed folds).
+//   k_fold_sum: lane j < kLPB of a one-warp block owns leaf blockIdx*kLPB + j
+//     of the sum pass (the label series of x, then the hood-energy series).
+//     It fetches the leaf with two cp.async.bulk copies (halves, one mbarrier
+//     each: no thread-issued loads compete with the chain's shared-memory
+//     reads) and starts the dependent left fold (fold_leaf,
+//     kernels.hpp:37-42) as soon as the first half has landed.  No tail: the
+//     grid releases the sq pass at once (griddepcontrol.launch_dependents).
+//   k_fold_sq: fetches its label leaves of x BEFORE griddepcontrol.wait (x
+//     and the layout come from the MAP launches, complete by then); after
+//     the wait every block evaluates mu of its own labels from the sum-pass
+//     partials (the pairwise tree of kernels.hpp:45-51, redundantly per
+//     block, instead of a serial last-block tail between the passes), folds
+//     (x - mu)^2 (engine.cpp:213-217), and the last block (ticket) runs the
+//     sigma and total-energy trees, publishes the parameters and records the
+//     EM iteration (em_record).
+// Leaves are fetched as the 16-byte-aligned superset of [src, src + len):
+// rows start at an even double, the data at offset 0 or 1; x and the
+// hood-energy ring are allocated with 2 doubles of slack for the round-up.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kFoldPitch = kFoldLeaf + 2;  // doubles per staged leaf (16-B rows)
+constexpr uint32_t kFoldHalf = kFoldLeaf / 2;
+constexpr int kSqThreads = 128;
+constexpr uint32_t kRootCap = 2048;             // chunk roots per series (2M partials)
+
+struct FoldArgs {
+  const double* x;         // R region means grouped by label (stable)
+  const uint32_t* layout;  // n[M] | label_start[M+1] | leaf_start[M+2]
+  uint32_t M;
+  const double* hist;      // hood-energy ring (ring x Hs)
+  uint64_t Hs;
+  int ring;
+  const uint32_t* unconv;  // nullptr: standalone update_parameters
+  int map_max;
+  int fixed;
+  double* params;          // mu[M] | sigma[M]: previous in, new out
+  double* partials;        // sum-pass leaf partials (all series)
+  double* sq_partials;     // sq-pass leaf partials (label series)
+  double* em_out;          // [total, T, mu(M), sigma(M)]
+  uint32_t* done;          // sq-pass ticket (re-armed by the last block)
+  EmEpilogueArgs ep;
+  int merged;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
+  uint32_t ok = 0;
+  uint32_t spins = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar))
+        : "memory");
+    if (!ok && ++spins > (1u << 26)) __trap();  // a lost copy: fail loudly, never hang
+  }
+}
+
+// Issue the fetch of leaf [src, src + len) into row; returns the data offset
+// (0|1) and the staged length in doubles of the first half (*n0).
+__device__ __forceinline__ uint32_t fetch_leaf(double* row, const double* src, uint32_t len,
+                                               uint64_t* bar2, uint32_t* n0_out) {
+  const uint32_t off = (reinterpret_cast<uintptr_t>(src) & 15u) ? 1u : 0u;
+  const double* base = src - off;
+  const uint32_t n = (off + len + 1u) & ~1u;
+  const uint32_t n0 = n < kFoldHalf ? n : kFoldHalf;
+  mbar_expect(&bar2[0], n0 * 8u);
+  bulk_g2s(row, base, n0 * 8u, &bar2[0]);
+  if (n > n0) {
+    mbar_expect(&bar2[1], (n - n0) * 8u);
+    bulk_g2s(row + n0, base + n0, (n - n0) * 8u, &bar2[1]);
+  }
+  *n0_out = n0;
+  return off;
+}
+
+// Left fold of term(v[i]) over [i, end) onto acc, software-pipelined: the
+// next 16 operands are read from shared memory while 16 dependent adds retire.
+template <bool kSq>
+__device__ __forceinline__ double fold_span(const double* v, uint32_t i, uint32_t end, double acc,
+                                            double mu) {
+  auto term = [&](double x) {
+    if (kSq) {
+      const double d = __dsub_rn(x, mu);
+      return __dmul_rn(d, d);
+    }
+    return x;
+  };
+  constexpr int kG = 16;
+  double cur[kG], nxt[kG];
+  if (i + kG <= end) {
+#pragma unroll
+    for (int j = 0; j < kG; ++j) cur[j] = v[i + j];
+    while (i + 2 * kG <= end) {
+#pragma unroll
+      for (int j = 0; j < kG; ++j) nxt[j] = v[i + kG + j];
+#pragma unroll
+      for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, term(cur[j]));
+#pragma unroll
+      for (int j = 0; j < kG; ++j) cur[j] = nxt[j];
+      i += kG;
+    }
+#pragma unroll
+    for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, term(cur[j]));
+    i += kG;
+  }
+  for (; i < end; ++i) acc = __dadd_rn(acc, term(v[i]));
+  return acc;
+}
+
+// fold_leaf over a fetched row: the first half as soon as it lands, then the
+// rest.  len >= 1.
+template <bool kSq>
+__device__ __forceinline__ double fold_fetched(const double* row, uint32_t off, uint32_t len,
+                                               uint32_t n0, uint64_t* bar2, double mu) {
+  const double* v = row + off;
+  const uint32_t first_end = min(len, n0 - off);
+  mbar_wait0(&bar2[0]);
+  if ((threadIdx.x & 31) == 0) PROBE_BLK_T(kSq, 4);
+  double acc = v[0];
+  if (kSq) {
+    const double d = __dsub_rn(acc, mu);
+    acc = __dmul_rn(d, d);
+  }
+  acc = fold_span<kSq>(v, 1, first_end, acc, mu);
+  if ((threadIdx.x & 31) == 0) PROBE_BLK_T(kSq, 5);
+  if (len > first_end) {
+    mbar_wait0(&bar2[1]);
+    acc = fold_span<kSq>(v, first_end, len, acc, mu);
+  }
+  return acc;
+}
+
+// The pairwise tree of kernels.hpp:45-51 (bottom-up adjacent pairing, an odd
+// last element carried up unchanged == the split at bit_floor(n-1)), by one
+// warp in registers.  Lane l holds the aligned block p[l*B, l*B + B) (B a
+// power of two): the block's own tree is exactly a node of the series'
+// tree, so the lanes reduce their blocks in registers and the <= 32 block
+// roots finish with shuffles.
+template <int B>
+__device__ __forceinline__ double regs_tree(double (&e)[B], uint32_t r) {
+#pragma unroll
+  for (int w = B; w > 1; w /= 2) {
+    const uint32_t pr = r / 2;
+#pragma unroll
+    for (int j = 0; j < w / 2; ++j) {
+      const double s = __dadd_rn(e[2 * j], e[2 * j + 1]);
+      e[j] = uint32_t(j) < pr ? s : ((uint32_t(j) == pr && (r & 1u)) ? e[2 * j] : e[j]);
+    }
+    r = pr + (r & 1u);
+  }
+  return e[0];
+}
+
+__device__ __forceinline__ double lanes_tree(double v, uint32_t m) {
+  const uint32_t lane = threadIdx.x & 31;
+  while (m > 1) {
+    const uint32_t pr = m / 2;
+    const double a = __shfl_sync(0xffffffffu, v, (2 * lane) & 31);
+    const double b = __shfl_sync(0xffffffffu, v, (2 * lane + 1) & 31);
+    const double c = __shfl_sync(0xffffffffu, v, (m - 1) & 31);
+    v = lane < pr ? __dadd_rn(a, b) : ((lane == pr && (m & 1u)) ? c : v);
+    m = pr + (m & 1u);
+  }
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
+template <int B, bool kGlobal>
+__device__ __forceinline__ double warp_tree_b(const double* p, uint32_t cnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lo = lane * B;
+  const uint32_t r = cnt > lo ? min(cnt - lo, uint32_t(B)) : 0u;
+  double e[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) e[k] = uint32_t(k) < r ? (kGlobal ? __ldcg(p + lo + k) : p[lo + k]) : 0.0;
+  const double v = regs_tree<B>(e, r);
+  return lanes_tree(v, (cnt + B - 1) / B);
+}
+
+// Root of the tree over p[0, cnt), 1 <= cnt <= 1024 (kGlobal: p in global
+// memory, read through L2), by one warp; every lane gets it.
+template <bool kGlobal>
+__device__ double warp_tree(const double* p, uint32_t cnt) {
+  if (cnt <= 32) return warp_tree_b<1, kGlobal>(p, cnt);
+  if (cnt <= 64) return warp_tree_b<2, kGlobal>(p, cnt);
+  if (cnt <= 128) return warp_tree_b<4, kGlobal>(p, cnt);
+  if (cnt <= 256) return warp_tree_b<8, kGlobal>(p, cnt);
+  if (cnt <= 512) return warp_tree_b<16, kGlobal>(p, cnt);
+  return warp_tree_b<32, kGlobal>(p, cnt);
+}
+
+// The whole series' tree by the block: aligned 1024-partial chunks (a
+// chunk's root is exactly the level-10 node of the series' tree) by the
+// warps in parallel, roots in shared memory, then the tree over the roots
+// (<= kRootCap, in 1024-root chunks again if needed).  Called by every
+// thread; cnt in [1, 1024 * kRootCap]; returns the root to every thread.
+__device__ double block_series_tree(const double* __restrict__ p, uint32_t cnt, double* roots) {
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (cnt <= kFoldLeaf) {  // one warp; the block takes it from shared memory
+    if (warp == 0) {
+      const double r = warp_tree<true>(p, cnt);
+      if (lane == 0) roots[0] = r;
+    }
+  } else {
+    uint32_t nch = (cnt + kFoldLeaf - 1) / kFoldLeaf;
+    for (uint32_t c = warp; c < nch; c += nw) {
+      const double r =
+          warp_tree<true>(p + uint64_t(c) * kFoldLeaf, min(kFoldLeaf, cnt - c * kFoldLeaf));
+      if (lane == 0) roots[c] = r;
+    }
+    __syncthreads();
+    while (nch > 1) {  // roots of roots: aligned 1024-chunks again
+      const uint32_t nn = (nch + kFoldLeaf - 1) / kFoldLeaf;
+      double r = 0.0;
+      if (warp < nn) r = warp_tree<false>(roots + warp * kFoldLeaf, min(kFoldLeaf, nch - warp * kFoldLeaf));
+      __syncthreads();
+      if (warp < nn && lane == 0) roots[warp] = r;
+      __syncthreads();
+      nch = nn;
+    }
+  }
+  __syncthreads();
+  const double r = roots[0];
+  __syncthreads();
+  return r;
+}
+
+// Sum pass for few leaves (one block per SM): the warp stages its leaves with
+// 16-byte loads (first halves, then the second halves in flight while the
+// chains fold the first) -- the freshly scattered x lands faster this way
+// than through bulk copies (measured: a bulk copy of a just-written x leaf
+// can take ~2.8 us, the same copy again ~0.3 us).
+template <int kLPB>
+__global__ void __launch_bounds__(32) k_fold_sum_ldg(FoldArgs a) {
+  extern __shared__ __align__(16) double stage[];  // kLPB x kFoldPitch
+  const uint32_t lane = threadIdx.x;
+  PROBE_BLK(0, 0);
+  pdl_wait();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  PROBE_BLK(0, 1);
+  if (em_skipped(a.unconv)) return;
+  const uint32_t M = a.M;
+  const uint32_t* n = a.layout;
+  const uint32_t* label_start = a.layout + M;
+  const uint32_t* leaf_start = a.layout + 2 * M + 1;
+  const uint32_t total = leaf_start[M + 1];
+  const double2* base[kLPB];
+  uint32_t len[kLPB], off[kLPB], n2[kLPB];
+  int T = 0;
+  if (a.unconv) T = executed_iters(a.unconv, a.map_max, a.fixed);
+#pragma unroll
+  for (int j = 0; j < kLPB; ++j) {
+    const uint32_t leaf = blockIdx.x * kLPB + j;
+    len[j] = 0;
+    off[j] = 0;
+    n2[j] = 0;
+    base[j] = nullptr;
+    if (leaf < total) {
+      const uint32_t sr = series_of(leaf_start, M + 1, leaf);
+      const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
+      const double* src;
+      uint64_t slen;
+      if (sr < M) {
+        src = a.x + label_start[sr] + b;
+        slen = n[sr];
+      } else {  // the hood-energy row of the last executed MAP iteration (optimize.cpp:64-65)
+        src = a.hist + uint64_t((T - 1) % a.ring) * a.Hs + b;
+        slen = a.Hs;
+      }
+      const uint64_t rem = slen - b;
+      len[j] = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
+      off[j] = (reinterpret_cast<uintptr_t>(src) & 15u) ? 1u : 0u;
+      base[j] = reinterpret_cast<const double2*>(src - off[j]);
+      n2[j] = (off[j] + len[j] + 1u) / 2u;  // 16-byte vectors, <= 513
+    }
+  }
+  constexpr uint32_t kH2 = kFoldHalf / 2;  // vectors in the first part (256)
+  {
+    double2 r[kLPB][kH2 / 32];
+#pragma unroll
+    for (int j = 0; j < kLPB; ++j)
+#pragma unroll
+      for (int q = 0; q < int(kH2 / 32); ++q) {
+        const uint32_t i = q * 32 + lane;
+        r[j][q] = i < n2[j] ? __ldcg(base[j] + i) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+    for (int j = 0; j < kLPB; ++j)
+#pragma unroll
+      for (int q = 0; q < int(kH2 / 32); ++q)
+        reinterpret_cast<double2*>(stage + j * kFoldPitch)[q * 32 + lane] = r[j][q];
+  }
+  __syncwarp();
+  PROBE_BLK_T(0, 2);
+  constexpr int kQ2 = (kFoldPitch / 2 - kH2 + 31) / 32;  // second-part vectors per lane (9)
+  double2 r2[kLPB][kQ2];
+#pragma unroll
+  for (int j = 0; j < kLPB; ++j)
+#pragma unroll
+    for (int q = 0; q < kQ2; ++q) {
+      const uint32_t i = kH2 + q * 32 + lane;
+      r2[j][q] = i < n2[j] ? __ldcg(base[j] + i) : make_double2(0.0, 0.0);
+    }
+  // the chains fold the first parts while the second parts are in flight
+  uint32_t my_len = 0, my_off = 0;
+#pragma unroll
+  for (int j = 0; j < kLPB; ++j)
+    if (lane == uint32_t(j)) {
+      my_len = len[j];
+      my_off = off[j];
+    }
+  const double* v = stage + lane * kFoldPitch + my_off;
+  const uint32_t first_end = min(my_len, kFoldHalf - my_off);
+  double acc = 0.0;
+  if (my_len) acc = fold_span<false>(v, 1, first_end, v[0], 0.0);
+  if ((lane & 31) == 0) PROBE_BLK_T(0, 5);
+#pragma unroll
+  for (int j = 0; j < kLPB; ++j)
+#pragma unroll
+    for (int q = 0; q < kQ2; ++q) {
+      const uint32_t i = kH2 + q * 32 + lane;
+      if (i < kFoldPitch / 2) reinterpret_cast<double2*>(stage + j * kFoldPitch)[i] = r2[j][q];
+    }
+  __syncwarp();
+  if (my_len) {
+    if (my_len > first_end) acc = fold_span<false>(v, first_end, my_len, acc, 0.0);
+    a.partials[blockIdx.x * kLPB + lane] = acc;
+  }
+  PROBE_BLK_T(0, 3);
+}
+
+template <int kLPB>
+__global__ void __launch_bounds__(32) k_fold_sum(FoldArgs a) {
+  extern __shared__ __align__(16) double stage[];  // kLPB x kFoldPitch
+  __shared__ __align__(8) uint64_t bar[kLPB][2];
+  const uint32_t lane = threadIdx.x;
+  if (lane < kLPB) {
+    mbar_init1(&bar[lane][0]);
+    mbar_init1(&bar[lane][1]);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  PROBE_BLK(0, 0);
+  pdl_wait();
+  // release the sq pass now: its blocks fetch their x leaves while this grid folds
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  PROBE_BLK(0, 1);
+  if (em_skipped(a.unconv)) return;
+  const uint32_t M = a.M;
+  const uint32_t* n = a.layout;
+  const uint32_t* label_start = a.layout + M;
+  const uint32_t* leaf_start = a.layout + 2 * M + 1;
+  const uint32_t leaf = blockIdx.x * kLPB + lane;
+  if (lane >= kLPB || leaf >= leaf_start[M + 1]) return;
+  const uint32_t sr = series_of(leaf_start, M + 1, leaf);
+  const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
+  const double* src;
+  uint64_t slen;
+  if (sr < M) {
+    src = a.x + label_start[sr] + b;
+    slen = n[sr];
+  } else {  // the hood-energy row of the last executed MAP iteration (optimize.cpp:64-65)
+    const int T = executed_iters(a.unconv, a.map_max, a.fixed);
+    src = a.hist + uint64_t((T - 1) % a.ring) * a.Hs + b;
+    slen = a.Hs;
+  }
+  const uint64_t rem = slen - b;
+  const uint32_t len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
+  double* row = stage + lane * kFoldPitch;
+  uint32_t n0;
+  const uint32_t off = fetch_leaf(row, src, len, bar[lane], &n0);
+  PROBE_BLK_T(0, 2);
+  a.partials[leaf] = fold_fetched<false>(row, off, len, n0, bar[lane], 0.0);
+  PROBE_BLK_T(0, 3);
+#ifdef DPMRF_PROBE
+  {  // experiment: the same two fetches again (warm), timed to completion
+    __shared__ __align__(8) uint64_t bar2[kLPB][2];
+    mbar_init1(&bar2[lane][0]);
+    mbar_init1(&bar2[lane][1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const unsigned long long t0 = gtimer();
+    uint32_t n0b;
+    fetch_leaf(row, src, len, bar2[lane], &n0b);
+    mbar_wait0(&bar2[lane][0]);
+    const unsigned long long t1 = gtimer();
+    if (len > n0b - off) mbar_wait0(&bar2[lane][1]);
+    const unsigned long long t2 = gtimer();
+    if (lane == 0 && blockIdx.x < 256) {
+      g_probe_blk[0][blockIdx.x][6] = t1 - t0;
+      g_probe_blk[0][blockIdx.x][7] = t2 - t0;
+    }
+  }
+#endif
+}
+
+template <int kLPB>
+__global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
+  extern __shared__ __align__(16) double stage[];  // kLPB x kFoldPitch | kRootCap
+  __shared__ __align__(8) uint64_t bar[kLPB][2];
+  __shared__ uint32_t sr_s[kLPB], len_s[kLPB], off_s[kLPB], n0_s[kLPB];
+  __shared__ double mu_s[kLPB];
+  __shared__ uint32_t lay[4 * kMaxLabels + 4];  // the layout, read once
+  __shared__ double root_s[kMaxLabels + 1];
+  __shared__ double mu_all[kMaxLabels];
+  __shared__ EmPrefetch pf;
+  __shared__ double lt_s[2 * kLogTable];  // log_fast's table, read before the wait
+  __shared__ bool last;
+  double* roots = stage + kLPB * kFoldPitch;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr uint32_t kWarps = kSqThreads / 32;
+  const uint32_t M = a.M;
+  const uint32_t* n = lay;
+  const uint32_t* label_start = lay + M;
+  const uint32_t* leaf_start = lay + 2 * M + 1;
+  const uint32_t first = blockIdx.x * kLPB;
+  if (tid < kLPB) {
+    mbar_init1(&bar[tid][0]);
+    mbar_init1(&bar[tid][1]);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // before the wait: x, the layout, the skip flag and the MAP counters are
+  // the MAP launches' (complete once the sum pass released this grid); the
+  // EM history is the previous EM's
+  const bool skipped = em_skipped(a.unconv);
+  for (uint32_t i = tid; i < 4 * M + 4; i += kSqThreads) lay[i] = a.layout[i];
+  for (uint32_t i = tid; i < 2 * kLogTable; i += kSqThreads)
+    lt_s[i] = i < kLogTable ? g_log_table.hi[i] : g_log_table.lo[i - kLogTable];
+  if (a.merged && !skipped && tid == kSqThreads - 32) em_prefetch(a.ep, &pf);
+  __syncthreads();
+  PROBE_BLK(1, 0);
+  if (!skipped && tid < kLPB) {
+    const uint32_t leaf = first + tid;
+    uint32_t len = 0;
+    if (leaf < leaf_start[M]) {
+      const uint32_t sr = series_of(leaf_start, M, leaf);
+      const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
+      const uint64_t rem = n[sr] - b;
+      len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
+      sr_s[tid] = sr;
+      off_s[tid] = fetch_leaf(stage + tid * kFoldPitch, a.x + label_start[sr] + b, len, bar[tid],
+                              &n0_s[tid]);
+    }
+    len_s[tid] = len;
+  }
+  pdl_wait();  // the sum pass is complete: its partials are visible
+  PROBE_BLK(1, 1);
+  if (skipped) return;  // (uniform: no block takes a ticket)
+  __syncthreads();
+  // mu of this block's labels (consecutive series s_lo..s_hi) from the
+  // sum-pass partials, one warp per label; the block holding a label's
+  // first leaf publishes it
+  if (len_s[0] != 0) {
+    const uint32_t s_lo = sr_s[0];
+    uint32_t s_hi = s_lo;
+    for (int j = 1; j < kLPB; ++j)
+      if (len_s[j] != 0) s_hi = sr_s[j];
+    auto publish = [&](uint32_t s, double folded) {  // (one thread)
+      const double mu = __ddiv_rn(folded, static_cast<double>(n[s]));
+      root_s[s - s_lo] = mu;
+      if (leaf_start[s] >= first && leaf_start[s] < first + kLPB) a.params[s] = mu;
+    };
+    bool short_series = true;
+    for (uint32_t s = s_lo; s <= s_hi; ++s)
+      short_series = short_series && leaf_start[s + 1] - leaf_start[s] <= kFoldLeaf;
+    if (short_series) {
+      for (uint32_t s = s_lo + warp; s <= s_hi; s += kWarps) {
+        const uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
+        if (cnt == 0) continue;  // (a label without leaves is held by no block)
+        const double folded = warp_tree<true>(a.partials + leaf_start[s], cnt);
+        if (lane == 0) publish(s, folded);
+      }
+    } else {
+      for (uint32_t s = s_lo; s <= s_hi; ++s) {
+        const uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
+        if (cnt == 0) continue;
+        const double folded = block_series_tree(a.partials + leaf_start[s], cnt, roots);
+        if (tid == 0) publish(s, folded);
+      }
+    }
+    __syncthreads();
+    if (tid < kLPB && len_s[tid] != 0) mu_s[tid] = root_s[sr_s[tid] - s_lo];
+  }
+  __syncthreads();
+  PROBE_BLK(1, 2);
+  if (tid < kLPB && len_s[tid] != 0) {
+    a.sq_partials[first + tid] = fold_fetched<true>(stage + tid * kFoldPitch, off_s[tid],
+                                                    len_s[tid], n0_s[tid], bar[tid], mu_s[tid]);
+    if (tid == 0) PROBE_BLK_T(1, 3);
+  }
+  if (a.merged && (executed_iters(a.unconv, a.map_max, a.fixed) & 1)) {
+    // device-resident loop: the next EM starts from buffer 0, so an odd
+    // number of MAP iterations leaves the committed labels to move back
+    // (read by the next launch: the kernel boundary orders it)
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint64_t words = a.ep.R / 4;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.ep.lab1);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(a.ep.lab0);
+    const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + tid;
+    for (uint64_t w = g; w < words; w += stride) dst[w] = src[w];
+    for (uint64_t v = words * 4 + g; v < a.ep.R; v += stride) a.ep.lab0[v] = a.ep.lab1[v];
+  }
+  // ---- last block: sigma + total-energy trees, parameters, EM record ----
+  if (warp == 0) __threadfence();  // (warp 0 wrote the partials and the mu)
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  PROBE_TAIL(1, 0);
+  const uint32_t nseries = M + 1;
+  auto series_ptr = [&](uint32_t s) {
+    return s < M ? a.sq_partials + leaf_start[s] : a.partials + leaf_start[M];
+  };
+  auto series_cnt = [&](uint32_t s) {
+    return s < M ? leaf_start[s + 1] - leaf_start[s] : leaf_start[M + 1] - leaf_start[M];
+  };
+#ifdef DPMRF_PROBE
+  {  // i-cache experiment: the same trees + device log once, results discarded
+    __shared__ double sink_s[8];
+    for (uint32_t s = warp; s < nseries; s += kWarps) {
+      const uint32_t cnt = series_cnt(s);
+      if (cnt <= kFoldLeaf) {
+        const double r = cnt ? warp_tree<true>(series_ptr(s), cnt) : 0.0;
+        if (lane == 0) sink_s[s & 7] = r;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) g_probe_tail[0][0] = gtimer();
+    if (tid < M) sink_s[tid] = log_fast(__ldcg(a.params + M + tid), lt_s, lt_s + kLogTable);
+    __syncthreads();
+    if (tid == 0) g_probe_tail[0][1] = gtimer();
+    if (tid == 0) g_probe_tail[0][2] = static_cast<unsigned long long>(sink_s[0] != 12345.0);
+  }
+#endif
+  // every label's mu (published by the blocks above; empty labels keep the
+  // previous one), loaded beside the trees' partials
+  for (uint32_t s = tid; s < M; s += kSqThreads) mu_all[s] = __ldcg(a.params + s);
+  bool all_short = true;
+  for (uint32_t s = 0; s < nseries; ++s) all_short = all_short && series_cnt(s) <= kFoldLeaf;
+  if (all_short) {  // one warp per series, all at once
+    for (uint32_t s = warp; s < nseries; s += kWarps) {
+      const uint32_t cnt = series_cnt(s);
+      const double r = cnt ? warp_tree<true>(series_ptr(s), cnt) : 0.0;
+      if (lane == 0) root_s[s] = r;
+    }
+  } else {
+    for (uint32_t s = 0; s < nseries; ++s) {
+      const uint32_t cnt = series_cnt(s);
+      const double r = cnt ? block_series_tree(series_ptr(s), cnt, roots) : 0.0;
+      if (tid == 0) root_s[s] = r;
+    }
+  }
+  __syncthreads();
+  for (uint32_t s = tid; s < nseries; s += kSqThreads) {
+    const double folded = root_s[s];
+    if (s < M) {
+      double sg = a.params[M + s];
+      if (n[s] != 0) {  // empty labels keep their previous parameters (engine.cpp:209-220)
+        const double sd = __dsqrt_rn(__ddiv_rn(folded, static_cast<double>(n[s])));
+        sg = sd < kSigmaFloor ? kSigmaFloor : sd;
+        a.params[M + s] = sg;
+      }
+      a.em_out[2 + s] = mu_all[s];
+      a.em_out[2 + M + s] = sg;
+    } else {
+      // total energy: dpp::reduce(..., 0.0) -> identity only for empty input
+      a.em_out[0] = series_cnt(M) == 0 ? 0.0 : folded;
+      a.em_out[1] = static_cast<double>(a.unconv ? executed_iters(a.unconv, a.map_max, a.fixed) : 0);
+    }
+  }
+  __syncthreads();
+  PROBE_TAIL(1, 1);
+  if (a.merged && tid < 32) em_record(a.ep, true, &pf, lt_s, lt_s + kLogTable);
+  if (tid == 0) *a.done = 0;  // re-arm the ticket for the next launch
+  PROBE_TAIL(1, 2);
+}
+
+// ---------------------------------------------------------------------------
 // Device-resident EM loop (no host round trip between EM iterations).
 // k_em_prologue arms the MAP counters and folds the previous epilogue's stop
 // decision into the state (so every kernel of this EM sees one value);
@@ -1005,7 +1648,7 @@ __global__ void __launch_bounds__(256)
 
 __global__ void k_log_cr(const double* x, double* out, uint64_t n) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = log_cr(x[i]);
+  if (i < n) out[i] = log_fast(x[i], g_log_table.hi, g_log_table.lo);
 }
 
 __global__ void k_init_labels(uint8_t* lab, uint32_t R, uint32_t M, uint64_t seed) {
@@ -1648,34 +2291,37 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
                (const uint32_t*)tile_base, (const uint32_t*)layout, x);
     ++n;
   }
-  const size_t leaf_smem = size_t(8) * 1056 * sizeof(double);  // 8 leaves (the tail: 8 x 1056)
-  // few leaves (2560^2: ~300): 2 per block -- more SMs stage, the first
-  // stage is shorter (+1%); many (16384^2: ~16 000): 8 per block (the 67 KB
-  // stage caps 3 blocks per SM)
+  // few leaves (2560^2: ~300): 2 per block, one block per SM -- latency;
+  // many (16384^2: ~16 000): 8 per sum block / 4 per sq block (three blocks
+  // per SM by shared memory) -- enough chains in flight for HBM
   const bool few = max_leaves <= uint64_t(4) * kNumSMs;
-  const unsigned lg = grid_for(max_leaves, few ? 2 : kLeavesPerBlock);
+  const uint64_t label_leaves = (uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M;
   const EmEpilogueArgs epv = ep ? *ep : EmEpilogueArgs{};
-  if (!scatter_only && few) {
-    ensure_dynamic_smem(k_leaf_fold<false, 2>, leaf_smem);
-    ensure_dynamic_smem(k_leaf_fold<true, 2>, leaf_smem);
-    launch_pdl(k_leaf_fold<false, 2>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
-               (const uint32_t*)layout, M, hist, Hs, ring, unconv, map_max, fixed, params,
-               partials, em_out, mb.done.get(), epv, 0, hood_parts, 0u, ~0u, 0);
-    launch_pdl(k_leaf_fold<true, 2>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
-               (const uint32_t*)layout, M, (const double*)nullptr, uint64_t(0), 1, unconv,
-               map_max, fixed, params, partials, em_out, mb.done.get() + 1, epv, ep ? 1 : 0,
-               (const double*)nullptr, 0u, ~0u, 0);
-    n += 2;
-  } else if (!scatter_only) {
-    ensure_dynamic_smem(k_leaf_fold<false>, leaf_smem);
-    ensure_dynamic_smem(k_leaf_fold<true>, leaf_smem);
-    launch_pdl(k_leaf_fold<false>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
-               (const uint32_t*)layout, M, hist, Hs, ring, unconv, map_max, fixed, params,
-               partials, em_out, mb.done.get(), epv, 0, hood_parts, 0u, ~0u, 0);
-    launch_pdl(k_leaf_fold<true>, dim3(lg), dim3(256), leaf_smem, s, (const double*)x,
-               (const uint32_t*)layout, M, (const double*)nullptr, uint64_t(0), 1, unconv,
-               map_max, fixed, params, partials, em_out, mb.done.get() + 1, epv, ep ? 1 : 0,
-               (const double*)nullptr, 0u, ~0u, 0);
+  if (!scatter_only) {
+    if (label_leaves > uint64_t(kRootCap) * kFoldLeaf ||
+        (Hs + kFoldLeaf - 1) / kFoldLeaf > uint64_t(kRootCap) * kFoldLeaf)
+      fail(DPMRF_INVALID_ARGUMENT, "M-step: series too long for the fold trees");
+    const FoldArgs fa{x,       layout,        M,     hist,      Hs,
+                      ring,    unconv,        map_max, fixed,   params,
+                      partials, mb.sq_partials.get(), em_out, mb.done.get() + 1, epv,
+                      ep ? 1 : 0};
+    if (few) {
+      constexpr int kS = 2, kQ = 2;
+      const size_t ss = size_t(kS) * kFoldPitch * sizeof(double);
+      const size_t sq = (size_t(kQ) * kFoldPitch + kRootCap) * sizeof(double);
+      ensure_dynamic_smem(k_fold_sum_ldg<kS>, ss);
+      ensure_dynamic_smem(k_fold_sq<kQ>, sq);
+      launch_pdl(k_fold_sum_ldg<kS>, dim3(grid_for(max_leaves, kS)), dim3(32), ss, s, fa);
+      launch_pdl(k_fold_sq<kQ>, dim3(grid_for(label_leaves, kQ)), dim3(kSqThreads), sq, s, fa);
+    } else {
+      constexpr int kS = 8, kQ = 4;
+      const size_t ss = size_t(kS) * kFoldPitch * sizeof(double);
+      const size_t sq = (size_t(kQ) * kFoldPitch + kRootCap) * sizeof(double);
+      ensure_dynamic_smem(k_fold_sum<kS>, ss);
+      ensure_dynamic_smem(k_fold_sq<kQ>, sq);
+      launch_pdl(k_fold_sum<kS>, dim3(grid_for(max_leaves, kS)), dim3(32), ss, s, fa);
+      launch_pdl(k_fold_sq<kQ>, dim3(grid_for(label_leaves, kQ)), dim3(kSqThreads), sq, s, fa);
+    }
     n += 2;
   }
   if (launches) *launches += n;
@@ -1780,6 +2426,19 @@ void launch_row_leaves(const double* hist, int ring, uint64_t Hs, const uint32_t
              Hs, unconv, map_max, fixed, hb, he, out);
 }
 
+void init_log_table() {
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(dev)) return;
+  k_init_log_table<<<1, 128>>>();
+  CK_LAUNCH();
+  CK(cudaDeviceSynchronize());
+  done.insert(dev);
+}
+
 void launch_log_cr(const double* x, double* out, uint64_t n, cudaStream_t s) {
   if (!n) return;
   k_log_cr<<<grid_for(n, 256), 256, 0, s>>>(x, out, n);
@@ -1793,8 +2452,9 @@ void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs) {
   mb.tile_base.ensure(uint64_t(tiles_g) * M);
   mb.chunk_sum.ensure(((uint64_t(tiles_g) + kTileChunk - 1) / kTileChunk) * M);
   mb.layout.ensure(4 * M + 4);
-  mb.x.ensure(R);
+  mb.x.ensure(uint64_t(R) + 2);  // (+2: the folds fetch 16-byte-aligned supersets)
   mb.partials.ensure((uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M + (Hs + kFoldLeaf - 1) / kFoldLeaf + 1);
+  mb.sq_partials.ensure((uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M);
   if (!mb.done.get()) {
     CK(cudaMalloc(reinterpret_cast<void**>(&mb.done.p), 2 * sizeof(uint32_t)));
     mb.done.cap = 2;
@@ -1863,3 +2523,13 @@ void launch_series_offsets(const uint32_t* h_off, uint64_t H, uint64_t S, uint32
 }
 
 }  // namespace dpmrf_b200
+
+#ifdef DPMRF_PROBE
+extern "C" int dpmrf_probe_read(unsigned long long* blk, unsigned long long* tail) {
+  if (cudaMemcpyFromSymbol(blk, dpmrf_b200::g_probe_blk, sizeof(dpmrf_b200::g_probe_blk)) !=
+      cudaSuccess)
+    return 1;
+  return cudaMemcpyFromSymbol(tail, dpmrf_b200::g_probe_tail, sizeof(dpmrf_b200::g_probe_tail)) !=
+         cudaSuccess;
+}
+#endif

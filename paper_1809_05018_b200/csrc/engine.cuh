@@ -103,7 +103,8 @@ struct MStepBuffers {
   DevBuf<uint32_t> tile_base;    // tiles x M
   DevBuf<uint32_t> layout;       // n[M] | label_start[M+1] | leaf_start[M+2]
   DevBuf<double> x;              // R values grouped by label (stable)
-  DevBuf<double> partials;       // leaf partials of all series
+  DevBuf<double> partials;       // leaf partials of all series (sum pass)
+  DevBuf<double> sq_partials;    // leaf partials of the label series (sq pass)
   DevBuf<uint32_t> done;         // last-block tickets of the two leaf-fold kernels
   DevBuf<uint32_t> chunk_sum;    // per-1024-tile-chunk label counts (large graphs)
   DevBuf<uint32_t> err;
@@ -152,6 +153,8 @@ void launch_partition_select(const uint8_t* lab_even, const uint8_t* lab_odd, co
                              uint8_t* lab_full, double* row_full, cudaStream_t s);
 // log_cr over n values (diagnostics / tests of the device log).
 void launch_log_cr(const double* x, double* out, uint64_t n, cudaStream_t s);
+// Builds the per-device table of the EM loop's device log once (blocking).
+void init_log_table();
 
 // Allocates every M-step buffer up front (required before stream capture).
 void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs);

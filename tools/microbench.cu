@@ -3,6 +3,7 @@
 // barrier cost vs grid size, and back-to-back empty kernels in a CUDA graph.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o microbench tools/microbench.cu
 #include <cooperative_groups.h>
+#include "../paper_1809_05018_b200/csrc/common.cuh"
 #include <chrono>
 #include <cstdio>
 #include <vector>
@@ -13,6 +14,24 @@ __global__ void dadd_chain(double* out, double x, int n, long long* cycles) {
   double acc = x;
   const long long t0 = clock64();
   for (int i = 0; i < n; ++i) acc = __dadd_rn(acc, x);
+  const long long t1 = clock64();
+  out[0] = acc;
+  cycles[0] = t1 - t0;
+}
+
+// Dependent FP64 op chains: DFMA, DMUL, correctly rounded div / sqrt.
+template <int kOp>
+__global__ void fp64_chain(double* out, double x, int n, long long* cycles) {
+  double acc = x;
+  const long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    if (kOp == 0) acc = __fma_rn(acc, x, 1e-300);
+    if (kOp == 1) acc = __dmul_rn(acc, x);
+    if (kOp == 2) acc = __ddiv_rn(x, acc);
+    if (kOp == 3) acc = __dsqrt_rn(acc);
+    if (kOp == 4) acc = log(acc + 2.0);
+    if (kOp == 5) acc = dpmrf_b200::log_cr(acc + 2.0);
+  }
   const long long t1 = clock64();
   out[0] = acc;
   cycles[0] = t1 - t0;
@@ -132,6 +151,22 @@ int main() {
   dadd_chain<<<1, 1>>>(d, 1e-9, n, c);
   cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
   printf("dependent DADD: %.2f cycles/op\n", double(h) / n);
+  {
+    const char* names[] = {"DFMA", "DMUL", "__ddiv_rn", "__dsqrt_rn", "log (libdevice)", "log_cr"};
+    const int ns[] = {n, n, 1 << 14, 1 << 14, 1 << 12, 1 << 10};
+    for (int op = 0; op < 6; ++op) {
+      switch (op) {
+        case 0: fp64_chain<0><<<1, 1>>>(d, 1.0000001, ns[op], c); break;
+        case 1: fp64_chain<1><<<1, 1>>>(d, 1.0000001, ns[op], c); break;
+        case 2: fp64_chain<2><<<1, 1>>>(d, 1.0000001, ns[op], c); break;
+        case 3: fp64_chain<3><<<1, 1>>>(d, 1.0000001, ns[op], c); break;
+        case 4: fp64_chain<4><<<1, 1>>>(d, 1.0000001, ns[op], c); break;
+        case 5: fp64_chain<5><<<1, 1>>>(d, 1.0000001, ns[op], c); break;
+      }
+      cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+      printf("dependent %s: %.2f cycles/op\n", names[op], double(h) / ns[op]);
+    }
+  }
   lds_chain<<<1, 256>>>(d, n, c);
   cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
   printf("dependent LDS+DADD fold (unroll 8): %.2f cycles/element\n", double(h) / n);
