@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "engine.cuh"
+#include "fold_trees.cuh"
 
 namespace dpmrf_b200 {
 
@@ -986,7 +987,6 @@ __global__ void __launch_bounds__(256)
 constexpr uint32_t kFoldPitch = kFoldLeaf + 2;  // doubles per staged leaf (16-B rows)
 constexpr uint32_t kFoldHalf = kFoldLeaf / 2;
 constexpr int kSqThreads = 128;
-constexpr uint32_t kRootCap = 2048;             // chunk roots per series (2M partials)
 
 struct FoldArgs {
   const double* x;         // R region means grouped by label (stable)
@@ -1005,6 +1005,7 @@ struct FoldArgs {
   uint32_t* done;          // sq-pass ticket (re-armed by the last block)
   EmEpilogueArgs ep;
   int merged;
+  uint32_t root_cap;       // shared chunk-root slots of the sq pass (>= all series' chunks)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1115,100 +1116,6 @@ __device__ __forceinline__ double fold_fetched(const double* row, uint32_t off, 
   return acc;
 }
 
-// The pairwise tree of kernels.hpp:45-51 (bottom-up adjacent pairing, an odd
-// last element carried up unchanged == the split at bit_floor(n-1)), by one
-// warp in registers.  Lane l holds the aligned block p[l*B, l*B + B) (B a
-// power of two): the block's own tree is exactly a node of the series'
-// tree, so the lanes reduce their blocks in registers and the <= 32 block
-// roots finish with shuffles.
-template <int B>
-__device__ __forceinline__ double regs_tree(double (&e)[B], uint32_t r) {
-#pragma unroll
-  for (int w = B; w > 1; w /= 2) {
-    const uint32_t pr = r / 2;
-#pragma unroll
-    for (int j = 0; j < w / 2; ++j) {
-      const double s = __dadd_rn(e[2 * j], e[2 * j + 1]);
-      e[j] = uint32_t(j) < pr ? s : ((uint32_t(j) == pr && (r & 1u)) ? e[2 * j] : e[j]);
-    }
-    r = pr + (r & 1u);
-  }
-  return e[0];
-}
-
-__device__ __forceinline__ double lanes_tree(double v, uint32_t m) {
-  const uint32_t lane = threadIdx.x & 31;
-  while (m > 1) {
-    const uint32_t pr = m / 2;
-    const double a = __shfl_sync(0xffffffffu, v, (2 * lane) & 31);
-    const double b = __shfl_sync(0xffffffffu, v, (2 * lane + 1) & 31);
-    const double c = __shfl_sync(0xffffffffu, v, (m - 1) & 31);
-    v = lane < pr ? __dadd_rn(a, b) : ((lane == pr && (m & 1u)) ? c : v);
-    m = pr + (m & 1u);
-  }
-  return __shfl_sync(0xffffffffu, v, 0);
-}
-
-template <int B, bool kGlobal>
-__device__ __forceinline__ double warp_tree_b(const double* p, uint32_t cnt) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t lo = lane * B;
-  const uint32_t r = cnt > lo ? min(cnt - lo, uint32_t(B)) : 0u;
-  double e[B];
-#pragma unroll
-  for (int k = 0; k < B; ++k) e[k] = uint32_t(k) < r ? (kGlobal ? __ldcg(p + lo + k) : p[lo + k]) : 0.0;
-  const double v = regs_tree<B>(e, r);
-  return lanes_tree(v, (cnt + B - 1) / B);
-}
-
-// Root of the tree over p[0, cnt), 1 <= cnt <= 1024 (kGlobal: p in global
-// memory, read through L2), by one warp; every lane gets it.
-template <bool kGlobal>
-__device__ double warp_tree(const double* p, uint32_t cnt) {
-  if (cnt <= 32) return warp_tree_b<1, kGlobal>(p, cnt);
-  if (cnt <= 64) return warp_tree_b<2, kGlobal>(p, cnt);
-  if (cnt <= 128) return warp_tree_b<4, kGlobal>(p, cnt);
-  if (cnt <= 256) return warp_tree_b<8, kGlobal>(p, cnt);
-  if (cnt <= 512) return warp_tree_b<16, kGlobal>(p, cnt);
-  return warp_tree_b<32, kGlobal>(p, cnt);
-}
-
-// The whole series' tree by the block: aligned 1024-partial chunks (a
-// chunk's root is exactly the level-10 node of the series' tree) by the
-// warps in parallel, roots in shared memory, then the tree over the roots
-// (<= kRootCap, in 1024-root chunks again if needed).  Called by every
-// thread; cnt in [1, 1024 * kRootCap]; returns the root to every thread.
-__device__ double block_series_tree(const double* __restrict__ p, uint32_t cnt, double* roots) {
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  if (cnt <= kFoldLeaf) {  // one warp; the block takes it from shared memory
-    if (warp == 0) {
-      const double r = warp_tree<true>(p, cnt);
-      if (lane == 0) roots[0] = r;
-    }
-  } else {
-    uint32_t nch = (cnt + kFoldLeaf - 1) / kFoldLeaf;
-    for (uint32_t c = warp; c < nch; c += nw) {
-      const double r =
-          warp_tree<true>(p + uint64_t(c) * kFoldLeaf, min(kFoldLeaf, cnt - c * kFoldLeaf));
-      if (lane == 0) roots[c] = r;
-    }
-    __syncthreads();
-    while (nch > 1) {  // roots of roots: aligned 1024-chunks again
-      const uint32_t nn = (nch + kFoldLeaf - 1) / kFoldLeaf;
-      double r = 0.0;
-      if (warp < nn) r = warp_tree<false>(roots + warp * kFoldLeaf, min(kFoldLeaf, nch - warp * kFoldLeaf));
-      __syncthreads();
-      if (warp < nn && lane == 0) roots[warp] = r;
-      __syncthreads();
-      nch = nn;
-    }
-  }
-  __syncthreads();
-  const double r = roots[0];
-  __syncthreads();
-  return r;
-}
-
 // Sum pass for few leaves (one block per SM): the warp stages its leaves with
 // 16-byte loads (first halves, then the second halves in flight while the
 // chains fold the first) -- the freshly scattered x lands faster this way
@@ -1296,7 +1203,19 @@ __global__ void __launch_bounds__(32) k_fold_sum_ldg(FoldArgs a) {
   const double* v = stage + lane * kFoldPitch + my_off;
   const uint32_t first_end = min(my_len, kFoldHalf - my_off);
   double acc = 0.0;
+#ifdef DPMRF_PROBE
+  const long long c0 = clock64();
+  const unsigned long long g0 = gtimer();
+#endif
   if (my_len) acc = fold_span<false>(v, 1, first_end, v[0], 0.0);
+#ifdef DPMRF_PROBE
+  const long long c1 = clock64();
+  const unsigned long long g1 = gtimer();
+  if (lane == 0 && blockIdx.x < 256) {
+    g_probe_blk[0][blockIdx.x][6] = static_cast<unsigned long long>(c1 - c0);
+    g_probe_blk[0][blockIdx.x][7] = g1 - g0;
+  }
+#endif
   if ((lane & 31) == 0) PROBE_BLK_T(0, 5);
 #pragma unroll
   for (int j = 0; j < kLPB; ++j)
@@ -1356,30 +1275,11 @@ __global__ void __launch_bounds__(32) k_fold_sum(FoldArgs a) {
   PROBE_BLK_T(0, 2);
   a.partials[leaf] = fold_fetched<false>(row, off, len, n0, bar[lane], 0.0);
   PROBE_BLK_T(0, 3);
-#ifdef DPMRF_PROBE
-  {  // experiment: the same two fetches again (warm), timed to completion
-    __shared__ __align__(8) uint64_t bar2[kLPB][2];
-    mbar_init1(&bar2[lane][0]);
-    mbar_init1(&bar2[lane][1]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const unsigned long long t0 = gtimer();
-    uint32_t n0b;
-    fetch_leaf(row, src, len, bar2[lane], &n0b);
-    mbar_wait0(&bar2[lane][0]);
-    const unsigned long long t1 = gtimer();
-    if (len > n0b - off) mbar_wait0(&bar2[lane][1]);
-    const unsigned long long t2 = gtimer();
-    if (lane == 0 && blockIdx.x < 256) {
-      g_probe_blk[0][blockIdx.x][6] = t1 - t0;
-      g_probe_blk[0][blockIdx.x][7] = t2 - t0;
-    }
-  }
-#endif
 }
 
 template <int kLPB>
 __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
-  extern __shared__ __align__(16) double stage[];  // kLPB x kFoldPitch | kRootCap
+  extern __shared__ __align__(16) double stage[];  // kLPB x kFoldPitch | root_cap | 4 x scratch
   __shared__ __align__(8) uint64_t bar[kLPB][2];
   __shared__ uint32_t sr_s[kLPB], len_s[kLPB], off_s[kLPB], n0_s[kLPB];
   __shared__ double mu_s[kLPB];
@@ -1392,6 +1292,7 @@ __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
   double* roots = stage + kLPB * kFoldPitch;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr uint32_t kWarps = kSqThreads / 32;
+  double* qw = roots + a.root_cap + warp * kTreeScratch;  // this warp's tree scratch
   const uint32_t M = a.M;
   const uint32_t* n = lay;
   const uint32_t* label_start = lay + M;
@@ -1450,14 +1351,14 @@ __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
       for (uint32_t s = s_lo + warp; s <= s_hi; s += kWarps) {
         const uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
         if (cnt == 0) continue;  // (a label without leaves is held by no block)
-        const double folded = warp_tree<true>(a.partials + leaf_start[s], cnt);
+        const double folded = warp_tree<true>(a.partials + leaf_start[s], cnt, qw);
         if (lane == 0) publish(s, folded);
       }
     } else {
       for (uint32_t s = s_lo; s <= s_hi; ++s) {
         const uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
         if (cnt == 0) continue;
-        const double folded = block_series_tree(a.partials + leaf_start[s], cnt, roots);
+        const double folded = block_series_tree(a.partials + leaf_start[s], cnt, roots, qw);
         if (tid == 0) publish(s, folded);
       }
     }
@@ -1466,9 +1367,24 @@ __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
   }
   __syncthreads();
   PROBE_BLK(1, 2);
+  // the terms (x - mu)^2 (engine.cpp:213-217) by the whole block, in place;
+  // the chains then fold plain sums (one dependent DADD per element)
+#pragma unroll
+  for (int j = 0; j < kLPB; ++j) {
+    if (len_s[j] == 0) continue;
+    mbar_wait0(&bar[j][0]);
+    if (len_s[j] > n0_s[j] - off_s[j]) mbar_wait0(&bar[j][1]);
+    double* v = stage + j * kFoldPitch + off_s[j];
+    const double mu = mu_s[j];
+    for (uint32_t i = tid; i < len_s[j]; i += kSqThreads) {
+      const double d = __dsub_rn(v[i], mu);
+      v[i] = __dmul_rn(d, d);
+    }
+  }
+  __syncthreads();
   if (tid < kLPB && len_s[tid] != 0) {
-    a.sq_partials[first + tid] = fold_fetched<true>(stage + tid * kFoldPitch, off_s[tid],
-                                                    len_s[tid], n0_s[tid], bar[tid], mu_s[tid]);
+    const double* v = stage + tid * kFoldPitch + off_s[tid];
+    a.sq_partials[first + tid] = fold_span<false>(v, 1, len_s[tid], v[0], 0.0);
     if (tid == 0) PROBE_BLK_T(1, 3);
   }
   if (a.merged && (executed_iters(a.unconv, a.map_max, a.fixed) & 1)) {
@@ -1498,40 +1414,45 @@ __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
   auto series_cnt = [&](uint32_t s) {
     return s < M ? leaf_start[s + 1] - leaf_start[s] : leaf_start[M + 1] - leaf_start[M];
   };
-#ifdef DPMRF_PROBE
-  {  // i-cache experiment: the same trees + device log once, results discarded
-    __shared__ double sink_s[8];
-    for (uint32_t s = warp; s < nseries; s += kWarps) {
-      const uint32_t cnt = series_cnt(s);
-      if (cnt <= kFoldLeaf) {
-        const double r = cnt ? warp_tree<true>(series_ptr(s), cnt) : 0.0;
-        if (lane == 0) sink_s[s & 7] = r;
-      }
-    }
-    __syncthreads();
-    if (tid == 0) g_probe_tail[0][0] = gtimer();
-    if (tid < M) sink_s[tid] = log_fast(__ldcg(a.params + M + tid), lt_s, lt_s + kLogTable);
-    __syncthreads();
-    if (tid == 0) g_probe_tail[0][1] = gtimer();
-    if (tid == 0) g_probe_tail[0][2] = static_cast<unsigned long long>(sink_s[0] != 12345.0);
-  }
-#endif
   // every label's mu (published by the blocks above; empty labels keep the
   // previous one), loaded beside the trees' partials
   for (uint32_t s = tid; s < M; s += kSqThreads) mu_all[s] = __ldcg(a.params + s);
+  PROBE_TAIL(0, 2);
   bool all_short = true;
   for (uint32_t s = 0; s < nseries; ++s) all_short = all_short && series_cnt(s) <= kFoldLeaf;
   if (all_short) {  // one warp per series, all at once
     for (uint32_t s = warp; s < nseries; s += kWarps) {
       const uint32_t cnt = series_cnt(s);
-      const double r = cnt ? warp_tree<true>(series_ptr(s), cnt) : 0.0;
+      const double r = cnt ? warp_tree<true>(series_ptr(s), cnt, qw) : 0.0;
       if (lane == 0) root_s[s] = r;
     }
   } else {
+    // every series' aligned 1024-partial chunks by the warps at once (a
+    // chunk's root is the level-10 node of its series' tree), then one warp
+    // per series over its chunk roots
+    uint32_t total_chunks = 0;
+    for (uint32_t s = 0; s < nseries; ++s) total_chunks += (series_cnt(s) + kFoldLeaf - 1) / kFoldLeaf;
+    for (uint32_t c = warp; c < total_chunks; c += kWarps) {
+      uint32_t s = 0, base = 0;
+      while (c >= base + (series_cnt(s) + kFoldLeaf - 1) / kFoldLeaf) {
+        base += (series_cnt(s) + kFoldLeaf - 1) / kFoldLeaf;
+        ++s;
+      }
+      const uint32_t q = c - base, cnt = series_cnt(s);
+      const double r = warp_tree<true>(series_ptr(s) + uint64_t(q) * kFoldLeaf,
+                                       min(kFoldLeaf, cnt - q * kFoldLeaf), qw);
+      if (lane == 0) roots[c] = r;
+    }
+    __syncthreads();
+    PROBE_TAIL(0, 0);
+    uint32_t base = 0;
     for (uint32_t s = 0; s < nseries; ++s) {
-      const uint32_t cnt = series_cnt(s);
-      const double r = cnt ? block_series_tree(series_ptr(s), cnt, roots) : 0.0;
-      if (tid == 0) root_s[s] = r;
+      const uint32_t nch = (series_cnt(s) + kFoldLeaf - 1) / kFoldLeaf;
+      if (warp == s % kWarps) {
+        const double r = nch ? warp_tree<false>(roots + base, nch, qw) : 0.0;
+        if (lane == 0) root_s[s] = r;
+      }
+      base += nch;
     }
   }
   __syncthreads();
@@ -2298,17 +2219,20 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
   const uint64_t label_leaves = (uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M;
   const EmEpilogueArgs epv = ep ? *ep : EmEpilogueArgs{};
   if (!scatter_only) {
-    if (label_leaves > uint64_t(kRootCap) * kFoldLeaf ||
-        (Hs + kFoldLeaf - 1) / kFoldLeaf > uint64_t(kRootCap) * kFoldLeaf)
-      fail(DPMRF_INVALID_ARGUMENT, "M-step: series too long for the fold trees");
+    // chunk roots: every series' 1024-partial chunks at once in the tail
+    const uint64_t chunks = (label_leaves + kFoldLeaf - 1) / kFoldLeaf + M +
+                            ((Hs + kFoldLeaf - 1) / kFoldLeaf + kFoldLeaf - 1) / kFoldLeaf + 1;
+    if (chunks > 8192) fail(DPMRF_INVALID_ARGUMENT, "M-step: series too long for the fold trees");
+    const uint32_t root_cap = static_cast<uint32_t>((chunks + 31) / 32 * 32);
     const FoldArgs fa{x,       layout,        M,     hist,      Hs,
                       ring,    unconv,        map_max, fixed,   params,
                       partials, mb.sq_partials.get(), em_out, mb.done.get() + 1, epv,
-                      ep ? 1 : 0};
+                      ep ? 1 : 0, root_cap};
     if (few) {
       constexpr int kS = 2, kQ = 2;
       const size_t ss = size_t(kS) * kFoldPitch * sizeof(double);
-      const size_t sq = (size_t(kQ) * kFoldPitch + kRootCap) * sizeof(double);
+      const size_t sq = (size_t(kQ) * kFoldPitch + root_cap + (kSqThreads / 32) * kTreeScratch) *
+                        sizeof(double);
       ensure_dynamic_smem(k_fold_sum_ldg<kS>, ss);
       ensure_dynamic_smem(k_fold_sq<kQ>, sq);
       launch_pdl(k_fold_sum_ldg<kS>, dim3(grid_for(max_leaves, kS)), dim3(32), ss, s, fa);
@@ -2316,7 +2240,8 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
     } else {
       constexpr int kS = 8, kQ = 4;
       const size_t ss = size_t(kS) * kFoldPitch * sizeof(double);
-      const size_t sq = (size_t(kQ) * kFoldPitch + kRootCap) * sizeof(double);
+      const size_t sq = (size_t(kQ) * kFoldPitch + root_cap + (kSqThreads / 32) * kTreeScratch) *
+                        sizeof(double);
       ensure_dynamic_smem(k_fold_sum<kS>, ss);
       ensure_dynamic_smem(k_fold_sq<kQ>, sq);
       launch_pdl(k_fold_sum<kS>, dim3(grid_for(max_leaves, kS)), dim3(32), ss, s, fa);

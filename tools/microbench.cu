@@ -85,6 +85,52 @@ __global__ void leaf_chain_smem(double* out, long long* cycles) {
   if (threadIdx.x == 0) cycles[0] = t1 - t0;
 }
 
+// The M-step's fold_span (common path of the fold kernels) on 2 lanes of a
+// one-warp block; cycles AND globaltimer ns (-> the SM clock during the chain).
+__device__ __noinline__ double dpmrf_probe_fold(const double* v, uint32_t i, uint32_t end, double acc) {
+  constexpr int kG = 16;
+  double cur[kG], nxt[kG];
+  if (i + kG <= end) {
+#pragma unroll
+    for (int j = 0; j < kG; ++j) cur[j] = v[i + j];
+    while (i + 2 * kG <= end) {
+#pragma unroll
+      for (int j = 0; j < kG; ++j) nxt[j] = v[i + kG + j];
+#pragma unroll
+      for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, cur[j]);
+#pragma unroll
+      for (int j = 0; j < kG; ++j) cur[j] = nxt[j];
+      i += kG;
+    }
+#pragma unroll
+    for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, cur[j]);
+    i += kG;
+  }
+  for (; i < end; ++i) acc = __dadd_rn(acc, v[i]);
+  return acc;
+}
+
+__global__ void fold_span_probe(double* out, long long* cycles) {
+  __shared__ __align__(16) double s[2][1026];
+  for (int i = threadIdx.x; i < 2 * 1026; i += blockDim.x) (&s[0][0])[i] = 1.0 + i * 1e-9;
+  __syncwarp();
+  unsigned long long g0, g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  const long long t0 = clock64();
+  double acc = 0.0;
+  if (threadIdx.x < 2) {
+    const double* v = s[threadIdx.x];
+    acc = dpmrf_probe_fold(v, 1, 1024, v[0]);
+  }
+  const long long t1 = clock64();
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  out[threadIdx.x] = acc;
+  if (threadIdx.x == 0) {
+    cycles[0] = t1 - t0;
+    cycles[1] = (long long)(g1 - g0);
+  }
+}
+
 // Same chain with operands already in registers (the DADD-latency floor).
 __global__ void leaf_chain_regs(double* out, long long* cycles) {
   if (threadIdx.x >= 8) return;
@@ -165,6 +211,15 @@ int main() {
       }
       cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
       printf("dependent %s: %.2f cycles/op\n", names[op], double(h) / ns[op]);
+    }
+  }
+  {
+    long long hc[2];
+    for (int rep = 0; rep < 3; ++rep) {
+      fold_span_probe<<<1, 32>>>(d, c);
+      cudaMemcpy(hc, c, 16, cudaMemcpyDeviceToHost);
+      printf("fold_span 1023 adds: %lld cycles, %lld ns -> %.0f MHz, %.2f cycles/add\n", hc[0], hc[1],
+             1e3 * hc[0] / double(hc[1]), hc[0] / 1023.0);
     }
   }
   lds_chain<<<1, 256>>>(d, n, c);

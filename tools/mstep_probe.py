@@ -41,8 +41,6 @@ def main():
         tail = np.zeros((2, 4), np.uint64)
         assert fn(blk.ctypes.data, tail.ctypes.data) == 0
         valid = [(blk[k][:, 0] > 0) for k in range(2)]
-        if "--new" in sys.argv:  # k_fold_*: slots 2 = fetched, 3 = chain done; sq 2 = mu done
-            pass
         t0 = int(blk[0][valid[0], 0].min())
         rec = {"optimize_ms": r.stats["optimize_ms"], "em_us": r.stats["optimize_ms"] * 1e3 / em}
         for k, nm in ((0, "sum"), (1, "sq")):
@@ -77,8 +75,13 @@ def main():
                                        int(blk[k][i][6]), int(blk[k][i][7]))
                                       for i, x, y in zip(idx, d0, d3)]
             rec[f"k{k}_first_wait_hist"] = np.histogram(d0, bins=[0, .5, 1, 1.5, 2, 2.5, 3, 5])[0].tolist()
-        rec["icache_trees_warm_us"] = (int(tail[0][0]) - int(tail[1][0])) / 1e3
-        rec["icache_log_cold_us"] = (int(tail[0][1]) - int(tail[0][0])) / 1e3
+        b0 = blk[0][valid[0]]
+        cyc, ns = b0[:, 6].astype(np.float64), b0[:, 7].astype(np.float64)
+        okc = ns > 0
+        rec["sum_first_span_cycles_ns_mhz"] = [float(np.median(cyc[okc])), float(np.median(ns[okc])),
+                                               float(np.median(cyc[okc] / ns[okc] * 1e3))]
+        rec["tail_mu_loads_us"] = (int(tail[0][2]) - t0) / 1e3
+        rec["tail_chunks_us"] = (int(tail[0][0]) - t0) / 1e3
         out.append(rec)
         print(json.dumps(rec))
     ctx.close()
