@@ -143,7 +143,8 @@ void dpmrf_context::prepare() {
     const uint32_t* hs = h_err + 2;
     const uint32_t* so = series_alias ? h_off.get() : s_off_buf.get();
     if (hs[1] <= 32767u) adj_k = hs[0] <= 4 ? 4 : (hs[0] <= 8 ? 8 : 0);
-    if (hs[3] < 0xFFFFu && Hs > 0)
+    // (the packed hood pass indexes hoods with 32 bits)
+    if (hs[3] < 0xFFFFu && Hs > 0 && Hs < (uint64_t(1) << 32) - 256)
       hood_k = hs[2] <= 9 ? 8 : (hs[2] <= 13 && use_k12 ? 12 : (hs[2] <= 17 ? 16 : 0));
     if (adj_k) launch_pack_adjacency(g_off.get(), g_nbr.get(), R, adj_k,
                                      adj_pk.ensure(uint64_t(R) * adj_k), stream);
@@ -171,6 +172,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     if (const char* e = std::getenv("DPMRF_CSR")) c->use_packed = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_NO_K12")) c->use_k12 = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_UNFUSED")) c->use_fused = e[0] == '0';
+    if (const char* e = std::getenv("DPMRF_CLUSTER_SQ")) c->ms.cluster_sq = e[0] != '0';
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));

@@ -603,15 +603,19 @@ __global__ void k_init_log_table() {
   }
 }
 
+// vals: this EM's [total, T, mu(M), sigma(M)] -- a.em_out, or the caller's
+// shared-memory copy (saves the global round trip).
 __device__ void em_record(const EmEpilogueArgs& a, bool merged, const EmPrefetch* pf = nullptr,
-                          const double* thi = g_log_table.hi, const double* tlo = g_log_table.lo) {
+                          const double* thi = g_log_table.hi, const double* tlo = g_log_table.lo,
+                          const double* vals = nullptr) {
   const int lane = threadIdx.x & 31;
   const int T = pf ? pf->T : executed_iters(a.unconv, a.map_max, a.fixed);
   const uint32_t e = pf ? pf->e : a.unconv[kEmCount];
   const uint32_t M = a.M;
+  if (!vals) vals = a.em_out;
   double* rec = a.em_rec + uint64_t(e) * (3 + 3 * M);
   for (uint32_t l = lane; l < M; l += 32) {  // one lane per label evaluates the device log
-    const double mu = a.em_out[2 + l], sg = a.em_out[2 + M + l];
+    const double mu = vals[2 + l], sg = vals[2 + M + l];
     const double ls = log_fast(sg, thi, tlo);
     rec[3 + l] = mu;
     rec[3 + M + l] = sg;
@@ -622,7 +626,7 @@ __device__ void em_record(const EmEpilogueArgs& a, bool merged, const EmPrefetch
   }
   __syncwarp();
   if (lane != 0) return;
-  const double total = a.em_out[0];
+  const double total = vals[0];
   a.em_hist[e] = total;
   uint32_t conv = 0;
   if (int(e) + 1 >= a.L + 1) {
@@ -1481,6 +1485,183 @@ __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// k_fold_sq_cluster: the sq pass and the EM tail as ONE thread-block cluster
+// of kClCtas CTAs, for graphs with few label leaves (2560^2: ~100).  Same
+// arithmetic and fetch schedule as k_fold_sq, but the cross-block combine
+// runs through distributed shared memory instead of a global ticket: each
+// CTA pushes its sq partials, and the mu of every label whose first leaf it
+// holds, into CTA 0's shared memory (st.shared::cluster); one cluster
+// barrier; CTA 0 then runs the sigma trees and the EM record straight from
+// shared memory.  CTA 0's last warp folds the total-energy tree (series M of
+// the sum pass) while the chains run, so it is off the critical path.
+// ---------------------------------------------------------------------------
+constexpr int kClCtas = 8;
+constexpr int kClThreads = 128;
+constexpr uint32_t kClMaxPer = 24;  // staged label leaves per CTA
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// store v into CTA `cta`'s copy of the shared variable *p (same layout in every CTA)
+__device__ __forceinline__ void st_cluster(double* p, uint32_t cta, double v) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(cta));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+__global__ void __launch_bounds__(kClThreads) k_fold_sq_cluster(FoldArgs a, uint32_t per,
+                                                                uint32_t sq_cap) {
+  extern __shared__ __align__(16) double stage[];  // per x kFoldPitch | sqp[sq_cap] | scratch
+  __shared__ __align__(8) uint64_t bar[kClMaxPer][2];
+  __shared__ uint32_t sr_s[kClMaxPer], len_s[kClMaxPer], off_s[kClMaxPer], n0_s[kClMaxPer];
+  __shared__ double mu_s[kClMaxPer];
+  __shared__ uint32_t lay[4 * kMaxLabels + 4];
+  __shared__ double root_s[kMaxLabels + 1];
+  __shared__ double vals[2 + 2 * kMaxLabels];  // CTA 0: [total, T, mu(M), sigma(M)]
+  __shared__ double mu_pub[kMaxLabels];         // CTA 0: mu pushed by the label's first CTA
+  __shared__ EmPrefetch pf;
+  __shared__ double lt_s[2 * kLogTable];
+  double* sqp = stage + per * kFoldPitch;  // CTA 0: sq partials of every label leaf
+  double* qw = sqp + sq_cap;               // CTA 0's last warp: tree scratch
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr uint32_t kWarps = kClThreads / 32;
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t M = a.M;
+  const uint32_t* n = lay;
+  const uint32_t* label_start = lay + M;
+  const uint32_t* leaf_start = lay + 2 * M + 1;
+  const uint32_t first = rank * per;
+  if (tid < per) {
+    mbar_init1(&bar[tid][0]);
+    mbar_init1(&bar[tid][1]);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // (every CTA of the cluster has started before anyone writes remote
+  // shared memory: arrive now, wait after the grid dependency)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  // before the wait (as k_fold_sq): x, the layout, the skip flag and the MAP
+  // counters are the MAP launches'; params and the EM history the previous EM's
+  const bool skipped = em_skipped(a.unconv);  // (the same value in every CTA)
+  for (uint32_t i = tid; i < 4 * M + 4; i += kClThreads) lay[i] = a.layout[i];
+  if (rank == 0) {
+    for (uint32_t i = tid; i < 2 * kLogTable; i += kClThreads)
+      lt_s[i] = i < kLogTable ? g_log_table.hi[i] : g_log_table.lo[i - kLogTable];
+    // a label without vertices keeps its parameters (engine.cpp:209-220)
+    for (uint32_t l = tid; l < M; l += kClThreads) {
+      vals[2 + l] = a.params[l];
+      vals[2 + M + l] = a.params[M + l];
+    }
+    if (a.merged && !skipped && tid == 32) em_prefetch(a.ep, &pf);
+  }
+  __syncthreads();
+  if (!skipped && tid < per) {
+    const uint32_t leaf = first + tid;
+    uint32_t len = 0;
+    if (leaf < leaf_start[M]) {
+      const uint32_t sr = series_of(leaf_start, M, leaf);
+      const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
+      const uint64_t rem = n[sr] - b;
+      len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
+      sr_s[tid] = sr;
+      off_s[tid] = fetch_leaf(stage + tid * kFoldPitch, a.x + label_start[sr] + b, len, bar[tid],
+                              &n0_s[tid]);
+    }
+    len_s[tid] = len;
+  }
+  pdl_wait();  // the sum pass is complete: its partials are visible
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  if (skipped) return;  // (uniform over the cluster)
+  __syncthreads();
+  const int T = executed_iters(a.unconv, a.map_max, a.fixed);
+  // mu of this CTA's labels from the sum-pass partials, one warp per label
+  if (per && len_s[0] != 0) {
+    const uint32_t s_lo = sr_s[0];
+    uint32_t s_hi = s_lo;
+    for (uint32_t j = 1; j < per; ++j)
+      if (len_s[j] != 0) s_hi = sr_s[j];
+    for (uint32_t s = s_lo + warp; s <= s_hi; s += kWarps) {
+      const uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
+      if (cnt == 0) continue;  // (a label without leaves is held by no CTA)
+      const double folded = warp_tree512<true>(a.partials + leaf_start[s], cnt);
+      if (lane == 0) {
+        const double mu = __ddiv_rn(folded, static_cast<double>(n[s]));
+        root_s[s - s_lo] = mu;
+        if (leaf_start[s] >= first && leaf_start[s] < first + per) st_cluster(&mu_pub[s], 0, mu);
+      }
+    }
+    __syncthreads();
+    if (tid < per && len_s[tid] != 0) mu_s[tid] = root_s[sr_s[tid] - s_lo];
+  }
+  __syncthreads();
+  // the terms (x - mu)^2 (engine.cpp:213-217) by the whole CTA, in place
+  for (uint32_t j = 0; j < per; ++j) {
+    if (len_s[j] == 0) continue;
+    mbar_wait0(&bar[j][0]);
+    if (len_s[j] > n0_s[j] - off_s[j]) mbar_wait0(&bar[j][1]);
+    double* v = stage + j * kFoldPitch + off_s[j];
+    const double mu = mu_s[j];
+    for (uint32_t i = tid; i < len_s[j]; i += kClThreads) {
+      const double d = __dsub_rn(v[i], mu);
+      v[i] = __dmul_rn(d, d);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // the dependent chains (fold_leaf), one lane per staged leaf
+    if (tid < per && len_s[tid] != 0) {
+      const double* v = stage + tid * kFoldPitch + off_s[tid];
+      st_cluster(&sqp[first + tid], 0, fold_span<false>(v, 1, len_s[tid], v[0], 0.0));
+    }
+  } else {
+    if (rank == 0 && warp == kWarps - 1) {
+      // total energy: dpp::reduce(..., 0.0) over the last executed MAP row
+      // (optimize.cpp:64-65) -- identity only for empty input
+      const uint32_t cnt = leaf_start[M + 1] - leaf_start[M];
+      const double r = cnt ? warp_tree<true>(a.partials + leaf_start[M], cnt, qw) : 0.0;
+      if (lane == 0) {
+        vals[0] = r;
+        vals[1] = static_cast<double>(T);
+      }
+    }
+    if (a.merged && (T & 1)) {
+      // device-resident loop: the next EM starts from buffer 0, so an odd
+      // number of MAP iterations moves the committed labels back
+      const uint64_t stride = uint64_t(kClCtas) * (kClThreads - 32);
+      const uint64_t g = uint64_t(rank) * (kClThreads - 32) + (tid - 32);
+      const uint64_t words = a.ep.R / 4;
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(a.ep.lab1);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(a.ep.lab0);
+      for (uint64_t w = g; w < words; w += stride) dst[w] = src[w];
+      for (uint64_t v = words * 4 + g; v < a.ep.R; v += stride) a.ep.lab0[v] = a.ep.lab1[v];
+    }
+  }
+  cluster_sync_all();  // every sq partial and mu is in CTA 0's shared memory
+  if (rank != 0) return;
+  for (uint32_t s = warp; s < M; s += kWarps) {
+    const uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
+    if (cnt == 0) continue;  // empty labels keep their previous parameters
+    const double folded = warp_tree512<false>(sqp + leaf_start[s], cnt);
+    if (lane == 0) {
+      vals[2 + s] = mu_pub[s];
+      const double sd = __dsqrt_rn(__ddiv_rn(folded, static_cast<double>(n[s])));
+      vals[2 + M + s] = sd < kSigmaFloor ? kSigmaFloor : sd;
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < 2 + 2 * M; i += kClThreads) {
+    a.em_out[i] = vals[i];
+    if (i >= 2) a.params[i - 2] = vals[i];
+  }
+  if (a.merged && tid < 32) em_record(a.ep, true, &pf, lt_s, lt_s + kLogTable, vals);
+}
+
+// ---------------------------------------------------------------------------
 // Device-resident EM loop (no host round trip between EM iterations).
 // k_em_prologue arms the MAP counters and folds the previous epilogue's stop
 // decision into the state (so every kernel of this EM sees one value);
@@ -1665,6 +1846,14 @@ constexpr int fused_min_blocks(int mt, int kh, int vp = 1) {
   return mt == 2 && kh == 8 ? (vp == 2 ? DPMRF_FUSED_MINB_VP2 : DPMRF_FUSED_MINB)
                             : (mt == 5 ? DPMRF_FUSED_MINB_M5 : 1);
 }
+#ifndef DPMRF_HOIST_MEAN
+#define DPMRF_HOIST_MEAN 0
+#endif
+// The static region mean is read before griddepcontrol.wait on the
+// one-vertex instances (2560^2: part of the +10% of the index diet); the
+// two-vertex instance reads it after the wait (hoisting both means costs it
+// spills: 16384^2 662 vs 675 EM-it/s).
+constexpr bool kHoistMean = DPMRF_HOIST_MEAN != 0;
 constexpr int kWinRegs = 3;  // window rows held in registers (default L = 3)
 constexpr uint32_t kVertsPerThreadMin = 1u << 20;  // owned vertices for 2 per thread
 template <int MT, int K>
@@ -1682,6 +1871,17 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
 
 
 bool map_fused_supported(const MapArgs& a) { return a.adj_k && a.hood_k; }
+
+namespace {
+// The launch's copy of the arguments with the ring rows of hood iteration th.
+MapArgs with_rows(const MapArgs& a, int th) {
+  MapArgs r = a;
+  const int R1 = a.ring > 0 ? a.ring : 1;
+  r.row_t = th >= 0 ? th % R1 : 0;
+  r.row_p = th >= 1 ? (th - 1) % R1 : 0;
+  return r;
+}
+}  // namespace
 
 bool mstep_tail_fusable(uint32_t R, uint32_t M) {
   const uint64_t tiles = (uint64_t(R) + kTileVerts - 1) / kTileVerts;
@@ -1705,8 +1905,12 @@ void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
   const ScatterArgs scv = tail ? *sc : ScatterArgs{};
   const size_t smem = tail ? scatter_small_smem(sc->M) : 0;
   const dim3 g(nh + nv + ns), blk(kVtxThreads);
+  MapArgs ar = with_rows(a, t - 1);
+  // fixed work: only the last vertex pass's label counts are ever read (by
+  // the M-step's grouping), so the other passes skip their block counts
+  if (a.fixed && t != map_max - 1) ar.tile_counts = nullptr;
 #define MF4(MT, KV, KH, VP)                                                              \
-  launch_pdl(k_map_fused<MT, KV, KH, VP>, g, blk, smem, s, a, lab_in, lab_out, minE_prev,  \
+  launch_pdl(k_map_fused<MT, KV, KH, VP>, g, blk, smem, s, ar, lab_in, lab_out, minE_prev,  \
              minE_cur, t, nh, nv, scv)
 #define MF(MT, KV, KH) MF4(MT, KV, KH, 1)
   if (a.M == 5 && a.adj_k == 8 && a.hood_k == 16) {  // config C's layout: label loop unrolled
@@ -1775,9 +1979,10 @@ void launch_vertex_argmin(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_
 void launch_hood_sums(const MapArgs& a, int t, cudaStream_t s) {
   const dim3 g(grid_for(a.h_end - a.h_begin, kHoodThreads)), blk(kHoodThreads);
   if (a.hood_k) {
-    if (a.hood_k == 8) launch_pdl(k_hood_packed<8>, g, blk, 0, s, a, t);
-    else if (a.hood_k == 12) launch_pdl(k_hood_packed<12>, g, blk, 0, s, a, t);
-    else launch_pdl(k_hood_packed<16>, g, blk, 0, s, a, t);
+    const MapArgs ar = with_rows(a, t);
+    if (a.hood_k == 8) launch_pdl(k_hood_packed<8>, g, blk, 0, s, ar, t);
+    else if (a.hood_k == 12) launch_pdl(k_hood_packed<12>, g, blk, 0, s, ar, t);
+    else launch_pdl(k_hood_packed<16>, g, blk, 0, s, ar, t);
     return;
   }
   launch_pdl(k_hood_sums, g, blk, 0, s, a.s_off, a.h_mem, (const double*)a.minE, a.hist,
@@ -1830,12 +2035,15 @@ __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
   const uint32_t v0 = a.v_begin + blk * (kVtxThreads * P) + threadIdx.x;
   int16_t d[P][K];
   uint8_t old[P], cov[P];
+  double xs[P];
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     const uint32_t v = v0 + j * kVtxThreads;
+    xs[j] = 0.0;
     if (v < a.v_end) {
       load_i16<K>(a.adj_pk + uint64_t(v) * K, d[j]);
       cov[j] = a.cover[v];
+      if (kHoistMean || P == 1) xs[j] = a.mean[v];
     }
   }
   pdl_wait();
@@ -1862,9 +2070,11 @@ __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
     for (int k = 0; k < K; ++k) {
       const bool ok = d[j][k] != INT16_MIN;
       deg += ok;
-      nb[k] = ok ? lab_in[int64_t(v) + d[j][k]] : uint8_t(0xFF);
+      // (u32 wrap-around: v + d is a vertex id whenever the slot is present)
+      nb[k] = ok ? lab_in[v + static_cast<uint32_t>(static_cast<int32_t>(d[j][k]))]
+                 : uint8_t(0xFF);
     }
-    const double x = a.mean[v];
+    const double x = kHoistMean || P == 1 ? xs[j] : a.mean[v];
     const double* T = a.terms;
     double best;
     uint32_t best_l;
@@ -1946,11 +2156,17 @@ __device__ __forceinline__ void load_hood_row(const uint16_t* __restrict__ row,
 // One hood's sum (left fold of its members' minima in slot order,
 // engine.cpp:147-152) + record + window test (engine.cpp:154-169); returns 1
 // when the hood is not converged.
+//
+// The ring rows of iterations t and t-1 come precomputed with the launch
+// (MapArgs::row_t / row_p, set by with_rows): no per-thread modulo, and the
+// hood index stays 32-bit (one wide multiply-add per address).
 template <int K>
 __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restrict__ minE, int t,
-                                         uint64_t h, uint32_t base, const uint32_t (&u)[K / 2]) {
+                                         uint32_t h, uint32_t base, const uint32_t (&u)[K / 2]) {
   const int R1 = a.ring;
   const int nwin = t >= a.L ? a.L : 0;
+  double* __restrict__ row_t = a.hist + uint64_t(a.row_t) * a.Hs;
+  const double* __restrict__ row_p = a.hist + uint64_t(a.row_p) * a.Hs;
   // Window test with an equal-run count: eq[h] = how many predecessors of
   // the previous row are bit-identical to it (a hood whose members' minima
   // did not change sums to the same bits).  Only row t-1 and the count are
@@ -1963,7 +2179,7 @@ __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restr
   double p1 = 0.0;
   uint32_t e1 = 0;
   if (t >= 1) {
-    p1 = a.hist[uint64_t((t - 1) % R1) * a.Hs + h];
+    p1 = row_p[h];
     e1 = a.eq[h];
   }
   double e[K];
@@ -1972,13 +2188,15 @@ __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restr
     const uint32_t dk = (u[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
     e[k] = dk != 0xFFFFu ? minE[base + dk] : 0.0;
   }
+  // Absent slots add +0.0, which leaves every partial sum unchanged: a
+  // minimum energy is never -0.0 (label_energy's q >= +0 and log sigma is
+  // finite, so neither rounded sum can be -0), hence no partial sum is -0
+  // and x + (+0) == x bit for bit (NaN stays the canonical NaN).  Same
+  // bits as folding only the present members, without the selects.
   double sum = minE[base];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const uint32_t dk = (u[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
-    if (dk != 0xFFFFu) sum = __dadd_rn(sum, e[k]);
-  }
-  a.hist[uint64_t(t % R1) * a.Hs + h] = sum;
+  for (int k = 0; k < K; ++k) sum = __dadd_rn(sum, e[k]);
+  row_t[h] = sum;
   int ok = nwin > 0;
   const bool same = t >= 1 && sum == p1;  // (false for NaN)
   a.eq[h] = static_cast<uint8_t>(same ? min(e1 + 1u, 255u) : 0u);
@@ -1987,12 +2205,15 @@ __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restr
       ok = 0;
     } else if (e1 + 1 < uint32_t(nwin)) {
       // rows t-1-e1 .. t-1 equal p1 (their comparisons are implied); read the rest
+      int row = a.row_p - int(e1) - 1;  // row of iteration t - (e1 + 2)
+      if (row < 0) row += R1;
       for (int i = int(e1) + 2; i <= nwin; ++i) {
-        const double p = a.hist[uint64_t((t - i) % R1) * a.Hs + h];
+        const double p = a.hist[uint64_t(row) * a.Hs + h];
         if (!(fabs(__dsub_rn(sum, p)) < a.tol)) {
           ok = 0;
           break;
         }
+        row = row == 0 ? R1 - 1 : row - 1;
       }
     }
   }
@@ -2007,13 +2228,13 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
                                                  const double* __restrict__ minE, int t,
                                                  uint32_t blk, int skip_t) {
   static_assert(K == 8 || K == 12 || K == 16, "hood pack width");
-  const uint64_t h = a.h_begin + uint64_t(blk) * kHoodThreads + threadIdx.x;
+  const uint32_t h = static_cast<uint32_t>(a.h_begin) + blk * kHoodThreads + threadIdx.x;
   const bool live = h < a.h_end;
   uint32_t base = 0;
   uint32_t u[K / 2];
   if (live) {
     base = a.hood_base[h];
-    load_hood_row<K>(a.hood_pk + h * K, u);
+    load_hood_row<K>(a.hood_pk + uint64_t(h) * K, u);
   }
   pdl_wait();
   int not_conv = 0;
@@ -2228,7 +2449,21 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
                       ring,    unconv,        map_max, fixed,   params,
                       partials, mb.sq_partials.get(), em_out, mb.done.get() + 1, epv,
                       ep ? 1 : 0, root_cap};
-    if (few) {
+    const uint64_t hood_leaves = (Hs + kFoldLeaf - 1) / kFoldLeaf;
+    if (few && mb.cluster_sq && label_leaves <= uint64_t(kClCtas) * kClMaxPer &&
+        hood_leaves <= kFoldLeaf) {
+      // the sq pass + EM tail as one cluster (distributed shared memory)
+      constexpr int kS = 2;
+      const size_t ss = size_t(kS) * kFoldPitch * sizeof(double);
+      const uint32_t per = static_cast<uint32_t>((label_leaves + kClCtas - 1) / kClCtas);
+      const uint32_t sq_cap = static_cast<uint32_t>((label_leaves + 1) / 2 * 2);
+      const size_t sc = (size_t(per) * kFoldPitch + sq_cap + kTreeScratch) * sizeof(double);
+      ensure_dynamic_smem(k_fold_sum_ldg<kS>, ss);
+      ensure_dynamic_smem(k_fold_sq_cluster, sc);
+      launch_pdl(k_fold_sum_ldg<kS>, dim3(grid_for(max_leaves, kS)), dim3(32), ss, s, fa);
+      launch_pdl_cluster(k_fold_sq_cluster, dim3(kClCtas), dim3(kClThreads), sc, kClCtas, s, fa,
+                         per, sq_cap);
+    } else if (few) {
       constexpr int kS = 2, kQ = 2;
       const size_t ss = size_t(kS) * kFoldPitch * sizeof(double);
       const size_t sq = (size_t(kQ) * kFoldPitch + root_cap + (kSqThreads / 32) * kTreeScratch) *

@@ -46,6 +46,9 @@ struct MapArgs {
   uint32_t* unconv;  // per MAP iteration count of unconverged hoods
   uint32_t* tile_counts;  // 2 x tiles x M: label counts per 256-vertex tile, by iteration parity
   uint32_t tiles;
+  // Per launch (set by the launchers from the hood iteration th): the ring
+  // rows of iterations th and th-1, so no thread evaluates a modulo.
+  int row_t, row_p;
 };
 
 // Number of 256-vertex label tiles (== vertex-kernel blocks).
@@ -109,6 +112,7 @@ struct MStepBuffers {
   DevBuf<uint32_t> chunk_sum;    // per-1024-tile-chunk label counts (large graphs)
   DevBuf<uint32_t> err;
   DevBuf<double> em_scratch;
+  bool cluster_sq = true;  // small graphs: sq pass + EM tail as one cluster (DPMRF_CLUSTER_SQ=0: off)
 };
 
 // update_parameters (engine.cpp:193-223) over the labels left by the last

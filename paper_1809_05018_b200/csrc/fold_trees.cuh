@@ -94,6 +94,17 @@ __device__ double warp_tree(const double* p, uint32_t cnt, double* q) {
   return lanes_tree(regs_tree<32>(e, r), (cnt + 31) / 32);
 }
 
+// warp_tree for cnt <= 512 without scratch: up to 16 partials per lane in
+// registers (the same aligned blocks, so the same tree).
+template <bool kGlobal>
+__device__ __forceinline__ double warp_tree512(const double* p, uint32_t cnt) {
+  if (cnt <= 32) return warp_tree_regs<1, kGlobal>(p, cnt);
+  if (cnt <= 64) return warp_tree_regs<2, kGlobal>(p, cnt);
+  if (cnt <= 128) return warp_tree_regs<4, kGlobal>(p, cnt);
+  if (cnt <= 256) return warp_tree_regs<8, kGlobal>(p, cnt);
+  return warp_tree_regs<16, kGlobal>(p, cnt);
+}
+
 // The whole series' tree by the block: aligned 1024-partial chunks (a
 // chunk's root is exactly the level-10 node of the series' tree) by the
 // warps in parallel, roots in shared memory, then the tree over the roots

@@ -314,12 +314,14 @@ def test_concurrent_calls_on_one_context_serialize(ctx):
     assert not errors, errors
 
 
-@pytest.mark.parametrize("env", ["DPMRF_NO_K12"])
-def test_opt_in_layouts_agree(env, monkeypatch):
-    """16-slot rows for brick hoods (DPMRF_NO_K12=1) reproduce the fixtures
-    and the default path."""
+@pytest.mark.parametrize("env,val", [("DPMRF_NO_K12", "1"), ("DPMRF_CLUSTER_SQ", "0")])
+def test_opt_in_layouts_agree(env, val, monkeypatch):
+    """16-slot rows for brick hoods (DPMRF_NO_K12=1), and the grid-wide sq
+    pass with its global-ticket tail instead of the one-cluster sq pass on
+    small graphs (DPMRF_CLUSTER_SQ=0), reproduce the fixtures and the
+    default path."""
     from paper_1809_05018_b200 import inputs
-    monkeypatch.setenv(env, "1")
+    monkeypatch.setenv(env, val)
     c = E.Context(0)
     monkeypatch.delenv(env)
     base = E.Context(0)
