@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <map>
 #include <mutex>
 #include <set>
 #include <stdexcept>
@@ -104,19 +105,21 @@ struct HostBuf {
   }
 };
 
-// Opt a kernel into `bytes` of dynamic shared memory on the current device,
-// once per (kernel, device); thread-safe.
+// Opt a kernel into at least `bytes` of dynamic shared memory on the current
+// device (the attribute only grows: a kernel launched with several sizes
+// keeps the largest); thread-safe.
 template <class F>
 inline void ensure_dynamic_smem(F* kernel, size_t bytes) {
   static std::mutex mu;
-  static std::set<std::tuple<const void*, int, size_t>> done;
+  static std::map<std::pair<const void*, int>, size_t> set_to;
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, bytes);
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
   std::lock_guard<std::mutex> lock(mu);
-  if (done.count(key)) return;
+  auto it = set_to.find(key);
+  if (it != set_to.end() && it->second >= bytes) return;
   CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-  done.insert(key);
+  set_to[key] = bytes;
 }
 
 // Programmatic Dependent Launch: a kernel launched this way may be scheduled

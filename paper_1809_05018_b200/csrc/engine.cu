@@ -1495,8 +1495,15 @@ __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
 // shared memory.  CTA 0's last warp folds the total-energy tree (series M of
 // the sum pass) while the chains run, so it is off the critical path.
 // ---------------------------------------------------------------------------
+#ifndef DPMRF_CL_THREADS
+#define DPMRF_CL_THREADS 128
+#endif
+#ifndef DPMRF_CL_BLOCKSQ
+#define DPMRF_CL_BLOCKSQ 0
+#endif
 constexpr int kClCtas = 8;
-constexpr int kClThreads = 128;
+constexpr int kClThreads = DPMRF_CL_THREADS;
+constexpr bool kClBlockSq = DPMRF_CL_BLOCKSQ != 0;
 constexpr uint32_t kClMaxPer = 24;  // staged label leaves per CTA
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -1537,6 +1544,7 @@ __global__ void __launch_bounds__(kClThreads) k_fold_sq_cluster(FoldArgs a, uint
   const uint32_t* label_start = lay + M;
   const uint32_t* leaf_start = lay + 2 * M + 1;
   const uint32_t first = rank * per;
+  PROBE_BLK(1, 0);
   if (tid < per) {
     mbar_init1(&bar[tid][0]);
     mbar_init1(&bar[tid][1]);
@@ -1576,6 +1584,7 @@ __global__ void __launch_bounds__(kClThreads) k_fold_sq_cluster(FoldArgs a, uint
   }
   pdl_wait();  // the sum pass is complete: its partials are visible
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  PROBE_BLK(1, 1);
   if (skipped) return;  // (uniform over the cluster)
   __syncthreads();
   const int T = executed_iters(a.unconv, a.map_max, a.fixed);
@@ -1599,25 +1608,42 @@ __global__ void __launch_bounds__(kClThreads) k_fold_sq_cluster(FoldArgs a, uint
     if (tid < per && len_s[tid] != 0) mu_s[tid] = root_s[sr_s[tid] - s_lo];
   }
   __syncthreads();
-  // the terms (x - mu)^2 (engine.cpp:213-217) by the whole CTA, in place
-  for (uint32_t j = 0; j < per; ++j) {
-    if (len_s[j] == 0) continue;
-    mbar_wait0(&bar[j][0]);
-    if (len_s[j] > n0_s[j] - off_s[j]) mbar_wait0(&bar[j][1]);
-    double* v = stage + j * kFoldPitch + off_s[j];
-    const double mu = mu_s[j];
-    for (uint32_t i = tid; i < len_s[j]; i += kClThreads) {
-      const double d = __dsub_rn(v[i], mu);
-      v[i] = __dmul_rn(d, d);
+  if (kClBlockSq) {
+    // the terms (x - mu)^2 (engine.cpp:213-217) by the whole CTA, in place
+    for (uint32_t j = 0; j < per; ++j) {
+      if (len_s[j] == 0) continue;
+      mbar_wait0(&bar[j][0]);
+      if (len_s[j] > n0_s[j] - off_s[j]) mbar_wait0(&bar[j][1]);
+      double* v = stage + j * kFoldPitch + off_s[j];
+      const double mu = mu_s[j];
+#pragma unroll 4
+      for (uint32_t i = tid; i < len_s[j]; i += kClThreads) {
+        const double d = __dsub_rn(v[i], mu);
+        v[i] = __dmul_rn(d, d);
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
+  PROBE_BLK(1, 2);
   if (warp == 0) {
-    // the dependent chains (fold_leaf), one lane per staged leaf
+    // the dependent chains (fold_leaf) over (x - mu)^2 (engine.cpp:213-217),
+    // one lane per staged leaf (kClBlockSq: squared above; else the squares
+    // are computed in the chain, off its dependent path)
     if (tid < per && len_s[tid] != 0) {
       const double* v = stage + tid * kFoldPitch + off_s[tid];
-      st_cluster(&sqp[first + tid], 0, fold_span<false>(v, 1, len_s[tid], v[0], 0.0));
+      double r;
+      if (kClBlockSq) {
+        r = fold_span<false>(v, 1, len_s[tid], v[0], 0.0);
+      } else {
+        mbar_wait0(&bar[tid][0]);
+        if (len_s[tid] > n0_s[tid] - off_s[tid]) mbar_wait0(&bar[tid][1]);
+        const double mu = mu_s[tid];
+        const double d0 = __dsub_rn(v[0], mu);
+        r = fold_span<true>(v, 1, len_s[tid], __dmul_rn(d0, d0), mu);
+      }
+      st_cluster(&sqp[first + tid], 0, r);
     }
+    PROBE_BLK_T(1, 3);
   } else {
     if (rank == 0 && warp == kWarps - 1) {
       // total energy: dpp::reduce(..., 0.0) over the last executed MAP row
@@ -1643,6 +1669,7 @@ __global__ void __launch_bounds__(kClThreads) k_fold_sq_cluster(FoldArgs a, uint
   }
   cluster_sync_all();  // every sq partial and mu is in CTA 0's shared memory
   if (rank != 0) return;
+  PROBE_TAIL(1, 0);
   for (uint32_t s = warp; s < M; s += kWarps) {
     const uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
     if (cnt == 0) continue;  // empty labels keep their previous parameters
@@ -1658,7 +1685,9 @@ __global__ void __launch_bounds__(kClThreads) k_fold_sq_cluster(FoldArgs a, uint
     a.em_out[i] = vals[i];
     if (i >= 2) a.params[i - 2] = vals[i];
   }
+  PROBE_TAIL(1, 1);
   if (a.merged && tid < 32) em_record(a.ep, true, &pf, lt_s, lt_s + kLogTable, vals);
+  PROBE_TAIL(1, 2);
 }
 
 // ---------------------------------------------------------------------------

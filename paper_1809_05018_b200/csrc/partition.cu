@@ -38,6 +38,7 @@
 // one device; device-to-device copies and a counter-sum kernel -- the same
 // schedule without NVLink, which is how one GPU tests the partition logic).
 #include <dlfcn.h>
+#include <cstdlib>
 #include <nccl.h>  // types and enums only; every symbol comes from dlsym
 
 #include <algorithm>
@@ -78,8 +79,12 @@ struct Nccl {
     return n;
   }
   void load() {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    // DPMRF_NCCL_LIB: another library with the same entry points (the test
+    // suite's in-process multi-rank shim, tests/nccl_shim)
+    const char* alt = std::getenv("DPMRF_NCCL_LIB");
+    void* h = alt && alt[0] ? dlopen(alt, RTLD_NOW | RTLD_GLOBAL)
+                            : dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h && !(alt && alt[0])) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) fail(DPMRF_NCCL_ERROR, std::string("cannot load libnccl.so.2: ") + dlerror());
     auto sym = [&](const char* name) {
       void* p = dlsym(h, name);
@@ -886,6 +891,8 @@ extern "C" dpmrf_status dpmrf_group_create_nccl(dpmrf_context* ctx, const uint8_
     g->rank = rank;
     g->use_graph = false;  // NCCL calls are enqueued directly (no capture)
     if (const char* e = std::getenv("DPMRF_GROUP_GRAPH")) g->use_graph = e[0] == '1';
+    // DPMRF_GROUP_SPLIT=0: one hood pass after the exchange (no overlap)
+    if (const char* e = std::getenv("DPMRF_GROUP_SPLIT")) g->split = e[0] != '0';
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof u);
     NK(nccl.CommInitRank(&g->comm, world, u, rank));
