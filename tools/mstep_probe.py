@@ -4,7 +4,7 @@
     DPMRF_CUDA_LIB=build/variants/probe.so python tools/mstep_probe.py [B|D] [reps]
 
 Runs the bench's config (fixed work), then reads the %globaltimer stamps the
-probe build writes (engine.cu PROBE_*) for the LAST EM iteration's sum-pass
+probe build writes (mstep.cu PROBE_*) for the LAST EM iteration's sum-pass
 (k=0) and sq-pass (k=1) folds: per block entry / after pdl_wait / staged /
 chain done, and the ticket block's ticket / trees / end.  Prints times in us
 relative to the sum pass's first block entry."""
