@@ -112,6 +112,8 @@ struct MStepBuffers {
   DevBuf<uint32_t> chunk_sum;    // per-1024-tile-chunk label counts (large graphs)
   DevBuf<uint32_t> err;
   DevBuf<double> em_scratch;
+  DevBuf<double> roots;          // chunk roots of the sum | sq passes (many-leaf graphs)
+  DevBuf<uint32_t> tickets;      // per-chunk leaf tickets of both passes
   bool cluster_sq = true;  // small graphs: sq pass + EM tail as one cluster (DPMRF_CLUSTER_SQ=0: off)
 };
 

@@ -657,7 +657,24 @@ struct FoldArgs {
   EmEpilogueArgs ep;
   int merged;
   uint32_t root_cap;       // shared chunk-root slots of the sq pass (>= all series' chunks)
+  // Many-leaf graphs: chunk roots folded by the passes themselves (nullptr:
+  // the trees read the leaf partials).  A chunk is an aligned run of 1024
+  // leaves of one series; its root is exactly the level-10 node of the
+  // series' tree (fold_trees.cuh), so a series' root is the tree over its
+  // chunk roots.
+  double* roots_sum;       // chunk roots of the sum pass (all series)
+  double* roots_sq;        // chunk roots of the sq pass (label series)
+  uint32_t* tickets;       // per chunk: leaves folded so far (sum | sq halves; self re-arming)
 };
+
+constexpr uint32_t kMaxChunks = 8192;  // chunk tickets per pass
+
+// first chunk of series s: the chunks of the series before it
+__device__ __forceinline__ uint32_t chunk_base(const uint32_t* leaf_start, uint32_t s) {
+  uint32_t b = 0;
+  for (uint32_t i = 0; i < s; ++i) b += (leaf_start[i + 1] - leaf_start[i] + kFoldLeaf - 1) / kFoldLeaf;
+  return b;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -765,6 +782,45 @@ __device__ __forceinline__ double fold_fetched(const double* row, uint32_t off, 
     acc = fold_span<kSq>(v, first_end, len, acc, mu);
   }
   return acc;
+}
+
+// Called by one whole warp after its lanes wrote their leaf partials (lane
+// holds `leaf` when valid): count the leaves into their chunks; the warp
+// whose leaves complete a chunk folds that chunk's root (the tree over its
+// <= 1024 partials, read through L2) and re-arms the chunk's ticket.
+__device__ void chunk_tickets(const uint32_t* leaf_start, uint32_t nseries, uint32_t leaf,
+                              bool valid, const double* parts, double* roots, uint32_t* tickets,
+                              double* q) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t gch = 0xFFFFFFFFu, base = 0, len = 0;
+  if (valid) {
+    const uint32_t sr = series_of(leaf_start, nseries, leaf);
+    const uint32_t qi = (leaf - leaf_start[sr]) / kFoldLeaf;
+    gch = chunk_base(leaf_start, sr) + qi;
+    base = leaf_start[sr] + qi * kFoldLeaf;
+    len = min(kFoldLeaf, leaf_start[sr + 1] - base);
+  }
+  __threadfence();  // (each lane's partial) before the tickets
+  const uint32_t grp = __match_any_sync(0xffffffffu, gch);
+  bool last = false;
+  if (valid && uint32_t(__ffs(grp) - 1) == lane) {
+    const uint32_t c = __popc(grp);
+    last = atomicAdd(&tickets[gch], c) + c == len;
+  }
+  uint32_t lasts = __ballot_sync(0xffffffffu, last);
+  if (lasts) __threadfence();
+  while (lasts) {
+    const int src = __ffs(lasts) - 1;
+    lasts &= lasts - 1;
+    const uint32_t g = __shfl_sync(0xffffffffu, gch, src);
+    const uint32_t b = __shfl_sync(0xffffffffu, base, src);
+    const uint32_t n = __shfl_sync(0xffffffffu, len, src);
+    const double r = warp_tree<true>(parts + b, n, q);
+    if (lane == 0) {
+      roots[g] = r;
+      tickets[g] = 0;
+    }
+  }
 }
 
 // Sum pass for few leaves (one block per SM): the warp stages its leaves with
@@ -905,27 +961,33 @@ __global__ void __launch_bounds__(32) k_fold_sum(FoldArgs a) {
   const uint32_t* label_start = a.layout + M;
   const uint32_t* leaf_start = a.layout + 2 * M + 1;
   const uint32_t leaf = blockIdx.x * kLPB + lane;
-  if (lane >= kLPB || leaf >= leaf_start[M + 1]) return;
-  const uint32_t sr = series_of(leaf_start, M + 1, leaf);
-  const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
-  const double* src;
-  uint64_t slen;
-  if (sr < M) {
-    src = a.x + label_start[sr] + b;
-    slen = n[sr];
-  } else {  // the hood-energy row of the last executed MAP iteration (optimize.cpp:64-65)
-    const int T = executed_iters(a.unconv, a.map_max, a.fixed);
-    src = a.hist + uint64_t((T - 1) % a.ring) * a.Hs + b;
-    slen = a.Hs;
+  const bool valid = lane < kLPB && leaf < leaf_start[M + 1];
+  if (valid) {
+    const uint32_t sr = series_of(leaf_start, M + 1, leaf);
+    const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
+    const double* src;
+    uint64_t slen;
+    if (sr < M) {
+      src = a.x + label_start[sr] + b;
+      slen = n[sr];
+    } else {  // the hood-energy row of the last executed MAP iteration (optimize.cpp:64-65)
+      const int T = executed_iters(a.unconv, a.map_max, a.fixed);
+      src = a.hist + uint64_t((T - 1) % a.ring) * a.Hs + b;
+      slen = a.Hs;
+    }
+    const uint64_t rem = slen - b;
+    const uint32_t len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
+    double* row = stage + lane * kFoldPitch;
+    uint32_t n0;
+    const uint32_t off = fetch_leaf(row, src, len, bar[lane], &n0);
+    PROBE_BLK_T(0, 2);
+    a.partials[leaf] = fold_fetched<false>(row, off, len, n0, bar[lane], 0.0);
+    PROBE_BLK_T(0, 3);
   }
-  const uint64_t rem = slen - b;
-  const uint32_t len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
-  double* row = stage + lane * kFoldPitch;
-  uint32_t n0;
-  const uint32_t off = fetch_leaf(row, src, len, bar[lane], &n0);
-  PROBE_BLK_T(0, 2);
-  a.partials[leaf] = fold_fetched<false>(row, off, len, n0, bar[lane], 0.0);
-  PROBE_BLK_T(0, 3);
+  if (a.roots_sum) {
+    __syncwarp();  // (the stage is free: every chain is done)
+    chunk_tickets(leaf_start, M + 1, leaf, valid, a.partials, a.roots_sum, a.tickets, stage);
+  }
 }
 
 template <int kLPB>
@@ -998,7 +1060,15 @@ __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
     bool short_series = true;
     for (uint32_t s = s_lo; s <= s_hi; ++s)
       short_series = short_series && leaf_start[s + 1] - leaf_start[s] <= kFoldLeaf;
-    if (short_series) {
+    if (a.roots_sum) {  // the sum pass folded the chunk roots: a short tree per label
+      for (uint32_t s = s_lo + warp; s <= s_hi; s += kWarps) {
+        const uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
+        if (cnt == 0) continue;
+        const double folded = warp_tree<true>(a.roots_sum + chunk_base(leaf_start, s),
+                                              (cnt + kFoldLeaf - 1) / kFoldLeaf, qw);
+        if (lane == 0) publish(s, folded);
+      }
+    } else if (short_series) {
       for (uint32_t s = s_lo + warp; s <= s_hi; s += kWarps) {
         const uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
         if (cnt == 0) continue;  // (a label without leaves is held by no block)
@@ -1038,6 +1108,9 @@ __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
     a.sq_partials[first + tid] = fold_span<false>(v, 1, len_s[tid], v[0], 0.0);
     if (tid == 0) PROBE_BLK_T(1, 3);
   }
+  if (a.roots_sq && warp == 0)
+    chunk_tickets(leaf_start, M, first + tid, tid < kLPB && len_s[tid] != 0, a.sq_partials,
+                  a.roots_sq, a.tickets + kMaxChunks, qw);
   if (a.merged && (executed_iters(a.unconv, a.map_max, a.fixed) & 1)) {
     // device-resident loop: the next EM starts from buffer 0, so an odd
     // number of MAP iterations leaves the committed labels to move back
@@ -1071,7 +1144,17 @@ __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
   PROBE_TAIL(0, 2);
   bool all_short = true;
   for (uint32_t s = 0; s < nseries; ++s) all_short = all_short && series_cnt(s) <= kFoldLeaf;
-  if (all_short) {  // one warp per series, all at once
+  if (a.roots_sum && a.roots_sq) {
+    // the passes folded every chunk root: one warp per series over its roots
+    for (uint32_t s = warp; s < nseries; s += kWarps) {
+      const uint32_t cnt = series_cnt(s);
+      const double r = cnt ? warp_tree<true>((s < M ? a.roots_sq : a.roots_sum) +
+                                                 chunk_base(leaf_start, s),
+                                             (cnt + kFoldLeaf - 1) / kFoldLeaf, qw)
+                           : 0.0;
+      if (lane == 0) root_s[s] = r;
+    }
+  } else if (all_short) {  // one warp per series, all at once
     for (uint32_t s = warp; s < nseries; s += kWarps) {
       const uint32_t cnt = series_cnt(s);
       const double r = cnt ? warp_tree<true>(series_ptr(s), cnt, qw) : 0.0;
@@ -1513,10 +1596,10 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
                             ((Hs + kFoldLeaf - 1) / kFoldLeaf + kFoldLeaf - 1) / kFoldLeaf + 1;
     if (chunks > 8192) fail(DPMRF_INVALID_ARGUMENT, "M-step: series too long for the fold trees");
     const uint32_t root_cap = static_cast<uint32_t>((chunks + 31) / 32 * 32);
-    const FoldArgs fa{x,       layout,        M,     hist,      Hs,
-                      ring,    unconv,        map_max, fixed,   params,
-                      partials, mb.sq_partials.get(), em_out, mb.done.get() + 1, epv,
-                      ep ? 1 : 0, root_cap};
+    FoldArgs fa{x,       layout,        M,     hist,      Hs,
+                ring,    unconv,        map_max, fixed,   params,
+                partials, mb.sq_partials.get(), em_out, mb.done.get() + 1, epv,
+                ep ? 1 : 0, root_cap, nullptr, nullptr, nullptr};
     const uint64_t hood_leaves = (Hs + kFoldLeaf - 1) / kFoldLeaf;
     if (few && mb.cluster_sq && label_leaves <= uint64_t(kClCtas) * kClMaxPer &&
         hood_leaves <= kFoldLeaf) {
@@ -1542,6 +1625,13 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
       launch_pdl(k_fold_sq<kQ>, dim3(grid_for(label_leaves, kQ)), dim3(kSqThreads), sq, s, fa);
     } else {
       constexpr int kS = 8, kQ = 4;
+      // chunk roots folded by the passes (series of <= 1024 chunks)
+      if (label_leaves <= uint64_t(kFoldLeaf) * kFoldLeaf && hood_leaves <= uint64_t(kFoldLeaf) * kFoldLeaf &&
+          chunks <= kMaxChunks) {
+        fa.roots_sum = mb.roots.get();
+        fa.roots_sq = mb.roots.get() + kMaxChunks;
+        fa.tickets = mb.tickets.get();
+      }
       const size_t ss = size_t(kS) * kFoldPitch * sizeof(double);
       const size_t sq = (size_t(kQ) * kFoldPitch + root_cap + (kSqThreads / 32) * kTreeScratch) *
                         sizeof(double);
@@ -1687,6 +1777,12 @@ void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs) {
     CK(cudaMalloc(reinterpret_cast<void**>(&mb.done.p), 2 * sizeof(uint32_t)));
     mb.done.cap = 2;
     CK(cudaMemset(mb.done.p, 0, 2 * sizeof(uint32_t)));  // tickets re-arm themselves after
+  }
+  if (!mb.tickets.get()) {  // chunk tickets of both passes (zero; re-armed by their folders)
+    CK(cudaMalloc(reinterpret_cast<void**>(&mb.tickets.p), 2 * kMaxChunks * sizeof(uint32_t)));
+    mb.tickets.cap = 2 * kMaxChunks;
+    CK(cudaMemset(mb.tickets.p, 0, 2 * kMaxChunks * sizeof(uint32_t)));
+    mb.roots.ensure(2 * kMaxChunks);
   }
 }
 
