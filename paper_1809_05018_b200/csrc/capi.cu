@@ -173,6 +173,7 @@ extern "C" dpmrf_status dpmrf_context_create(int device, dpmrf_context** out) {
     if (const char* e = std::getenv("DPMRF_NO_K12")) c->use_k12 = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_UNFUSED")) c->use_fused = e[0] == '0';
     if (const char* e = std::getenv("DPMRF_CLUSTER_SQ")) c->ms.cluster_sq = e[0] != '0';
+    if (const char* e = std::getenv("DPMRF_STREAM")) c->ms.stream = e[0] != '0';
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));

@@ -114,6 +114,8 @@ struct MStepBuffers {
   DevBuf<double> em_scratch;
   DevBuf<double> roots;          // chunk roots of the sum | sq passes (many-leaf graphs)
   DevBuf<uint32_t> tickets;      // per-chunk leaf tickets of both passes
+  DevBuf<uint32_t> stream_cnt;   // k_mstep_stream's grid barrier / series / block counters
+  bool stream = true;            // many-leaf graphs: one persistent streaming fold (DPMRF_STREAM=0: two passes)
   bool cluster_sq = true;  // small graphs: sq pass + EM tail as one cluster (DPMRF_CLUSTER_SQ=0: off)
 };
 

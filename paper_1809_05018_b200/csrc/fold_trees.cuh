@@ -105,6 +105,15 @@ __device__ __forceinline__ double warp_tree512(const double* p, uint32_t cnt) {
   return warp_tree_regs<16, kGlobal>(p, cnt);
 }
 
+// warp_tree for cnt <= 1024 without scratch: the two aligned 512-halves are
+// the level-9 nodes, paired at level 10 when both exist.
+template <bool kGlobal>
+__device__ __forceinline__ double warp_tree1024(const double* p, uint32_t cnt) {
+  if (cnt <= 512) return warp_tree512<kGlobal>(p, cnt);
+  const double lo = warp_tree512<kGlobal>(p, 512);
+  return __dadd_rn(lo, warp_tree512<kGlobal>(p + 512, cnt - 512));
+}
+
 // The whole series' tree by the block: aligned 1024-partial chunks (a
 // chunk's root is exactly the level-10 node of the series' tree) by the
 // warps in parallel, roots in shared memory, then the tree over the roots

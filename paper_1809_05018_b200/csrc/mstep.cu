@@ -787,14 +787,21 @@ __device__ __forceinline__ double fold_fetched(const double* row, uint32_t off, 
 // Called by one whole warp after its lanes wrote their leaf partials (lane
 // holds `leaf` when valid): count the leaves into their chunks; the warp
 // whose leaves complete a chunk folds that chunk's root (the tree over its
-// <= 1024 partials, read through L2) and re-arms the chunk's ticket.
+// <= 1024 partials, read through L2) and re-arms the chunk's ticket.  With
+// series counters (sc), the warp completing a series' last chunk also folds
+// the series root (the tree over its chunk roots) and hands it to
+// on_series(s, root) on lane 0.
+struct NoSeries {
+  __device__ void operator()(uint32_t, double) const {}
+};
+template <class F = NoSeries>
 __device__ void chunk_tickets(const uint32_t* leaf_start, uint32_t nseries, uint32_t leaf,
                               bool valid, const double* parts, double* roots, uint32_t* tickets,
-                              double* q) {
+                              double* q, uint32_t* sc = nullptr, F on_series = F{}) {
   const uint32_t lane = threadIdx.x & 31;
-  uint32_t gch = 0xFFFFFFFFu, base = 0, len = 0;
+  uint32_t gch = 0xFFFFFFFFu, base = 0, len = 0, sr = 0;
   if (valid) {
-    const uint32_t sr = series_of(leaf_start, nseries, leaf);
+    sr = series_of(leaf_start, nseries, leaf);
     const uint32_t qi = (leaf - leaf_start[sr]) / kFoldLeaf;
     gch = chunk_base(leaf_start, sr) + qi;
     base = leaf_start[sr] + qi * kFoldLeaf;
@@ -815,10 +822,27 @@ __device__ void chunk_tickets(const uint32_t* leaf_start, uint32_t nseries, uint
     const uint32_t g = __shfl_sync(0xffffffffu, gch, src);
     const uint32_t b = __shfl_sync(0xffffffffu, base, src);
     const uint32_t n = __shfl_sync(0xffffffffu, len, src);
-    const double r = warp_tree<true>(parts + b, n, q);
+    const uint32_t s = __shfl_sync(0xffffffffu, sr, src);
+    const double r = q ? warp_tree<true>(parts + b, n, q) : warp_tree1024<true>(parts + b, n);
+    uint32_t series_done = 0;
     if (lane == 0) {
       roots[g] = r;
       tickets[g] = 0;
+      if (sc) {
+        __threadfence();
+        const uint32_t nch = (leaf_start[s + 1] - leaf_start[s] + kFoldLeaf - 1) / kFoldLeaf;
+        series_done = atomicAdd(&sc[s], 1u) + 1 == nch;
+      }
+    }
+    if (__shfl_sync(0xffffffffu, series_done, 0)) {
+      __threadfence();
+      const uint32_t nch = (leaf_start[s + 1] - leaf_start[s] + kFoldLeaf - 1) / kFoldLeaf;
+      const double root = q ? warp_tree<true>(roots + chunk_base(leaf_start, s), nch, q)
+                            : warp_tree1024<true>(roots + chunk_base(leaf_start, s), nch);
+      if (lane == 0) {
+        on_series(s, root);
+        sc[s] = 0;
+      }
     }
   }
 }
@@ -1421,6 +1445,262 @@ __global__ void __launch_bounds__(kClThreads) k_fold_sq_cluster(FoldArgs a, uint
 }
 
 // ---------------------------------------------------------------------------
+// k_mstep_stream: both M-step passes of many-leaf graphs (16384^2: ~16 000
+// sum-pass leaves) as ONE persistent kernel.  Lane j < C of a one-warp block
+// is a chain that walks the leaves gid, gid + G*C, ... (gid = block*C + j);
+// each leaf streams through the lane's ring of NS shared-memory slots in
+// 256-double quarters (one cp.async.bulk + one mbarrier per slot), the next
+// quarters in flight while the chain folds the current one, so every SM
+// keeps ~30 chains busy instead of running whole-leaf waves.  After each
+// round the warp counts its leaves into their chunks (chunk_tickets): the
+// warp completing a chunk folds its root, the warp completing a series folds
+// the series root and publishes mu (sum pass), sigma (sq pass) or the total
+// energy.  Between the passes every block waits at a grid barrier (the grid
+// is sized by occupancy, so all blocks are resident), then folds (x - mu)^2
+// (engine.cpp:213-217) -- x read again, largely from L2.  The last block
+// (ticket) completes the EM output and record.
+// ---------------------------------------------------------------------------
+#ifndef DPMRF_STREAM_C
+#define DPMRF_STREAM_C 16
+#endif
+#ifndef DPMRF_STREAM_NS
+#define DPMRF_STREAM_NS 3
+#endif
+#ifndef DPMRF_STREAM_W
+#define DPMRF_STREAM_W 1
+#endif
+constexpr int kStreamChains = DPMRF_STREAM_C;  // chains (lanes) per warp
+constexpr int kStreamWarps = DPMRF_STREAM_W;   // warps per block (independent rings)
+
+constexpr int kStreamSlots = DPMRF_STREAM_NS;  // ring slots per chain
+constexpr uint32_t kQuarter = 256;
+constexpr uint32_t kSlotPitch = kQuarter + 2;  // doubles per slot (16-byte aligned superset)
+
+struct StreamCounters {  // zeroed once; re-armed by the kernel itself
+  uint32_t gen;     // launches completed (the ready flags of launch g read g + 1)
+  uint32_t done;    // blocks finished
+  uint32_t ready[kMaxLabels];             // per label: mu published (== gen + 1)
+  uint32_t series[2 * (kMaxLabels + 1)];  // chunks completed per series (sum | sq)
+};
+
+__device__ __forceinline__ void mbar_wait_par(uint64_t* bar, uint32_t par) {
+  uint32_t ok = 0, spins = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(par)
+        : "memory");
+    if (!ok && ++spins > (1u << 26)) __trap();  // a lost copy: fail loudly, never hang
+  }
+}
+
+struct StreamView {
+  const uint32_t* n;
+  const uint32_t* label_start;
+  const uint32_t* leaf_start;
+  const double* x;
+  const double* hood_row;
+  uint64_t Hs;
+  uint32_t M;
+  // leaf -> [src, src + len) of its series, and the series
+  __device__ __forceinline__ uint32_t span(bool sq, uint32_t leaf, const double*& src,
+                                           uint32_t& len) const {
+    const uint32_t sr = series_of(leaf_start, sq ? M : M + 1, leaf);
+    const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
+    const uint64_t slen = sr < M ? n[sr] : Hs;
+    src = (sr < M ? x + label_start[sr] : hood_row) + b;
+    const uint64_t rem = slen - b;
+    len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
+    return sr;
+  }
+};
+
+// One task stream per chain: tasks 0..nsum-1 are the sum-pass leaves (label
+// series, then the hood-energy series), tasks nsum.. the sq-pass leaves;
+// chain c takes tasks c, c + S, c + 2S, ... (S chains in the grid), so every
+// chain folds the same number of leaves (+-1) and no grid barrier separates
+// the passes: an sq task first waits for its label's mu flag (published by
+// the warp completing that label's sum series -- long done by then, the
+// label leaves come first).
+template <int C, int W, int NS>
+__device__ void stream_tasks(const FoldArgs& a, const StreamView& v, double* ring,
+                             uint64_t* bars, StreamCounters* cnt, uint32_t gen) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t M = a.M;
+  const uint32_t stride = gridDim.x * W * C;
+  // sq tasks start at P: after every sum task, and in a later round than
+  // every label leaf, so no round of any warp both folds a label leaf and
+  // waits for a mu (a warp never waits on its own round: deadlock-free)
+  const uint32_t nsum = v.leaf_start[M + 1], nlab = v.leaf_start[M];
+  const uint32_t P = max(nsum, (nlab + stride - 1) / stride * stride);
+  const uint32_t ntask = P + nlab;
+  const uint32_t g0 = (blockIdx.x * W + warp) * C;
+  const uint32_t gid = g0 + lane;
+  const uint32_t rounds = ntask > g0 ? (ntask - g0 + stride - 1) / stride : 0u;
+  uint32_t ph = 0;  // this chain's slot parities
+  // task -> fetched span
+  auto task_span = [&](uint32_t t, const double*& src, uint32_t& len) -> uint32_t {
+    return t < nsum ? v.span(false, t, src, len) : v.span(true, t - P, src, len);
+  };
+  auto issue = [&](uint32_t pos) {
+    if (lane >= uint32_t(C)) return;
+    const uint32_t k = pos >> 2, qq = pos & 3u;
+    if (k >= rounds) return;
+    const uint32_t t = gid + k * stride;
+    if (t >= ntask || (t >= nsum && t < P)) return;
+    const double* src;
+    uint32_t len;
+    task_span(t, src, len);
+    if (qq * kQuarter >= len) return;
+    const double* s0 = src + qq * kQuarter;
+    const uint32_t n = min(kQuarter, len - qq * kQuarter);
+    const uint32_t off = (reinterpret_cast<uintptr_t>(s0) & 15u) ? 1u : 0u;
+    const uint32_t nd = (off + n + 1u) & ~1u;
+    uint64_t* b = bars + (pos % NS);
+    mbar_expect(b, nd * 8u);
+    bulk_g2s(ring + (pos % NS) * kSlotPitch, s0 - off, nd * 8u, b);
+  };
+  for (uint32_t p = 0; p < uint32_t(NS); ++p) issue(p);
+  for (uint32_t k = 0; k < rounds; ++k) {
+    const uint32_t t = gid + k * stride;
+    const bool has = lane < uint32_t(C) && t < ntask && (t < nsum || t >= P);
+    const bool sq = t >= P;
+    double acc = 0.0, mu = 0.0;
+    const double* src = nullptr;
+    uint32_t len = 0;
+    if (has) {
+      const uint32_t sr = task_span(t, src, len);
+      if (sq) {  // this label's mu (engine.cpp:207-208) must be published
+        uint32_t seen = 0, spins = 0;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(seen) : "l"(&cnt->ready[sr]) : "memory");
+          if (seen == gen + 1) break;
+          __nanosleep(128);
+          if (++spins > (1u << 26)) __trap();
+        }
+        mu = __ldcg(a.params + sr);
+      }
+    }
+#pragma unroll 1
+    for (uint32_t qq = 0; qq < 4; ++qq) {
+      const uint32_t pos = 4 * k + qq;
+      if (has && qq * kQuarter < len) {
+        const uint32_t slot = pos % NS;
+        mbar_wait_par(bars + slot, (ph >> slot) & 1u);
+        ph ^= 1u << slot;
+        const double* s0 = src + qq * kQuarter;
+        const uint32_t n = min(kQuarter, len - qq * kQuarter);
+        const double* w =
+            ring + slot * kSlotPitch + ((reinterpret_cast<uintptr_t>(s0) & 15u) ? 1 : 0);
+        if (sq) {
+          if (qq == 0) {
+            const double d = __dsub_rn(w[0], mu);
+            acc = fold_span<true>(w, 1, n, __dmul_rn(d, d), mu);
+          } else {
+            acc = fold_span<true>(w, 0, n, acc, mu);
+          }
+        } else {
+          acc = fold_span<false>(w, qq == 0 ? 1 : 0, n, qq == 0 ? w[0] : acc, 0.0);
+        }
+      }
+      // the slot is free again: refill it with the quarter NS positions ahead
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(pos + NS);
+    }
+    if (has) {
+      if (sq) a.sq_partials[t - P] = acc;
+      else a.partials[t] = acc;
+    }
+    __syncwarp();
+    // chunk / series tickets of this round's sum leaves, then its sq leaves
+    if (__any_sync(0xffffffffu, has && !sq))
+      chunk_tickets(v.leaf_start, M + 1, t, has && !sq, a.partials, a.roots_sum, a.tickets,
+                    nullptr, cnt->series, [&](uint32_t s, double root) {
+                      if (s < M) {
+                        a.params[s] = __ddiv_rn(root, static_cast<double>(v.n[s]));
+                        __threadfence();
+                        asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&cnt->ready[s]),
+                                     "r"(gen + 1)
+                                     : "memory");
+                      } else {
+                        a.em_out[0] = root;  // total energy (optimize.cpp:64-65)
+                      }
+                    });
+    if (__any_sync(0xffffffffu, has && sq))
+      chunk_tickets(v.leaf_start, M, t - P, has && sq, a.sq_partials, a.roots_sq,
+                    a.tickets + kMaxChunks, nullptr, cnt->series + (kMaxLabels + 1),
+                    [&](uint32_t s, double root) {
+                      const double sd = __dsqrt_rn(__ddiv_rn(root, static_cast<double>(v.n[s])));
+                      a.params[M + s] = sd < kSigmaFloor ? kSigmaFloor : sd;
+                    });
+  }
+}
+
+template <int C, int W, int NS>
+__global__ void __launch_bounds__(32 * W) k_mstep_stream(FoldArgs a, StreamCounters* cnt) {
+  extern __shared__ __align__(16) double sm[];  // W x C x NS x kSlotPitch
+  __shared__ __align__(8) uint64_t bar[W * C][NS];
+  __shared__ uint32_t lay[4 * kMaxLabels + 4];
+  __shared__ uint32_t last;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (lane < uint32_t(C))
+    for (int k = 0; k < NS; ++k) mbar_init1(&bar[warp * C + lane][k]);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  PROBE_BLK(0, 0);
+  pdl_wait();
+  PROBE_BLK(0, 1);
+  if (em_skipped(a.unconv)) return;
+  const uint32_t M = a.M;
+  for (uint32_t i = tid; i < 4 * M + 4; i += 32 * W) lay[i] = a.layout[i];
+  const uint32_t gen = cnt->gen;  // (advanced by the previous launch's last block)
+  __syncthreads();
+  const int T = a.unconv ? executed_iters(a.unconv, a.map_max, a.fixed) : 0;
+  StreamView v{lay, lay + M, lay + 2 * M + 1, a.x,
+               a.hist && T > 0 ? a.hist + uint64_t((T - 1) % a.ring) * a.Hs : nullptr, a.Hs, M};
+  const uint32_t chain = warp * C + (lane < uint32_t(C) ? lane : 0u);
+  stream_tasks<C, W, NS>(a, v, sm + chain * NS * kSlotPitch, &bar[chain][0], cnt, gen);
+  PROBE_BLK(0, 4);
+  if (a.merged && (T & 1)) {
+    // device-resident loop: the next EM starts from buffer 0, so an odd
+    // number of MAP iterations moves the committed labels back
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint64_t words = a.ep.R / 4;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.ep.lab1);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(a.ep.lab0);
+    const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + tid;
+    for (uint64_t w = g; w < words; w += stride) dst[w] = src[w];
+    for (uint64_t x = words * 4 + g; x < a.ep.R; x += stride) a.ep.lab0[x] = a.ep.lab1[x];
+  }
+  // ---- last block: the EM output [total, T, mu, sigma] and record ----
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    last = atomicAdd(&cnt->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || warp != 0) return;
+  __threadfence();
+  PROBE_TAIL(0, 0);
+  if (lane == 0) {
+    // dpp::reduce(..., 0.0): identity only for empty input
+    if (v.leaf_start[M + 1] == v.leaf_start[M]) a.em_out[0] = 0.0;
+    a.em_out[1] = static_cast<double>(T);
+    cnt->done = 0;
+    cnt->gen = gen + 1;  // (this launch's ready flags read gen + 1)
+  }
+  // (labels without vertices keep their previous parameters, engine.cpp:209-220)
+  for (uint32_t s = lane; s < M; s += 32) {
+    a.em_out[2 + s] = __ldcg(a.params + s);
+    a.em_out[2 + M + s] = __ldcg(a.params + M + s);
+  }
+  __syncwarp();
+  if (a.merged) em_record(a.ep, true);
+  PROBE_TAIL(0, 1);
+}
+
+// ---------------------------------------------------------------------------
 // Device-resident EM loop (no host round trip between EM iterations).
 // k_em_prologue arms the MAP counters and folds the previous epilogue's stop
 // decision into the state (so every kernel of this EM sees one value);
@@ -1623,6 +1903,27 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
       ensure_dynamic_smem(k_fold_sq<kQ>, sq);
       launch_pdl(k_fold_sum_ldg<kS>, dim3(grid_for(max_leaves, kS)), dim3(32), ss, s, fa);
       launch_pdl(k_fold_sq<kQ>, dim3(grid_for(label_leaves, kQ)), dim3(kSqThreads), sq, s, fa);
+    } else if (mb.stream && label_leaves <= uint64_t(kFoldLeaf) * kFoldLeaf &&
+               hood_leaves <= uint64_t(kFoldLeaf) * kFoldLeaf && chunks <= kMaxChunks) {
+      // both passes + the EM tail in one persistent streaming kernel
+      fa.roots_sum = mb.roots.get();
+      fa.roots_sq = mb.roots.get() + kMaxChunks;
+      fa.tickets = mb.tickets.get();
+      constexpr int kC = kStreamChains, kW = kStreamWarps, kNS = kStreamSlots;
+      const size_t sm = size_t(kW) * kC * kNS * kSlotPitch * sizeof(double);
+      ensure_dynamic_smem(k_mstep_stream<kC, kW, kNS>, sm);
+      static int per_sm[64] = {0};  // resident blocks per SM, per device
+      int dev = 0;
+      CK(cudaGetDevice(&dev));
+      if (!per_sm[dev & 63])
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev & 63],
+                                                         k_mstep_stream<kC, kW, kNS>, 32 * kW, sm));
+      const uint64_t need = (max_leaves + label_leaves + kC * kW - 1) / (kC * kW);
+      const unsigned grid = static_cast<unsigned>(
+          std::max<uint64_t>(1, std::min<uint64_t>(need, uint64_t(per_sm[dev & 63]) * kNumSMs)));
+      launch_pdl(k_mstep_stream<kC, kW, kNS>, dim3(grid), dim3(32 * kW), sm, s, fa,
+                 reinterpret_cast<StreamCounters*>(mb.stream_cnt.get()));
+      n -= 1;  // (one launch for both passes)
     } else {
       constexpr int kS = 8, kQ = 4;
       // chunk roots folded by the passes (series of <= 1024 chunks)
@@ -1783,6 +2084,12 @@ void mstep_reserve(MStepBuffers& mb, uint32_t R, uint32_t M, uint64_t Hs) {
     mb.tickets.cap = 2 * kMaxChunks;
     CK(cudaMemset(mb.tickets.p, 0, 2 * kMaxChunks * sizeof(uint32_t)));
     mb.roots.ensure(2 * kMaxChunks);
+  }
+  if (!mb.stream_cnt.get()) {
+    const size_t words = (sizeof(StreamCounters) + 3) / 4;
+    CK(cudaMalloc(reinterpret_cast<void**>(&mb.stream_cnt.p), words * sizeof(uint32_t)));
+    mb.stream_cnt.cap = words;
+    CK(cudaMemset(mb.stream_cnt.p, 0, words * sizeof(uint32_t)));
   }
 }
 

@@ -347,3 +347,31 @@ def test_opt_in_layouts_agree(env, val, monkeypatch):
     finally:
         c.close()
         base.close()
+
+
+@pytest.mark.parametrize("size,brick,M", [(4096, False, 2), (4096, True, 3)])
+def test_stream_fold_matches_two_pass(size, brick, M, monkeypatch):
+    """Many-leaf graphs (> 4 x 148 leaves): the persistent streaming M-step
+    (k_mstep_stream: quarter-leaf ring per chain, chunk/series tickets, grid
+    barrier between the passes, label move-back on odd MAP counts) equals the
+    two-pass folds (DPMRF_STREAM=0) bit for bit, with and without early exits,
+    over the EM trace."""
+    from paper_1809_05018_b200 import inputs
+    monkeypatch.setenv("DPMRF_STREAM", "0")
+    two = E.Context(0)
+    monkeypatch.delenv("DPMRF_STREAM")
+    one = E.Context(0)
+    try:
+        sl = inputs.synthetic_slice(size, 8, seed=21, brick=brick)
+        for c in (one, two):
+            c.set_graph(sl.graph)
+            c.build_neighborhoods(sl.cliques)
+        for fixed in (False, True):
+            cfg = E.OptimizerConfig(num_labels=M, em_max_iters=7, rng_seed=21)
+            got = one.optimize(cfg, fixed_work=fixed, multilabel=M != 2, trace_level=E.TRACE_EM)
+            want = two.optimize(cfg, fixed_work=fixed, multilabel=M != 2, trace_level=E.TRACE_EM)
+            same(got, want, full=False)
+            assert got.stats["kernel_launches"] < want.stats["kernel_launches"]
+    finally:
+        one.close()
+        two.close()
