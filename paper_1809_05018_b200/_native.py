@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as ct
 import os
+import sys
 
 import numpy as np
 
@@ -148,9 +149,24 @@ def _load(path, api):
     return lib
 
 
+def _prefer_bundled_nccl():
+    """The NCCL transport dlopens libnccl.so.2 on first use.  In a Python
+    process that also uses PyTorch, load the NCCL wheel torch links against
+    (nvidia/nccl/lib): a libnccl.so.2 loaded first from the system path would
+    be reused for torch's own dependency and lacks symbols torch needs."""
+    if os.environ.get("DPMRF_NCCL_LIB"):
+        return
+    for base in sys.path:
+        cand = os.path.join(base, "nvidia", "nccl", "lib", "libnccl.so.2")
+        if base and os.path.exists(cand):
+            os.environ["DPMRF_NCCL_LIB"] = cand
+            return
+
+
 def cuda():
     global _cuda
     if _cuda is None:
+        _prefer_bundled_nccl()
         _cuda = _load(CUDA_LIB, CUDA_API)
     return _cuda
 

@@ -129,16 +129,9 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
                   MStepBuffers& mb, cudaStream_t s, uint64_t* launches,
                   bool counts_ready = true, bool scattered = false,
                   const EmEpilogueArgs* ep = nullptr, const double* hood_parts = nullptr);
-// Partitioned optimize, distributed M-step folds: the label grouping (every
-// rank), this rank's label-series leaves [lo, hi) of one pass (no trees), the
-// trees in one block over allgathered partials (+ hood-series partials).
-void launch_mstep_scatter(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab,
-                          const uint32_t* unconv, int map_max, int fixed, uint64_t Hs,
-                          double* params, double* em_out, MStepBuffers& mb, cudaStream_t s,
-                          uint64_t* launches);
-void launch_leaf_range(bool sq, uint32_t M, uint64_t Hs, const uint32_t* unconv, int map_max,
-                       int fixed, double* params, double* em_out, MStepBuffers& mb, uint32_t lo,
-                       uint32_t hi, cudaStream_t s);
+// Partitioned optimize (distributed M-step, partition.cu): the pairwise trees
+// in one block over the gathered label-series partials (mb.partials, global
+// leaf order) and the hood-series partials.
 void launch_fold_trees(bool sq, uint32_t M, uint64_t Hs, const uint32_t* unconv, int map_max,
                        int fixed, double* params, double* em_out, MStepBuffers& mb,
                        const double* hood_parts, cudaStream_t s);
@@ -153,12 +146,6 @@ void launch_row_leaves(const double* hist, int ring, uint64_t Hs, const uint32_t
 
 void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s);
 void launch_em_epilogue(const EmEpilogueArgs& a, cudaStream_t s);
-// Partitioned optimize: own vertex / series range of the final labels and of
-// the last executed hood-energy row into the allgather buffers.
-void launch_partition_select(const uint8_t* lab_even, const uint8_t* lab_odd, const double* hist,
-                             int ring, uint64_t Hs, const uint32_t* unconv, int map_max, int fixed,
-                             uint32_t vb, uint32_t ve, uint64_t hb, uint64_t he,
-                             uint8_t* lab_full, double* row_full, cudaStream_t s);
 // log_cr over n values (diagnostics / tests of the device log).
 void launch_log_cr(const double* x, double* out, uint64_t n, cudaStream_t s);
 // Builds the per-device table of the EM loop's device log once (blocking).

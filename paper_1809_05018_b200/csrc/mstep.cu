@@ -44,9 +44,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 //   update_parameters  engine.cpp:193-223 (sort_by_key stable, reduce_by_key
 //                      fold_range per run, kernels.hpp:226-253)
 //   dpp::reduce        kernels.hpp:124-139 (total energy, optimize.cpp:64-65)
-// Launches per EM iteration: k_tile_offsets, k_label_tiles (stable scatter),
-// k_leaf_fold<sum> and k_leaf_fold<sq>, each leaf kernel finishing with the
-// pairwise tree in its last block.  The per-tile label counts come from the
+// Launches per EM iteration: the grouping (k_label_scatter_small, or
+// k_tile_chunks / k_tile_offsets / k_label_tiles on large graphs), then the
+// folds: k_fold_sum_ldg + k_fold_sq_cluster (few leaves), k_mstep_stream
+// (many leaves), each finishing with the pairwise trees.  The per-tile label counts come from the
 // last executed vertex pass (double-buffered by iteration parity).
 // ---------------------------------------------------------------------------
 // Stable rank of each vertex among the tile's vertices of the same label:
@@ -195,18 +196,11 @@ __device__ __forceinline__ uint32_t series_of(const uint32_t* leaf_start, uint32
 
 // Leaf folds (fold_leaf, kernels.hpp:37-42): each 1024-element leaf is a
 // strictly sequential left fold seeded by its first element -- the chain of
-// dependent adds cannot be reassociated without changing bits.  A block of
-// 256 threads stages kLeavesPerBlock leaves into shared memory with all its
-// loads in flight at once, then one lane per leaf runs the dependent chain
-// out of shared memory (rows padded to 1025 doubles: distinct banks).
-// kSq folds (x - mu)^2 (engine.cpp:213-217).  Series M (sum pass only) is
-// the hood-energy row of the last executed MAP iteration (the EM total
-// energy, optimize.cpp:64-65), located from the device counters.
-// The LAST block to finish (atomic ticket after a fence) combines every
-// series' leaf partials with the pairwise tree of kernels.hpp:45-51 --
-// bottom-up adjacent pairing == the split at bit_floor(n-1) -- and writes
-// mu (sum pass) / sigma and the published parameters (sq pass) and the
-// total energy.
+// dependent adds cannot be reassociated without changing bits.  Leaf
+// partials combine with the pairwise tree of kernels.hpp:45-51 (bottom-up
+// adjacent pairing == the split at bit_floor(n-1), fold_trees.cuh).
+// kLeavesPerBlock: leaves per block of k_row_leaves (the partitioned run's
+// hood-series leaves, staged by the whole block, one chain per leaf).
 #ifndef DPMRF_LEAVES_PER_BLOCK
 #define DPMRF_LEAVES_PER_BLOCK 8
 #endif
@@ -292,188 +286,35 @@ __device__ void em_record(const EmEpilogueArgs& a, bool merged, const EmPrefetch
     for (int t = 0; t < a.map_max; ++t) a.unconv[t] = 0;
 }
 
-template <bool kSq, int kLPB = kLeavesPerBlock>
+// Trees only (the partitioned run): every rank folded its own leaves and the
+// partials were gathered into `partials` (label series, global leaf order)
+// and hood_parts (the hood-energy series); one block runs the pairwise trees
+// of kernels.hpp:45-51 (block_series_tree) and publishes mu (sum pass) or
+// sigma and the EM output (sq pass), exactly as the one-device M-step.
+template <bool kSq>
 __global__ void __launch_bounds__(256)
-    k_leaf_fold(const double* __restrict__ x, const uint32_t* __restrict__ layout, uint32_t M,
-                const double* __restrict__ hist, uint64_t Hs, int ring,
-                const uint32_t* __restrict__ unconv, int map_max, int fixed, double* params,
-                double* partials, double* em_out, uint32_t* done, EmEpilogueArgs ep,
-                int merged, const double* __restrict__ hood_parts, uint32_t leaf_lo,
-                uint32_t leaf_hi, int tail_mode) {
-  // tail_mode 0: fold [leaf_lo, leaf_hi) of every series, the last block
-  //              (ticket) runs the trees and the parameter update;
-  //           1: fold this rank's [leaf_lo, leaf_hi) of the label series only,
-  //              no trees (partitioned run: the partials are allgathered);
-  //           2: one block, trees only, over allgathered label partials and
-  //              the hood-series partials in hood_parts.
-  extern __shared__ double stage[];  // kLPB x kLeafStride
-  PROBE_BLK(kSq, 0);
+    k_fold_trees(const uint32_t* __restrict__ layout, uint32_t M,
+                 const uint32_t* __restrict__ unconv, int map_max, int fixed, double* params,
+                 const double* __restrict__ partials, const double* __restrict__ hood_parts,
+                 double* em_out) {
+  extern __shared__ double scratch[];  // roots (root_cap) | 8 warps x kTreeScratch
+  __shared__ uint32_t lay[4 * kMaxLabels + 4];
   pdl_wait();
-  PROBE_BLK(kSq, 1);
-  const uint32_t* n = layout;
-  const uint32_t* label_start = layout + M;
-  const uint32_t* leaf_start = layout + 2 * M + 1;
-  const uint32_t nseries = kSq ? M : M + 1;
-  const uint32_t all_end = leaf_start[tail_mode == 1 ? M : nseries];  // (beside the skip flag)
-  if (em_skipped(unconv)) return;  // uniform: no block takes a ticket
-  const uint32_t total = tail_mode == 2 ? 0u : min(all_end, leaf_hi);
-  const uint32_t first = leaf_lo + blockIdx.x * kLPB;
-  if (first < total) {
-    const double* hood_row = nullptr;
-    if (!kSq && unconv && !hood_parts) {
-      const int T = executed_iters(unconv, map_max, fixed);
-      hood_row = hist + uint64_t((T - 1) % ring) * Hs;
-    }
-    __shared__ const double* src_s[kLPB];
-    __shared__ uint32_t len_s[kLPB];
-    __shared__ double mu_s[kLPB];
-    if (threadIdx.x < kLPB) {
-      const uint32_t leaf = first + threadIdx.x;
-      uint32_t len = 0;
-      const double* src = nullptr;
-      double mu = 0.0;
-      if (leaf < total) {
-        const uint32_t sr = series_of(leaf_start, nseries, leaf);
-        if (!kSq && sr == M && hood_parts) {
-          // partitioned run: each rank folded its own hood-series leaves
-          partials[leaf] = hood_parts[leaf - leaf_start[M]];
-        } else {
-          const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
-          const uint64_t slen = sr < M ? n[sr] : Hs;
-          src = (sr < M ? x + label_start[sr] : hood_row) + b;
-          const uint64_t rem = slen - b;
-          len = static_cast<uint32_t>(rem < kFoldLeaf ? rem : uint64_t(kFoldLeaf));
-          if (kSq) mu = params[sr];
-        }
-      }
-      src_s[threadIdx.x] = src;
-      len_s[threadIdx.x] = len;
-      mu_s[threadIdx.x] = mu;
-    }
-    __syncthreads();
-    // Two-stage staging: all warps stage the first half of every leaf; then
-    // warp 0's chain lanes fold those 512 elements while warps 1-7 stage the
-    // second halves and signal named barrier 1, which the chain lanes wait on
-    // at the midpoint -- the second half's loads hide behind the first
-    // half's dependent adds.
-    constexpr uint32_t kHalf = kFoldLeaf / 2;
-    {
-      constexpr int kPerA = kLPB * int(kHalf) / 256;  // 16
-      double r[kPerA];
-#pragma unroll
-      for (int q = 0; q < kPerA; ++q) {
-        const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
-        const uint32_t j = flat / kHalf, i = flat % kHalf;
-        r[q] = i < len_s[j] ? __ldcg(src_s[j] + i) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < kPerA; ++q) {
-        const uint32_t flat = uint32_t(q) * 256u + threadIdx.x;
-        stage[(flat / kHalf) * kLeafStride + flat % kHalf] = r[q];
-      }
-    }
-    __syncthreads();
-    PROBE_BLK(kSq, 2);
-    if (threadIdx.x >= 32) {
-      constexpr uint32_t kN = kLPB * kHalf;  // 4096 second-half elements
-      constexpr int kPerB = int((kN + 223) / 224);       // over warps 1-7
-      double r[kPerB];
-      const uint32_t tb = threadIdx.x - 32;
-#pragma unroll
-      for (int q = 0; q < kPerB; ++q) {
-        const uint32_t flat = uint32_t(q) * 224u + tb;
-        const uint32_t j = flat / kHalf, i = kHalf + flat % kHalf;
-        r[q] = flat < kN && i < len_s[j] ? __ldcg(src_s[j] + i) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < kPerB; ++q) {
-        const uint32_t flat = uint32_t(q) * 224u + tb;
-        if (flat < kN) stage[(flat / kHalf) * kLeafStride + kHalf + flat % kHalf] = r[q];
-      }
-      __threadfence_block();
-      asm volatile("bar.arrive 1, 256;" ::: "memory");
-    } else {
-      const bool chain = threadIdx.x < kLPB && len_s[threadIdx.x] != 0;
-      const uint32_t len = chain ? len_s[threadIdx.x] : 0u;
-      const double* v = stage + threadIdx.x * kLeafStride;
-      const double mu = (kSq && chain) ? mu_s[threadIdx.x] : 0.0;
-      // element term: x (sum pass) or (x - mu)^2 (sq pass); independent of acc
-      auto term = [&](double x) {
-        if (kSq) {
-          const double d = __dsub_rn(x, mu);
-          return __dmul_rn(d, d);
-        }
-        return x;
-      };
-      // Software-pipelined chain over [i, end): the next 16 operands are read
-      // from shared memory while the current 16 dependent adds retire.
-      auto fold = [&](double acc, uint32_t i, uint32_t end) {
-        constexpr int kG = 16;
-        double cur[kG], nxt[kG];
-        if (i + kG <= end) {
-#pragma unroll
-          for (int j = 0; j < kG; ++j) cur[j] = v[i + j];
-          while (i + 2 * kG <= end) {
-#pragma unroll
-            for (int j = 0; j < kG; ++j) nxt[j] = v[i + kG + j];
-#pragma unroll
-            for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, term(cur[j]));
-#pragma unroll
-            for (int j = 0; j < kG; ++j) cur[j] = nxt[j];
-            i += kG;
-          }
-#pragma unroll
-          for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, term(cur[j]));
-          i += kG;
-        }
-        for (; i < end; ++i) acc = __dadd_rn(acc, term(v[i]));
-        return acc;
-      };
-      double acc = 0.0;
-      if (chain) acc = fold(term(v[0]), 1, len < kHalf ? len : kHalf);
-      __syncwarp();
-      if (threadIdx.x == 0) PROBE_BLK_T(kSq, 4);
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // the second halves are staged
-      if (threadIdx.x == 0) PROBE_BLK_T(kSq, 5);
-      if (chain) {
-        if (len > kHalf) acc = fold(acc, kHalf, len);
-        partials[first + threadIdx.x] = acc;
-        if (threadIdx.x == 0) PROBE_BLK_T(kSq, 3);
-      }
-    }
-  }
-  if (kSq && merged) {
-    // device-resident loop: the next EM starts from buffer 0, so an odd
-    // number of MAP iterations leaves the committed labels to move back
-    if (executed_iters(unconv, map_max, fixed) & 1) {
-      const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-      for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < ep.R; v += stride)
-        ep.lab0[v] = ep.lab1[v];
-    }
-  }
-  // ---- last block: trees + epilogue ----
-  if (tail_mode == 1) return;
-  __shared__ bool last;
-  if (tail_mode == 0) {
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    PROBE_TAIL(kSq, 0);
-  } else if (!kSq && hood_parts) {  // trees only: place the hood-series partials
-    const uint32_t h0 = leaf_start[M], nh = leaf_start[M + 1] - h0;
-    for (uint32_t i = threadIdx.x; i < nh; i += blockDim.x) partials[h0 + i] = hood_parts[i];
-    __syncthreads();
-  }
-  __shared__ EmPrefetch pf;
-  if (kSq && merged && threadIdx.x == 0) em_prefetch(ep, &pf);
-  constexpr uint32_t kStageDoubles = 8 * kLeafStride;  // (the tail's stage: 8 x 1056)
-  static_assert(8 * 1056 >= kStageDoubles, "tail stage");
-  auto finish = [&](uint32_t s, double folded) {  // parameters / total energy of series s
+  if (em_skipped(unconv)) return;
+  for (uint32_t i = threadIdx.x; i < 4 * M + 4; i += blockDim.x) lay[i] = layout[i];
+  __syncthreads();
+  const uint32_t* n = lay;
+  const uint32_t* leaf_start = lay + 2 * M + 1;
+  const uint32_t nch_max = (leaf_start[M + 1] + kFoldLeaf - 1) / kFoldLeaf + 1;
+  double* roots = scratch;
+  double* qw = scratch + (nch_max + 1) / 2 * 2 + (threadIdx.x >> 5) * kTreeScratch;
+  for (uint32_t s = 0; s < (kSq ? M : M + 1); ++s) {
+    const uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
+    const double* p = s < M ? partials + leaf_start[s] : hood_parts;
+    const double folded = cnt ? block_series_tree(p, cnt, roots, qw) : 0.0;
+    if (threadIdx.x != 0) continue;
     if (s < M) {
-      if (n[s] != 0) {  // empty labels keep their previous parameters
+      if (n[s] != 0) {  // empty labels keep their previous parameters (engine.cpp:209-220)
         const double count = static_cast<double>(n[s]);
         if (!kSq) {
           params[s] = __ddiv_rn(folded, count);
@@ -488,133 +329,15 @@ __global__ void __launch_bounds__(256)
       }
     } else {
       // total energy: dpp::reduce(..., 0.0) -> identity only for empty input
-      em_out[0] = (leaf_start[M + 1] == leaf_start[M]) ? 0.0 : folded;
+      em_out[0] = cnt == 0 ? 0.0 : folded;
       em_out[1] = static_cast<double>(unconv ? executed_iters(unconv, map_max, fixed) : 0);
     }
-  };
-  const uint32_t all_leaves = leaf_start[nseries];
-  if (nseries <= kTileThreads / 32 && all_leaves <= kStageDoubles) {
-    // every series' tree at once: one warp per series in shared memory
-    for (uint32_t i = threadIdx.x; i < all_leaves; i += blockDim.x) stage[i] = __ldcg(partials + i);
-    __syncthreads();
-    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (w < nseries) {
-      double* p = stage + leaf_start[w];
-      uint32_t cnt = leaf_start[w + 1] - leaf_start[w];
-      while (cnt > 1) {
-        const uint32_t pairs = cnt / 2;
-        for (uint32_t base = 0; base < pairs; base += 32) {
-          const uint32_t i = base + lane;
-          const double v = i < pairs ? __dadd_rn(p[2 * i], p[2 * i + 1]) : 0.0;
-          __syncwarp();
-          if (i < pairs) p[i] = v;
-          __syncwarp();
-        }
-        if ((cnt & 1u) && lane == 0) p[pairs] = p[cnt - 1];
-        __syncwarp();
-        cnt = pairs + (cnt & 1u);
-      }
-      if (lane == 0) finish(w, cnt ? p[0] : 0.0);
-    }
-    __syncthreads();
-    PROBE_TAIL(kSq, 1);
-    if (kSq && merged && threadIdx.x < 32) em_record(ep, true, &pf);
-    if (threadIdx.x == 0 && tail_mode == 0) *done = 0;  // re-arm the ticket for the next launch
-    PROBE_TAIL(kSq, 2);
-    return;
   }
-  for (uint32_t s = 0; s < nseries; ++s) {
-    uint32_t cnt = leaf_start[s + 1] - leaf_start[s];
-    double* p = partials + leaf_start[s];
-    // Long series: reduce aligned 1024-partial chunks first (one warp per
-    // chunk, bottom-up adjacent pairing in shared memory); a chunk's root is
-    // exactly the level-10 node of the series' tree, and the tree continues
-    // over the roots (written in place, below every unread element).
-    while (cnt > kStageDoubles) {
-      const uint32_t nch = (cnt + 1023) / 1024;
-      const uint32_t wch = threadIdx.x >> 5, ln = threadIdx.x & 31;
-      for (uint32_t c0 = 0; c0 < nch; c0 += blockDim.x >> 5) {
-        const uint32_t c = c0 + wch;
-        double* q = stage + wch * 1056;
-        uint32_t m = 0;
-        if (c < nch) {
-          m = min(1024u, cnt - c * 1024);
-          for (uint32_t i = ln; i < m; i += 32) q[i] = __ldcg(p + uint64_t(c) * 1024 + i);
-        }
-        __syncthreads();  // every chunk of this group is read before any root is written
-        if (c < nch) {
-          __syncwarp();
-          while (m > 1) {
-            const uint32_t pairs = m / 2;
-            for (uint32_t i0 = 0; i0 < pairs; i0 += 32) {
-              const uint32_t i = i0 + ln;
-              const double v = i < pairs ? __dadd_rn(q[2 * i], q[2 * i + 1]) : 0.0;
-              __syncwarp();
-              if (i < pairs) q[i] = v;
-              __syncwarp();
-            }
-            if ((m & 1u) && ln == 0) q[pairs] = q[m - 1];
-            __syncwarp();
-            m = pairs + (m & 1u);
-          }
-          if (ln == 0) p[c] = q[0];
-        }
-        __syncthreads();
-      }
-      cnt = nch;
-    }
-    if (cnt >= 1 && cnt <= kStageDoubles) {  // (an empty label has no partials at all)
-      // the tree levels run in shared memory (one global round trip in total)
-      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) stage[i] = __ldcg(p + i);
-      __syncthreads();
-      while (cnt > 1) {
-        const uint32_t pairs = cnt / 2;
-        for (uint32_t base = 0; base < pairs; base += blockDim.x) {
-          const uint32_t i = base + threadIdx.x;
-          const double v = i < pairs ? __dadd_rn(stage[2 * i], stage[2 * i + 1]) : 0.0;
-          __syncthreads();
-          if (i < pairs) stage[i] = v;
-          __syncthreads();
-        }
-        if (cnt & 1u) {
-          if (threadIdx.x == 0) stage[pairs] = stage[cnt - 1];
-          __syncthreads();
-        }
-        cnt = pairs + (cnt & 1u);
-      }
-      if (threadIdx.x == 0) p[0] = stage[0];
-      __syncthreads();
-      cnt = 1;
-    }
-    while (cnt > 1) {
-      const uint32_t pairs = cnt / 2;
-      for (uint32_t base = 0; base < pairs; base += blockDim.x) {
-        const uint32_t i = base + threadIdx.x;
-        double v = 0.0;
-        if (i < pairs) v = __dadd_rn(__ldcg(p + 2 * i), __ldcg(p + 2 * i + 1));
-        __syncthreads();
-        if (i < pairs) p[i] = v;
-        __syncthreads();
-      }
-      if (cnt & 1u) {
-        if (threadIdx.x == 0) p[pairs] = __ldcg(p + cnt - 1);
-        __syncthreads();
-      }
-      cnt = pairs + (cnt & 1u);
-    }
-    if (threadIdx.x == 0) finish(s, __ldcg(p));
-    __syncthreads();
-  }
-  if (kSq && merged && threadIdx.x < 32) {
-    __syncwarp();
-    em_record(ep, true, &pf);
-  }
-  if (threadIdx.x == 0 && tail_mode == 0) *done = 0;  // re-arm the ticket for the next launch
 }
 
 
 // ---------------------------------------------------------------------------
-// M-step folds, TMA-fed (the single-device path; k_leaf_fold above serves the
+// M-step folds, TMA-fed (the single-device path; k_fold_trees above serves the
 // partitioned schedule's distributed folds).
 //   k_fold_sum: lane j < kLPB of a one-warp block owns leaf blockIdx*kLPB + j
 //     of the sum pass (the label series of x, then the hood-energy series).
@@ -1727,27 +1450,6 @@ __global__ void k_em_epilogue(EmEpilogueArgs a) {
   em_record(a, false);
 }
 
-// Partitioned optimize: this partition's share of the committed labels and of
-// the last executed MAP iteration's hood-energy row, copied into the buffers
-// the per-EM allgather assembles (the M-step then reads them as if the run
-// were on one device).
-__global__ void k_partition_select(const uint8_t* lab_even, const uint8_t* lab_odd,
-                                   const double* hist, int ring, uint64_t Hs,
-                                   const uint32_t* unconv, int map_max, int fixed, uint32_t vb,
-                                   uint32_t ve, uint64_t hb, uint64_t he, uint8_t* lab_full,
-                                   double* row_full) {
-  pdl_wait();
-  if (em_skipped(unconv)) return;
-  const int T = executed_iters(unconv, map_max, fixed);
-  const uint8_t* lab = (T & 1) ? lab_odd : lab_even;
-  const double* row = hist + uint64_t((T - 1) % ring) * Hs;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  const uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (uint64_t v = vb + i0; v < ve; v += stride) lab_full[v] = lab[v];
-  if (row_full)
-    for (uint64_t h = hb + i0; h < he; h += stride) row_full[h] = row[h];
-}
-
 // Partitioned optimize: this rank's leaves of the hood-energy series (its
 // series range starts on a leaf boundary) folded from the last executed MAP
 // row -- fold_leaf, kernels.hpp:37-42 -- into out[leaf - first_leaf], so the
@@ -1815,8 +1517,7 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
                 const uint8_t* lab_odd, const uint32_t* unconv, int map_max, int fixed,
                 const double* hist, uint64_t Hs, int ring, double* params, double* em_out,
                 MStepBuffers& mb, cudaStream_t s, uint64_t* launches, bool counts_ready,
-                bool scattered, const EmEpilogueArgs* ep, const double* hood_parts,
-                bool scatter_only = false) {
+                bool scattered, const EmEpilogueArgs* ep, const double* hood_parts) {
   mstep_reserve(mb, R, M, Hs);
   const uint32_t tiles = static_cast<uint32_t>((uint64_t(R) + kTileVerts - 1) / kTileVerts);
   uint32_t* counts = mb.counts.get();
@@ -1870,7 +1571,7 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
   const bool few = max_leaves <= uint64_t(4) * kNumSMs;
   const uint64_t label_leaves = (uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M;
   const EmEpilogueArgs epv = ep ? *ep : EmEpilogueArgs{};
-  if (!scatter_only) {
+  {
     // chunk roots: every series' 1024-partial chunks at once in the tail
     const uint64_t chunks = (label_leaves + kFoldLeaf - 1) / kFoldLeaf + M +
                             ((Hs + kFoldLeaf - 1) / kFoldLeaf + kFoldLeaf - 1) / kFoldLeaf + 1;
@@ -1961,57 +1662,23 @@ void launch_mstep(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab
              em_out, mb, s, launches, counts_ready, scattered, ep, hood_parts);
 }
 
-// Partitioned M-step, distributed folds (see partition.cu): the grouping on
-// every rank, then per pass this rank's label-series leaves [lo, hi) (no
-// trees), and -- after the partials are allgathered -- the trees in one block.
-void launch_mstep_scatter(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab,
-                          const uint32_t* unconv, int map_max, int fixed, uint64_t Hs,
-                          double* params, double* em_out, MStepBuffers& mb, cudaStream_t s,
-                          uint64_t* launches) {
-  mstep_core(mean, R, M, lab, lab, unconv, map_max, fixed, nullptr, Hs, 1, params, em_out, mb, s,
-             launches, /*counts_ready=*/false, /*scattered=*/false, nullptr, nullptr,
-             /*scatter_only=*/true);
-}
-
-void launch_leaf_range(bool sq, uint32_t M, uint64_t Hs, const uint32_t* unconv, int map_max,
-                       int fixed, double* params, double* em_out, MStepBuffers& mb, uint32_t lo,
-                       uint32_t hi, cudaStream_t s) {
-  if (hi <= lo) return;
-  const size_t leaf_smem = size_t(8) * 1056 * sizeof(double);
-  const dim3 g(grid_for(hi - lo, kLeavesPerBlock));
-  const EmEpilogueArgs epv{};
-  if (sq) {
-    ensure_dynamic_smem(k_leaf_fold<true>, leaf_smem);
-    launch_pdl(k_leaf_fold<true>, g, dim3(256), leaf_smem, s, (const double*)mb.x.get(),
-               (const uint32_t*)mb.layout.get(), M, (const double*)nullptr, Hs, 1, unconv,
-               map_max, fixed, params, mb.partials.get(), em_out, mb.done.get() + 1, epv, 0,
-               (const double*)nullptr, lo, hi, 1);
-  } else {
-    ensure_dynamic_smem(k_leaf_fold<false>, leaf_smem);
-    launch_pdl(k_leaf_fold<false>, g, dim3(256), leaf_smem, s, (const double*)mb.x.get(),
-               (const uint32_t*)mb.layout.get(), M, (const double*)nullptr, Hs, 1, unconv,
-               map_max, fixed, params, mb.partials.get(), em_out, mb.done.get(), epv, 0,
-               (const double*)nullptr, lo, hi, 1);
-  }
-}
-
 void launch_fold_trees(bool sq, uint32_t M, uint64_t Hs, const uint32_t* unconv, int map_max,
                        int fixed, double* params, double* em_out, MStepBuffers& mb,
                        const double* hood_parts, cudaStream_t s) {
-  const size_t leaf_smem = size_t(8) * 1056 * sizeof(double);
-  const EmEpilogueArgs epv{};
+  (void)Hs;
+  const uint64_t leaves = mb.partials.cap;  // >= every series' leaves
+  const size_t smem = (((leaves + kFoldLeaf - 1) / kFoldLeaf + 2) / 2 * 2 + 8 * kTreeScratch) *
+                      sizeof(double);
   if (sq) {
-    ensure_dynamic_smem(k_leaf_fold<true>, leaf_smem);
-    launch_pdl(k_leaf_fold<true>, dim3(1), dim3(256), leaf_smem, s, (const double*)mb.x.get(),
-               (const uint32_t*)mb.layout.get(), M, (const double*)nullptr, Hs, 1, unconv,
-               map_max, fixed, params, mb.partials.get(), em_out, mb.done.get() + 1, epv, 0,
-               (const double*)nullptr, 0u, 0u, 2);
+    ensure_dynamic_smem(k_fold_trees<true>, smem);
+    launch_pdl(k_fold_trees<true>, dim3(1), dim3(256), smem, s, (const uint32_t*)mb.layout.get(),
+               M, unconv, map_max, fixed, params, (const double*)mb.partials.get(), hood_parts,
+               em_out);
   } else {
-    ensure_dynamic_smem(k_leaf_fold<false>, leaf_smem);
-    launch_pdl(k_leaf_fold<false>, dim3(1), dim3(256), leaf_smem, s, (const double*)mb.x.get(),
-               (const uint32_t*)mb.layout.get(), M, (const double*)nullptr, Hs, 1, unconv,
-               map_max, fixed, params, mb.partials.get(), em_out, mb.done.get(), epv, 0,
-               hood_parts, 0u, 0u, 2);
+    ensure_dynamic_smem(k_fold_trees<false>, smem);
+    launch_pdl(k_fold_trees<false>, dim3(1), dim3(256), smem, s, (const uint32_t*)mb.layout.get(),
+               M, unconv, map_max, fixed, params, (const double*)mb.partials.get(), hood_parts,
+               em_out);
   }
 }
 
@@ -2022,16 +1689,6 @@ void launch_em_prologue(uint32_t* unconv, int map_max, cudaStream_t s) {
 void launch_em_epilogue(const EmEpilogueArgs& a, cudaStream_t s) {
   const unsigned g = std::min<unsigned>(grid_for(a.R ? a.R : 1, 256), 4 * kNumSMs);
   launch_pdl(k_em_epilogue, dim3(g), dim3(256), 0, s, a);
-}
-
-void launch_partition_select(const uint8_t* lab_even, const uint8_t* lab_odd, const double* hist,
-                             int ring, uint64_t Hs, const uint32_t* unconv, int map_max, int fixed,
-                             uint32_t vb, uint32_t ve, uint64_t hb, uint64_t he,
-                             uint8_t* lab_full, double* row_full, cudaStream_t s) {
-  const uint64_t n = std::max<uint64_t>(ve - vb, he - hb);
-  const unsigned g = std::min<unsigned>(grid_for(n ? n : 1, 256), 4 * kNumSMs);
-  launch_pdl(k_partition_select, dim3(g), dim3(256), 0, s, lab_even, lab_odd, hist, ring, Hs,
-             unconv, map_max, fixed, vb, ve, hb, he, lab_full, row_full);
 }
 
 void launch_row_leaves(const double* hist, int ring, uint64_t Hs, const uint32_t* unconv,

@@ -18,19 +18,25 @@
 //                                    runs on a side stream, the boundary
 //                                    series after it)
 //                              sum of the unconverged-hood counters
-//   per EM iteration           own labels + own hood-series leaf partials
-//                              (the row folded into 1024-element leaves on the
-//                              rank that owns it) -> allgather; the same
-//                              M-step + EM bookkeeping everywhere
+//   per EM iteration           distributed M-step (k_part_*): own label
+//                              counts -> allgather; own vertices scattered
+//                              into their segments of the label-grouped x;
+//                              head fragments (<= 1023 values per label) ->
+//                              allgather; own leaves folded (both passes),
+//                              leaf partials -> allgather; the same trees
+//                              and EM bookkeeping on every rank.  The own
+//                              hood-series leaves (the row folded into
+//                              1024-element leaves on the rank that owns
+//                              them) -> allgather.
+//   after the EM loop          the labels, gathered once.
 //
 // Everything runs in stream order with the device-side early exit of the
 // single-GPU path (skipped iterations still move their -- stale but never
-// read -- halos, so the schedule is static and capturable).  The allgathered
-// labels and leaf partials make the M-step input identical to the one-device
-// run (series ranges start on leaf boundaries, so every leaf is folded whole,
-// in order, on one rank), so the results are bit-identical to dpmrf_optimize.
-// Per EM at 16384^2 / 8 ranks this moves 5.5 MB of labels + 86 KB of
-// partials instead of 5.5 MB + the 88 MB hood-energy row.
+// read -- halos, so the schedule is static and capturable).  Every leaf is
+// folded whole, in order, on one rank and every tree sees the same partials,
+// so the results are bit-identical to dpmrf_optimize.  Per EM at 16384^2 / 8
+// ranks a rank receives ~0.3 MB (counts, 16 KB of heads per rank, leaf
+// partials) instead of the 5.5 MB label gather plus a full-R regroup.
 //
 // Transports: NCCL (one process per GPU; libnccl.so.2 loaded at run time,
 // grouped ncclSend/ncclRecv for the halos, ncclAllReduce for the counters,
@@ -43,11 +49,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
+#include <initializer_list>
 #include <cstring>
 #include <memory>
 #include <vector>
 
 #include "context.cuh"
+#include "scan.cuh"
 
 using namespace dpmrf_b200;
 
@@ -80,11 +89,15 @@ struct Nccl {
   }
   void load() {
     // DPMRF_NCCL_LIB: another library with the same entry points (the test
-    // suite's in-process multi-rank shim, tests/nccl_shim)
+    // suite's in-process multi-rank shim, tests/nccl_shim).  RTLD_LOCAL: the
+    // symbols are used through dlsym only, and must not shadow the NCCL a
+    // later-loaded library (libtorch_cuda) links against.
     const char* alt = std::getenv("DPMRF_NCCL_LIB");
-    void* h = alt && alt[0] ? dlopen(alt, RTLD_NOW | RTLD_GLOBAL)
-                            : dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h && !(alt && alt[0])) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    // an NCCL the process already loaded (e.g. by PyTorch) is reused as is
+    void* h = alt && alt[0] ? dlopen(alt, RTLD_NOW | RTLD_LOCAL)
+                            : dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL | RTLD_NOLOAD);
+    if (!h && !(alt && alt[0])) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h && !(alt && alt[0])) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
     if (!h) fail(DPMRF_NCCL_ERROR, std::string("cannot load libnccl.so.2: ") + dlerror());
     auto sym = [&](const char* name) {
       void* p = dlsym(h, name);
@@ -185,6 +198,281 @@ __global__ void k_sum_counters(CounterPtrs c, int W, int t) {
   for (int r = 0; r < W; ++r) c.p[r][t] = s;
 }
 
+// ---- distributed M-step ----------------------------------------------------------------
+// update_parameters (engine.cpp:193-223) without gathering the labels: the
+// label-grouped array x is the stable sort of ALL region means by label, so
+// rank r's vertices form, per label l, the contiguous segment
+// [label_start[l] + off_r[l], + n_r[l]) of x (off_r[l] = the counts of the
+// ranks before it).  Each rank scatters its own vertices there, owns the
+// 1024-element leaves of x that START in its segments, and folds them
+// (fold_leaf, kernels.hpp:37-42) -- a leaf straddling into the next ranks'
+// segments reads their "head" fragments (<= 1023 elements per label, up to
+// the next leaf boundary), which are allgathered.  The leaf partials are
+// allgathered too and every rank runs the same trees.  Per EM and rank this
+// exchanges M counts, M x 1024 head values and its leaf partials instead of
+// all R labels, and nobody regroups vertices it does not own.
+constexpr uint32_t kPartLPB = 8;  // leaves per fold block (one chain per leaf)
+
+// (the EM skip flag and the final-label buffer, as engine_dev.cuh's
+// em_skipped / final_labels: unconv[-4] = EM loop stopped; the last executed
+// MAP iteration T selects the buffer by parity)
+__device__ __forceinline__ bool part_em_skipped(const uint32_t* unconv) {
+  return unconv && unconv[-4] != 0;
+}
+__device__ __forceinline__ const uint8_t* part_final_labels(const uint8_t* even, const uint8_t* odd,
+                                                            const uint32_t* unconv, int map_max,
+                                                            int fixed) {
+  int T = map_max;
+  if (!fixed)
+    for (int t = 0; t < map_max; ++t)
+      if (unconv[t] == 0) {
+        T = t + 1;
+        break;
+      }
+  return (T & 1) ? odd : even;
+}
+
+// per-rank metadata written by k_part_layout (u32):
+//   [0, M)   off_r[l]      this rank's offset inside label l's segment of x
+//   [M, 2M)  own_first[l]  first owned leaf of label l (index within the label)
+//   [2M,3M)  own_end[l]    one past the last owned leaf
+//   [3M,4M)  own_base[l]   ordinal of own_first[l] among this rank's owned leaves
+//   [4M]     owned leaves in total
+__device__ __forceinline__ uint32_t head_len(uint32_t off, uint32_t n) {
+  const uint32_t to_boundary = (kFoldLeaf - off % kFoldLeaf) % kFoldLeaf;
+  return min(n, to_boundary);
+}
+
+// own label counts (stable tile ranks as k_label_tiles<0>) + per-tile counts
+__global__ void __launch_bounds__(256)
+    k_part_count(const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
+                 int map_max, int fixed, uint32_t vb, uint32_t ve, uint32_t M,
+                 uint32_t* __restrict__ tile_counts, uint32_t* __restrict__ cnt) {
+  extern __shared__ uint32_t wcnt[];  // [warp][M]
+  pdl_wait();
+  if (part_em_skipped(unconv)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint8_t* lab = part_final_labels(lab_even, lab_odd, unconv, map_max, fixed);
+  for (uint32_t i = threadIdx.x; i < 8 * M; i += 256) wcnt[i] = 0;
+  __syncthreads();
+  const uint32_t v = vb + blockIdx.x * 256 + threadIdx.x;
+  const bool valid = v < ve;
+  const uint32_t l = valid ? lab[v] : 0xFFFFFFFFu;
+  const unsigned peers = __match_any_sync(0xffffffffu, l);
+  if (valid && __popc(peers & ((1u << lane) - 1u)) == 0) wcnt[warp * M + l] = __popc(peers);
+  __syncthreads();
+  for (uint32_t q = threadIdx.x; q < M; q += 256) {
+    uint32_t c = 0;
+    for (int w = 0; w < 8; ++w) c += wcnt[w * M + q];
+    tile_counts[uint64_t(blockIdx.x) * M + q] = c;
+    if (c) atomicAdd(&cnt[q], c);
+  }
+}
+
+// global layout (n | label_start | leaf_start, as the one-device M-step) and
+// this rank's metadata, from the gathered counts allcnt[W][M]
+__global__ void k_part_layout(const uint32_t* __restrict__ allcnt, int W, int r, uint32_t M,
+                              uint64_t Hs, const uint32_t* unconv, uint32_t* __restrict__ layout,
+                              uint32_t* __restrict__ meta) {
+  pdl_wait();
+  if (part_em_skipped(unconv) || threadIdx.x != 0) return;
+  uint32_t* n = layout;
+  uint32_t* label_start = layout + M;
+  uint32_t* leaf_start = layout + 2 * M + 1;
+  uint32_t s = 0, lf = 0, owned = 0;
+  for (uint32_t l = 0; l < M; ++l) {
+    uint32_t tot = 0, off = 0;
+    for (int q = 0; q < W; ++q) {
+      if (q < r) off += allcnt[q * M + l];
+      tot += allcnt[q * M + l];
+    }
+    n[l] = tot;
+    label_start[l] = s;
+    leaf_start[l] = lf;
+    s += tot;
+    lf += (tot + kFoldLeaf - 1) / kFoldLeaf;
+    const uint32_t mine = allcnt[r * M + l];
+    // leaves j with off <= 1024 j < off + mine
+    const uint32_t first = (off + kFoldLeaf - 1) / kFoldLeaf;
+    const uint32_t end = mine ? (off + mine + kFoldLeaf - 1) / kFoldLeaf : first;
+    meta[l] = off;
+    meta[M + l] = first;
+    meta[2 * M + l] = end > first ? end : first;
+    meta[3 * M + l] = owned;
+    owned += end > first ? end - first : 0;
+  }
+  label_start[M] = s;
+  leaf_start[M] = lf;
+  leaf_start[M + 1] = lf + uint32_t((Hs + kFoldLeaf - 1) / kFoldLeaf);
+  meta[4 * M] = owned;
+}
+
+// x positions of this rank's tiles: label_start + off_r + the counts of its
+// earlier tiles (one block, chunks of 1024 tiles)
+__global__ void __launch_bounds__(1024)
+    k_part_tile_base(const uint32_t* __restrict__ tile_counts, uint32_t tiles, uint32_t M,
+                     const uint32_t* unconv, const uint32_t* __restrict__ layout,
+                     const uint32_t* __restrict__ meta, uint32_t* __restrict__ tile_base) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry_s;
+  pdl_wait();
+  if (part_em_skipped(unconv)) return;
+  for (uint32_t l = 0; l < M; ++l) {
+    uint32_t carry = layout[M + l] + meta[l];
+    for (uint32_t c0 = 0; c0 < tiles; c0 += 1024) {
+      const uint32_t i = c0 + threadIdx.x;
+      const uint32_t v = i < tiles ? tile_counts[uint64_t(i) * M + l] : 0u;
+      uint32_t total = 0;
+      const uint32_t ex = block_exclusive_scan(v, warp_sums, &total);
+      if (i < tiles) tile_base[uint64_t(i) * M + l] = carry + ex;
+      carry += total;
+      __syncthreads();
+    }
+  }
+  (void)carry_s;
+}
+
+// stable scatter of this rank's region means into x (k_label_tiles<1>)
+__global__ void __launch_bounds__(256)
+    k_part_scatter(const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
+                   int map_max, int fixed, uint32_t vb, uint32_t ve, uint32_t M,
+                   const double* __restrict__ mean, const uint32_t* __restrict__ tile_base,
+                   double* __restrict__ x) {
+  extern __shared__ uint32_t wcnt[];  // [warp][M]
+  pdl_wait();
+  if (part_em_skipped(unconv)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint8_t* lab = part_final_labels(lab_even, lab_odd, unconv, map_max, fixed);
+  for (uint32_t i = threadIdx.x; i < 8 * M; i += 256) wcnt[i] = 0;
+  __syncthreads();
+  const uint32_t v = vb + blockIdx.x * 256 + threadIdx.x;
+  const bool valid = v < ve;
+  const uint32_t l = valid ? lab[v] : 0xFFFFFFFFu;
+  const unsigned peers = __match_any_sync(0xffffffffu, l);
+  const uint32_t rank_in_warp = __popc(peers & ((1u << lane) - 1u));
+  if (valid && rank_in_warp == 0) wcnt[warp * M + l] = __popc(peers);
+  __syncthreads();
+  if (valid) {
+    uint32_t before = 0;
+    for (int w = 0; w < warp; ++w) before += wcnt[w * M + l];
+    x[tile_base[uint64_t(blockIdx.x) * M + l] + before + rank_in_warp] = mean[v];
+  }
+}
+
+// this rank's head fragments -> heads[l * 1024 ...] (its allgather slot)
+__global__ void k_part_pack_heads(const double* __restrict__ x, const uint32_t* unconv,
+                                  const uint32_t* __restrict__ layout,
+                                  const uint32_t* __restrict__ allcnt, int r, uint32_t M,
+                                  const uint32_t* __restrict__ meta, double* __restrict__ heads) {
+  pdl_wait();
+  if (part_em_skipped(unconv)) return;
+  for (uint32_t l = blockIdx.x; l < M; l += gridDim.x) {
+    const uint32_t off = meta[l], len = head_len(off, allcnt[r * M + l]);
+    const uint64_t base = uint64_t(layout[M + l]) + off;
+    for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) heads[uint64_t(l) * kFoldLeaf + i] = x[base + i];
+  }
+}
+
+// the later ranks' head fragments into x (the straddling leaves this rank owns)
+__global__ void k_part_unpack_heads(const double* __restrict__ heads, const uint32_t* unconv,
+                                    const uint32_t* __restrict__ layout,
+                                    const uint32_t* __restrict__ allcnt, int W, int r, uint32_t M,
+                                    double* __restrict__ x) {
+  pdl_wait();
+  if (part_em_skipped(unconv)) return;
+  for (uint32_t ql = blockIdx.x; ql < uint32_t(W) * M; ql += gridDim.x) {
+    const int q = int(ql / M);
+    const uint32_t l = ql % M;
+    if (q <= r) continue;
+    uint32_t off = 0;
+    for (int p = 0; p < q; ++p) off += allcnt[p * M + l];
+    const uint32_t len = head_len(off, allcnt[q * M + l]);
+    const uint64_t base = uint64_t(layout[M + l]) + off;
+    const double* src = heads + (uint64_t(q) * M + l) * kFoldLeaf;
+    for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) x[base + i] = src[i];
+  }
+}
+
+// fold this rank's owned leaves (kSq: (x - mu)^2, engine.cpp:213-217) ->
+// pk[ordinal] (the allgather slot) and partials[global leaf]
+template <bool kSq>
+__global__ void __launch_bounds__(256)
+    k_part_fold(const double* __restrict__ x, const uint32_t* unconv,
+                const uint32_t* __restrict__ layout, const uint32_t* __restrict__ meta,
+                uint32_t M, const double* __restrict__ params, double* __restrict__ pk,
+                double* __restrict__ partials) {
+  extern __shared__ double stage[];  // kPartLPB x (kFoldLeaf + 1)
+  __shared__ uint64_t src_s[kPartLPB];
+  __shared__ uint32_t len_s[kPartLPB], leaf_s[kPartLPB];
+  __shared__ double mu_s[kPartLPB];
+  pdl_wait();
+  if (part_em_skipped(unconv)) return;
+  const uint32_t owned = meta[4 * M];
+  const uint32_t o0 = blockIdx.x * kPartLPB;
+  if (o0 >= owned) return;
+  if (threadIdx.x < kPartLPB) {
+    const uint32_t o = o0 + threadIdx.x;
+    uint32_t len = 0;
+    if (o < owned) {
+      uint32_t l = 0;  // the label whose owned ordinals [own_base, + count) hold o
+      while (o >= meta[3 * M + l] + (meta[2 * M + l] - meta[M + l])) ++l;
+      const uint32_t j = meta[M + l] + (o - meta[3 * M + l]);
+      const uint32_t n = layout[l];
+      const uint64_t b = uint64_t(j) * kFoldLeaf;
+      len = static_cast<uint32_t>(n - b < kFoldLeaf ? n - b : uint64_t(kFoldLeaf));
+      src_s[threadIdx.x] = uint64_t(layout[M + l]) + b;
+      leaf_s[threadIdx.x] = layout[2 * M + 1 + l] + j;
+      mu_s[threadIdx.x] = kSq ? params[l] : 0.0;
+    }
+    len_s[threadIdx.x] = len;
+  }
+  __syncthreads();
+  constexpr uint32_t kStride = kFoldLeaf + 1;
+  for (uint32_t f = threadIdx.x; f < kPartLPB * kFoldLeaf; f += blockDim.x) {
+    const uint32_t j = f / kFoldLeaf, i = f % kFoldLeaf;
+    if (i < len_s[j]) {
+      double v = __ldcg(x + src_s[j] + i);
+      if (kSq) {
+        const double d = __dsub_rn(v, mu_s[j]);
+        v = __dmul_rn(d, d);
+      }
+      stage[j * kStride + i] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kPartLPB && len_s[threadIdx.x]) {
+    const double* v = stage + threadIdx.x * kStride;
+    double acc = v[0];
+    for (uint32_t i = 1; i < len_s[threadIdx.x]; ++i) acc = __dadd_rn(acc, v[i]);
+    pk[o0 + threadIdx.x] = acc;
+    partials[leaf_s[threadIdx.x]] = acc;
+  }
+}
+
+// every rank's owned-leaf partials (pk[q][ordinal]) -> partials[global leaf]
+__global__ void k_part_unpack_partials(const double* __restrict__ pk, uint64_t chunk_l,
+                                       const uint32_t* unconv, const uint32_t* __restrict__ layout,
+                                       const uint32_t* __restrict__ allcnt, int W, int r,
+                                       uint32_t M, double* __restrict__ partials) {
+  pdl_wait();
+  if (part_em_skipped(unconv)) return;
+  for (int q = blockIdx.x; q < W; q += gridDim.x) {
+    if (q == r) continue;
+    uint32_t ord = 0;
+    for (uint32_t l = 0; l < M; ++l) {
+      uint32_t off = 0;
+      for (int p = 0; p < q; ++p) off += allcnt[p * M + l];
+      const uint32_t mine = allcnt[q * M + l];
+      const uint32_t first = (off + kFoldLeaf - 1) / kFoldLeaf;
+      const uint32_t end = mine ? (off + mine + kFoldLeaf - 1) / kFoldLeaf : first;
+      const uint32_t cnt = end > first ? end - first : 0;
+      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x)
+        partials[layout[2 * M + 1 + l] + first + i] = pk[uint64_t(q) * chunk_l + ord + i];
+      ord += cnt;
+    }
+  }
+}
+
 // ---- per-partition device state ---------------------------------------------------
 struct Part {
   int r = 0;
@@ -198,6 +486,10 @@ struct Part {
   DevBuf<double> minE, hist, hpart, params, em_out, terms, em_rec, em_hist;
   DevBuf<uint32_t> state;  // [em_done, pending, em_count, pad | unconv[map_max]]
   DevBuf<uint8_t> eq;      // equal-run counts of the window test (owned series)
+  // distributed M-step: gathered label counts [W][M], this rank's metadata,
+  // head fragments [W][M][1024], owned-leaf partials [W][chunk_l]
+  DevBuf<uint32_t> allcnt, meta;
+  DevBuf<double> heads, pk;
   MStepBuffers ms;
   MapArgs a{};
   EmEpilogueArgs ep{};
@@ -287,6 +579,11 @@ __global__ void k_interior(const uint32_t* __restrict__ s_off, const uint32_t* _
   }
 }
 
+// upper bound of the leaves a rank owns in the distributed M-step
+uint64_t owned_leaf_cap(const dpmrf_group* g, uint32_t M) {
+  return (uint64_t(g->chunkV) + kFoldLeaf - 1) / kFoldLeaf + M + 1;
+}
+
 // Ranges + halo windows for the context's current structure.
 void plan(dpmrf_group* g) {
   dpmrf_context* ctx = g->ctx;
@@ -342,10 +639,15 @@ void plan(dpmrf_group* g) {
     }
   const int mine = g->local() ? 0 : g->rank;
   (void)mine;
-  // per EM: labels (u8) + the hood-energy series' leaf partials (f64)
-  g->gather_bytes = g->local()
-                        ? uint64_t(W) * (W - 1) * (g->chunkV + 8 * (g->chunkH / kFoldLeaf))
-                        : uint64_t(W - 1) * (g->chunkV + 8 * (g->chunkH / kFoldLeaf));
+  // per EM and receiving rank (distributed M-step): the other ranks' label
+  // counts, hood-series leaf partials, head fragments and owned-leaf
+  // partials of both passes (the labels are gathered once per optimize)
+  {
+    const uint64_t M = ctx->trace_M ? ctx->trace_M : 2;
+    const uint64_t per = 4 * M + 8 * (g->chunkH / kFoldLeaf) + 8 * M * kFoldLeaf +
+                         2 * 8 * owned_leaf_cap(g, uint32_t(M));
+    g->gather_bytes = (g->local() ? uint64_t(W) : 1) * (W - 1) * per;
+  }
   // interior series ranges (one small D2H per partition, planning time only)
   {
     uint32_t* io = ctx->tmp_u32[4].ensure(2 * W);
@@ -434,51 +736,38 @@ void sum_counters(dpmrf_group* g, int t, cudaStream_t st, uint64_t* k) {
   NK(nccl.AllReduce(u, u, 1, ncclUint32, ncclSum, g->comm, st));
 }
 
-// Committed labels and the last hood-energy row, assembled on every partition.
-void allgather(dpmrf_group* g, cudaStream_t st) {
+// Per-rank slots of `count` elements assembled on every partition: slot r of
+// buf(part r) -> slot r of buf(every part) (in-place ncclAllGather; device
+// copies on the local transport).  Several buffers go in one NCCL group.
+struct SlotBuf {
+  std::function<void*(Part&)> buf;
+  uint64_t count;
+  ncclDataType_t type;
+  size_t elem;
+};
+void gather_slots(dpmrf_group* g, std::initializer_list<SlotBuf> bufs, cudaStream_t st) {
   const int W = g->world;
   if (W == 1) return;
-  const uint64_t cv = g->chunkV, chl = g->chunkH / kFoldLeaf;
   if (g->local()) {
-    for (int s = 0; s < W; ++s)
-      for (int d = 0; d < W; ++d) {
-        if (s == d) continue;
-        Part& ps = *g->parts[s];
-        Part& pd = *g->parts[d];
-        CK(cudaMemcpyAsync(pd.lab_full.get() + s * cv, ps.lab_full.get() + s * cv, cv,
-                           cudaMemcpyDeviceToDevice, st));
-        CK(cudaMemcpyAsync(pd.hpart.get() + s * chl, ps.hpart.get() + s * chl, 8 * chl,
-                           cudaMemcpyDeviceToDevice, st));
-      }
+    for (const SlotBuf& b : bufs)
+      for (int sp = 0; sp < W; ++sp)
+        for (int d = 0; d < W; ++d) {
+          if (sp == d || !b.count) continue;
+          const uint64_t bytes = b.count * b.elem;
+          CK(cudaMemcpyAsync(static_cast<char*>(b.buf(*g->parts[d])) + sp * bytes,
+                             static_cast<char*>(b.buf(*g->parts[sp])) + sp * bytes, bytes,
+                             cudaMemcpyDeviceToDevice, st));
+        }
     return;
   }
   Nccl& nccl = Nccl::get();
   Part& p = *g->parts[0];
-  const int me = g->rank;
   NK(nccl.GroupStart());
-  NK(nccl.AllGather(p.lab_full.get() + me * cv, p.lab_full.get(), cv, ncclUint8, g->comm, st));
-  NK(nccl.AllGather(p.hpart.get() + me * chl, p.hpart.get(), chl, ncclFloat64, g->comm, st));
-  NK(nccl.GroupEnd());
-}
-
-// The M-step's label-series leaf partials of every rank (equal chunks of
-// chunk_l leaves, in place in each rank's partials array).
-void allgather_partials(dpmrf_group* g, uint64_t chunk_l, cudaStream_t st) {
-  const int W = g->world;
-  if (W == 1) return;
-  if (g->local()) {
-    for (int s = 0; s < W; ++s)
-      for (int d = 0; d < W; ++d) {
-        if (s == d) continue;
-        CK(cudaMemcpyAsync(g->parts[d]->ms.partials.get() + s * chunk_l,
-                           g->parts[s]->ms.partials.get() + s * chunk_l, 8 * chunk_l,
-                           cudaMemcpyDeviceToDevice, st));
-      }
-    return;
+  for (const SlotBuf& b : bufs) {
+    char* base = static_cast<char*>(b.buf(p));
+    NK(nccl.AllGather(base + g->rank * b.count * b.elem, base, b.count, b.type, g->comm, st));
   }
-  Nccl& nccl = Nccl::get();
-  double* buf = g->parts[0]->ms.partials.get();
-  NK(nccl.AllGather(buf + g->rank * chunk_l, buf, chunk_l, ncclFloat64, g->comm, st));
+  NK(nccl.GroupEnd());
 }
 
 bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dpmrf_run_options& o,
@@ -509,8 +798,6 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
   const uint64_t padV = uint64_t(g->chunkV) * W, padH = g->chunkH * W;
   const uint64_t rec_stride = 3 + 3 * uint64_t(M);
   const int ring = L + 1;
-  // label-series leaves per rank in the distributed folds (upper bound R/1024 + M)
-  const uint64_t chunk_l = ((uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M + W - 1) / W;
   const bool packed = !(o.flags & DPMRF_RUN_CSR);
   for (auto& pp : g->parts) {
     Part& p = *pp;
@@ -549,7 +836,7 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
     a.eq = a.hood_k ? p.eq.ensure(Hs ? Hs : 1) : nullptr;
     uint32_t* state = p.state.ensure(uint64_t(map_max) + 4);
     a.unconv = state + 4;
-    a.tile_counts = nullptr;  // the M-step counts the gathered labels itself
+    a.tile_counts = nullptr;  // the distributed M-step counts its own labels
     a.tiles = label_tiles(R);
     p.hpart.ensure(padH / kFoldLeaf);
     p.params.ensure(2 * M);
@@ -557,9 +844,10 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
     p.em_rec.ensure(uint64_t(em_max ? em_max : 1) * rec_stride);
     p.em_hist.ensure(uint64_t(em_max ? em_max : 1));
     mstep_reserve(p.ms, R, M, Hs);
-    p.ms.partials.ensure(std::max<uint64_t>(uint64_t(W) * chunk_l + (Hs + kFoldLeaf - 1) / kFoldLeaf + 1,
-                                            (uint64_t(R) + kFoldLeaf - 1) / kFoldLeaf + M +
-                                                (Hs + kFoldLeaf - 1) / kFoldLeaf + 1));
+    p.allcnt.ensure(uint64_t(W) * M);
+    p.meta.ensure(4 * uint64_t(M) + 1);
+    p.heads.ensure(uint64_t(W) * M * kFoldLeaf);
+    p.pk.ensure(uint64_t(W) * owned_leaf_cap(g, M));
     EmEpilogueArgs& ep = p.ep;
     ep = EmEpilogueArgs{};
     ep.unconv = a.unconv;
@@ -593,6 +881,7 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
 
   if (em_max > 0) {
     result = g->parts[0]->lab_full.get();
+    int final_buf = 0;  // label buffer holding the final labels (device loop: 0)
     uint64_t em_kernels = 0;
     auto enqueue_em = [&](int parity) {
       uint64_t k = 0;
@@ -658,39 +947,91 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
         // skip one latency-bound collective per MAP iteration.
         if (!fixed) sum_counters(g, t, st, &k);
       }
+      // ---- distributed M-step (see k_part_count .. k_part_unpack_partials) ----
+      const uint64_t cap_l = owned_leaf_cap(g, M);
+      const size_t wsm = 8 * M * sizeof(uint32_t);
       for (auto& pp : g->parts) {
         Part& p = *pp;
-        launch_partition_select(p.lab[parity].get(), p.lab[parity ^ 1].get(), p.a.hist, ring, Hs,
-                                p.a.unconv, map_max, fixed, p.vb, p.ve, p.hb, p.he,
-                                p.lab_full.get(), nullptr, st);
+        const uint32_t ntiles = (p.ve - p.vb + 255) / 256;
+        const uint8_t* le = p.lab[parity].get();
+        const uint8_t* lo_ = p.lab[parity ^ 1].get();
+        CK(cudaMemsetAsync(p.allcnt.get() + uint64_t(p.r) * M, 0, M * sizeof(uint32_t), st));
+        if (ntiles) {
+          launch_pdl(k_part_count, dim3(ntiles), dim3(256), wsm, st, le, lo_,
+                     (const uint32_t*)p.a.unconv, map_max, fixed, p.vb, p.ve, M,
+                     p.ms.counts.get(), p.allcnt.get() + uint64_t(p.r) * M);
+          ++k;
+        }
         launch_row_leaves(p.a.hist, ring, Hs, p.a.unconv, map_max, fixed, p.hb, p.he,
                           p.hpart.get() + p.hb / kFoldLeaf, st);
-        k += 2;
+        ++k;
       }
-      allgather(g, st);
+      gather_slots(g, {SlotBuf{[](Part& q) -> void* { return q.allcnt.get(); }, M, ncclUint32, 4},
+                       SlotBuf{[](Part& q) -> void* { return q.hpart.get(); },
+                               g->chunkH / kFoldLeaf, ncclFloat64, 8}},
+                   st);
       for (auto& pp : g->parts) {
         Part& p = *pp;
-        // the grouping by label on every rank (all labels are gathered)
-        launch_mstep_scatter(p.a.mean, R, M, p.lab_full.get(), p.a.unconv, map_max, fixed, Hs,
-                             p.params.get(), p.em_out.get(), p.ms, st, &k);
+        const uint32_t ntiles = (p.ve - p.vb + 255) / 256;
+        const uint32_t* u = p.a.unconv;
+        launch_pdl(k_part_layout, dim3(1), dim3(32), 0, st, (const uint32_t*)p.allcnt.get(), W,
+                   p.r, M, Hs, u, p.ms.layout.get(), p.meta.get());
+        launch_pdl(k_part_tile_base, dim3(1), dim3(1024), 0, st, (const uint32_t*)p.ms.counts.get(),
+                   ntiles, M, u, (const uint32_t*)p.ms.layout.get(), (const uint32_t*)p.meta.get(),
+                   p.ms.tile_base.get());
+        k += 2;
+        if (ntiles) {
+          launch_pdl(k_part_scatter, dim3(ntiles), dim3(256), wsm, st,
+                     (const uint8_t*)p.lab[parity].get(), (const uint8_t*)p.lab[parity ^ 1].get(),
+                     u, map_max, fixed, p.vb, p.ve, M, (const double*)p.a.mean,
+                     (const uint32_t*)p.ms.tile_base.get(), p.ms.x.get());
+          ++k;
+        }
+        launch_pdl(k_part_pack_heads, dim3(std::min<uint32_t>(M, 64)), dim3(256), 0, st,
+                   (const double*)p.ms.x.get(), u, (const uint32_t*)p.ms.layout.get(),
+                   (const uint32_t*)p.allcnt.get(), p.r, M, (const uint32_t*)p.meta.get(),
+                   p.heads.get() + uint64_t(p.r) * M * kFoldLeaf);
+        ++k;
       }
-      // Distributed folds: each rank folds its chunk of the label-series
-      // leaves, the partials are allgathered, every rank runs the trees (the
-      // same bits everywhere) -- per pass, sum then (x - mu)^2.
+      gather_slots(g, {SlotBuf{[](Part& q) -> void* { return q.heads.get(); },
+                               uint64_t(M) * kFoldLeaf, ncclFloat64, 8}},
+                   st);
+      for (auto& pp : g->parts) {
+        Part& p = *pp;
+        launch_pdl(k_part_unpack_heads, dim3(std::min<uint32_t>(W * M, 256)), dim3(256), 0, st,
+                   (const double*)p.heads.get(), (const uint32_t*)p.a.unconv,
+                   (const uint32_t*)p.ms.layout.get(), (const uint32_t*)p.allcnt.get(), W, p.r, M,
+                   p.ms.x.get());
+        ++k;
+      }
+      // per pass (sum, then (x - mu)^2): owned leaves, gathered partials, the
+      // same trees on every rank (the same bits everywhere)
+      const size_t fsm = size_t(kPartLPB) * (kFoldLeaf + 1) * sizeof(double);
+      ensure_dynamic_smem(k_part_fold<false>, fsm);
+      ensure_dynamic_smem(k_part_fold<true>, fsm);
+      const unsigned fgrid = grid_for(cap_l, kPartLPB);
       for (int pass = 0; pass < 2; ++pass) {
         for (auto& pp : g->parts) {
           Part& p = *pp;
-          const uint32_t lo = uint32_t(uint64_t(p.r) * chunk_l);
-          launch_leaf_range(pass == 1, M, Hs, p.a.unconv, map_max, fixed, p.params.get(),
-                            p.em_out.get(), p.ms, lo, uint32_t(lo + chunk_l), st);
+          launch_pdl(pass ? k_part_fold<true> : k_part_fold<false>, dim3(fgrid), dim3(256), fsm,
+                     st, (const double*)p.ms.x.get(), (const uint32_t*)p.a.unconv,
+                     (const uint32_t*)p.ms.layout.get(), (const uint32_t*)p.meta.get(), M,
+                     (const double*)p.params.get(), p.pk.get() + uint64_t(p.r) * cap_l,
+                     p.ms.partials.get());
           ++k;
         }
-        allgather_partials(g, chunk_l, st);
+        gather_slots(g, {SlotBuf{[](Part& q) -> void* { return q.pk.get(); }, cap_l,
+                                 ncclFloat64, 8}},
+                     st);
         for (auto& pp : g->parts) {
           Part& p = *pp;
+          launch_pdl(k_part_unpack_partials, dim3(std::min<int>(W, 64)), dim3(256), 0, st,
+                     (const double*)p.pk.get(), cap_l, (const uint32_t*)p.a.unconv,
+                     (const uint32_t*)p.ms.layout.get(), (const uint32_t*)p.allcnt.get(), W, p.r,
+                     M, p.ms.partials.get());
           launch_fold_trees(pass == 1, M, Hs, p.a.unconv, map_max, fixed, p.params.get(),
                             p.em_out.get(), p.ms, p.hpart.get(), st);
-          ++k;
+          k += 2;
         }
       }
       for (auto& pp : g->parts) {
@@ -835,7 +1176,18 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
         ctx->stats.em_iters = em + 1;
         if (conv && !fixed) break;
       }
+      final_buf = cur;
     }
+    // the labels are gathered once, after the EM loop (every rank's owned range)
+    for (auto& pp : g->parts) {
+      Part& p = *pp;
+      if (p.ve > p.vb)
+        CK(cudaMemcpyAsync(p.lab_full.get() + p.vb, p.lab[final_buf].get() + p.vb, p.ve - p.vb,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    gather_slots(g, {SlotBuf{[](Part& q) -> void* { return q.lab_full.get(); }, g->chunkV,
+                             ncclUint8, 1}},
+                 st);
     ctx->stats.series = Hs;
   }
   uint32_t* l32 = ctx->labels32.ensure(R);

@@ -5,11 +5,12 @@ Each rank runs the MAP kernels' arithmetic (numpy, the exact IEEE operation
 order of label_energy, model.hpp:66-72, and of the slot-order hood fold,
 engine.cpp:147-152) over only the vertices / series it owns, moves the halo
 windows of parallel.halo_windows with isend/irecv, sums the unconverged-hood
-counters with all_reduce and allgathers the committed labels and the leaf
-partials of the last hood-energy row (each rank folds its own 1024-element
-leaves) per EM iteration; the M-step and EM total are the C oracle's
-(update_parameters, engine.cpp:193-223, with its folds distributed over the
-ranks as in partition.cu; dpp::reduce, kernels.hpp:124-139).
+counters with all_reduce and, per EM iteration, allgathers the leaf partials
+of the last hood-energy row (each rank folds its own 1024-element leaves)
+and runs the distributed M-step of partition.cu (label counts, head
+fragments and owned-leaf partials allgathered -- never the labels, which are
+gathered once at the end); the folds and the EM total are the C oracle's
+(update_parameters, engine.cpp:193-223; dpp::reduce, kernels.hpp:124-139).
 The result must equal the oracle's one-process optimize bit for bit, which
 checks the partition plan and the exchange schedule independently of CUDA.
 """
@@ -23,45 +24,69 @@ from oracle import C
 from paper_1809_05018_b200.parallel import halo_windows
 
 
-def _distributed_update(orc, mean, labels, mu, sigma, world, rank):
-    """update_parameters (engine.cpp:193-223) with the folds distributed as in
-    partition.cu: stable grouping by label on every rank, each rank folds an
-    equal chunk of the label-series leaves (fold_leaf), the partials are
-    allgathered, every rank runs fold_tree per label -- sum pass, then the
-    (x - mu)^2 pass."""
+def _distributed_update(orc, mean_own, lab_own, mu, sigma, world, rank):
+    """update_parameters (engine.cpp:193-223) distributed as in partition.cu
+    (k_part_count .. k_part_unpack_partials): no rank sees the others'
+    labels.  Every rank counts its own labels per label, the counts are
+    allgathered; rank r's vertices are label l's segment [off_r, off_r + n_r)
+    of the stable grouping x; a rank folds the 1024-element leaves that START
+    in its segments, reading the later ranks' head fragments (their first
+    elements up to the next leaf boundary, allgathered) where a leaf straddles;
+    the owned-leaf partials are allgathered and every rank runs fold_tree per
+    label -- sum pass, then the (x - mu)^2 pass."""
     M = len(mu)
-    R = len(mean)
-    order = np.argsort(labels, kind="stable")
-    counts = np.bincount(labels, minlength=M)
-    starts = np.concatenate([[0], np.cumsum(counts)])
-    x = mean[order]
-    leaves_of = [(int(n) + 1023) // 1024 for n in counts]
-    leaf_start = np.concatenate([[0], np.cumsum(leaves_of)]).astype(np.int64)
-    chunk = ((R + 1023) // 1024 + M + world - 1) // world
+    cnt = np.bincount(lab_own, minlength=M).astype(np.int64)
+    allcnt = _allgather(cnt, M, world).reshape(world, M)
+    n = allcnt.sum(axis=0)
+    off = np.concatenate([np.zeros((1, M), np.int64), np.cumsum(allcnt, axis=0)])  # [q][l]
+    seg = [mean_own[lab_own == l] for l in range(M)]  # (stable: vertex order)
+    head_len = lambda o, c: min(c, (1024 - o % 1024) % 1024)  # noqa: E731
+    heads = np.zeros(M * 1024)
+    for l in range(M):
+        h = head_len(int(off[rank][l]), int(cnt[l]))
+        heads[l * 1024:l * 1024 + h] = seg[l][:h]
+    all_heads = _allgather(heads, M * 1024, world).reshape(world, M, 1024)
+
+    def owned(q, l):  # leaves j with off_q <= 1024 j < off_q + n_q
+        o, c = int(off[q][l]), int(allcnt[q][l])
+        first = (o + 1023) // 1024
+        return range(first, (o + c + 1023) // 1024 if c else first)
+
+    cap = (len(mean_own) + 1023) // 1024 + M + 1
+    leaves_of = [(int(c) + 1023) // 1024 for c in n]
     mu, sigma = mu.copy(), sigma.copy()
     for sq in (False, True):
-        own = np.zeros(chunk)
-        for k in range(chunk):
-            leaf = rank * chunk + k
-            if leaf >= leaf_start[M]:
-                break
-            lbl = int(np.searchsorted(leaf_start, leaf, side="right") - 1)
-            b = starts[lbl] + (leaf - leaf_start[lbl]) * 1024
-            e = min(b + 1024, starts[lbl + 1])
-            seg = x[b:e]
-            if sq:
-                d = seg - mu[lbl]
-                seg = d * d
-            own[k] = orc.fold_range(seg)
-        parts = _allgather(own, chunk, world)
-        for lbl in range(M):
-            if counts[lbl] == 0:
+        own = np.zeros(cap)
+        k = 0
+        for l in range(M):
+            for j in owned(rank, l):
+                b = 1024 * j - int(off[rank][l])
+                vals = list(seg[l][b:b + 1024])
+                q = rank + 1
+                while len(vals) < 1024 and 1024 * j + len(vals) < n[l] and q < world:
+                    h = head_len(int(off[q][l]), int(allcnt[q][l]))
+                    vals += list(all_heads[q, l, :h])[:1024 - len(vals)]
+                    q += 1
+                v = np.asarray(vals)
+                if sq:
+                    d = v - mu[l]
+                    v = d * d
+                own[k] = orc.fold_range(v)
+                k += 1
+        gathered = _allgather(own, cap, world).reshape(world, cap)
+        for l in range(M):
+            if n[l] == 0:
                 continue  # empty labels keep their parameters (engine.cpp:209-211)
-            folded = orc.fold_tree(parts[leaf_start[lbl]:leaf_start[lbl + 1]])
+            parts = np.zeros(leaves_of[l])
+            for q in range(world):
+                base = sum(len(owned(q, ll)) for ll in range(l))
+                for i, j in enumerate(owned(q, l)):
+                    parts[j] = gathered[q][base + i]
+            folded = orc.fold_tree(parts)
             if not sq:
-                mu[lbl] = folded / float(counts[lbl])
+                mu[l] = folded / float(n[l])
             else:
-                sigma[lbl] = max(np.sqrt(folded / float(counts[lbl])), 1e-3)
+                sigma[l] = max(np.sqrt(folded / float(n[l])), 1e-3)
     return mu, sigma
 
 
@@ -167,9 +192,6 @@ def optimize_rank(graph, hoods, cfg, fixed_work=False):
             if not fixed_work and int(unconv.item()) == 0:
                 break
         cur = (cur + T) & 1
-        own_lab = np.zeros(plan.chunk_v, np.int64)
-        own_lab[:ve - vb] = lab[cur][vb:ve]
-        full_lab = _allgather(own_lab, plan.chunk_v, world)[:R]
         # the rank's hood-series leaves (its series range starts on a leaf
         # boundary) folded locally; only the leaf partials are exchanged
         chunk_l = plan.chunk_h // 1024
@@ -178,8 +200,8 @@ def optimize_rank(graph, hoods, cfg, fixed_work=False):
         for i in range((he - hb + 1023) // 1024):
             own_parts[i] = orc.fold_range(row_own[i * 1024:(i + 1) * 1024])
         parts = _allgather(own_parts, chunk_l, world)[:(Hs + 1023) // 1024]
-        lab[cur][:] = full_lab  # (every rank now holds all committed labels)
-        mu, sigma = _distributed_update(orc, mean, full_lab, mu, sigma, world, rank)
+        mu, sigma = _distributed_update(orc, mean[vb:ve], lab[cur][vb:ve], mu, sigma, world,
+                                        rank)
         total = orc.fold_tree(parts) if len(parts) else 0.0
         totals.append(total)
         em_T.append(T)
@@ -188,4 +210,8 @@ def optimize_rank(graph, hoods, cfg, fixed_work=False):
             abs(total - em_hist[-1 - i]) < tol for i in range(1, L + 1))
         if conv and not fixed_work:
             break
-    return lab[cur].astype(np.uint32), mu, sigma, totals, em_T
+    # the labels are gathered once, after the EM loop
+    own_lab = np.zeros(plan.chunk_v, np.int64)
+    own_lab[:ve - vb] = lab[cur][vb:ve]
+    full_lab = _allgather(own_lab, plan.chunk_v, world)[:R]
+    return full_lab.astype(np.uint32), mu, sigma, totals, em_T
