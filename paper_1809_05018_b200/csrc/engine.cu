@@ -286,7 +286,10 @@ constexpr int fused_min_blocks(int mt, int kh, int vp = 1) {
 // spills: 16384^2 662 vs 675 EM-it/s).
 constexpr bool kHoistMean = DPMRF_HOIST_MEAN != 0;
 constexpr int kWinRegs = 3;  // window rows held in registers (default L = 3)
-constexpr uint32_t kVertsPerThreadMin = 1u << 20;  // owned vertices for 2 per thread
+#ifndef DPMRF_VP2_MIN
+#define DPMRF_VP2_MIN (1u << 20)
+#endif
+constexpr uint32_t kVertsPerThreadMin = DPMRF_VP2_MIN;  // owned vertices for 2 per thread
 template <int MT, int K>
 __global__ void __launch_bounds__(kVtxThreads)
     k_vertex_packed(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,

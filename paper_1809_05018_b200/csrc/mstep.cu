@@ -484,6 +484,37 @@ __device__ __forceinline__ double fold_span(const double* v, uint32_t i, uint32_
   return acc;
 }
 
+// fold_span<true> with the squares of the next group computed while the
+// current group's dependent adds retire (the terms are independent of acc)
+__device__ __forceinline__ double fold_span_sq(const double* v, uint32_t i, uint32_t end,
+                                               double acc, double mu) {
+  auto term = [&](double x) {
+    const double d = __dsub_rn(x, mu);
+    return __dmul_rn(d, d);
+  };
+  constexpr int kG = 16;
+  double cur[kG], nxt[kG];
+  if (i + kG <= end) {
+#pragma unroll
+    for (int j = 0; j < kG; ++j) cur[j] = term(v[i + j]);
+    while (i + 2 * kG <= end) {
+#pragma unroll
+      for (int j = 0; j < kG; ++j) nxt[j] = v[i + kG + j];
+#pragma unroll
+      for (int j = 0; j < kG; ++j) {
+        acc = __dadd_rn(acc, cur[j]);
+        cur[j] = term(nxt[j]);
+      }
+      i += kG;
+    }
+#pragma unroll
+    for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, cur[j]);
+    i += kG;
+  }
+  for (; i < end; ++i) acc = __dadd_rn(acc, term(v[i]));
+  return acc;
+}
+
 // fold_leaf over a fetched row: the first half as soon as it lands, then the
 // rest.  len >= 1.
 template <bool kSq>
@@ -981,6 +1012,10 @@ __global__ void __launch_bounds__(kSqThreads) k_fold_sq(FoldArgs a) {
 constexpr int kClCtas = 8;
 constexpr int kClThreads = DPMRF_CL_THREADS;
 constexpr bool kClBlockSq = DPMRF_CL_BLOCKSQ != 0;
+#ifndef DPMRF_CL_SQPIPE
+#define DPMRF_CL_SQPIPE 1
+#endif
+constexpr bool kClSqPipe = DPMRF_CL_SQPIPE != 0;  // squares one group ahead of the adds
 constexpr uint32_t kClMaxPer = 24;  // staged label leaves per CTA
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -1116,7 +1151,8 @@ __global__ void __launch_bounds__(kClThreads) k_fold_sq_cluster(FoldArgs a, uint
         if (len_s[tid] > n0_s[tid] - off_s[tid]) mbar_wait0(&bar[tid][1]);
         const double mu = mu_s[tid];
         const double d0 = __dsub_rn(v[0], mu);
-        r = fold_span<true>(v, 1, len_s[tid], __dmul_rn(d0, d0), mu);
+        r = kClSqPipe ? fold_span_sq(v, 1, len_s[tid], __dmul_rn(d0, d0), mu)
+                      : fold_span<true>(v, 1, len_s[tid], __dmul_rn(d0, d0), mu);
       }
       st_cluster(&sqp[first + tid], 0, r);
     }
