@@ -1303,15 +1303,21 @@ __device__ void stream_tasks(const FoldArgs& a, const StreamView& v, double* rin
   auto task_span = [&](uint32_t t, const double*& src, uint32_t& len) -> uint32_t {
     return t < nsum ? v.span(false, t, src, len) : v.span(true, t - P, src, len);
   };
+  // the span of the task being fetched, cached across its quarters
+  uint32_t ct = 0xFFFFFFFFu, clen = 0;
+  const double* csrc = nullptr;
   auto issue = [&](uint32_t pos) {
     if (lane >= uint32_t(C)) return;
     const uint32_t k = pos >> 2, qq = pos & 3u;
     if (k >= rounds) return;
     const uint32_t t = gid + k * stride;
     if (t >= ntask || (t >= nsum && t < P)) return;
-    const double* src;
-    uint32_t len;
-    task_span(t, src, len);
+    if (t != ct) {
+      task_span(t, csrc, clen);
+      ct = t;
+    }
+    const double* src = csrc;
+    const uint32_t len = clen;
     if (qq * kQuarter >= len) return;
     const double* s0 = src + qq * kQuarter;
     const uint32_t n = min(kQuarter, len - qq * kQuarter);
@@ -1356,9 +1362,9 @@ __device__ void stream_tasks(const FoldArgs& a, const StreamView& v, double* rin
         if (sq) {
           if (qq == 0) {
             const double d = __dsub_rn(w[0], mu);
-            acc = fold_span<true>(w, 1, n, __dmul_rn(d, d), mu);
+            acc = fold_span_sq(w, 1, n, __dmul_rn(d, d), mu);
           } else {
-            acc = fold_span<true>(w, 0, n, acc, mu);
+            acc = fold_span_sq(w, 0, n, acc, mu);
           }
         } else {
           acc = fold_span<false>(w, qq == 0 ? 1 : 0, n, qq == 0 ? w[0] : acc, 0.0);

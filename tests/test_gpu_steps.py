@@ -138,3 +138,24 @@ def test_update_parameters_long_series(orc, R, frac0):
         c.close()
     mu, sg = orc.update_parameters(mean, labels, prev.mu, prev.sigma)
     assert np.array_equal(got.mu, mu) and np.array_equal(got.sigma, sg)
+
+
+@pytest.mark.parametrize("R,used", [(1_500_000, [1, 3]), (400_000, [0, 4]), (3_000, [2])])
+def test_update_parameters_empty_labels_every_fold_path(orc, R, used):
+    """M = 5 with only some labels populated, on the three fold paths of the
+    M-step (R = 1.5 M: the persistent streaming kernel; 400 k: the two-grid
+    folds; 3 k: the one-cluster sq pass): the populated labels' mu / sigma
+    equal the reference's folds, the empty ones keep their parameters
+    (engine.cpp:209-220)."""
+    rng = np.random.default_rng(R)
+    mean = rng.random(R) * 255.0
+    labels = rng.choice(np.array(used, np.uint32), R)
+    c = E.Context(0)
+    try:
+        c.set_graph(E.RegionGraph(np.zeros(R + 1, np.uint32), np.zeros(0, np.uint32), mean))
+        prev = E.LabelParams(np.arange(5, dtype=np.float64) + 7.5, np.arange(5, dtype=np.float64) + 1)
+        got = c.update_parameters(labels, prev)
+    finally:
+        c.close()
+    mu, sg = orc.update_parameters(mean, labels, prev.mu, prev.sigma)
+    assert np.array_equal(got.mu, mu) and np.array_equal(got.sigma, sg)
