@@ -264,11 +264,13 @@ __global__ void k_compact_offsets(const uint32_t* __restrict__ h_off, uint64_t H
 namespace {
 // The 2-label, <= 8-slot instance fits 32 registers without spilling, so it
 // runs 8 blocks per SM.
-// The config C instance (5 labels, <= 16 slots) at 5 blocks per SM: 48
-// registers, an 8-byte spill, +2.5% over the compiler's 56 (6 or 8 blocks
-// spill more and lose 4-8%); the other wide instances keep the compiler's choice.
+// The config C instances (5 labels) at 8 blocks per SM: 32 registers and a
+// 40-byte spill, one wave of 2048 threads per SM (2560^2 brick: 12.8 k vs
+// 12.5 k EM-it/s at 5 blocks / 48 registers, 12.4 k at 6 / 40; before the
+// round-2 instruction diet 5 blocks won); the other wide instances keep the
+// compiler's choice.
 #ifndef DPMRF_FUSED_MINB_M5
-#define DPMRF_FUSED_MINB_M5 5
+#define DPMRF_FUSED_MINB_M5 8
 #endif
 #ifndef DPMRF_FUSED_MINB_VP2
 #define DPMRF_FUSED_MINB_VP2 8
