@@ -384,9 +384,11 @@ def run_slice(args, E, torch, d: Dist):
     labels_out = np.zeros(R, np.uint32)
     fixed, ml = c["fixed"], M != 2
 
+    act = getattr(args, "active_set", False)
+
     def step(timing=False):
         return ctx.optimize(cfg, fixed_work=fixed, multilabel=ml, trace_level=E.TRACE_NONE,
-                            kernel_timing=timing, labels_out=labels_out)
+                            kernel_timing=timing, labels_out=labels_out, active_set=act)
 
     for _ in range(args.warmup):  # the timed configuration (graphs captured here, not timed)
         step()
@@ -432,7 +434,8 @@ def run_slice(args, E, torch, d: Dist):
     def e2e_leg(trace_level, sink=None, n=max(3, args.steps)):
         call = lambda: ctx.optimize_arrays(g_pin, h_pin, cfg, fixed_work=fixed,  # noqa: E731
                                            multilabel=ml, trace_level=trace_level,
-                                           labels_out=lab_pin, trace_sink=sink)
+                                           labels_out=lab_pin, trace_sink=sink,
+                                           active_set=act)
         for _ in range(args.warmup):  # untimed, like the device leg's warm-up
             call()
         d.barrier()
@@ -483,6 +486,10 @@ def run_slice(args, E, torch, d: Dist):
                    "em_iters_per_step": ems / args.steps, "map_iters_per_step": maps / args.steps,
                    "l2": "flushed between timed steps (256 MiB write)",
                    "parallelism": f"slice-sharded x{d.world} (no data-path collective)",
+                   "map_loop": ("active set (extension, --active-set: only items whose inputs "
+                                "changed are re-evaluated; identical results, less than the "
+                                "reference's per-iteration work)") if act else
+                               "dense (every vertex and hood, every MAP iteration)",
                    "timing": "CUDA events on the library stream around each optimize(); "
                              "max over ranks"},
         "vertex_label_evals_per_s": d.sum(M * S * maps) / total_dev_s,
@@ -734,7 +741,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--active-set", action="store_true",
+                    help="the active-set MAP loop (extension, DPMRF_RUN_ACTIVE_SET): same "
+                         "results, re-evaluates only what changed -- not the reference's "
+                         "per-iteration work, so never the headline line")
     args = ap.parse_args()
+    if os.environ.get("DPMRF_BENCH_ACTIVE") == "1":  # (tools/ab.sh variants)
+        args.active_set = True
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

@@ -74,10 +74,17 @@ enum {
   DPMRF_RUN_UNFUSED = 512u,     /* separate vertex and hood kernels per MAP iteration; default
                                    (packed layouts): map_max + 1 launches per EM iteration, each
                                    running the hood pass of t-1 with the vertex pass of t */
-  DPMRF_RUN_HOST_LOG = 128u     /* host round trip per EM iteration (log(sigma) on the host);
+  DPMRF_RUN_HOST_LOG = 128u,    /* host round trip per EM iteration (log(sigma) on the host);
                                    default: EM iterations run back to back on the device with a
                                    correctly rounded device log, verified against the host libm
                                    afterwards (rerun with host logs on any difference) */
+  DPMRF_RUN_ACTIVE_SET = 1024u  /* extension, opt-in: from the third MAP iteration of an EM on,
+                                   re-evaluate only the vertices whose inputs changed (a
+                                   neighbor's label) and fold only the hoods whose members'
+                                   minima changed or whose window is still open; bit-identical
+                                   results, but less than the reference's per-iteration work.
+                                   Fused layouts of the grid (M=2) and brick (M=5) graphs, trace
+                                   levels NONE / EM, one device; ignored otherwise */
 };
 
 typedef struct dpmrf_run_options {
@@ -99,7 +106,7 @@ typedef struct dpmrf_run_stats {
   uint64_t series;           /* hood-energy series length (nonempty hoods) */
   double map_loop_ms;        /* fused MAP launches (events around each EM's chain of them) */
   uint64_t map_loop_launches;
-  int32_t reserved0;         /* always 0 */
+  int32_t active_set;        /* 1: the active-set MAP loop ran (DPMRF_RUN_ACTIVE_SET) */
   int32_t graphs;            /* 1: EM iterations replayed from CUDA graphs */
   int32_t device_loop;       /* 1: the result came from the device-resident EM loop */
   uint32_t device_log_fallbacks; /* reruns because a device log(sigma) differed from the host's */

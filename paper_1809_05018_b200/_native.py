@@ -45,7 +45,7 @@ class CRunStats(ct.Structure):
                 ("mstep_ms", F64), ("vertex_launches", U64), ("hood_launches", U64),
                 ("kernel_launches", U64), ("em_iters", I32), ("map_iters_total", I32),
                 ("series", U64), ("map_loop_ms", F64), ("map_loop_launches", U64),
-                ("reserved0", I32), ("graphs", I32), ("device_loop", I32),
+                ("active_set", I32), ("graphs", I32), ("device_loop", I32),
                 ("device_log_fallbacks", U32)]
 
 

@@ -637,6 +637,28 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     a.hist = ctx->hist.ensure(uint64_t(a.ring) * Hs + 2);  // (+2: aligned leaf fetches)
     a.flags = full ? ctx->flags.ensure(uint64_t(map_max) * Hs) : nullptr;
     a.eq = a.hood_k ? ctx->hood_eq.ensure(Hs) : nullptr;  // (packed hood pass only)
+    // active-set MAP loop (opt-in extension; include/dpmrf_cuda.h)
+    const bool active = (o.flags & DPMRF_RUN_ACTIVE_SET) && fused && !full && Hs > 0 &&
+                        map_active_supported(a);
+    if (active) {
+      const uint64_t Rp = (uint64_t(R) + 15) & ~15ull, Hp = (Hs + 15) & ~15ull;  // 16-B rows
+      a.act_vflag = ctx->act_vflag.ensure(2 * Rp);
+      a.act_hflag = ctx->act_hflag.ensure(2 * Hp);
+      a.act_hval = ctx->act_hval.ensure(Hs + 2);  // (+2: aligned leaf fetches in the M-step)
+      a.act_lastp = ctx->act_lastp.ensure(Hs);
+      if (ctx->inv_gen != ctx->generation) {
+        const uint32_t* so = ctx->series_alias ? ctx->h_off.get() : ctx->s_off_buf.get();
+        build_vertex_series(so, ctx->h_mem.get(), Hs, R, ctx->S, ctx->inv_off.ensure(uint64_t(R) + 1),
+                            ctx->inv_ser.ensure(ctx->S ? ctx->S : 1), ctx->inv_cursor.ensure(R ? R : 1),
+                            ctx->scan, st);
+        CK(cudaMemsetAsync(a.act_vflag, 0, 2 * Rp, st));  // (padding bytes stay 0)
+        CK(cudaMemsetAsync(a.act_hflag, 0, 2 * Hp, st));
+        ctx->inv_gen = ctx->generation;
+      }
+      a.inv_off = ctx->inv_off.get();
+      a.inv_ser = ctx->inv_ser.get();
+    }
+    ctx->stats.active_set = active ? 1 : 0;
     // [em_done, pending_done, em_count, pad | per-MAP-iteration counters]
     uint32_t* state = ctx->unconv.ensure(uint64_t(map_max) + 4);
     a.unconv = state + 4;
@@ -748,7 +770,9 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
                            st));
       }
       record(ev++);
-      launch_mstep(a.mean, R, M, lab[parity], lab[parity ^ 1], a.hist, Hs, a.ring, a.unconv,
+      // (active set: the latest sum of every series, not the last ring row)
+      launch_mstep(a.mean, R, M, lab[parity], lab[parity ^ 1], active ? a.act_hval : a.hist, Hs,
+                   active ? 1 : a.ring, a.unconv,
                    map_max, fixed, params, em_out, ctx->ms, st, &k, /*counts_ready=*/true,
                    /*scattered=*/merged, merged ? &ep : nullptr);
       record(ev++);
@@ -808,7 +832,9 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       key.p2[2] = a.adj_pk;
       key.p2[3] = a.hood_pk;
       key.p2[4] = a.hood_base;
-      key.layout = a.adj_k * 100 + a.hood_k;
+      key.layout = a.adj_k * 100 + a.hood_k + (active ? 100000 : 0);
+      key.p2[5] = a.act_vflag;
+      key.p2[6] = a.act_hval;
       if (!ctx->graph_valid || std::memcmp(&key, &ctx->graph_key, sizeof key) != 0) {
         ctx->drop_graphs();
         for (int parity = 0; parity < (device_loop ? 1 : 2); ++parity) {

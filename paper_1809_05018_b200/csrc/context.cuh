@@ -65,6 +65,12 @@ struct dpmrf_context {
   dpmrf_b200::DevBuf<uint8_t> lab[2];
   dpmrf_b200::DevBuf<double> minE, hist, terms, params, em_out;
   dpmrf_b200::DevBuf<uint8_t> flags, hood_eq;
+  // active-set MAP loop (DPMRF_RUN_ACTIVE_SET): flags, latest series sums,
+  // last-folded iterations, and the vertex -> series index (per generation)
+  dpmrf_b200::DevBuf<uint8_t> act_vflag, act_hflag, act_lastp;
+  dpmrf_b200::DevBuf<double> act_hval;
+  dpmrf_b200::DevBuf<uint32_t> inv_off, inv_ser, inv_cursor;
+  uint64_t inv_gen = ~0ull;
   dpmrf_b200::DevBuf<uint32_t> unconv, labels32;
   dpmrf_b200::MStepBuffers ms;
   dpmrf_b200::ScanWorkspace scan;

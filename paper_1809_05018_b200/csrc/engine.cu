@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "engine_dev.cuh"
+#include "scan.cuh"
 
 namespace dpmrf_b200 {
 
@@ -275,9 +276,13 @@ namespace {
 #ifndef DPMRF_FUSED_MINB_VP2
 #define DPMRF_FUSED_MINB_VP2 8
 #endif
-constexpr int fused_min_blocks(int mt, int kh, int vp = 1) {
-  return mt == 2 && kh == 8 ? (vp == 2 ? DPMRF_FUSED_MINB_VP2 : DPMRF_FUSED_MINB)
-                            : (mt == 5 ? DPMRF_FUSED_MINB_M5 : 1);
+#ifndef DPMRF_ACT_MINB
+#define DPMRF_ACT_MINB 8
+#endif
+constexpr int fused_min_blocks(int mt, int kh, int vp = 1, bool act = false) {
+  return act ? DPMRF_ACT_MINB
+             : (mt == 2 && kh == 8 ? (vp == 2 ? DPMRF_FUSED_MINB_VP2 : DPMRF_FUSED_MINB)
+                                   : (mt == 5 ? DPMRF_FUSED_MINB_M5 : 1));
 }
 #ifndef DPMRF_HOIST_MEAN
 #define DPMRF_HOIST_MEAN 0
@@ -288,6 +293,14 @@ constexpr int fused_min_blocks(int mt, int kh, int vp = 1) {
 // spills: 16384^2 662 vs 675 EM-it/s).
 constexpr bool kHoistMean = DPMRF_HOIST_MEAN != 0;
 constexpr int kWinRegs = 3;  // window rows held in registers (default L = 3)
+constexpr uint32_t kSpan = 16;  // items per thread in the active-set sparse passes
+#ifdef DPMRF_PROBE
+// processed vertices / series per MAP iteration in active-set runs (probe builds)
+__device__ unsigned long long g_act_probe[2][64];
+#define ACT_PROBE(k, t) atomicAdd(&g_act_probe[k][(t) & 63], 1ull)
+#else
+#define ACT_PROBE(k, t) do {} while (0)
+#endif
 #ifndef DPMRF_VP2_MIN
 #define DPMRF_VP2_MIN (1u << 20)
 #endif
@@ -298,8 +311,8 @@ __global__ void __launch_bounds__(kVtxThreads)
                     int t);
 template <int K>
 __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t);
-template <int MT, int KV, int KH, int VP>
-__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
+template <int MT, int KV, int KH, int VP, bool kAct = false>
+__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP, kAct))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
                 uint32_t nh, uint32_t nv, ScatterArgs sc);
@@ -307,6 +320,14 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
 
 
 bool map_fused_supported(const MapArgs& a) { return a.adj_k && a.hood_k; }
+
+// The fused layouts with an active-set instance: the grid graphs with two
+// labels (configs A, B, D, E) and the brick graphs with five (config C).
+bool map_active_supported(const MapArgs& a) {
+  if (!map_fused_supported(a)) return false;
+  if (a.hood_k == 12) return a.M == 5 && a.adj_k == 8;
+  return a.M == 2 && a.adj_k == 4 && a.hood_k == 8;
+}
 
 namespace {
 // The launch's copy of the arguments with the ring rows of hood iteration th.
@@ -345,6 +366,23 @@ void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
   // fixed work: only the last vertex pass's label counts are ever read (by
   // the M-step's grouping), so the other passes skip their block counts
   if (a.fixed && t != map_max - 1) ar.tile_counts = nullptr;
+  if (a.act_vflag) {  // active-set instances (map_active_supported)
+    // sparse passes: one thread per kSpan items (see vertex_sparse_body)
+    const bool sh = t - 1 > a.L, sv = t >= 2 && !ar.tile_counts;
+    const uint32_t nh2 = t >= 1 ? grid_for(a.h_end - a.h_begin,
+                                           uint64_t(kHoodThreads) * (sh ? kSpan : 1)) : 0u;
+    const uint32_t nv2 = t < map_max ? grid_for(a.v_end - a.v_begin,
+                                                uint64_t(kVtxThreads) * (sv ? kSpan : vp)) : 0u;
+    const dim3 g2(nh2 + nv2 + ns);
+#define MFA(MT, KV, KH, VP)                                                                 \
+  launch_pdl(k_map_fused<MT, KV, KH, VP, true>, g2, blk, smem, s, ar, lab_in, lab_out,       \
+             minE_prev, minE_cur, t, nh2, nv2, scv)
+    if (k12) MFA(5, 8, 12, 1);
+    else if (vp == 2) MFA(2, 4, 8, 2);
+    else MFA(2, 4, 8, 1);
+#undef MFA
+    return;
+  }
 #define MF4(MT, KV, KH, VP)                                                              \
   launch_pdl(k_map_fused<MT, KV, KH, VP>, g, blk, smem, s, ar, lab_in, lab_out, minE_prev,  \
              minE_cur, t, nh, nv, scv)
@@ -461,32 +499,123 @@ __device__ __forceinline__ void load_i16(const int16_t* __restrict__ p, int16_t 
 // overlap the predecessor's drain -- and the skip decision (the previous
 // iteration's unconverged counter) is read beside the first dependent loads
 // rather than ahead of them: one memory round trip less per launch.
-template <int MT, int K, int P = 1>
+// Energies of every label (label_energy, model.hpp:66-72, in that order) and
+// the argmin with ties to the smaller label (engine.cpp:115-145: strict <).
+template <int MT, int K>
+__device__ __forceinline__ void vertex_argmin_packed(const MapArgs& a, uint32_t M, double x,
+                                                     const uint8_t (&nb)[K], uint32_t deg,
+                                                     double& best, uint32_t& best_l) {
+  const double* T = a.terms;
+  if constexpr (MT == 2) {
+    uint32_t ones = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) ones += (nb[k] == 1);
+    const double e0 = label_energy(x, T[0], T[2], T[4], a.beta, ones);
+    const double e1 = label_energy(x, T[1], T[3], T[5], a.beta, deg - ones);
+    best = e0;
+    best_l = 0;
+    if (e1 < best) {
+      best = e1;
+      best_l = 1;
+    }
+  } else {
+    best = 0.0;
+    best_l = 0;
+    for (uint32_t l = 0; l < M; ++l) {
+      uint32_t same = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) same += (nb[k] == l);
+      const double e = label_energy(x, T[l], T[M + l], T[2 * M + l], a.beta, deg - same);
+      if (l == 0 || e < best) {
+        best = e;
+        best_l = l;
+      }
+    }
+  }
+}
+
+// Active-set flag slices (rows padded to 16 bytes: the sparse passes read
+// 16 flags per thread with one vector load).
+__device__ __forceinline__ uint64_t act_vpitch(const MapArgs& a) { return (uint64_t(a.R) + 15) & ~15ull; }
+__device__ __forceinline__ uint64_t act_hpitch(const MapArgs& a) { return (a.Hs + 15) & ~15ull; }
+__device__ __forceinline__ uint8_t* act_vflags(const MapArgs& a, int t) {
+  return a.act_vflag + uint64_t(t & 1) * act_vpitch(a);
+}
+__device__ __forceinline__ uint8_t* act_hflags(const MapArgs& a, int t) {
+  return a.act_hflag + uint64_t(t & 1) * act_hpitch(a);
+}
+
+// After vertex v of iteration t (t >= 1) computed (best, best_l) from its
+// old label: who is evaluated next.  A new label re-evaluates the neighbors
+// (their discord counts) and v (the label double buffer); a new minimum v
+// (the minima double buffer) and -- once the hood pass is flag-driven
+// (t > L) -- every series v is in.
+template <int K>
+__device__ __forceinline__ void act_mark(const MapArgs& a, int t, uint32_t v, const int16_t (&d)[K],
+                                         uint32_t old, uint32_t best_l, double best,
+                                         double prev) {
+  uint8_t* vnext = act_vflags(a, t + 1);
+  const bool lab_changed = best_l != old;
+  const bool min_changed = __double_as_longlong(prev) != __double_as_longlong(best);
+  if (lab_changed || min_changed) vnext[v] = 1;
+  if (lab_changed) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (d[k] != INT16_MIN) vnext[v + static_cast<uint32_t>(static_cast<int32_t>(d[k]))] = 1;
+  }
+  if (min_changed && t > a.L) {
+    uint8_t* hmark = act_hflags(a, t);
+    for (uint32_t i = a.inv_off[v]; i < a.inv_off[v + 1]; ++i) hmark[a.inv_ser[i]] = 1;
+  }
+}
+
+template <int MT, int K, int P = 1, bool kAct = false>
 __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
                                                    const uint8_t* __restrict__ lab_in,
                                                    uint8_t* __restrict__ lab_out,
                                                    double* __restrict__ minE, int t,
-                                                   uint32_t blk, int skip_t) {
+                                                   uint32_t blk, int skip_t,
+                                                   const double* __restrict__ minE_prev = nullptr) {
   const uint32_t M = MT > 0 ? uint32_t(MT) : a.M;
   const uint32_t v0 = a.v_begin + blk * (kVtxThreads * P) + threadIdx.x;
+  // active-set (a.act_vflag): iterations 0 and 1 evaluate every vertex (new
+  // label terms; the minima double buffer is stale from the last EM), later
+  // ones only the flagged vertices, whose structure is read once the flag
+  // is known
+  constexpr bool act = kAct;
+  const bool sparse = act && t >= 2;
   int16_t d[P][K];
-  uint8_t old[P], cov[P];
+  uint8_t old[P], cov[P], run[P];
   double xs[P];
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     const uint32_t v = v0 + j * kVtxThreads;
     xs[j] = 0.0;
-    if (v < a.v_end) {
+    run[j] = 1;
+    if (v < a.v_end && !sparse) {
       load_i16<K>(a.adj_pk + uint64_t(v) * K, d[j]);
       cov[j] = a.cover[v];
       if (kHoistMean || P == 1) xs[j] = a.mean[v];
     }
   }
   pdl_wait();
+  uint8_t* vcur = act ? act_vflags(a, t) : nullptr;
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     const uint32_t v = v0 + j * kVtxThreads;
-    if (v < a.v_end) old[j] = lab_in[v];
+    if (v < a.v_end) {
+      if (act) {
+        run[j] = !sparse || vcur[v];
+        if (run[j]) vcur[v] = 0;
+        if (sparse && run[j]) {
+          load_i16<K>(a.adj_pk + uint64_t(v) * K, d[j]);
+          cov[j] = a.cover[v];
+          if (kHoistMean || P == 1) xs[j] = a.mean[v];
+        }
+      }
+      // (a vertex not re-evaluated keeps its label: the output buffer holds it)
+      old[j] = run[j] ? lab_in[v] : lab_out[v];
+    }
   }
   if (map_iter_skipped(a.unconv, skip_t, a.fixed)) return;  // uniform over the grid
   uint32_t nl[P];
@@ -495,6 +624,10 @@ __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
     const uint32_t v = v0 + j * kVtxThreads;
     nl[j] = 0;
     if (v >= a.v_end) continue;
+    if (!run[j]) {
+      nl[j] = old[j];
+      continue;
+    }
     if (!cov[j]) {
       lab_out[v] = old[j];
       nl[j] = old[j];
@@ -511,38 +644,13 @@ __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
                  : uint8_t(0xFF);
     }
     const double x = kHoistMean || P == 1 ? xs[j] : a.mean[v];
-    const double* T = a.terms;
     double best;
     uint32_t best_l;
-    if constexpr (MT == 2) {
-      uint32_t ones = 0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) ones += (nb[k] == 1);
-      const double e0 = label_energy(x, T[0], T[2], T[4], a.beta, ones);
-      const double e1 = label_energy(x, T[1], T[3], T[5], a.beta, deg - ones);
-      best = e0;
-      best_l = 0;
-      if (e1 < best) {
-        best = e1;
-        best_l = 1;
-      }
-    } else {
-      best = 0.0;
-      best_l = 0;
-      for (uint32_t l = 0; l < M; ++l) {
-        uint32_t same = 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) same += (nb[k] == l);
-        const double e = label_energy(x, T[l], T[M + l], T[2 * M + l], a.beta, deg - same);
-        if (l == 0 || e < best) {
-          best = e;
-          best_l = l;
-        }
-      }
-    }
+    vertex_argmin_packed<MT, K>(a, M, x, nb, deg, best, best_l);
     minE[v] = best;
     lab_out[v] = static_cast<uint8_t>(best_l);
     nl[j] = best_l;
+    if (kAct && t >= 1) act_mark<K>(a, t, v, d[j], old[j], best_l, best, minE_prev[v]);
   }
   if (a.tile_counts) {
 #pragma unroll
@@ -598,7 +706,9 @@ __device__ __forceinline__ void load_hood_row(const uint16_t* __restrict__ row,
 // hood index stays 32-bit (one wide multiply-add per address).
 template <int K>
 __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restrict__ minE, int t,
-                                         uint32_t h, uint32_t base, const uint32_t (&u)[K / 2]) {
+                                         uint32_t h, uint32_t base, const uint32_t (&u)[K / 2],
+                                         const double* p1_over = nullptr,
+                                         double* sum_out = nullptr, uint32_t* eq_out = nullptr) {
   const int R1 = a.ring;
   const int nwin = t >= a.L ? a.L : 0;
   double* __restrict__ row_t = a.hist + uint64_t(a.row_t) * a.Hs;
@@ -615,7 +725,7 @@ __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restr
   double p1 = 0.0;
   uint32_t e1 = 0;
   if (t >= 1) {
-    p1 = row_p[h];
+    p1 = p1_over ? *p1_over : row_p[h];
     e1 = a.eq[h];
   }
   double e[K];
@@ -635,7 +745,10 @@ __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restr
   row_t[h] = sum;
   int ok = nwin > 0;
   const bool same = t >= 1 && sum == p1;  // (false for NaN)
-  a.eq[h] = static_cast<uint8_t>(same ? min(e1 + 1u, 255u) : 0u);
+  const uint32_t eq_new = same ? min(e1 + 1u, 255u) : 0u;
+  a.eq[h] = static_cast<uint8_t>(eq_new);
+  if (sum_out) *sum_out = sum;
+  if (eq_out) *eq_out = eq_new;
   if (nwin) {
     if (!(fabs(__dsub_rn(sum, p1)) < a.tol)) {
       ok = 0;
@@ -659,16 +772,20 @@ __device__ __forceinline__ int hood_eval(const MapArgs& a, const double* __restr
 
 // (static structure before griddepcontrol.wait, skip decision beside the
 // first dependent loads -- see vertex_packed_body)
-template <int K>
+template <int K, bool kAct = false>
 __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
                                                  const double* __restrict__ minE, int t,
                                                  uint32_t blk, int skip_t) {
   static_assert(K == 8 || K == 12 || K == 16, "hood pack width");
   const uint32_t h = static_cast<uint32_t>(a.h_begin) + blk * kHoodThreads + threadIdx.x;
   const bool live = h < a.h_end;
+  // active-set, after the window opened (t > L): only flagged series fold,
+  // and their structure is read once the flag is known
+  constexpr bool act = kAct;
+  const bool sparse = act && t > a.L;
   uint32_t base = 0;
   uint32_t u[K / 2];
-  if (live) {
+  if (live && !sparse) {
     base = a.hood_base[h];
     load_hood_row<K>(a.hood_pk + uint64_t(h) * K, u);
   }
@@ -676,11 +793,149 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
   int not_conv = 0;
   if (live) {
     if (map_iter_skipped(a.unconv, skip_t, a.fixed)) return;  // uniform over the grid
-    not_conv = hood_eval<K>(a, minE, t, h, base, u);
+    if constexpr (!act) {
+      not_conv = hood_eval<K>(a, minE, t, h, base, u);
+    } else {
+      uint8_t* flag = act_hflags(a, t) + h;
+      const bool run = !sparse || *flag;
+      if (run) {
+        *flag = 0;
+        double over = 0.0;
+        const double* p1o = nullptr;
+        if (sparse) {
+          base = a.hood_base[h];
+          load_hood_row<K>(a.hood_pk + uint64_t(h) * K, u);
+          if (a.act_lastp[h] != uint8_t(t - 1)) {
+            // folded again after converged iterations: every window row
+            // since equals its last sum (their ring slots are stale)
+            over = a.act_hval[h];
+            p1o = &over;
+            int row = a.row_p;
+            for (int i = 0; i < a.L; ++i) {
+              a.hist[uint64_t(row) * a.Hs + h] = over;
+              row = row == 0 ? a.ring - 1 : row - 1;
+            }
+          }
+        }
+        double sum;
+        uint32_t eqn;
+        not_conv = hood_eval<K>(a, minE, t, h, base, u, p1o, &sum, &eqn);
+        a.act_hval[h] = sum;
+        a.act_lastp[h] = static_cast<uint8_t>(t);
+        // still open (not converged, or converged on a run shorter than the
+        // window): fold again in the next iteration
+        if (t + 1 > a.L && (not_conv || eqn < uint32_t(a.L)))
+          act_hflags(a, t + 1)[h] = 1;
+      }
+    }
   }
   if (!live && map_iter_skipped(a.unconv, skip_t, a.fixed)) return;
   const int bu = __syncthreads_count(not_conv);
   if (threadIdx.x == 0 && bu) atomicAdd(&a.unconv[t], uint32_t(bu));
+}
+
+// ---- active-set sparse passes (t >= 2 vertices, t > L series) ----
+// One thread per 16 consecutive items: a 16-byte load of their flags, and
+// only the flagged ones are evaluated (grids 16x smaller than the dense
+// passes, so launching blocks of mostly idle threads costs nothing).
+template <int MT, int K>
+__device__ __forceinline__ void vertex_sparse_body(const MapArgs& a,
+                                                   const uint8_t* __restrict__ lab_in,
+                                                   uint8_t* __restrict__ lab_out,
+                                                   double* __restrict__ minE,
+                                                   const double* __restrict__ minE_prev, int t,
+                                                   uint32_t blk, int skip_t) {
+  const uint32_t M = MT > 0 ? uint32_t(MT) : a.M;
+  const uint32_t v0 = a.v_begin + (blk * kVtxThreads + threadIdx.x) * kSpan;
+  pdl_wait();
+  if (map_iter_skipped(a.unconv, skip_t, a.fixed)) return;  // uniform over the grid
+  if (v0 >= a.v_end) return;
+  uint8_t* vcur = act_vflags(a, t);
+  const uint4 f4 = *reinterpret_cast<const uint4*>(vcur + v0);
+  if ((f4.x | f4.y | f4.z | f4.w) == 0) return;
+  const uint32_t w[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll 1
+  for (uint32_t i = 0; i < kSpan; ++i) {
+    if (((w[i >> 2] >> (8 * (i & 3))) & 0xFFu) == 0) continue;
+    const uint32_t v = v0 + i;
+    vcur[v] = 0;
+    ACT_PROBE(0, t);
+    int16_t d[K];
+    load_i16<K>(a.adj_pk + uint64_t(v) * K, d);
+    const uint8_t old = lab_in[v];
+    if (!a.cover[v]) {
+      lab_out[v] = old;
+      continue;
+    }
+    uint8_t nb[K];
+    uint32_t deg = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool ok = d[k] != INT16_MIN;
+      deg += ok;
+      nb[k] = ok ? lab_in[v + static_cast<uint32_t>(static_cast<int32_t>(d[k]))] : uint8_t(0xFF);
+    }
+    double best;
+    uint32_t best_l;
+    vertex_argmin_packed<MT, K>(a, M, a.mean[v], nb, deg, best, best_l);
+    minE[v] = best;
+    lab_out[v] = static_cast<uint8_t>(best_l);
+    act_mark<K>(a, t, v, d, old, best_l, best, minE_prev[v]);
+  }
+}
+
+// one flagged series of a sparse pass (t > L); returns 1 when not converged
+template <int K>
+__device__ __forceinline__ int hood_active_item(const MapArgs& a, const double* __restrict__ minE,
+                                                int t, uint32_t h) {
+  act_hflags(a, t)[h] = 0;
+  ACT_PROBE(1, t);
+  const uint32_t base = a.hood_base[h];
+  uint32_t u[K / 2];
+  load_hood_row<K>(a.hood_pk + uint64_t(h) * K, u);
+  double over = 0.0;
+  const double* p1o = nullptr;
+  if (a.act_lastp[h] != uint8_t(t - 1)) {
+    // folded again after converged iterations: every window row since
+    // equals its last sum (their ring slots are stale)
+    over = a.act_hval[h];
+    p1o = &over;
+    int row = a.row_p;
+    for (int i = 0; i < a.L; ++i) {
+      a.hist[uint64_t(row) * a.Hs + h] = over;
+      row = row == 0 ? a.ring - 1 : row - 1;
+    }
+  }
+  double sum;
+  uint32_t eqn;
+  const int nc = hood_eval<K>(a, minE, t, h, base, u, p1o, &sum, &eqn);
+  a.act_hval[h] = sum;
+  a.act_lastp[h] = static_cast<uint8_t>(t);
+  // still open (not converged, or converged on a run shorter than the
+  // window): fold again in the next iteration
+  if (nc || eqn < uint32_t(a.L)) act_hflags(a, t + 1)[h] = 1;
+  return nc;
+}
+
+template <int K>
+__device__ __forceinline__ void hood_sparse_body(const MapArgs& a, const double* __restrict__ minE,
+                                                 int t, uint32_t blk, int skip_t) {
+  const uint32_t h0 = static_cast<uint32_t>(a.h_begin) + (blk * kHoodThreads + threadIdx.x) * kSpan;
+  pdl_wait();
+  if (map_iter_skipped(a.unconv, skip_t, a.fixed)) return;  // uniform over the grid
+  int cnt = 0;
+  if (h0 < a.h_end) {
+    const uint4 f4 = *reinterpret_cast<const uint4*>(act_hflags(a, t) + h0);
+    if ((f4.x | f4.y | f4.z | f4.w) != 0) {
+      const uint32_t w[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll 1
+      for (uint32_t i = 0; i < kSpan; ++i)
+        if ((w[i >> 2] >> (8 * (i & 3))) & 0xFFu) cnt += hood_active_item<K>(a, minE, t, h0 + i);
+    }
+  }
+  // unconverged series of this iteration (the early exit, optimize.cpp:59)
+  const int wsum = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&a.unconv[t], uint32_t(wsum));
 }
 
 template <int K>
@@ -696,8 +951,8 @@ __global__ void __launch_bounds__(kHoodThreads) k_hood_packed(MapArgs a, int t) 
 // iteration, the speculative pass only wrote buffers nothing reads any more
 // (labels into the buffer t-1 consumed, minima into the other half of the
 // double-buffered minima, label counts into the other parity slot).
-template <int MT, int KV, int KH, int VP>
-__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
+template <int MT, int KV, int KH, int VP, bool kAct>
+__global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP, kAct))
     k_map_fused(MapArgs a, const uint8_t* __restrict__ lab_in, uint8_t* __restrict__ lab_out,
                 const double* __restrict__ minE_prev, double* __restrict__ minE_cur, int t,
                 uint32_t nh, uint32_t nv, ScatterArgs sc) {
@@ -705,7 +960,10 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
   static_assert(kVtxThreads == kTileThreads, "scatter tiles are vertex blocks");
   extern __shared__ uint32_t fused_smem[];
   if (blockIdx.x < nh) {
-    hood_packed_body<KH>(a, minE_prev, t - 1, blockIdx.x, t - 1);
+    if (kAct && t - 1 > a.L)
+      hood_sparse_body<KH>(a, minE_prev, t - 1, blockIdx.x, t - 1);
+    else
+      hood_packed_body<KH, kAct>(a, minE_prev, t - 1, blockIdx.x, t - 1);
   } else if (blockIdx.x >= nh + nv) {
     // last launch (t = map_max): the M-step's label scatter runs beside the
     // hood pass of the last iteration -- it reads only the committed labels
@@ -715,10 +973,31 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP))
       label_scatter_small_body<true>(sc.lab_even, sc.lab_odd, a.unconv, a.unconv, t, a.fixed,
                                      sc.R, sc.M, sc.Hs, sc.mean, sc.counts, sc.tiles, sc.layout,
                                      sc.x, blockIdx.x - nh - nv, fused_smem);
+  } else if (kAct && t >= 2 && !a.tile_counts) {
+    vertex_sparse_body<MT, KV>(a, lab_in, lab_out, minE_cur, minE_prev, t, blockIdx.x - nh,
+                               t > 0 ? t - 1 : 0);
   } else {
-    vertex_packed_body<MT, KV, VP>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh,
-                                   t > 0 ? t - 1 : 0);
+    vertex_packed_body<MT, KV, VP, kAct>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh,
+                                         t > 0 ? t - 1 : 0, minE_prev);
   }
+}
+
+// ---- vertex -> series index (active-set MAP) ----
+// inv_off[v + 1] = number of series containing v; after the scan, the
+// series ids of vertex v are inv_ser[inv_off[v] .. inv_off[v + 1]) (any order:
+// the flags they set commute).
+__global__ void k_inv_count(const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ h_mem,
+                            uint64_t Hs, uint32_t* __restrict__ cnt) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t h = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; h < Hs; h += stride)
+    for (uint32_t j = s_off[h]; j < s_off[h + 1]; ++j) atomicAdd(&cnt[h_mem[j]], 1u);
+}
+__global__ void k_inv_fill(const uint32_t* __restrict__ s_off, const uint32_t* __restrict__ h_mem,
+                           uint64_t Hs, uint32_t* __restrict__ cursor, uint32_t* __restrict__ ser) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t h = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; h < Hs; h += stride)
+    for (uint32_t j = s_off[h]; j < s_off[h + 1]; ++j)
+      ser[atomicAdd(&cursor[h_mem[j]], 1u)] = static_cast<uint32_t>(h);
 }
 
 // ---- pack builders ----
@@ -781,6 +1060,24 @@ __global__ void k_pack_hoods(const uint32_t* __restrict__ s_off, const uint32_t*
 }
 
 }  // namespace
+
+void build_vertex_series(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, uint32_t R,
+                         uint64_t S, uint32_t* inv_off, uint32_t* inv_ser, uint32_t* cursor,
+                         ScanWorkspace& ws, cudaStream_t s) {
+  CK(cudaMemsetAsync(inv_off, 0, (uint64_t(R) + 1) * sizeof(uint32_t), s));
+  const unsigned g = std::min<unsigned>(grid_for(Hs ? Hs : 1, 256), 16 * kNumSMs);
+  if (Hs) {
+    k_inv_count<<<g, 256, 0, s>>>(s_off, h_mem, Hs, inv_off);
+    CK_LAUNCH();
+  }
+  exclusive_scan_u32(inv_off, inv_off, uint64_t(R) + 1, nullptr, ws, s);
+  CK(cudaMemcpyAsync(cursor, inv_off, uint64_t(R) * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  if (Hs) {
+    k_inv_fill<<<g, 256, 0, s>>>(s_off, h_mem, Hs, cursor, inv_ser);
+    CK_LAUNCH();
+  }
+  (void)S;
+}
 
 void launch_pack_stats(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, uint64_t A,
                        const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, uint64_t S,
@@ -856,3 +1153,12 @@ void launch_series_offsets(const uint32_t* h_off, uint64_t H, uint64_t S, uint32
 }
 
 }  // namespace dpmrf_b200
+
+#ifdef DPMRF_PROBE
+extern "C" int dpmrf_probe_read_act(unsigned long long* out) {  // [2][64], then zeroed
+  if (cudaMemcpyFromSymbol(out, dpmrf_b200::g_act_probe, sizeof(dpmrf_b200::g_act_probe)) != cudaSuccess)
+    return 1;
+  unsigned long long z[2][64] = {};
+  return cudaMemcpyToSymbol(dpmrf_b200::g_act_probe, z, sizeof z) != cudaSuccess;
+}
+#endif

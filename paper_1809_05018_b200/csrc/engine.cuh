@@ -49,6 +49,18 @@ struct MapArgs {
   // Per launch (set by the launchers from the hood iteration th): the ring
   // rows of iterations th and th-1, so no thread evaluates a modulo.
   int row_t, row_p;
+  // Active-set MAP loop (DPMRF_RUN_ACTIVE_SET; act_vflag == nullptr: off).
+  // An item is re-evaluated only when an input of it changed: a vertex when
+  // a neighbor's label (or its own label / minimum, for the double buffers)
+  // changed in the previous iteration, a series (nonempty hood) when a
+  // member's minimum changed or its window test is still open.  The kernels
+  // derive the per-iteration slices from the MAP iteration.
+  uint8_t* act_vflag;        // 2 x R: vertex flags by iteration parity
+  uint8_t* act_hflag;        // 2 x Hs: series flags by iteration parity
+  double* act_hval;          // Hs: latest sum of every series
+  uint8_t* act_lastp;        // Hs: MAP iteration a series was last folded in
+  const uint32_t* inv_off;   // R + 1: vertex -> series CSR
+  const uint32_t* inv_ser;   // S: the series containing each vertex
 };
 
 // Number of 256-vertex label tiles (== vertex-kernel blocks).
@@ -97,6 +109,12 @@ struct ScatterArgs {
   double* x;
 };
 bool mstep_tail_fusable(uint32_t R, uint32_t M);
+bool map_active_supported(const MapArgs& a);
+struct ScanWorkspace;
+// vertex -> series CSR (inv_off R+1, inv_ser S) for the active-set MAP loop
+void build_vertex_series(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, uint32_t R,
+                         uint64_t S, uint32_t* inv_off, uint32_t* inv_ser, uint32_t* cursor,
+                         ScanWorkspace& ws, cudaStream_t s);
 
 void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
                       const double* minE_prev, double* minE_cur, int t, int map_max,

@@ -32,7 +32,7 @@ DPMRF_CUDA_ERROR, DPMRF_NCCL_ERROR, DPMRF_INTERNAL_ERROR = 4, 5, 6
 
 TRACE_NONE, TRACE_EM, TRACE_FULL = 0, 1, 2
 RUN_FIXED_WORK, RUN_MULTILABEL, RUN_KERNEL_TIMING, RUN_NO_GRAPH = 1, 2, 4, 16
-RUN_HOST_LOG, RUN_CSR, RUN_UNFUSED = 128, 256, 512
+RUN_HOST_LOG, RUN_CSR, RUN_UNFUSED, RUN_ACTIVE_SET = 128, 256, 512, 1024
 
 K_SIGMA_FLOOR = 1e-3  # kSigmaFloor, model.hpp:9
 
@@ -466,17 +466,20 @@ class Context:
     def optimize(self, config: OptimizerConfig, *, fixed_work=False, multilabel=False,
                  trace_level=TRACE_FULL, kernel_timing=False, labels_out=None,
                  graphs=True, host_log=False, csr=False, fused=True,
-                 trace_sink: Optional["TraceSink"] = None) -> OptimizeResult:
+                 trace_sink: Optional["TraceSink"] = None,
+                 active_set=False) -> OptimizeResult:
         """optimize (optimize.cpp:31-74) on the resident graph + hoods.
         multilabel=True allows num_labels != 2 (extension; the reference's
         validate_config rejects it, optimize.cpp:14).  trace_sink: caller-owned
         (pinned) buffers the full trace is streamed into (dpmrf_set_trace_sink);
-        the returned MapIterationLogs are views into it."""
+        the returned MapIterationLogs are views into it.  active_set=True
+        (extension, DPMRF_RUN_ACTIVE_SET): re-evaluate only what changed --
+        same results, less than the reference's per-iteration work."""
         M = config.num_labels
         flags = (RUN_FIXED_WORK if fixed_work else 0) | (RUN_MULTILABEL if multilabel else 0) | \
             (RUN_KERNEL_TIMING if kernel_timing else 0) | (RUN_HOST_LOG if host_log else 0) | \
             (RUN_CSR if csr else 0) | (0 if fused else RUN_UNFUSED) | \
-            (0 if graphs else RUN_NO_GRAPH)
+            (0 if graphs else RUN_NO_GRAPH) | (RUN_ACTIVE_SET if active_set else 0)
         opts = N.CRunOptions(flags, trace_level)
         cfg = config.c()
         labels = labels_out if labels_out is not None else np.zeros(self.R, np.uint32)
@@ -501,12 +504,14 @@ class Context:
     def optimize_arrays(self, graph: RegionGraph, hoods: NeighborhoodSet,
                         config: OptimizerConfig, *, fixed_work=False, multilabel=False,
                         trace_level=TRACE_FULL, labels_out=None,
-                        trace_sink: Optional["TraceSink"] = None) -> OptimizeResult:
+                        trace_sink: Optional["TraceSink"] = None,
+                        active_set=False) -> OptimizeResult:
         """optimize(backend, graph, hoods, config) in ONE C-ABI call
         (dpmrf_optimize_arrays): host arrays in, labels / params out."""
         M = config.num_labels
         self._attach(trace_sink)
-        flags = (RUN_FIXED_WORK if fixed_work else 0) | (RUN_MULTILABEL if multilabel else 0)
+        flags = (RUN_FIXED_WORK if fixed_work else 0) | (RUN_MULTILABEL if multilabel else 0) | \
+            (RUN_ACTIVE_SET if active_set else 0)
         opts = N.CRunOptions(flags, trace_level)
         cfg = config.c()
         off, nbr, mean = _u32(graph.offsets), _u32(graph.neighbors), _f64(graph.region_mean)

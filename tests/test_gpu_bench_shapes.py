@@ -100,6 +100,11 @@ def test_bench_shape_vs_reference(ctx, name):
     for level in (E.TRACE_EM, E.TRACE_FULL):
         r = ctx.optimize(cfg, fixed_work=True, multilabel=multilabel, trace_level=level)
         check_result(rec, r, level)
+    # the active-set MAP loop (extension) reproduces the same fixture
+    r = ctx.optimize(cfg, fixed_work=True, multilabel=multilabel, trace_level=E.TRACE_EM,
+                     active_set=True)
+    assert r.stats["active_set"] == 1
+    check_result(rec, r, E.TRACE_EM)
 
 
 @pytest.mark.skipif("D" not in SHAPES, reason="no D fixture")

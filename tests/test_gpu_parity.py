@@ -375,3 +375,31 @@ def test_stream_fold_matches_two_pass(size, brick, M, monkeypatch):
     finally:
         one.close()
         two.close()
+
+
+@pytest.mark.parametrize("size,block,brick,M,seed", [
+    (512, 8, False, 2, 3), (1000, 8, False, 2, 9), (768, 8, True, 5, 4), (2560, 8, False, 2, 42),
+    (4096, 8, False, 2, 21), (2560, 8, True, 5, 42)])
+def test_active_set_matches_dense(ctx, size, block, brick, M, seed):
+    """active_set=True (extension, DPMRF_RUN_ACTIVE_SET): vertices re-evaluated
+    only when a neighbor's label (or their own label / minimum) changed,
+    series folded only when a member's minimum changed or their window is
+    open -- the labels, parameters and every EM record (total energy, MAP
+    count, converged flag) equal the dense run's bit for bit, with and
+    without early exits."""
+    from paper_1809_05018_b200 import inputs
+    sl = inputs.synthetic_slice(size, block, brick=brick, seed=seed)
+    ctx.set_graph(sl.graph)
+    ctx.build_neighborhoods(sl.cliques)
+    for fixed in (False, True):
+        cfg = E.OptimizerConfig(num_labels=M, em_max_iters=8, rng_seed=seed)
+        want = ctx.optimize(cfg, fixed_work=fixed, multilabel=M != 2, trace_level=E.TRACE_EM)
+        got = ctx.optimize(cfg, fixed_work=fixed, multilabel=M != 2, trace_level=E.TRACE_EM,
+                           active_set=True)
+        assert got.stats["active_set"] == 1
+        same(got, want, full=False)
+        assert got.stats["map_iters_total"] == want.stats["map_iters_total"]
+    # a full trace falls back to the dense loop (every row is needed)
+    r = ctx.optimize(E.OptimizerConfig(num_labels=M, em_max_iters=2, rng_seed=seed),
+                     multilabel=M != 2, trace_level=E.TRACE_FULL, active_set=True)
+    assert r.stats["active_set"] == 0

@@ -18,10 +18,17 @@ def b():
     return ctx.optimize_arrays(g, h, cfg, fixed_work=True, trace_level=E.TRACE_NONE, labels_out=lab)
 def c():
     return ctx.optimize(cfg, fixed_work=True, trace_level=E.TRACE_NONE, labels_out=lab)
-res = {"sethoods+optimize": [], "optimize_arrays": [], "optimize_only": []}
-for f in (a, b, c): f(); f()
+def d():
+    ctx.set_graph(g); ctx.set_hoods(h)
+cfg0 = E.OptimizerConfig(em_max_iters=0, rng_seed=42)
+def e():  # upload + prepare + no EM
+    return ctx.optimize_arrays(g, h, cfg0, fixed_work=True, trace_level=E.TRACE_NONE, labels_out=lab)
+res = {"sethoods+optimize": [], "optimize_arrays": [], "optimize_only": [], "upload_only": [],
+       "arrays_em0": []}
+for f in (a, b, c, d, e): f(); f()
 for rep in range(30):
-    for name, f in (("sethoods+optimize", a), ("optimize_arrays", b), ("optimize_only", c)):
+    for name, f in (("sethoods+optimize", a), ("optimize_arrays", b), ("optimize_only", c),
+                    ("upload_only", d), ("arrays_em0", e)):
         torch.cuda.synchronize(); t0 = time.perf_counter(); r = f(); res[name].append((time.perf_counter() - t0) * 1e3)
         if name == "optimize_only": dev = r.stats["optimize_ms"]
 for k, v in res.items(): print(k, "median %.3f ms  min %.3f" % (statistics.median(v), min(v)))
