@@ -83,8 +83,9 @@ enum {
                                    neighbor's label) and fold only the hoods whose members'
                                    minima changed or whose window is still open; bit-identical
                                    results, but less than the reference's per-iteration work.
-                                   Fused layouts of the grid (M=2) and brick (M=5) graphs, trace
-                                   levels NONE / EM, one device; ignored otherwise */
+                                   The first EM iteration runs dense.  Grid graphs with two
+                                   labels, trace levels NONE / EM, device-resident loop, one
+                                   device; ignored otherwise (dpmrf_run_stats.active_set) */
 };
 
 typedef struct dpmrf_run_options {

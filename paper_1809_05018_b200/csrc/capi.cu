@@ -639,7 +639,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     a.eq = a.hood_k ? ctx->hood_eq.ensure(Hs) : nullptr;  // (packed hood pass only)
     // active-set MAP loop (opt-in extension; include/dpmrf_cuda.h)
     const bool active = (o.flags & DPMRF_RUN_ACTIVE_SET) && fused && !full && Hs > 0 &&
-                        map_active_supported(a);
+                        device_loop && map_active_supported(a);
     if (active) {
       const uint64_t Rp = (uint64_t(R) + 15) & ~15ull, Hp = (Hs + 15) & ~15ull;  // 16-B rows
       a.act_vflag = ctx->act_vflag.ensure(2 * Rp);
@@ -657,6 +657,22 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       }
       a.inv_off = ctx->inv_off.get();
       a.inv_ser = ctx->inv_ser.get();
+      // work lists of the sparse passes (tile flags zero; re-armed by the passes)
+      const uint64_t tv = (uint64_t(R) + 255) / 256, th = (Hs + 255) / 256;
+      const bool fresh = !ctx->act_vtile.get() || ctx->act_vtile.cap < 2 * tv ||
+                         !ctx->act_htile.get() || ctx->act_htile.cap < 2 * th;
+      a.act_vtile = ctx->act_vtile.ensure(2 * tv);
+      a.act_htile = ctx->act_htile.ensure(2 * th);
+      if (fresh) {
+        CK(cudaMemsetAsync(a.act_vtile, 0, 2 * tv * 4, st));
+        CK(cudaMemsetAsync(a.act_htile, 0, 2 * th * 4, st));
+      }
+      a.act_vlist = ctx->act_vlist.ensure(2 * tv);
+      a.act_hlist = ctx->act_hlist.ensure(2 * th);
+      a.act_stride = map_max + 1;
+      const uint64_t ncnt = 2 * uint64_t(std::max(em_max, 1)) * (map_max + 1);
+      a.act_cnt = ctx->act_cnt.ensure(ncnt);
+      CK(cudaMemsetAsync(a.act_cnt, 0, ncnt * 4, st));
     }
     ctx->stats.active_set = active ? 1 : 0;
     // [em_done, pending_done, em_count, pad | per-MAP-iteration counters]
@@ -725,9 +741,15 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
     sc.x = ctx->ms.x.get();
     if (merged)  // the MAP counters of the first EM (later ones are re-armed by the tail)
       CK(cudaMemsetAsync(a.unconv, 0, map_max * sizeof(uint32_t), st));
+    // active set: the first EM iteration (from random labels: nearly every
+    // item changes) runs dense, the later ones flag-driven
+    bool em_active = active;
+    MapArgs a_dense = a;
+    a_dense.act_vflag = nullptr;
     auto enqueue_em = [&](int parity) {
       uint64_t k = 0;
       size_t ev = 0;
+      const MapArgs& am = em_active ? a : a_dense;
       sc.lab_even = lab[parity];
       sc.lab_odd = lab[parity ^ 1];
       if (merged) {
@@ -738,6 +760,8 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
         CK(cudaMemcpyAsync(const_cast<double*>(a.terms), h_terms, 3 * M * 8,
                            cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(a.unconv, 0, map_max * sizeof(uint32_t), st));
+        if (a.act_cnt)  // (the EM counter stays 0 on the host-log loop)
+          CK(cudaMemsetAsync(a.act_cnt, 0, 2 * uint64_t(map_max + 1) * 4, st));
       }
       if (fused) {
         const uint64_t half = R ? R : 1;
@@ -745,7 +769,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
         // the PDL overlap between consecutive launches stays in the figure
         for (int t = 0; t <= map_max; ++t) {
           if (t == 0) record(ev++);
-          launch_map_fused(a, lab[(parity + t) & 1], lab[(parity + t + 1) & 1],
+          launch_map_fused(am, lab[(parity + t) & 1], lab[(parity + t + 1) & 1],
                            minE2 + uint64_t((t + 1) & 1) * half, minE2 + uint64_t(t & 1) * half,
                            t, map_max, st, merged ? &sc : nullptr);
           k += 1;
@@ -771,8 +795,8 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       }
       record(ev++);
       // (active set: the latest sum of every series, not the last ring row)
-      launch_mstep(a.mean, R, M, lab[parity], lab[parity ^ 1], active ? a.act_hval : a.hist, Hs,
-                   active ? 1 : a.ring, a.unconv,
+      launch_mstep(a.mean, R, M, lab[parity], lab[parity ^ 1], em_active ? a.act_hval : a.hist,
+                   Hs, em_active ? 1 : a.ring, a.unconv,
                    map_max, fixed, params, em_out, ctx->ms, st, &k, /*counts_ready=*/true,
                    /*scattered=*/merged, merged ? &ep : nullptr);
       record(ev++);
@@ -835,14 +859,19 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       key.layout = a.adj_k * 100 + a.hood_k + (active ? 100000 : 0);
       key.p2[5] = a.act_vflag;
       key.p2[6] = a.act_hval;
+      key.p2[7] = a.act_cnt;  // (the tile / list buffers follow R and Hs)
       if (!ctx->graph_valid || std::memcmp(&key, &ctx->graph_key, sizeof key) != 0) {
         ctx->drop_graphs();
-        for (int parity = 0; parity < (device_loop ? 1 : 2); ++parity) {
+        // (device loop: [0] the EM graph, [1] the dense first EM of an
+        //  active-set run; host-log loop: one graph per label parity)
+        const int ngraphs = device_loop ? (active ? 2 : 1) : 2;
+        for (int parity = 0; parity < ngraphs; ++parity) {
           cudaGraph_t g;
+          em_active = active && !(device_loop && parity == 1);
           CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
           capturing = true;
           try {
-            enqueue_em(parity);
+            enqueue_em(device_loop ? 0 : parity);
           } catch (...) {
             capturing = false;
             cudaStreamEndCapture(st, &g);
@@ -905,9 +934,11 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
                              nrows, cudaMemcpyDeviceToHost, cs));
       };
       for (int em = 0; em < em_max; ++em) {
+        const bool first_dense = active && em == 0;
         if (use_graph) {
-          CK(cudaGraphLaunch(ctx->graph_exec[0], st));
+          CK(cudaGraphLaunch(ctx->graph_exec[first_dense ? 1 : 0], st));
         } else {
+          em_active = active && !first_dense;
           enqueue_em(0);
         }
         if (stash) {

@@ -70,6 +70,7 @@ struct dpmrf_context {
   dpmrf_b200::DevBuf<uint8_t> act_vflag, act_hflag, act_lastp;
   dpmrf_b200::DevBuf<double> act_hval;
   dpmrf_b200::DevBuf<uint32_t> inv_off, inv_ser, inv_cursor;
+  dpmrf_b200::DevBuf<uint32_t> act_vtile, act_htile, act_vlist, act_hlist, act_cnt;
   uint64_t inv_gen = ~0ull;
   dpmrf_b200::DevBuf<uint32_t> unconv, labels32;
   dpmrf_b200::MStepBuffers ms;

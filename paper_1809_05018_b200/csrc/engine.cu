@@ -293,7 +293,10 @@ constexpr int fused_min_blocks(int mt, int kh, int vp = 1, bool act = false) {
 // spills: 16384^2 662 vs 675 EM-it/s).
 constexpr bool kHoistMean = DPMRF_HOIST_MEAN != 0;
 constexpr int kWinRegs = 3;  // window rows held in registers (default L = 3)
-constexpr uint32_t kSpan = 16;  // items per thread in the active-set sparse passes
+#ifndef DPMRF_ACT_BLOCKS
+#define DPMRF_ACT_BLOCKS (8 * 148)
+#endif
+constexpr uint32_t kActBlocks = DPMRF_ACT_BLOCKS;  // blocks per list-driven pass
 #ifdef DPMRF_PROBE
 // processed vertices / series per MAP iteration in active-set runs (probe builds)
 __device__ unsigned long long g_act_probe[2][64];
@@ -324,9 +327,10 @@ bool map_fused_supported(const MapArgs& a) { return a.adj_k && a.hood_k; }
 // The fused layouts with an active-set instance: the grid graphs with two
 // labels (configs A, B, D, E) and the brick graphs with five (config C).
 bool map_active_supported(const MapArgs& a) {
-  if (!map_fused_supported(a)) return false;
-  if (a.hood_k == 12) return a.M == 5 && a.adj_k == 8;
-  return a.M == 2 && a.adj_k == 4 && a.hood_k == 8;
+  // (brick graphs with five labels keep changing labels in every EM
+  // iteration: their flags stay dense and the dense loop is faster -- 12.8 k
+  // vs 5.9 k EM-it/s at 2560^2 -- so they keep the dense loop)
+  return map_fused_supported(a) && a.M == 2 && a.adj_k == 4 && a.hood_k == 8;
 }
 
 namespace {
@@ -367,18 +371,17 @@ void launch_map_fused(const MapArgs& a, const uint8_t* lab_in, uint8_t* lab_out,
   // the M-step's grouping), so the other passes skip their block counts
   if (a.fixed && t != map_max - 1) ar.tile_counts = nullptr;
   if (a.act_vflag) {  // active-set instances (map_active_supported)
-    // sparse passes: one thread per kSpan items (see vertex_sparse_body)
-    const bool sh = t - 1 > a.L, sv = t >= 2 && !ar.tile_counts;
-    const uint32_t nh2 = t >= 1 ? grid_for(a.h_end - a.h_begin,
-                                           uint64_t(kHoodThreads) * (sh ? kSpan : 1)) : 0u;
-    const uint32_t nv2 = t < map_max ? grid_for(a.v_end - a.v_begin,
-                                                uint64_t(kVtxThreads) * (sv ? kSpan : vp)) : 0u;
+    // list-driven passes: a fixed grid of kActBlocks blocks (per pass)
+    const bool sh = t - 1 >= 1, sv = t >= 2 && !ar.tile_counts;
+    const uint32_t nh2 = t >= 1 ? (sh ? std::min<uint32_t>(kActBlocks, grid_for(a.h_end - a.h_begin, kHoodThreads))
+                                      : grid_for(a.h_end - a.h_begin, kHoodThreads)) : 0u;
+    const uint32_t nv2 = t < map_max ? (sv ? std::min<uint32_t>(kActBlocks, grid_for(a.v_end - a.v_begin, kVtxThreads))
+                                           : grid_for(a.v_end - a.v_begin, uint64_t(kVtxThreads) * vp)) : 0u;
     const dim3 g2(nh2 + nv2 + ns);
 #define MFA(MT, KV, KH, VP)                                                                 \
   launch_pdl(k_map_fused<MT, KV, KH, VP, true>, g2, blk, smem, s, ar, lab_in, lab_out,       \
              minE_prev, minE_cur, t, nh2, nv2, scv)
-    if (k12) MFA(5, 8, 12, 1);
-    else if (vp == 2) MFA(2, 4, 8, 2);
+    if (vp == 2) MFA(2, 4, 8, 2);
     else MFA(2, 4, 8, 1);
 #undef MFA
     return;
@@ -545,6 +548,31 @@ __device__ __forceinline__ uint8_t* act_hflags(const MapArgs& a, int t) {
   return a.act_hflag + uint64_t(t & 1) * act_hpitch(a);
 }
 
+__device__ __forceinline__ uint32_t act_vtiles(const MapArgs& a) { return (a.R + 255) / 256; }
+__device__ __forceinline__ uint32_t act_htiles(const MapArgs& a) {
+  return static_cast<uint32_t>((a.Hs + 255) / 256);
+}
+// list counters of iteration t of the current EM: [0] vertex tiles, [1] series tiles
+__device__ __forceinline__ uint32_t* act_counts(const MapArgs& a, int t) {
+  const uint32_t e = a.unconv[kEmCount];
+  return a.act_cnt + 2 * (uint64_t(e) * a.act_stride + t);
+}
+// flag item idx for iteration t (vertex: k = 0, series: k = 1) and list its tile
+__device__ __forceinline__ void act_flag(const MapArgs& a, int k, int t, uint32_t idx) {
+  uint8_t* items = k == 0 ? act_vflags(a, t) : act_hflags(a, t);
+  if (items[idx]) return;  // (its tile is listed already)
+  items[idx] = 1;
+  const uint32_t tile = idx >> 8;
+  const uint32_t nt = k == 0 ? act_vtiles(a) : act_htiles(a);
+  uint32_t* tiles = (k == 0 ? a.act_vtile : a.act_htile) + uint64_t(t & 1) * nt;
+  // (a plain read first: a tile's 256 items must not all hit one atomic)
+  if (*reinterpret_cast<volatile uint32_t*>(&tiles[tile]) == 0u &&
+      atomicExch(&tiles[tile], 1u) == 0u) {
+    uint32_t* list = (k == 0 ? a.act_vlist : a.act_hlist) + uint64_t(t & 1) * nt;
+    list[atomicAdd(act_counts(a, t) + k, 1u)] = tile;
+  }
+}
+
 // After vertex v of iteration t (t >= 1) computed (best, best_l) from its
 // old label: who is evaluated next.  A new label re-evaluates the neighbors
 // (their discord counts) and v (the label double buffer); a new minimum v
@@ -554,19 +582,17 @@ template <int K>
 __device__ __forceinline__ void act_mark(const MapArgs& a, int t, uint32_t v, const int16_t (&d)[K],
                                          uint32_t old, uint32_t best_l, double best,
                                          double prev) {
-  uint8_t* vnext = act_vflags(a, t + 1);
   const bool lab_changed = best_l != old;
   const bool min_changed = __double_as_longlong(prev) != __double_as_longlong(best);
-  if (lab_changed || min_changed) vnext[v] = 1;
+  if (lab_changed || min_changed) act_flag(a, 0, t + 1, v);
   if (lab_changed) {
 #pragma unroll
     for (int k = 0; k < K; ++k)
-      if (d[k] != INT16_MIN) vnext[v + static_cast<uint32_t>(static_cast<int32_t>(d[k]))] = 1;
+      if (d[k] != INT16_MIN)
+        act_flag(a, 0, t + 1, v + static_cast<uint32_t>(static_cast<int32_t>(d[k])));
   }
-  if (min_changed && t > a.L) {
-    uint8_t* hmark = act_hflags(a, t);
-    for (uint32_t i = a.inv_off[v]; i < a.inv_off[v + 1]; ++i) hmark[a.inv_ser[i]] = 1;
-  }
+  if (min_changed)
+    for (uint32_t i = a.inv_off[v]; i < a.inv_off[v + 1]; ++i) act_flag(a, 1, t, a.inv_ser[i]);
 }
 
 template <int MT, int K, int P = 1, bool kAct = false>
@@ -600,6 +626,36 @@ __device__ __forceinline__ void vertex_packed_body(const MapArgs& a,
   }
   pdl_wait();
   uint8_t* vcur = act ? act_vflags(a, t) : nullptr;
+  if (kAct) {
+    // this pass consumes the tiles of parity t; the first pass of an EM also
+    // clears parity 1 (left over from the previous EM)
+    const uint32_t nt = act_vtiles(a);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        const uint32_t tile = blk * P + j;
+        if (tile < nt) {
+          a.act_vtile[uint64_t(t & 1) * nt + tile] = 0;
+          if (t == 0) a.act_vtile[nt + tile] = 0;
+        }
+      }
+    if (t == 0) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        const uint32_t v = v0 + j * kVtxThreads;
+        if (v < a.v_end) act_vflags(a, 1)[v] = 0;
+      }
+      // the series flags and tiles of parity 1 (marked from the next launch
+      // on; parity 0 is cleared by the dense hood pass of iteration 0)
+      const uint64_t nthreads =
+          uint64_t((a.v_end - a.v_begin + kVtxThreads * P - 1) / (kVtxThreads * P)) * kVtxThreads;
+      const uint64_t g = uint64_t(blk) * kVtxThreads + threadIdx.x;
+      uint8_t* h1 = act_hflags(a, 1);
+      for (uint64_t h = g; h < a.Hs; h += nthreads) h1[h] = 0;
+      const uint32_t ht = act_htiles(a);
+      for (uint64_t k = g; k < ht; k += nthreads) a.act_htile[ht + k] = 0;
+    }
+  }
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     const uint32_t v = v0 + j * kVtxThreads;
@@ -782,7 +838,7 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
   // active-set, after the window opened (t > L): only flagged series fold,
   // and their structure is read once the flag is known
   constexpr bool act = kAct;
-  const bool sparse = act && t > a.L;
+  const bool sparse = act && t >= 1;
   uint32_t base = 0;
   uint32_t u[K / 2];
   if (live && !sparse) {
@@ -798,6 +854,7 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
     } else {
       uint8_t* flag = act_hflags(a, t) + h;
       const bool run = !sparse || *flag;
+      if (threadIdx.x == 0) a.act_htile[uint64_t(t & 1) * act_htiles(a) + (h >> 8)] = 0;
       if (run) {
         *flag = 0;
         double over = 0.0;
@@ -824,8 +881,10 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
         a.act_lastp[h] = static_cast<uint8_t>(t);
         // still open (not converged, or converged on a run shorter than the
         // window): fold again in the next iteration
-        if (t + 1 > a.L && (not_conv || eqn < uint32_t(a.L)))
-          act_hflags(a, t + 1)[h] = 1;
+        // (dense only at t = 0: a series whose sum then stays unchanged is
+        // converged by iteration L without being folded again -- except a NaN
+        // sum, or a non-positive tolerance, which never converge)
+        if (isnan(sum) || !(a.tol > 0.0)) act_flag(a, 1, t + 1, h);
       }
     }
   }
@@ -835,52 +894,66 @@ __device__ __forceinline__ void hood_packed_body(const MapArgs& a,
 }
 
 // ---- active-set sparse passes (t >= 2 vertices, t > L series) ----
-// One thread per 16 consecutive items: a 16-byte load of their flags, and
-// only the flagged ones are evaluated (grids 16x smaller than the dense
-// passes, so launching blocks of mostly idle threads costs nothing).
+// A fixed grid of blocks walks the iteration's work list (the 256-item tiles
+// holding a flagged item, appended by act_flag during the previous launch):
+// block b takes tiles b, b + G, ...; in a tile, each flagged item is
+// evaluated by its own thread.  Few flagged tiles cost a few block
+// iterations; all of them (the first EM) cost what the dense pass costs,
+// without scheduling a block per tile.
 template <int MT, int K>
-__device__ __forceinline__ void vertex_sparse_body(const MapArgs& a,
+__device__ __forceinline__ void vertex_active_item(const MapArgs& a,
                                                    const uint8_t* __restrict__ lab_in,
                                                    uint8_t* __restrict__ lab_out,
                                                    double* __restrict__ minE,
                                                    const double* __restrict__ minE_prev, int t,
-                                                   uint32_t blk, int skip_t) {
+                                                   uint32_t v) {
   const uint32_t M = MT > 0 ? uint32_t(MT) : a.M;
-  const uint32_t v0 = a.v_begin + (blk * kVtxThreads + threadIdx.x) * kSpan;
+  int16_t d[K];
+  load_i16<K>(a.adj_pk + uint64_t(v) * K, d);
+  const uint8_t old = lab_in[v];
+  if (!a.cover[v]) {
+    lab_out[v] = old;
+    return;
+  }
+  uint8_t nb[K];
+  uint32_t deg = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const bool ok = d[k] != INT16_MIN;
+    deg += ok;
+    nb[k] = ok ? lab_in[v + static_cast<uint32_t>(static_cast<int32_t>(d[k]))] : uint8_t(0xFF);
+  }
+  double best;
+  uint32_t best_l;
+  vertex_argmin_packed<MT, K>(a, M, a.mean[v], nb, deg, best, best_l);
+  minE[v] = best;
+  lab_out[v] = static_cast<uint8_t>(best_l);
+  act_mark<K>(a, t, v, d, old, best_l, best, minE_prev[v]);
+}
+
+template <int MT, int K>
+__device__ __forceinline__ void vertex_list_body(const MapArgs& a,
+                                                 const uint8_t* __restrict__ lab_in,
+                                                 uint8_t* __restrict__ lab_out,
+                                                 double* __restrict__ minE,
+                                                 const double* __restrict__ minE_prev, int t,
+                                                 uint32_t blk, uint32_t nblk, int skip_t) {
   pdl_wait();
   if (map_iter_skipped(a.unconv, skip_t, a.fixed)) return;  // uniform over the grid
-  if (v0 >= a.v_end) return;
+  const uint32_t nt = act_vtiles(a);
+  const uint32_t n = act_counts(a, t)[0];
+  const uint32_t* list = a.act_vlist + uint64_t(t & 1) * nt;
+  uint32_t* tiles = a.act_vtile + uint64_t(t & 1) * nt;
   uint8_t* vcur = act_vflags(a, t);
-  const uint4 f4 = *reinterpret_cast<const uint4*>(vcur + v0);
-  if ((f4.x | f4.y | f4.z | f4.w) == 0) return;
-  const uint32_t w[4] = {f4.x, f4.y, f4.z, f4.w};
-#pragma unroll 1
-  for (uint32_t i = 0; i < kSpan; ++i) {
-    if (((w[i >> 2] >> (8 * (i & 3))) & 0xFFu) == 0) continue;
-    const uint32_t v = v0 + i;
-    vcur[v] = 0;
-    ACT_PROBE(0, t);
-    int16_t d[K];
-    load_i16<K>(a.adj_pk + uint64_t(v) * K, d);
-    const uint8_t old = lab_in[v];
-    if (!a.cover[v]) {
-      lab_out[v] = old;
-      continue;
+  for (uint32_t i = blk; i < n; i += nblk) {
+    const uint32_t tile = list[i];
+    if (threadIdx.x == 0) tiles[tile] = 0;
+    const uint32_t v = tile * kVtxThreads + threadIdx.x;
+    if (v < a.v_end && vcur[v]) {
+      vcur[v] = 0;
+      ACT_PROBE(0, t);
+      vertex_active_item<MT, K>(a, lab_in, lab_out, minE, minE_prev, t, v);
     }
-    uint8_t nb[K];
-    uint32_t deg = 0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const bool ok = d[k] != INT16_MIN;
-      deg += ok;
-      nb[k] = ok ? lab_in[v + static_cast<uint32_t>(static_cast<int32_t>(d[k]))] : uint8_t(0xFF);
-    }
-    double best;
-    uint32_t best_l;
-    vertex_argmin_packed<MT, K>(a, M, a.mean[v], nb, deg, best, best_l);
-    minE[v] = best;
-    lab_out[v] = static_cast<uint8_t>(best_l);
-    act_mark<K>(a, t, v, d, old, best_l, best, minE_prev[v]);
   }
 }
 
@@ -913,27 +986,34 @@ __device__ __forceinline__ int hood_active_item(const MapArgs& a, const double* 
   a.act_lastp[h] = static_cast<uint8_t>(t);
   // still open (not converged, or converged on a run shorter than the
   // window): fold again in the next iteration
-  if (nc || eqn < uint32_t(a.L)) act_hflags(a, t + 1)[h] = 1;
+  if (nc || eqn < uint32_t(a.L)) act_flag(a, 1, t + 1, h);
   return nc;
 }
 
 template <int K>
-__device__ __forceinline__ void hood_sparse_body(const MapArgs& a, const double* __restrict__ minE,
-                                                 int t, uint32_t blk, int skip_t) {
-  const uint32_t h0 = static_cast<uint32_t>(a.h_begin) + (blk * kHoodThreads + threadIdx.x) * kSpan;
+__device__ __forceinline__ void hood_list_body(const MapArgs& a, const double* __restrict__ minE,
+                                               int t, uint32_t blk, uint32_t nblk, int skip_t) {
   pdl_wait();
   if (map_iter_skipped(a.unconv, skip_t, a.fixed)) return;  // uniform over the grid
+  const uint32_t nt = act_htiles(a);
+  const uint32_t n = act_counts(a, t)[1];
+  const uint32_t* list = a.act_hlist + uint64_t(t & 1) * nt;
+  uint32_t* tiles = a.act_htile + uint64_t(t & 1) * nt;
+  const uint8_t* hcur = act_hflags(a, t);
   int cnt = 0;
-  if (h0 < a.h_end) {
-    const uint4 f4 = *reinterpret_cast<const uint4*>(act_hflags(a, t) + h0);
-    if ((f4.x | f4.y | f4.z | f4.w) != 0) {
-      const uint32_t w[4] = {f4.x, f4.y, f4.z, f4.w};
-#pragma unroll 1
-      for (uint32_t i = 0; i < kSpan; ++i)
-        if ((w[i >> 2] >> (8 * (i & 3))) & 0xFFu) cnt += hood_active_item<K>(a, minE, t, h0 + i);
-    }
+  for (uint32_t i = blk; i < n; i += nblk) {
+    const uint32_t tile = list[i];
+    if (threadIdx.x == 0) tiles[tile] = 0;
+    const uint32_t h = tile * kHoodThreads + threadIdx.x;
+    if (h < a.h_end && hcur[h]) cnt += hood_active_item<K>(a, minE, t, h);
   }
-  // unconverged series of this iteration (the early exit, optimize.cpp:59)
+  // unconverged series of this iteration (the early exit, optimize.cpp:59);
+  // before the window opens (t < L) no series converges, folded or not
+  if (t < a.L) {
+    if (blk == 0 && threadIdx.x == 0 && a.h_end > a.h_begin)
+      atomicAdd(&a.unconv[t], uint32_t(a.h_end - a.h_begin));
+    return;
+  }
   const int wsum = __reduce_add_sync(0xffffffffu, cnt);
   if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&a.unconv[t], uint32_t(wsum));
 }
@@ -960,8 +1040,8 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP, kAct
   static_assert(kVtxThreads == kTileThreads, "scatter tiles are vertex blocks");
   extern __shared__ uint32_t fused_smem[];
   if (blockIdx.x < nh) {
-    if (kAct && t - 1 > a.L)
-      hood_sparse_body<KH>(a, minE_prev, t - 1, blockIdx.x, t - 1);
+    if (kAct && t - 1 >= 1)
+      hood_list_body<KH>(a, minE_prev, t - 1, blockIdx.x, nh, t - 1);
     else
       hood_packed_body<KH, kAct>(a, minE_prev, t - 1, blockIdx.x, t - 1);
   } else if (blockIdx.x >= nh + nv) {
@@ -974,8 +1054,8 @@ __global__ void __launch_bounds__(kVtxThreads, fused_min_blocks(MT, KH, VP, kAct
                                      sc.R, sc.M, sc.Hs, sc.mean, sc.counts, sc.tiles, sc.layout,
                                      sc.x, blockIdx.x - nh - nv, fused_smem);
   } else if (kAct && t >= 2 && !a.tile_counts) {
-    vertex_sparse_body<MT, KV>(a, lab_in, lab_out, minE_cur, minE_prev, t, blockIdx.x - nh,
-                               t > 0 ? t - 1 : 0);
+    vertex_list_body<MT, KV>(a, lab_in, lab_out, minE_cur, minE_prev, t, blockIdx.x - nh, nv,
+                             t > 0 ? t - 1 : 0);
   } else {
     vertex_packed_body<MT, KV, VP, kAct>(a, lab_in, lab_out, minE_cur, t, blockIdx.x - nh,
                                          t > 0 ? t - 1 : 0, minE_prev);

@@ -61,6 +61,14 @@ struct MapArgs {
   uint8_t* act_lastp;        // Hs: MAP iteration a series was last folded in
   const uint32_t* inv_off;   // R + 1: vertex -> series CSR
   const uint32_t* inv_ser;   // S: the series containing each vertex
+  // work lists of the sparse passes: 256-item tiles holding a flagged item,
+  // appended once per (tile, parity) by whoever flags its first item
+  uint32_t* act_vtile;       // 2 x vertex tiles: tile flagged (by parity)
+  uint32_t* act_htile;       // 2 x series tiles
+  uint32_t* act_vlist;       // 2 x vertex tiles: flagged tile ids (by parity)
+  uint32_t* act_hlist;       // 2 x series tiles
+  uint32_t* act_cnt;         // per (EM, MAP iteration): [vertex tiles, series tiles] listed
+  int act_stride;            // map_max + 1
 };
 
 // Number of 256-vertex label tiles (== vertex-kernel blocks).

@@ -103,7 +103,7 @@ def test_bench_shape_vs_reference(ctx, name):
     # the active-set MAP loop (extension) reproduces the same fixture
     r = ctx.optimize(cfg, fixed_work=True, multilabel=multilabel, trace_level=E.TRACE_EM,
                      active_set=True)
-    assert r.stats["active_set"] == 1
+    assert r.stats["active_set"] == (1 if rec["case"]["M"] == 2 else 0)
     check_result(rec, r, E.TRACE_EM)
 
 

@@ -379,7 +379,7 @@ def test_stream_fold_matches_two_pass(size, brick, M, monkeypatch):
 
 @pytest.mark.parametrize("size,block,brick,M,seed", [
     (512, 8, False, 2, 3), (1000, 8, False, 2, 9), (768, 8, True, 5, 4), (2560, 8, False, 2, 42),
-    (4096, 8, False, 2, 21), (2560, 8, True, 5, 42)])
+    (4096, 8, False, 2, 21), (2304, 7, False, 2, 8), (2560, 8, True, 5, 42)])
 def test_active_set_matches_dense(ctx, size, block, brick, M, seed):
     """active_set=True (extension, DPMRF_RUN_ACTIVE_SET): vertices re-evaluated
     only when a neighbor's label (or their own label / minimum) changed,
@@ -396,7 +396,8 @@ def test_active_set_matches_dense(ctx, size, block, brick, M, seed):
         want = ctx.optimize(cfg, fixed_work=fixed, multilabel=M != 2, trace_level=E.TRACE_EM)
         got = ctx.optimize(cfg, fixed_work=fixed, multilabel=M != 2, trace_level=E.TRACE_EM,
                            active_set=True)
-        assert got.stats["active_set"] == 1
+        # (grid graphs with two labels; brick graphs keep the dense loop)
+        assert got.stats["active_set"] == (0 if brick else 1)
         same(got, want, full=False)
         assert got.stats["map_iters_total"] == want.stats["map_iters_total"]
     # a full trace falls back to the dense loop (every row is needed)
