@@ -490,6 +490,9 @@ def run_slice(args, E, torch, d: Dist):
                                 "changed are re-evaluated; identical results, less than the "
                                 "reference's per-iteration work)") if act else
                                "dense (every vertex and hood, every MAP iteration)",
+                   "structure": (f"packed (adjacency x{r.stats['packed_layout'] // 100}, "
+                                 f"hood x{r.stats['packed_layout'] % 100})"
+                                 if r.stats["packed_layout"] else "csr"),
                    "timing": "CUDA events on the library stream around each optimize(); "
                              "max over ranks"},
         "vertex_label_evals_per_s": d.sum(M * S * maps) / total_dev_s,

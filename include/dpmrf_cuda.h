@@ -111,6 +111,9 @@ typedef struct dpmrf_run_stats {
   int32_t graphs;            /* 1: EM iterations replayed from CUDA graphs */
   int32_t device_loop;       /* 1: the result came from the device-resident EM loop */
   uint32_t device_log_fallbacks; /* reruns because a device log(sigma) differed from the host's */
+  uint32_t packed_layout;    /* structure layout of the MAP loop: 100 * adjacency slots + hood
+                                slots (0: the CSR itself) */
+  uint32_t reserved0;
 } dpmrf_run_stats;
 
 /* ---- context ------------------------------------------------------------ */

@@ -46,7 +46,7 @@ class CRunStats(ct.Structure):
                 ("kernel_launches", U64), ("em_iters", I32), ("map_iters_total", I32),
                 ("series", U64), ("map_loop_ms", F64), ("map_loop_launches", U64),
                 ("active_set", I32), ("graphs", I32), ("device_loop", I32),
-                ("device_log_fallbacks", U32)]
+                ("device_log_fallbacks", U32), ("packed_layout", U32), ("reserved0", U32)]
 
 
 class CPhantomSpec(ct.Structure):

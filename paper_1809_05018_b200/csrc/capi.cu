@@ -675,6 +675,7 @@ bool run_optimize(dpmrf_context* ctx, const dpmrf_optimizer_config* cfg,
       CK(cudaMemsetAsync(a.act_cnt, 0, ncnt * 4, st));
     }
     ctx->stats.active_set = active ? 1 : 0;
+    ctx->stats.packed_layout = uint32_t(a.adj_k * 100 + a.hood_k);
     // [em_done, pending_done, em_count, pad | per-MAP-iteration counters]
     uint32_t* state = ctx->unconv.ensure(uint64_t(map_max) + 4);
     a.unconv = state + 4;

@@ -1105,7 +1105,13 @@ __global__ void k_pack_stats(const uint32_t* __restrict__ g_off, const uint32_t*
     const uint32_t lo = s_off[h], hi = uint64_t(s_off[h + 1]) < S ? s_off[h + 1] : uint32_t(S);
     if (hi < lo) continue;
     size = max(size, hi - lo);
-    if (hi > lo) span = max(span, h_mem[hi - 1] - h_mem[lo]);
+    if (hi > lo) {
+      // the packed layout stores members as deltas from the first, so it
+      // needs them ascending: an out-of-order hood disables it
+      bool asc = true;
+      for (uint32_t i = lo + 1; i < hi; ++i) asc &= h_mem[i] >= h_mem[i - 1];
+      span = max(span, asc ? h_mem[hi - 1] - h_mem[lo] : 0xFFFFFFFFu);
+    }
   }
   atomicMax(stats + 0, deg);
   atomicMax(stats + 1, dist);

@@ -137,6 +137,26 @@ def test_handmade_hoods_empty_and_uncovered(ctx, orc):
         same(orc.optimize(g, h, cfg, fixed_work=True), ctx.optimize(to_cfg(cfg), fixed_work=True))
 
 
+def test_handmade_hoods_out_of_order(ctx, orc):
+    # members not ascending (the API allows any order; the sum folds in slot
+    # order): the delta-packed hood layout must not be used for them
+    rng = np.random.default_rng(11)
+    n = 40
+    g = graph_from_edges(n, [(v, v + 1) for v in range(n - 1)], rng.uniform(0, 255, n))
+    mem, off = [], [0]
+    for v in range(n):
+        m = [v] + [u for u in (v - 1, v + 1) if 0 <= u < n]
+        rng.shuffle(m)
+        mem += m
+        off.append(len(mem))
+    h = Hoods(np.array(off, np.uint32), np.array(mem, np.uint32))
+    upload(ctx, g, h)
+    for seed in range(4):
+        cfg = Config(rng_seed=seed, em_max_iters=5)
+        same(orc.optimize(g, h, cfg), ctx.optimize(to_cfg(cfg)))
+        same(orc.optimize(g, h, cfg, fixed_work=True), ctx.optimize(to_cfg(cfg), fixed_work=True))
+
+
 def test_large_hood_leaf_tree_fold(ctx, orc):
     # a star hub with > 1024 neighbors: hood sums switch to the leaf/tree fold
     n = 2600
@@ -347,6 +367,43 @@ def test_opt_in_layouts_agree(env, val, monkeypatch):
     finally:
         c.close()
         base.close()
+
+
+def test_grids_with_holes_vs_oracle(ctx, orc):
+    """Row-major grids with missing edges and handmade hoods (uncovered
+    vertices, members up to three rows below and columns -1..3 of the first)
+    -- the packed layouts' delta ranges at small strides -- and low-degree
+    random graphs with one-member hoods."""
+    rng = np.random.default_rng(21)
+    layouts = set()
+    for i in range(30):
+        n = int(rng.integers(2, 80))
+        if i % 2:
+            g = random_graph(rng, n, float(rng.uniform(0.01, 0.06)))
+            h = Hoods(np.arange(n + 1, dtype=np.uint32), np.arange(n, dtype=np.uint32))
+        else:
+            W = int(rng.integers(2, 9))
+            n = W * int(rng.integers(1, 9))
+            edges = [(v, v + 1) for v in range(n) if (v + 1) % W and v + 1 < n and rng.random() < 0.8]
+            edges += [(v, v + W) for v in range(n - W) if rng.random() < 0.8]
+            g = graph_from_edges(n, edges, rng.uniform(0, 255, n))
+            off, mem = [0], []
+            for v in range(n):
+                if rng.random() < 0.15:
+                    continue
+                cand = (v + 1, v + 3, v + W, v + W + 1, v + 2 * W - 1, v + 3 * W + 2)
+                m = sorted({v} | {u for u in cand if u < n and rng.random() < 0.6})
+                mem += m
+                off.append(len(mem))
+            h = Hoods(np.array(off, np.uint32), np.array(mem, np.uint32))
+        upload(ctx, g, h)
+        cfg = Config(rng_seed=int(rng.integers(0, 2**62)), em_max_iters=int(rng.integers(1, 6)),
+                     beta=float(rng.uniform(0, 3)))
+        for fixed in (False, True):
+            r = ctx.optimize(to_cfg(cfg), fixed_work=fixed)
+            same(orc.optimize(g, h, cfg, fixed_work=fixed), r)
+            layouts.add(r.stats["packed_layout"])
+    assert 408 in layouts
 
 
 @pytest.mark.parametrize("size,brick,M", [(4096, False, 2), (4096, True, 3)])
