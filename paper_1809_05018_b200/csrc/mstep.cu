@@ -614,16 +614,38 @@ __global__ void __launch_bounds__(32) k_fold_sum_ldg(FoldArgs a) {
   pdl_wait();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   PROBE_BLK(0, 1);
-  if (em_skipped(a.unconv)) return;
   const uint32_t M = a.M;
-  const uint32_t* n = a.layout;
-  const uint32_t* label_start = a.layout + M;
-  const uint32_t* leaf_start = a.layout + 2 * M + 1;
-  const uint32_t total = leaf_start[M + 1];
+  // The layout, the skip flag and the MAP counters in ONE round trip (a lane
+  // per word) when they fit a warp, instead of a chain of dependent loads
+  // (skip flag -> leaf bounds -> series bounds) before the leaves' addresses.
+  const uint32_t nlay = 4 * M + 4;
+  const bool in_warp = nlay <= 32 && a.map_max <= 32;
+  uint32_t lw = 0, cw = 1, done = 0;
+  if (in_warp) {
+    if (lane < nlay) lw = a.layout[lane];
+    if (a.unconv) {
+      done = a.unconv[kEmDone];
+      if (!a.fixed && lane < uint32_t(a.map_max)) cw = a.unconv[lane];
+    }
+  } else {
+    done = a.unconv ? a.unconv[kEmDone] : 0u;
+  }
+  if (done) return;
+  auto lay = [&](uint32_t i) {
+    return in_warp ? __shfl_sync(0xffffffffu, lw, i) : a.layout[i];
+  };
+  const uint32_t total = lay(3 * M + 2);  // leaf_start[M + 1]
   const double2* base[kLPB];
   uint32_t len[kLPB], off[kLPB], n2[kLPB];
   int T = 0;
-  if (a.unconv) T = executed_iters(a.unconv, a.map_max, a.fixed);
+  if (a.unconv) {
+    if (!in_warp || a.fixed) {
+      T = executed_iters(a.unconv, a.map_max, a.fixed);
+    } else {  // executed_iters: one past the first zero counter, else map_max
+      const uint32_t z = __ballot_sync(0xffffffffu, lane < uint32_t(a.map_max) && cw == 0);
+      T = z ? __ffs(z) : a.map_max;
+    }
+  }
 #pragma unroll
   for (int j = 0; j < kLPB; ++j) {
     const uint32_t leaf = blockIdx.x * kLPB + j;
@@ -632,13 +654,14 @@ __global__ void __launch_bounds__(32) k_fold_sum_ldg(FoldArgs a) {
     n2[j] = 0;
     base[j] = nullptr;
     if (leaf < total) {
-      const uint32_t sr = series_of(leaf_start, M + 1, leaf);
-      const uint64_t b = uint64_t(leaf - leaf_start[sr]) * kFoldLeaf;
+      uint32_t sr = 0;  // series_of over leaf_start = layout[2M+1 ..]
+      while (sr < M && leaf >= lay(2 * M + 2 + sr)) ++sr;
+      const uint64_t b = uint64_t(leaf - lay(2 * M + 1 + sr)) * kFoldLeaf;
       const double* src;
       uint64_t slen;
       if (sr < M) {
-        src = a.x + label_start[sr] + b;
-        slen = n[sr];
+        src = a.x + lay(M + sr) + b;
+        slen = lay(sr);
       } else {  // the hood-energy row of the last executed MAP iteration (optimize.cpp:64-65)
         src = a.hist + uint64_t((T - 1) % a.ring) * a.Hs + b;
         slen = a.Hs;
