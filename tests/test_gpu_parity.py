@@ -191,6 +191,25 @@ def test_phantom_fixed_work_vs_oracle(ctx, orc, size, block, brick, M):
         same(orc.optimize(g, h, Config(rng_seed=5)), ctx.optimize(to_cfg(Config(rng_seed=5))))
 
 
+@pytest.mark.parametrize("map_max,window", [(31, 2), (32, 5), (33, 3), (40, 1)])
+def test_long_map_loops_vs_oracle(ctx, orc, map_max, window):
+    """MAP loops around the warp width: the sum pass reads the per-iteration
+    counters one lane each up to 32 iterations, a loop beyond (early exits
+    and fixed work)."""
+    from paper_1809_05018_b200 import inputs
+    sl = inputs.synthetic_slice(256, 8, seed=3)
+    g = Graph(sl.graph.offsets, sl.graph.neighbors, sl.graph.region_mean)
+    ctx.set_graph(sl.graph)
+    ctx.build_neighborhoods(sl.cliques)
+    hd = ctx.get_hoods()
+    h = Hoods(hd.offsets, hd.members)
+    for tol in (1e-6, 1e-300):  # (1e-300: only bit-equal sums converge)
+        cfg = Config(rng_seed=8, em_max_iters=4, map_max_iters=map_max, convergence_window=window,
+                     convergence_tol=tol)
+        for fixed in (False, True):
+            same(orc.optimize(g, h, cfg, fixed_work=fixed), ctx.optimize(to_cfg(cfg), fixed_work=fixed))
+
+
 def test_config_b_against_reference(ctx, ref):
     """Config B shape (2560^2, block 8) vs the reference library itself:
     reference semantics, full trace; and 2 EM of fixed work."""
