@@ -1113,10 +1113,18 @@ __global__ void k_pack_stats(const uint32_t* __restrict__ g_off, const uint32_t*
       span = max(span, asc ? h_mem[hi - 1] - h_mem[lo] : 0xFFFFFFFFu);
     }
   }
-  atomicMax(stats + 0, deg);
-  atomicMax(stats + 1, dist);
-  atomicMax(stats + 2, size);
-  atomicMax(stats + 3, span);
+  // one atomic per warp and statistic (not per thread: ~300k same-address
+  // atomics cost more than the scan itself)
+  deg = __reduce_max_sync(0xffffffffu, deg);
+  dist = __reduce_max_sync(0xffffffffu, dist);
+  size = __reduce_max_sync(0xffffffffu, size);
+  span = __reduce_max_sync(0xffffffffu, span);
+  if ((threadIdx.x & 31) == 0) {
+    if (deg) atomicMax(stats + 0, deg);
+    if (dist) atomicMax(stats + 1, dist);
+    if (size) atomicMax(stats + 2, size);
+    if (span) atomicMax(stats + 3, span);
+  }
 }
 
 template <int K>
