@@ -1231,8 +1231,8 @@ __global__ void __launch_bounds__(kClThreads) k_fold_sq_cluster(FoldArgs a, uint
 // sum-pass leaves) as ONE persistent kernel.  Lane j < C of a one-warp block
 // is a chain that walks the leaves gid, gid + G*C, ... (gid = block*C + j);
 // each leaf streams through the lane's ring of NS shared-memory slots in
-// 256-double quarters (one cp.async.bulk + one mbarrier per slot), the next
-// quarters in flight while the chain folds the current one, so every SM
+// kQuarter-double parts (one cp.async.bulk + one mbarrier per slot), the next
+// parts in flight while the chain folds the current one, so every SM
 // keeps ~30 chains busy instead of running whole-leaf waves.  After each
 // round the warp counts its leaves into their chunks (chunk_tickets): the
 // warp completing a chunk folds its root, the warp completing a series folds
@@ -1255,8 +1255,19 @@ constexpr int kStreamChains = DPMRF_STREAM_C;  // chains (lanes) per warp
 constexpr int kStreamWarps = DPMRF_STREAM_W;   // warps per block (independent rings)
 
 constexpr int kStreamSlots = DPMRF_STREAM_NS;  // ring slots per chain
-constexpr uint32_t kQuarter = 256;
+#ifndef DPMRF_STREAM_Q
+#define DPMRF_STREAM_Q 128  // (128: 4 one-warp blocks per SM, one per scheduler; 256
+                            //  fits only 2 -- D: M-step 136.6 -> 122 us/EM, +1%)
+#endif
+constexpr uint32_t kQuarter = DPMRF_STREAM_Q;  // doubles per streamed part of a leaf
+constexpr uint32_t kParts = kFoldLeaf / kQuarter;  // parts per leaf (power of two)
+static_assert(kParts * kQuarter == kFoldLeaf && (kParts & (kParts - 1)) == 0 && kQuarter % 16 == 0,
+              "a leaf streams in equal power-of-two parts");
 constexpr uint32_t kSlotPitch = kQuarter + 2;  // doubles per slot (16-byte aligned superset)
+#ifndef DPMRF_STREAM_PFENCE
+#define DPMRF_STREAM_PFENCE 1
+#endif
+constexpr bool kStreamProxyFence = DPMRF_STREAM_PFENCE != 0;
 
 struct StreamCounters {  // zeroed once; re-armed by the kernel itself
   uint32_t gen;     // launches completed (the ready flags of launch g read g + 1)
@@ -1331,7 +1342,7 @@ __device__ void stream_tasks(const FoldArgs& a, const StreamView& v, double* rin
   const double* csrc = nullptr;
   auto issue = [&](uint32_t pos) {
     if (lane >= uint32_t(C)) return;
-    const uint32_t k = pos >> 2, qq = pos & 3u;
+    const uint32_t k = pos / kParts, qq = pos % kParts;
     if (k >= rounds) return;
     const uint32_t t = gid + k * stride;
     if (t >= ntask || (t >= nsum && t < P)) return;
@@ -1372,8 +1383,8 @@ __device__ void stream_tasks(const FoldArgs& a, const StreamView& v, double* rin
       }
     }
 #pragma unroll 1
-    for (uint32_t qq = 0; qq < 4; ++qq) {
-      const uint32_t pos = 4 * k + qq;
+    for (uint32_t qq = 0; qq < kParts; ++qq) {
+      const uint32_t pos = kParts * k + qq;
       if (has && qq * kQuarter < len) {
         const uint32_t slot = pos % NS;
         mbar_wait_par(bars + slot, (ph >> slot) & 1u);
@@ -1394,7 +1405,7 @@ __device__ void stream_tasks(const FoldArgs& a, const StreamView& v, double* rin
         }
       }
       // the slot is free again: refill it with the quarter NS positions ahead
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (kStreamProxyFence) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(pos + NS);
     }
     if (has) {

@@ -4,7 +4,7 @@
 # a variant "name:VAR=val" runs build/variants/name.so with VAR=val in the environment
 O=$1; CFGS=$2; shift 2
 mkdir -p $O
-for round in 1 2 3; do
+for round in $(seq 1 ${ROUNDS:-3}); do
 for v in "$@"; do
   for c in $CFGS; do
     steps=10; [ "$c" = D ] && steps=5
