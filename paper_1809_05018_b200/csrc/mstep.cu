@@ -45,21 +45,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
 //                      fold_range per run, kernels.hpp:226-253)
 //   dpp::reduce        kernels.hpp:124-139 (total energy, optimize.cpp:64-65)
 // Launches per EM iteration: the grouping (k_label_scatter_small, or
-// k_tile_chunks / k_tile_offsets / k_label_tiles on large graphs), then the
+// k_tile_chunks / k_tile_offsets / k_label_scatter_warp on large graphs), then the
 // folds: k_fold_sum_ldg + k_fold_sq_cluster (few leaves), k_mstep_stream
 // (many leaves), each finishing with the pairwise trees.  The per-tile label counts come from the
 // last executed vertex pass (double-buffered by iteration parity).
 // ---------------------------------------------------------------------------
-// Stable rank of each vertex among the tile's vertices of the same label:
-// __match_any_sync gives the in-warp rank, per-warp counts in shared memory
-// the cross-warp offset.  kPass 0 counts, kPass 1 scatters the region mean to
-// its position in the label-grouped array x (== stable sort_by_key(labels)).
-template <int kPass>
+// Label counts per 256-vertex tile (when the vertex pass did not count
+// them): __match_any_sync groups the warp's lanes by label, per-warp counts
+// in shared memory are summed per tile.
 __global__ void __launch_bounds__(kTileThreads)
-    k_label_tiles(const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
-                  int map_max, int fixed, uint32_t R, uint32_t M, const double* __restrict__ mean,
-                  uint32_t* __restrict__ tile_counts, const uint32_t* __restrict__ tile_base,
-                  const uint32_t* __restrict__ layout, double* __restrict__ x) {
+    k_label_counts(const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
+                   int map_max, int fixed, uint32_t R, uint32_t M,
+                   uint32_t* __restrict__ tile_counts) {
   extern __shared__ uint32_t wcnt[];  // [warp][M]
   pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -76,22 +73,64 @@ __global__ void __launch_bounds__(kTileThreads)
   const uint32_t rank_in_warp = __popc(peers & ((1u << lane) - 1u));
   if (valid && rank_in_warp == 0) wcnt[warp * M + l] = __popc(peers);
   __syncthreads();
-  if (kPass == 1) {
-    if (valid) {
-      uint32_t before = 0;
-      for (int w = 0; w < warp; ++w) before += wcnt[w * M + l];
-      const uint32_t* label_start = layout + M;
-      x[label_start[l] + tile_base[tile * M + l] + before + rank_in_warp] = mean[v];
-    }
-  } else {
-    for (uint32_t q = threadIdx.x; q < M; q += kTileThreads) {
-      uint32_t c = 0;
-      for (int w = 0; w < kWarps; ++w) c += wcnt[w * M + q];
-      tile_counts[tile * M + q] = c;
-    }
+  for (uint32_t q = threadIdx.x; q < M; q += kTileThreads) {
+    uint32_t c = 0;
+    for (int w = 0; w < kWarps; ++w) c += wcnt[w * M + q];
+    tile_counts[tile * M + q] = c;
   }
 }
 
+// Stable grouping of the region means by label (== stable sort_by_key of the
+// labels, engine.cpp:201) with one WARP per 256-vertex tile (eight tiles per
+// block): the warp walks its tile in vertex order, 32 at a time; a lane's
+// position is its label's start + the tile's offset for that label + the
+// warp's running count of that label + its rank among the lanes of the same
+// label (__match_any_sync).  The running counts live in shared memory, so the
+// stable rank needs no block barrier; the tile's means and labels are loaded
+// up front (eight independent loads per lane in flight).  (One block per tile
+// with a per-warp count exchange: 41.8 us at 16384^2; this: M-step -15 us/EM.)
+constexpr int kScatterIters = kTileVerts / 32;
+__global__ void __launch_bounds__(kTileThreads)
+    k_label_scatter_warp(const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
+                         int map_max, int fixed, uint32_t R, uint32_t M,
+                         const double* __restrict__ mean, const uint32_t* __restrict__ tile_base,
+                         const uint32_t* __restrict__ layout, double* __restrict__ x) {
+  extern __shared__ uint32_t run_all[];  // [warp][M]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t tile = uint64_t(blockIdx.x) * (kTileThreads / 32) + warp;
+  uint32_t* run = run_all + warp * M;
+  for (uint32_t l = lane; l < M; l += 32) run[l] = 0;
+  const uint64_t v0 = tile * kTileVerts + lane;
+  double mv[kScatterIters];
+#pragma unroll
+  for (int i = 0; i < kScatterIters; ++i) {  // (means are static: before the wait)
+    const uint64_t v = v0 + 32 * i;
+    mv[i] = v < R ? mean[v] : 0.0;
+  }
+  pdl_wait();
+  if (em_skipped(unconv)) return;
+  const uint8_t* lab = final_labels(lab_even, lab_odd, unconv, map_max, fixed);
+  uint32_t lv[kScatterIters];
+#pragma unroll
+  for (int i = 0; i < kScatterIters; ++i) {
+    const uint64_t v = v0 + 32 * i;
+    lv[i] = v < R ? lab[v] : 0xFFFFFFFFu;
+  }
+  const uint32_t* label_start = layout + M;
+  const uint32_t* tb = tile_base + tile * M;
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < kScatterIters; ++i) {
+    const uint32_t l = lv[i];
+    const unsigned peers = __match_any_sync(0xffffffffu, l);
+    const uint32_t rank = __popc(peers & lt);
+    if (l != 0xFFFFFFFFu) x[label_start[l] + tb[l] + run[l] + rank] = mv[i];
+    __syncwarp();
+    if (l != 0xFFFFFFFFu && rank == 0) run[l] += __popc(peers);
+    __syncwarp();
+  }
+}
 
 __global__ void __launch_bounds__(kTileThreads)
     k_label_scatter_small(const uint8_t* lab_even, const uint8_t* lab_odd,
@@ -1608,9 +1647,8 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
   if (scattered) {
     // the grouping already ran beside the last hood pass (launch_map_fused)
   } else if (tiles && !counts_ready) {
-    k_label_tiles<0><<<tiles, kTileThreads, smem, s>>>(lab_even, lab_odd, unconv, map_max, fixed,
-                                                       R, M, mean, counts, nullptr, nullptr,
-                                                       nullptr);
+    k_label_counts<<<tiles, kTileThreads, smem, s>>>(lab_even, lab_odd, unconv, map_max, fixed,
+                                                     R, M, counts);
     CK_LAUNCH();
     ++n;
   }
@@ -1636,8 +1674,9 @@ void mstep_core(const double* mean, uint32_t R, uint32_t M, const uint8_t* lab_e
     ++n;
   }
   if (!scattered && tiles && uint64_t(tiles) * M > kSelfScanMax) {
-    launch_pdl(k_label_tiles<1>, dim3(tiles), dim3(kTileThreads), smem, s, lab_even, lab_odd,
-               unconv, map_max, fixed, R, M, mean, (uint32_t*)nullptr,
+    constexpr uint32_t kTilesPerBlock = kTileThreads / 32;
+    launch_pdl(k_label_scatter_warp, dim3((tiles + kTilesPerBlock - 1) / kTilesPerBlock),
+               dim3(kTileThreads), smem, s, lab_even, lab_odd, unconv, map_max, fixed, R, M, mean,
                (const uint32_t*)tile_base, (const uint32_t*)layout, x);
     ++n;
   }

@@ -243,7 +243,7 @@ __device__ __forceinline__ uint32_t head_len(uint32_t off, uint32_t n) {
   return min(n, to_boundary);
 }
 
-// own label counts (stable tile ranks as k_label_tiles<0>) + per-tile counts
+// own label counts (stable tile ranks as k_label_counts) + per-tile counts
 __global__ void __launch_bounds__(256)
     k_part_count(const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
                  int map_max, int fixed, uint32_t vb, uint32_t ve, uint32_t M,
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(1024)
   (void)carry_s;
 }
 
-// stable scatter of this rank's region means into x (k_label_tiles<1>)
+// stable scatter of this rank's region means into x (one block per tile)
 __global__ void __launch_bounds__(256)
     k_part_scatter(const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
                    int map_max, int fixed, uint32_t vb, uint32_t ve, uint32_t M,
