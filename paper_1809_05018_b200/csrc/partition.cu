@@ -332,30 +332,49 @@ __global__ void __launch_bounds__(1024)
   (void)carry_s;
 }
 
-// stable scatter of this rank's region means into x (one block per tile)
+// stable scatter of this rank's region means into x, one WARP per 256-vertex
+// tile (eight tiles per block), as k_label_scatter_warp (mstep.cu): the warp
+// walks its tile in vertex order with running per-label counts in shared
+// memory; tile_base holds each tile's absolute start per label
 __global__ void __launch_bounds__(256)
     k_part_scatter(const uint8_t* lab_even, const uint8_t* lab_odd, const uint32_t* unconv,
                    int map_max, int fixed, uint32_t vb, uint32_t ve, uint32_t M,
                    const double* __restrict__ mean, const uint32_t* __restrict__ tile_base,
                    double* __restrict__ x) {
-  extern __shared__ uint32_t wcnt[];  // [warp][M]
+  extern __shared__ uint32_t run_all[];  // [warp][M]
+  constexpr int kIters = 256 / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t tile = uint64_t(blockIdx.x) * 8 + warp;
+  uint32_t* run = run_all + warp * M;
+  for (uint32_t l = lane; l < M; l += 32) run[l] = 0;
+  const uint64_t v0 = vb + tile * 256 + lane;
+  double mv[kIters];
+#pragma unroll
+  for (int i = 0; i < kIters; ++i) {  // (means are static: before the wait)
+    const uint64_t v = v0 + 32 * i;
+    mv[i] = v < ve ? mean[v] : 0.0;
+  }
   pdl_wait();
   if (part_em_skipped(unconv)) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint8_t* lab = part_final_labels(lab_even, lab_odd, unconv, map_max, fixed);
-  for (uint32_t i = threadIdx.x; i < 8 * M; i += 256) wcnt[i] = 0;
-  __syncthreads();
-  const uint32_t v = vb + blockIdx.x * 256 + threadIdx.x;
-  const bool valid = v < ve;
-  const uint32_t l = valid ? lab[v] : 0xFFFFFFFFu;
-  const unsigned peers = __match_any_sync(0xffffffffu, l);
-  const uint32_t rank_in_warp = __popc(peers & ((1u << lane) - 1u));
-  if (valid && rank_in_warp == 0) wcnt[warp * M + l] = __popc(peers);
-  __syncthreads();
-  if (valid) {
-    uint32_t before = 0;
-    for (int w = 0; w < warp; ++w) before += wcnt[w * M + l];
-    x[tile_base[uint64_t(blockIdx.x) * M + l] + before + rank_in_warp] = mean[v];
+  uint32_t lv[kIters];
+#pragma unroll
+  for (int i = 0; i < kIters; ++i) {
+    const uint64_t v = v0 + 32 * i;
+    lv[i] = v < ve ? lab[v] : 0xFFFFFFFFu;
+  }
+  const uint32_t* tb = tile_base + tile * M;
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < kIters; ++i) {
+    const uint32_t l = lv[i];
+    const unsigned peers = __match_any_sync(0xffffffffu, l);
+    const uint32_t rank = __popc(peers & lt);
+    if (l != 0xFFFFFFFFu) x[tb[l] + run[l] + rank] = mv[i];
+    __syncwarp();
+    if (l != 0xFFFFFFFFu && rank == 0) run[l] += __popc(peers);
+    __syncwarp();
   }
 }
 
@@ -981,7 +1000,7 @@ bool run_partitioned(dpmrf_group* g, const dpmrf_optimizer_config* cfg, const dp
                    p.ms.tile_base.get());
         k += 2;
         if (ntiles) {
-          launch_pdl(k_part_scatter, dim3(ntiles), dim3(256), wsm, st,
+          launch_pdl(k_part_scatter, dim3((ntiles + 7) / 8), dim3(256), wsm, st,
                      (const uint8_t*)p.lab[parity].get(), (const uint8_t*)p.lab[parity ^ 1].get(),
                      u, map_max, fixed, p.vb, p.ve, M, (const double*)p.a.mean,
                      (const uint32_t*)p.ms.tile_base.get(), p.ms.x.get());
