@@ -95,6 +95,18 @@ void initial_params(uint32_t M, uint64_t seed, double* mu, double* sigma) {
 }  // namespace dpmrf_b200
 
 // ---- structure preparation ---------------------------------------------------
+// The packed-layout rule (host side; dev_adj_k / dev_hood_k in engine.cu are
+// the same rule on the device): neighbor lists of <= 4 / 8 with |u - v| <
+// 2^15 pack as int16 deltas; hoods of <= 9 / 13 / 17 ascending members
+// spanning < 2^16 pack as u16 deltas from the first (the packed hood pass
+// indexes hoods with 32 bits).
+void choose_packing(const uint32_t* hs, uint64_t Hs, bool use_k12, int* adj_k, int* hood_k) {
+  *adj_k = *hood_k = 0;
+  if (hs[1] <= 32767u) *adj_k = hs[0] <= 4 ? 4 : (hs[0] <= 8 ? 8 : 0);
+  if (hs[3] < 0xFFFFu && Hs > 0 && Hs < (uint64_t(1) << 32) - 256)
+    *hood_k = hs[2] <= 9 ? 8 : (hs[2] <= 13 && use_k12 ? 12 : (hs[2] <= 17 ? 16 : 0));
+}
+
 void dpmrf_context::prepare() {
   if (prepared) {
     if (prep_status != DPMRF_OK) fail(prep_status, prep_msg);
@@ -102,14 +114,25 @@ void dpmrf_context::prepare() {
   }
   need(has_graph, DPMRF_INVALID_ARGUMENT, "no region graph uploaded");
   need(has_hoods, DPMRF_INVALID_ARGUMENT, "no neighborhoods uploaded");
-  // validation and the packing statistics in one batch, one host sync
+  // ONE batch and one host sync: validation, the packing statistics, the
+  // cover flags and -- chosen on the device from those statistics -- the
+  // packed layouts (buffers sized for the largest K).  Every kernel of the
+  // batch clamps or skips what an invalid input would make unsafe; the
+  // error bits are checked after the sync, before anything else runs.
   uint32_t* err = prep_err.ensure(6);  // [error bits, empty hoods | deg, dist, size, span]
   CK(cudaMemsetAsync(err, 0, 6 * sizeof(uint32_t), stream));
   launch_validate(g_off.get(), g_nbr.get(), R, A, h_off.get(), h_mem.get(), H, S, err, err + 1,
                   stream);
-  if (use_packed && R > 0)
+  const bool pack = use_packed && R > 0;
+  const uint64_t Hp_max = (H + 255) / 256 * 256;
+  if (pack) {
     launch_pack_stats(g_off.get(), g_nbr.get(), R, A, h_off.get(), h_mem.get(), H, S, err + 2,
                       stream);
+    launch_pack_auto(g_off.get(), g_nbr.get(), R, h_off.get(), h_mem.get(), H, err, use_k12 ? 1 : 0,
+                     adj_pk.ensure(uint64_t(R) * 8), hood_base.ensure(Hp_max ? Hp_max : 1),
+                     hood_pk.ensure((Hp_max ? Hp_max : 1) * 16), stream);
+  }
+  launch_cover(h_mem.get(), S, cover.ensure(R), R, stream);
   uint32_t h_err[6];
   CK(cudaMemcpyAsync(h_err, err, sizeof h_err, cudaMemcpyDeviceToHost, stream));
   sync();
@@ -129,7 +152,6 @@ void dpmrf_context::prepare() {
     prep_msg = "region graph offsets are not a valid CSR";
   }
   if (prep_status != DPMRF_OK) fail(prep_status, prep_msg);
-  launch_cover(h_mem.get(), S, cover.ensure(R), R, stream);
   const uint32_t empties = h_err[1];
   Hs = H - empties;
   series_alias = empties == 0;
@@ -139,19 +161,16 @@ void dpmrf_context::prepare() {
   // packed layouts when every neighbor list / hood fits (all grid and brick
   // oversegmentations do); otherwise the kernels read the CSR directly
   adj_k = hood_k = 0;
-  if (use_packed && R > 0) {
-    const uint32_t* hs = h_err + 2;
-    const uint32_t* so = series_alias ? h_off.get() : s_off_buf.get();
-    if (hs[1] <= 32767u) adj_k = hs[0] <= 4 ? 4 : (hs[0] <= 8 ? 8 : 0);
-    // (the packed hood pass indexes hoods with 32 bits)
-    if (hs[3] < 0xFFFFu && Hs > 0 && Hs < (uint64_t(1) << 32) - 256)
-      hood_k = hs[2] <= 9 ? 8 : (hs[2] <= 13 && use_k12 ? 12 : (hs[2] <= 17 ? 16 : 0));
-    if (adj_k) launch_pack_adjacency(g_off.get(), g_nbr.get(), R, adj_k,
-                                     adj_pk.ensure(uint64_t(R) * adj_k), stream);
-    // (rows padded to whole 256-hood tiles)
-    const uint64_t Hp = (Hs + 255) / 256 * 256;
-    if (hood_k) launch_pack_hoods(so, h_mem.get(), Hs, hood_k, hood_base.ensure(Hp),
-                                  hood_pk.ensure(Hp * hood_k), stream);
+  if (pack) {
+    choose_packing(h_err + 2, Hs, use_k12, &adj_k, &hood_k);
+    // (the device built both layouts with this K already -- the hood rows
+    //  only when no hood is empty; then they are built from the compacted
+    //  series offsets here, rows padded to whole 256-hood tiles)
+    if (hood_k && !series_alias) {
+      const uint64_t Hp = (Hs + 255) / 256 * 256;
+      launch_pack_hoods(s_off_buf.get(), h_mem.get(), Hs, hood_k, hood_base.ensure(Hp),
+                        hood_pk.ensure(Hp * hood_k), stream);
+    }
   }
   // (no sync: everything that reads these runs later on the same stream)
 }

@@ -238,10 +238,14 @@ __global__ void k_validate(const uint32_t* __restrict__ g_off, const uint32_t* _
   if (empties) atomicAdd(empty_hoods, empties);
 }
 
-__global__ void k_cover(const uint32_t* __restrict__ h_mem, uint64_t S, uint8_t* cover) {
+// (runs before prepare() has checked the members: out-of-range ones skipped)
+__global__ void k_cover(const uint32_t* __restrict__ h_mem, uint64_t S, uint8_t* cover,
+                        uint32_t R) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < S; i += stride)
-    cover[h_mem[i]] = 1;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < S; i += stride) {
+    const uint32_t m = h_mem[i];
+    if (m < R) cover[m] = 1;
+  }
 }
 
 __global__ void k_nonempty_flags(const uint32_t* __restrict__ h_off, uint64_t H, uint32_t* f) {
@@ -1153,6 +1157,47 @@ __global__ void k_pack_hoods(const uint32_t* __restrict__ s_off, const uint32_t*
     out[h * K + k] = lo + 1 + k < hi ? static_cast<uint16_t>(h_mem[lo + 1 + k] - b) : uint16_t(0xFFFF);
 }
 
+// Packed layouts chosen ON THE DEVICE from the validation / statistics words
+// [error bits, empty hoods, deg, dist, size, span] of the same prepare()
+// batch -- the rule of choose_packing (capi.cu), so the host's sync finds the
+// layouts already built.  Nothing is written when the inputs are invalid or
+// (hoods) when empty hoods need the compacted series offsets.
+__device__ __forceinline__ int dev_adj_k(const uint32_t* e) {
+  if (e[0]) return 0;
+  return e[3] <= 32767u ? (e[2] <= 4 ? 4 : (e[2] <= 8 ? 8 : 0)) : 0;
+}
+__device__ __forceinline__ int dev_hood_k(const uint32_t* e, uint64_t H, int use_k12) {
+  if (e[0] || e[1]) return 0;
+  if (!(e[5] < 0xFFFFu && H > 0 && H < (uint64_t(1) << 32) - 256)) return 0;
+  return e[4] <= 9 ? 8 : (e[4] <= 13 && use_k12 ? 12 : (e[4] <= 17 ? 16 : 0));
+}
+__global__ void k_pack_adjacency_auto(const uint32_t* __restrict__ g_off,
+                                      const uint32_t* __restrict__ g_nbr, uint32_t R,
+                                      const uint32_t* e, int16_t* __restrict__ out) {
+  const uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= R) return;
+  const int K = dev_adj_k(e);
+  if (K == 0) return;
+  const uint32_t lo = g_off[v], hi = g_off[v + 1];
+  for (int k = 0; k < K; ++k)
+    out[v * K + k] = lo + k < hi ? static_cast<int16_t>(int64_t(g_nbr[lo + k]) - int64_t(v))
+                                 : int16_t(INT16_MIN);
+}
+__global__ void k_pack_hoods_auto(const uint32_t* __restrict__ h_off,
+                                  const uint32_t* __restrict__ h_mem, uint64_t H,
+                                  const uint32_t* e, int use_k12, uint32_t* __restrict__ base,
+                                  uint16_t* __restrict__ out) {
+  const uint64_t h = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (h >= H) return;
+  const int K = dev_hood_k(e, H, use_k12);
+  if (K == 0) return;
+  const uint32_t lo = h_off[h], hi = h_off[h + 1];
+  const uint32_t b = h_mem[lo];
+  base[h] = b;
+  for (int k = 0; k < K; ++k)
+    out[h * K + k] = lo + 1 + k < hi ? static_cast<uint16_t>(h_mem[lo + 1 + k] - b) : uint16_t(0xFFFF);
+}
+
 }  // namespace
 
 void build_vertex_series(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, uint32_t R,
@@ -1190,6 +1235,21 @@ void launch_pack_adjacency(const uint32_t* g_off, const uint32_t* g_nbr, uint32_
   else
     k_pack_adjacency<8><<<grid_for(R, 256), 256, 0, s>>>(g_off, g_nbr, R, out);
   CK_LAUNCH();
+}
+
+void launch_pack_auto(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R,
+                      const uint32_t* h_off, const uint32_t* h_mem, uint64_t H,
+                      const uint32_t* stats6, int use_k12, int16_t* adj_out, uint32_t* hood_base,
+                      uint16_t* hood_out, cudaStream_t s) {
+  if (R) {
+    k_pack_adjacency_auto<<<grid_for(R, 256), 256, 0, s>>>(g_off, g_nbr, R, stats6, adj_out);
+    CK_LAUNCH();
+  }
+  if (H) {
+    k_pack_hoods_auto<<<grid_for(H, 256), 256, 0, s>>>(h_off, h_mem, H, stats6, use_k12,
+                                                       hood_base, hood_out);
+    CK_LAUNCH();
+  }
 }
 
 void launch_pack_hoods(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, int k,
@@ -1230,7 +1290,7 @@ void launch_validate(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, u
 void launch_cover(const uint32_t* h_mem, uint64_t S, uint8_t* cover, uint32_t R, cudaStream_t s) {
   CK(cudaMemsetAsync(cover, 0, R ? R : 1, s));
   if (!S) return;
-  k_cover<<<std::min<unsigned>(grid_for(S, 256), 8 * kNumSMs), 256, 0, s>>>(h_mem, S, cover);
+  k_cover<<<std::min<unsigned>(grid_for(S, 256), 8 * kNumSMs), 256, 0, s>>>(h_mem, S, cover, R);
   CK_LAUNCH();
 }
 

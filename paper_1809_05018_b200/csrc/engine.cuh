@@ -202,6 +202,12 @@ void launch_pack_stats(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R,
                        uint32_t* stats, cudaStream_t s);
 void launch_pack_adjacency(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R, int k,
                            int16_t* out, cudaStream_t s);
+// the packed layouts with K chosen on the device from prepare()'s statistics
+// words (as choose_packing); buffers sized for the largest K (8 / 16)
+void launch_pack_auto(const uint32_t* g_off, const uint32_t* g_nbr, uint32_t R,
+                      const uint32_t* h_off, const uint32_t* h_mem, uint64_t H,
+                      const uint32_t* stats6, int use_k12, int16_t* adj_out, uint32_t* hood_base,
+                      uint16_t* hood_out, cudaStream_t s);
 void launch_pack_hoods(const uint32_t* s_off, const uint32_t* h_mem, uint64_t Hs, int k,
                        uint32_t* base, uint16_t* out, cudaStream_t s);
 // Offsets of the nonempty hoods (the runs reduce_by_key sees, engine.cpp:150).
