@@ -191,6 +191,24 @@ def test_phantom_fixed_work_vs_oracle(ctx, orc, size, block, brick, M):
         same(orc.optimize(g, h, Config(rng_seed=5)), ctx.optimize(to_cfg(Config(rng_seed=5))))
 
 
+def test_large_graph_grouping_path_vs_oracle(ctx, orc):
+    """tiles x labels > kSelfScanMax (8192) takes the large-graph grouping
+    (k_tile_chunks / k_tile_offsets / k_label_scatter_warp, one warp per
+    256-vertex tile) that otherwise only the 16384^2 bench shape reaches:
+    1024^2 block 4 (65 536 regions, 256 tiles) with 40 labels."""
+    from paper_1809_05018_b200 import inputs
+    sl = inputs.synthetic_slice(1024, 4, seed=3)
+    g = Graph(sl.graph.offsets, sl.graph.neighbors, sl.graph.region_mean)
+    ctx.set_graph(sl.graph)
+    ctx.build_neighborhoods(sl.cliques)
+    hd = ctx.get_hoods()
+    h = Hoods(hd.offsets, hd.members)
+    assert (len(g.offsets) - 1 + 255) // 256 * 40 > 8192
+    cfg = Config(num_labels=40, rng_seed=9, em_max_iters=3)
+    same(orc.optimize(g, h, cfg, fixed_work=True, allow_multilabel=True),
+         ctx.optimize(to_cfg(cfg), fixed_work=True, multilabel=True))
+
+
 @pytest.mark.parametrize("map_max,window", [(31, 2), (32, 5), (33, 3), (40, 1)])
 def test_long_map_loops_vs_oracle(ctx, orc, map_max, window):
     """MAP loops around the warp width: the sum pass reads the per-iteration
@@ -270,6 +288,32 @@ def test_errors(ctx):
         ctx.init_random(3, 4, 0)
     with pytest.raises(ValueError):
         ctx.update_parameters([0, 0, 2, 1], E.LabelParams(np.zeros(2), np.ones(2)))
+
+
+def test_invalid_csr_rejected_by_the_prepare_batch(ctx):
+    """prepare() builds the packed layouts and cover flags in the same batch as
+    the validation (before the host sees it): non-monotone offsets must still
+    come back as the reference's invalid_argument, with the context usable."""
+    g = graph_from_edges(4, [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)], [10, 12, 200, 210])
+    good = Hoods(np.array([0, 2, 4], np.uint32), np.array([0, 1, 2, 3], np.uint32))
+    bad_h = E.NeighborhoodSet(np.array([0, 3, 2, 4], np.uint32), np.array([0, 1, 2, 3], np.uint32))
+    for arrays in (False, True):
+        upload(ctx, g, good)
+        with pytest.raises(ValueError, match="neighborhood offsets"):
+            if arrays:
+                ctx.optimize_arrays(E.RegionGraph(g.offsets, g.neighbors, g.region_mean), bad_h,
+                                    E.OptimizerConfig())
+            else:
+                ctx.set_hoods(bad_h)
+                ctx.optimize(E.OptimizerConfig())
+    bad_g = E.RegionGraph(np.array([0, 3, 2, 9, 12], np.uint32), np.asarray(g.neighbors, np.uint32),
+                          np.asarray(g.region_mean, np.float64))
+    ctx.set_graph(bad_g)
+    ctx.set_hoods(E.NeighborhoodSet(good.offsets, good.members))
+    with pytest.raises(ValueError, match="region graph offsets"):
+        ctx.optimize(E.OptimizerConfig())
+    upload(ctx, g, good)  # the context recovers
+    ctx.optimize(E.OptimizerConfig(rng_seed=3))
 
 
 def test_two_vertices_per_thread_path(ctx):
