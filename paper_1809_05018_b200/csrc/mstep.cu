@@ -489,8 +489,15 @@ __device__ __forceinline__ uint32_t fetch_leaf(double* row, const double* src, u
   return off;
 }
 
+#ifndef DPMRF_FOLD_V2
+#define DPMRF_FOLD_V2 1
+#endif
+constexpr bool kFoldV2 = DPMRF_FOLD_V2 != 0;  // 16-byte shared-memory loads in the chains
+
 // Left fold of term(v[i]) over [i, end) onto acc, software-pipelined: the
-// next 16 operands are read from shared memory while 16 dependent adds retire.
+// next 16 operands are read from shared memory while 16 dependent adds retire
+// (kFoldV2: as 8 16-byte loads, after peeling one element to 16-byte
+// alignment; the adds keep their order, so the bits are the same).
 template <bool kSq>
 __device__ __forceinline__ double fold_span(const double* v, uint32_t i, uint32_t end, double acc,
                                             double mu) {
@@ -502,6 +509,37 @@ __device__ __forceinline__ double fold_span(const double* v, uint32_t i, uint32_
     return x;
   };
   constexpr int kG = 16;
+  if (kFoldV2) {
+    if (i < end && (reinterpret_cast<uintptr_t>(v + i) & 15u)) acc = __dadd_rn(acc, term(v[i++]));
+    constexpr int kP = kG / 2;
+    double2 cur[kP], nxt[kP];
+    if (i + kG <= end) {
+      const double2* w = reinterpret_cast<const double2*>(v + i);
+#pragma unroll
+      for (int j = 0; j < kP; ++j) cur[j] = w[j];
+      while (i + 2 * kG <= end) {
+#pragma unroll
+        for (int j = 0; j < kP; ++j) nxt[j] = w[kP + j];
+#pragma unroll
+        for (int j = 0; j < kP; ++j) {
+          acc = __dadd_rn(acc, term(cur[j].x));
+          acc = __dadd_rn(acc, term(cur[j].y));
+        }
+#pragma unroll
+        for (int j = 0; j < kP; ++j) cur[j] = nxt[j];
+        w += kP;
+        i += kG;
+      }
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+        acc = __dadd_rn(acc, term(cur[j].x));
+        acc = __dadd_rn(acc, term(cur[j].y));
+      }
+      i += kG;
+    }
+    for (; i < end; ++i) acc = __dadd_rn(acc, term(v[i]));
+    return acc;
+  }
   double cur[kG], nxt[kG];
   if (i + kG <= end) {
 #pragma unroll
@@ -532,6 +570,39 @@ __device__ __forceinline__ double fold_span_sq(const double* v, uint32_t i, uint
     return __dmul_rn(d, d);
   };
   constexpr int kG = 16;
+  if (kFoldV2) {
+    if (i < end && (reinterpret_cast<uintptr_t>(v + i) & 15u)) acc = __dadd_rn(acc, term(v[i++]));
+    constexpr int kP = kG / 2;
+    double cur[kG];
+    double2 nxt[kP];
+    if (i + kG <= end) {
+      const double2* w = reinterpret_cast<const double2*>(v + i);
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+        const double2 t = w[j];
+        cur[2 * j] = term(t.x);
+        cur[2 * j + 1] = term(t.y);
+      }
+      while (i + 2 * kG <= end) {
+#pragma unroll
+        for (int j = 0; j < kP; ++j) nxt[j] = w[kP + j];
+#pragma unroll
+        for (int j = 0; j < kP; ++j) {
+          acc = __dadd_rn(acc, cur[2 * j]);
+          cur[2 * j] = term(nxt[j].x);
+          acc = __dadd_rn(acc, cur[2 * j + 1]);
+          cur[2 * j + 1] = term(nxt[j].y);
+        }
+        w += kP;
+        i += kG;
+      }
+#pragma unroll
+      for (int j = 0; j < kG; ++j) acc = __dadd_rn(acc, cur[j]);
+      i += kG;
+    }
+    for (; i < end; ++i) acc = __dadd_rn(acc, term(v[i]));
+    return acc;
+  }
   double cur[kG], nxt[kG];
   if (i + kG <= end) {
 #pragma unroll
